@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""bench.py -- decode-step throughput of the compressed-KV hot path on B200.
+
+One step = one decode step of the whole model (Alg. 1's token -> layer loop
+order): for each of the l layers, flexq_append_kv (quantize the new
+token's K/V into the cache) then flexq_decode_attention over the
+cur_len = s + i cached tokens.  Steps cycle i = 1..n-1.  The
+workload at N = 1 is OPT-175B (BASELINE.json configs[3]: 96 heads x 128,
+s = 512, n = 32, batch 144, l = 96 -> 104 GB of compressed cache resident in
+HBM).  metric: algorithmic compressed-KV GB/s of the step (whole job), with
+tokens/s alongside.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config opt-175b] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, weak scaling)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compressed-KV decode attention GB/s and tokens/s vs HBM roofline at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=31)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="flexq", choices=["flexq", "reference"])
+    ap.add_argument("--config", default="opt-175b")
+    ap.add_argument("--layers", type=int, default=0, help="override model depth (0 = full)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """NVML SM clock / throttle-reason sampling during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def result(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "flexq" else "gloo"
+        if args.impl == "flexq":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+_ORACLE_STATE = {}
+
+
+def _oracle_task(task):
+    """One sequence (all heads) of one decode step through the oracle: append the
+    new token (quantize) then attention_f64 over cur_len tokens
+    (P:271-274).  The prompt cache is built once per worker process (untimed);
+    only the step itself is timed."""
+    import oracle
+    from paper_2303_06865_b200 import synth
+    seq, H, D, s, cur_len, seed = task
+    key = (H, D, s, cur_len)
+    if key not in _ORACLE_STATE:
+        T = cur_len
+        kc, vc = oracle.empty_cache(1, H, T, D), oracle.empty_cache(1, H, T, D)
+        kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (1, H, cur_len - 1, D)).numpy()
+        vp = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (1, H, cur_len - 1, D)).numpy()
+        oracle.append_kv(kp, vp, kc, vc, 0)
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW), (1, H, 1, D)).numpy()
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW), (1, H, 1, D)).numpy()
+        q = synth.fill(seed, synth.tensor_id(0, synth.Q), (1, H, D)).numpy()
+        _ORACLE_STATE[key] = (kc, vc, kn, vn, q)
+    kc, vc, kn, vn, q = _ORACLE_STATE[key]
+    t0 = time.perf_counter()
+    oracle.append_kv(kn, vn, kc, vc, cur_len - 1)
+    oracle.attention_f64(q, kc, vc, cur_len)
+    return time.perf_counter() - t0
+
+
+_POOL = None
+
+
+def cpu_oracle_baseline(w, budget_s: float, bytes_fn):
+    """Time the oracle, as it stands, on a bounded sample of the workload on all
+    host cores: one worker process per core, each task = one sequence x all
+    heads x one layer of one decode step at cur_len = s + n - 1.  Throughput =
+    sample bytes / (sum of per-task step times / cores).  Returns
+    (GB/s, sequence-layers/s, cores, sample description)."""
+    global _POOL
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    cores = os.cpu_count() or 1
+    cur_len = w.prompt_len + w.gen_len - 1
+    if _POOL is None:
+        import atexit
+        _POOL = mp.get_context("fork").Pool(cores)
+        atexit.register(_POOL.terminate)
+        _POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77) for i in range(cores)],
+                  chunksize=1)                                   # per-process setup + calibration
+    t1 = statistics.median(_POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77)
+                                                    for i in range(cores)], chunksize=1))
+    n_tasks = max(cores, int(budget_s / max(t1, 1e-4)) * cores)
+    n_tasks = min(n_tasks, 256 * cores)
+    times = _POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77)
+                                     for i in range(n_tasks)], chunksize=1)
+    busy = sum(times) / cores
+    nbytes = bytes_fn(n_tasks, cur_len)
+    gbs = nbytes / busy / 1e9
+    sample = (f"{n_tasks} tasks x (1 sequence x {w.heads} heads x 1 layer: append 1 token + attention_f64 at "
+              f"cur_len {cur_len}); {t1 * 1e3:.1f} ms per task single-thread; {cores} worker processes; "
+              f"rate = bytes / (sum task time / cores)")
+    return gbs, n_tasks / busy, cores, sample
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, local, pg = dist_setup(args)
+    if rank != 0:
+        return
+    from paper_2303_06865_b200 import workloads as wl
+    w = wl.CONFIGS[args.config]
+    if args.layers:
+        w = wl.Workload(w.name, w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len, args.layers, w.h2)
+    per = lambda n, cur: n * (wl.attention_bytes(1, w.h1, cur) + wl.append_bytes(1, w.h1))  # noqa: E731
+    budget = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gbs, seqs, cores, sample = cpu_oracle_baseline(w, budget, per)
+        if i >= args.warmup:
+            vals.append((gbs, seqs))
+    gbs = statistics.median(v[0] for v in vals)
+    seqs = statistics.median(v[1] for v in vals)
+    tok_s = seqs / w.layers
+    line = {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u4+f16->f32",
+            "data": "synthetic", "tokens_per_s": round(tok_s, 4),
+            "config": {"workload": f"{w.name}: batch {w.batch}, {w.heads}x{w.head_dim}, s={w.prompt_len}, "
+                                   f"n={w.gen_len}, l={w.layers}; oracle on a bounded per-step sample",
+                       "global_batch": w.batch, "seq_len": w.prompt_len + w.gen_len},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- flexq arm
+def run_flexq(args):
+    import torch
+    from paper_2303_06865_b200 import flexq as fq
+    from paper_2303_06865_b200 import synth
+    from paper_2303_06865_b200 import workloads as wl
+
+    world, rank, local, pg = dist_setup(args)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    fq.lib()
+
+    w = wl.CONFIGS[args.config]
+    if args.layers:
+        w = wl.Workload(w.name, w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len, args.layers, w.h2)
+    B_total = w.batch * (world if args.scaling == "weak" else 1)
+    if args.scaling == "weak":
+        B = w.batch
+    else:
+        per = (w.batch + world - 1) // world
+        B = max(0, min(per, w.batch - rank * per))
+    H, D, s, n, L = w.heads, w.head_dim, w.prompt_len, w.gen_len, w.layers
+    h1 = H * D
+    seed = synth.BASE_SEED + 3 + 1000 * rank
+    stream = torch.cuda.Stream(device=dev)
+
+    # ---- setup: compressed caches for all layers resident in HBM
+    with torch.cuda.stream(stream):
+        caches = [fq.KVCache(B, H, D, s, n, device=dev) for _ in range(L)]
+        kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=dev)
+        vp = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), device=dev)
+        for c in caches:                                  # prompt fill (prefill's KV, quantized)
+            fq.flexq_append_kv(kp, vp, c, pos=0)
+        del kp, vp
+        qs = synth.fill(seed, synth.tensor_id(0, synth.Q), (L, B, H, D), device=dev)
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW), (L, B, H, 1, D), device=dev)
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW), (L, B, H, 1, D), device=dev)
+        outs = torch.empty(L, B, H, D, dtype=torch.float16, device=dev)
+        ws = fq.make_workspace(caches[0])
+    torch.cuda.synchronize()
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    cache_bytes = sum(c.nbytes() for c in caches)
+
+    def step_calls(i, st):
+        cur = s + i
+        for j in range(L):
+            fq.flexq_append_kv(kn[j], vn[j], caches[j], pos=cur - 1, stream=st)
+            fq.flexq_decode_attention(qs[j], caches[j], cur, out=outs[j], workspace=ws, stream=st)
+
+    # one CUDA graph per decode step i = 1..n-1
+    steps_i = list(range(1, n))
+    graphs = {}
+    with torch.cuda.stream(stream):
+        step_calls(1, stream)                              # warm the launch path before capture
+    torch.cuda.synchronize()
+    for i in steps_i:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step_calls(i, stream)
+        graphs[i] = g
+    torch.cuda.synchronize()
+
+    def seq_of(k):
+        return steps_i[k % len(steps_i)]
+
+    step_bytes = {i: L * (wl.attention_bytes(B, h1, s + i) + wl.append_bytes(B, h1)) for i in steps_i}
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warmup + timed region (device events on the launching stream)
+    for k in range(args.warmup):
+        graphs[seq_of(k)].replay()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for k in range(args.steps):
+                i = seq_of(args.warmup + k)
+                graphs[i].replay()
+            ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if pg:
+        t = torch.tensor([ms], device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    job_bytes = B_total * sum(L * (wl.attention_bytes(1, h1, s + seq_of(args.warmup + k)) + wl.append_bytes(1, h1))
+                              for k in range(args.steps))
+    value_gbs = job_bytes / (ms / 1e3) / 1e9
+    tokens_per_s = B_total * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel: attention alone, one graph of L launches at cur_len = s + n - 1
+    cur_last = s + n - 1
+    ga = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(ga, stream=stream):
+        for j in range(L):
+            fq.flexq_decode_attention(qs[j], caches[j], cur_last, out=outs[j], workspace=ws, stream=stream)
+    gapp = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gapp, stream=stream):
+        for j in range(L):
+            fq.flexq_append_kv(kn[j], vn[j], caches[j], pos=cur_last - 1, stream=stream)
+    reps = 5
+    for g in (ga, gapp):
+        g.replay()
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        e[0].record(stream)
+        for _ in range(reps):
+            ga.replay()
+        e[1].record(stream)
+        for _ in range(reps):
+            gapp.replay()
+        e[2].record(stream)
+    torch.cuda.synchronize()
+    attn_us = e[0].elapsed_time(e[1]) * 1e3 / (reps * L)
+    app_us = e[1].elapsed_time(e[2]) * 1e3 / (reps * L)
+    attn_bytes = wl.attention_bytes(B, h1, cur_last)
+    peak, peak_kind = peaks()
+    achieved = attn_bytes / (attn_us * 1e-6) / 1e9
+
+    # ---- e2e: host buffers through the public API, H2D of the step's inputs and D2H of its outputs
+    e2e = None
+    if not args.no_e2e:
+        qh = qs.cpu().pin_memory()
+        knh = kn.cpu().pin_memory()
+        vnh = vn.cpu().pin_memory()
+        outh = torch.empty(outs.shape, dtype=outs.dtype).pin_memory()
+        qd = [torch.empty_like(qs[0]) for _ in range(2)]
+        knd = [torch.empty_like(kn[0]) for _ in range(2)]
+        vnd = [torch.empty_like(vn[0]) for _ in range(2)]
+        od = [torch.empty_like(outs[0]) for _ in range(2)]
+        copy = torch.cuda.Stream(device=dev)
+
+        def e2e_step(i):
+            cur = s + i
+            ready = [torch.cuda.Event() for _ in range(L)]
+            done = [torch.cuda.Event() for _ in range(L)]
+            for j in range(L):
+                b = j & 1
+                with torch.cuda.stream(copy):
+                    if j >= 2:
+                        copy.wait_event(done[j - 2])
+                        outh[j - 2].copy_(od[b], non_blocking=True)
+                    qd[b].copy_(qh[j], non_blocking=True)
+                    knd[b].copy_(knh[j], non_blocking=True)
+                    vnd[b].copy_(vnh[j], non_blocking=True)
+                    ready[j].record(copy)
+                stream.wait_event(ready[j])
+                fq.flexq_append_kv(knd[b], vnd[b], caches[j], pos=cur - 1, stream=stream)
+                fq.flexq_decode_attention(qd[b], caches[j], cur, out=od[b], workspace=ws, stream=stream)
+                done[j].record(stream)
+            with torch.cuda.stream(copy):
+                for j in range(max(0, L - 2), L):
+                    copy.wait_event(done[j])
+                    outh[j].copy_(od[j & 1], non_blocking=True)
+            stream.wait_stream(copy)
+
+        for k in range(2):
+            e2e_step(seq_of(k))
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_bytes = 0
+        ke = max(3, min(args.steps, 10))
+        x0.record(stream)
+        for k in range(ke):
+            i = seq_of(k)
+            e2e_step(i)
+            e2e_bytes += step_bytes[i]
+        x1.record(stream)
+        barrier()
+        ems = x0.elapsed_time(x1)
+        if pg:
+            t = torch.tensor([ems], device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e_job = e2e_bytes * (B_total / B if B else 0)
+        e2e = {"value": round(e2e_job / (ems / 1e3) / 1e9, 2),
+               "unit": "GB/s", "h2d_bytes_per_step": int(qh.nbytes + knh.nbytes + vnh.nbytes),
+               "d2h_bytes_per_step": int(outh.nbytes), "ms_per_step": round(ems / ke, 3),
+               "tokens_per_s": round(B_total * ke / (ems / 1e3), 2),
+               "how": "pinned host q/k_new/v_new per layer -> H2D on a copy stream (double-buffered), "
+                      "append+attention via the C ABI, D2H of every layer's output; CUDA events, max over ranks"}
+
+    # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        sweep = {}
+        for (r, c) in ((12288, 49152), (12288, 12288)):
+            x = synth.fill(seed, synth.tensor_id(0, synth.WEIGHT, c), (r, c), device=dev)
+            codes = torch.empty(r, c // 2, dtype=torch.uint8, device=dev)
+            meta = torch.empty(r, c // 64, 2, dtype=torch.float16, device=dev)
+            y = torch.empty_like(x)
+            with torch.cuda.stream(stream):
+                fq.flexq_quantize(x, codes, meta, stream=stream)
+                fq.flexq_dequantize(codes, meta, y, stream=stream)
+                tq, td = [], []
+                for _ in range(10):
+                    a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                    a0.record(stream)
+                    fq.flexq_quantize(x, codes, meta, stream=stream)
+                    a1.record(stream)
+                    fq.flexq_dequantize(codes, meta, y, stream=stream)
+                    a2.record(stream)
+                    a2.synchronize()
+                    tq.append(a0.elapsed_time(a1))
+                    td.append(a1.elapsed_time(a2))
+            nb = r * c * 2 + r * c // 2 + r * c // 64 * 4
+            sweep[f"{r}x{c}"] = {"quantize_us": round(statistics.median(tq) * 1e3, 1),
+                                 "quantize_gbs": round(nb / (statistics.median(tq) * 1e-3) / 1e9, 1),
+                                 "dequantize_us": round(statistics.median(td) * 1e3, 1),
+                                 "dequantize_gbs": round(nb / (statistics.median(td) * 1e-3) / 1e9, 1)}
+            del x, codes, meta, y
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per = lambda nseq, cur: nseq * (wl.attention_bytes(1, h1, cur) + wl.append_bytes(1, h1))  # noqa: E731
+        gbs, seqs, cores, sample = cpu_oracle_baseline(w, args.cpu_seconds, per)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "u4+f16->f32", "data": "synthetic (counter-based Irwin-Hall fp16, P:41/P:44)",
+            "tokens_per_s": round(tokens_per_s, 2),
+            "attention_tokens_per_s_per_layer": round(tokens_per_s * L, 1),
+            "config": {"workload": f"{w.name} decode step: batch {B} per GPU (global {B_total}), {H} heads x {D}, "
+                                   f"s={s}, n={n}, l={L} layers, append_kv + decode_attention per layer, "
+                                   f"steps cycle cur_len {s + 1}..{s + n - 1}",
+                       "global_batch": B_total, "seq_len": s + n, "parallelism": f"dp{world} (sequences)",
+                       "l2": f"working set {cache_bytes / 1e9:.1f} GB per GPU >> {l2 / 1e6:.0f} MB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "decode_attention_kernel<128>", "peak_kind": peak_kind,
+                         "bytes_per_launch": attn_bytes, "us_per_launch": round(attn_us, 2),
+                         "append_us_per_launch": round(app_us, 2),
+                         "attention_share_of_step": round(attn_us * L / (ms_step * 1e3), 4)},
+            "gpu_launches": args.steps * L * 2,
+            "clocks": clk.result(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "weight_sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_flexq(args)
+
+
+if __name__ == "__main__":
+    main()

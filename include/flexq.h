@@ -1,0 +1,119 @@
+/*
+ * flexq.h -- C ABI of the B200 (sm_100a) compressed-KV decode-attention library.
+ *
+ * The library implements the data-parallel hot path of FlexGen's approximate
+ * method (Sheng et al., arXiv 2303.06865, Sec. 4 "Approximate Methods"):
+ * group-wise asymmetric b-bit quantization of the KV cache, grouped along the
+ * hidden dimension, and decode-step attention over that
+ * compressed cache, with dequantization fused into the attention
+ * kernel.  Citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n; the
+ * readings of ambiguous passages (A..S) are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a CUDA device pointer on the current device and
+ *    must be 16-byte aligned (else FLEXQ_ERR_ALIGN).  The caller owns all
+ *    buffers; the library never allocates, frees or synchronizes.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered and asynchronous, and are safe to capture in CUDA graphs.
+ *  - Argument validation runs first, on the host, before any CUDA call; a
+ *    rejected call returns its status and writes nothing.  FLEXQ_ERR_CUDA is
+ *    returned when the launch itself fails; faults inside a kernel surface at
+ *    the caller's next synchronization.
+ *  - Inputs must be finite; NaN / Inf inputs give unspecified codes.
+ *  - fp16 = IEEE binary16 (`half`); half2 meta = {.x = scale, .y = min}.
+ *  - The library keeps no mutable global state: calls are reentrant.
+ */
+#ifndef FLEXQ_H
+#define FLEXQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLEXQ_ABI_VERSION 1
+
+typedef enum {
+    FLEXQ_OK = 0,
+    FLEXQ_ERR_NULL = 1,        /* a required pointer is NULL                                  */
+    FLEXQ_ERR_ARG = 2,         /* size / index out of range: a dimension < 1, bits not in
+                                  [1, 8], group_size < 1, pos < 0,
+                                  pos + n_new > prompt_len + gen_len, cur_len not in
+                                  [1, prompt_len + gen_len]                                  */
+    FLEXQ_ERR_ALIGN = 3,       /* a tensor pointer is not 16-byte aligned                     */
+    FLEXQ_ERR_UNSUPPORTED = 4, /* legal per the paper but not built: bits != 4, group_size
+                                  != 64 (P:846 fixes b = 4, g = 64), head_dim not in
+                                  {64, 128}, cols % group_size != 0 (reading I)             */
+    FLEXQ_ERR_WORKSPACE = 5,   /* workspace NULL or smaller than the size query              */
+    FLEXQ_ERR_CUDA = 6         /* a CUDA launch / attribute call failed                       */
+} flexq_status;
+
+/* = FLEXQ_ABI_VERSION. */
+int flexq_abi_version(void);
+
+/* Static, never-NULL description of a status code (unknown codes included). */
+const char *flexq_status_string(int status);
+
+/* Group-wise quantize (reading B): x fp16 [rows][cols] row-major;
+ * groups are runs of group_size contiguous elements along cols (for weights,
+ * the output-channel axis of the paper's x.w orientation).
+ * Per group: min, max; code = RNE(RN32(RN32(RN32(x-min) / RN32(max-min)) * 15));
+ * max == min -> codes 0, scale 0 (reading C).
+ *   codes_u8 [rows][cols/2]: element 2k in the low nibble of byte k.
+ *   meta_h2  [rows][cols/group_size] half2 {scale = f16((max-min)/15), min}.
+ * Supported: bits == 4, group_size == 64.  rows == 0 or cols == 0 is a no-op. */
+flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int bits, int group_size,
+                            void *codes_u8, void *meta_h2, void *stream);
+
+/* Inverse of flexq_quantize: out fp16 [rows][cols] =
+ * f16_RNE(clamp(fmaf(code, scale, min), -65504, 65504)) (reading R). */
+flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t rows, int64_t cols,
+                              int bits, int group_size, void *out_f16, void *stream);
+
+/* KV cache layout for one layer, T_cap = prompt_len + gen_len:
+ *   k_codes, v_codes: u8    [batch][heads][T_cap][head_dim/2]
+ *   k_meta,  v_meta:  half2 [batch][heads][T_cap][head_dim/group_size]
+ * Sizes in bytes (either output pointer may be NULL). */
+flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                  int bits, int group_size, size_t *codes_bytes, size_t *meta_bytes);
+
+/* KV update x_K <- Concat(x_K, t.w_K), same for V: quantizes
+ * k_new, v_new fp16 [batch][heads][n_new][head_dim] group-wise along head_dim
+ * and writes cache tokens [pos, pos + n_new) of every (batch, head).
+ * Prompt fill is pos = 0, n_new = prompt_len; a decode step is n_new = 1.
+ * Touches no other cache position. */
+flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
+                             int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                             int pos, int n_new, int bits, int group_size,
+                             void *k_codes, void *k_meta, void *v_codes, void *v_meta, void *stream);
+
+/* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
+ * arguments).  Layout: 256 B of scheduler counters, 4 B per (batch, head) of
+ * split tickets, then split-K partials.  The workspace must be zero-filled
+ * ONCE after allocation; every call restores the counters and tickets to
+ * zero before it completes (the partials are scratch), so one buffer serves
+ * any number of stream-ordered calls (not concurrent ones). */
+size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
+                                             int gen_len, int bits, int group_size);
+
+/* Decode-step attention over the compressed cache (reading K):
+ *   out fp16 [batch][heads][head_dim] =
+ *     softmax(q . K^[0:cur_len]^T / sqrt(head_dim)) . V^[0:cur_len]
+ * with K^, V^ = fmaf(code, scale, min) in fp32, never rounded to fp16 (reading
+ * M); q fp16 [batch][heads][head_dim].  Cache layout as above; tokens
+ * [cur_len, T_cap) are never read.  Accuracy: |out - exact| <=
+ * max(2e-3, 1e-2 |exact|) per element (reading Q). */
+flexq_status flexq_decode_attention(const void *q_f16,
+                                    const void *k_codes, const void *k_meta,
+                                    const void *v_codes, const void *v_meta,
+                                    int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                    int cur_len, int bits, int group_size, void *out_f16,
+                                    void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLEXQ_H */

@@ -1,0 +1,139 @@
+// flexq_api.cu -- the C ABI declared in include/flexq.h: host-side argument
+// validation (no CUDA call before it passes), then the kernel launchers.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/flexq.h"
+#include "flexq_internal.h"
+
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Shared checks for the quantizer configuration (b = 4, g = 64).
+flexq_status check_bits_group(int bits, int group_size) {
+    if (bits < 1 || bits > 8 || group_size < 1) return FLEXQ_ERR_ARG;
+    if (bits != flexq::kBits || group_size != flexq::kGroup) return FLEXQ_ERR_UNSUPPORTED;
+    return FLEXQ_OK;
+}
+
+flexq_status check_kv_dims(int batch, int heads, int head_dim, int prompt_len, int gen_len, int bits,
+                           int group_size) {
+    if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
+        int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX)
+        return FLEXQ_ERR_ARG;
+    flexq_status s = check_bits_group(bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (head_dim != 64 && head_dim != 128) return FLEXQ_ERR_UNSUPPORTED;
+    return FLEXQ_OK;
+}
+
+flexq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FLEXQ_OK : FLEXQ_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int flexq_abi_version(void) { return FLEXQ_ABI_VERSION; }
+
+const char* flexq_status_string(int s) {
+    switch (s) {
+        case FLEXQ_OK: return "ok";
+        case FLEXQ_ERR_NULL: return "null pointer";
+        case FLEXQ_ERR_ARG: return "argument out of range";
+        case FLEXQ_ERR_ALIGN: return "pointer not 16-byte aligned";
+        case FLEXQ_ERR_UNSUPPORTED: return "unsupported configuration (bits/group/head_dim/cols)";
+        case FLEXQ_ERR_WORKSPACE: return "workspace missing or too small";
+        case FLEXQ_ERR_CUDA: return "CUDA launch failed";
+        default: return "unknown status";
+    }
+}
+
+flexq_status flexq_quantize(const void* x_f16, int64_t rows, int64_t cols, int bits, int group_size,
+                            void* codes_u8, void* meta_h2, void* stream) {
+    if (rows < 0 || cols < 0) return FLEXQ_ERR_ARG;
+    flexq_status s = check_bits_group(bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (cols % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
+    if (rows == 0 || cols == 0) return FLEXQ_OK;
+    if (!x_f16 || !codes_u8 || !meta_h2) return FLEXQ_ERR_NULL;
+    if (!aligned16(x_f16) || !aligned16(codes_u8) || !aligned16(meta_h2)) return FLEXQ_ERR_ALIGN;
+    return from_cuda(flexq::launch_quantize(x_f16, rows, cols, codes_u8, meta_h2, nullptr, nullptr,
+                                            nullptr, flexq::RowMap{0, 0, 0},
+                                            static_cast<cudaStream_t>(stream)));
+}
+
+flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t rows, int64_t cols,
+                              int bits, int group_size, void* out_f16, void* stream) {
+    if (rows < 0 || cols < 0) return FLEXQ_ERR_ARG;
+    flexq_status s = check_bits_group(bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (cols % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
+    if (rows == 0 || cols == 0) return FLEXQ_OK;
+    if (!codes_u8 || !meta_h2 || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(codes_u8) || !aligned16(meta_h2) || !aligned16(out_f16)) return FLEXQ_ERR_ALIGN;
+    return from_cuda(flexq::launch_dequantize(codes_u8, meta_h2, rows, cols, out_f16,
+                                              static_cast<cudaStream_t>(stream)));
+}
+
+flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                  int bits, int group_size, size_t* codes_bytes, size_t* meta_bytes) {
+    if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
+        int64_t(prompt_len) + gen_len < 1 || bits < 1 || bits > 8 || group_size < 1)
+        return FLEXQ_ERR_ARG;
+    if (head_dim % group_size != 0 || (int64_t(head_dim) * bits) % 8 != 0) return FLEXQ_ERR_UNSUPPORTED;
+    const size_t rows = size_t(batch) * heads * (size_t(prompt_len) + gen_len);
+    if (codes_bytes) *codes_bytes = rows * size_t(head_dim) * bits / 8;
+    if (meta_bytes) *meta_bytes = rows * size_t(head_dim / group_size) * 4;
+    return FLEXQ_OK;
+}
+
+flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int batch, int heads,
+                             int head_dim, int prompt_len, int gen_len, int pos, int n_new, int bits,
+                             int group_size, void* k_codes, void* k_meta, void* v_codes, void* v_meta,
+                             void* stream) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s == FLEXQ_ERR_ARG) return s;
+    const int64_t t_cap = int64_t(prompt_len) + gen_len;
+    if (pos < 0 || n_new < 1 || int64_t(pos) + n_new > t_cap) return FLEXQ_ERR_ARG;
+    if (s != FLEXQ_OK) return s;
+    if (!k_new_f16 || !v_new_f16 || !k_codes || !k_meta || !v_codes || !v_meta) return FLEXQ_ERR_NULL;
+    if (!aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_codes) || !aligned16(k_meta) ||
+        !aligned16(v_codes) || !aligned16(v_meta))
+        return FLEXQ_ERR_ALIGN;
+    const int64_t rows = int64_t(batch) * heads * n_new;
+    return from_cuda(flexq::launch_quantize(k_new_f16, rows, head_dim, k_codes, k_meta, v_new_f16,
+                                            v_codes, v_meta, flexq::RowMap{n_new, t_cap, pos},
+                                            static_cast<cudaStream_t>(stream)));
+}
+
+size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
+                                             int gen_len, int bits, int group_size) {
+    if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
+    return flexq::attention_workspace_bytes(batch, heads, head_dim, prompt_len + gen_len);
+}
+
+flexq_status flexq_decode_attention(const void* q_f16, const void* k_codes, const void* k_meta,
+                                    const void* v_codes, const void* v_meta, int batch, int heads,
+                                    int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
+                                    int group_size, void* out_f16, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s == FLEXQ_ERR_ARG) return s;
+    const int t_cap = prompt_len + gen_len;
+    if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
+    if (s != FLEXQ_OK) return s;
+    if (!q_f16 || !k_codes || !k_meta || !v_codes || !v_meta || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(q_f16) || !aligned16(k_codes) || !aligned16(k_meta) || !aligned16(v_codes) ||
+        !aligned16(v_meta) || !aligned16(out_f16))
+        return FLEXQ_ERR_ALIGN;
+    if (!workspace ||
+        workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+        return FLEXQ_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
+    flexq::AttnArgs a{q_f16, k_codes, k_meta, v_codes, v_meta, out_f16, workspace,
+                      batch, heads, head_dim, t_cap, cur_len};
+    return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+"""Thin Python binding over the C ABI in include/flexq.h (libflexq.so).
+
+Argument marshalling only: torch tensors are passed as data pointers plus
+torch's current CUDA stream; every step of the path runs in the library's
+CUDA kernels.  There is no CPU fallback: if libflexq.so is missing and cannot
+be built, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+from . import build as _build
+
+_lib = None
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "flexq.h")
+
+FLEXQ_OK, FLEXQ_ERR_NULL, FLEXQ_ERR_ARG, FLEXQ_ERR_ALIGN, FLEXQ_ERR_UNSUPPORTED, FLEXQ_ERR_WORKSPACE, \
+    FLEXQ_ERR_CUDA = range(7)
+BITS, GROUP = 4, 64
+
+
+class FlexqError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {lib().flexq_status_string(status).decode()} (status {status})")
+
+
+def lib():
+    """Load libflexq.so (building it in-tree with nvcc if it is missing)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path):
+            try:
+                _build.build()
+            except Exception as e:  # noqa: BLE001
+                raise RuntimeError(f"libflexq.so is not built and the build failed: {e}") from e
+        L = ctypes.CDLL(path)
+        P, I, I64, SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        L.flexq_abi_version.restype = I
+        L.flexq_status_string.argtypes = [I]
+        L.flexq_status_string.restype = ctypes.c_char_p
+        L.flexq_quantize.argtypes = [P, I64, I64, I, I, P, P, P]
+        L.flexq_dequantize.argtypes = [P, P, I64, I64, I, I, P, P]
+        L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(SZ)]
+        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P, P, P, P]
+        L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
+        L.flexq_decode_attention_workspace_size.restype = SZ
+        L.flexq_decode_attention.argtypes = [P] * 5 + [I] * 8 + [P, P, SZ, P]
+        for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
+                  "flexq_decode_attention"):
+            getattr(L, f).restype = I
+        _lib = L
+    return _lib
+
+
+def header_symbols() -> list[str]:
+    """Names of the functions declared in include/flexq.h."""
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(flexq_[a-z0-9_]+)\s*\(", src)))
+
+
+def _check(status: int, what: str):
+    if status != FLEXQ_OK:
+        raise FlexqError(status, what)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _need(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous CUDA {dtype} tensor")
+
+
+# ---------------------------------------------------------------- quantizer
+def flexq_quantize(x: torch.Tensor, codes=None, meta=None, bits: int = BITS, group_size: int = GROUP,
+                   stream=None):
+    """x fp16 [rows][cols] -> (codes u8 [rows][cols/2], meta fp16 [rows][cols/g][2] = (scale, min))."""
+    _need(x, torch.float16, "x")
+    rows, cols = x.shape
+    if codes is None:
+        codes = torch.empty(rows, cols // 2, dtype=torch.uint8, device=x.device)
+    if meta is None:
+        meta = torch.empty(rows, cols // group_size, 2, dtype=torch.float16, device=x.device)
+    _check(lib().flexq_quantize(x.data_ptr(), rows, cols, bits, group_size, codes.data_ptr(),
+                                meta.data_ptr(), _stream(stream)), "flexq_quantize")
+    return codes, meta
+
+
+def flexq_dequantize(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: int = BITS,
+                     group_size: int = GROUP, stream=None) -> torch.Tensor:
+    rows, half_cols = codes.shape
+    cols = half_cols * 2
+    if out is None:
+        out = torch.empty(rows, cols, dtype=torch.float16, device=codes.device)
+    _check(lib().flexq_dequantize(codes.data_ptr(), meta.data_ptr(), rows, cols, bits, group_size,
+                                  out.data_ptr(), _stream(stream)), "flexq_dequantize")
+    return out
+
+
+# ---------------------------------------------------------------- KV cache
+class KVCache:
+    """One layer's compressed KV cache (layout of include/flexq.h)."""
+
+    def __init__(self, batch: int, heads: int, head_dim: int, prompt_len: int, gen_len: int,
+                 device="cuda", bits: int = BITS, group_size: int = GROUP):
+        self.batch, self.heads, self.head_dim = batch, heads, head_dim
+        self.prompt_len, self.gen_len = prompt_len, gen_len
+        self.bits, self.group_size = bits, group_size
+        T = prompt_len + gen_len
+        self.t_cap = T
+        self.k_codes = torch.zeros(batch, heads, T, head_dim // 2, dtype=torch.uint8, device=device)
+        self.v_codes = torch.zeros_like(self.k_codes)
+        self.k_meta = torch.zeros(batch, heads, T, head_dim // group_size, 2, dtype=torch.float16, device=device)
+        self.v_meta = torch.zeros_like(self.k_meta)
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.k_codes, self.v_codes, self.k_meta, self.v_meta))
+
+
+def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS, group_size=GROUP):
+    c, m = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits, group_size,
+                                      ctypes.byref(c), ctypes.byref(m)), "flexq_kv_cache_bytes")
+    return c.value, m.value
+
+
+def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, pos: int, stream=None):
+    """k_new, v_new fp16 [B][H][n_new][D] -> cache tokens [pos, pos + n_new)."""
+    _need(k_new, torch.float16, "k_new")
+    _need(v_new, torch.float16, "v_new")
+    B, H, n_new, D = k_new.shape
+    _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
+                                 cache.gen_len, pos, n_new, cache.bits, cache.group_size,
+                                 cache.k_codes.data_ptr(), cache.k_meta.data_ptr(),
+                                 cache.v_codes.data_ptr(), cache.v_meta.data_ptr(), _stream(stream)),
+           "flexq_append_kv")
+
+
+def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
+                                          group_size=GROUP) -> int:
+    return int(lib().flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len,
+                                                           bits, group_size))
+
+
+def make_workspace(cache: KVCache) -> torch.Tensor:
+    n = flexq_decode_attention_workspace_size(cache.batch, cache.heads, cache.head_dim, cache.prompt_len,
+                                              cache.gen_len, cache.bits, cache.group_size)
+    return torch.zeros(n, dtype=torch.uint8, device=cache.k_codes.device)
+
+
+def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=None, workspace=None,
+                           stream=None) -> torch.Tensor:
+    """q fp16 [B][H][D] -> out fp16 [B][H][D] over cache tokens [0, cur_len)."""
+    _need(q, torch.float16, "q")
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = make_workspace(cache)
+    _check(lib().flexq_decode_attention(q.data_ptr(), cache.k_codes.data_ptr(), cache.k_meta.data_ptr(),
+                                        cache.v_codes.data_ptr(), cache.v_meta.data_ptr(), cache.batch,
+                                        cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
+                                        cur_len, cache.bits, cache.group_size, out.data_ptr(),
+                                        workspace.data_ptr(), workspace.numel(), _stream(stream)),
+           "flexq_decode_attention")
+    return out

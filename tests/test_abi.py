@@ -1,0 +1,97 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/flexq.h declares, and rejects bad arguments on the host before
+any CUDA call (include/flexq.h "Conventions")."""
+import ctypes
+
+import pytest
+
+from paper_2303_06865_b200 import flexq as fq
+
+A = 0x10000          # fake 16-byte-aligned "device" pointers: validation never dereferences
+U = 0x10008          # misaligned
+
+
+@pytest.fixture(scope="module")
+def L():
+    return fq.lib()
+
+
+def test_exports_every_header_symbol(L):
+    syms = fq.header_symbols()
+    assert {"flexq_quantize", "flexq_dequantize", "flexq_append_kv", "flexq_decode_attention",
+            "flexq_decode_attention_workspace_size", "flexq_status_string", "flexq_abi_version",
+            "flexq_kv_cache_bytes"} <= set(syms)
+    for s in syms:
+        assert hasattr(L, s), s
+
+
+def test_version_and_status_strings(L):
+    assert L.flexq_abi_version() == 1
+    for s in range(-2, 10):
+        assert L.flexq_status_string(s)            # never NULL
+
+
+def test_quantize_validation(L):
+    q = L.flexq_quantize
+    assert q(A, -1, 128, 4, 64, A, A, None) == fq.FLEXQ_ERR_ARG
+    assert q(A, 4, 128, 0, 64, A, A, None) == fq.FLEXQ_ERR_ARG      # bits < 1
+    assert q(A, 4, 128, 9, 64, A, A, None) == fq.FLEXQ_ERR_ARG      # bits > 8
+    assert q(A, 4, 128, 4, 0, A, A, None) == fq.FLEXQ_ERR_ARG
+    assert q(A, 4, 128, 3, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert q(A, 4, 128, 4, 32, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert q(A, 4, 100, 4, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED   # partial group (reading I)
+    assert q(None, 4, 128, 4, 64, A, A, None) == fq.FLEXQ_ERR_NULL
+    assert q(A, 4, 128, 4, 64, None, A, None) == fq.FLEXQ_ERR_NULL
+    assert q(U, 4, 128, 4, 64, A, A, None) == fq.FLEXQ_ERR_ALIGN
+    assert q(A, 0, 128, 4, 64, None, None, None) == fq.FLEXQ_OK      # empty: no-op, no launch
+    assert q(A, 4, 0, 4, 64, None, None, None) == fq.FLEXQ_OK
+
+
+def test_dequantize_validation(L):
+    d = L.flexq_dequantize
+    assert d(A, A, 4, 128, 4, 65, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert d(A, A, 4, 128, 10, 64, A, None) == fq.FLEXQ_ERR_ARG
+    assert d(A, None, 4, 128, 4, 64, A, None) == fq.FLEXQ_ERR_NULL
+    assert d(A, A, 4, 128, 4, 64, U, None) == fq.FLEXQ_ERR_ALIGN
+    assert d(A, A, 0, 128, 4, 64, A, None) == fq.FLEXQ_OK
+
+
+def test_append_validation(L):
+    f = L.flexq_append_kv
+
+    def call(B=2, H=3, D=128, s=8, n=4, pos=0, nn=1, bits=4, g=64, k=A, kc=A):
+        return f(k, A, B, H, D, s, n, pos, nn, bits, g, kc, A, A, A, None)
+    assert call(B=0) == fq.FLEXQ_ERR_ARG
+    assert call(pos=-1) == fq.FLEXQ_ERR_ARG
+    assert call(pos=12) == fq.FLEXQ_ERR_ARG            # pos + n_new > s + n
+    assert call(pos=10, nn=3) == fq.FLEXQ_ERR_ARG
+    assert call(nn=0) == fq.FLEXQ_ERR_ARG
+    assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(bits=2) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(k=None) == fq.FLEXQ_ERR_NULL
+    assert call(kc=U) == fq.FLEXQ_ERR_ALIGN
+
+
+def test_attention_validation(L):
+    f = L.flexq_decode_attention
+    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+    assert ws > 0
+    assert L.flexq_decode_attention_workspace_size(0, 3, 128, 8, 4, 4, 64) == 0
+
+    def call(cur=5, D=128, q=A, out=A, w=A, wb=ws, g=64):
+        return f(q, A, A, A, A, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
+    assert call(cur=0) == fq.FLEXQ_ERR_ARG
+    assert call(cur=13) == fq.FLEXQ_ERR_ARG             # cur_len > s + n
+    assert call(D=32) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(g=128) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(q=None) == fq.FLEXQ_ERR_NULL
+    assert call(out=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
+    assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
+
+
+def test_kv_cache_bytes(L):
+    c, m = fq.flexq_kv_cache_bytes(144, 96, 128, 512, 32)
+    rows = 144 * 96 * 544
+    assert c == rows * 64 and m == rows * 8
+    assert (c + m) * 16 == rows * 128 * 2 * 4.5     # 4.5 bits per element

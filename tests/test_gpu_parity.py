@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Codes, metadata and dequantized values must be
+byte-identical (north_star, SURVEY 8(c) "GPU parity contract"); attention
+outputs must satisfy |gpu - oracle_f64| <= max(2e-3, 1e-2 |oracle|)
+elementwise (reading Q).  Oracle inputs are regenerated on the host by
+synth (never copied back from the device)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2303_06865_b200 import flexq as fq
+from paper_2303_06865_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-3, 1e-2
+
+
+def assert_attn_close(got: np.ndarray, ref: np.ndarray, what=""):
+    got = got.astype(np.float64)
+    err = np.abs(got - ref)
+    bad = err > np.maximum(ATOL, RTOL * np.abs(ref))
+    assert not bad.any(), (f"{what}: {bad.sum()} of {bad.size} elements out of tolerance; "
+                           f"max abs err {err.max():.3e}")
+
+
+# ---------------------------------------------------------------- quantize
+QUANT_CASES = [
+    ("default", lambda: synth.fill(31, 1, (37, 192))),
+    ("ragged_rows_wide", lambda: synth.fill(31, 2, (5, 4096))),
+    ("outliers", lambda: synth.with_outliers(synth.fill(31, 3, (300, 128)))),
+    ("ties", lambda: synth.ties(31, 4, (257, 64))),
+    ("extreme", lambda: synth.extreme(31, 5, 512, 128)),
+    ("one_group", lambda: synth.fill(31, 6, (1, 64))),
+]
+
+
+@pytest.mark.parametrize("name,make", QUANT_CASES, ids=[c[0] for c in QUANT_CASES])
+def test_quantize_bit_exact(orc, cuda, name, make):
+    x = make()
+    codes, meta = fq.flexq_quantize(x.to(cuda))
+    torch.cuda.synchronize()
+    oc, om = orc.quantize(x.numpy(), 4, 64)
+    assert np.array_equal(codes.cpu().numpy(), orc.pack4(oc)), name
+    assert np.array_equal(meta.cpu().numpy().view(np.uint16), om), name
+
+
+def test_quantize_large_grid_stride(orc, cuda):
+    """More groups than the grid's threads: exercises the grid-stride loop."""
+    rows, cols = 4099, 1024
+    x = synth.fill(32, 1, (rows, cols))
+    codes, meta = fq.flexq_quantize(x.to(cuda))
+    oc, om = orc.quantize(x.numpy(), 4, 64)
+    assert np.array_equal(codes.cpu().numpy(), orc.pack4(oc))
+    assert np.array_equal(meta.cpu().numpy().view(np.uint16), om)
+
+
+@pytest.mark.parametrize("name,make", QUANT_CASES, ids=[c[0] for c in QUANT_CASES])
+def test_dequantize_bit_exact(orc, cuda, name, make):
+    x = make()
+    oc, om = orc.quantize(x.numpy(), 4, 64)
+    codes = torch.from_numpy(orc.pack4(oc)).to(cuda)
+    meta = torch.from_numpy(om.view(np.float16)).to(cuda)
+    out = fq.flexq_dequantize(codes, meta)
+    ref = orc.dequantize(oc, om, 4, 64)
+    assert np.array_equal(out.cpu().numpy().view(np.uint16), ref.view(np.uint16)), name
+
+
+# ---------------------------------------------------------------- append
+@pytest.mark.parametrize("D", [64, 128])
+def test_append_kv_bit_exact(orc, cuda, D):
+    B, H, s, n = 3, 5, 70, 6
+    k = synth.fill(33, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D))
+    v = synth.with_outliers(synth.fill(33, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D)))
+    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+    okc, ovc = orc.empty_cache(B, H, s + n, D), orc.empty_cache(B, H, s + n, D)
+    orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+    for step in range(1, 4):
+        kn = synth.fill(33, synth.tensor_id(0, synth.K_NEW, step), (B, H, 1, D))
+        vn = synth.fill(33, synth.tensor_id(0, synth.V_NEW, step), (B, H, 1, D))
+        fq.flexq_append_kv(kn.to(cuda), vn.to(cuda), cache, pos=s + step - 1)
+        orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(cache.k_codes.cpu().numpy(), orc.pack4(okc[0]))
+    assert np.array_equal(cache.v_codes.cpu().numpy(), orc.pack4(ovc[0]))
+    assert np.array_equal(cache.k_meta.cpu().numpy().view(np.uint16), okc[1])
+    assert np.array_equal(cache.v_meta.cpu().numpy().view(np.uint16), ovc[1])
+    # untouched positions stay zero
+    assert int(cache.k_codes[:, :, s + 3:].abs().sum()) == 0
+
+
+# ---------------------------------------------------------------- attention
+def build_case(orc, cuda, B, H, D, s, n, n_steps, seed, outliers=False, qfactor=1):
+    """Prompt fill + n_steps single-token appends on both sides; returns the
+    GPU cache, the oracle caches, q (fp16) and cur_len = s + n_steps."""
+    k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D))
+    v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D))
+    if outliers:
+        k, v = synth.with_outliers(k), synth.with_outliers(v)
+    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    okc, ovc = orc.empty_cache(B, H, s + n, D), orc.empty_cache(B, H, s + n, D)
+    if s > 0:
+        fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+        orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+    for step in range(1, n_steps + 1):
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW, step), (B, H, 1, D))
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, 1, D))
+        fq.flexq_append_kv(kn.to(cuda), vn.to(cuda), cache, pos=s + step - 1)
+        orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
+    q = synth.peaky(synth.fill(seed, synth.tensor_id(0, synth.Q, n_steps), (B, H, D)), qfactor)
+    return cache, okc, ovc, q, s + n_steps
+
+
+ATTN_CASES = [
+    # name, B, H, D, s, n, steps, outliers, qfactor
+    ("tiny_config", 4, 12, 64, 512, 1, 1, False, 1),          # BASELINE configs[0], in full
+    ("tiny_outliers_peaky16", 4, 12, 64, 512, 1, 1, True, 16),
+    ("d128_ragged_split", 2, 3, 128, 100, 8, 3, False, 1),     # cur_len 103: ragged tail, split-K
+    ("d128_peaky64_outliers", 2, 4, 128, 300, 4, 2, True, 64),
+    ("d128_one_token", 3, 2, 128, 0, 4, 1, False, 1),           # cur_len = 1
+    ("d128_stage_multiple", 1, 2, 128, 64, 32, 0, False, 16),   # cur_len 64 = 2 full stages
+    ("d64_long", 1, 3, 64, 1024, 32, 2, True, 16),
+    ("d128_many_heads_nosplit", 24, 128, 128, 40, 2, 1, False, 1),  # B*H = 3072: no split
+]
+
+
+@pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
+def test_attention_parity(orc, cuda, case):
+    name, B, H, D, s, n, steps, outl, qf = case
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, steps, seed=40, outliers=outl, qfactor=qf)
+    ws = fq.make_workspace(cache)
+    out = fq.flexq_decode_attention(q.to(cuda), cache, cur, workspace=ws)
+    torch.cuda.synchronize()
+    ref = orc.attention_f64(q.numpy(), okc, ovc, cur)
+    assert_attn_close(out.cpu().numpy(), ref, name)
+    ctrl = 256 + 4 * B * H           # ticket counter + per-(b, h) split tickets (include/flexq.h)
+    assert int(ws[:ctrl].sum()) == 0, "workspace control words must be restored to zero"
+    # a second call on the same workspace gives the identical result
+    out2 = fq.flexq_decode_attention(q.to(cuda), cache, cur, workspace=ws)
+    assert torch.equal(out, out2)
+
+
+def test_attention_every_cur_len_small(orc, cuda):
+    """cur_len sweeps 1..70 over one cache (stage boundaries at 32, 64)."""
+    B, H, D, s, n = 1, 2, 128, 64, 6
+    cache, okc, ovc, q, _ = build_case(orc, cuda, B, H, D, s, n, 6, seed=41)
+    ws = fq.make_workspace(cache)
+    for cur in list(range(1, 71)):
+        out = fq.flexq_decode_attention(q.to(cuda), cache, cur, workspace=ws)
+        ref = orc.attention_f64(q.numpy(), okc, ovc, cur)
+        assert_attn_close(out.cpu().numpy(), ref, f"cur_len={cur}")
+
+
+def test_attention_cuda_graph_replay(orc, cuda):
+    """append + attention captured in a CUDA graph give the same bytes on replay."""
+    B, H, D, s, n = 2, 8, 128, 200, 4
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, 0, seed=42)
+    kn = synth.fill(42, 99, (B, H, 1, D)).to(cuda)
+    vn = synth.fill(42, 98, (B, H, 1, D)).to(cuda)
+    qd = q.to(cuda)
+    ws = fq.make_workspace(cache)
+    out = torch.empty_like(qd)
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        fq.flexq_append_kv(kn, vn, cache, pos=s)
+        fq.flexq_decode_attention(qd, cache, s + 1, out=out, workspace=ws)
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    eager = out.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fq.flexq_append_kv(kn, vn, cache, pos=s)
+        fq.flexq_decode_attention(qd, cache, s + 1, out=out, workspace=ws)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    orc.append_kv(kn.cpu().numpy(), vn.cpu().numpy(), okc, ovc, s)
+    assert_attn_close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, s + 1), "graph")
+
+
+# ---------------------------------------------------------------- full size, sampled
+def test_opt175b_full_size_sampled(orc, cuda):
+    """BASELINE configs[3] at full size on one GPU (B=144, H=96, D=128, s=512,
+    step 31 -> cur_len 543), the launch configuration bench.py times; the
+    oracle recomputes 12 sampled (b, h) heads from host-regenerated inputs."""
+    B, H, D, s, n = 144, 96, 128, 512, 32
+    seed = synth.BASE_SEED + 3
+    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=cuda)
+    v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), device=cuda)
+    fq.flexq_append_kv(k, v, cache, pos=0)
+    del k, v
+    steps = 31
+    for step in range(1, steps + 1):
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW, step), (B, H, 1, D), device=cuda)
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, 1, D), device=cuda)
+        fq.flexq_append_kv(kn, vn, cache, pos=s + step - 1)
+    q = synth.fill(seed, synth.tensor_id(0, synth.Q, steps), (B, H, D), device=cuda)
+    out = fq.flexq_decode_attention(q, cache, s + steps).cpu().numpy()
+    rng = np.random.default_rng(7)
+    samples = [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(10)]
+    for b, h in samples:
+        kp = synth.gather(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), [b, h, slice(None), slice(None)])
+        vp = synth.gather(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), [b, h, slice(None), slice(None)])
+        okc, ovc = orc.empty_cache(1, 1, s + n, D), orc.empty_cache(1, 1, s + n, D)
+        orc.append_kv(kp.numpy(), vp.numpy(), okc, ovc, 0)
+        for step in range(1, steps + 1):
+            kn = synth.gather(seed, synth.tensor_id(0, synth.K_NEW, step), (B, H, 1, D), [b, h, slice(None), slice(None)])
+            vn = synth.gather(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, 1, D), [b, h, slice(None), slice(None)])
+            orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
+        # codes of this head are bit-exact ...
+        assert np.array_equal(cache.k_codes[b, h, :s + steps].cpu().numpy(), orc.pack4(okc[0][0, 0, :s + steps]))
+        assert np.array_equal(cache.v_meta[b, h, :s + steps].cpu().numpy().view(np.uint16), ovc[1][0, 0, :s + steps])
+        # ... and the attention output is in tolerance
+        qh = synth.gather(seed, synth.tensor_id(0, synth.Q, steps), (B, H, D), [b, h, slice(None)])
+        ref = orc.attention_f64(qh.numpy(), okc, ovc, s + steps)
+        assert_attn_close(out[b:b + 1, h:h + 1], ref, f"(b={b}, h={h})")
