@@ -47,6 +47,14 @@ def parse():
 
 
 # ---------------------------------------------------------------- helpers
+_T0 = time.time()
+
+
+def log(msg: str):
+    sys.stderr.write(f"[bench {time.time() - _T0:7.1f}s] {msg}\n")
+    sys.stderr.flush()
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -122,26 +130,13 @@ def dist_setup(args):
 _ORACLE_STATE = {}
 
 
-def _oracle_task(task):
+def _oracle_task(_):
     """One sequence (all heads) of one decode step through the oracle: append the
     new token (quantize) then attention_f64 over cur_len tokens
-    (P:271-274).  The prompt cache is built once per worker process (untimed);
-    only the step itself is timed."""
+    (P:271-274).  Inputs are prepared in the parent before the fork (numpy
+    only in the workers: no torch thread pool after fork); only the step is timed."""
     import oracle
-    from paper_2303_06865_b200 import synth
-    seq, H, D, s, cur_len, seed = task
-    key = (H, D, s, cur_len)
-    if key not in _ORACLE_STATE:
-        T = cur_len
-        kc, vc = oracle.empty_cache(1, H, T, D), oracle.empty_cache(1, H, T, D)
-        kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (1, H, cur_len - 1, D)).numpy()
-        vp = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (1, H, cur_len - 1, D)).numpy()
-        oracle.append_kv(kp, vp, kc, vc, 0)
-        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW), (1, H, 1, D)).numpy()
-        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW), (1, H, 1, D)).numpy()
-        q = synth.fill(seed, synth.tensor_id(0, synth.Q), (1, H, D)).numpy()
-        _ORACLE_STATE[key] = (kc, vc, kn, vn, q)
-    kc, vc, kn, vn, q = _ORACLE_STATE[key]
+    kc, vc, kn, vn, q, cur_len = _ORACLE_STATE["inputs"]
     t0 = time.perf_counter()
     oracle.append_kv(kn, vn, kc, vc, cur_len - 1)
     oracle.attention_f64(q, kc, vc, cur_len)
@@ -160,26 +155,33 @@ def cpu_oracle_baseline(w, budget_s: float, bytes_fn):
     global _POOL
     import multiprocessing as mp
     import oracle
+    from paper_2303_06865_b200 import synth
     oracle.build()
     cores = os.cpu_count() or 1
     cur_len = w.prompt_len + w.gen_len - 1
+    H, D = w.heads, w.head_dim
     if _POOL is None:
         import atexit
+        seed = synth.BASE_SEED + 77
+        kc, vc = oracle.empty_cache(1, H, cur_len, D), oracle.empty_cache(1, H, cur_len, D)
+        kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (1, H, cur_len - 1, D)).numpy()
+        vp = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (1, H, cur_len - 1, D)).numpy()
+        oracle.append_kv(kp, vp, kc, vc, 0)
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW), (1, H, 1, D)).numpy()
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW), (1, H, 1, D)).numpy()
+        q = synth.fill(seed, synth.tensor_id(0, synth.Q), (1, H, D)).numpy()
+        _ORACLE_STATE["inputs"] = (kc, vc, kn, vn, q, cur_len)
         _POOL = mp.get_context("fork").Pool(cores)
         atexit.register(_POOL.terminate)
-        _POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77) for i in range(cores)],
-                  chunksize=1)                                   # per-process setup + calibration
-    t1 = statistics.median(_POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77)
-                                                    for i in range(cores)], chunksize=1))
+    t1 = statistics.median(_POOL.map(_oracle_task, range(cores), chunksize=1))
     n_tasks = max(cores, int(budget_s / max(t1, 1e-4)) * cores)
     n_tasks = min(n_tasks, 256 * cores)
-    times = _POOL.map(_oracle_task, [(i, w.heads, w.head_dim, w.prompt_len, cur_len, 77)
-                                     for i in range(n_tasks)], chunksize=1)
+    times = _POOL.map(_oracle_task, range(n_tasks), chunksize=1)
     busy = sum(times) / cores
     nbytes = bytes_fn(n_tasks, cur_len)
     gbs = nbytes / busy / 1e9
-    sample = (f"{n_tasks} tasks x (1 sequence x {w.heads} heads x 1 layer: append 1 token + attention_f64 at "
-              f"cur_len {cur_len}); {t1 * 1e3:.1f} ms per task single-thread; {cores} worker processes; "
+    sample = (f"{n_tasks} tasks x (1 sequence x {H} heads x 1 layer: append 1 token + attention_f64 at "
+              f"cur_len {cur_len}); {t1 * 1e3:.1f} ms per task; {cores} worker processes; "
               f"rate = bytes / (sum task time / cores)")
     return gbs, n_tasks / busy, cores, sample
 
@@ -243,6 +245,7 @@ def run_flexq(args):
     stream = torch.cuda.Stream(device=dev)
 
     # ---- setup: compressed caches for all layers resident in HBM
+    log("setup")
     with torch.cuda.stream(stream):
         caches = [fq.KVCache(B, H, D, s, n, device=dev) for _ in range(L)]
         kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=dev)
@@ -266,6 +269,7 @@ def run_flexq(args):
             fq.flexq_decode_attention(qs[j], caches[j], cur, out=outs[j], workspace=ws, stream=st)
 
     # one CUDA graph per decode step i = 1..n-1
+    log("prompt fill done; capturing graphs")
     steps_i = list(range(1, n))
     graphs = {}
     with torch.cuda.stream(stream):
@@ -289,6 +293,7 @@ def run_flexq(args):
         torch.cuda.synchronize()
 
     # ---- warmup + timed region (device events on the launching stream)
+    log("graphs captured; timing")
     for k in range(args.warmup):
         graphs[seq_of(k)].replay()
     barrier()
@@ -313,6 +318,7 @@ def run_flexq(args):
     tokens_per_s = B_total * args.steps / (ms / 1e3)
 
     # ---- dominant kernel: attention alone, one graph of L launches at cur_len = s + n - 1
+    log("timed; per-kernel pass")
     cur_last = s + n - 1
     ga = torch.cuda.CUDAGraph()
     with torch.cuda.graph(ga, stream=stream):
@@ -343,6 +349,7 @@ def run_flexq(args):
     achieved = attn_bytes / (attn_us * 1e-6) / 1e9
 
     # ---- e2e: host buffers through the public API, H2D of the step's inputs and D2H of its outputs
+    log("e2e")
     e2e = None
     if not args.no_e2e:
         qh = qs.cpu().pin_memory()
@@ -406,6 +413,7 @@ def run_flexq(args):
                       "append+attention via the C ABI, D2H of every layer's output; CUDA events, max over ranks"}
 
     # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
+    log("sweep")
     sweep = None
     if rank == 0 and not args.no_sweep:
         sweep = {}
@@ -436,6 +444,7 @@ def run_flexq(args):
             del x, codes, meta, y
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
+    log("cpu baseline")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per = lambda nseq, cur: nseq * (wl.attention_bytes(1, h1, cur) + wl.append_bytes(1, h1))  # noqa: E731

@@ -32,6 +32,8 @@
 //    merges them with the log-sum-exp rule.
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "flexq_internal.h"
 
@@ -39,16 +41,15 @@ namespace flexq {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
-constexpr int kStages = 4;
 constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 64;
 constexpr float kRescaleThresh = 8.0f; // log2 units: p <= 2^8 between rescales
 
-template <int D>
+template <int D, int CH_>
 struct Cfg {
     static constexpr int LPT = D / 32;                 // lanes per token
     static constexpr int TPI = 32 / LPT;               // tokens per warp iteration
-    static constexpr int CH = (D == 128) ? 32 : 64;    // tokens per stage
+    static constexpr int CH = CH_;                     // tokens per stage
     static constexpr int CB = D / 2;                   // code bytes per token
     static constexpr int MB = D / 16;                  // meta bytes per token (D/64 half2)
     static constexpr int ITERS = CH / TPI;
@@ -115,12 +116,25 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
 // Nibble e of word w as a float carrying 2^kShift[e]:
 // e = 0..4 in place (bits 4e..4e+3); e = 5..7 from w >> 12 at bits 8..19.
 constexpr uint32_t kMagic = 0x4B000000u;  // 2^23
-__device__ __forceinline__ void unpack8(uint32_t w, float2 (&f)[4]) {
+// The magic exponent must live in a register: LOP3 takes one immediate, so
+// (w & mask) | magic is a single LOP3 only when magic is not an immediate.
+__device__ __forceinline__ uint32_t magic_reg() {
+    uint32_t m;
+    asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(m));
+    return m;
+}
+template <uint32_t M>
+__device__ __forceinline__ float nib(uint32_t w, uint32_t magic) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(M), "r"(magic));  // (a & b) | c
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void unpack8(uint32_t w, uint32_t magic, float2 (&f)[4]) {
     const uint32_t w12 = w >> 12;
-    float2 u0 = make_float2(__uint_as_float((w & 0x0000Fu) | kMagic), __uint_as_float((w & 0x000F0u) | kMagic));
-    float2 u1 = make_float2(__uint_as_float((w & 0x00F00u) | kMagic), __uint_as_float((w & 0x0F000u) | kMagic));
-    float2 u2 = make_float2(__uint_as_float((w & 0xF0000u) | kMagic), __uint_as_float((w12 & 0x00F00u) | kMagic));
-    float2 u3 = make_float2(__uint_as_float((w12 & 0x0F000u) | kMagic), __uint_as_float((w12 & 0xF0000u) | kMagic));
+    float2 u0 = make_float2(nib<0x0000Fu>(w, magic), nib<0x000F0u>(w, magic));
+    float2 u1 = make_float2(nib<0x00F00u>(w, magic), nib<0x0F000u>(w, magic));
+    float2 u2 = make_float2(nib<0xF0000u>(w, magic), nib<0x00F00u>(w12, magic));
+    float2 u3 = make_float2(nib<0x0F000u>(w12, magic), nib<0xF0000u>(w12, magic));
     const float2 bias = make_float2(-8388608.0f, -8388608.0f);
     f[0] = __fadd2_rn(u0, bias);   // exact: (c0, 16 c1)
     f[1] = __fadd2_rn(u1, bias);   // (256 c2, 4096 c3)
@@ -159,10 +173,11 @@ struct Params {
     float qscale;        // log2(e) / sqrt(D)
 };
 
-template <int D>
+template <int D, int CH, int kStages>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 decode_attention_kernel(const Params P) {
-    using C = Cfg<D>;
+    using C = Cfg<D, CH>;
+    static_assert(CH % C::TPI == 0 && CH <= 64, "stage size");
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -238,6 +253,7 @@ decode_attention_kernel(const Params P) {
     float qsum = 0.0f;                    // sum of q * qscale over the lane's 32 columns
     float2 acc[16];
     float m = -INFINITY, l = 0.0f, bsum = 0.0f;
+    const uint32_t magic = magic_reg();
 
     for (int it = 0;; ++it) {
         const int slot = it % kStages;
@@ -282,16 +298,16 @@ decode_attention_kernel(const Params P) {
             float2 d0 = make_float2(0.0f, 0.0f), d1 = d0;
             {
                 float2 f[4];
-                unpack8(kw.x, f);
+                unpack8(kw.x, magic, f);
                 d0 = __ffma2_rn(qp[0], f[0], d0); d1 = __ffma2_rn(qp[1], f[1], d1);
                 d0 = __ffma2_rn(qp[2], f[2], d0); d1 = __ffma2_rn(qp[3], f[3], d1);
-                unpack8(kw.y, f);
+                unpack8(kw.y, magic, f);
                 d0 = __ffma2_rn(qp[4], f[0], d0); d1 = __ffma2_rn(qp[5], f[1], d1);
                 d0 = __ffma2_rn(qp[6], f[2], d0); d1 = __ffma2_rn(qp[7], f[3], d1);
-                unpack8(kw.z, f);
+                unpack8(kw.z, magic, f);
                 d0 = __ffma2_rn(qp[8], f[0], d0); d1 = __ffma2_rn(qp[9], f[1], d1);
                 d0 = __ffma2_rn(qp[10], f[2], d0); d1 = __ffma2_rn(qp[11], f[3], d1);
-                unpack8(kw.w, f);
+                unpack8(kw.w, magic, f);
                 d0 = __ffma2_rn(qp[12], f[0], d0); d1 = __ffma2_rn(qp[13], f[1], d1);
                 d0 = __ffma2_rn(qp[14], f[2], d0); d1 = __ffma2_rn(qp[15], f[3], d1);
             }
@@ -328,16 +344,16 @@ decode_attention_kernel(const Params P) {
             const float2 a2 = make_float2(a, a);
             {
                 float2 f[4];
-                unpack8(vw.x, f);
+                unpack8(vw.x, magic, f);
                 acc[0] = __ffma2_rn(a2, f[0], acc[0]); acc[1] = __ffma2_rn(a2, f[1], acc[1]);
                 acc[2] = __ffma2_rn(a2, f[2], acc[2]); acc[3] = __ffma2_rn(a2, f[3], acc[3]);
-                unpack8(vw.y, f);
+                unpack8(vw.y, magic, f);
                 acc[4] = __ffma2_rn(a2, f[0], acc[4]); acc[5] = __ffma2_rn(a2, f[1], acc[5]);
                 acc[6] = __ffma2_rn(a2, f[2], acc[6]); acc[7] = __ffma2_rn(a2, f[3], acc[7]);
-                unpack8(vw.z, f);
+                unpack8(vw.z, magic, f);
                 acc[8] = __ffma2_rn(a2, f[0], acc[8]); acc[9] = __ffma2_rn(a2, f[1], acc[9]);
                 acc[10] = __ffma2_rn(a2, f[2], acc[10]); acc[11] = __ffma2_rn(a2, f[3], acc[11]);
-                unpack8(vw.w, f);
+                unpack8(vw.w, magic, f);
                 acc[12] = __ffma2_rn(a2, f[0], acc[12]); acc[13] = __ffma2_rn(a2, f[1], acc[13]);
                 acc[14] = __ffma2_rn(a2, f[2], acc[14]); acc[15] = __ffma2_rn(a2, f[3], acc[15]);
             }
@@ -437,9 +453,9 @@ decode_attention_kernel(const Params P) {
     }
 }
 
-template <int D>
+template <int D, int CH, int S>
 constexpr size_t smem_bytes() {
-    return size_t(kWarpsPerCta) * kStages * (Cfg<D>::STAGE + 8 + sizeof(Desc));
+    return size_t(kWarpsPerCta) * S * (Cfg<D, CH>::STAGE + 8 + sizeof(Desc));
 }
 
 int sm_count() {
@@ -453,15 +469,15 @@ int sm_count() {
     return sms;
 }
 
-template <int D>
+template <int D, int CH, int S>
 int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-        cudaFuncSetAttribute(decode_attention_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem_bytes<D>()));
+        cudaFuncSetAttribute(decode_attention_kernel<D, CH, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem_bytes<D, CH, S>()));
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, decode_attention_kernel<D>, kWarpsPerCta * 32,
-                                                      smem_bytes<D>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, decode_attention_kernel<D, CH, S>, kWarpsPerCta * 32,
+                                                      smem_bytes<D, CH, S>());
         occ = o > 0 ? o : 1;
     }
     return occ;
@@ -480,10 +496,10 @@ WsLayout ws_layout(int bh, int d) {
     return w;
 }
 
-template <int D>
+template <int D, int CH, int S>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const int occ = ctas_per_sm<D>();
+    const int occ = ctas_per_sm<D, CH, S>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * kWarpsPerCta;
     // context split: only when (b, h) units cannot fill the resident warps
@@ -496,7 +512,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         if (nsplit < 1) nsplit = 1;
     }
     int split_len = (a.cur_len + nsplit - 1) / nsplit;
-    split_len = (split_len + Cfg<D>::CH - 1) / Cfg<D>::CH * Cfg<D>::CH;
+    split_len = (split_len + CH - 1) / CH * CH;
     nsplit = (a.cur_len + split_len - 1) / split_len;
     const int units = bh * nsplit;
     const int ctas = min(ctas_resident, (units + kWarpsPerCta - 1) / kWarpsPerCta);
@@ -520,7 +536,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
-    decode_attention_kernel<D><<<ctas, kWarpsPerCta * 32, smem_bytes<D>(), stream>>>(P);
+    decode_attention_kernel<D, CH, S><<<ctas, kWarpsPerCta * 32, smem_bytes<D, CH, S>(), stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -530,9 +546,41 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int /*t_cap
     return ws_layout(batch * heads, head_dim).total;
 }
 
+// Stage geometry (tokens per stage CH, ring depth S).  The defaults come from
+// the B200 sweep recorded in DESIGN.md; FLEXQ_ATTN_CFG="<CH>,<S>" selects
+// another compiled variant (tuning only).
+static int tune_variant() {
+    static int v = -2;
+    if (v == -2) {
+        v = -1;
+        const char* e = getenv("FLEXQ_ATTN_CFG");
+        if (e) {
+            int ch = 0, st = 0;
+            if (sscanf(e, "%d,%d", &ch, &st) == 2) v = ch * 16 + st;
+        }
+    }
+    return v;
+}
+
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
-    if (a.head_dim == 128) return launch<128>(a, stream);
-    return launch<64>(a, stream);
+    const int v = tune_variant();
+    if (a.head_dim == 128) {
+        switch (v) {
+            case 32 * 16 + 2: return launch<128, 32, 2>(a, stream);
+            case 32 * 16 + 3: return launch<128, 32, 3>(a, stream);
+            case 32 * 16 + 4: return launch<128, 32, 4>(a, stream);
+            case 16 * 16 + 3: return launch<128, 16, 3>(a, stream);
+            case 16 * 16 + 4: return launch<128, 16, 4>(a, stream);
+            case 16 * 16 + 5: return launch<128, 16, 5>(a, stream);
+            case 64 * 16 + 2: return launch<128, 64, 2>(a, stream);
+            default: return launch<128, 32, 4>(a, stream);
+        }
+    }
+    switch (v) {
+        case 32 * 16 + 4: return launch<64, 32, 4>(a, stream);
+        case 64 * 16 + 2: return launch<64, 64, 2>(a, stream);
+        default: return launch<64, 64, 3>(a, stream);
+    }
 }
 
 }  // namespace flexq
