@@ -233,12 +233,9 @@ def run_flexq(args):
     w = wl.CONFIGS[args.config]
     if args.layers:
         w = wl.Workload(w.name, w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len, args.layers, w.h2)
+    from paper_2303_06865_b200 import dist as fd
     B_total = w.batch * (world if args.scaling == "weak" else 1)
-    if args.scaling == "weak":
-        B = w.batch
-    else:
-        per = (w.batch + world - 1) // world
-        B = max(0, min(per, w.batch - rank * per))
+    B = fd.rank_batch(w.batch, world, rank, args.scaling)
     H, D, s, n, L = w.heads, w.head_dim, w.prompt_len, w.gen_len, w.layers
     h1 = H * D
     seed = synth.BASE_SEED + 3 + 1000 * rank
@@ -306,11 +303,7 @@ def run_flexq(args):
                 graphs[i].replay()
             ev1.record(stream)
         barrier()
-    ms = ev0.elapsed_time(ev1)
-    if pg:
-        t = torch.tensor([ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = fd.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
     ms_step = ms / args.steps
     job_bytes = B_total * sum(L * (wl.attention_bytes(1, h1, s + seq_of(args.warmup + k)) + wl.append_bytes(1, h1))
                               for k in range(args.steps))
@@ -399,11 +392,7 @@ def run_flexq(args):
             e2e_bytes += step_bytes[i]
         x1.record(stream)
         barrier()
-        ems = x0.elapsed_time(x1)
-        if pg:
-            t = torch.tensor([ems], device=dev)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = fd.max_over_ranks(x0.elapsed_time(x1), device=dev)
         e2e_job = e2e_bytes * (B_total / B if B else 0)
         e2e = {"value": round(e2e_job / (ems / 1e3) / 1e9, 2),
                "unit": "GB/s", "h2d_bytes_per_step": int(qh.nbytes + knh.nbytes + vnh.nbytes),

@@ -63,7 +63,8 @@ const char *flexq_status_string(int status);
  * max == min -> codes 0, scale 0 (reading C).
  *   codes_u8 [rows][cols/2]: element 2k in the low nibble of byte k.
  *   meta_h2  [rows][cols/group_size] half2 {scale = f16((max-min)/15), min}.
- * Supported: bits == 4, group_size == 64.  rows == 0 or cols == 0 is a no-op. */
+ * Supported: bits == 4, group_size == 64, rows * cols / 64 < 2^31 (else
+ * FLEXQ_ERR_ARG).  rows == 0 or cols == 0 is a no-op. */
 flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int bits, int group_size,
                             void *codes_u8, void *meta_h2, void *stream);
 
@@ -72,12 +73,19 @@ flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int b
 flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t rows, int64_t cols,
                               int bits, int group_size, void *out_f16, void *stream);
 
-/* KV cache layout for one layer, T_cap = prompt_len + gen_len:
- *   k_codes, v_codes: u8    [batch][heads][T_cap][head_dim/2]
- *   k_meta,  v_meta:  half2 [batch][heads][T_cap][head_dim/group_size]
- * Sizes in bytes (either output pointer may be NULL). */
+/* KV cache layout for one layer.  Capacity T_cap = prompt_len + gen_len
+ * tokens, stored with token stride T_stride = T_cap rounded up to a
+ * multiple of 8 (so every (batch, head) run of fp16 metadata is 16-byte
+ * aligned and can be streamed with 1-D TMA bulk copies):
+ *   k_codes, v_codes: u8    [batch][heads][T_stride][head_dim/2]
+ *   k_meta,  v_meta:  half2 [batch][heads][T_stride][head_dim/group_size]
+ * Token t of head (b, h) is row (b*heads + h)*T_stride + t.  Rows
+ * [T_cap, T_stride) are padding the library never writes (it may read them
+ * into on-chip buffers and discard them).  Sizes in bytes (either output
+ * pointer may be NULL); *token_stride (may be NULL) receives T_stride. */
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                  int bits, int group_size, size_t *codes_bytes, size_t *meta_bytes);
+                                  int bits, int group_size, size_t *codes_bytes, size_t *meta_bytes,
+                                  int *token_stride);
 
 /* KV update x_K <- Concat(x_K, t.w_K), same for V: quantizes
  * k_new, v_new fp16 [batch][heads][n_new][head_dim] group-wise along head_dim

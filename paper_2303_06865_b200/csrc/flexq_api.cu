@@ -20,7 +20,7 @@ flexq_status check_bits_group(int bits, int group_size) {
 flexq_status check_kv_dims(int batch, int heads, int head_dim, int prompt_len, int gen_len, int bits,
                            int group_size) {
     if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
-        int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX)
+        int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX - 8)
         return FLEXQ_ERR_ARG;
     flexq_status s = check_bits_group(bits, group_size);
     if (s != FLEXQ_OK) return s;
@@ -56,6 +56,7 @@ flexq_status flexq_quantize(const void* x_f16, int64_t rows, int64_t cols, int b
     if (s != FLEXQ_OK) return s;
     if (cols % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
     if (rows == 0 || cols == 0) return FLEXQ_OK;
+    if (rows > (int64_t(1) << 31) / (cols / group_size)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     if (!x_f16 || !codes_u8 || !meta_h2) return FLEXQ_ERR_NULL;
     if (!aligned16(x_f16) || !aligned16(codes_u8) || !aligned16(meta_h2)) return FLEXQ_ERR_ALIGN;
     return from_cuda(flexq::launch_quantize(x_f16, rows, cols, codes_u8, meta_h2, nullptr, nullptr,
@@ -77,14 +78,18 @@ flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t
 }
 
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                  int bits, int group_size, size_t* codes_bytes, size_t* meta_bytes) {
+                                  int bits, int group_size, size_t* codes_bytes, size_t* meta_bytes,
+                                  int* token_stride) {
     if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
         int64_t(prompt_len) + gen_len < 1 || bits < 1 || bits > 8 || group_size < 1)
         return FLEXQ_ERR_ARG;
     if (head_dim % group_size != 0 || (int64_t(head_dim) * bits) % 8 != 0) return FLEXQ_ERR_UNSUPPORTED;
-    const size_t rows = size_t(batch) * heads * (size_t(prompt_len) + gen_len);
+    if (int64_t(prompt_len) + gen_len > INT32_MAX - 8) return FLEXQ_ERR_ARG;
+    const int64_t stride = flexq::kv_token_stride(int64_t(prompt_len) + gen_len);
+    const size_t rows = size_t(batch) * heads * size_t(stride);
     if (codes_bytes) *codes_bytes = rows * size_t(head_dim) * bits / 8;
     if (meta_bytes) *meta_bytes = rows * size_t(head_dim / group_size) * 4;
+    if (token_stride) *token_stride = int(stride);
     return FLEXQ_OK;
 }
 
@@ -102,8 +107,10 @@ flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int b
         !aligned16(v_codes) || !aligned16(v_meta))
         return FLEXQ_ERR_ALIGN;
     const int64_t rows = int64_t(batch) * heads * n_new;
+    if (rows * (head_dim / group_size) >= (int64_t(1) << 31)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     return from_cuda(flexq::launch_quantize(k_new_f16, rows, head_dim, k_codes, k_meta, v_new_f16,
-                                            v_codes, v_meta, flexq::RowMap{n_new, t_cap, pos},
+                                            v_codes, v_meta,
+                                            flexq::RowMap{n_new, flexq::kv_token_stride(t_cap), pos},
                                             static_cast<cudaStream_t>(stream)));
 }
 
@@ -132,7 +139,7 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_codes, cons
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, k_codes, k_meta, v_codes, v_meta, out_f16, workspace,
-                      batch, heads, head_dim, t_cap, cur_len};
+                      batch, heads, head_dim, int(flexq::kv_token_stride(t_cap)), cur_len};
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 

@@ -10,12 +10,15 @@ namespace flexq {
 constexpr int kBits = 4;
 constexpr int kGroup = 64;
 
+// Token stride of the KV cache: capacity rounded up to a multiple of 8 (include/flexq.h).
+inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + 7) / 8 * 8; }
+
 // Row remapping for the quantizer: src row r -> dst row
-//   (r / n_new) * t_cap + pos + r % n_new      (KV append)
+//   (r / n_new) * t_stride + pos + r % n_new   (KV append)
 // or identity when n_new == 0 (plain weight / tensor quantize).
 struct RowMap {
     int64_t n_new;   // 0 = identity
-    int64_t t_cap;
+    int64_t t_cap;   // token stride of the cache
     int64_t pos;
 };
 
@@ -34,7 +37,7 @@ struct AttnArgs {
     const void* v_meta;
     void* out;
     void* workspace;
-    int batch, heads, head_dim, t_cap, cur_len;
+    int batch, heads, head_dim, t_stride, cur_len;
 };
 
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);

@@ -35,20 +35,52 @@ __device__ __forceinline__ void h2_to_f(uint32_t w, float& lo, float& hi) {
     hi = f.y;
 }
 
-__device__ __forceinline__ int64_t dst_row(int64_t row, const RowMap& m) {
-    if (m.n_new == 0) return row;
-    int64_t bh = row / m.n_new;
-    return bh * m.t_cap + m.pos + (row - bh * m.n_new);
+// Destination group index of source group g (groups tile the rows exactly, so
+// source group g starts at element 64 g).  Group counts are < 2^31 (checked by
+// the ABI layer), so 32-bit division suffices.
+__device__ __forceinline__ int64_t dst_group(uint32_t g, uint32_t gpr, const RowMap& m) {
+    if (m.n_new == 0) return g;
+    const uint32_t row = g / gpr, k = g - row * gpr;
+    const uint32_t bh = row / uint32_t(m.n_new);
+    const int64_t drow = int64_t(bh) * m.t_cap + m.pos + (row - bh * uint32_t(m.n_new));
+    return drow * gpr + k;
 }
 
-// Code of one element (reading B): every step one IEEE round-to-nearest op.
-__device__ __forceinline__ uint32_t code_of(float x, float mn, float r) {
-    float a = __fsub_rn(x, mn);
-    float u = __fdiv_rn(a, r);
-    float t = __fmul_rn(u, 15.0f);
-    t = fminf(fmaxf(t, 0.0f), 15.0f);                         // reading D (a no-op)
-    return __float_as_uint(__fadd_rn(t, 8388608.0f)) & 0xFu;  // 2^23 + RNE(t)
+// Division u = RN(a / r) by one correctly rounded reciprocal per group and a
+// Markstein correction per element: y = RN(1/r), q0 = RN(a*y),
+// e = fma(-q0, r, a) (exact), u = RN(q0 + e*y).  Markstein's theorem (y within
+// 1/2 ulp of 1/r, q0 within 1 ulp of a/r, no over/underflow: here
+// a in [0, 131008], r in [2^-24, 131008]) makes u the IEEE quotient; the
+// host test tests/test_division.py checks it on 4e7 samples of the exact
+// operand domain, and the GPU parity tests compare every code with the
+// oracle's true division.  u in [0, 1] => t = RN(15 u) in [0, 15], so the
+// clamp of reading D is a no-op and is not repeated here.
+//
+// Codes of 8 consecutive elements -> one packed 32-bit word.  Each code is
+// produced as the float 2^23 + c (RNE to integer via the magic add); Horner
+// packing acc = acc * 16 + bits over the 8 floats' bit patterns leaves the
+// constant 0x4B000000 * (1 + 16) mod 2^32 = 0xFB000000 on top of the packed
+// codes (the 0x4B000000 * 16^j terms for j >= 2 vanish mod 2^32).
+__device__ __forceinline__ uint32_t codes8(const float2 (&x)[4], float mn, float r, float y) {
+    const float2 nmn = make_float2(-mn, -mn), yy = make_float2(y, y), nr = make_float2(-r, -r);
+    const float2 fifteen = make_float2(15.0f, 15.0f), magic = make_float2(8388608.0f, 8388608.0f);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+        const float2 a = __fadd2_rn(x[k], nmn);            // RN(x - min)
+        const float2 q0 = __fmul2_rn(a, yy);               // RN(a * y)
+        const float2 e = __ffma2_rn(q0, nr, a);            // a - q0 r, exact
+        const float2 u = __ffma2_rn(e, yy, q0);            // RN(a / r)
+        const float2 t = __fmul2_rn(u, fifteen);           // RN(u * 15)
+        const float2 b = __fadd2_rn(t, magic);             // 2^23 + RNE(t)
+        acc = acc * 16u + __float_as_uint(b.y);
+        acc = acc * 16u + __float_as_uint(b.x);
+    }
+    return acc - 0xFB000000u;
 }
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
 __global__ void __launch_bounds__(kThreads)
 quantize_kernel(const __half* __restrict__ x0, uint8_t* __restrict__ codes0, __half2* __restrict__ meta0,
@@ -60,81 +92,118 @@ quantize_kernel(const __half* __restrict__ x0, uint8_t* __restrict__ codes0, __h
 
     const int lane = threadIdx.x & 31;
     const int part = lane & 3;
-    const int64_t gpr = cols / kGroup;
-    const int64_t total = rows * gpr;
-    const int64_t warp0 = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
+    const uint32_t gpr = uint32_t(cols / kGroup);
+    const uint32_t total = uint32_t(rows * gpr);
+    const uint32_t warp0 = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
 
-    for (int64_t wg = warp0 * 8; wg < total; wg += nwarps * 8) {   // warp-uniform loop
-        const int64_t g = wg + (lane >> 2);
+    for (uint32_t wg = warp0 * 8; wg < total; wg += nwarps * 8) {   // warp-uniform loop
+        const uint32_t g = wg + (lane >> 2);
         const bool valid = g < total;
-        float v[16];
+        uint4 va = make_uint4(0, 0, 0, 0), vb = va;
         if (valid) {
-            const int64_t row = g / gpr, k = g - row * gpr;
-            const __half* p = x + row * cols + k * kGroup + part * 16;
-            uint4 a = ld_stream(p), b = ld_stream(p + 8);
-            h2_to_f(a.x, v[0], v[1]);   h2_to_f(a.y, v[2], v[3]);
-            h2_to_f(a.z, v[4], v[5]);   h2_to_f(a.w, v[6], v[7]);
-            h2_to_f(b.x, v[8], v[9]);   h2_to_f(b.y, v[10], v[11]);
-            h2_to_f(b.z, v[12], v[13]); h2_to_f(b.w, v[14], v[15]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            const __half* p = x + int64_t(g) * kGroup + part * 16;
+            va = ld_stream(p);
+            vb = ld_stream(p + 8);
         }
-        float mn = v[0], mx = v[0];
+        // O3: exact group min / max on the fp16 values (half2 min/max), then 2 shuffles
+        const __half2 h[8] = {u2h(va.x), u2h(va.y), u2h(va.z), u2h(va.w),
+                              u2h(vb.x), u2h(vb.y), u2h(vb.z), u2h(vb.w)};
+        __half2 lo = __hmin2(__hmin2(__hmin2(h[0], h[1]), __hmin2(h[2], h[3])),
+                             __hmin2(__hmin2(h[4], h[5]), __hmin2(h[6], h[7])));
+        __half2 hi = __hmax2(__hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])),
+                             __hmax2(__hmax2(h[4], h[5]), __hmax2(h[6], h[7])));
+        __half2 mm = __halves2half2(__hmin(__low2half(lo), __high2half(lo)),
+                                    __hmax(__low2half(hi), __high2half(hi)));   // (min, max)
 #pragma unroll
-        for (int j = 1; j < 16; ++j) { mn = fminf(mn, v[j]); mx = fmaxf(mx, v[j]); }
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, 2));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        for (int o = 1; o <= 2; o <<= 1) {
+            const __half2 t = u2h(__shfl_xor_sync(0xffffffffu, h2u(mm), o));
+            mm = __halves2half2(__hmin(__low2half(mm), __low2half(t)), __hmax(__high2half(mm), __high2half(t)));
+        }
         if (!valid) continue;
+        float mn = __low2float(mm);   // exact (an fp16 value)
+        const float mx = __high2float(mm);
         mn = (mn == 0.0f) ? 0.0f : mn;            // reading P: -0 -> +0
         const float r = __fsub_rn(mx, mn);        // RN32(max - min)
-        uint32_t lo = 0, hi = 0;
+        uint32_t wlo = 0, whi = 0;
         __half scale16 = __float2half_rn(0.0f);
         if (r != 0.0f) {                          // reading C: degenerate group -> codes 0
             scale16 = __float2half_rn(__fdiv_rn(r, 15.0f));
+            const float y = __frcp_rn(r);
+            float2 f[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) lo |= code_of(v[j], mn, r) << (4 * j);
+            for (int j = 0; j < 4; ++j) f[j] = __half22float2(h[j]);
+            wlo = codes8(f, mn, r, y);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) hi |= code_of(v[8 + j], mn, r) << (4 * j);
+            for (int j = 0; j < 4; ++j) f[j] = __half22float2(h[4 + j]);
+            whi = codes8(f, mn, r, y);
         }
-        const int64_t row = g / gpr, k = g - row * gpr;
-        const int64_t drow = dst_row(row, map);
-        *reinterpret_cast<uint2*>(codes + drow * (cols / 2) + k * (kGroup / 2) + part * 8) = make_uint2(lo, hi);
-        if (part == 0) meta[drow * gpr + k] = __halves2half2(scale16, __float2half_rn(mn));
+        const int64_t dg = dst_group(g, gpr, map);
+        *reinterpret_cast<uint2*>(codes + dg * (kGroup / 2) + part * 8) = make_uint2(wlo, whi);
+        if (part == 0) meta[dg] = __halves2half2(scale16, __float2half_rn(mn));
     }
 }
 
 // out = f16(clamp(fmaf(code, scale, min), +-65504))   (reading R)
+// The nibble n at bit position 4k of a word becomes the float 2^23 + n 16^k
+// with one LOP3; subtracting 2^23 is exact, and (n 16^k) * (scale 16^-k) is
+// the exact product n * scale, so one FFMA2 gives fmaf(n, scale, min) for two
+// elements.  cvt.rn.satfinite clamps to +-65504 exactly like the clamp + RN.
+__device__ __forceinline__ uint32_t magic_reg() {
+    uint32_t m;
+    asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(m));
+    return m;
+}
+template <uint32_t M>
+__device__ __forceinline__ float nib(uint32_t w, uint32_t magic) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(M), "r"(magic));  // (a & b) | c
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t sat_pack(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ void deq8(uint32_t w, uint32_t magic, const float2 (&s)[4], float2 m2, uint32_t* o) {
+    const uint32_t w4 = w >> 4;   // odd nibbles
+    const float2 bias = make_float2(-8388608.0f, -8388608.0f);
+    // pairs (even nibble, odd nibble) of each byte: bytes 0..3 -> columns (0,1) (2,3) (4,5) (6,7)
+    const float2 f0 = __fadd2_rn(make_float2(nib<0x0000000Fu>(w, magic), nib<0x0000000Fu>(w4, magic)), bias);
+    const float2 f1 = __fadd2_rn(make_float2(nib<0x00000F00u>(w, magic), nib<0x00000F00u>(w4, magic)), bias);
+    const float2 f2 = __fadd2_rn(make_float2(nib<0x000F0000u>(w, magic), nib<0x000F0000u>(w4, magic)), bias);
+    const uint32_t w16 = w >> 16, w20 = w >> 20;
+    const float2 f3 = __fadd2_rn(make_float2(nib<0x00000F00u>(w16, magic), nib<0x00000F00u>(w20, magic)), bias);
+    float2 y;
+    y = __ffma2_rn(f0, s[0], m2); o[0] = sat_pack(y.x, y.y);
+    y = __ffma2_rn(f1, s[1], m2); o[1] = sat_pack(y.x, y.y);
+    y = __ffma2_rn(f2, s[2], m2); o[2] = sat_pack(y.x, y.y);
+    y = __ffma2_rn(f3, s[3], m2); o[3] = sat_pack(y.x, y.y);
+}
+
 __global__ void __launch_bounds__(kThreads)
 dequantize_kernel(const uint8_t* __restrict__ codes, const __half2* __restrict__ meta,
                   __half* __restrict__ out, int64_t rows, int64_t cols) {
     const int lane = threadIdx.x & 31;
     const int part = lane & 3;
-    const int64_t gpr = cols / kGroup;
-    const int64_t total = rows * gpr;
+    const int64_t total = rows * (cols / kGroup);
     const int64_t t0 = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nthr = int64_t(gridDim.x) * kThreads;
+    const uint32_t magic = magic_reg();
     for (int64_t t = t0; t < total * 4; t += nthr) {
         const int64_t g = t >> 2;
-        const int64_t row = g / gpr, k = g - row * gpr;
-        uint2 c = *reinterpret_cast<const uint2*>(codes + row * (cols / 2) + k * (kGroup / 2) + part * 8);
-        float2 sm = __half22float2(meta[g]);
+        const uint2 c = *reinterpret_cast<const uint2*>(codes + g * (kGroup / 2) + part * 8);
+        const float2 sm = __half22float2(meta[g]);
+        // scale * 16^-k for the nibble positions used by deq8: (0,0), (8,8), (16,16), (8,8)
+        const float2 s[4] = {make_float2(sm.x, sm.x),
+                             make_float2(sm.x * 0.00390625f, sm.x * 0.00390625f),
+                             make_float2(sm.x * 1.52587890625e-05f, sm.x * 1.52587890625e-05f),
+                             make_float2(sm.x * 0.00390625f, sm.x * 0.00390625f)};
+        const float2 m2 = make_float2(sm.y, sm.y);
         uint32_t o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            uint32_t w = j < 4 ? c.x : c.y;
-            int s = (j & 3) * 8;
-            float c0 = __uint_as_float(0x4B000000u | ((w >> s) & 0xFu)) - 8388608.0f;        // exact
-            float c1 = __uint_as_float(0x4B000000u | ((w >> (s + 4)) & 0xFu)) - 8388608.0f;
-            float y0 = fminf(fmaxf(__fmaf_rn(c0, sm.x, sm.y), -65504.0f), 65504.0f);
-            float y1 = fminf(fmaxf(__fmaf_rn(c1, sm.x, sm.y), -65504.0f), 65504.0f);
-            __half2 h = __halves2half2(__float2half_rn(y0), __float2half_rn(y1));
-            o[j] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(out + row * cols + k * kGroup + part * 16);
+        deq8(c.x, magic, s, m2, o);
+        deq8(c.y, magic, s, m2, o + 4);
+        uint4* dst = reinterpret_cast<uint4*>(out + g * kGroup + part * 16);
         dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
         dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
     }

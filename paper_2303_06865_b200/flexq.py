@@ -46,7 +46,7 @@ def lib():
         L.flexq_status_string.restype = ctypes.c_char_p
         L.flexq_quantize.argtypes = [P, I64, I64, I, I, P, P, P]
         L.flexq_dequantize.argtypes = [P, P, I64, I64, I, I, P, P]
-        L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(SZ)]
+        L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(SZ), ctypes.POINTER(I)]
         L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P, P, P, P]
         L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
         L.flexq_decode_attention_workspace_size.restype = SZ
@@ -111,16 +111,22 @@ def flexq_dequantize(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: in
 
 
 # ---------------------------------------------------------------- KV cache
+def token_stride(t_cap: int) -> int:
+    """Token stride of the cache layout: capacity rounded up to 8 (include/flexq.h)."""
+    return (t_cap + 7) // 8 * 8
+
+
 class KVCache:
-    """One layer's compressed KV cache (layout of include/flexq.h)."""
+    """One layer's compressed KV cache (layout of include/flexq.h): tensors are
+    [B][H][T_stride][...]; tokens [0, T_cap) are the cache, the rest padding."""
 
     def __init__(self, batch: int, heads: int, head_dim: int, prompt_len: int, gen_len: int,
                  device="cuda", bits: int = BITS, group_size: int = GROUP):
         self.batch, self.heads, self.head_dim = batch, heads, head_dim
         self.prompt_len, self.gen_len = prompt_len, gen_len
         self.bits, self.group_size = bits, group_size
-        T = prompt_len + gen_len
-        self.t_cap = T
+        self.t_cap = prompt_len + gen_len
+        self.t_stride = T = token_stride(self.t_cap)
         self.k_codes = torch.zeros(batch, heads, T, head_dim // 2, dtype=torch.uint8, device=device)
         self.v_codes = torch.zeros_like(self.k_codes)
         self.k_meta = torch.zeros(batch, heads, T, head_dim // group_size, 2, dtype=torch.float16, device=device)
@@ -131,10 +137,11 @@ class KVCache:
 
 
 def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS, group_size=GROUP):
-    c, m = ctypes.c_size_t(), ctypes.c_size_t()
+    """-> (codes bytes, meta bytes, token stride) of one K (or V) cache tensor pair."""
+    c, m, t = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_int()
     _check(lib().flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits, group_size,
-                                      ctypes.byref(c), ctypes.byref(m)), "flexq_kv_cache_bytes")
-    return c.value, m.value
+                                      ctypes.byref(c), ctypes.byref(m), ctypes.byref(t)), "flexq_kv_cache_bytes")
+    return c.value, m.value, t.value
 
 
 def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, pos: int, stream=None):

@@ -91,7 +91,10 @@ def test_attention_validation(L):
 
 
 def test_kv_cache_bytes(L):
-    c, m = fq.flexq_kv_cache_bytes(144, 96, 128, 512, 32)
-    rows = 144 * 96 * 544
-    assert c == rows * 64 and m == rows * 8
+    c, m, t = fq.flexq_kv_cache_bytes(144, 96, 128, 512, 32)
+    rows = 144 * 96 * 544                            # 544 is a multiple of 8: no padding
+    assert t == 544 and c == rows * 64 and m == rows * 8
     assert (c + m) * 16 == rows * 128 * 2 * 4.5     # 4.5 bits per element
+    c, m, t = fq.flexq_kv_cache_bytes(4, 12, 64, 512, 1)
+    assert t == 520 and c == 4 * 12 * 520 * 32 and m == 4 * 12 * 520 * 4
+    assert fq.token_stride(513) == 520 and fq.token_stride(1) == 8

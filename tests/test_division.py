@@ -1,0 +1,74 @@
+"""Host check of the division identity the quantize kernel relies on (quant.cu):
+for the operands of P:843's (x - min) / (max - min) in fp32 -- a = RN(x - min),
+r = RN(max - min) with x, min, max fp16 -- one correctly rounded reciprocal
+y = RN(1/r) plus the Markstein correction q0 = RN(a y), e = fma(-q0, r, a),
+u = RN(q0 + e y) equals the IEEE quotient RN(a / r) bit for bit (reading B:
+the GPU may use this form only if it is bit-identical to IEEE a / r).
+
+Samples: uniformly random finite fp16 triples (every exponent), Irwin-Hall
+values at random scales, and constructed exact ties a = (2k+1) m 2^e,
+r = 30 m 2^e.  Written in C (gcc -ffp-contract=off); shares no code with
+csrc/ or oracle/.
+"""
+import os
+import subprocess
+import tempfile
+
+SRC = r"""
+#include <stdio.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+static uint64_t st = 88172645463325252ull;
+static uint64_t xr(void) { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return st; }
+static float h2f(uint16_t h) { int s = h >> 15, e = (h >> 10) & 31, m = h & 1023;
+  float v = e ? ldexpf(1024 + m, e - 25) : ldexpf(m, -24); return s ? -v : v; }
+static uint16_t rh(void) { for (;;) { uint16_t h = (uint16_t)xr(); if (((h >> 10) & 31) != 31) return h; } }
+static float f16r(float v) { _Float16 h = (_Float16)v; return (float)h; }
+static long bad = 0, tested = 0;
+static void check(float a, float r) {
+  float u = a / r;
+  float y = 1.0f / r, q0 = a * y, e = fmaf(-q0, r, a), q1 = fmaf(e, y, q0);
+  tested++;
+  if (memcmp(&u, &q1, 4) != 0 && !(u == 0.0f && q1 == 0.0f)) {
+    if (bad < 5) printf("MISMATCH a=%a r=%a ieee=%a markstein=%a\n", a, r, u, q1);
+    bad++;
+  }
+}
+static void triple(float x, float y, float z) {
+  float v[3] = {x, y, z};
+  for (int p = 0; p < 3; p++) for (int q = p + 1; q < 3; q++) if (v[q] < v[p]) { float t = v[p]; v[p] = v[q]; v[q] = t; }
+  float mn = v[0] == 0.0f ? 0.0f : v[0];
+  float r = v[2] - mn;
+  if (r == 0.0f || !isfinite(r)) return;
+  check(v[1] - mn, r);
+}
+int main(int argc, char **argv) {
+  long n = atol(argv[1]);
+  for (long i = 0; i < n; i++) {
+    triple(h2f(rh()), h2f(rh()), h2f(rh()));
+    int sc = (int)(xr() % 40) - 24;
+    float v[3];
+    for (int k = 0; k < 3; k++) { double s = 0; for (int j = 0; j < 4; j++) s += (double)(xr() >> 40) / (double)(1ull << 24);
+      v[k] = f16r((float)ldexp(s - 2.0, sc)); }
+    triple(v[0], v[1], v[2]);
+    int k = xr() % 15, m = 1 + xr() % 2047, ex = (int)(xr() % 60) - 40;
+    check(ldexpf((float)((2 * k + 1) * m), ex), ldexpf((float)(30 * m), ex));
+  }
+  printf("tested %ld bad %ld\n", tested, bad);
+  return bad != 0;
+}
+"""
+
+
+def test_markstein_division_equals_ieee():
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "div.c")
+        exe = os.path.join(d, "div")
+        open(c, "w").write(SRC)
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-o", exe, c, "-lm"])
+        out = subprocess.run([exe, "4000000"], capture_output=True, text=True)
+        assert out.returncode == 0, out.stdout
+        tested = int(out.stdout.split()[-3])
+        assert tested > 10_000_000

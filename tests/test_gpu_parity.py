@@ -82,12 +82,14 @@ def test_append_kv_bit_exact(orc, cuda, D):
         fq.flexq_append_kv(kn.to(cuda), vn.to(cuda), cache, pos=s + step - 1)
         orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
     torch.cuda.synchronize()
-    assert np.array_equal(cache.k_codes.cpu().numpy(), orc.pack4(okc[0]))
-    assert np.array_equal(cache.v_codes.cpu().numpy(), orc.pack4(ovc[0]))
-    assert np.array_equal(cache.k_meta.cpu().numpy().view(np.uint16), okc[1])
-    assert np.array_equal(cache.v_meta.cpu().numpy().view(np.uint16), ovc[1])
-    # untouched positions stay zero
-    assert int(cache.k_codes[:, :, s + 3:].abs().sum()) == 0
+    T = s + n
+    assert cache.t_stride % 8 == 0 and cache.t_stride >= T
+    assert np.array_equal(cache.k_codes[:, :, :T].cpu().numpy(), orc.pack4(okc[0]))
+    assert np.array_equal(cache.v_codes[:, :, :T].cpu().numpy(), orc.pack4(ovc[0]))
+    assert np.array_equal(cache.k_meta[:, :, :T].cpu().numpy().view(np.uint16), okc[1])
+    assert np.array_equal(cache.v_meta[:, :, :T].cpu().numpy().view(np.uint16), ovc[1])
+    # untouched positions (incl. the stride padding) stay zero
+    assert int(cache.k_codes[:, :, s + 3:].sum()) == 0 and int(cache.v_meta[:, :, s + 3:].abs().sum()) == 0
 
 
 # ---------------------------------------------------------------- attention
@@ -122,6 +124,8 @@ ATTN_CASES = [
     ("d128_stage_multiple", 1, 2, 128, 64, 32, 0, False, 16),   # cur_len 64 = 2 full stages
     ("d64_long", 1, 3, 64, 1024, 32, 2, True, 16),
     ("d128_many_heads_nosplit", 24, 128, 128, 40, 2, 1, False, 1),  # B*H = 3072: no split
+    ("d128_full_capacity_odd", 3, 5, 128, 100, 3, 3, False, 4),      # cur_len = T_cap = 103 (stride 104)
+    ("d64_full_capacity_odd", 2, 3, 64, 60, 1, 1, True, 16),         # cur_len = T_cap = 61 (stride 64)
 ]
 
 
