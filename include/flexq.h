@@ -73,29 +73,32 @@ flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int b
 flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t rows, int64_t cols,
                               int bits, int group_size, void *out_f16, void *stream);
 
-/* KV cache layout for one layer.  Capacity T_cap = prompt_len + gen_len
- * tokens, stored with token stride T_stride = T_cap rounded up to a
- * multiple of 8 (so every (batch, head) run of fp16 metadata is 16-byte
- * aligned and can be streamed with 1-D TMA bulk copies):
- *   k_codes, v_codes: u8    [batch][heads][T_stride][head_dim/2]
- *   k_meta,  v_meta:  half2 [batch][heads][T_stride][head_dim/group_size]
- * Token t of head (b, h) is row (b*heads + h)*T_stride + t.  Rows
- * [T_cap, T_stride) are padding the library never writes (it may read them
- * into on-chip buffers and discard them).  Sizes in bytes (either output
- * pointer may be NULL); *token_stride (may be NULL) receives T_stride. */
+/* KV cache layout for one layer (one buffer holds K and V).  Capacity
+ * T_cap = prompt_len + gen_len tokens, stored in chunks of 32 tokens
+ * per (batch, head); T_stride = T_cap rounded up to a multiple of 32.  With
+ * D = head_dim, CB = D/2 code bytes and MB = D/16 metadata bytes per token,
+ * one chunk is 36*D bytes:
+ *     [K codes 32 x CB][V codes 32 x CB][K meta 32 x MB][V meta 32 x MB]
+ * and the buffer is u8 [batch][heads][T_stride/32][36*D].  Token t of head
+ * (b, h) lives in chunk (b*heads + h)*T_stride/32 + t/32, slot t%32; its K
+ * codes are D/2 bytes (element 2k in the low nibble of byte k), its K
+ * meta D/64 half2 {scale, min} (groups of 64 along D).  A chunk is the
+ * unit the attention kernel streams with one 1-D TMA bulk copy.  Tokens
+ * [T_cap, T_stride) are padding the library never writes.
+ * *cache_bytes (may be NULL) receives the buffer size, *token_stride (may be
+ * NULL) T_stride.  Supported: bits == 4, group_size == 64, head_dim in {64, 128}. */
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                  int bits, int group_size, size_t *codes_bytes, size_t *meta_bytes,
-                                  int *token_stride);
+                                  int bits, int group_size, size_t *cache_bytes, int *token_stride);
 
 /* KV update x_K <- Concat(x_K, t.w_K), same for V: quantizes
  * k_new, v_new fp16 [batch][heads][n_new][head_dim] group-wise along head_dim
- * and writes cache tokens [pos, pos + n_new) of every (batch, head).
- * Prompt fill is pos = 0, n_new = prompt_len; a decode step is n_new = 1.
- * Touches no other cache position. */
+ * and writes cache tokens [pos, pos + n_new) of every (batch, head)
+ * into kv_cache (layout above).  Prompt fill is pos = 0, n_new = prompt_len;
+ * a decode step is n_new = 1.  Touches no other cache position. */
 flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
                              int batch, int heads, int head_dim, int prompt_len, int gen_len,
                              int pos, int n_new, int bits, int group_size,
-                             void *k_codes, void *k_meta, void *v_codes, void *v_meta, void *stream);
+                             void *kv_cache, void *stream);
 
 /* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
  * arguments).  Layout: 256 B of scheduler counters, 4 B per (batch, head) of
@@ -110,12 +113,11 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
  *   out fp16 [batch][heads][head_dim] =
  *     softmax(q . K^[0:cur_len]^T / sqrt(head_dim)) . V^[0:cur_len]
  * with K^, V^ = fmaf(code, scale, min) in fp32, never rounded to fp16 (reading
- * M); q fp16 [batch][heads][head_dim].  Cache layout as above; tokens
- * [cur_len, T_cap) are never read.  Accuracy: |out - exact| <=
+ * M); q fp16 [batch][heads][head_dim].  Cache layout as above; tokens at
+ * positions >= cur_len do not influence the result (the kernel may stream the
+ * rest of the last 32-token chunk into shared memory and discard it).  Accuracy: |out - exact| <=
  * max(2e-3, 1e-2 |exact|) per element (reading Q). */
-flexq_status flexq_decode_attention(const void *q_f16,
-                                    const void *k_codes, const void *k_meta,
-                                    const void *v_codes, const void *v_meta,
+flexq_status flexq_decode_attention(const void *q_f16, const void *kv_cache,
                                     int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                     int cur_len, int bits, int group_size, void *out_f16,
                                     void *workspace, size_t workspace_bytes, void *stream);

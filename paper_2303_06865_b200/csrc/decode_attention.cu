@@ -44,8 +44,11 @@ constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 64;
 constexpr float kRescaleThresh = 8.0f; // log2 units: p <= 2^8 between rescales
 
+// One stage = one 32-token cache chunk (include/flexq.h layout), streamed
+// with a single bulk copy; its smem image has the HBM chunk's layout.
 template <int D, int CH_>
 struct Cfg {
+    static_assert(CH_ == kChunk, "a stage is one cache chunk");
     static constexpr int LPT = D / 32;                 // lanes per token
     static constexpr int TPI = 32 / LPT;               // tokens per warp iteration
     static constexpr int CH = CH_;                     // tokens per stage
@@ -55,7 +58,8 @@ struct Cfg {
     static constexpr int OFF_VC = CH * CB;
     static constexpr int OFF_KM = 2 * CH * CB;
     static constexpr int OFF_VM = 2 * CH * CB + CH * MB;
-    static constexpr int OFF_Q = 2 * CH * (CB + MB);
+    static constexpr int CHUNK = 2 * CH * (CB + MB);  // = 36 D bytes
+    static constexpr int OFF_Q = CHUNK;
     static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
     static_assert(STAGE % 16 == 0, "stage alignment");
     static_assert(CH % TPI == 0, "stage must hold whole warp iterations");
@@ -148,16 +152,13 @@ struct Desc {        // per-slot descriptor (shared memory)
 
 struct Params {
     const __half* q;
-    const uint8_t* kc;
-    const uint8_t* km;
-    const uint8_t* vc;
-    const uint8_t* vm;
+    const uint8_t* kv;   // chunked KV cache
     __half* out;
     uint32_t* ctrl;      // [0] next ticket, [1] finished warps
     uint32_t* tickets;   // per (b, h): finished splits
     float* part;         // [unit][D] partial numerators
     float2* ml;          // [unit] (m, l)
-    int bh_total, t_stride, cur_len, nsplit, split_len;
+    int bh_total, chunks, cur_len, nsplit, split_len;
     float qscale;        // log2(e) / sqrt(D)
 };
 
@@ -297,22 +298,16 @@ decode_attention_kernel(const Params P) {
             d.unit = p_unit; d.bh = p_bh; d.n = n;
             d.flags = (p_tok == p_first ? 1 : 0) | (p_tok + n >= p_end ? 2 : 0);
             if (lane == 0) {
-                // one elected lane: 4-5 TMA bulk copies onto the slot's mbarrier.  The token
-                // stride is a multiple of 8 (include/flexq.h), so every source is 16-B aligned;
-                // the meta size is rounded up to 16 B (reads at most 3 padding tokens).
+                // one elected lane: one TMA bulk copy of the 32-token chunk (K, V codes
+                // and metadata; p_tok is a multiple of 32) + q on a unit's first stage.
                 uint8_t* sb = ring + slot * C::STAGE;
-                const int64_t row = int64_t(p_bh) * P.t_stride + p_tok;
-                const uint32_t cbytes = uint32_t(n) * C::CB;
-                const uint32_t mbytes = (uint32_t(n) * C::MB + 15u) & ~15u;
-                const uint32_t qbytes = (d.flags & 1) ? 2u * D : 0u;
+                const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
+                const bool first = d.flags & 1;
                 desc[slot] = d;
                 fence_proxy_async();
-                mbar_expect_tx(&bars[slot], 2 * cbytes + 2 * mbytes + qbytes);
-                bulk_g2s(sb, P.kc + row * C::CB, cbytes, &bars[slot], policy);
-                bulk_g2s(sb + C::OFF_VC, P.vc + row * C::CB, cbytes, &bars[slot], policy);
-                bulk_g2s(sb + C::OFF_KM, P.km + row * C::MB, mbytes, &bars[slot], policy);
-                bulk_g2s(sb + C::OFF_VM, P.vm + row * C::MB, mbytes, &bars[slot], policy);
-                if (qbytes) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, qbytes, &bars[slot], policy);
+                mbar_expect_tx(&bars[slot], C::CHUNK + (first ? 2 * D : 0));
+                bulk_g2s(sb, P.kv + chunk * C::CHUNK, C::CHUNK, &bars[slot], policy);
+                if (first) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
             }
             p_tok += n;
             if (p_tok >= p_end) next_unit();
@@ -537,17 +532,14 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     Params P;
     P.q = static_cast<const __half*>(a.q);
-    P.kc = static_cast<const uint8_t*>(a.k_codes);
-    P.km = static_cast<const uint8_t*>(a.k_meta);
-    P.vc = static_cast<const uint8_t*>(a.v_codes);
-    P.vm = static_cast<const uint8_t*>(a.v_meta);
+    P.kv = static_cast<const uint8_t*>(a.kv);
     P.out = static_cast<__half*>(a.out);
     P.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
     P.tickets = reinterpret_cast<uint32_t*>(ws + w.tickets);
     P.part = reinterpret_cast<float*>(ws + w.part);
     P.ml = reinterpret_cast<float2*>(ws + w.ml);
     P.bh_total = bh;
-    P.t_stride = a.t_stride;
+    P.chunks = a.chunks;
     P.cur_len = a.cur_len;
     P.nsplit = nsplit;
     P.split_len = split_len;
@@ -575,7 +567,7 @@ int tune_variant() {
 
 }  // namespace
 
-size_t attention_workspace_bytes(int batch, int heads, int head_dim, int /*t_cap*/) {
+size_t attention_workspace_bytes(int batch, int heads, int head_dim) {
     return ws_layout(batch * heads, head_dim).total;
 }
 
@@ -583,20 +575,17 @@ cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     const int v = tune_variant();
     if (a.head_dim == 128) {
         switch (v) {
-            case FLEXQ_V(32, 2, 4): return launch<128, 32, 2, 4>(a, stream);
             case FLEXQ_V(32, 3, 4): return launch<128, 32, 3, 4>(a, stream);
             case FLEXQ_V(32, 3, 5): return launch<128, 32, 3, 5>(a, stream);
             case FLEXQ_V(32, 4, 4): return launch<128, 32, 4, 4>(a, stream);
-            case FLEXQ_V(64, 2, 2): return launch<128, 64, 2, 2>(a, stream);
-            case FLEXQ_V(64, 2, 4): return launch<128, 64, 2, 4>(a, stream);
-            case FLEXQ_V(16, 4, 4): return launch<128, 16, 4, 4>(a, stream);
+            case FLEXQ_V(32, 2, 2): return launch<128, 32, 2, 2>(a, stream);
             default: return launch<128, 32, 2, 4>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(32, 2, 4): return launch<64, 32, 2, 4>(a, stream);
-        case FLEXQ_V(64, 3, 4): return launch<64, 64, 3, 4>(a, stream);
-        default: return launch<64, 64, 2, 4>(a, stream);
+        case FLEXQ_V(32, 3, 4): return launch<64, 32, 3, 4>(a, stream);
+        case FLEXQ_V(32, 4, 4): return launch<64, 32, 4, 4>(a, stream);
+        default: return launch<64, 32, 2, 4>(a, stream);
     }
 }
 

@@ -20,7 +20,7 @@ flexq_status check_bits_group(int bits, int group_size) {
 flexq_status check_kv_dims(int batch, int heads, int head_dim, int prompt_len, int gen_len, int bits,
                            int group_size) {
     if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
-        int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX - 8)
+        int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX - flexq::kChunk)
         return FLEXQ_ERR_ARG;
     flexq_status s = check_bits_group(bits, group_size);
     if (s != FLEXQ_OK) return s;
@@ -59,9 +59,7 @@ flexq_status flexq_quantize(const void* x_f16, int64_t rows, int64_t cols, int b
     if (rows > (int64_t(1) << 31) / (cols / group_size)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     if (!x_f16 || !codes_u8 || !meta_h2) return FLEXQ_ERR_NULL;
     if (!aligned16(x_f16) || !aligned16(codes_u8) || !aligned16(meta_h2)) return FLEXQ_ERR_ALIGN;
-    return from_cuda(flexq::launch_quantize(x_f16, rows, cols, codes_u8, meta_h2, nullptr, nullptr,
-                                            nullptr, flexq::RowMap{0, 0, 0},
-                                            static_cast<cudaStream_t>(stream)));
+    return from_cuda(flexq::launch_quantize(x_f16, rows, cols, codes_u8, meta_h2, static_cast<cudaStream_t>(stream)));
 }
 
 flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t rows, int64_t cols,
@@ -78,50 +76,40 @@ flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t
 }
 
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                  int bits, int group_size, size_t* codes_bytes, size_t* meta_bytes,
-                                  int* token_stride) {
-    if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
-        int64_t(prompt_len) + gen_len < 1 || bits < 1 || bits > 8 || group_size < 1)
-        return FLEXQ_ERR_ARG;
-    if (head_dim % group_size != 0 || (int64_t(head_dim) * bits) % 8 != 0) return FLEXQ_ERR_UNSUPPORTED;
-    if (int64_t(prompt_len) + gen_len > INT32_MAX - 8) return FLEXQ_ERR_ARG;
+                                  int bits, int group_size, size_t* cache_bytes, int* token_stride) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s != FLEXQ_OK) return s;
     const int64_t stride = flexq::kv_token_stride(int64_t(prompt_len) + gen_len);
-    const size_t rows = size_t(batch) * heads * size_t(stride);
-    if (codes_bytes) *codes_bytes = rows * size_t(head_dim) * bits / 8;
-    if (meta_bytes) *meta_bytes = rows * size_t(head_dim / group_size) * 4;
+    if (cache_bytes)
+        *cache_bytes = size_t(batch) * heads * size_t(stride / flexq::kChunk) * size_t(flexq::kv_chunk_bytes(head_dim));
     if (token_stride) *token_stride = int(stride);
     return FLEXQ_OK;
 }
 
 flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int batch, int heads,
                              int head_dim, int prompt_len, int gen_len, int pos, int n_new, int bits,
-                             int group_size, void* k_codes, void* k_meta, void* v_codes, void* v_meta,
-                             void* stream) {
+                             int group_size, void* kv_cache, void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
     if (s == FLEXQ_ERR_ARG) return s;
     const int64_t t_cap = int64_t(prompt_len) + gen_len;
     if (pos < 0 || n_new < 1 || int64_t(pos) + n_new > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
-    if (!k_new_f16 || !v_new_f16 || !k_codes || !k_meta || !v_codes || !v_meta) return FLEXQ_ERR_NULL;
-    if (!aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_codes) || !aligned16(k_meta) ||
-        !aligned16(v_codes) || !aligned16(v_meta))
-        return FLEXQ_ERR_ALIGN;
+    if (!k_new_f16 || !v_new_f16 || !kv_cache) return FLEXQ_ERR_NULL;
+    if (!aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(kv_cache)) return FLEXQ_ERR_ALIGN;
     const int64_t rows = int64_t(batch) * heads * n_new;
     if (rows * (head_dim / group_size) >= (int64_t(1) << 31)) return FLEXQ_ERR_ARG;   // < 2^31 groups
-    return from_cuda(flexq::launch_quantize(k_new_f16, rows, head_dim, k_codes, k_meta, v_new_f16,
-                                            v_codes, v_meta,
-                                            flexq::RowMap{n_new, flexq::kv_token_stride(t_cap), pos},
-                                            static_cast<cudaStream_t>(stream)));
+    const flexq::KvDst d{n_new, pos, flexq::kv_token_stride(t_cap) / flexq::kChunk};
+    return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, kv_cache, d,
+                                             static_cast<cudaStream_t>(stream)));
 }
 
 size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
                                              int gen_len, int bits, int group_size) {
     if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
-    return flexq::attention_workspace_bytes(batch, heads, head_dim, prompt_len + gen_len);
+    return flexq::attention_workspace_bytes(batch, heads, head_dim);
 }
 
-flexq_status flexq_decode_attention(const void* q_f16, const void* k_codes, const void* k_meta,
-                                    const void* v_codes, const void* v_meta, int batch, int heads,
+flexq_status flexq_decode_attention(const void* q_f16, const void* kv_cache, int batch, int heads,
                                     int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
                                     int group_size, void* out_f16, void* workspace,
                                     size_t workspace_bytes, void* stream) {
@@ -130,16 +118,13 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_codes, cons
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
-    if (!q_f16 || !k_codes || !k_meta || !v_codes || !v_meta || !out_f16) return FLEXQ_ERR_NULL;
-    if (!aligned16(q_f16) || !aligned16(k_codes) || !aligned16(k_meta) || !aligned16(v_codes) ||
-        !aligned16(v_meta) || !aligned16(out_f16))
-        return FLEXQ_ERR_ALIGN;
-    if (!workspace ||
-        workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+    if (!q_f16 || !kv_cache || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(q_f16) || !aligned16(kv_cache) || !aligned16(out_f16)) return FLEXQ_ERR_ALIGN;
+    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
-    flexq::AttnArgs a{q_f16, k_codes, k_meta, v_codes, v_meta, out_f16, workspace,
-                      batch, heads, head_dim, int(flexq::kv_token_stride(t_cap)), cur_len};
+    flexq::AttnArgs a{q_f16, kv_cache, out_f16, workspace, batch, heads, head_dim,
+                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len};
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 

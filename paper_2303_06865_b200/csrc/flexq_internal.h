@@ -10,37 +10,37 @@ namespace flexq {
 constexpr int kBits = 4;
 constexpr int kGroup = 64;
 
-// Token stride of the KV cache: capacity rounded up to a multiple of 8 (include/flexq.h).
-inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + 7) / 8 * 8; }
+// KV cache layout (include/flexq.h): per (batch, head), a run of chunks of
+// kChunk tokens; chunk = [K codes kChunk x D/2][V codes kChunk x D/2]
+//                        [K meta kChunk x D/16][V meta kChunk x D/16]  bytes.
+constexpr int kChunk = 32;
+inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + kChunk - 1) / kChunk * kChunk; }
+inline int64_t kv_chunk_bytes(int64_t d) { return int64_t(kChunk) * (d + d / 8); }   // 36 d
 
-// Row remapping for the quantizer: src row r -> dst row
-//   (r / n_new) * t_stride + pos + r % n_new   (KV append)
-// or identity when n_new == 0 (plain weight / tensor quantize).
-struct RowMap {
-    int64_t n_new;   // 0 = identity
-    int64_t t_cap;   // token stride of the cache
+// Destination of a KV append: source rows are (bh, t) with t in [0, n_new),
+// written at token pos + t of head bh.
+struct KvDst {
+    int64_t n_new;
     int64_t pos;
+    int64_t chunks;   // chunks per (batch, head) = token stride / kChunk
 };
 
 cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* codes, void* meta,
-                            const void* x2, void* codes2, void* meta2, RowMap map,
                             cudaStream_t stream);
-
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* kv,
+                             KvDst dst, cudaStream_t stream);
 cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols,
                               void* out, cudaStream_t stream);
 
 struct AttnArgs {
     const void* q;
-    const void* k_codes;
-    const void* k_meta;
-    const void* v_codes;
-    const void* v_meta;
+    const void* kv;
     void* out;
     void* workspace;
-    int batch, heads, head_dim, t_stride, cur_len;
+    int batch, heads, head_dim, chunks, cur_len;
 };
 
-size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
+size_t attention_workspace_bytes(int batch, int heads, int head_dim);
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
 
 }  // namespace flexq

@@ -11,6 +11,7 @@
 // loads; group min/max by two xor-shuffles; each lane stores 8 B of packed
 // codes (a warp writes 256 contiguous bytes); lane 0 of the group stores the
 // half2 {scale, min}.  HBM-bound: 2 B read + 0.5625 B written per element.
+// The KV append is the same kernel writing into the chunked cache layout.
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -28,23 +29,33 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
     return r;
 }
 
-__device__ __forceinline__ void h2_to_f(uint32_t w, float& lo, float& hi) {
-    __half2 h = *reinterpret_cast<__half2*>(&w);
-    float2 f = __half22float2(h);   // exact
-    lo = f.x;
-    hi = f.y;
-}
-
-// Destination group index of source group g (groups tile the rows exactly, so
-// source group g starts at element 64 g).  Group counts are < 2^31 (checked by
-// the ABI layer), so 32-bit division suffices.
-__device__ __forceinline__ int64_t dst_group(uint32_t g, uint32_t gpr, const RowMap& m) {
-    if (m.n_new == 0) return g;
-    const uint32_t row = g / gpr, k = g - row * gpr;
-    const uint32_t bh = row / uint32_t(m.n_new);
-    const int64_t drow = int64_t(bh) * m.t_cap + m.pos + (row - bh * uint32_t(m.n_new));
-    return drow * gpr + k;
-}
+// Byte offsets of the packed codes (8 B per lane) and of the half2 meta of
+// source group g.  Plain tensors: row-major [rows][cols/2] codes, [rows][cols/64]
+// meta.  KV append: the chunked cache layout of include/flexq.h; source row
+// r = bh * n_new + t goes to token pos + t of head bh, K (kv = 0) or V (kv = 1).
+struct PlainDst {
+    __device__ __forceinline__ void operator()(uint32_t g, uint32_t /*gpr*/, int /*kv*/, int64_t& codes_off,
+                                               int64_t& meta_off) const {
+        codes_off = int64_t(g) * (kGroup / 2);
+        meta_off = int64_t(g) * 4;
+    }
+};
+struct KvChunkDst {
+    KvDst d;
+    int cb;   // code bytes per token (D/2)
+    __device__ __forceinline__ void operator()(uint32_t g, uint32_t gpr, int kv, int64_t& codes_off,
+                                               int64_t& meta_off) const {
+        const uint32_t row = g / gpr, k = g - row * gpr;
+        const uint32_t bh = row / uint32_t(d.n_new);
+        const int64_t t = d.pos + (row - bh * uint32_t(d.n_new));
+        const int64_t chunk = int64_t(bh) * d.chunks + (t >> 5);
+        const int slot = int(t & (kChunk - 1));
+        const int64_t base = chunk * (int64_t(kChunk) * (2 * cb + cb / 4));   // kv_chunk_bytes(2 cb)
+        const int mb = cb / 8;                                                 // meta bytes per token
+        codes_off = base + (kv * kChunk + slot) * cb + k * (kGroup / 2);
+        meta_off = base + 2 * kChunk * cb + (kv * kChunk + slot) * mb + k * 4;
+    }
+};
 
 // Division u = RN(a / r) by one correctly rounded reciprocal per group and a
 // Markstein correction per element: y = RN(1/r), q0 = RN(a*y),
@@ -63,7 +74,6 @@ __device__ __forceinline__ int64_t dst_group(uint32_t g, uint32_t gpr, const Row
 // codes (the 0x4B000000 * 16^j terms for j >= 2 vanish mod 2^32).
 __device__ __forceinline__ uint32_t codes8(const float2 (&x)[4], float mn, float r, float y) {
     const float2 nmn = make_float2(-mn, -mn), yy = make_float2(y, y), nr = make_float2(-r, -r);
-    const float2 fifteen = make_float2(15.0f, 15.0f), magic = make_float2(8388608.0f, 8388608.0f);
     uint32_t acc = 0;
 #pragma unroll
     for (int k = 3; k >= 0; --k) {
@@ -71,10 +81,14 @@ __device__ __forceinline__ uint32_t codes8(const float2 (&x)[4], float mn, float
         const float2 q0 = __fmul2_rn(a, yy);               // RN(a * y)
         const float2 e = __ffma2_rn(q0, nr, a);            // a - q0 r, exact
         const float2 u = __ffma2_rn(e, yy, q0);            // RN(a / r)
-        const float2 t = __fmul2_rn(u, fifteen);           // RN(u * 15)
-        const float2 b = __fadd2_rn(t, magic);             // 2^23 + RNE(t)
-        acc = acc * 16u + __float_as_uint(b.y);
-        acc = acc * 16u + __float_as_uint(b.x);
+        // t = RN(u * 15) and the magic add stay scalar __fmul_rn / __fadd_rn: ptxas
+        // contracts a packed mul.rn.f32x2 + add.rn.f32x2 pair into one FFMA2 (single
+        // rounding), which breaks RNE at exact .5 ties (reading A); the scalar
+        // round-to-nearest intrinsics are never merged.
+        const float t0 = __fmul_rn(u.x, 15.0f), t1 = __fmul_rn(u.y, 15.0f);
+        const float b0 = __fadd_rn(t0, 8388608.0f), b1 = __fadd_rn(t1, 8388608.0f);   // 2^23 + RNE(t)
+        acc = acc * 16u + __float_as_uint(b1);
+        acc = acc * 16u + __float_as_uint(b0);
     }
     return acc - 0xFB000000u;
 }
@@ -82,13 +96,14 @@ __device__ __forceinline__ uint32_t codes8(const float2 (&x)[4], float mn, float
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
+// codes_base / meta_base: byte base pointers of the destination (the same
+// buffer for the KV cache); blockIdx.y selects source x0 (K) or x1 (V).
+template <class Dst>
 __global__ void __launch_bounds__(kThreads)
-quantize_kernel(const __half* __restrict__ x0, uint8_t* __restrict__ codes0, __half2* __restrict__ meta0,
-                const __half* __restrict__ x1, uint8_t* __restrict__ codes1, __half2* __restrict__ meta1,
-                int64_t rows, int64_t cols, RowMap map) {
-    const __half* x = blockIdx.y ? x1 : x0;
-    uint8_t* codes = blockIdx.y ? codes1 : codes0;
-    __half2* meta = blockIdx.y ? meta1 : meta0;
+quantize_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, uint8_t* __restrict__ codes_base,
+                uint8_t* __restrict__ meta_base, int64_t rows, int64_t cols, Dst dst) {
+    const int kv = blockIdx.y;
+    const __half* x = kv ? x1 : x0;
 
     const int lane = threadIdx.x & 31;
     const int part = lane & 3;
@@ -138,9 +153,10 @@ quantize_kernel(const __half* __restrict__ x0, uint8_t* __restrict__ codes0, __h
             for (int j = 0; j < 4; ++j) f[j] = __half22float2(h[4 + j]);
             whi = codes8(f, mn, r, y);
         }
-        const int64_t dg = dst_group(g, gpr, map);
-        *reinterpret_cast<uint2*>(codes + dg * (kGroup / 2) + part * 8) = make_uint2(wlo, whi);
-        if (part == 0) meta[dg] = __halves2half2(scale16, __float2half_rn(mn));
+        int64_t co, mo;
+        dst(g, gpr, kv, co, mo);
+        *reinterpret_cast<uint2*>(codes_base + co + part * 8) = make_uint2(wlo, whi);
+        if (part == 0) *reinterpret_cast<__half2*>(meta_base + mo) = __halves2half2(scale16, __float2half_rn(mn));
     }
 }
 
@@ -223,18 +239,29 @@ int num_sms() {
 }  // namespace
 
 cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* codes, void* meta,
-                            const void* x2, void* codes2, void* meta2, RowMap map,
                             cudaStream_t stream) {
     const int64_t groups = rows * (cols / kGroup);
     if (groups == 0) return cudaSuccess;
     int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;
     const int64_t cap = int64_t(num_sms()) * 8;
     if (blocks > cap) blocks = cap;
-    dim3 grid(unsigned(blocks), x2 ? 2u : 1u);
-    quantize_kernel<<<grid, kThreads, 0, stream>>>(
-        static_cast<const __half*>(x), static_cast<uint8_t*>(codes), static_cast<__half2*>(meta),
-        static_cast<const __half*>(x2), static_cast<uint8_t*>(codes2), static_cast<__half2*>(meta2),
-        rows, cols, map);
+    quantize_kernel<PlainDst><<<unsigned(blocks), kThreads, 0, stream>>>(
+        static_cast<const __half*>(x), nullptr, static_cast<uint8_t*>(codes), static_cast<uint8_t*>(meta), rows,
+        cols, PlainDst{});
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* kv, KvDst d,
+                             cudaStream_t stream) {
+    const int64_t groups = rows * (head_dim / kGroup);
+    if (groups == 0) return cudaSuccess;
+    int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;
+    const int64_t cap = int64_t(num_sms()) * 8;
+    if (blocks > cap) blocks = cap;
+    dim3 grid(unsigned(blocks), 2u);
+    quantize_kernel<KvChunkDst><<<grid, kThreads, 0, stream>>>(
+        static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<uint8_t*>(kv),
+        static_cast<uint8_t*>(kv), rows, head_dim, KvChunkDst{d, head_dim / 2});
     return cudaGetLastError();
 }
 

@@ -46,11 +46,11 @@ def lib():
         L.flexq_status_string.restype = ctypes.c_char_p
         L.flexq_quantize.argtypes = [P, I64, I64, I, I, P, P, P]
         L.flexq_dequantize.argtypes = [P, P, I64, I64, I, I, P, P]
-        L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(SZ), ctypes.POINTER(I)]
-        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P, P, P, P]
+        L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(I)]
+        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P]
         L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
         L.flexq_decode_attention_workspace_size.restype = SZ
-        L.flexq_decode_attention.argtypes = [P] * 5 + [I] * 8 + [P, P, SZ, P]
+        L.flexq_decode_attention.argtypes = [P, P] + [I] * 8 + [P, P, SZ, P]
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
                   "flexq_decode_attention"):
             getattr(L, f).restype = I
@@ -111,14 +111,19 @@ def flexq_dequantize(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: in
 
 
 # ---------------------------------------------------------------- KV cache
+CHUNK = 32   # tokens per cache chunk (include/flexq.h)
+
+
 def token_stride(t_cap: int) -> int:
-    """Token stride of the cache layout: capacity rounded up to 8 (include/flexq.h)."""
-    return (t_cap + 7) // 8 * 8
+    """Token stride of the cache layout: capacity rounded up to a chunk (include/flexq.h)."""
+    return (t_cap + CHUNK - 1) // CHUNK * CHUNK
 
 
 class KVCache:
-    """One layer's compressed KV cache (layout of include/flexq.h): tensors are
-    [B][H][T_stride][...]; tokens [0, T_cap) are the cache, the rest padding."""
+    """One layer's compressed K + V cache in the chunked layout of include/flexq.h:
+    `kv` u8 [B][H][T_stride/32][36*D], chunk = [K codes 32 x D/2][V codes 32 x D/2]
+    [K meta 32 x D/16][V meta 32 x D/16].  The *_codes() / *_meta() accessors are
+    layout views for tests and inspection (tokens [0, T_stride))."""
 
     def __init__(self, batch: int, heads: int, head_dim: int, prompt_len: int, gen_len: int,
                  device="cuda", bits: int = BITS, group_size: int = GROUP):
@@ -126,22 +131,39 @@ class KVCache:
         self.prompt_len, self.gen_len = prompt_len, gen_len
         self.bits, self.group_size = bits, group_size
         self.t_cap = prompt_len + gen_len
-        self.t_stride = T = token_stride(self.t_cap)
-        self.k_codes = torch.zeros(batch, heads, T, head_dim // 2, dtype=torch.uint8, device=device)
-        self.v_codes = torch.zeros_like(self.k_codes)
-        self.k_meta = torch.zeros(batch, heads, T, head_dim // group_size, 2, dtype=torch.float16, device=device)
-        self.v_meta = torch.zeros_like(self.k_meta)
+        self.t_stride = token_stride(self.t_cap)
+        self.chunks = self.t_stride // CHUNK
+        self.kv = torch.zeros(batch, heads, self.chunks, 36 * head_dim, dtype=torch.uint8, device=device)
 
     def nbytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.k_codes, self.v_codes, self.k_meta, self.v_meta))
+        return self.kv.numel()
+
+    def _part(self, offset: int, per_token: int) -> torch.Tensor:
+        B, H, NC = self.batch, self.heads, self.chunks
+        x = self.kv[..., offset:offset + CHUNK * per_token].reshape(B, H, NC, CHUNK, per_token)
+        return x.reshape(B, H, NC * CHUNK, per_token)
+
+    def k_codes(self) -> torch.Tensor:            # u8 [B][H][T_stride][D/2]
+        return self._part(0, self.head_dim // 2)
+
+    def v_codes(self) -> torch.Tensor:
+        return self._part(CHUNK * self.head_dim // 2, self.head_dim // 2)
+
+    def k_meta(self) -> torch.Tensor:             # fp16 [B][H][T_stride][D/64][2] = (scale, min)
+        m = self._part(CHUNK * self.head_dim, self.head_dim // 16)
+        return m.contiguous().view(torch.float16).view(self.batch, self.heads, self.t_stride, -1, 2)
+
+    def v_meta(self) -> torch.Tensor:
+        m = self._part(CHUNK * self.head_dim + CHUNK * self.head_dim // 16, self.head_dim // 16)
+        return m.contiguous().view(torch.float16).view(self.batch, self.heads, self.t_stride, -1, 2)
 
 
 def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS, group_size=GROUP):
-    """-> (codes bytes, meta bytes, token stride) of one K (or V) cache tensor pair."""
-    c, m, t = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_int()
+    """-> (cache bytes of one layer (K and V), token stride)."""
+    c, t = ctypes.c_size_t(), ctypes.c_int()
     _check(lib().flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits, group_size,
-                                      ctypes.byref(c), ctypes.byref(m), ctypes.byref(t)), "flexq_kv_cache_bytes")
-    return c.value, m.value, t.value
+                                      ctypes.byref(c), ctypes.byref(t)), "flexq_kv_cache_bytes")
+    return c.value, t.value
 
 
 def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, pos: int, stream=None):
@@ -151,9 +173,7 @@ def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, po
     B, H, n_new, D = k_new.shape
     _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
                                  cache.gen_len, pos, n_new, cache.bits, cache.group_size,
-                                 cache.k_codes.data_ptr(), cache.k_meta.data_ptr(),
-                                 cache.v_codes.data_ptr(), cache.v_meta.data_ptr(), _stream(stream)),
-           "flexq_append_kv")
+                                 cache.kv.data_ptr(), _stream(stream)), "flexq_append_kv")
 
 
 def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
@@ -165,7 +185,7 @@ def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, ge
 def make_workspace(cache: KVCache) -> torch.Tensor:
     n = flexq_decode_attention_workspace_size(cache.batch, cache.heads, cache.head_dim, cache.prompt_len,
                                               cache.gen_len, cache.bits, cache.group_size)
-    return torch.zeros(n, dtype=torch.uint8, device=cache.k_codes.device)
+    return torch.zeros(n, dtype=torch.uint8, device=cache.kv.device)
 
 
 def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=None, workspace=None,
@@ -176,9 +196,8 @@ def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=No
         out = torch.empty_like(q)
     if workspace is None:
         workspace = make_workspace(cache)
-    _check(lib().flexq_decode_attention(q.data_ptr(), cache.k_codes.data_ptr(), cache.k_meta.data_ptr(),
-                                        cache.v_codes.data_ptr(), cache.v_meta.data_ptr(), cache.batch,
-                                        cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
+    _check(lib().flexq_decode_attention(q.data_ptr(), cache.kv.data_ptr(), cache.batch, cache.heads,
+                                        cache.head_dim, cache.prompt_len, cache.gen_len,
                                         cur_len, cache.bits, cache.group_size, out.data_ptr(),
                                         workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "flexq_decode_attention")

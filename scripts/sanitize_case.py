@@ -1,0 +1,45 @@
+"""Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_case.py
+
+Covers: quantize/dequantize with a ragged row count, prompt fill + 1-token
+append, attention with split-K (few heads) and without, and a cache whose
+capacity is not a multiple of the token stride (cur_len = T_cap, last head:
+the metadata bulk copy rounds up into the stride padding).
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2303_06865_b200 import flexq as fq  # noqa: E402
+from paper_2303_06865_b200 import synth  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda:0")
+    x = synth.fill(1, 1, (37, 192), device=dev)
+    c, m = fq.flexq_quantize(x)
+    fq.flexq_dequantize(c, m)
+    for (B, H, D, s, n) in [(2, 3, 128, 100, 3), (1, 2, 64, 61, 0), (8, 40, 128, 33, 2)]:
+        if n == 0:
+            n = 1
+        cache = fq.KVCache(B, H, D, s, n, device=dev)
+        k = synth.fill(2, 1, (B, H, s, D), device=dev)
+        v = synth.fill(2, 2, (B, H, s, D), device=dev)
+        fq.flexq_append_kv(k, v, cache, pos=0)
+        for i in range(n):
+            kn = synth.fill(2, 10 + i, (B, H, 1, D), device=dev)
+            fq.flexq_append_kv(kn, kn, cache, pos=s + i)
+        q = synth.fill(2, 3, (B, H, D), device=dev)
+        ws = fq.make_workspace(cache)
+        for cur in (1, s, s + n):
+            fq.flexq_decode_attention(q, cache, cur, workspace=ws)
+    torch.cuda.synchronize()
+    print("sanitize case ok")
+
+
+if __name__ == "__main__":
+    main()

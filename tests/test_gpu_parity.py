@@ -83,13 +83,13 @@ def test_append_kv_bit_exact(orc, cuda, D):
         orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
     torch.cuda.synchronize()
     T = s + n
-    assert cache.t_stride % 8 == 0 and cache.t_stride >= T
-    assert np.array_equal(cache.k_codes[:, :, :T].cpu().numpy(), orc.pack4(okc[0]))
-    assert np.array_equal(cache.v_codes[:, :, :T].cpu().numpy(), orc.pack4(ovc[0]))
-    assert np.array_equal(cache.k_meta[:, :, :T].cpu().numpy().view(np.uint16), okc[1])
-    assert np.array_equal(cache.v_meta[:, :, :T].cpu().numpy().view(np.uint16), ovc[1])
+    assert cache.t_stride % 32 == 0 and cache.t_stride >= T
+    assert np.array_equal(cache.k_codes()[:, :, :T].cpu().numpy(), orc.pack4(okc[0]))
+    assert np.array_equal(cache.v_codes()[:, :, :T].cpu().numpy(), orc.pack4(ovc[0]))
+    assert np.array_equal(cache.k_meta()[:, :, :T].cpu().numpy().view(np.uint16), okc[1])
+    assert np.array_equal(cache.v_meta()[:, :, :T].cpu().numpy().view(np.uint16), ovc[1])
     # untouched positions (incl. the stride padding) stay zero
-    assert int(cache.k_codes[:, :, s + 3:].sum()) == 0 and int(cache.v_meta[:, :, s + 3:].abs().sum()) == 0
+    assert int(cache.k_codes()[:, :, s + 3:].sum()) == 0 and int(cache.v_meta()[:, :, s + 3:].abs().sum()) == 0
 
 
 # ---------------------------------------------------------------- attention
@@ -204,6 +204,8 @@ def test_opt175b_full_size_sampled(orc, cuda):
         fq.flexq_append_kv(kn, vn, cache, pos=s + step - 1)
     q = synth.fill(seed, synth.tensor_id(0, synth.Q, steps), (B, H, D), device=cuda)
     out = fq.flexq_decode_attention(q, cache, s + steps).cpu().numpy()
+    kc_all = cache.k_codes().cpu().numpy()
+    vm_all = cache.v_meta().cpu().numpy().view(np.uint16)
     rng = np.random.default_rng(7)
     samples = [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(10)]
     for b, h in samples:
@@ -216,8 +218,8 @@ def test_opt175b_full_size_sampled(orc, cuda):
             vn = synth.gather(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, 1, D), [b, h, slice(None), slice(None)])
             orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s + step - 1)
         # codes of this head are bit-exact ...
-        assert np.array_equal(cache.k_codes[b, h, :s + steps].cpu().numpy(), orc.pack4(okc[0][0, 0, :s + steps]))
-        assert np.array_equal(cache.v_meta[b, h, :s + steps].cpu().numpy().view(np.uint16), ovc[1][0, 0, :s + steps])
+        assert np.array_equal(kc_all[b, h, :s + steps], orc.pack4(okc[0][0, 0, :s + steps]))
+        assert np.array_equal(vm_all[b, h, :s + steps], ovc[1][0, 0, :s + steps])
         # ... and the attention output is in tolerance
         qh = synth.gather(seed, synth.tensor_id(0, synth.Q, steps), (B, H, D), [b, h, slice(None)])
         ref = orc.attention_f64(qh.numpy(), okc, ovc, s + steps)
