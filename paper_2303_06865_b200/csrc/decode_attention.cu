@@ -8,11 +8,16 @@
 // Design:
 //  * Persistent kernel, one warp = one work unit = (b, h, context split);
 //    units handed out by an atomic ticket in the workspace (self-resetting).
-//  * Each warp owns an S-stage shared-memory ring.  One stage = CH tokens of
-//    K codes, V codes and K/V fp16 (scale, min) pairs, loaded by one elected
-//    lane with 1-D TMA bulk copies (cp.async.bulk -> mbarrier complete_tx);
-//    the first stage of a unit also carries q.  Loads run S-1 stages ahead
-//    of the math, across units.
+//  * Each warp owns an S-stage shared-memory ring.  A stage is the K half or
+//    the V half of one 32-token cache chunk (codes + fp16 (scale, min)),
+//    one contiguous run in HBM, loaded by one elected lane with a single 1-D
+//    TMA bulk copy (cp.async.bulk -> mbarrier complete_tx); q rides with the
+//    unit's first stage.  Loads run S-1 stages ahead of the math, across units.
+//  * Two passes per unit, no online rescaling: pass 1 streams the unit's K
+//    halves and writes every score (log2 domain) to a per-warp smem buffer,
+//    pass 2 takes the exact max, streams the V halves and accumulates
+//    p_t = 2^(s_t - M).  Only one of q (pass 1) or the V accumulators (pass
+//    2) is live at a time, which keeps the register footprint small.
 //  * Lane layout: D/32 lanes per token, 16 B of codes (32 nibbles) per lane.
 //    Dequantization is factored out of the inner loop (lever a):
 //      score = sum_g [ scale_g * sum_{j in g} q_j c_j + min_g * sum_{j in g} q_j ]
@@ -22,18 +27,16 @@
 //    is folded into q on the K side and removed once at the end on the V
 //    side), one packed FADD2 per pair removes the 2^23 bias exactly, one
 //    packed FFMA2 per pair accumulates.
-//  * Online softmax in the exp2 domain with a warp-uniform running max that
-//    is only raised when a score exceeds it by > 8 (so p <= 2^8, no
-//    overflow); the final result divides by the sum taken against the same
-//    max, so it is exact math, not an approximation.
 //  * End of unit: reduce-scatter of the 32 per-lane accumulators across the
-//    token lanes (28 shuffles), each lane writes D/32 outputs.  Split units
-//    write (acc, m, l) partials; the last split of a (b, h) (atomic ticket)
-//    merges them with the log-sum-exp rule.
+//    token lanes (28 shuffles), each lane writes D/32 outputs.  Units of a
+//    split (b, h) write (acc, m, l) partials; the last split (atomic ticket)
+//    merges them with the log-sum-exp rule (online-softmax combine).
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "flexq_internal.h"
 
@@ -42,27 +45,24 @@ namespace {
 
 constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 64;
-constexpr float kRescaleThresh = 8.0f; // log2 units: p <= 2^8 between rescales
+constexpr int kMaxUnitTokens = 1024;   // score buffer per warp (4 KB); longer contexts split
 
-// One stage = one 32-token cache chunk (include/flexq.h layout), streamed
-// with a single bulk copy; its smem image has the HBM chunk's layout.
-template <int D, int CH_>
+// One stage = one half (K or V) of a 32-token cache chunk; its smem image has
+// the HBM layout [codes 32 x D/2][meta 32 x D/16].
+template <int D>
 struct Cfg {
-    static_assert(CH_ == kChunk, "a stage is one cache chunk");
     static constexpr int LPT = D / 32;                 // lanes per token
     static constexpr int TPI = 32 / LPT;               // tokens per warp iteration
-    static constexpr int CH = CH_;                     // tokens per stage
+    static constexpr int CH = kChunk;                  // tokens per stage
     static constexpr int CB = D / 2;                   // code bytes per token
     static constexpr int MB = D / 16;                  // meta bytes per token (D/64 half2)
     static constexpr int ITERS = CH / TPI;
-    static constexpr int OFF_VC = CH * CB;
-    static constexpr int OFF_KM = 2 * CH * CB;
-    static constexpr int OFF_VM = 2 * CH * CB + CH * MB;
-    static constexpr int CHUNK = 2 * CH * (CB + MB);  // = 36 D bytes
-    static constexpr int OFF_Q = CHUNK;
-    static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
-    static_assert(STAGE % 16 == 0, "stage alignment");
-    static_assert(CH % TPI == 0, "stage must hold whole warp iterations");
+    static constexpr int HALF = CH * (CB + MB);        // K or V half of a chunk (18 D bytes)
+    static constexpr int CHUNK = 2 * HALF;
+    static constexpr int OFF_M = CH * CB;              // meta inside a half
+    static constexpr int OFF_Q = HALF;
+    static constexpr int STAGE = HALF + 2 * D;         // + q (fp16) for the unit's first stage
+    static_assert(STAGE % 16 == 0 && HALF % 16 == 0, "stage alignment");
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -146,9 +146,10 @@ __device__ __forceinline__ float2 inv_shift(int pair) {
 struct Desc {        // per-slot descriptor (shared memory)
     int unit;        // work unit id (-1: none)
     int bh;          // (batch, head) index of the unit
-    int n;           // tokens in this stage
-    int flags;       // bit0 first stage of unit, bit1 last stage of unit
+    int t0;          // first token of the stage, relative to the unit
+    int flags;       // kFirst | kV | kLastK | kLast, tokens in the stage << 8
 };
+constexpr int kFirst = 1, kV = 2, kLastK = 4, kLast = 8;
 
 struct Params {
     const __half* q;
@@ -162,100 +163,82 @@ struct Params {
     float qscale;        // log2(e) / sqrt(D)
 };
 
-// Per-lane consumer state of the current unit.
-struct Lane {
-    float2 qp[16];   // q * qscale * 2^-k, pairs in unpack8 order
-    float qsum;      // sum of q * qscale over the lane's 32 columns
-    float2 acc[16];  // sum_t (p_t scale_t) c_tj 16^k
-    float m, l, bsum;
-};
-
-// One warp iteration: TPI tokens, one per LPT-lane group.  FULL = every token valid.
-template <int D, int CH, bool FULL>
-__device__ __forceinline__ void consume_iter(Lane& L, const uint8_t* sb, int tok, int n, int sg, int grp,
-                                             uint32_t magic) {
-    using C = Cfg<D, CH>;
-    const bool valid = FULL || tok < n;
-    // ---- K: partial dot over the lane's 32 columns, then the group affine terms
+// Pass 1, one warp iteration: scores of TPI tokens -> smem (log2 domain).
+template <int D, bool FULL>
+__device__ __forceinline__ void k_iter(const float2 (&qp)[16], float qsum, const uint8_t* sb, float* sc, int t0,
+                                       int tok, int n, int sg, int grp, uint32_t magic, float& mx) {
+    using C = Cfg<D>;
     const uint4 kw = lds128(sb + tok * C::CB + sg * 16);
-    const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_KM + tok * C::MB + grp * 4));
+    const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_M + tok * C::MB + grp * 4));
     float2 d0 = make_float2(0.0f, 0.0f), d1 = d0;
-    {
-        float2 f[4];
-        unpack8(kw.x, magic, f);
-        d0 = __ffma2_rn(L.qp[0], f[0], d0); d1 = __ffma2_rn(L.qp[1], f[1], d1);
-        d0 = __ffma2_rn(L.qp[2], f[2], d0); d1 = __ffma2_rn(L.qp[3], f[3], d1);
-        unpack8(kw.y, magic, f);
-        d0 = __ffma2_rn(L.qp[4], f[0], d0); d1 = __ffma2_rn(L.qp[5], f[1], d1);
-        d0 = __ffma2_rn(L.qp[6], f[2], d0); d1 = __ffma2_rn(L.qp[7], f[3], d1);
-        unpack8(kw.z, magic, f);
-        d0 = __ffma2_rn(L.qp[8], f[0], d0); d1 = __ffma2_rn(L.qp[9], f[1], d1);
-        d0 = __ffma2_rn(L.qp[10], f[2], d0); d1 = __ffma2_rn(L.qp[11], f[3], d1);
-        unpack8(kw.w, magic, f);
-        d0 = __ffma2_rn(L.qp[12], f[0], d0); d1 = __ffma2_rn(L.qp[13], f[1], d1);
-        d0 = __ffma2_rn(L.qp[14], f[2], d0); d1 = __ffma2_rn(L.qp[15], f[3], d1);
-    }
+    float2 f[4];
+    unpack8(kw.x, magic, f);
+    d0 = __ffma2_rn(qp[0], f[0], d0); d1 = __ffma2_rn(qp[1], f[1], d1);
+    d0 = __ffma2_rn(qp[2], f[2], d0); d1 = __ffma2_rn(qp[3], f[3], d1);
+    unpack8(kw.y, magic, f);
+    d0 = __ffma2_rn(qp[4], f[0], d0); d1 = __ffma2_rn(qp[5], f[1], d1);
+    d0 = __ffma2_rn(qp[6], f[2], d0); d1 = __ffma2_rn(qp[7], f[3], d1);
+    unpack8(kw.z, magic, f);
+    d0 = __ffma2_rn(qp[8], f[0], d0); d1 = __ffma2_rn(qp[9], f[1], d1);
+    d0 = __ffma2_rn(qp[10], f[2], d0); d1 = __ffma2_rn(qp[11], f[3], d1);
+    unpack8(kw.w, magic, f);
+    d0 = __ffma2_rn(qp[12], f[0], d0); d1 = __ffma2_rn(qp[13], f[1], d1);
+    d0 = __ffma2_rn(qp[14], f[2], d0); d1 = __ffma2_rn(qp[15], f[3], d1);
     d0 = __fadd2_rn(d0, d1);
-    float s = fmaf(km.x, d0.x + d0.y, km.y * L.qsum);
+    float s = fmaf(km.x, d0.x + d0.y, km.y * qsum);
 #pragma unroll
     for (int o = 1; o < C::LPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (!FULL) s = valid ? s : -INFINITY;
-
-    // ---- online softmax (log2 domain), warp-uniform max raised lazily
-    if (__any_sync(0xffffffffu, s > L.m + kRescaleThresh)) {
-        float mx = s;
-#pragma unroll
-        for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const float mnew = fmaxf(L.m, mx);
-        const float sc = ex2(L.m - mnew);     // m = -inf -> 0
-        const float2 sc2 = make_float2(sc, sc);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) L.acc[k] = __fmul2_rn(L.acc[k], sc2);
-        L.l *= sc;
-        L.bsum *= sc;
-        L.m = mnew;
-    }
-    float p = ex2(s - L.m);
-    if (!FULL) p = valid ? p : 0.0f;
-    L.l += p;
-
-    // ---- V: acc_j += (p * scale) * c_j ; bias += p * min
-    const uint4 vw = lds128(sb + C::OFF_VC + tok * C::CB + sg * 16);
-    float2 vm = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_VM + tok * C::MB + grp * 4));
-    if (!FULL) {
-        vm.x = valid ? vm.x : 0.0f;
-        vm.y = valid ? vm.y : 0.0f;
-    }
-    const float a = p * vm.x;
-    L.bsum = fmaf(p, vm.y, L.bsum);
-    const float2 a2 = make_float2(a, a);
-    {
-        float2 f[4];
-        unpack8(vw.x, magic, f);
-        L.acc[0] = __ffma2_rn(a2, f[0], L.acc[0]); L.acc[1] = __ffma2_rn(a2, f[1], L.acc[1]);
-        L.acc[2] = __ffma2_rn(a2, f[2], L.acc[2]); L.acc[3] = __ffma2_rn(a2, f[3], L.acc[3]);
-        unpack8(vw.y, magic, f);
-        L.acc[4] = __ffma2_rn(a2, f[0], L.acc[4]); L.acc[5] = __ffma2_rn(a2, f[1], L.acc[5]);
-        L.acc[6] = __ffma2_rn(a2, f[2], L.acc[6]); L.acc[7] = __ffma2_rn(a2, f[3], L.acc[7]);
-        unpack8(vw.z, magic, f);
-        L.acc[8] = __ffma2_rn(a2, f[0], L.acc[8]); L.acc[9] = __ffma2_rn(a2, f[1], L.acc[9]);
-        L.acc[10] = __ffma2_rn(a2, f[2], L.acc[10]); L.acc[11] = __ffma2_rn(a2, f[3], L.acc[11]);
-        unpack8(vw.w, magic, f);
-        L.acc[12] = __ffma2_rn(a2, f[0], L.acc[12]); L.acc[13] = __ffma2_rn(a2, f[1], L.acc[13]);
-        L.acc[14] = __ffma2_rn(a2, f[2], L.acc[14]); L.acc[15] = __ffma2_rn(a2, f[3], L.acc[15]);
+    if (FULL || tok < n) {
+        mx = fmaxf(mx, s);
+        if (sg == 0) sc[t0 + tok] = s;
     }
 }
 
-template <int D, int CH, int S, int WPC>
+// Pass 2, one warp iteration: acc_j += (p scale) c_j, bias += p min for TPI tokens.
+template <int D, bool FULL>
+__device__ __forceinline__ void v_iter(float2 (&acc)[16], float& l, float& bsum, const uint8_t* sb,
+                                       const float* sc, float M, int t0, int tok, int n, int sg, int grp,
+                                       uint32_t magic) {
+    using C = Cfg<D>;
+    const uint4 vw = lds128(sb + tok * C::CB + sg * 16);
+    float2 vm = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_M + tok * C::MB + grp * 4));
+    float p = ex2(sc[t0 + tok] - M);
+    if (!FULL) {
+        const bool valid = tok < n;
+        p = valid ? p : 0.0f;
+        vm.x = valid ? vm.x : 0.0f;
+        vm.y = valid ? vm.y : 0.0f;
+    }
+    l += p;
+    const float a = p * vm.x;
+    bsum = fmaf(p, vm.y, bsum);
+    const float2 a2 = make_float2(a, a);
+    float2 f[4];
+    unpack8(vw.x, magic, f);
+    acc[0] = __ffma2_rn(a2, f[0], acc[0]); acc[1] = __ffma2_rn(a2, f[1], acc[1]);
+    acc[2] = __ffma2_rn(a2, f[2], acc[2]); acc[3] = __ffma2_rn(a2, f[3], acc[3]);
+    unpack8(vw.y, magic, f);
+    acc[4] = __ffma2_rn(a2, f[0], acc[4]); acc[5] = __ffma2_rn(a2, f[1], acc[5]);
+    acc[6] = __ffma2_rn(a2, f[2], acc[6]); acc[7] = __ffma2_rn(a2, f[3], acc[7]);
+    unpack8(vw.z, magic, f);
+    acc[8] = __ffma2_rn(a2, f[0], acc[8]); acc[9] = __ffma2_rn(a2, f[1], acc[9]);
+    acc[10] = __ffma2_rn(a2, f[2], acc[10]); acc[11] = __ffma2_rn(a2, f[3], acc[11]);
+    unpack8(vw.w, magic, f);
+    acc[12] = __ffma2_rn(a2, f[0], acc[12]); acc[13] = __ffma2_rn(a2, f[1], acc[13]);
+    acc[14] = __ffma2_rn(a2, f[2], acc[14]); acc[15] = __ffma2_rn(a2, f[3], acc[15]);
+}
+
+template <int D, int S, int WPC>
 __global__ void __launch_bounds__(WPC * 32, (16 / WPC) > 0 ? (16 / WPC) : 1)
 decode_attention_kernel(const Params P) {
-    using C = Cfg<D, CH>;
+    using C = Cfg<D>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * S * C::STAGE) + warp * S;
-    Desc* desc = reinterpret_cast<Desc*>(smem + WPC * S * (C::STAGE + 8)) + warp * S;
+    float* scores = reinterpret_cast<float*>(smem + WPC * S * C::STAGE) + warp * kMaxUnitTokens;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + kMaxUnitTokens * 4)) + warp * S;
+    Desc* desc = reinterpret_cast<Desc*>(smem + WPC * (S * (C::STAGE + 8) + kMaxUnitTokens * 4)) + warp * S;
 
     const int units = P.bh_total * P.nsplit;
     const uint64_t policy = evict_first_policy();
@@ -265,8 +248,9 @@ decode_attention_kernel(const Params P) {
     }
     __syncwarp();
 
-    // ---------------- producer state (warp-collective; lane 0 issues the bulk copies)
-    int p_unit = -1, p_bh = 0, p_tok = 0, p_end = 0, p_first = 0;
+    // ---------------- producer (warp-uniform state; lane 0 issues the copies)
+    int p_unit = -1, p_bh = 0, p_first = 0, p_end = 0, p_tok = 0;
+    bool p_v = false;
     auto next_unit = [&]() {
         int t = 0;
         if (lane == 0) t = int(atomicAdd(P.ctrl, 1u));
@@ -284,171 +268,216 @@ decode_attention_kernel(const Params P) {
         }
         p_tok = p_first = split * P.split_len;
         p_end = min(P.cur_len, p_tok + P.split_len);
+        p_v = false;
     };
     auto issue = [&](int slot) {
-        Desc d;
-        if (p_unit < 0) {
-            d.unit = -1; d.bh = 0; d.n = 0; d.flags = 0;
-            if (lane == 0) {
-                desc[slot] = d;
-                mbar_expect_tx(&bars[slot], 0);   // the phase completes with no bytes
+        if (lane == 0) {
+            Desc d;
+            uint32_t bytes = 0;
+            if (p_unit >= 0) {
+                const bool first = !p_v && p_tok == p_first;
+                const bool last_of_pass = p_tok + C::CH >= p_end;
+                d.unit = p_unit;
+                d.bh = p_bh;
+                d.t0 = p_tok - p_first;
+                d.flags = (first ? kFirst : 0) | (p_v ? kV : 0) | (!p_v && last_of_pass ? kLastK : 0) |
+                          (p_v && last_of_pass ? kLast : 0) | (min(C::CH, p_end - p_tok) << 8);
+                bytes = C::HALF + (first ? 2 * D : 0);
+            } else {
+                d.unit = -1; d.bh = 0; d.t0 = 0; d.flags = 0;
             }
-        } else {
-            const int n = min(CH, p_end - p_tok);
-            d.unit = p_unit; d.bh = p_bh; d.n = n;
-            d.flags = (p_tok == p_first ? 1 : 0) | (p_tok + n >= p_end ? 2 : 0);
-            if (lane == 0) {
-                // one elected lane: one TMA bulk copy of the 32-token chunk (K, V codes
-                // and metadata; p_tok is a multiple of 32) + q on a unit's first stage.
+            desc[slot] = d;
+            fence_proxy_async();
+            mbar_expect_tx(&bars[slot], bytes);
+            if (p_unit >= 0) {
                 uint8_t* sb = ring + slot * C::STAGE;
                 const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
-                const bool first = d.flags & 1;
-                desc[slot] = d;
-                fence_proxy_async();
-                mbar_expect_tx(&bars[slot], C::CHUNK + (first ? 2 * D : 0));
-                bulk_g2s(sb, P.kv + chunk * C::CHUNK, C::CHUNK, &bars[slot], policy);
-                if (first) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
+                bulk_g2s(sb, P.kv + chunk * C::CHUNK + (p_v ? C::HALF : 0), C::HALF, &bars[slot], policy);
+                if (d.flags & kFirst) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
             }
-            p_tok += n;
-            if (p_tok >= p_end) next_unit();
+        }
+        if (p_unit >= 0) {
+            p_tok += C::CH;
+            if (p_tok >= p_end) {
+                if (!p_v) {
+                    p_v = true;
+                    p_tok = p_first;
+                } else {
+                    next_unit();
+                }
+            }
         }
     };
 
     next_unit();
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < S - 1; ++s) issue(s);
 
-    // ---------------- consumer
+    // ---------------- consumer: per unit, pass 1 (K stages) then pass 2 (V stages)
     const int tl = lane / C::LPT;         // token slot in an iteration
     const int sg = lane % C::LPT;         // 16-byte segment of the token row
     const int grp = sg >> 1;              // quantization group of the segment (64 = 2 x 32)
     const uint32_t magic = magic_reg();
-    Lane L;
-    L.qsum = 0.0f;
-    L.m = -INFINITY;
-    L.l = L.bsum = 0.0f;
 
     int slot = 0;
     uint32_t parity = 0;
-    for (;;) {
+    auto next_stage = [&](Desc& d) -> const uint8_t* {   // issue ahead, wait for the current slot
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
-        const Desc d = desc[slot];
-        if (d.unit < 0) break;
-        const uint8_t* sb = ring + slot * C::STAGE;
-
-        if (d.flags & 1) {   // first stage of a unit: load q, reset state
-            const uint4 q0 = lds128(sb + C::OFF_Q + sg * 64);
-            const uint4 q1 = lds128(sb + C::OFF_Q + sg * 64 + 16);
-            const uint4 q2 = lds128(sb + C::OFF_Q + sg * 64 + 32);
-            const uint4 q3 = lds128(sb + C::OFF_Q + sg * 64 + 48);
-            const uint32_t qw[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
-                                     q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
-            float qs = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {     // pair k = columns 2k, 2k+1 = word k/4, pair k%4
-                float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qw[k]));
-                f = __fmul2_rn(f, make_float2(P.qscale, P.qscale));
-                qs += f.x + f.y;
-                L.qp[k] = __fmul2_rn(f, inv_shift(k & 3));
-            }
-            L.qsum = qs;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) L.acc[k] = make_float2(0.0f, 0.0f);
-            L.m = -INFINITY;
-            L.l = 0.0f;
-            L.bsum = 0.0f;
-        }
-
-        if (d.n == CH) {
-#pragma unroll
-            for (int i = 0; i < C::ITERS; ++i) consume_iter<D, CH, true>(L, sb, i * C::TPI + tl, CH, sg, grp, magic);
-        } else {
-#pragma unroll 1
-            for (int i = 0; i < C::ITERS; ++i) {
-                if (i * C::TPI >= d.n) break;
-                consume_iter<D, CH, false>(L, sb, i * C::TPI + tl, d.n, sg, grp, magic);
-            }
-        }
+        d = desc[slot];
+        return ring + slot * C::STAGE;
+    };
+    auto release = [&]() {
         __syncwarp();
         if (++slot == S) {
             slot = 0;
             parity ^= 1u;
         }
+    };
 
-        if (d.flags & 2) {   // last stage of the unit: reduce and write
+#pragma unroll 1
+    for (;;) {
+        Desc d;
+        const uint8_t* sb = next_stage(d);
+        if (d.unit < 0) break;
+        const int bh = d.bh;
+        const int unit = d.unit;
+
+        // ------------------------------------------------ pass 1: scores -> smem
+        float M;
+        {
+            float2 qp[16];                    // q * qscale * 2^-k, pairs in unpack8 order
+            float qsum = 0.0f;
+            {
+                const uint4 q0 = lds128(sb + C::OFF_Q + sg * 64);
+                const uint4 q1 = lds128(sb + C::OFF_Q + sg * 64 + 16);
+                const uint4 q2 = lds128(sb + C::OFF_Q + sg * 64 + 32);
+                const uint4 q3 = lds128(sb + C::OFF_Q + sg * 64 + 48);
+                const uint32_t qw[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                                         q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
 #pragma unroll
-            for (int k = 0; k < 16; ++k) L.acc[k] = __fmul2_rn(L.acc[k], inv_shift(k & 3));
-            float l = L.l, bsum = L.bsum;
-#pragma unroll
-            for (int o = C::LPT; o < 32; o <<= 1) {
-                l += __shfl_xor_sync(0xffffffffu, l, o);
-                bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
-            }
-            // reduce-scatter of the 32 accumulators over the token lanes
-            float v[32];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) { v[2 * k] = L.acc[k].x; v[2 * k + 1] = L.acc[k].y; }
-            int width = 32;   // live entries
-            int base = 0;     // column offset (within the 32-column segment) of v[0]
-#pragma unroll
-            for (int o = 16; o >= C::LPT; o >>= 1) {
-                const bool upper = (lane & o) != 0;
-                const int half = width >> 1;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    if (k < half) {
-                        const float send = upper ? v[k] : v[k + half];
-                        const float keep = upper ? v[k + half] : v[k];
-                        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
+                for (int k = 0; k < 16; ++k) {     // pair k = columns 2k, 2k+1 = word k/4, pair k%4
+                    float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qw[k]));
+                    f = __fmul2_rn(f, make_float2(P.qscale, P.qscale));
+                    qsum += f.x + f.y;
+                    qp[k] = __fmul2_rn(f, inv_shift(k & 3));
                 }
-                if (upper) base += half;
-                width = half;
             }
-            // lane now holds columns [32 sg + base, + D/32)
-            const int col0 = sg * 32 + base;
-            const int bh = d.bh;
-            if (P.nsplit == 1) {
-                const float inv = 1.0f / l;
-                __half* dst = P.out + int64_t(bh) * D + col0;
-                if constexpr (D == 128) {
-                    __half2 h0 = __floats2half2_rn((v[0] + bsum) * inv, (v[1] + bsum) * inv);
-                    __half2 h1 = __floats2half2_rn((v[2] + bsum) * inv, (v[3] + bsum) * inv);
-                    uint2 w;
-                    w.x = *reinterpret_cast<uint32_t*>(&h0);
-                    w.y = *reinterpret_cast<uint32_t*>(&h1);
-                    *reinterpret_cast<uint2*>(dst) = w;
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (;;) {
+                const int n = d.flags >> 8;
+                if (n == C::CH) {
+#pragma unroll
+                    for (int i = 0; i < C::ITERS; ++i)
+                        k_iter<D, true>(qp, qsum, sb, scores, d.t0, i * C::TPI + tl, n, sg, grp, magic, mx);
                 } else {
-                    *reinterpret_cast<__half2*>(dst) = __floats2half2_rn((v[0] + bsum) * inv, (v[1] + bsum) * inv);
+#pragma unroll 1
+                    for (int i = 0; i * C::TPI < n; ++i)
+                        k_iter<D, false>(qp, qsum, sb, scores, d.t0, i * C::TPI + tl, n, sg, grp, magic, mx);
                 }
-            } else {
-                float* dst = P.part + int64_t(d.unit) * D + col0;
+                const bool last = d.flags & kLastK;
+                release();
+                if (last) break;
+                sb = next_stage(d);
+            }
 #pragma unroll
-                for (int k = 0; k < D / 32; ++k) dst[k] = v[k] + bsum;
-                if (lane == 0) P.ml[d.unit] = make_float2(L.m, l);
-                __threadfence();
-                __syncwarp();
-                uint32_t done = 0;
-                if (lane == 0) done = atomicAdd(&P.tickets[bh], 1u);
-                done = __shfl_sync(0xffffffffu, done, 0);
-                if (done == uint32_t(P.nsplit - 1)) {   // last split of this (b, h): merge
-                    __threadfence();
-                    float M = -INFINITY;
-                    for (int s2 = 0; s2 < P.nsplit; ++s2) M = fmaxf(M, __ldcg(&P.ml[bh * P.nsplit + s2].x));
-                    for (int c = lane; c < D; c += 32) {
-                        float num = 0.0f, den = 0.0f;
-                        for (int s2 = 0; s2 < P.nsplit; ++s2) {
-                            const int u = bh * P.nsplit + s2;
-                            const float2 mlv = __ldcg(&P.ml[u]);
-                            const float w = ex2(mlv.x - M);
-                            num = fmaf(w, __ldcg(&P.part[int64_t(u) * D + c]), num);
-                            den = fmaf(w, mlv.y, den);
-                        }
-                        P.out[int64_t(bh) * D + c] = __float2half_rn(num / den);
-                    }
-                    if (lane == 0) P.tickets[bh] = 0u;   // leave the workspace zeroed
+            for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            M = mx;
+        }
+
+        // ------------------------------------------------ pass 2: P.V with p = 2^(s - M)
+        float2 acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
+        float l = 0.0f, bsum = 0.0f;
+#pragma unroll 1
+        for (;;) {
+            sb = next_stage(d);
+            const int n = d.flags >> 8;
+            if (n == C::CH) {
+#pragma unroll
+                for (int i = 0; i < C::ITERS; ++i)
+                    v_iter<D, true>(acc, l, bsum, sb, scores, M, d.t0, i * C::TPI + tl, n, sg, grp, magic);
+            } else {
+#pragma unroll 1
+                for (int i = 0; i * C::TPI < n; ++i)
+                    v_iter<D, false>(acc, l, bsum, sb, scores, M, d.t0, i * C::TPI + tl, n, sg, grp, magic);
+            }
+            const bool last = d.flags & kLast;
+            release();
+            if (last) break;
+        }
+
+        // ------------------------------------------------ end of unit: reduce over token lanes, write
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = __fmul2_rn(acc[k], inv_shift(k & 3));
+#pragma unroll
+        for (int o = C::LPT; o < 32; o <<= 1) {
+            l += __shfl_xor_sync(0xffffffffu, l, o);
+            bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+        }
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) { v[2 * k] = acc[k].x; v[2 * k + 1] = acc[k].y; }
+        int width = 32;   // live entries
+        int base = 0;     // column offset (within the 32-column segment) of v[0]
+#pragma unroll
+        for (int o = 16; o >= C::LPT; o >>= 1) {
+            const bool upper = (lane & o) != 0;
+            const int half = width >> 1;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k < half) {
+                    const float send = upper ? v[k] : v[k + half];
+                    const float keep = upper ? v[k + half] : v[k];
+                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
+            }
+            if (upper) base += half;
+            width = half;
+        }
+        // lane now holds columns [32 sg + base, + D/32)
+        const int col0 = sg * 32 + base;
+        if (P.nsplit == 1) {
+            const float inv = 1.0f / l;
+            __half* dst = P.out + int64_t(bh) * D + col0;
+            if constexpr (D == 128) {
+                __half2 h0 = __floats2half2_rn((v[0] + bsum) * inv, (v[1] + bsum) * inv);
+                __half2 h1 = __floats2half2_rn((v[2] + bsum) * inv, (v[3] + bsum) * inv);
+                uint2 w;
+                w.x = *reinterpret_cast<uint32_t*>(&h0);
+                w.y = *reinterpret_cast<uint32_t*>(&h1);
+                *reinterpret_cast<uint2*>(dst) = w;
+            } else {
+                *reinterpret_cast<__half2*>(dst) = __floats2half2_rn((v[0] + bsum) * inv, (v[1] + bsum) * inv);
+            }
+        } else {
+            float* dst = P.part + int64_t(unit) * D + col0;
+#pragma unroll
+            for (int k = 0; k < D / 32; ++k) dst[k] = v[k] + bsum;
+            if (lane == 0) P.ml[unit] = make_float2(M, l);
+            __threadfence();
+            __syncwarp();
+            uint32_t done = 0;
+            if (lane == 0) done = atomicAdd(&P.tickets[bh], 1u);
+            done = __shfl_sync(0xffffffffu, done, 0);
+            if (done == uint32_t(P.nsplit - 1)) {   // last split of this (b, h): merge
+                __threadfence();
+                float Mx = -INFINITY;
+                for (int s2 = 0; s2 < P.nsplit; ++s2) Mx = fmaxf(Mx, __ldcg(&P.ml[bh * P.nsplit + s2].x));
+                for (int c = lane; c < D; c += 32) {
+                    float num = 0.0f, den = 0.0f;
+                    for (int s2 = 0; s2 < P.nsplit; ++s2) {
+                        const int u = bh * P.nsplit + s2;
+                        const float2 mlv = __ldcg(&P.ml[u]);
+                        const float w = ex2(mlv.x - Mx);
+                        num = fmaf(w, __ldcg(&P.part[int64_t(u) * D + c]), num);
+                        den = fmaf(w, mlv.y, den);
+                    }
+                    P.out[int64_t(bh) * D + c] = __float2half_rn(num / den);
+                }
+                if (lane == 0) P.tickets[bh] = 0u;   // leave the workspace zeroed
             }
         }
     }
@@ -465,9 +494,9 @@ decode_attention_kernel(const Params P) {
     }
 }
 
-template <int D, int CH, int S, int WPC>
+template <int D, int S, int WPC>
 constexpr size_t smem_bytes() {
-    return size_t(WPC) * S * (Cfg<D, CH>::STAGE + 8 + sizeof(Desc));
+    return size_t(WPC) * (S * (Cfg<D>::STAGE + 8 + sizeof(Desc)) + kMaxUnitTokens * 4);
 }
 
 int sm_count() {
@@ -481,14 +510,14 @@ int sm_count() {
     return sms;
 }
 
-template <int D, int CH, int S, int WPC>
+template <int D, int S, int WPC>
 int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-        auto k = decode_attention_kernel<D, CH, S, WPC>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, CH, S, WPC>()));
+        auto k = decode_attention_kernel<D, S, WPC>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, S, WPC>()));
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, CH, S, WPC>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, S, WPC>());
         occ = o > 0 ? o : 1;
     }
     return occ;
@@ -497,38 +526,48 @@ int ctas_per_sm() {
 struct WsLayout {
     size_t ctrl, tickets, part, ml, total;
 };
-WsLayout ws_layout(int bh, int d) {
+// Split-K partial slots: kMaxSplitUnits for occupancy splits, plus one per
+// (b, h) and kMaxUnitTokens-long piece when the capacity exceeds a unit.
+int64_t split_slots(int bh, int t_cap) {
+    const int64_t pieces = (t_cap + kMaxUnitTokens - 1) / kMaxUnitTokens;
+    return pieces > 1 ? std::max<int64_t>(kMaxSplitUnits, int64_t(bh) * pieces) : kMaxSplitUnits;
+}
+WsLayout ws_layout(int bh, int d, int t_cap) {
     WsLayout w;
+    const int64_t slots = split_slots(bh, t_cap);
     w.ctrl = 0;
     w.tickets = 256;
     w.part = (w.tickets + size_t(bh) * 4 + 255) / 256 * 256;
-    w.ml = w.part + size_t(kMaxSplitUnits) * d * 4;
-    w.total = w.ml + size_t(kMaxSplitUnits) * 8;
+    w.ml = w.part + size_t(slots) * d * 4;
+    w.total = w.ml + size_t(slots) * 8;
     return w;
 }
 
-template <int D, int CH, int S, int WPC>
+template <int D, int S, int WPC>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const int occ = ctas_per_sm<D, CH, S, WPC>();
+    const int occ = ctas_per_sm<D, S, WPC>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
     // context split: only when (b, h) units cannot fill the resident warps
-    int nsplit = 1;
-    if (bh < warps_resident) {
+    // context split: forced when a unit would exceed the score buffer, else only
+    // when (b, h) units cannot fill the resident warps
+    const int min_split = (a.cur_len + kMaxUnitTokens - 1) / kMaxUnitTokens;
+    int nsplit = min_split;
+    if (int64_t(bh) * nsplit < warps_resident) {
         nsplit = (warps_resident + bh - 1) / bh;
         const int max_by_len = (a.cur_len + kMinSplitTokens - 1) / kMinSplitTokens;
         nsplit = min(nsplit, max_by_len);
-        nsplit = min(nsplit, kMaxSplitUnits / bh);
-        if (nsplit < 1) nsplit = 1;
+        nsplit = int(std::min<int64_t>(nsplit, split_slots(bh, a.t_cap) / bh));
+        nsplit = max(nsplit, min_split);
     }
     int split_len = (a.cur_len + nsplit - 1) / nsplit;
-    split_len = (split_len + CH - 1) / CH * CH;
+    split_len = (split_len + kChunk - 1) / kChunk * kChunk;
     nsplit = (a.cur_len + split_len - 1) / split_len;
     const int units = bh * nsplit;
     const int ctas = min(ctas_resident, (units + WPC - 1) / WPC);
 
-    const WsLayout w = ws_layout(bh, D);
+    const WsLayout w = ws_layout(bh, D, a.t_cap);
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     Params P;
     P.q = static_cast<const __half*>(a.q);
@@ -544,7 +583,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
-    decode_attention_kernel<D, CH, S, WPC><<<ctas, WPC * 32, smem_bytes<D, CH, S, WPC>(), stream>>>(P);
+    decode_attention_kernel<D, S, WPC><<<ctas, WPC * 32, smem_bytes<D, S, WPC>(), stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -567,25 +606,26 @@ int tune_variant() {
 
 }  // namespace
 
-size_t attention_workspace_bytes(int batch, int heads, int head_dim) {
-    return ws_layout(batch * heads, head_dim).total;
+size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) {
+    return ws_layout(batch * heads, head_dim, t_cap).total;
 }
 
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     const int v = tune_variant();
     if (a.head_dim == 128) {
         switch (v) {
-            case FLEXQ_V(32, 3, 4): return launch<128, 32, 3, 4>(a, stream);
-            case FLEXQ_V(32, 3, 5): return launch<128, 32, 3, 5>(a, stream);
-            case FLEXQ_V(32, 4, 4): return launch<128, 32, 4, 4>(a, stream);
-            case FLEXQ_V(32, 2, 2): return launch<128, 32, 2, 2>(a, stream);
-            default: return launch<128, 32, 2, 4>(a, stream);
+            case FLEXQ_V(32, 2, 4): return launch<128, 2, 4>(a, stream);
+            case FLEXQ_V(32, 4, 4): return launch<128, 4, 4>(a, stream);
+            case FLEXQ_V(32, 3, 6): return launch<128, 3, 6>(a, stream);
+            case FLEXQ_V(32, 2, 2): return launch<128, 2, 2>(a, stream);
+            case FLEXQ_V(32, 3, 2): return launch<128, 3, 2>(a, stream);
+            default: return launch<128, 3, 4>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(32, 3, 4): return launch<64, 32, 3, 4>(a, stream);
-        case FLEXQ_V(32, 4, 4): return launch<64, 32, 4, 4>(a, stream);
-        default: return launch<64, 32, 2, 4>(a, stream);
+        case FLEXQ_V(32, 2, 4): return launch<64, 2, 4>(a, stream);
+        case FLEXQ_V(32, 4, 4): return launch<64, 4, 4>(a, stream);
+        default: return launch<64, 3, 4>(a, stream);
     }
 }
 

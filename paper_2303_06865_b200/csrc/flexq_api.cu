@@ -106,7 +106,7 @@ flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int b
 size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
                                              int gen_len, int bits, int group_size) {
     if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
-    return flexq::attention_workspace_bytes(batch, heads, head_dim);
+    return flexq::attention_workspace_bytes(batch, heads, head_dim, prompt_len + gen_len);
 }
 
 flexq_status flexq_decode_attention(const void* q_f16, const void* kv_cache, int batch, int heads,
@@ -120,11 +120,11 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* kv_cache, int
     if (s != FLEXQ_OK) return s;
     if (!q_f16 || !kv_cache || !out_f16) return FLEXQ_ERR_NULL;
     if (!aligned16(q_f16) || !aligned16(kv_cache) || !aligned16(out_f16)) return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim))
+    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, kv_cache, out_f16, workspace, batch, heads, head_dim,
-                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len};
+                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap};
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 

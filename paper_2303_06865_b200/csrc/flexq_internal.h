@@ -11,8 +11,8 @@ constexpr int kBits = 4;
 constexpr int kGroup = 64;
 
 // KV cache layout (include/flexq.h): per (batch, head), a run of chunks of
-// kChunk tokens; chunk = [K codes kChunk x D/2][V codes kChunk x D/2]
-//                        [K meta kChunk x D/16][V meta kChunk x D/16]  bytes.
+// kChunk tokens; chunk = [K codes kChunk x D/2][K meta kChunk x D/16]
+//                        [V codes kChunk x D/2][V meta kChunk x D/16]  bytes.
 constexpr int kChunk = 32;
 inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + kChunk - 1) / kChunk * kChunk; }
 inline int64_t kv_chunk_bytes(int64_t d) { return int64_t(kChunk) * (d + d / 8); }   // 36 d
@@ -37,10 +37,10 @@ struct AttnArgs {
     const void* kv;
     void* out;
     void* workspace;
-    int batch, heads, head_dim, chunks, cur_len;
+    int batch, heads, head_dim, chunks, cur_len, t_cap;
 };
 
-size_t attention_workspace_bytes(int batch, int heads, int head_dim);
+size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
 
 }  // namespace flexq

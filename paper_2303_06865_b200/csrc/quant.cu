@@ -50,10 +50,11 @@ struct KvChunkDst {
         const int64_t t = d.pos + (row - bh * uint32_t(d.n_new));
         const int64_t chunk = int64_t(bh) * d.chunks + (t >> 5);
         const int slot = int(t & (kChunk - 1));
-        const int64_t base = chunk * (int64_t(kChunk) * (2 * cb + cb / 4));   // kv_chunk_bytes(2 cb)
-        const int mb = cb / 8;                                                 // meta bytes per token
-        codes_off = base + (kv * kChunk + slot) * cb + k * (kGroup / 2);
-        meta_off = base + 2 * kChunk * cb + (kv * kChunk + slot) * mb + k * 4;
+        const int mb = cb / 8;                                            // meta bytes per token
+        const int half = kChunk * (cb + mb);                              // K or V half of a chunk
+        const int64_t base = chunk * (2 * half) + kv * half;              // kv_chunk_bytes(2 cb)
+        codes_off = base + slot * cb + k * (kGroup / 2);
+        meta_off = base + kChunk * cb + slot * mb + k * 4;
     }
 };
 

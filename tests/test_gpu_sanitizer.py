@@ -15,7 +15,7 @@ def test_compute_sanitizer(cuda, tool):
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not available")
-    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", "--kernel-name", "regex:flexq",
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", "--kernel-name", "kns=flexq",
                         sys.executable, os.path.join(ROOT, "scripts", "sanitize_case.py")],
                        capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
