@@ -236,6 +236,8 @@ def run_flexq(args):
     from paper_2303_06865_b200 import dist as fd
     B_total = w.batch * (world if args.scaling == "weak" else 1)
     B = fd.rank_batch(w.batch, world, rank, args.scaling)
+    if B == 0:
+        raise SystemExit(f"--scaling strong needs batch ({w.batch}) >= ranks ({world})")
     H, D, s, n, L = w.heads, w.head_dim, w.prompt_len, w.gen_len, w.layers
     h1 = H * D
     seed = synth.BASE_SEED + 3 + 1000 * rank

@@ -73,32 +73,35 @@ flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int b
 flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t rows, int64_t cols,
                               int bits, int group_size, void *out_f16, void *stream);
 
-/* KV cache layout for one layer (one buffer holds K and V).  Capacity
- * T_cap = prompt_len + gen_len tokens, stored in chunks of 32 tokens
- * per (batch, head); T_stride = T_cap rounded up to a multiple of 32.  With
- * D = head_dim, CB = D/2 code bytes and MB = D/16 metadata bytes per token,
- * one chunk is 36*D bytes:
- *     [K codes 32 x CB][V codes 32 x CB][K meta 32 x MB][V meta 32 x MB]
- * and the buffer is u8 [batch][heads][T_stride/32][36*D].  Token t of head
- * (b, h) lives in chunk (b*heads + h)*T_stride/32 + t/32, slot t%32; its K
- * codes are D/2 bytes (element 2k in the low nibble of byte k), its K
- * meta D/64 half2 {scale, min} (groups of 64 along D).  A chunk is the
- * unit the attention kernel streams with one 1-D TMA bulk copy.  Tokens
- * [T_cap, T_stride) are padding the library never writes.
- * *cache_bytes (may be NULL) receives the buffer size, *token_stride (may be
- * NULL) T_stride.  Supported: bits == 4, group_size == 64, head_dim in {64, 128}. */
+/* KV cache layout for one layer: a K cache buffer and a V cache buffer of
+ * identical layout.  Capacity T_cap = prompt_len + gen_len tokens,
+ * stored in chunks of 32 tokens per (batch, head); T_stride = T_cap rounded
+ * up to a multiple of 32.  With D = head_dim, CB = D/2 code bytes and
+ * MB = D/16 metadata bytes per token, one chunk is 18*D bytes:
+ *     [codes 32 x CB][meta 32 x MB]
+ * and each buffer is u8 [batch][heads][T_stride/32][18*D].  Token t of head
+ * (b, h) lives in chunk (b*heads + h)*T_stride/32 + t/32, slot t%32: codes at
+ * slot*CB (element 2k in the low nibble of byte k), meta at
+ * 32*CB + slot*MB as D/64 half2 {scale, min} (groups of 64 along D).
+ * The chunks of one head are contiguous, so the attention kernel streams any
+ * run of them with one 1-D TMA bulk copy.  Tokens [T_cap, T_stride) are
+ * padding the library never writes.
+ * *cache_bytes (may be NULL) receives the size of ONE buffer (K or V),
+ * *token_stride (may be NULL) T_stride.  Supported: bits == 4,
+ * group_size == 64, head_dim in {64, 128}. */
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                   int bits, int group_size, size_t *cache_bytes, int *token_stride);
 
 /* KV update x_K <- Concat(x_K, t.w_K), same for V: quantizes
  * k_new, v_new fp16 [batch][heads][n_new][head_dim] group-wise along head_dim
  * and writes cache tokens [pos, pos + n_new) of every (batch, head)
- * into kv_cache (layout above).  Prompt fill is pos = 0, n_new = prompt_len;
- * a decode step is n_new = 1.  Touches no other cache position. */
+ * into k_cache / v_cache (layout above).  Prompt fill is pos = 0,
+ * n_new = prompt_len; a decode step is n_new = 1.  Touches no other cache
+ * position. */
 flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
                              int batch, int heads, int head_dim, int prompt_len, int gen_len,
                              int pos, int n_new, int bits, int group_size,
-                             void *kv_cache, void *stream);
+                             void *k_cache, void *v_cache, void *stream);
 
 /* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
  * arguments).  Layout: 256 B of scheduler counters, 4 B per (batch, head) of
@@ -117,7 +120,7 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
  * positions >= cur_len do not influence the result (the kernel may stream the
  * rest of the last 32-token chunk into shared memory and discard it).  Accuracy: |out - exact| <=
  * max(2e-3, 1e-2 |exact|) per element (reading Q). */
-flexq_status flexq_decode_attention(const void *q_f16, const void *kv_cache,
+flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, const void *v_cache,
                                     int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                     int cur_len, int bits, int group_size, void *out_f16,
                                     void *workspace, size_t workspace_bytes, void *stream);

@@ -8,11 +8,12 @@
 // Design:
 //  * Persistent kernel, one warp = one work unit = (b, h, context split);
 //    units handed out by an atomic ticket in the workspace (self-resetting).
-//  * Each warp owns an S-stage shared-memory ring.  A stage is the K half or
-//    the V half of one 32-token cache chunk (codes + fp16 (scale, min)),
-//    one contiguous run in HBM, loaded by one elected lane with a single 1-D
-//    TMA bulk copy (cp.async.bulk -> mbarrier complete_tx); q rides with the
-//    unit's first stage.  Loads run S-1 stages ahead of the math, across units.
+//  * Each warp owns an S-stage shared-memory ring.  A stage is NCH consecutive
+//    32-token chunks of the K cache (pass 1) or of the V cache (pass 2) --
+//    codes + fp16 (scale, min), one contiguous run in HBM -- loaded by one
+//    elected lane with a single 1-D TMA bulk copy (cp.async.bulk -> mbarrier
+//    complete_tx); q rides with the unit's first stage.  Loads run S-1 stages
+//    ahead of the math, across units.
 //  * Two passes per unit, no online rescaling: pass 1 streams the unit's K
 //    halves and writes every score (log2 domain) to a per-warp smem buffer,
 //    pass 2 takes the exact max, streams the V halves and accumulates
@@ -47,22 +48,25 @@ constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 64;
 constexpr int kMaxUnitTokens = 1024;   // score buffer per warp (4 KB); longer contexts split
 
-// One stage = one half (K or V) of a 32-token cache chunk; its smem image has
-// the HBM layout [codes 32 x D/2][meta 32 x D/16].
-template <int D>
+// One stage = NCH consecutive 32-token chunks of one cache (K or V); its smem
+// image has the HBM layout: per chunk [codes 32 x D/2][meta 32 x D/16].
+template <int D, int NCH>
 struct Cfg {
     static constexpr int LPT = D / 32;                 // lanes per token
     static constexpr int TPI = 32 / LPT;               // tokens per warp iteration
-    static constexpr int CH = kChunk;                  // tokens per stage
+    static constexpr int CH = kChunk * NCH;            // tokens per stage
     static constexpr int CB = D / 2;                   // code bytes per token
     static constexpr int MB = D / 16;                  // meta bytes per token (D/64 half2)
     static constexpr int ITERS = CH / TPI;
-    static constexpr int HALF = CH * (CB + MB);        // K or V half of a chunk (18 D bytes)
-    static constexpr int CHUNK = 2 * HALF;
-    static constexpr int OFF_M = CH * CB;              // meta inside a half
-    static constexpr int OFF_Q = HALF;
-    static constexpr int STAGE = HALF + 2 * D;         // + q (fp16) for the unit's first stage
-    static_assert(STAGE % 16 == 0 && HALF % 16 == 0, "stage alignment");
+    static constexpr int CHB = kChunk * (CB + MB);     // chunk bytes (18 D)
+    static constexpr int OFF_M = kChunk * CB;          // meta inside a chunk
+    static constexpr int OFF_Q = NCH * CHB;
+    static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
+    static_assert(STAGE % 16 == 0 && CHB % 16 == 0, "stage alignment");
+    static_assert(kChunk % TPI == 0, "an iteration stays inside one chunk");
+    // byte offsets of iteration i's codes / meta rows (token slot 0 of the iteration)
+    static constexpr int code_off(int i) { return (i * TPI / kChunk) * CHB + (i * TPI % kChunk) * CB; }
+    static constexpr int meta_off(int i) { return (i * TPI / kChunk) * CHB + OFF_M + (i * TPI % kChunk) * MB; }
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -153,7 +157,8 @@ constexpr int kFirst = 1, kV = 2, kLastK = 4, kLast = 8;
 
 struct Params {
     const __half* q;
-    const uint8_t* kv;   // chunked KV cache
+    const uint8_t* kc;   // chunked K cache
+    const uint8_t* vc;   // chunked V cache
     __half* out;
     uint32_t* ctrl;      // [0] next ticket, [1] finished warps
     uint32_t* tickets;   // per (b, h): finished splits
@@ -163,13 +168,15 @@ struct Params {
     float qscale;        // log2(e) / sqrt(D)
 };
 
-// Pass 1, one warp iteration: scores of TPI tokens -> smem (log2 domain).
-template <int D, bool FULL>
-__device__ __forceinline__ void k_iter(const float2 (&qp)[16], float qsum, const uint8_t* sb, float* sc, int t0,
-                                       int tok, int n, int sg, int grp, uint32_t magic, float& mx) {
-    using C = Cfg<D>;
-    const uint4 kw = lds128(sb + tok * C::CB + sg * 16);
-    const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_M + tok * C::MB + grp * 4));
+// Pass 1, one warp iteration (tokens i*TPI + [0, TPI) of the stage): scores -> smem (log2 domain).
+// lc / lm: the lane's byte offsets inside a token row (codes / meta).
+template <int D, int NCH, bool FULL>
+__device__ __forceinline__ void k_iter(int i, const float2 (&qp)[16], float qsum, const uint8_t* sb, float* sc,
+                                       int t0, int tl, int n, int lc, int lm, int sg, uint32_t magic, float& mx) {
+    using C = Cfg<D, NCH>;
+    const int tok = i * C::TPI + tl;
+    const uint4 kw = lds128(sb + C::code_off(i) + lc);
+    const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::meta_off(i) + lm));
     float2 d0 = make_float2(0.0f, 0.0f), d1 = d0;
     float2 f[4];
     unpack8(kw.x, magic, f);
@@ -195,13 +202,14 @@ __device__ __forceinline__ void k_iter(const float2 (&qp)[16], float qsum, const
 }
 
 // Pass 2, one warp iteration: acc_j += (p scale) c_j, bias += p min for TPI tokens.
-template <int D, bool FULL>
-__device__ __forceinline__ void v_iter(float2 (&acc)[16], float& l, float& bsum, const uint8_t* sb,
-                                       const float* sc, float M, int t0, int tok, int n, int sg, int grp,
+template <int D, int NCH, bool FULL>
+__device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float& bsum, const uint8_t* sb,
+                                       const float* sc, float M, int t0, int tl, int n, int lc, int lm,
                                        uint32_t magic) {
-    using C = Cfg<D>;
-    const uint4 vw = lds128(sb + tok * C::CB + sg * 16);
-    float2 vm = __half22float2(*reinterpret_cast<const __half2*>(sb + C::OFF_M + tok * C::MB + grp * 4));
+    using C = Cfg<D, NCH>;
+    const int tok = i * C::TPI + tl;
+    const uint4 vw = lds128(sb + C::code_off(i) + lc);
+    float2 vm = __half22float2(*reinterpret_cast<const __half2*>(sb + C::meta_off(i) + lm));
     float p = ex2(sc[t0 + tok] - M);
     if (!FULL) {
         const bool valid = tok < n;
@@ -228,10 +236,10 @@ __device__ __forceinline__ void v_iter(float2 (&acc)[16], float& l, float& bsum,
     acc[14] = __ffma2_rn(a2, f[2], acc[14]); acc[15] = __ffma2_rn(a2, f[3], acc[15]);
 }
 
-template <int D, int S, int WPC>
+template <int D, int NCH, int S, int WPC>
 __global__ void __launch_bounds__(WPC * 32, (16 / WPC) > 0 ? (16 / WPC) : 1)
 decode_attention_kernel(const Params P) {
-    using C = Cfg<D>;
+    using C = Cfg<D, NCH>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -280,9 +288,10 @@ decode_attention_kernel(const Params P) {
                 d.unit = p_unit;
                 d.bh = p_bh;
                 d.t0 = p_tok - p_first;
+                const int n = min(C::CH, p_end - p_tok);
                 d.flags = (first ? kFirst : 0) | (p_v ? kV : 0) | (!p_v && last_of_pass ? kLastK : 0) |
-                          (p_v && last_of_pass ? kLast : 0) | (min(C::CH, p_end - p_tok) << 8);
-                bytes = C::HALF + (first ? 2 * D : 0);
+                          (p_v && last_of_pass ? kLast : 0) | (n << 8);
+                bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB + (first ? 2 * D : 0);
             } else {
                 d.unit = -1; d.bh = 0; d.t0 = 0; d.flags = 0;
             }
@@ -292,7 +301,8 @@ decode_attention_kernel(const Params P) {
             if (p_unit >= 0) {
                 uint8_t* sb = ring + slot * C::STAGE;
                 const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
-                bulk_g2s(sb, P.kv + chunk * C::CHUNK + (p_v ? C::HALF : 0), C::HALF, &bars[slot], policy);
+                const uint32_t data = bytes - ((d.flags & kFirst) ? 2 * D : 0);
+                bulk_g2s(sb, (p_v ? P.vc : P.kc) + chunk * C::CHB, data, &bars[slot], policy);
                 if (d.flags & kFirst) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
             }
         }
@@ -316,7 +326,8 @@ decode_attention_kernel(const Params P) {
     // ---------------- consumer: per unit, pass 1 (K stages) then pass 2 (V stages)
     const int tl = lane / C::LPT;         // token slot in an iteration
     const int sg = lane % C::LPT;         // 16-byte segment of the token row
-    const int grp = sg >> 1;              // quantization group of the segment (64 = 2 x 32)
+    const int lc = tl * C::CB + sg * 16;  // lane's codes offset inside an iteration's rows
+    const int lm = tl * C::MB + (sg >> 1) * 4;   // lane's meta (group of the segment) offset
     const uint32_t magic = magic_reg();
 
     int slot = 0;
@@ -370,11 +381,12 @@ decode_attention_kernel(const Params P) {
                 if (n == C::CH) {
 #pragma unroll
                     for (int i = 0; i < C::ITERS; ++i)
-                        k_iter<D, true>(qp, qsum, sb, scores, d.t0, i * C::TPI + tl, n, sg, grp, magic, mx);
+                        k_iter<D, NCH, true>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
                 } else {
-#pragma unroll 1
-                    for (int i = 0; i * C::TPI < n; ++i)
-                        k_iter<D, false>(qp, qsum, sb, scores, d.t0, i * C::TPI + tl, n, sg, grp, magic, mx);
+#pragma unroll
+                    for (int i = 0; i < C::ITERS; ++i)
+                        if (i * C::TPI < n)
+                            k_iter<D, NCH, false>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
                 }
                 const bool last = d.flags & kLastK;
                 release();
@@ -398,11 +410,12 @@ decode_attention_kernel(const Params P) {
             if (n == C::CH) {
 #pragma unroll
                 for (int i = 0; i < C::ITERS; ++i)
-                    v_iter<D, true>(acc, l, bsum, sb, scores, M, d.t0, i * C::TPI + tl, n, sg, grp, magic);
+                    v_iter<D, NCH, true>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
             } else {
-#pragma unroll 1
-                for (int i = 0; i * C::TPI < n; ++i)
-                    v_iter<D, false>(acc, l, bsum, sb, scores, M, d.t0, i * C::TPI + tl, n, sg, grp, magic);
+#pragma unroll
+                for (int i = 0; i < C::ITERS; ++i)
+                    if (i * C::TPI < n)
+                        v_iter<D, NCH, false>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
             }
             const bool last = d.flags & kLast;
             release();
@@ -494,9 +507,9 @@ decode_attention_kernel(const Params P) {
     }
 }
 
-template <int D, int S, int WPC>
+template <int D, int NCH, int S, int WPC>
 constexpr size_t smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D>::STAGE + 8 + sizeof(Desc)) + kMaxUnitTokens * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + kMaxUnitTokens * 4);
 }
 
 int sm_count() {
@@ -510,14 +523,14 @@ int sm_count() {
     return sms;
 }
 
-template <int D, int S, int WPC>
+template <int D, int NCH, int S, int WPC>
 int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-        auto k = decode_attention_kernel<D, S, WPC>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, S, WPC>()));
+        auto k = decode_attention_kernel<D, NCH, S, WPC>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, NCH, S, WPC>()));
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, S, WPC>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, NCH, S, WPC>());
         occ = o > 0 ? o : 1;
     }
     return occ;
@@ -543,10 +556,10 @@ WsLayout ws_layout(int bh, int d, int t_cap) {
     return w;
 }
 
-template <int D, int S, int WPC>
+template <int D, int NCH, int S, int WPC>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const int occ = ctas_per_sm<D, S, WPC>();
+    const int occ = ctas_per_sm<D, NCH, S, WPC>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
     // context split: only when (b, h) units cannot fill the resident warps
@@ -562,7 +575,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         nsplit = max(nsplit, min_split);
     }
     int split_len = (a.cur_len + nsplit - 1) / nsplit;
-    split_len = (split_len + kChunk - 1) / kChunk * kChunk;
+    split_len = (split_len + Cfg<D, NCH>::CH - 1) / Cfg<D, NCH>::CH * Cfg<D, NCH>::CH;
     nsplit = (a.cur_len + split_len - 1) / split_len;
     const int units = bh * nsplit;
     const int ctas = min(ctas_resident, (units + WPC - 1) / WPC);
@@ -571,7 +584,8 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     Params P;
     P.q = static_cast<const __half*>(a.q);
-    P.kv = static_cast<const uint8_t*>(a.kv);
+    P.kc = static_cast<const uint8_t*>(a.k_cache);
+    P.vc = static_cast<const uint8_t*>(a.v_cache);
     P.out = static_cast<__half*>(a.out);
     P.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
     P.tickets = reinterpret_cast<uint32_t*>(ws + w.tickets);
@@ -583,7 +597,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
-    decode_attention_kernel<D, S, WPC><<<ctas, WPC * 32, smem_bytes<D, S, WPC>(), stream>>>(P);
+    decode_attention_kernel<D, NCH, S, WPC><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC>(), stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -610,22 +624,23 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) 
     return ws_layout(batch * heads, head_dim, t_cap).total;
 }
 
+// FLEXQ_ATTN_CFG="<stage tokens>,<S>,<WPC>" (tuning only).
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     const int v = tune_variant();
     if (a.head_dim == 128) {
         switch (v) {
-            case FLEXQ_V(32, 2, 4): return launch<128, 2, 4>(a, stream);
-            case FLEXQ_V(32, 4, 4): return launch<128, 4, 4>(a, stream);
-            case FLEXQ_V(32, 3, 6): return launch<128, 3, 6>(a, stream);
-            case FLEXQ_V(32, 2, 2): return launch<128, 2, 2>(a, stream);
-            case FLEXQ_V(32, 3, 2): return launch<128, 3, 2>(a, stream);
-            default: return launch<128, 3, 4>(a, stream);
+            case FLEXQ_V(32, 3, 4): return launch<128, 1, 3, 4>(a, stream);
+            case FLEXQ_V(32, 2, 4): return launch<128, 1, 2, 4>(a, stream);
+            case FLEXQ_V(64, 3, 3): return launch<128, 2, 3, 3>(a, stream);
+            case FLEXQ_V(64, 3, 4): return launch<128, 2, 3, 4>(a, stream);
+            case FLEXQ_V(64, 2, 2): return launch<128, 2, 2, 2>(a, stream);
+            default: return launch<128, 2, 2, 4>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(32, 2, 4): return launch<64, 2, 4>(a, stream);
-        case FLEXQ_V(32, 4, 4): return launch<64, 4, 4>(a, stream);
-        default: return launch<64, 3, 4>(a, stream);
+        case FLEXQ_V(32, 3, 4): return launch<64, 1, 3, 4>(a, stream);
+        case FLEXQ_V(64, 3, 4): return launch<64, 2, 3, 4>(a, stream);
+        default: return launch<64, 2, 2, 4>(a, stream);
     }
 }
 

@@ -77,6 +77,7 @@ flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t
 
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                   int bits, int group_size, size_t* cache_bytes, int* token_stride) {
+    // bytes of ONE cache buffer (K or V)
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
     if (s != FLEXQ_OK) return s;
     const int64_t stride = flexq::kv_token_stride(int64_t(prompt_len) + gen_len);
@@ -88,18 +89,19 @@ flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt
 
 flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int batch, int heads,
                              int head_dim, int prompt_len, int gen_len, int pos, int n_new, int bits,
-                             int group_size, void* kv_cache, void* stream) {
+                             int group_size, void* k_cache, void* v_cache, void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
     if (s == FLEXQ_ERR_ARG) return s;
     const int64_t t_cap = int64_t(prompt_len) + gen_len;
     if (pos < 0 || n_new < 1 || int64_t(pos) + n_new > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
-    if (!k_new_f16 || !v_new_f16 || !kv_cache) return FLEXQ_ERR_NULL;
-    if (!aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(kv_cache)) return FLEXQ_ERR_ALIGN;
+    if (!k_new_f16 || !v_new_f16 || !k_cache || !v_cache) return FLEXQ_ERR_NULL;
+    if (!aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_cache) || !aligned16(v_cache))
+        return FLEXQ_ERR_ALIGN;
     const int64_t rows = int64_t(batch) * heads * n_new;
     if (rows * (head_dim / group_size) >= (int64_t(1) << 31)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     const flexq::KvDst d{n_new, pos, flexq::kv_token_stride(t_cap) / flexq::kChunk};
-    return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, kv_cache, d,
+    return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, k_cache, v_cache, d,
                                              static_cast<cudaStream_t>(stream)));
 }
 
@@ -109,7 +111,8 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
     return flexq::attention_workspace_bytes(batch, heads, head_dim, prompt_len + gen_len);
 }
 
-flexq_status flexq_decode_attention(const void* q_f16, const void* kv_cache, int batch, int heads,
+flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, const void* v_cache, int batch,
+                                    int heads,
                                     int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
                                     int group_size, void* out_f16, void* workspace,
                                     size_t workspace_bytes, void* stream) {
@@ -118,12 +121,13 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* kv_cache, int
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
-    if (!q_f16 || !kv_cache || !out_f16) return FLEXQ_ERR_NULL;
-    if (!aligned16(q_f16) || !aligned16(kv_cache) || !aligned16(out_f16)) return FLEXQ_ERR_ALIGN;
+    if (!q_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16))
+        return FLEXQ_ERR_ALIGN;
     if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
-    flexq::AttnArgs a{q_f16, kv_cache, out_f16, workspace, batch, heads, head_dim,
+    flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap};
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }

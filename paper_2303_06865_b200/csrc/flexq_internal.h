@@ -10,12 +10,11 @@ namespace flexq {
 constexpr int kBits = 4;
 constexpr int kGroup = 64;
 
-// KV cache layout (include/flexq.h): per (batch, head), a run of chunks of
-// kChunk tokens; chunk = [K codes kChunk x D/2][K meta kChunk x D/16]
-//                        [V codes kChunk x D/2][V meta kChunk x D/16]  bytes.
+// KV cache layout (include/flexq.h): K and V caches each hold, per (batch,
+// head), a run of chunks of kChunk tokens; chunk = [codes kChunk x D/2][meta kChunk x D/16].
 constexpr int kChunk = 32;
 inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + kChunk - 1) / kChunk * kChunk; }
-inline int64_t kv_chunk_bytes(int64_t d) { return int64_t(kChunk) * (d + d / 8); }   // 36 d
+inline int64_t kv_chunk_bytes(int64_t d) { return int64_t(kChunk) * (d / 2 + d / 16); }   // 18 d
 
 // Destination of a KV append: source rows are (bh, t) with t in [0, n_new),
 // written at token pos + t of head bh.
@@ -27,14 +26,15 @@ struct KvDst {
 
 cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* codes, void* meta,
                             cudaStream_t stream);
-cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* kv,
-                             KvDst dst, cudaStream_t stream);
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
+                             void* v_cache, KvDst dst, cudaStream_t stream);
 cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols,
                               void* out, cudaStream_t stream);
 
 struct AttnArgs {
     const void* q;
-    const void* kv;
+    const void* k_cache;
+    const void* v_cache;
     void* out;
     void* workspace;
     int batch, heads, head_dim, chunks, cur_len, t_cap;

@@ -43,7 +43,7 @@ struct PlainDst {
 struct KvChunkDst {
     KvDst d;
     int cb;   // code bytes per token (D/2)
-    __device__ __forceinline__ void operator()(uint32_t g, uint32_t gpr, int kv, int64_t& codes_off,
+    __device__ __forceinline__ void operator()(uint32_t g, uint32_t gpr, int /*kv*/, int64_t& codes_off,
                                                int64_t& meta_off) const {
         const uint32_t row = g / gpr, k = g - row * gpr;
         const uint32_t bh = row / uint32_t(d.n_new);
@@ -51,8 +51,7 @@ struct KvChunkDst {
         const int64_t chunk = int64_t(bh) * d.chunks + (t >> 5);
         const int slot = int(t & (kChunk - 1));
         const int mb = cb / 8;                                            // meta bytes per token
-        const int half = kChunk * (cb + mb);                              // K or V half of a chunk
-        const int64_t base = chunk * (2 * half) + kv * half;              // kv_chunk_bytes(2 cb)
+        const int64_t base = chunk * (kChunk * (cb + mb));                // kv_chunk_bytes(2 cb)
         codes_off = base + slot * cb + k * (kGroup / 2);
         meta_off = base + kChunk * cb + slot * mb + k * 4;
     }
@@ -97,14 +96,18 @@ __device__ __forceinline__ uint32_t codes8(const float2 (&x)[4], float mn, float
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
-// codes_base / meta_base: byte base pointers of the destination (the same
-// buffer for the KV cache); blockIdx.y selects source x0 (K) or x1 (V).
+// blockIdx.y selects source x0 -> (codes0, meta0) or x1 -> (codes1, meta1):
+// byte base pointers of the destination (the same cache buffer for codes and
+// meta of the KV cache).
 template <class Dst>
 __global__ void __launch_bounds__(kThreads)
-quantize_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, uint8_t* __restrict__ codes_base,
-                uint8_t* __restrict__ meta_base, int64_t rows, int64_t cols, Dst dst) {
+quantize_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, uint8_t* __restrict__ codes0,
+                uint8_t* __restrict__ meta0, uint8_t* __restrict__ codes1, uint8_t* __restrict__ meta1,
+                int64_t rows, int64_t cols, Dst dst) {
     const int kv = blockIdx.y;
     const __half* x = kv ? x1 : x0;
+    uint8_t* codes_base = kv ? codes1 : codes0;
+    uint8_t* meta_base = kv ? meta1 : meta0;
 
     const int lane = threadIdx.x & 31;
     const int part = lane & 3;
@@ -247,13 +250,13 @@ cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* cod
     const int64_t cap = int64_t(num_sms()) * 8;
     if (blocks > cap) blocks = cap;
     quantize_kernel<PlainDst><<<unsigned(blocks), kThreads, 0, stream>>>(
-        static_cast<const __half*>(x), nullptr, static_cast<uint8_t*>(codes), static_cast<uint8_t*>(meta), rows,
-        cols, PlainDst{});
+        static_cast<const __half*>(x), nullptr, static_cast<uint8_t*>(codes), static_cast<uint8_t*>(meta), nullptr,
+        nullptr, rows, cols, PlainDst{});
     return cudaGetLastError();
 }
 
-cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* kv, KvDst d,
-                             cudaStream_t stream) {
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
+                             void* v_cache, KvDst d, cudaStream_t stream) {
     const int64_t groups = rows * (head_dim / kGroup);
     if (groups == 0) return cudaSuccess;
     int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;
@@ -261,8 +264,9 @@ cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int hea
     if (blocks > cap) blocks = cap;
     dim3 grid(unsigned(blocks), 2u);
     quantize_kernel<KvChunkDst><<<grid, kThreads, 0, stream>>>(
-        static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<uint8_t*>(kv),
-        static_cast<uint8_t*>(kv), rows, head_dim, KvChunkDst{d, head_dim / 2});
+        static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<uint8_t*>(k_cache),
+        static_cast<uint8_t*>(k_cache), static_cast<uint8_t*>(v_cache), static_cast<uint8_t*>(v_cache), rows,
+        head_dim, KvChunkDst{d, head_dim / 2});
     return cudaGetLastError();
 }
 

@@ -47,10 +47,10 @@ def lib():
         L.flexq_quantize.argtypes = [P, I64, I64, I, I, P, P, P]
         L.flexq_dequantize.argtypes = [P, P, I64, I64, I, I, P, P]
         L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(I)]
-        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P]
+        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P, P]
         L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
         L.flexq_decode_attention_workspace_size.restype = SZ
-        L.flexq_decode_attention.argtypes = [P, P] + [I] * 8 + [P, P, SZ, P]
+        L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 8 + [P, P, SZ, P]
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
                   "flexq_decode_attention"):
             getattr(L, f).restype = I
@@ -120,10 +120,10 @@ def token_stride(t_cap: int) -> int:
 
 
 class KVCache:
-    """One layer's compressed K + V cache in the chunked layout of include/flexq.h:
-    `kv` u8 [B][H][T_stride/32][36*D], chunk = [K codes 32 x D/2][V codes 32 x D/2]
-    [K meta 32 x D/16][V meta 32 x D/16].  The *_codes() / *_meta() accessors are
-    layout views for tests and inspection (tokens [0, T_stride))."""
+    """One layer's compressed KV cache in the chunked layout of include/flexq.h:
+    `k` and `v` are u8 [B][H][T_stride/32][18*D], chunk = [codes 32 x D/2][meta 32 x D/16].
+    The *_codes() / *_meta() accessors are layout views (copies) for tests and
+    inspection, over tokens [0, T_stride)."""
 
     def __init__(self, batch: int, heads: int, head_dim: int, prompt_len: int, gen_len: int,
                  device="cuda", bits: int = BITS, group_size: int = GROUP):
@@ -133,33 +133,39 @@ class KVCache:
         self.t_cap = prompt_len + gen_len
         self.t_stride = token_stride(self.t_cap)
         self.chunks = self.t_stride // CHUNK
-        self.kv = torch.zeros(batch, heads, self.chunks, 36 * head_dim, dtype=torch.uint8, device=device)
+        self.k = torch.zeros(batch, heads, self.chunks, 18 * head_dim, dtype=torch.uint8, device=device)
+        self.v = torch.zeros_like(self.k)
 
     def nbytes(self) -> int:
-        return self.kv.numel()
+        return self.k.numel() + self.v.numel()
 
-    def _part(self, offset: int, per_token: int) -> torch.Tensor:
+    def _part(self, buf: torch.Tensor, offset: int, per_token: int) -> torch.Tensor:
         B, H, NC = self.batch, self.heads, self.chunks
-        x = self.kv[..., offset:offset + CHUNK * per_token].reshape(B, H, NC, CHUNK, per_token)
+        x = buf[..., offset:offset + CHUNK * per_token].reshape(B, H, NC, CHUNK, per_token)
         return x.reshape(B, H, NC * CHUNK, per_token)
 
-    def k_codes(self) -> torch.Tensor:            # u8 [B][H][T_stride][D/2]
-        return self._part(0, self.head_dim // 2)
+    def _codes(self, buf) -> torch.Tensor:        # u8 [B][H][T_stride][D/2]
+        return self._part(buf, 0, self.head_dim // 2)
 
-    def v_codes(self) -> torch.Tensor:
-        return self._part(CHUNK * self.head_dim // 2, self.head_dim // 2)
-
-    def k_meta(self) -> torch.Tensor:             # fp16 [B][H][T_stride][D/64][2] = (scale, min)
-        m = self._part(CHUNK * self.head_dim, self.head_dim // 16)
+    def _meta(self, buf) -> torch.Tensor:         # fp16 [B][H][T_stride][D/64][2] = (scale, min)
+        m = self._part(buf, CHUNK * self.head_dim // 2, self.head_dim // 16)
         return m.contiguous().view(torch.float16).view(self.batch, self.heads, self.t_stride, -1, 2)
 
-    def v_meta(self) -> torch.Tensor:
-        m = self._part(CHUNK * self.head_dim + CHUNK * self.head_dim // 16, self.head_dim // 16)
-        return m.contiguous().view(torch.float16).view(self.batch, self.heads, self.t_stride, -1, 2)
+    def k_codes(self):
+        return self._codes(self.k)
+
+    def v_codes(self):
+        return self._codes(self.v)
+
+    def k_meta(self):
+        return self._meta(self.k)
+
+    def v_meta(self):
+        return self._meta(self.v)
 
 
 def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS, group_size=GROUP):
-    """-> (cache bytes of one layer (K and V), token stride)."""
+    """-> (bytes of one cache buffer (K or V) of one layer, token stride)."""
     c, t = ctypes.c_size_t(), ctypes.c_int()
     _check(lib().flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits, group_size,
                                       ctypes.byref(c), ctypes.byref(t)), "flexq_kv_cache_bytes")
@@ -173,7 +179,7 @@ def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, po
     B, H, n_new, D = k_new.shape
     _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
                                  cache.gen_len, pos, n_new, cache.bits, cache.group_size,
-                                 cache.kv.data_ptr(), _stream(stream)), "flexq_append_kv")
+                                 cache.k.data_ptr(), cache.v.data_ptr(), _stream(stream)), "flexq_append_kv")
 
 
 def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
@@ -185,7 +191,7 @@ def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, ge
 def make_workspace(cache: KVCache) -> torch.Tensor:
     n = flexq_decode_attention_workspace_size(cache.batch, cache.heads, cache.head_dim, cache.prompt_len,
                                               cache.gen_len, cache.bits, cache.group_size)
-    return torch.zeros(n, dtype=torch.uint8, device=cache.kv.device)
+    return torch.zeros(n, dtype=torch.uint8, device=cache.k.device)
 
 
 def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=None, workspace=None,
@@ -196,7 +202,8 @@ def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=No
         out = torch.empty_like(q)
     if workspace is None:
         workspace = make_workspace(cache)
-    _check(lib().flexq_decode_attention(q.data_ptr(), cache.kv.data_ptr(), cache.batch, cache.heads,
+    _check(lib().flexq_decode_attention(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
+                                        cache.heads,
                                         cache.head_dim, cache.prompt_len, cache.gen_len,
                                         cur_len, cache.bits, cache.group_size, out.data_ptr(),
                                         workspace.data_ptr(), workspace.numel(), _stream(stream)),

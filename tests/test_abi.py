@@ -60,7 +60,7 @@ def test_append_validation(L):
     f = L.flexq_append_kv
 
     def call(B=2, H=3, D=128, s=8, n=4, pos=0, nn=1, bits=4, g=64, k=A, kv=A):
-        return f(k, A, B, H, D, s, n, pos, nn, bits, g, kv, None)
+        return f(k, A, B, H, D, s, n, pos, nn, bits, g, A, kv, None)
     assert call(B=0) == fq.FLEXQ_ERR_ARG
     assert call(pos=-1) == fq.FLEXQ_ERR_ARG
     assert call(pos=12) == fq.FLEXQ_ERR_ARG            # pos + n_new > s + n
@@ -80,7 +80,7 @@ def test_attention_validation(L):
     assert L.flexq_decode_attention_workspace_size(0, 3, 128, 8, 4, 4, 64) == 0
 
     def call(cur=5, D=128, q=A, kv=A, out=A, w=A, wb=ws, g=64):
-        return f(q, kv, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
+        return f(q, A, kv, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
     assert call(cur=0) == fq.FLEXQ_ERR_ARG
     assert call(cur=13) == fq.FLEXQ_ERR_ARG             # cur_len > s + n
     assert call(D=32) == fq.FLEXQ_ERR_UNSUPPORTED
@@ -95,10 +95,10 @@ def test_attention_validation(L):
 def test_kv_cache_bytes(L):
     c, t = fq.flexq_kv_cache_bytes(144, 96, 128, 512, 32)
     assert t == 544                                   # 544 = 17 chunks of 32: no padding
-    assert c == 144 * 96 * 17 * 36 * 128
-    assert c * 8 == 144 * 96 * 544 * 128 * 2 * 4.5   # 4.5 bits per K/V element
+    assert c == 144 * 96 * 17 * 18 * 128              # one buffer (K or V)
+    assert c * 8 == 144 * 96 * 544 * 128 * 4.5        # 4.5 bits per element
     c, t = fq.flexq_kv_cache_bytes(4, 12, 64, 512, 1)
-    assert t == 544 and c == 4 * 12 * 17 * 36 * 64
+    assert t == 544 and c == 4 * 12 * 17 * 18 * 64
     assert fq.token_stride(513) == 544 and fq.token_stride(1) == 32 and fq.token_stride(32) == 32
     with __import__("pytest").raises(fq.FlexqError):
         fq.flexq_kv_cache_bytes(1, 1, 96, 8, 8)
