@@ -50,6 +50,7 @@ def lib():
         L.oracle_append_kv.argtypes = [P, P] + [i32] * 8 + [P, P, P, P]
         L.oracle_attention_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P]
         L.oracle_attention_f32.argtypes = [P] * 5 + [i32] * 7 + [P]
+        L.oracle_attention_topk_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P, P, P]
         _lib = L
     return _lib
 
@@ -156,3 +157,22 @@ def attention_f32(q, k_cache, v_cache, cur_len: int, group: int = 64, kv_f16: bo
     _check(lib().oracle_attention_f32(_p(q), _p(kc), _p(km), _p(vc), _p(vm), B, H, D, T_cap, cur_len,
                                       group, int(kv_f16), _p(out)), "attention_f32")
     return out
+
+
+def attention_topk_f64(q, k_cache, v_cache, cur_len: int, keep: int, group: int = 64, sel=None):
+    """Top-K sparse decode attention.
+    -> (out float64 [B][H][D], kept mask u8 [B][H][cur_len], scores float64 [B][H][cur_len]).
+    sel: optional kept mask to evaluate instead of selecting."""
+    q = _h(q)
+    B, H, D = q.shape
+    kc, km = k_cache
+    vc, vm = v_cache
+    T_cap = kc.shape[2]
+    out = np.zeros((B, H, D), np.float64)
+    mask = np.zeros((B, H, cur_len), np.uint8)
+    scores = np.zeros((B, H, cur_len), np.float64)
+    sel_arr = None if sel is None else np.ascontiguousarray(sel, dtype=np.uint8)
+    _check(lib().oracle_attention_topk_f64(_p(q), _p(kc), _p(km), _p(vc), _p(vm), B, H, D, T_cap, cur_len,
+                                           group, keep, _p(sel_arr) if sel_arr is not None else None,
+                                           _p(mask), _p(scores), _p(out)), "attention_topk_f64")
+    return out, mask, scores

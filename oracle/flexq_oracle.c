@@ -311,3 +311,69 @@ int oracle_attention_f32(const uint16_t *q, const uint8_t *k_codes, const uint16
     free(e);
     return OK;
 }
+
+/* ------------------------------------------------------------------ NEXT-1 */
+/* Top-K sparse attention ("for each query, we calculate the indices
+ * of its Top-K tokens from the K cache ... drop the other tokens and only load
+ * a subset of the V cache"): scores s_t as in oracle_attention_f64;
+ * keep the `keep` highest scores (equal scores: lower token index first);
+ * softmax renormalised over the kept set; o = sum_kept p_t V^_t.
+ * sel_in (optional): 0/1 mask [B][H][cur_len] of a kept set to evaluate
+ * instead of selecting (lets a test score a set chosen elsewhere).
+ * sel_out (optional): the kept mask; scores_out (optional): s_t (double).
+ * Selection is the definition written out: token t is kept iff
+ * #{u : s_u > s_t or (s_u == s_t and u < t)} < keep  (O(n^2)). */
+int oracle_attention_topk_f64(const uint16_t *q, const uint8_t *k_codes, const uint16_t *k_meta,
+                              const uint8_t *v_codes, const uint16_t *v_meta,
+                              int B, int H, int D, int T_cap, int cur_len, int group, int keep,
+                              const uint8_t *sel_in, uint8_t *sel_out, double *scores_out, double *out)
+{
+    if (B < 1 || H < 1 || D < 1 || T_cap < 1 || group < 1) return ERR_ARG;
+    if (cur_len < 1 || cur_len > T_cap || keep < 1 || keep > cur_len) return ERR_ARG;
+    if (D % group != 0) return ERR_UNSUPPORTED;
+    double *s = (double *)malloc(sizeof(double) * (size_t)cur_len);
+    uint8_t *kept = (uint8_t *)malloc((size_t)cur_len);
+    if (!s || !kept) { free(s); free(kept); return ERR_ARG; }
+    for (int b = 0; b < B; ++b)
+        for (int h = 0; h < H; ++h) {
+            int64_t bh = (int64_t)b * H + h;
+            const uint16_t *qh = q + bh * D;
+            for (int t = 0; t < cur_len; ++t) {
+                int64_t row = bh * T_cap + t;
+                double acc = 0.0;
+                for (int j = 0; j < D; ++j)
+                    acc += (double)oracle_f16_to_f32(qh[j]) *
+                           (double)cache_elem(k_codes, k_meta, row, D, group, j, 0);
+                s[t] = acc / sqrt((double)D);
+                if (scores_out) scores_out[bh * cur_len + t] = s[t];
+            }
+            for (int t = 0; t < cur_len; ++t) {
+                if (sel_in) {
+                    kept[t] = sel_in[bh * cur_len + t] ? 1 : 0;
+                } else {
+                    int rank = 0;
+                    for (int u = 0; u < cur_len; ++u)
+                        if (s[u] > s[t] || (s[u] == s[t] && u < t)) ++rank;
+                    kept[t] = rank < keep;
+                }
+                if (sel_out) sel_out[bh * cur_len + t] = kept[t];
+            }
+            double mx = -INFINITY;
+            for (int t = 0; t < cur_len; ++t)
+                if (kept[t] && s[t] > mx) mx = s[t];
+            double z = 0.0;
+            for (int t = 0; t < cur_len; ++t)
+                if (kept[t]) z += exp(s[t] - mx);
+            for (int j = 0; j < D; ++j) {
+                double o = 0.0;
+                for (int t = 0; t < cur_len; ++t)
+                    if (kept[t])
+                        o += exp(s[t] - mx) / z *
+                             (double)cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j, 0);
+                out[bh * D + j] = o;
+            }
+        }
+    free(s);
+    free(kept);
+    return OK;
+}

@@ -236,8 +236,10 @@ __device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float
     acc[14] = __ffma2_rn(a2, f[2], acc[14]); acc[15] = __ffma2_rn(a2, f[3], acc[15]);
 }
 
-template <int D, int NCH, int S, int WPC>
-__global__ void __launch_bounds__(WPC * 32, (16 / WPC) > 0 ? (16 / WPC) : 1)
+// UNR: unroll factor of the full-stage loops (code size vs. scheduling freedom:
+// fully unrolled K and V bodies overflow the instruction cache).
+template <int D, int NCH, int S, int WPC, int UNR>
+__global__ void __launch_bounds__(WPC * 32, (20 / WPC) > 0 ? (20 / WPC) : 1)
 decode_attention_kernel(const Params P) {
     using C = Cfg<D, NCH>;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -379,11 +381,11 @@ decode_attention_kernel(const Params P) {
             for (;;) {
                 const int n = d.flags >> 8;
                 if (n == C::CH) {
-#pragma unroll
+#pragma unroll UNR
                     for (int i = 0; i < C::ITERS; ++i)
                         k_iter<D, NCH, true>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
                 } else {
-#pragma unroll
+#pragma unroll 1
                     for (int i = 0; i < C::ITERS; ++i)
                         if (i * C::TPI < n)
                             k_iter<D, NCH, false>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
@@ -408,11 +410,11 @@ decode_attention_kernel(const Params P) {
             sb = next_stage(d);
             const int n = d.flags >> 8;
             if (n == C::CH) {
-#pragma unroll
+#pragma unroll UNR
                 for (int i = 0; i < C::ITERS; ++i)
                     v_iter<D, NCH, true>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
             } else {
-#pragma unroll
+#pragma unroll 1
                 for (int i = 0; i < C::ITERS; ++i)
                     if (i * C::TPI < n)
                         v_iter<D, NCH, false>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
@@ -523,11 +525,11 @@ int sm_count() {
     return sms;
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int UNR>
 int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-        auto k = decode_attention_kernel<D, NCH, S, WPC>;
+        auto k = decode_attention_kernel<D, NCH, S, WPC, UNR>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, NCH, S, WPC>()));
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, NCH, S, WPC>());
@@ -556,10 +558,10 @@ WsLayout ws_layout(int bh, int d, int t_cap) {
     return w;
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int UNR>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const int occ = ctas_per_sm<D, NCH, S, WPC>();
+    const int occ = ctas_per_sm<D, NCH, S, WPC, UNR>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
     // context split: only when (b, h) units cannot fill the resident warps
@@ -597,7 +599,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
-    decode_attention_kernel<D, NCH, S, WPC><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC>(), stream>>>(P);
+    decode_attention_kernel<D, NCH, S, WPC, UNR><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC>(), stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -610,13 +612,13 @@ int tune_variant() {
     if (v == -2) {
         v = -1;
         const char* e = getenv("FLEXQ_ATTN_CFG");
-        int ch = 0, st = 0, wpc = 0;
-        if (e && sscanf(e, "%d,%d,%d", &ch, &st, &wpc) == 3) v = ch * 256 + st * 16 + wpc;
+        int ch = 0, st = 0, wpc = 0, unr = 2;
+        if (e && sscanf(e, "%d,%d,%d,%d", &ch, &st, &wpc, &unr) >= 3) v = ((ch * 16 + st) * 16 + wpc) * 16 + unr;
     }
     return v;
 }
 
-#define FLEXQ_V(ch, s, w) ((ch) * 256 + (s) * 16 + (w))
+#define FLEXQ_V(ch, s, w, u) ((((ch) * 16 + (s)) * 16 + (w)) * 16 + (u))
 
 }  // namespace
 
@@ -624,23 +626,26 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) 
     return ws_layout(batch * heads, head_dim, t_cap).total;
 }
 
-// FLEXQ_ATTN_CFG="<stage tokens>,<S>,<WPC>" (tuning only).
+// FLEXQ_ATTN_CFG="<stage tokens>,<S>,<WPC>[,<unroll>]" (tuning only).
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     const int v = tune_variant();
     if (a.head_dim == 128) {
         switch (v) {
-            case FLEXQ_V(32, 3, 4): return launch<128, 1, 3, 4>(a, stream);
-            case FLEXQ_V(32, 2, 4): return launch<128, 1, 2, 4>(a, stream);
-            case FLEXQ_V(64, 3, 3): return launch<128, 2, 3, 3>(a, stream);
-            case FLEXQ_V(64, 3, 4): return launch<128, 2, 3, 4>(a, stream);
-            case FLEXQ_V(64, 2, 2): return launch<128, 2, 2, 2>(a, stream);
-            default: return launch<128, 2, 2, 4>(a, stream);
+            case FLEXQ_V(64, 2, 4, 8): return launch<128, 2, 2, 4, 8>(a, stream);
+            case FLEXQ_V(64, 2, 4, 1): return launch<128, 2, 2, 4, 1>(a, stream);
+            case FLEXQ_V(64, 2, 4, 4): return launch<128, 2, 2, 4, 4>(a, stream);
+            case FLEXQ_V(64, 3, 4, 2): return launch<128, 2, 3, 4, 2>(a, stream);
+            case FLEXQ_V(32, 3, 4, 2): return launch<128, 1, 3, 4, 2>(a, stream);
+            case FLEXQ_V(32, 4, 4, 2): return launch<128, 1, 4, 4, 2>(a, stream);
+            case FLEXQ_V(32, 2, 4, 2): return launch<128, 1, 2, 4, 2>(a, stream);
+            case FLEXQ_V(32, 2, 4, 4): return launch<128, 1, 2, 4, 4>(a, stream);
+            default: return launch<128, 2, 2, 4, 2>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(32, 3, 4): return launch<64, 1, 3, 4>(a, stream);
-        case FLEXQ_V(64, 3, 4): return launch<64, 2, 3, 4>(a, stream);
-        default: return launch<64, 2, 2, 4>(a, stream);
+        case FLEXQ_V(64, 2, 4, 4): return launch<64, 2, 2, 4, 4>(a, stream);
+        case FLEXQ_V(64, 3, 4, 2): return launch<64, 2, 3, 4, 2>(a, stream);
+        default: return launch<64, 2, 2, 4, 2>(a, stream);
     }
 }
 

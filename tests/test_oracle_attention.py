@@ -149,3 +149,64 @@ def test_cur_len_prefix_only(orc):
     kc[0][:, :, 20:] = 15
     vc[0][:, :, 20:] = 15
     assert np.array_equal(orc.attention_f64(q, kc, vc, 20), o)
+
+
+# ---------------------------------------------------------------- NEXT-1: Top-K sparse attention
+def test_topk_keep_all_equals_dense(orc):
+    """keep fraction 1.0 -> identical to dense attention."""
+    q, kc, vc, _, _ = make_cache(orc, 2, 3, 128, 77, seed=51)
+    dense = orc.attention_f64(q, kc, vc, 77)
+    sparse, mask, _ = orc.attention_topk_f64(q, kc, vc, 77, keep=77)
+    assert mask.all()
+    assert np.abs(sparse - dense).max() < 1e-12
+
+
+def test_topk_selection_is_top_scores(orc):
+    """The kept set is exactly the `keep` largest scores (independent numpy argsort)."""
+    q, kc, vc, _, _ = make_cache(orc, 2, 2, 64, 130, seed=52)
+    keep = 13                                         # ceil(0.1 * 130), P:854 "top 10%"
+    _, mask, scores = orc.attention_topk_f64(q, kc, vc, 130, keep=keep)
+    K = deq_f32(orc, kc).astype(np.float64)
+    s_ref = np.einsum("bhd,bhtd->bht", q.astype(np.float64), K) / np.sqrt(64)
+    assert np.abs(scores - s_ref).max() < 1e-9
+    for b in range(2):
+        for h in range(2):
+            order = np.lexsort((np.arange(130), -scores[b, h]))   # score desc, index asc
+            want = np.zeros(130, np.uint8)
+            want[order[:keep]] = 1
+            assert np.array_equal(mask[b, h], want)
+            assert mask[b, h].sum() == keep
+
+
+def test_topk_renormalised_and_dominant_key(orc):
+    """one dominant key and keep = 1 -> output = that key's V^ row; weights
+    renormalised over the kept set sum to 1 (checked through V = constant rows)."""
+    B, H, D, T = 1, 1, 64, 20
+    k = synth.fill(53, 1, (B, H, T, D)).numpy() * np.float16(0.01)
+    k[0, 0, 5] = np.float16(1.0)
+    v = synth.fill(53, 2, (B, H, T, D)).numpy()
+    kc, vc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
+    orc.append_kv(k, v, kc, vc, 0)
+    q = (k[:, :, 5, :].astype(np.float32) * 4).astype(np.float16)
+    out, mask, _ = orc.attention_topk_f64(q, kc, vc, T, keep=1)
+    assert mask[0, 0].tolist() == [int(t == 5) for t in range(T)]
+    V = deq_f32(orc, vc).astype(np.float64)
+    assert np.abs(out[0, 0] - V[0, 0, 5]).max() < 1e-12
+    # constant V rows -> output equals the constant for any kept set (weights sum to 1)
+    vconst = np.full((B, H, T, D), np.float16(1.5))
+    vc2 = orc.empty_cache(B, H, T, D)
+    orc.append_kv(k, vconst, orc.empty_cache(B, H, T, D), vc2, 0)
+    out2, _, _ = orc.attention_topk_f64(q, kc, vc2, T, keep=7)
+    assert np.abs(out2 - 1.5).max() < 1e-12
+
+
+def test_topk_converges_to_dense(orc):
+    """SPEC 'Invariants': max deviation from dense is non-increasing as the kept
+    fraction grows (0.1, 0.25, 0.5, 1.0) on a fixed instance."""
+    q, kc, vc, _, _ = make_cache(orc, 1, 4, 128, 200, seed=54)
+    q = (q.astype(np.float32) * 4).astype(np.float16)
+    dense = orc.attention_f64(q, kc, vc, 200)
+    devs = [np.abs(orc.attention_topk_f64(q, kc, vc, 200, keep=int(np.ceil(f * 200)))[0] - dense).max()
+            for f in (0.1, 0.25, 0.5, 1.0)]
+    assert all(devs[i + 1] <= devs[i] + 1e-15 for i in range(3)), devs
+    assert devs[-1] < 1e-12
