@@ -46,7 +46,7 @@ namespace {
 
 constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 64;
-constexpr int kMaxUnitTokens = 1024;   // score buffer per warp (4 KB); longer contexts split
+constexpr int kMinUnitTokens = 512;    // smallest per-warp score buffer of any variant (sizes the workspace)
 
 // One stage = NCH consecutive 32-token chunks of one cache (K or V); its smem
 // image has the HBM layout: per chunk [codes 32 x D/2][meta 32 x D/16].
@@ -238,7 +238,8 @@ __device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float
 
 // UNR: unroll factor of the full-stage loops (code size vs. scheduling freedom:
 // fully unrolled K and V bodies overflow the instruction cache).
-template <int D, int NCH, int S, int WPC, int UNR>
+// MAXT: per-warp score buffer (tokens); longer contexts are split into units of <= MAXT.
+template <int D, int NCH, int S, int WPC, int UNR, int MAXT>
 __global__ void __launch_bounds__(WPC * 32, (20 / WPC) > 0 ? (20 / WPC) : 1)
 decode_attention_kernel(const Params P) {
     using C = Cfg<D, NCH>;
@@ -246,9 +247,9 @@ decode_attention_kernel(const Params P) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
-    float* scores = reinterpret_cast<float*>(smem + WPC * S * C::STAGE) + warp * kMaxUnitTokens;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + kMaxUnitTokens * 4)) + warp * S;
-    Desc* desc = reinterpret_cast<Desc*>(smem + WPC * (S * (C::STAGE + 8) + kMaxUnitTokens * 4)) + warp * S;
+    float* scores = reinterpret_cast<float*>(smem + WPC * S * C::STAGE) + warp * MAXT;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 4)) + warp * S;
+    Desc* desc = reinterpret_cast<Desc*>(smem + WPC * (S * (C::STAGE + 8) + MAXT * 4)) + warp * S;
 
     const int units = P.bh_total * P.nsplit;
     const uint64_t policy = evict_first_policy();
@@ -509,9 +510,9 @@ decode_attention_kernel(const Params P) {
     }
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + kMaxUnitTokens * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + MAXT * 4);
 }
 
 int sm_count() {
@@ -525,14 +526,14 @@ int sm_count() {
     return sms;
 }
 
-template <int D, int NCH, int S, int WPC, int UNR>
+template <int D, int NCH, int S, int WPC, int UNR, int MAXT>
 int ctas_per_sm() {
     static int occ = -1;
     if (occ < 0) {
-        auto k = decode_attention_kernel<D, NCH, S, WPC, UNR>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, NCH, S, WPC>()));
+        auto k = decode_attention_kernel<D, NCH, S, WPC, UNR, MAXT>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, NCH, S, WPC, MAXT>()));
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, NCH, S, WPC>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem_bytes<D, NCH, S, WPC, MAXT>());
         occ = o > 0 ? o : 1;
     }
     return occ;
@@ -542,9 +543,9 @@ struct WsLayout {
     size_t ctrl, tickets, part, ml, total;
 };
 // Split-K partial slots: kMaxSplitUnits for occupancy splits, plus one per
-// (b, h) and kMaxUnitTokens-long piece when the capacity exceeds a unit.
+// (b, h) and unit-long piece when the capacity exceeds the smallest unit.
 int64_t split_slots(int bh, int t_cap) {
-    const int64_t pieces = (t_cap + kMaxUnitTokens - 1) / kMaxUnitTokens;
+    const int64_t pieces = (t_cap + kMinUnitTokens - 1) / kMinUnitTokens;
     return pieces > 1 ? std::max<int64_t>(kMaxSplitUnits, int64_t(bh) * pieces) : kMaxSplitUnits;
 }
 WsLayout ws_layout(int bh, int d, int t_cap) {
@@ -558,16 +559,16 @@ WsLayout ws_layout(int bh, int d, int t_cap) {
     return w;
 }
 
-template <int D, int NCH, int S, int WPC, int UNR>
+template <int D, int NCH, int S, int WPC, int UNR, int MAXT>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const int occ = ctas_per_sm<D, NCH, S, WPC, UNR>();
+    const int occ = ctas_per_sm<D, NCH, S, WPC, UNR, MAXT>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
     // context split: only when (b, h) units cannot fill the resident warps
     // context split: forced when a unit would exceed the score buffer, else only
     // when (b, h) units cannot fill the resident warps
-    const int min_split = (a.cur_len + kMaxUnitTokens - 1) / kMaxUnitTokens;
+    const int min_split = (a.cur_len + MAXT - 1) / MAXT;
     int nsplit = min_split;
     if (int64_t(bh) * nsplit < warps_resident) {
         nsplit = (warps_resident + bh - 1) / bh;
@@ -599,7 +600,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
-    decode_attention_kernel<D, NCH, S, WPC, UNR><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC>(), stream>>>(P);
+    decode_attention_kernel<D, NCH, S, WPC, UNR, MAXT><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC, MAXT>(), stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -607,18 +608,19 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
 // defaults come from the B200 sweep recorded in DESIGN.md; the environment
 // variable FLEXQ_ATTN_CFG="<CH>,<S>,<WPC>" selects another compiled variant
 // (tuning only).
-int tune_variant() {
-    static int v = -2;
+int64_t tune_variant() {
+    static int64_t v = -2;
     if (v == -2) {
         v = -1;
         const char* e = getenv("FLEXQ_ATTN_CFG");
-        int ch = 0, st = 0, wpc = 0, unr = 2;
-        if (e && sscanf(e, "%d,%d,%d,%d", &ch, &st, &wpc, &unr) >= 3) v = ((ch * 16 + st) * 16 + wpc) * 16 + unr;
+        int ch = 0, st = 0, wpc = 0, unr = 4, mt = 1024;
+        if (e && sscanf(e, "%d,%d,%d,%d,%d", &ch, &st, &wpc, &unr, &mt) >= 3)
+            v = ((((int64_t(ch) * 16 + st) * 16 + wpc) * 16 + unr) * 4096) + mt;
     }
     return v;
 }
 
-#define FLEXQ_V(ch, s, w, u) ((((ch) * 16 + (s)) * 16 + (w)) * 16 + (u))
+#define FLEXQ_V(ch, s, w, u, mt) (((((int64_t(ch) * 16 + (s)) * 16 + (w)) * 16 + (u)) * 4096) + (mt))
 
 }  // namespace
 
@@ -626,26 +628,24 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) 
     return ws_layout(batch * heads, head_dim, t_cap).total;
 }
 
-// FLEXQ_ATTN_CFG="<stage tokens>,<S>,<WPC>[,<unroll>]" (tuning only).
+// FLEXQ_ATTN_CFG="<stage tokens>,<S>,<WPC>,<unroll>,<score tokens>" (tuning only).
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
-    const int v = tune_variant();
+    const int64_t v = tune_variant();
     if (a.head_dim == 128) {
         switch (v) {
-            case FLEXQ_V(64, 2, 4, 8): return launch<128, 2, 2, 4, 8>(a, stream);
-            case FLEXQ_V(64, 2, 4, 1): return launch<128, 2, 2, 4, 1>(a, stream);
-            case FLEXQ_V(64, 2, 4, 4): return launch<128, 2, 2, 4, 4>(a, stream);
-            case FLEXQ_V(64, 3, 4, 2): return launch<128, 2, 3, 4, 2>(a, stream);
-            case FLEXQ_V(32, 3, 4, 2): return launch<128, 1, 3, 4, 2>(a, stream);
-            case FLEXQ_V(32, 4, 4, 2): return launch<128, 1, 4, 4, 2>(a, stream);
-            case FLEXQ_V(32, 2, 4, 2): return launch<128, 1, 2, 4, 2>(a, stream);
-            case FLEXQ_V(32, 2, 4, 4): return launch<128, 1, 2, 4, 4>(a, stream);
-            default: return launch<128, 2, 2, 4, 2>(a, stream);
+            case FLEXQ_V(64, 2, 4, 4, 1024): return launch<128, 2, 2, 4, 4, 1024>(a, stream);
+            case FLEXQ_V(64, 2, 4, 8, 1024): return launch<128, 2, 2, 4, 8, 1024>(a, stream);
+            case FLEXQ_V(64, 2, 2, 4, 576): return launch<128, 2, 2, 2, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 1, 4, 576): return launch<128, 2, 2, 1, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 4, 4, 576): return launch<128, 2, 2, 4, 4, 576>(a, stream);
+            case FLEXQ_V(32, 2, 4, 4, 576): return launch<128, 1, 2, 4, 4, 576>(a, stream);
+            case FLEXQ_V(32, 3, 2, 4, 576): return launch<128, 1, 3, 2, 4, 576>(a, stream);
+            default: return launch<128, 2, 2, 4, 4, 1024>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(64, 2, 4, 4): return launch<64, 2, 2, 4, 4>(a, stream);
-        case FLEXQ_V(64, 3, 4, 2): return launch<64, 2, 3, 4, 2>(a, stream);
-        default: return launch<64, 2, 2, 4, 2>(a, stream);
+        case FLEXQ_V(64, 2, 2, 4, 576): return launch<64, 2, 2, 2, 4, 576>(a, stream);
+        default: return launch<64, 2, 2, 4, 4, 1024>(a, stream);
     }
 }
 
