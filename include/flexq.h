@@ -125,6 +125,22 @@ flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, cons
                                     int cur_len, int bits, int group_size, void *out_f16,
                                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* Top-K sparse decode attention, FlexGen's "4-bit-S":
+ * scores s_t = q . K^_t / sqrt(head_dim) for t in [0, cur_len); the `keep`
+ * highest scores are kept (equal scores: lower token index first); out fp16
+ * [batch][heads][head_dim] = sum over kept t of p_t V^_t, softmax
+ * renormalised over the kept set.  Only the kept V rows are read
+ * (P:856).  The paper keeps the top 10%: keep = ceil(0.1 * cur_len).
+ * sel_i32 (optional, may be NULL): int32 [batch][heads][keep] receives the
+ * kept token indices in ascending order.  Workspace as for
+ * flexq_decode_attention.  Supported: cur_len <= 1152 (else
+ * FLEXQ_ERR_UNSUPPORTED); 1 <= keep <= cur_len (else FLEXQ_ERR_ARG). */
+flexq_status flexq_decode_attention_topk(const void *q_f16, const void *k_cache, const void *v_cache,
+                                         int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                         int cur_len, int keep, int bits, int group_size, void *out_f16,
+                                         void *sel_i32, void *workspace, size_t workspace_bytes,
+                                         void *stream);
+
 #ifdef __cplusplus
 }
 #endif

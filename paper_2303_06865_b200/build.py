@@ -27,6 +27,7 @@ SOURCES = {
     "flexq_api.cu": [],
     "quant.cu": ["-fmad=false", "-prec-div=true", "-ftz=false"],
     "decode_attention.cu": [],
+    "decode_attention_topk.cu": [],
 }
 
 
@@ -46,7 +47,8 @@ def _stale(out: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, "flexq_internal.h"), os.path.join(INCLUDE, "flexq.h"), __file__]
+    headers = [os.path.join(CSRC, "flexq_internal.h"), os.path.join(CSRC, "attn_common.cuh"),
+               os.path.join(INCLUDE, "flexq.h"), __file__]
     objs = []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)

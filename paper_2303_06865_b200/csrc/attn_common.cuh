@@ -1,0 +1,280 @@
+// attn_common.cuh -- shared pieces of the decode-attention kernels (dense and
+// Top-K sparse): stage geometry of the chunked KV cache, PTX helpers (mbarrier,
+// 1-D TMA bulk copy), the nibble -> float unpack, and the per-iteration K-score
+// and P.V bodies.  See decode_attention.cu for the design notes.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "flexq_internal.h"
+
+namespace flexq {
+namespace {
+
+// One stage = NCH consecutive 32-token chunks of one cache (K or V); its smem
+// image has the HBM layout: per chunk [codes 32 x D/2][meta 32 x D/16].
+template <int D, int NCH>
+struct Cfg {
+    static constexpr int LPT = D / 32;                 // lanes per token
+    static constexpr int TPI = 32 / LPT;               // tokens per warp iteration
+    static constexpr int CH = kChunk * NCH;            // tokens per stage
+    static constexpr int CB = D / 2;                   // code bytes per token
+    static constexpr int MB = D / 16;                  // meta bytes per token (D/64 half2)
+    static constexpr int ITERS = CH / TPI;
+    static constexpr int CHB = kChunk * (CB + MB);     // chunk bytes (18 D)
+    static constexpr int OFF_M = kChunk * CB;          // meta inside a chunk
+    static constexpr int OFF_Q = NCH * CHB;
+    static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
+    static_assert(STAGE % 16 == 0 && CHB % 16 == 0, "stage alignment");
+    static_assert(kChunk % TPI == 0, "an iteration stays inside one chunk");
+    // byte offsets of iteration i's codes / meta rows (token slot 0 of the iteration)
+    static constexpr int code_off(int i) { return (i * TPI / kChunk) * CHB + (i * TPI % kChunk) * CB; }
+    static constexpr int meta_off(int i) { return (i * TPI / kChunk) * CHB + OFF_M + (i * TPI % kChunk) * MB; }
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    return *reinterpret_cast<const uint4*>(p);
+}
+
+// Nibble e of a 32-bit code word as the float 2^23 + c_e * 16^k:
+// e = 0..4 in place (bits 4e..4e+3, k = e); e = 5..7 from w >> 12 at bits
+// 8..19 (k = e - 3).  The magic exponent lives in a register so that
+// (w & mask) | magic is a single LOP3 (LOP3 takes one immediate).
+__device__ __forceinline__ uint32_t magic_reg() {
+    uint32_t m;
+    asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(m));
+    return m;
+}
+template <uint32_t M>
+__device__ __forceinline__ float nib(uint32_t w, uint32_t magic) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(M), "r"(magic));  // (a & b) | c
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ void unpack8(uint32_t w, uint32_t magic, float2 (&f)[4]) {
+    const uint32_t w12 = w >> 12;
+    const float2 bias = make_float2(-8388608.0f, -8388608.0f);
+    f[0] = __fadd2_rn(make_float2(nib<0x0000Fu>(w, magic), nib<0x000F0u>(w, magic)), bias);     // (c0, 16 c1)
+    f[1] = __fadd2_rn(make_float2(nib<0x00F00u>(w, magic), nib<0x0F000u>(w, magic)), bias);     // (256 c2, 4096 c3)
+    f[2] = __fadd2_rn(make_float2(nib<0xF0000u>(w, magic), nib<0x00F00u>(w12, magic)), bias);   // (65536 c4, 256 c5)
+    f[3] = __fadd2_rn(make_float2(nib<0x0F000u>(w12, magic), nib<0xF0000u>(w12, magic)), bias); // (4096 c6, 65536 c7)
+}
+// 2^-k of the two nibbles of pair p (order of unpack8).
+__device__ __forceinline__ float2 inv_shift(int pair) {
+    switch (pair) {
+        case 0: return make_float2(1.0f, 0.0625f);
+        case 1: return make_float2(0.00390625f, 0.000244140625f);
+        case 2: return make_float2(1.52587890625e-05f, 0.00390625f);
+        default: return make_float2(0.000244140625f, 1.52587890625e-05f);
+    }
+}
+
+struct Desc {        // per-slot descriptor (shared memory)
+    int unit;        // work unit id (-1: none)
+    int bh;          // (batch, head) index of the unit
+    int t0;          // first token of the stage, relative to the unit
+    int flags;       // kFirst | kV | kLastK | kLast, tokens in the stage << 8
+};
+constexpr int kFirst = 1, kV = 2, kLastK = 4, kLast = 8;
+
+struct Params {
+    const __half* q;
+    const uint8_t* kc;   // chunked K cache
+    const uint8_t* vc;   // chunked V cache
+    __half* out;
+    uint32_t* ctrl;      // [0] next ticket, [1] finished warps
+    uint32_t* tickets;   // per (b, h): finished splits
+    float* part;         // [unit][D] partial numerators
+    float2* ml;          // [unit] (m, l)
+    int bh_total, chunks, cur_len, nsplit, split_len;
+    float qscale;        // log2(e) / sqrt(D)
+};
+
+// Pass 1, one warp iteration (tokens i*TPI + [0, TPI) of the stage): scores -> smem (log2 domain).
+// lc / lm: the lane's byte offsets inside a token row (codes / meta).
+template <int D, int NCH, bool FULL>
+__device__ __forceinline__ void k_iter(int i, const float2 (&qp)[16], float qsum, const uint8_t* sb, float* sc,
+                                       int t0, int tl, int n, int lc, int lm, int sg, uint32_t magic, float& mx) {
+    using C = Cfg<D, NCH>;
+    const int tok = i * C::TPI + tl;
+    const uint4 kw = lds128(sb + C::code_off(i) + lc);
+    const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::meta_off(i) + lm));
+    float2 d0 = make_float2(0.0f, 0.0f), d1 = d0;
+    float2 f[4];
+    unpack8(kw.x, magic, f);
+    d0 = __ffma2_rn(qp[0], f[0], d0); d1 = __ffma2_rn(qp[1], f[1], d1);
+    d0 = __ffma2_rn(qp[2], f[2], d0); d1 = __ffma2_rn(qp[3], f[3], d1);
+    unpack8(kw.y, magic, f);
+    d0 = __ffma2_rn(qp[4], f[0], d0); d1 = __ffma2_rn(qp[5], f[1], d1);
+    d0 = __ffma2_rn(qp[6], f[2], d0); d1 = __ffma2_rn(qp[7], f[3], d1);
+    unpack8(kw.z, magic, f);
+    d0 = __ffma2_rn(qp[8], f[0], d0); d1 = __ffma2_rn(qp[9], f[1], d1);
+    d0 = __ffma2_rn(qp[10], f[2], d0); d1 = __ffma2_rn(qp[11], f[3], d1);
+    unpack8(kw.w, magic, f);
+    d0 = __ffma2_rn(qp[12], f[0], d0); d1 = __ffma2_rn(qp[13], f[1], d1);
+    d0 = __ffma2_rn(qp[14], f[2], d0); d1 = __ffma2_rn(qp[15], f[3], d1);
+    d0 = __fadd2_rn(d0, d1);
+    float s = fmaf(km.x, d0.x + d0.y, km.y * qsum);
+#pragma unroll
+    for (int o = 1; o < C::LPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (FULL || tok < n) {
+        mx = fmaxf(mx, s);
+        if (sg == 0) sc[t0 + tok] = s;
+    }
+}
+
+// acc_j += (p scale) c_j over the lane's 32 columns, bias += p min, l += p.
+__device__ __forceinline__ void v_accum(float2 (&acc)[16], float& l, float& bsum, uint4 vw, float2 vm, float p,
+                                        uint32_t magic) {
+    l += p;
+    const float a = p * vm.x;
+    bsum = fmaf(p, vm.y, bsum);
+    const float2 a2 = make_float2(a, a);
+    float2 f[4];
+    unpack8(vw.x, magic, f);
+    acc[0] = __ffma2_rn(a2, f[0], acc[0]); acc[1] = __ffma2_rn(a2, f[1], acc[1]);
+    acc[2] = __ffma2_rn(a2, f[2], acc[2]); acc[3] = __ffma2_rn(a2, f[3], acc[3]);
+    unpack8(vw.y, magic, f);
+    acc[4] = __ffma2_rn(a2, f[0], acc[4]); acc[5] = __ffma2_rn(a2, f[1], acc[5]);
+    acc[6] = __ffma2_rn(a2, f[2], acc[6]); acc[7] = __ffma2_rn(a2, f[3], acc[7]);
+    unpack8(vw.z, magic, f);
+    acc[8] = __ffma2_rn(a2, f[0], acc[8]); acc[9] = __ffma2_rn(a2, f[1], acc[9]);
+    acc[10] = __ffma2_rn(a2, f[2], acc[10]); acc[11] = __ffma2_rn(a2, f[3], acc[11]);
+    unpack8(vw.w, magic, f);
+    acc[12] = __ffma2_rn(a2, f[0], acc[12]); acc[13] = __ffma2_rn(a2, f[1], acc[13]);
+    acc[14] = __ffma2_rn(a2, f[2], acc[14]); acc[15] = __ffma2_rn(a2, f[3], acc[15]);
+}
+
+// Pass 2, one warp iteration: acc_j += (p scale) c_j, bias += p min for TPI tokens.
+template <int D, int NCH, bool FULL>
+__device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float& bsum, const uint8_t* sb,
+                                       const float* sc, float M, int t0, int tl, int n, int lc, int lm,
+                                       uint32_t magic) {
+    using C = Cfg<D, NCH>;
+    const int tok = i * C::TPI + tl;
+    const uint4 vw = lds128(sb + C::code_off(i) + lc);
+    float2 vm = __half22float2(*reinterpret_cast<const __half2*>(sb + C::meta_off(i) + lm));
+    float p = ex2(sc[t0 + tok] - M);
+    if (!FULL) {
+        const bool valid = tok < n;
+        p = valid ? p : 0.0f;
+        vm.x = valid ? vm.x : 0.0f;
+        vm.y = valid ? vm.y : 0.0f;
+    }
+    v_accum(acc, l, bsum, vw, vm, p, magic);
+}
+
+// q (fp16, 64 B of the lane's 32 columns at qs) -> qp = q * qscale * 2^-k (unpack8
+// pair order) and qsum = sum of q * qscale.
+__device__ __forceinline__ void load_q(const uint8_t* qs, float qscale, float2 (&qp)[16], float& qsum) {
+    const uint4 q0 = lds128(qs), q1 = lds128(qs + 16), q2 = lds128(qs + 32), q3 = lds128(qs + 48);
+    const uint32_t qw[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                             q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {     // pair k = columns 2k, 2k+1 = word k/4, pair k%4
+        float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qw[k]));
+        f = __fmul2_rn(f, make_float2(qscale, qscale));
+        acc += f.x + f.y;
+        qp[k] = __fmul2_rn(f, inv_shift(k & 3));
+    }
+    qsum = acc;
+}
+
+// End of a unit: remove the 16^k factors, reduce (acc, l, bsum) over the token
+// lanes (reduce-scatter for acc: lane keeps D/32 columns), and return the
+// lane's column offset col0; v[0 .. D/32) = sum_t (p scale) c + bias (unnormalised).
+template <int D>
+__device__ __forceinline__ int reduce_unit(float2 (&acc)[16], float& l, float& bsum, int lane, int sg,
+                                           float (&v)[32]) {
+    constexpr int LPT = D / 32;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = __fmul2_rn(acc[k], inv_shift(k & 3));
+#pragma unroll
+    for (int o = LPT; o < 32; o <<= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+        bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { v[2 * k] = acc[k].x; v[2 * k + 1] = acc[k].y; }
+    int width = 32;   // live entries
+    int base = 0;     // column offset (within the 32-column segment) of v[0]
+#pragma unroll
+    for (int o = 16; o >= LPT; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+        const int half = width >> 1;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (k < half) {
+                const float send = upper ? v[k] : v[k + half];
+                const float keep = upper ? v[k + half] : v[k];
+                v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        if (upper) base += half;
+        width = half;
+    }
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) v[k] += bsum;
+    return sg * 32 + base;
+}
+
+// out[col0 .. col0 + D/32) = v / l as fp16.
+template <int D>
+__device__ __forceinline__ void write_out(__half* dst, const float (&v)[32], float l) {
+    const float inv = 1.0f / l;
+    if constexpr (D == 128) {
+        __half2 h0 = __floats2half2_rn(v[0] * inv, v[1] * inv);
+        __half2 h1 = __floats2half2_rn(v[2] * inv, v[3] * inv);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(dst) = w;
+    } else {
+        *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(v[0] * inv, v[1] * inv);
+    }
+}
+
+}  // namespace
+}  // namespace flexq

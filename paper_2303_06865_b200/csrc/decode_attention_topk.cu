@@ -1,0 +1,351 @@
+// decode_attention_topk.cu -- Top-K sparse decode attention over the 4-bit
+// compressed KV cache (FlexGen Sec. 4 "Sparse Attention", PAPER.md P:853-857,
+// SPEC S:496-504).
+//
+//   s_t = q . K^_t / sqrt(D) for every cached token (pass 1, full K stream);
+//   keep the `keep` largest s_t (equal scores: lower token index first);
+//   out = sum_{t kept} p_t V^_t with p renormalised over the kept set.
+//
+// Only the kept V rows are loaded ("only load a subset of the V cache",
+// P:856): at keep = 10% the step reads K (0.5625 B/elem) + 10% of V instead of
+// all of V, ~55% of the dense bytes.
+//
+// Design: persistent warps, one warp = one (b, h) (no context split; the
+// per-warp score buffer holds kTopkMaxTokens).  Pass 1 is the dense kernel's
+// TMA-bulk-staged K pass (attn_common.cuh).  Selection is an exact 4-round
+// radix select (8-bit digits) on order-preserving 32-bit keys of the fp32
+// scores, a warp-local smem histogram per round; ties at the threshold key go
+// to the lowest token indices (ballot prefix counts), so the kept set is the
+// definition's.  Pass 2 gathers the kept V rows straight from HBM (16 B per
+// lane, 128-bit loads, software-prefetched one group ahead) into the same
+// register accumulators as the dense P.V.
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "attn_common.cuh"
+#include "flexq_internal.h"
+
+namespace flexq {
+namespace {
+
+struct TopkParams {
+    const __half* q;
+    const uint8_t* kc;
+    const uint8_t* vc;
+    __half* out;
+    int32_t* sel;        // optional [bh][keep] kept token indices (ascending)
+    uint32_t* ctrl;      // [0] next ticket, [1] finished warps (workspace)
+    int bh_total, chunks, cur_len, keep;
+    float qscale;
+};
+
+__device__ __forceinline__ uint32_t order_key(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
+}
+
+__device__ __forceinline__ uint4 ldg_nc128(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ldg_nc32(const void* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+template <int D, int NCH, int S, int WPC>
+__global__ void __launch_bounds__(WPC * 32)
+decode_attention_topk_kernel(const TopkParams P) {
+    using C = Cfg<D, NCH>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    uint8_t* ring = smem + warp * (S * C::STAGE);
+    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (kTopkMaxTokens * 6 + 256 * 4);
+    float* scores = reinterpret_cast<float*>(wsm);
+    uint16_t* kept = reinterpret_cast<uint16_t*>(wsm + kTopkMaxTokens * 4);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + kTopkMaxTokens * 6);
+    uint8_t* tail = smem + WPC * (S * C::STAGE + kTopkMaxTokens * 6 + 256 * 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tail) + warp * S;
+    Desc* desc = reinterpret_cast<Desc*>(tail + WPC * S * 8) + warp * S;
+
+    const uint64_t policy = evict_first_policy();
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_proxy_async();
+    }
+    __syncwarp();
+
+    // ---------------- producer: K stages of whole (b, h) units
+    int p_bh = -1, p_tok = 0;
+    auto next_unit = [&]() {
+        int t = 0;
+        if (lane == 0) t = int(atomicAdd(P.ctrl, 1u));
+        t = __shfl_sync(0xffffffffu, t, 0);
+        p_bh = t < P.bh_total ? t : -1;
+        p_tok = 0;
+    };
+    auto issue = [&](int slot) {
+        if (lane == 0) {
+            Desc d;
+            uint32_t bytes = 0;
+            if (p_bh >= 0) {
+                const int n = min(C::CH, P.cur_len - p_tok);
+                d.unit = p_bh;
+                d.bh = p_bh;
+                d.t0 = p_tok;
+                d.flags = (p_tok == 0 ? kFirst : 0) | (p_tok + C::CH >= P.cur_len ? kLastK : 0) | (n << 8);
+                bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
+            } else {
+                d.unit = -1; d.bh = 0; d.t0 = 0; d.flags = 0;
+            }
+            desc[slot] = d;
+            fence_proxy_async();
+            mbar_expect_tx(&bars[slot], bytes + ((d.flags & kFirst) ? 2 * D : 0));
+            if (p_bh >= 0) {
+                uint8_t* sb = ring + slot * C::STAGE;
+                const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
+                bulk_g2s(sb, P.kc + chunk * C::CHB, bytes, &bars[slot], policy);
+                if (d.flags & kFirst) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
+            }
+        }
+        if (p_bh >= 0) {
+            p_tok += C::CH;
+            if (p_tok >= P.cur_len) next_unit();
+        }
+    };
+    next_unit();
+#pragma unroll 1
+    for (int s = 0; s < S - 1; ++s) issue(s);
+
+    const int tl = lane / C::LPT;
+    const int sg = lane % C::LPT;
+    const int lc = tl * C::CB + sg * 16;
+    const int lm = tl * C::MB + (sg >> 1) * 4;
+    const uint32_t magic = magic_reg();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int n_tok = P.cur_len;
+    const int keep = P.keep;
+
+    int slot = 0;
+    uint32_t parity = 0;
+#pragma unroll 1
+    for (;;) {
+        issue(slot == 0 ? S - 1 : slot - 1);
+        mbar_wait(&bars[slot], parity);
+        Desc d = desc[slot];
+        if (d.unit < 0) break;
+        const int bh = d.bh;
+        const uint8_t* sb = ring + slot * C::STAGE;
+
+        // ------------------------------------------------ pass 1: all scores -> smem
+        float M;
+        {
+            float2 qp[16];
+            float qsum;
+            load_q(sb + C::OFF_Q + sg * 64, P.qscale, qp, qsum);
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (;;) {
+                const int n = d.flags >> 8;
+                if (n == C::CH) {
+#pragma unroll 4
+                    for (int i = 0; i < C::ITERS; ++i)
+                        k_iter<D, NCH, true>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                } else {
+#pragma unroll 1
+                    for (int i = 0; i < C::ITERS; ++i)
+                        if (i * C::TPI < n)
+                            k_iter<D, NCH, false>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                }
+                const bool last = d.flags & kLastK;
+                __syncwarp();
+                if (++slot == S) {
+                    slot = 0;
+                    parity ^= 1u;
+                }
+                if (last) break;
+                issue(slot == 0 ? S - 1 : slot - 1);
+                mbar_wait(&bars[slot], parity);
+                d = desc[slot];
+                sb = ring + slot * C::STAGE;
+            }
+#pragma unroll
+            for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            M = mx;   // the largest score is always kept, so M is the kept set's max
+        }
+
+        // ------------------------------------------------ select: key of rank `keep` (radix, 4 x 8 bits)
+        uint32_t prefix = 0, pmask = 0;
+        int krem = keep;                       // rank still to find among keys matching prefix
+#pragma unroll 1
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int b = lane; b < 256; b += 32) hist[b] = 0;
+            __syncwarp();
+            for (int t = lane; t < n_tok; t += 32) {
+                const uint32_t k = order_key(scores[t]);
+                if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+            }
+            __syncwarp();
+            int c[8], local = 0;                // lane owns bins 255-8*lane .. 248-8*lane (descending)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                c[i] = int(hist[255 - (lane * 8 + i)]);
+                local += c[i];
+            }
+            int incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int excl = incl - local;
+            const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && krem <= incl);
+            const int src = __ffs(hit) - 1;
+            int digit = 0, above = 0;
+            if (lane == src) {
+                int acc = excl;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (acc + c[i] >= krem) {
+                        digit = 255 - (lane * 8 + i);
+                        above = acc;
+                        break;
+                    }
+                    acc += c[i];
+                }
+            }
+            digit = __shfl_sync(0xffffffffu, digit, src);
+            above = __shfl_sync(0xffffffffu, above, src);
+            krem -= above;
+            prefix |= uint32_t(digit) << shift;
+            pmask |= 255u << shift;
+            __syncwarp();
+        }
+        // kept: key > T, or key == T among the first krem such tokens by index
+        {
+            int base = 0, ties = 0;
+#pragma unroll 1
+            for (int t0 = 0; t0 < n_tok; t0 += 32) {
+                const int t = t0 + lane;
+                const bool in = t < n_tok;
+                const uint32_t k = in ? order_key(scores[t]) : 0u;
+                const bool gt = in && k > prefix;
+                const bool eq = in && k == prefix;
+                const unsigned beq = __ballot_sync(0xffffffffu, eq);
+                const bool keepit = gt || (eq && ties + __popc(beq & lt_mask) < krem);
+                const unsigned bk = __ballot_sync(0xffffffffu, keepit);
+                if (keepit) kept[base + __popc(bk & lt_mask)] = uint16_t(t);
+                base += __popc(bk);
+                ties += __popc(beq);
+            }
+            __syncwarp();
+            if (P.sel)
+                for (int j = lane; j < keep; j += 32) P.sel[int64_t(bh) * keep + j] = kept[j];
+        }
+
+        // ------------------------------------------------ pass 2: gather the kept V rows
+        float2 acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
+        float l = 0.0f, bsum = 0.0f;
+        const uint8_t* vbase = P.vc + int64_t(bh) * P.chunks * C::CHB;
+        auto row_of = [&](int j, int& t) -> bool {
+            t = j < keep ? int(kept[j]) : 0;
+            return j < keep;
+        };
+        int t_cur;
+        bool v_cur = row_of(tl, t_cur);
+        const uint8_t* rc = vbase + (t_cur >> 5) * C::CHB + (t_cur & 31) * C::CB + sg * 16;
+        uint4 w_cur = v_cur ? ldg_nc128(rc) : make_uint4(0, 0, 0, 0);
+        uint32_t m_cur = v_cur ? ldg_nc32(vbase + (t_cur >> 5) * C::CHB + C::OFF_M + (t_cur & 31) * C::MB +
+                                          (sg >> 1) * 4)
+                               : 0u;
+#pragma unroll 1
+        for (int g = 0; g * C::TPI < keep; ++g) {
+            int t_nxt;
+            const bool v_nxt = row_of((g + 1) * C::TPI + tl, t_nxt);
+            uint4 w_nxt = make_uint4(0, 0, 0, 0);
+            uint32_t m_nxt = 0u;
+            if (v_nxt) {   // prefetch the next group's rows
+                const uint8_t* cb = vbase + (t_nxt >> 5) * C::CHB;
+                w_nxt = ldg_nc128(cb + (t_nxt & 31) * C::CB + sg * 16);
+                m_nxt = ldg_nc32(cb + C::OFF_M + (t_nxt & 31) * C::MB + (sg >> 1) * 4);
+            }
+            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&m_cur));
+            float p = ex2(scores[t_cur] - M);
+            if (!v_cur) {
+                p = 0.0f;
+                vm = make_float2(0.0f, 0.0f);
+            }
+            v_accum(acc, l, bsum, w_cur, vm, p, magic);
+            t_cur = t_nxt;
+            v_cur = v_nxt;
+            w_cur = w_nxt;
+            m_cur = m_nxt;
+        }
+        float v[32];
+        const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
+        write_out<D>(P.out + int64_t(bh) * D + col0, v, l);
+        __syncwarp();
+    }
+
+    if (lane == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * WPC;
+        if (atomicAdd(P.ctrl + 1, 1u) == total - 1) {
+            P.ctrl[0] = 0u;
+            P.ctrl[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+template <int D, int NCH, int S, int WPC>
+constexpr size_t topk_smem_bytes() {
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + kTopkMaxTokens * 6 + 256 * 4);
+}
+
+template <int D, int NCH, int S, int WPC>
+cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
+    static int occ = -1;
+    auto k = decode_attention_topk_kernel<D, NCH, S, WPC>;
+    const size_t smem = topk_smem_bytes<D, NCH, S, WPC>();
+    if (occ < 0) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem);
+        occ = o > 0 ? o : 1;
+    }
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int bh = a.batch * a.heads;
+    const int ctas = min(sms * occ, (bh + WPC - 1) / WPC);
+    TopkParams P;
+    P.q = static_cast<const __half*>(a.q);
+    P.kc = static_cast<const uint8_t*>(a.k_cache);
+    P.vc = static_cast<const uint8_t*>(a.v_cache);
+    P.out = static_cast<__half*>(a.out);
+    P.sel = static_cast<int32_t*>(a.sel);
+    P.ctrl = static_cast<uint32_t*>(a.workspace);
+    P.bh_total = bh;
+    P.chunks = a.chunks;
+    P.cur_len = a.cur_len;
+    P.keep = a.keep;
+    P.qscale = 1.4426950408889634f / sqrtf(float(D));
+    k<<<ctas, WPC * 32, smem, stream>>>(P);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
+    if (a.head_dim == 128) return launch_topk<128, 2, 2, 4>(a, stream);
+    return launch_topk<64, 2, 2, 4>(a, stream);
+}
+
+}  // namespace flexq

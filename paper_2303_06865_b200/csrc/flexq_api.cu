@@ -132,4 +132,26 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, cons
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
+flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache, const void* v_cache,
+                                         int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                         int cur_len, int keep, int bits, int group_size, void* out_f16,
+                                         void* sel_i32, void* workspace, size_t workspace_bytes, void* stream) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s == FLEXQ_ERR_ARG) return s;
+    const int t_cap = prompt_len + gen_len;
+    if (cur_len < 1 || cur_len > t_cap || keep < 1 || keep > cur_len) return FLEXQ_ERR_ARG;
+    if (s != FLEXQ_OK) return s;
+    if (cur_len > flexq::kTopkMaxTokens) return FLEXQ_ERR_UNSUPPORTED;
+    if (!q_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16) ||
+        (sel_i32 && !aligned16(sel_i32)))
+        return FLEXQ_ERR_ALIGN;
+    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+        return FLEXQ_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
+    flexq::TopkArgs a{q_f16, k_cache, v_cache, out_f16, sel_i32, workspace, batch, heads, head_dim,
+                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, keep};
+    return from_cuda(flexq::launch_decode_attention_topk(a, static_cast<cudaStream_t>(stream)));
+}
+
 }  // extern "C"

@@ -43,4 +43,18 @@ struct AttnArgs {
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
 
+// Top-K sparse attention: one warp per (b, h), so the context is
+// bounded by the per-warp score buffer.
+constexpr int kTopkMaxTokens = 1152;
+struct TopkArgs {
+    const void* q;
+    const void* k_cache;
+    const void* v_cache;
+    void* out;
+    void* sel;          // optional int32 [batch*heads][keep]
+    void* workspace;    // scheduler counters (same workspace as the dense kernel)
+    int batch, heads, head_dim, chunks, cur_len, keep;
+};
+cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream);
+
 }  // namespace flexq

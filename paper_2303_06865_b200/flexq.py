@@ -51,8 +51,9 @@ def lib():
         L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
         L.flexq_decode_attention_workspace_size.restype = SZ
         L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 8 + [P, P, SZ, P]
+        L.flexq_decode_attention_topk.argtypes = [P, P, P] + [I] * 9 + [P, P, P, SZ, P]
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
-                  "flexq_decode_attention"):
+                  "flexq_decode_attention", "flexq_decode_attention_topk"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -208,4 +209,27 @@ def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=No
                                         cur_len, cache.bits, cache.group_size, out.data_ptr(),
                                         workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "flexq_decode_attention")
+    return out
+
+
+def topk_keep(cur_len: int, fraction: float = 0.1) -> int:
+    """Tokens kept by FlexGen's Top-K sparse attention: ceil(fraction * cur_len)."""
+    import math
+    return max(1, min(cur_len, math.ceil(fraction * cur_len - 1e-9)))
+
+
+def flexq_decode_attention_topk(q: torch.Tensor, cache: KVCache, cur_len: int, keep: int, out=None, sel=None,
+                                workspace=None, stream=None) -> torch.Tensor:
+    """Top-K sparse decode attention.  sel: optional int32 [B][H][keep] output
+    receiving the kept token indices (ascending)."""
+    _need(q, torch.float16, "q")
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = make_workspace(cache)
+    _check(lib().flexq_decode_attention_topk(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
+                                             cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
+                                             cur_len, keep, cache.bits, cache.group_size, out.data_ptr(),
+                                             _ptr(sel), workspace.data_ptr(), workspace.numel(), _stream(stream)),
+           "flexq_decode_attention_topk")
     return out

@@ -102,3 +102,20 @@ def test_kv_cache_bytes(L):
     assert fq.token_stride(513) == 544 and fq.token_stride(1) == 32 and fq.token_stride(32) == 32
     with __import__("pytest").raises(fq.FlexqError):
         fq.flexq_kv_cache_bytes(1, 1, 96, 8, 8)
+
+
+def test_topk_validation(L):
+    f = L.flexq_decode_attention_topk
+    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+
+    def call(cur=5, keep=2, D=128, q=A, out=A, sel=None, w=A, s=8, n=4):
+        return f(q, A, A, 2, 3, D, s, n, cur, keep, 4, 64, out, sel, w, ws, None)
+    assert call(keep=0) == fq.FLEXQ_ERR_ARG
+    assert call(keep=6) == fq.FLEXQ_ERR_ARG          # keep > cur_len
+    assert call(cur=13) == fq.FLEXQ_ERR_ARG
+    assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(cur=1153, keep=5, s=1200, n=0) == fq.FLEXQ_ERR_UNSUPPORTED   # beyond the score buffer
+    assert call(q=None) == fq.FLEXQ_ERR_NULL
+    assert call(sel=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
+    assert fq.topk_keep(543) == 55 and fq.topk_keep(130) == 13 and fq.topk_keep(5) == 1

@@ -224,3 +224,42 @@ def test_opt175b_full_size_sampled(orc, cuda):
         qh = synth.gather(seed, synth.tensor_id(0, synth.Q, steps), (B, H, D), [b, h, slice(None)])
         ref = orc.attention_f64(qh.numpy(), okc, ovc, s + steps)
         assert_attn_close(out[b:b + 1, h:h + 1], ref, f"(b={b}, h={h})")
+
+
+# ---------------------------------------------------------------- NEXT-1: Top-K sparse attention
+TOPK_CASES = [
+    # name, B, H, D, s, n, steps, outliers, qfactor, keep fraction
+    ("d128_10pct", 3, 8, 128, 300, 4, 3, False, 4, 0.1),
+    ("d64_10pct_outliers", 2, 6, 64, 512, 1, 1, True, 16, 0.1),
+    ("d128_keep_all", 1, 4, 128, 70, 2, 1, False, 1, 1.0),
+    ("d128_keep_one", 2, 3, 128, 90, 2, 2, False, 8, 0.0),
+    ("d128_opt175b_len", 2, 16, 128, 512, 32, 31, False, 1, 0.1),
+]
+
+
+@pytest.mark.parametrize("case", TOPK_CASES, ids=[c[0] for c in TOPK_CASES])
+def test_topk_attention_parity(orc, cuda, case):
+    """The GPU's kept set must be a valid top-`keep` set of the oracle's scores
+    (several sets are correct when scores tie within rounding), and the output
+    must match the oracle evaluated on that set within reading Q's tolerance."""
+    name, B, H, D, s, n, steps, outl, qf, frac = case
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, steps, seed=60, outliers=outl, qfactor=qf)
+    keep = fq.topk_keep(cur, frac) if frac > 0 else 1
+    sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
+    out = fq.flexq_decode_attention_topk(q.to(cuda), cache, cur, keep, sel=sel)
+    torch.cuda.synchronize()
+    sel = sel.cpu().numpy()
+    _, omask, scores = orc.attention_topk_f64(q.numpy(), okc, ovc, cur, keep)
+    mask = np.zeros((B, H, cur), np.uint8)
+    for b in range(B):
+        for h in range(H):
+            idx = sel[b, h]
+            assert np.all(np.diff(idx) > 0) and idx.min() >= 0 and idx.max() < cur, (b, h)
+            mask[b, h, idx] = 1
+            sc = scores[b, h]
+            eps = 1e-4 * max(1.0, np.abs(sc).max())
+            if keep < cur:
+                assert sc[idx].min() >= sc[mask[b, h] == 0].max() - eps, (b, h)
+    assert (mask != omask).sum() <= 2 * B * H          # differences only at near-ties
+    ref, _, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, cur, keep, sel=mask)
+    assert_attn_close(out.cpu().numpy(), ref, name)
