@@ -45,17 +45,20 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
+    """Build libflexq.so (or, for A/B tuning, libflexq_<tag>.so with extra -D defines)."""
+    build_dir = BUILD + ("_" + tag if tag else "")
+    lib = LIB if not tag else LIB.replace("libflexq.so", f"libflexq_{tag}.so")
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, "flexq_internal.h"), os.path.join(CSRC, "attn_common.cuh"),
                os.path.join(INCLUDE, "flexq.h"), __file__]
     objs = []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", s, "-o", o]
+            cmd = [nvcc(), *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -63,15 +66,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(r.stderr)
             with open(o + ".ptxas.txt", "w") as f:
                 f.write(r.stderr)
-    if force or _stale(LIB, objs):
-        tmp = LIB + ".tmp%d" % os.getpid()
+    if force or _stale(lib, objs):
+        tmp = lib + ".tmp%d" % os.getpid()
         cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    if "--ab" in sys.argv:   # A/B library for tuning: fp32-magic nibble unpack
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=0",), tag="f32unpack"))

@@ -77,37 +77,96 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
     return *reinterpret_cast<const uint4*>(p);
 }
 
-// Nibble e of a 32-bit code word as the float 2^23 + c_e * 16^k:
-// e = 0..4 in place (bits 4e..4e+3, k = e); e = 5..7 from w >> 12 at bits
-// 8..19 (k = e - 3).  The magic exponent lives in a register so that
-// (w & mask) | magic is a single LOP3 (LOP3 takes one immediate).
+#ifndef FLEXQ_H16_UNPACK
+#define FLEXQ_H16_UNPACK 0
+#endif
+
+// Nibble -> float conversion of one 32-bit code word (8 codes, columns e = 0..7
+// of the word).  Two implementations (FLEXQ_H16_UNPACK):
+//  1: fp16 magic.  (w & 0x000F000F) | 0x64006400 is the half2
+//    (1024 + c0, 1024 + c4) in ONE LOP3 for two codes; the mixed-precision
+//    add.rn.f32.f16 (SASS FHADD, FMA pipe) subtracts 1024 exactly while widening
+//    to fp32.  Pairs: f[0] = (c0, c4), f[1] = 16 (c1, c5), f[2] = (c2, c6),
+//    f[3] = 16 (c3, c7)  (w >> 8 supplies c2, c3, c6, c7).
+//  0 (default): fp32 magic.  (w & 0xF<<4e) | 0x4B000000 = 2^23 + c_e 16^e (one LOP3 per
+//    code, e = 5..7 from w >> 12), one FADD2 removes 2^23 per pair.
+//    Pairs: f[0] = (c0, 16 c1), f[1] = (256 c2, 4096 c3), f[2] = (65536 c4, 256 c5),
+//    f[3] = (4096 c6, 65536 c7).
+// Either way the value is exact; the power-of-two factor is folded into q on
+// the K side and removed once per unit on the V side (inv_shift).  The magic
+// constant lives in a register so that (w & mask) | magic is a single LOP3.
 __device__ __forceinline__ uint32_t magic_reg() {
     uint32_t m;
+#if FLEXQ_H16_UNPACK
+    asm volatile("mov.b32 %0, 0x64006400;" : "=r"(m));
+#else
     asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(m));
+#endif
     return m;
 }
 template <uint32_t M>
-__device__ __forceinline__ float nib(uint32_t w, uint32_t magic) {
+__device__ __forceinline__ uint32_t lop_and_or(uint32_t w, uint32_t magic) {
     uint32_t r;
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(M), "r"(magic));  // (a & b) | c
-    return __uint_as_float(r);
+    return r;
+}
+__device__ __forceinline__ float2 fhadd2(uint32_t h2, float b) {   // (f32(h.lo) + b, f32(h.hi) + b)
+    unsigned short lo, hi;
+    asm("mov.b32 {%0,%1}, %2;" : "=h"(lo), "=h"(hi) : "r"(h2));
+    float x, y;
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(x) : "h"(lo), "f"(b));
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(y) : "h"(hi), "f"(b));
+    return make_float2(x, y);
+}
+// -1024.0f held in a register (FHADD has no immediate form; a compile-time
+// constant gets re-materialised with a MOV before every FHADD).
+__device__ __forceinline__ float neg1024_reg() {
+    float r;
+    asm volatile("mov.b32 %0, 0xC4800000;" : "=f"(r));
+    return r;
 }
 __device__ __forceinline__ void unpack8(uint32_t w, uint32_t magic, float2 (&f)[4]) {
+#if FLEXQ_H16_UNPACK
+    const uint32_t w8 = w >> 8;
+    float nb;   // -1024 (register); passed through an empty asm so it is not re-materialised
+    asm("mov.b32 %0, %1;" : "=f"(nb) : "r"(magic ^ 0x64006400u ^ 0xC4800000u));
+    f[0] = fhadd2(lop_and_or<0x000F000Fu>(w, magic), nb);    // (c0, c4)
+    f[1] = fhadd2(lop_and_or<0x00F000F0u>(w, magic), nb);    // 16 (c1, c5)
+    f[2] = fhadd2(lop_and_or<0x000F000Fu>(w8, magic), nb);   // (c2, c6)
+    f[3] = fhadd2(lop_and_or<0x00F000F0u>(w8, magic), nb);   // 16 (c3, c7)
+#else
     const uint32_t w12 = w >> 12;
     const float2 bias = make_float2(-8388608.0f, -8388608.0f);
-    f[0] = __fadd2_rn(make_float2(nib<0x0000Fu>(w, magic), nib<0x000F0u>(w, magic)), bias);     // (c0, 16 c1)
-    f[1] = __fadd2_rn(make_float2(nib<0x00F00u>(w, magic), nib<0x0F000u>(w, magic)), bias);     // (256 c2, 4096 c3)
-    f[2] = __fadd2_rn(make_float2(nib<0xF0000u>(w, magic), nib<0x00F00u>(w12, magic)), bias);   // (65536 c4, 256 c5)
-    f[3] = __fadd2_rn(make_float2(nib<0x0F000u>(w12, magic), nib<0xF0000u>(w12, magic)), bias); // (4096 c6, 65536 c7)
+    f[0] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x0000Fu>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x000F0u>(w, magic))), bias);
+    f[1] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x00F00u>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x0F000u>(w, magic))), bias);
+    f[2] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0xF0000u>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x00F00u>(w12, magic))), bias);
+    f[3] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x0F000u>(w12, magic)),
+                                  __uint_as_float(lop_and_or<0xF0000u>(w12, magic))), bias);
+#endif
 }
-// 2^-k of the two nibbles of pair p (order of unpack8).
+// 2^-k of the two codes of pair p (order of unpack8).
 __device__ __forceinline__ float2 inv_shift(int pair) {
+#if FLEXQ_H16_UNPACK
+    return (pair & 1) ? make_float2(0.0625f, 0.0625f) : make_float2(1.0f, 1.0f);
+#else
     switch (pair) {
         case 0: return make_float2(1.0f, 0.0625f);
         case 1: return make_float2(0.00390625f, 0.000244140625f);
         case 2: return make_float2(1.52587890625e-05f, 0.00390625f);
         default: return make_float2(0.000244140625f, 1.52587890625e-05f);
     }
+#endif
+}
+// Word-local column of element h (0 = .x, 1 = .y) of pair p (order of unpack8).
+__host__ __device__ constexpr int pair_col(int p, int h) {
+#if FLEXQ_H16_UNPACK
+    return p + 4 * h;
+#else
+    return 2 * p + h;
+#endif
 }
 
 struct Desc {        // per-slot descriptor (shared memory)
@@ -205,19 +264,21 @@ __device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float
     v_accum(acc, l, bsum, vw, vm, p, magic);
 }
 
-// q (fp16, 64 B of the lane's 32 columns at qs) -> qp = q * qscale * 2^-k (unpack8
-// pair order) and qsum = sum of q * qscale.
+// q (fp16, 64 B of the lane's 32 columns at qs) -> qp[4w + p] = q * qscale * 2^-k
+// at the columns of pair p of word w (unpack8 order), and qsum = sum of q * qscale.
 __device__ __forceinline__ void load_q(const uint8_t* qs, float qscale, float2 (&qp)[16], float& qsum) {
-    const uint4 q0 = lds128(qs), q1 = lds128(qs + 16), q2 = lds128(qs + 32), q3 = lds128(qs + 48);
-    const uint32_t qw[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
-                             q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+    const __half* qh = reinterpret_cast<const __half*>(qs);
     float acc = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {     // pair k = columns 2k, 2k+1 = word k/4, pair k%4
-        float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qw[k]));
-        f = __fmul2_rn(f, make_float2(qscale, qscale));
-        acc += f.x + f.y;
-        qp[k] = __fmul2_rn(f, inv_shift(k & 3));
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float x = __half2float(qh[8 * w + pair_col(p, 0)]) * qscale;
+            const float y = __half2float(qh[8 * w + pair_col(p, 1)]) * qscale;
+            acc += x + y;
+            const float2 sh = inv_shift(p);
+            qp[4 * w + p] = make_float2(x * sh.x, y * sh.y);
+        }
     }
     qsum = acc;
 }
@@ -237,7 +298,10 @@ __device__ __forceinline__ int reduce_unit(float2 (&acc)[16], float& l, float& b
         bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
     }
 #pragma unroll
-    for (int k = 0; k < 16; ++k) { v[2 * k] = acc[k].x; v[2 * k + 1] = acc[k].y; }
+    for (int k = 0; k < 16; ++k) {   // natural column order: v[col] (static register renaming)
+        v[8 * (k / 4) + pair_col(k & 3, 0)] = acc[k].x;
+        v[8 * (k / 4) + pair_col(k & 3, 1)] = acc[k].y;
+    }
     int width = 32;   // live entries
     int base = 0;     // column offset (within the 32-column segment) of v[0]
 #pragma unroll

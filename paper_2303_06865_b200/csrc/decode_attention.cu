@@ -53,7 +53,7 @@ constexpr int kMinUnitTokens = 512;    // smallest per-warp score buffer of any 
 // fully unrolled K and V bodies overflow the instruction cache).
 // MAXT: per-warp score buffer (tokens); longer contexts are split into units of <= MAXT.
 template <int D, int NCH, int S, int WPC, int UNR, int MAXT>
-__global__ void __launch_bounds__(WPC * 32, (20 / WPC) > 0 ? (20 / WPC) : 1)
+__global__ void __launch_bounds__(WPC * 32, (16 / WPC) > 0 ? (16 / WPC) : 1)
 decode_attention_kernel(const Params P) {
     using C = Cfg<D, NCH>;
     extern __shared__ __align__(128) uint8_t smem[];

@@ -33,7 +33,7 @@ def lib():
     """Load libflexq.so (building it in-tree with nvcc if it is missing)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("FLEXQ_LIB", _build.LIB)   # FLEXQ_LIB: A/B tuning builds only
         if not os.path.exists(path):
             try:
                 _build.build()
