@@ -78,5 +78,6 @@ def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "")
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
-    if "--ab" in sys.argv:   # A/B library for tuning: fp32-magic nibble unpack
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=0",), tag="f32unpack"))
+    if "--ab" in sys.argv:   # A/B libraries for tuning
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=1",), tag="h16unpack"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=1",), tag="kidp4a"))

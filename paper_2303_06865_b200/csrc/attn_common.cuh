@@ -190,31 +190,136 @@ struct Params {
     float qscale;        // log2(e) / sqrt(D)
 };
 
+#ifndef FLEXQ_K_IDP4A
+#define FLEXQ_K_IDP4A 0
+#endif
+
+// The lane's view of q for pass 1 (FLEXQ_K_IDP4A):
+//  0 (default): qp[4w + p] = q * qscale * 2^-k at the columns of pair p of word w
+//     (unpack8 order), qsum = sum q * qscale; the dot product runs on FFMA2.
+//  1: q as a 24-bit fixed-point integer per lane (scale 2^(23 - e), |q| < 2^e),
+//     split into three byte limbs packed to match the codes' lo / hi nibbles;
+//     the dot product runs on IDP.4A (exact in int32; q values within 2^-14 of
+//     the lane's max are represented exactly, smaller ones to 2^-23 of the max).
+struct KQuery {
+#if FLEXQ_K_IDP4A
+    uint32_t lo[3][4], hi[3][4];   // limb L of the q bytes at the lo / hi nibble columns of word w
+    float pscale;                  // qscale * 2^(e - 23)
+#else
+    float2 qp[16];
+#endif
+    float qsum;                    // sum of q * qscale over the lane's 32 columns
+};
+
+#if FLEXQ_K_IDP4A
+__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+    int r;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+#endif
+
+// q (fp16, 64 B of the lane's 32 columns at qs) -> KQuery.
+__device__ __forceinline__ void load_q(const uint8_t* qs, float qscale, KQuery& kq) {
+    const __half* qh = reinterpret_cast<const __half*>(qs);
+#if FLEXQ_K_IDP4A
+    float q[32], mx = 0.0f, sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        q[j] = __half2float(qh[j]);
+        mx = fmaxf(mx, fabsf(q[j]));
+        sum += q[j];
+    }
+    int e = 0;
+    frexpf(mx, &e);                                   // mx < 2^e (mx = 0 -> e = 0)
+    const float up = ldexpf(1.0f, 23 - e);
+    kq.pscale = qscale * ldexpf(1.0f, e - 23);
+    kq.qsum = sum * qscale;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+        for (int L = 0; L < 3; ++L) {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int ql = __float2int_rn(q[8 * w + 2 * b] * up);       // exact scaling, |.| < 2^23
+                const int qh2 = __float2int_rn(q[8 * w + 2 * b + 1] * up);
+                const uint32_t bl = uint32_t(ql >> (8 * L)) & 0xFFu;         // limb 2 keeps the sign byte
+                const uint32_t bh = uint32_t(qh2 >> (8 * L)) & 0xFFu;
+                lo |= bl << (8 * b);
+                hi |= bh << (8 * b);
+            }
+            kq.lo[L][w] = lo;
+            kq.hi[L][w] = hi;
+        }
+    }
+#else
+    float acc = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float x = __half2float(qh[8 * w + pair_col(p, 0)]) * qscale;
+            const float y = __half2float(qh[8 * w + pair_col(p, 1)]) * qscale;
+            acc += x + y;
+            const float2 sh = inv_shift(p);
+            kq.qp[4 * w + p] = make_float2(x * sh.x, y * sh.y);
+        }
+    }
+    kq.qsum = acc;
+#endif
+}
+
 // Pass 1, one warp iteration (tokens i*TPI + [0, TPI) of the stage): scores -> smem (log2 domain).
 // lc / lm: the lane's byte offsets inside a token row (codes / meta).
 template <int D, int NCH, bool FULL>
-__device__ __forceinline__ void k_iter(int i, const float2 (&qp)[16], float qsum, const uint8_t* sb, float* sc,
-                                       int t0, int tl, int n, int lc, int lm, int sg, uint32_t magic, float& mx) {
+__device__ __forceinline__ void k_iter(int i, const KQuery& kq, const uint8_t* sb, float* sc, int t0, int tl,
+                                       int n, int lc, int lm, int sg, uint32_t magic, float& mx) {
     using C = Cfg<D, NCH>;
     const int tok = i * C::TPI + tl;
     const uint4 kw = lds128(sb + C::code_off(i) + lc);
     const float2 km = __half22float2(*reinterpret_cast<const __half2*>(sb + C::meta_off(i) + lm));
+#if FLEXQ_K_IDP4A
+    const uint32_t wv[4] = {kw.x, kw.y, kw.z, kw.w};
+    uint32_t a0 = 0, a1 = 0;
+    int a2 = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        const uint32_t lo = wv[w] & 0x0F0F0F0Fu;         // codes of columns 0, 2, 4, 6 as bytes
+        const uint32_t hi = (wv[w] >> 4) & 0x0F0F0F0Fu;  // columns 1, 3, 5, 7
+        a0 = dp4a_uu(lo, kq.lo[0][w], a0);
+        a0 = dp4a_uu(hi, kq.hi[0][w], a0);
+        a1 = dp4a_uu(lo, kq.lo[1][w], a1);
+        a1 = dp4a_uu(hi, kq.hi[1][w], a1);
+        a2 = dp4a_us(lo, kq.lo[2][w], a2);
+        a2 = dp4a_us(hi, kq.hi[2][w], a2);
+    }
+    const float P = fmaf(float(a2), 65536.0f, fmaf(float(a1), 256.0f, float(a0)));
+    float s = fmaf(km.x, P * kq.pscale, km.y * kq.qsum);
+    (void)magic;
+#else
     float2 d0 = make_float2(0.0f, 0.0f), d1 = d0;
     float2 f[4];
     unpack8(kw.x, magic, f);
-    d0 = __ffma2_rn(qp[0], f[0], d0); d1 = __ffma2_rn(qp[1], f[1], d1);
-    d0 = __ffma2_rn(qp[2], f[2], d0); d1 = __ffma2_rn(qp[3], f[3], d1);
+    d0 = __ffma2_rn(kq.qp[0], f[0], d0); d1 = __ffma2_rn(kq.qp[1], f[1], d1);
+    d0 = __ffma2_rn(kq.qp[2], f[2], d0); d1 = __ffma2_rn(kq.qp[3], f[3], d1);
     unpack8(kw.y, magic, f);
-    d0 = __ffma2_rn(qp[4], f[0], d0); d1 = __ffma2_rn(qp[5], f[1], d1);
-    d0 = __ffma2_rn(qp[6], f[2], d0); d1 = __ffma2_rn(qp[7], f[3], d1);
+    d0 = __ffma2_rn(kq.qp[4], f[0], d0); d1 = __ffma2_rn(kq.qp[5], f[1], d1);
+    d0 = __ffma2_rn(kq.qp[6], f[2], d0); d1 = __ffma2_rn(kq.qp[7], f[3], d1);
     unpack8(kw.z, magic, f);
-    d0 = __ffma2_rn(qp[8], f[0], d0); d1 = __ffma2_rn(qp[9], f[1], d1);
-    d0 = __ffma2_rn(qp[10], f[2], d0); d1 = __ffma2_rn(qp[11], f[3], d1);
+    d0 = __ffma2_rn(kq.qp[8], f[0], d0); d1 = __ffma2_rn(kq.qp[9], f[1], d1);
+    d0 = __ffma2_rn(kq.qp[10], f[2], d0); d1 = __ffma2_rn(kq.qp[11], f[3], d1);
     unpack8(kw.w, magic, f);
-    d0 = __ffma2_rn(qp[12], f[0], d0); d1 = __ffma2_rn(qp[13], f[1], d1);
-    d0 = __ffma2_rn(qp[14], f[2], d0); d1 = __ffma2_rn(qp[15], f[3], d1);
+    d0 = __ffma2_rn(kq.qp[12], f[0], d0); d1 = __ffma2_rn(kq.qp[13], f[1], d1);
+    d0 = __ffma2_rn(kq.qp[14], f[2], d0); d1 = __ffma2_rn(kq.qp[15], f[3], d1);
     d0 = __fadd2_rn(d0, d1);
-    float s = fmaf(km.x, d0.x + d0.y, km.y * qsum);
+    float s = fmaf(km.x, d0.x + d0.y, km.y * kq.qsum);
+#endif
 #pragma unroll
     for (int o = 1; o < C::LPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (FULL || tok < n) {
@@ -262,25 +367,6 @@ __device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float
         vm.y = valid ? vm.y : 0.0f;
     }
     v_accum(acc, l, bsum, vw, vm, p, magic);
-}
-
-// q (fp16, 64 B of the lane's 32 columns at qs) -> qp[4w + p] = q * qscale * 2^-k
-// at the columns of pair p of word w (unpack8 order), and qsum = sum of q * qscale.
-__device__ __forceinline__ void load_q(const uint8_t* qs, float qscale, float2 (&qp)[16], float& qsum) {
-    const __half* qh = reinterpret_cast<const __half*>(qs);
-    float acc = 0.0f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const float x = __half2float(qh[8 * w + pair_col(p, 0)]) * qscale;
-            const float y = __half2float(qh[8 * w + pair_col(p, 1)]) * qscale;
-            acc += x + y;
-            const float2 sh = inv_shift(p);
-            qp[4 * w + p] = make_float2(x * sh.x, y * sh.y);
-        }
-    }
-    qsum = acc;
 }
 
 // End of a unit: remove the 16^k factors, reduce (acc, l, bsum) over the token

@@ -56,13 +56,13 @@ template <int D, int NCH, int S, int WPC, int UNR, int MAXT>
 __global__ void __launch_bounds__(WPC * 32, (16 / WPC) > 0 ? (16 / WPC) : 1)
 decode_attention_kernel(const Params P) {
     using C = Cfg<D, NCH>;
+    static_assert(S >= 2 && S <= 4, "ring depth");
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
     float* scores = reinterpret_cast<float*>(smem + WPC * S * C::STAGE) + warp * MAXT;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 4)) + warp * S;
-    Desc* desc = reinterpret_cast<Desc*>(smem + WPC * (S * (C::STAGE + 8) + MAXT * 4)) + warp * S;
 
     const int units = P.bh_total * P.nsplit;
     const uint64_t policy = evict_first_policy();
@@ -72,67 +72,62 @@ decode_attention_kernel(const Params P) {
     }
     __syncwarp();
 
-    // ---------------- producer (warp-uniform state; lane 0 issues the copies)
-    int p_unit = -1, p_bh = 0, p_first = 0, p_end = 0, p_tok = 0;
-    bool p_v = false;
+    // Unit geometry: unit u = (b, h, split); tokens [first, first + len), nst stages per pass.
+    auto geo = [&](int u, int& bh, int& first, int& len) {
+        int split = 0;
+        bh = u;
+        if (P.nsplit > 1) {
+            bh = u / P.nsplit;
+            split = u - bh * P.nsplit;
+        }
+        first = split * P.split_len;
+        len = min(P.cur_len - first, P.split_len);
+    };
+
+    // ---------------- producer (warp-uniform state; lane 0 issues the copies).
+    // Stage sequence per unit: nst K stages, then nst V stages.  Unit ids go
+    // through a 3-entry register FIFO to the consumer, which lags by <= S-1 stages.
+    int p_unit = -1, p_stage = 0, p_nst = 0;
+    const uint8_t* p_k = nullptr;   // first K chunk of the unit
+    const uint8_t* p_v = nullptr;   // first V chunk
+    const __half* p_q = nullptr;
+    int p_len = 0;
+    int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
     auto next_unit = [&]() {
         int t = 0;
         if (lane == 0) t = int(atomicAdd(P.ctrl, 1u));
         t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= units) {
-            p_unit = -1;
-            return;
+        p_unit = t < units ? t : -1;
+        p_stage = 0;
+        if (p_unit >= 0) {
+            int bh, first;
+            geo(p_unit, bh, first, p_len);
+            p_nst = (p_len + C::CH - 1) / C::CH;
+            const int64_t c0 = int64_t(bh) * P.chunks + (first >> 5);
+            p_k = P.kc + c0 * C::CHB;
+            p_v = P.vc + c0 * C::CHB;
+            p_q = P.q + int64_t(bh) * D;
         }
-        p_unit = t;
-        int split = 0;
-        p_bh = t;
-        if (P.nsplit > 1) {
-            p_bh = t / P.nsplit;
-            split = t - p_bh * P.nsplit;
-        }
-        p_tok = p_first = split * P.split_len;
-        p_end = min(P.cur_len, p_tok + P.split_len);
-        p_v = false;
+        if (fcount == 0) fq0 = p_unit; else if (fcount == 1) fq1 = p_unit; else fq2 = p_unit;
+        ++fcount;
     };
     auto issue = [&](int slot) {
+        if (p_unit < 0) {
+            if (lane == 0) mbar_expect_tx(&bars[slot], 0);   // keeps the phase sequence; nothing to load
+            return;
+        }
+        const bool vpass = p_stage >= p_nst;
+        const int si = vpass ? p_stage - p_nst : p_stage;
+        const int n = min(C::CH, p_len - si * C::CH);
         if (lane == 0) {
-            Desc d;
-            uint32_t bytes = 0;
-            if (p_unit >= 0) {
-                const bool first = !p_v && p_tok == p_first;
-                const bool last_of_pass = p_tok + C::CH >= p_end;
-                d.unit = p_unit;
-                d.bh = p_bh;
-                d.t0 = p_tok - p_first;
-                const int n = min(C::CH, p_end - p_tok);
-                d.flags = (first ? kFirst : 0) | (p_v ? kV : 0) | (!p_v && last_of_pass ? kLastK : 0) |
-                          (p_v && last_of_pass ? kLast : 0) | (n << 8);
-                bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB + (first ? 2 * D : 0);
-            } else {
-                d.unit = -1; d.bh = 0; d.t0 = 0; d.flags = 0;
-            }
-            desc[slot] = d;
-            fence_proxy_async();
-            mbar_expect_tx(&bars[slot], bytes);
-            if (p_unit >= 0) {
-                uint8_t* sb = ring + slot * C::STAGE;
-                const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
-                const uint32_t data = bytes - ((d.flags & kFirst) ? 2 * D : 0);
-                bulk_g2s(sb, (p_v ? P.vc : P.kc) + chunk * C::CHB, data, &bars[slot], policy);
-                if (d.flags & kFirst) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
-            }
+            const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
+            const bool first = p_stage == 0;
+            uint8_t* sb = ring + slot * C::STAGE;
+            mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0));
+            bulk_g2s(sb, (vpass ? p_v : p_k) + int64_t(si) * (NCH * C::CHB), bytes, &bars[slot], policy);
+            if (first) bulk_g2s(sb + C::OFF_Q, p_q, 2 * D, &bars[slot], policy);
         }
-        if (p_unit >= 0) {
-            p_tok += C::CH;
-            if (p_tok >= p_end) {
-                if (!p_v) {
-                    p_v = true;
-                    p_tok = p_first;
-                } else {
-                    next_unit();
-                }
-            }
-        }
+        if (++p_stage == 2 * p_nst) next_unit();
     };
 
     next_unit();
@@ -148,10 +143,9 @@ decode_attention_kernel(const Params P) {
 
     int slot = 0;
     uint32_t parity = 0;
-    auto next_stage = [&](Desc& d) -> const uint8_t* {   // issue ahead, wait for the current slot
+    auto acquire = [&]() -> const uint8_t* {   // issue ahead, then wait for the current slot
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
-        d = desc[slot];
         return ring + slot * C::STAGE;
     };
     auto release = [&]() {
@@ -164,36 +158,39 @@ decode_attention_kernel(const Params P) {
 
 #pragma unroll 1
     for (;;) {
-        Desc d;
-        const uint8_t* sb = next_stage(d);
-        if (d.unit < 0) break;
-        const int bh = d.bh;
-        const int unit = d.unit;
+        const int unit = fq0;              // pop the consumer's next unit
+        fq0 = fq1;
+        fq1 = fq2;
+        --fcount;
+        if (unit < 0) break;
+        int bh, first, len;
+        geo(unit, bh, first, len);
+        const int nst = (len + C::CH - 1) / C::CH;
 
         // ------------------------------------------------ pass 1: scores -> smem
         float M;
         {
-            float2 qp[16];                    // q * qscale * 2^-k, pairs in unpack8 order
-            float qsum;
-            load_q(sb + C::OFF_Q + sg * 64, P.qscale, qp, qsum);
+            const uint8_t* sb = acquire();
+            KQuery kq;                        // the lane's q for pass 1
+            load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
 #pragma unroll 1
-            for (;;) {
-                const int n = d.flags >> 8;
+            for (int st = 0;;) {
+                const int t0 = st * C::CH;
+                const int n = min(C::CH, len - t0);
                 if (n == C::CH) {
 #pragma unroll UNR
                     for (int i = 0; i < C::ITERS; ++i)
-                        k_iter<D, NCH, true>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                        k_iter<D, NCH, true>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
                 } else {
-#pragma unroll 1
+#pragma unroll UNR
                     for (int i = 0; i < C::ITERS; ++i)
                         if (i * C::TPI < n)
-                            k_iter<D, NCH, false>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                            k_iter<D, NCH, false>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
                 }
-                const bool last = d.flags & kLastK;
                 release();
-                if (last) break;
-                sb = next_stage(d);
+                if (++st == nst) break;
+                sb = acquire();
             }
 #pragma unroll
             for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -206,22 +203,21 @@ decode_attention_kernel(const Params P) {
         for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
         float l = 0.0f, bsum = 0.0f;
 #pragma unroll 1
-        for (;;) {
-            sb = next_stage(d);
-            const int n = d.flags >> 8;
+        for (int st = 0; st < nst; ++st) {
+            const uint8_t* sb = acquire();
+            const int t0 = st * C::CH;
+            const int n = min(C::CH, len - t0);
             if (n == C::CH) {
 #pragma unroll UNR
                 for (int i = 0; i < C::ITERS; ++i)
-                    v_iter<D, NCH, true>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
+                    v_iter<D, NCH, true>(i, acc, l, bsum, sb, scores, M, t0, tl, n, lc, lm, magic);
             } else {
-#pragma unroll 1
+#pragma unroll UNR
                 for (int i = 0; i < C::ITERS; ++i)
                     if (i * C::TPI < n)
-                        v_iter<D, NCH, false>(i, acc, l, bsum, sb, scores, M, d.t0, tl, n, lc, lm, magic);
+                        v_iter<D, NCH, false>(i, acc, l, bsum, sb, scores, M, t0, tl, n, lc, lm, magic);
             }
-            const bool last = d.flags & kLast;
             release();
-            if (last) break;
         }
 
         // ------------------------------------------------ end of unit: reduce over token lanes, write
@@ -273,7 +269,7 @@ decode_attention_kernel(const Params P) {
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + MAXT * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 4);
 }
 
 int sm_count() {
@@ -401,6 +397,9 @@ cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
             case FLEXQ_V(64, 2, 4, 4, 576): return launch<128, 2, 2, 4, 4, 576>(a, stream);
             case FLEXQ_V(32, 2, 4, 4, 576): return launch<128, 1, 2, 4, 4, 576>(a, stream);
             case FLEXQ_V(32, 3, 2, 4, 576): return launch<128, 1, 3, 2, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 4, 2, 1024): return launch<128, 2, 2, 4, 2, 1024>(a, stream);
+            case FLEXQ_V(64, 3, 4, 4, 576): return launch<128, 2, 3, 4, 4, 576>(a, stream);
+            case FLEXQ_V(32, 3, 4, 4, 576): return launch<128, 1, 3, 4, 4, 576>(a, stream);
             default: return launch<128, 2, 2, 4, 4, 1024>(a, stream);
         }
     }

@@ -144,9 +144,8 @@ decode_attention_topk_kernel(const TopkParams P) {
         // ------------------------------------------------ pass 1: all scores -> smem
         float M;
         {
-            float2 qp[16];
-            float qsum;
-            load_q(sb + C::OFF_Q + sg * 64, P.qscale, qp, qsum);
+            KQuery kq;
+            load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
 #pragma unroll 1
             for (;;) {
@@ -154,12 +153,12 @@ decode_attention_topk_kernel(const TopkParams P) {
                 if (n == C::CH) {
 #pragma unroll 4
                     for (int i = 0; i < C::ITERS; ++i)
-                        k_iter<D, NCH, true>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                        k_iter<D, NCH, true>(i, kq, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
                 } else {
 #pragma unroll 1
                     for (int i = 0; i < C::ITERS; ++i)
                         if (i * C::TPI < n)
-                            k_iter<D, NCH, false>(i, qp, qsum, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                            k_iter<D, NCH, false>(i, kq, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
                 }
                 const bool last = d.flags & kLastK;
                 __syncwarp();
