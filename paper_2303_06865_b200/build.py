@@ -80,4 +80,4 @@ if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
     if "--ab" in sys.argv:   # A/B libraries for tuning
         print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=1",), tag="h16unpack"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=1",), tag="kidp4a"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=0",), tag="kffma2"))

@@ -191,13 +191,13 @@ struct Params {
 };
 
 #ifndef FLEXQ_K_IDP4A
-#define FLEXQ_K_IDP4A 0
+#define FLEXQ_K_IDP4A 1
 #endif
 
 // The lane's view of q for pass 1 (FLEXQ_K_IDP4A):
-//  0 (default): qp[4w + p] = q * qscale * 2^-k at the columns of pair p of word w
+//  0: qp[4w + p] = q * qscale * 2^-k at the columns of pair p of word w
 //     (unpack8 order), qsum = sum q * qscale; the dot product runs on FFMA2.
-//  1: q as a 24-bit fixed-point integer per lane (scale 2^(23 - e), |q| < 2^e),
+//  1 (default): q as a 24-bit fixed-point integer per lane (scale 2^(23 - e), |q| < 2^e),
 //     split into three byte limbs packed to match the codes' lo / hi nibbles;
 //     the dot product runs on IDP.4A (exact in int32; q values within 2^-14 of
 //     the lane's max are represented exactly, smaller ones to 2^-23 of the max).
