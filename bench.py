@@ -342,6 +342,10 @@ def run_flexq(args):
     attn_bytes = wl.attention_bytes(B, h1, cur_last)
     peak, peak_kind = peaks()
     achieved = attn_bytes / (attn_us * 1e-6) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    if os.path.exists(tp) and w.name == "opt-175b" and B == 144:
+        traffic = json.load(open(tp))["dram_bytes_per_launch"]
 
     # ---- e2e: host buffers through the public API, H2D of the step's inputs and D2H of its outputs
     log("e2e")
@@ -456,7 +460,8 @@ def run_flexq(args):
                        "global_batch": B_total, "seq_len": s + n, "parallelism": f"dp{world} (sequences)",
                        "l2": f"working set {cache_bytes / 1e9:.1f} GB per GPU >> {l2 / 1e6:.0f} MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": "profiles/attention_traffic.json (ncu --set full, same launch shape)",
                          "kernel": "decode_attention_kernel<128>", "peak_kind": peak_kind,
                          "bytes_per_launch": attn_bytes, "us_per_launch": round(attn_us, 2),
                          "append_us_per_launch": round(app_us, 2),

@@ -40,14 +40,31 @@ struct PlainDst {
         meta_off = int64_t(g) * 4;
     }
 };
+// Unsigned division by a runtime constant d < 2^31 via multiply-high
+// (Granlund-Montgomery): q = (umulhi(x, mul) + x) >> shift for x < 2^31.
+struct FastDiv {
+    uint32_t d, mul, shift;
+    static FastDiv make(uint32_t d) {
+        FastDiv f;
+        f.d = d;
+        f.shift = 0;
+        while ((1ull << f.shift) < d) ++f.shift;
+        f.mul = uint32_t(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+        return f;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t x) const { return (__umulhi(x, mul) + x) >> shift; }
+};
+
 struct KvChunkDst {
     KvDst d;
-    int cb;   // code bytes per token (D/2)
-    __device__ __forceinline__ void operator()(uint32_t g, uint32_t gpr, int /*kv*/, int64_t& codes_off,
+    FastDiv nnew;   // divisor n_new
+    int gpr_log2;   // log2(groups per row) (head_dim / 64 = 1 or 2)
+    int cb;         // code bytes per token (D/2)
+    __device__ __forceinline__ void operator()(uint32_t g, uint32_t /*gpr*/, int /*kv*/, int64_t& codes_off,
                                                int64_t& meta_off) const {
-        const uint32_t row = g / gpr, k = g - row * gpr;
-        const uint32_t bh = row / uint32_t(d.n_new);
-        const int64_t t = d.pos + (row - bh * uint32_t(d.n_new));
+        const uint32_t row = g >> gpr_log2, k = g & ((1u << gpr_log2) - 1u);
+        const uint32_t bh = nnew.div(row);
+        const int64_t t = d.pos + (row - bh * nnew.d);
         const int64_t chunk = int64_t(bh) * d.chunks + (t >> 5);
         const int slot = int(t & (kChunk - 1));
         const int mb = cb / 8;                                            // meta bytes per token
@@ -266,7 +283,7 @@ cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int hea
     quantize_kernel<KvChunkDst><<<grid, kThreads, 0, stream>>>(
         static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<uint8_t*>(k_cache),
         static_cast<uint8_t*>(k_cache), static_cast<uint8_t*>(v_cache), static_cast<uint8_t*>(v_cache), rows,
-        head_dim, KvChunkDst{d, head_dim / 2});
+        head_dim, KvChunkDst{d, FastDiv::make(uint32_t(d.n_new)), head_dim == 128 ? 1 : 0, head_dim / 2});
     return cudaGetLastError();
 }
 

@@ -25,28 +25,35 @@ FULL_METRICS = [
 
 def launches(path):
     rows = list(csv.reader(open(path)))
-    # ncu --csv launch list: header line contains "Kernel Name" and "Metric Value"
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[hi]
-    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    tot = collections.defaultdict(float)
-    cnt = collections.Counter()
+    ik, iv, iu, im, iid = (hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit"),
+                           hdr.index("Metric Name"), hdr.index("ID"))
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    per = collections.defaultdict(dict)      # launch id -> {name, metric: value}
     for r in rows[hi + 1:]:
         if len(r) <= iv:
             continue
-        name = r[ik].split("(")[0].replace("void ", "")
-        v = float(r[iv].replace(",", ""))
-        unit = r[iu]
-        ns = v * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}.get(unit, 1)
-        tot[name] += ns
-        cnt[name] += 1
-    allns = sum(tot.values())
+        d = per[r[iid]]
+        d["name"] = r[ik].split("(")[0].replace("void ", "")
+        d[r[im]] = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+    tot = collections.defaultdict(float)
+    byt = collections.defaultdict(float)
+    cnt = collections.Counter()
+    for d in per.values():
+        t = d.get("gpu__time_duration.sum", 0.0)
+        tot[d["name"]] += t
+        byt[d["name"]] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        cnt[d["name"]] += 1
+    allus = sum(tot.values())
     print(f"# ncu launch list: {path}\n")
-    print("Per-launch device time, `--metrics gpu__time_duration.sum --clock-control none` (cold-cache, "
-          "serialised: compare shares, not absolutes).\n")
-    print("| kernel | launches | total us | mean us | share |\n|---|---|---|---|---|")
+    print("Per-launch device time, `--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+          "--clock-control none` (cold-cache, serialised: compare shares, not absolutes).\n")
+    print("| kernel | launches | total us | mean us | share of time | DRAM bytes / launch |\n|---|---|---|---|---|---|")
     for k in sorted(tot, key=lambda x: -tot[x]):
-        print(f"| `{k}` | {cnt[k]} | {tot[k] / 1e3:.1f} | {tot[k] / cnt[k] / 1e3:.2f} | {tot[k] / allns:.3f} |")
+        print(f"| `{k}` | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.2f} | {tot[k] / allus:.3f} | "
+              f"{byt[k] / cnt[k] / 1e6:.2f} MB |")
 
 
 def full(path):

@@ -129,6 +129,20 @@ ATTN_CASES = [
 ]
 
 
+def test_attention_q_wide_dynamic_range(orc, cuda):
+    """q with one channel per head at 2^12 x the rest (the pass-1 fixed-point q of
+    each lane is scaled to its own max, so the small channels are represented to
+    2^-24 of that max): still within reading Q's tolerance."""
+    B, H, D, s, n = 2, 4, 128, 200, 4
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, 2, seed=44)
+    q = q.clone()
+    q[..., 5] = torch.where(q[..., 5] >= 0, 1.0, -1.0).to(torch.float16) * 4096   # |q| ~ 2^12 vs ~1
+    q = (q.float() * 0.001).to(torch.float16)                                      # keep the softmax O(1)
+    out = fq.flexq_decode_attention(q.to(cuda), cache, cur)
+    ref = orc.attention_f64(q.numpy(), okc, ovc, cur)
+    assert_attn_close(out.cpu().numpy(), ref, "wide-range q")
+
+
 @pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
 def test_attention_parity(orc, cuda, case):
     name, B, H, D, s, n, steps, outl, qf = case
