@@ -342,6 +342,33 @@ def run_flexq(args):
     attn_bytes = wl.attention_bytes(B, h1, cur_last)
     peak, peak_kind = peaks()
     achieved = attn_bytes / (attn_us * 1e-6) / 1e9
+
+    # ---- NEXT-1: Top-K sparse attention (keep 10%) at the same shape
+    topk = None
+    if cur_last <= 1152:
+        keep = fq.topk_keep(cur_last)
+        gt = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gt, stream=stream):
+            for j in range(L):
+                fq.flexq_decode_attention_topk(qs[j], caches[j], cur_last, keep, out=outs[j], workspace=ws,
+                                               stream=stream)
+        gt.replay()
+        torch.cuda.synchronize()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            t0e.record(stream)
+            for _ in range(reps):
+                gt.replay()
+            t1e.record(stream)
+        torch.cuda.synchronize()
+        tk_us = t0e.elapsed_time(t1e) * 1e3 / (reps * L)
+        kv_row = h1 // 2 + h1 // 64 * 4                      # one token's K (or V) bytes over all heads
+        tk_bytes = B * (cur_last * kv_row + keep * kv_row + 2 * h1 * 2)
+        topk = {"keep": keep, "cur_len": cur_last, "us_per_launch": round(tk_us, 2),
+                "algorithmic_bytes_per_launch": tk_bytes, "GBps": round(tk_bytes / (tk_us * 1e-6) / 1e9, 1),
+                "speedup_vs_dense": round(attn_us / tk_us, 3),
+                "note": "bytes = K for all tokens + V for the kept 10% (P:856) + q + out; the V gather "
+                        "reads each kept token's 4-token quad row"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tp) and w.name == "opt-175b" and B == 144:
@@ -471,6 +498,7 @@ def run_flexq(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "weight_sweep": sweep,
+            "topk_sparse": topk,
         }
         print(json.dumps(line), flush=True)
     if pg:

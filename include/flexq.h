@@ -74,15 +74,20 @@ flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t
                               int bits, int group_size, void *out_f16, void *stream);
 
 /* KV cache layout for one layer: a K cache buffer and a V cache buffer of
- * identical layout.  Capacity T_cap = prompt_len + gen_len tokens,
+ * identical size.  Capacity T_cap = prompt_len + gen_len tokens,
  * stored in chunks of 32 tokens per (batch, head); T_stride = T_cap rounded
  * up to a multiple of 32.  With D = head_dim, CB = D/2 code bytes and
  * MB = D/16 metadata bytes per token, one chunk is 18*D bytes:
  *     [codes 32 x CB][meta 32 x MB]
  * and each buffer is u8 [batch][heads][T_stride/32][18*D].  Token t of head
- * (b, h) lives in chunk (b*heads + h)*T_stride/32 + t/32, slot t%32: codes at
- * slot*CB (element 2k in the low nibble of byte k), meta at
- * 32*CB + slot*MB as D/64 half2 {scale, min} (groups of 64 along D).
+ * (b, h) lives in chunk (b*heads + h)*T_stride/32 + t/32, slot s = t%32.
+ * Meta (both caches): 32*CB + s*MB, D/64 half2 {scale, min} (groups of 64
+ * along D).  Codes: two codes per byte, column 2i in the low nibble
+ * (S:520), and
+ *   K: token-major -- byte i of the token's row at s*CB + i;
+ *   V: quad-interleaved -- byte k of the 32-bit word at ((s/4)*CB + i)*4 is
+ *      token 4*(s/4) + k's byte i (so one word holds 4 tokens of a column
+ *      pair, the shape the PV integer dot product consumes).
  * The chunks of one head are contiguous, so the attention kernel streams any
  * run of them with one 1-D TMA bulk copy.  Tokens [T_cap, T_stride) are
  * padding the library never writes.

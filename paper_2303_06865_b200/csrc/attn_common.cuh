@@ -25,6 +25,7 @@ struct Cfg {
     static constexpr int OFF_M = kChunk * CB;          // meta inside a chunk
     static constexpr int OFF_Q = NCH * CHB;
     static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
+    static constexpr int CPL_WORDS = D / 64;           // V pass: column-pair words per lane per quad
     static_assert(STAGE % 16 == 0 && CHB % 16 == 0, "stage alignment");
     static_assert(kChunk % TPI == 0, "an iteration stays inside one chunk");
     // byte offsets of iteration i's codes / meta rows (token slot 0 of the iteration)
@@ -211,7 +212,6 @@ struct KQuery {
     float qsum;                    // sum of q * qscale over the lane's 32 columns
 };
 
-#if FLEXQ_K_IDP4A
 __device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -222,7 +222,6 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
     return r;
 }
-#endif
 
 // q (fp16, 64 B of the lane's 32 columns at qs) -> KQuery.
 __device__ __forceinline__ void load_q(const uint8_t* qs, float qscale, KQuery& kq) {
@@ -367,6 +366,140 @@ __device__ __forceinline__ void v_iter(int i, float2 (&acc)[16], float& l, float
         vm.y = valid ? vm.y : 0.0f;
     }
     v_accum(acc, l, bsum, vw, vm, p, magic);
+}
+
+// ---------------------------------------------------------------- pass 2 (dense): V
+// V chunk codes are quad-interleaved (include/flexq.h): word (quad qd, column pair pj)
+// holds, in byte k, token 4qd+k's codes of columns 2pj (low nibble) and 2pj+1 (high).
+// So w & 0x0F0F0F0F is column 2pj of 4 tokens as bytes and (w >> 4) & 0x0F0F0F0F
+// column 2pj+1: IDP.4A against the 4 tokens' weights needs no transposition.
+// Lane l owns columns [CPL l, CPL (l+1)) (CPL = D/32; one quantization group).
+// Per stage the weights a_t = p_t scale_tg of each group are turned into 24-bit
+// fixed point against the stage's max (scale 2^(23-e)), split into 3 byte limbs
+// (smem table [group][quad][limb]); int32 limb sums are flushed to fp32 per stage.
+template <int D, int NCH>
+constexpr int kLimbWords = (D / 64) * (NCH * kChunk / 4) * 4;   // [group][quad][4 words]
+
+template <int D>
+struct VAcc {
+    static constexpr int CPL = D / 32;   // columns per lane
+    float acc[CPL];                      // sum_t a_t c_tj, fp32
+    float l, bsum[D / 64];               // the lane's tokens: sum p, sum p min_g
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+        l = 0.0f;
+#pragma unroll
+        for (int g = 0; g < D / 64; ++g) bsum[g] = 0.0f;
+    }
+    // warp-reduce l and the lane's group bias; v[c] = acc + bias (unnormalised); returns col0
+    __device__ __forceinline__ int finish(int lane, float (&v)[32], float& lsum) {
+        float b[D / 64];
+#pragma unroll
+        for (int g = 0; g < D / 64; ++g) b[g] = bsum[g];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+            for (int g = 0; g < D / 64; ++g) b[g] += __shfl_xor_sync(0xffffffffu, b[g], o);
+        }
+        lsum = l;
+        const int col0 = lane * CPL;
+        const float bias = (D / 64 == 1 || col0 < 64) ? b[0] : b[D / 64 - 1];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) v[c] = acc[c] + bias;
+        return col0;
+    }
+};
+
+template <int D, int NCH>
+__device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const float* sc, float M, int n, int lane,
+                                        uint32_t* limbs) {
+    using C = Cfg<D, NCH>;
+    constexpr int G = D / 64;           // groups per token
+    constexpr int Q = C::CH / 4;        // quads per stage
+    constexpr int TPL = C::CH / 32;     // tokens per lane in the weight pre-pass
+    // ---- weights: lane handles tokens lane + 32 i of the stage
+    float a[TPL][G];
+    float amax[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) amax[g] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) {
+        const int t = lane + 32 * i;
+        const bool valid = t < n;
+        const float p = valid ? ex2(sc[t] - M) : 0.0f;
+        va.l += p;
+        const uint8_t* mrow = sb + (t / kChunk) * C::CHB + C::OFF_M + (t % kChunk) * C::MB;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float2 sm = __half22float2(*reinterpret_cast<const __half2*>(mrow + 4 * g));
+            sm.x = valid ? sm.x : 0.0f;
+            sm.y = valid ? sm.y : 0.0f;
+            a[i][g] = p * sm.x;
+            va.bsum[g] = fmaf(p, sm.y, va.bsum[g]);
+            amax[g] = fmaxf(amax[g], a[i][g]);
+        }
+    }
+    float inv[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) amax[g] = fmaxf(amax[g], __shfl_xor_sync(0xffffffffu, amax[g], o));
+        int e = 0;
+        frexpf(amax[g], &e);                      // amax < 2^e (0 -> e = 0)
+        const float up = ldexpf(1.0f, 23 - e);
+        inv[g] = ldexpf(1.0f, e - 23);
+        uint8_t* tb = reinterpret_cast<uint8_t*>(limbs + g * Q * 4);
+#pragma unroll
+        for (int i = 0; i < TPL; ++i) {
+            const int t = lane + 32 * i;
+            const uint32_t ai = uint32_t(__float2int_rn(a[i][g] * up));     // < 2^23, >= 0
+            uint8_t* q = tb + (t >> 2) * 16 + (t & 3);                        // [quad][limb word][token byte]
+            q[0] = uint8_t(ai);
+            q[4] = uint8_t(ai >> 8);
+            q[8] = uint8_t(ai >> 16);
+        }
+    }
+    __syncwarp();
+    // ---- IDP.4A over quads: lane's CPL columns = CPL/2 column-pair words per quad
+    constexpr int W = C::CPL_WORDS;
+    const int g = (lane * (D / 32)) / 64;
+    uint32_t s0[2 * W], s1[2 * W], s2[2 * W];
+#pragma unroll
+    for (int c = 0; c < 2 * W; ++c) { s0[c] = 0u; s1[c] = 0u; s2[c] = 0u; }
+    const uint32_t* lt = limbs + g * Q * 4;
+#pragma unroll 4
+    for (int qd = 0; qd < Q; ++qd) {
+        const uint4 lm = *reinterpret_cast<const uint4*>(lt + qd * 4);       // limbs 0..2 (+ pad)
+        const uint8_t* crow = sb + (qd / 8) * C::CHB + ((qd % 8) * C::CB + lane * W) * 4;
+        uint32_t wv[W];
+        if constexpr (W == 2) {
+            const uint2 x = *reinterpret_cast<const uint2*>(crow);
+            wv[0] = x.x;
+            wv[W - 1] = x.y;
+        } else {
+            wv[0] = *reinterpret_cast<const uint32_t*>(crow);
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t lo = wv[w] & 0x0F0F0F0Fu;
+            const uint32_t hi = (wv[w] >> 4) & 0x0F0F0F0Fu;
+            s0[2 * w] = dp4a_uu(lo, lm.x, s0[2 * w]);
+            s1[2 * w] = dp4a_uu(lo, lm.y, s1[2 * w]);
+            s2[2 * w] = dp4a_uu(lo, lm.z, s2[2 * w]);
+            s0[2 * w + 1] = dp4a_uu(hi, lm.x, s0[2 * w + 1]);
+            s1[2 * w + 1] = dp4a_uu(hi, lm.y, s1[2 * w + 1]);
+            s2[2 * w + 1] = dp4a_uu(hi, lm.z, s2[2 * w + 1]);
+        }
+    }
+    // ---- flush: acc += (s2 2^16 + s1 2^8 + s0) * 2^(e - 23)
+#pragma unroll
+    for (int c = 0; c < 2 * W; ++c) {
+        const float f = fmaf(float(s2[c]), 65536.0f, fmaf(float(s1[c]), 256.0f, float(s0[c])));
+        va.acc[c] = fmaf(f, (G == 1 || g == 0) ? inv[0] : inv[G - 1], va.acc[c]);
+    }
+    __syncwarp();   // limb table reuse by the next stage
 }
 
 // End of a unit: remove the 16^k factors, reduce (acc, l, bsum) over the token

@@ -62,7 +62,9 @@ decode_attention_kernel(const Params P) {
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
     float* scores = reinterpret_cast<float*>(smem + WPC * S * C::STAGE) + warp * MAXT;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 4)) + warp * S;
+    uint32_t* limbs = reinterpret_cast<uint32_t*>(smem + WPC * (S * C::STAGE + MAXT * 4)) + warp * (kLimbWords<D, NCH>);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 4 + kLimbWords<D, NCH> * 4)) +
+                     warp * S;
 
     const int units = P.bh_total * P.nsplit;
     const uint64_t policy = evict_first_policy();
@@ -198,31 +200,22 @@ decode_attention_kernel(const Params P) {
         }
 
         // ------------------------------------------------ pass 2: P.V with p = 2^(s - M)
-        float2 acc[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
-        float l = 0.0f, bsum = 0.0f;
+        // V codes are quad-interleaved (include/flexq.h): lanes own columns, IDP.4A over
+        // 4 tokens at a time against per-stage fixed-point weights a_t = p_t scale_tg.
+        VAcc<D> va;
+        va.init();
 #pragma unroll 1
         for (int st = 0; st < nst; ++st) {
             const uint8_t* sb = acquire();
             const int t0 = st * C::CH;
             const int n = min(C::CH, len - t0);
-            if (n == C::CH) {
-#pragma unroll UNR
-                for (int i = 0; i < C::ITERS; ++i)
-                    v_iter<D, NCH, true>(i, acc, l, bsum, sb, scores, M, t0, tl, n, lc, lm, magic);
-            } else {
-#pragma unroll UNR
-                for (int i = 0; i < C::ITERS; ++i)
-                    if (i * C::TPI < n)
-                        v_iter<D, NCH, false>(i, acc, l, bsum, sb, scores, M, t0, tl, n, lc, lm, magic);
-            }
+            v_stage<D, NCH>(va, sb, scores + t0, M, n, lane, limbs);
             release();
         }
 
-        // ------------------------------------------------ end of unit: reduce over token lanes, write
-        float v[32];
-        const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
+        // ------------------------------------------------ end of unit: reduce l / bias, write
+        float v[32], l;
+        const int col0 = va.finish(lane, v, l);
         if (P.nsplit == 1) {
             write_out<D>(P.out + int64_t(bh) * D + col0, v, l);
         } else {
@@ -269,7 +262,7 @@ decode_attention_kernel(const Params P) {
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 4 + kLimbWords<D, NCH> * 4);
 }
 
 int sm_count() {
@@ -391,21 +384,21 @@ cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     if (a.head_dim == 128) {
         switch (v) {
             case FLEXQ_V(64, 2, 4, 4, 1024): return launch<128, 2, 2, 4, 4, 1024>(a, stream);
-            case FLEXQ_V(64, 2, 4, 8, 1024): return launch<128, 2, 2, 4, 8, 1024>(a, stream);
-            case FLEXQ_V(64, 2, 2, 4, 576): return launch<128, 2, 2, 2, 4, 576>(a, stream);
             case FLEXQ_V(64, 2, 1, 4, 576): return launch<128, 2, 2, 1, 4, 576>(a, stream);
-            case FLEXQ_V(64, 2, 4, 4, 576): return launch<128, 2, 2, 4, 4, 576>(a, stream);
-            case FLEXQ_V(32, 2, 4, 4, 576): return launch<128, 1, 2, 4, 4, 576>(a, stream);
-            case FLEXQ_V(32, 3, 2, 4, 576): return launch<128, 1, 3, 2, 4, 576>(a, stream);
-            case FLEXQ_V(64, 2, 4, 2, 1024): return launch<128, 2, 2, 4, 2, 1024>(a, stream);
-            case FLEXQ_V(64, 3, 4, 4, 576): return launch<128, 2, 3, 4, 4, 576>(a, stream);
-            case FLEXQ_V(32, 3, 4, 4, 576): return launch<128, 1, 3, 4, 4, 576>(a, stream);
-            default: return launch<128, 2, 2, 4, 4, 1024>(a, stream);
+            case FLEXQ_V(64, 2, 3, 4, 576): return launch<128, 2, 2, 3, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 2, 8, 576): return launch<128, 2, 2, 2, 8, 576>(a, stream);
+            case FLEXQ_V(64, 2, 2, 4, 1024): return launch<128, 2, 2, 2, 4, 1024>(a, stream);
+            case FLEXQ_V(32, 3, 3, 4, 576): return launch<128, 1, 3, 3, 4, 576>(a, stream);
+            case FLEXQ_V(32, 3, 1, 4, 576): return launch<128, 1, 3, 1, 4, 576>(a, stream);
+            case FLEXQ_V(32, 2, 3, 4, 576): return launch<128, 1, 2, 3, 4, 576>(a, stream);
+            case FLEXQ_V(32, 4, 2, 4, 576): return launch<128, 1, 4, 2, 4, 576>(a, stream);
+            default: return launch<128, 2, 2, 2, 4, 576>(a, stream);
         }
     }
     switch (v) {
-        case FLEXQ_V(64, 2, 2, 4, 576): return launch<64, 2, 2, 2, 4, 576>(a, stream);
-        default: return launch<64, 2, 2, 4, 4, 1024>(a, stream);
+        case FLEXQ_V(64, 2, 4, 4, 1024): return launch<64, 2, 2, 4, 4, 1024>(a, stream);
+        case FLEXQ_V(32, 3, 3, 4, 576): return launch<64, 1, 3, 3, 4, 576>(a, stream);
+        default: return launch<64, 2, 2, 2, 4, 576>(a, stream);
     }
 }
 

@@ -16,9 +16,10 @@
 // radix select (8-bit digits) on order-preserving 32-bit keys of the fp32
 // scores, a warp-local smem histogram per round; ties at the threshold key go
 // to the lowest token indices (ballot prefix counts), so the kept set is the
-// definition's.  Pass 2 gathers the kept V rows straight from HBM (16 B per
-// lane, 128-bit loads, software-prefetched one group ahead) into the same
-// register accumulators as the dense P.V.
+// definition's.  Pass 2 gathers the kept V rows straight from HBM (the token's
+// quad row of the quad-interleaved V chunk, 64 B per lane in 128-bit loads,
+// its byte extracted with PRMT, software-prefetched one group ahead) into
+// fp32 register accumulators.
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -252,38 +253,55 @@ decode_attention_topk_kernel(const TopkParams P) {
         for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
         float l = 0.0f, bsum = 0.0f;
         const uint8_t* vbase = P.vc + int64_t(bh) * P.chunks * C::CHB;
+        // V codes are quad-interleaved (include/flexq.h): token t's 16 B segment sg
+        // (column pairs 16 sg .. 16 sg + 15) is byte t % 4 of 16 consecutive words
+        // of its quad row; load the 64 B and gather that byte with PRMT.
+        auto load_row = [&](int t, uint4 (&raw)[4], uint32_t& meta) {
+            const uint8_t* cb = vbase + (t >> 5) * C::CHB;
+            const uint8_t* q = cb + ((((t & 31) >> 2) * C::CB) + 16 * sg) * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) raw[i] = ldg_nc128(q + 16 * i);
+            meta = ldg_nc32(cb + C::OFF_M + (t & 31) * C::MB + (sg >> 1) * 4);
+        };
+        auto row_bytes = [&](int t, const uint4 (&raw)[4]) -> uint4 {
+            const uint32_t k = uint32_t(t & 3);
+            const uint32_t sel = k | ((k + 4) << 4);
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t a = __byte_perm(raw[j].x, raw[j].y, sel);   // bytes k of words 4j, 4j+1
+                const uint32_t b = __byte_perm(raw[j].z, raw[j].w, sel);   // words 4j+2, 4j+3
+                o[j] = __byte_perm(a, b, 0x5410);
+            }
+            return make_uint4(o[0], o[1], o[2], o[3]);
+        };
         auto row_of = [&](int j, int& t) -> bool {
             t = j < keep ? int(kept[j]) : 0;
             return j < keep;
         };
         int t_cur;
         bool v_cur = row_of(tl, t_cur);
-        const uint8_t* rc = vbase + (t_cur >> 5) * C::CHB + (t_cur & 31) * C::CB + sg * 16;
-        uint4 w_cur = v_cur ? ldg_nc128(rc) : make_uint4(0, 0, 0, 0);
-        uint32_t m_cur = v_cur ? ldg_nc32(vbase + (t_cur >> 5) * C::CHB + C::OFF_M + (t_cur & 31) * C::MB +
-                                          (sg >> 1) * 4)
-                               : 0u;
+        uint4 r_cur[4] = {};
+        uint32_t m_cur = 0u;
+        if (v_cur) load_row(t_cur, r_cur, m_cur);
 #pragma unroll 1
         for (int g = 0; g * C::TPI < keep; ++g) {
             int t_nxt;
             const bool v_nxt = row_of((g + 1) * C::TPI + tl, t_nxt);
-            uint4 w_nxt = make_uint4(0, 0, 0, 0);
+            uint4 r_nxt[4] = {};
             uint32_t m_nxt = 0u;
-            if (v_nxt) {   // prefetch the next group's rows
-                const uint8_t* cb = vbase + (t_nxt >> 5) * C::CHB;
-                w_nxt = ldg_nc128(cb + (t_nxt & 31) * C::CB + sg * 16);
-                m_nxt = ldg_nc32(cb + C::OFF_M + (t_nxt & 31) * C::MB + (sg >> 1) * 4);
-            }
+            if (v_nxt) load_row(t_nxt, r_nxt, m_nxt);   // prefetch the next group's rows
             float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&m_cur));
             float p = ex2(scores[t_cur] - M);
             if (!v_cur) {
                 p = 0.0f;
                 vm = make_float2(0.0f, 0.0f);
             }
-            v_accum(acc, l, bsum, w_cur, vm, p, magic);
+            v_accum(acc, l, bsum, row_bytes(t_cur, r_cur), vm, p, magic);
             t_cur = t_nxt;
             v_cur = v_nxt;
-            w_cur = w_nxt;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) r_cur[i] = r_nxt[i];
             m_cur = m_nxt;
         }
         float v[32];

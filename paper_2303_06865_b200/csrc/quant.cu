@@ -39,6 +39,11 @@ struct PlainDst {
         codes_off = int64_t(g) * (kGroup / 2);
         meta_off = int64_t(g) * 4;
     }
+    // the lane's 16 codes (8 bytes, element 2i in the low nibble of byte i)
+    __device__ __forceinline__ void store_codes(uint8_t* base, int64_t co, int part, int /*kv*/, uint32_t lo,
+                                                uint32_t hi) const {
+        *reinterpret_cast<uint2*>(base + co + part * 8) = make_uint2(lo, hi);
+    }
 };
 // Unsigned division by a runtime constant d < 2^31 via multiply-high
 // (Granlund-Montgomery): q = (umulhi(x, mul) + x) >> shift for x < 2^31.
@@ -60,7 +65,10 @@ struct KvChunkDst {
     FastDiv nnew;   // divisor n_new
     int gpr_log2;   // log2(groups per row) (head_dim / 64 = 1 or 2)
     int cb;         // code bytes per token (D/2)
-    __device__ __forceinline__ void operator()(uint32_t g, uint32_t /*gpr*/, int /*kv*/, int64_t& codes_off,
+    // codes_off: K -> byte offset of the token's codes of group k (token-major rows);
+    //            V -> byte offset of the first column-pair word of group k in the token's
+    //               quad, plus the token's byte lane (t % 4)   (include/flexq.h layout).
+    __device__ __forceinline__ void operator()(uint32_t g, uint32_t /*gpr*/, int kv, int64_t& codes_off,
                                                int64_t& meta_off) const {
         const uint32_t row = g >> gpr_log2, k = g & ((1u << gpr_log2) - 1u);
         const uint32_t bh = nnew.div(row);
@@ -69,8 +77,23 @@ struct KvChunkDst {
         const int slot = int(t & (kChunk - 1));
         const int mb = cb / 8;                                            // meta bytes per token
         const int64_t base = chunk * (kChunk * (cb + mb));                // kv_chunk_bytes(2 cb)
-        codes_off = base + slot * cb + k * (kGroup / 2);
+        if (kv == 0)
+            codes_off = base + slot * cb + k * (kGroup / 2);
+        else
+            codes_off = base + ((slot >> 2) * cb + k * (kGroup / 2)) * 4 + (slot & 3);
         meta_off = base + kChunk * cb + slot * mb + k * 4;
+    }
+    __device__ __forceinline__ void store_codes(uint8_t* base, int64_t co, int part, int kv, uint32_t lo,
+                                                uint32_t hi) const {
+        if (kv == 0) {
+            *reinterpret_cast<uint2*>(base + co + part * 8) = make_uint2(lo, hi);
+        } else {   // V: byte i (column pair part*8 + i of the group) -> word (quad, pair), byte t % 4
+            uint8_t* p = base + co + part * 32;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[4 * i] = uint8_t(lo >> (8 * i));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[16 + 4 * i] = uint8_t(hi >> (8 * i));
+        }
     }
 };
 
@@ -176,7 +199,7 @@ quantize_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, ui
         }
         int64_t co, mo;
         dst(g, gpr, kv, co, mo);
-        *reinterpret_cast<uint2*>(codes_base + co + part * 8) = make_uint2(wlo, whi);
+        dst.store_codes(codes_base, co, part, kv, wlo, whi);
         if (part == 0) *reinterpret_cast<__half2*>(meta_base + mo) = __halves2half2(scale16, __float2half_rn(mn));
     }
 }

@@ -122,7 +122,8 @@ def token_stride(t_cap: int) -> int:
 
 class KVCache:
     """One layer's compressed KV cache in the chunked layout of include/flexq.h:
-    `k` and `v` are u8 [B][H][T_stride/32][18*D], chunk = [codes 32 x D/2][meta 32 x D/16].
+    `k` and `v` are u8 [B][H][T_stride/32][18*D], chunk = [codes 32 x D/2][meta 32 x D/16]
+    (K codes token-major, V codes quad-interleaved).
     The *_codes() / *_meta() accessors are layout views (copies) for tests and
     inspection, over tokens [0, T_stride)."""
 
@@ -156,7 +157,11 @@ class KVCache:
         return self._codes(self.k)
 
     def v_codes(self):
-        return self._codes(self.v)
+        """V codes as token-major rows.  In memory each chunk's V codes are
+        quad-interleaved: word (quad, column pair) holds token 4 quad + k in byte k."""
+        B, H, NC, cb = self.batch, self.heads, self.chunks, self.head_dim // 2
+        x = self.v[..., :CHUNK * cb].reshape(B, H, NC, CHUNK // 4, cb, 4)
+        return x.permute(0, 1, 2, 3, 5, 4).reshape(B, H, NC * CHUNK, cb)
 
     def k_meta(self):
         return self._meta(self.k)
