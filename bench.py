@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--same-device", action="store_true",
+                    help="all ranks on cuda:0 with gloo (functional test of the N > 1 path on one GPU)")
     return ap.parse_args()
 
 
@@ -115,10 +117,12 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:          # functional test of the multi-rank path on one GPU (gloo)
+        local = 0
     pg = None
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "flexq" else "gloo"
+        backend = "nccl" if args.impl == "flexq" and not args.same_device else "gloo"
         if args.impl == "flexq":
             torch.cuda.set_device(local)
         dist.init_process_group(backend)

@@ -392,13 +392,16 @@ cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
             case FLEXQ_V(32, 3, 1, 4, 576): return launch<128, 1, 3, 1, 4, 576>(a, stream);
             case FLEXQ_V(32, 2, 3, 4, 576): return launch<128, 1, 2, 3, 4, 576>(a, stream);
             case FLEXQ_V(32, 4, 2, 4, 576): return launch<128, 1, 4, 2, 4, 576>(a, stream);
-            default: return launch<128, 2, 2, 2, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 2, 4, 576): return launch<128, 2, 2, 2, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 3, 4, 1088): return launch<128, 2, 2, 3, 4, 1088>(a, stream);
+            default: return launch<128, 2, 2, 3, 4, 576>(a, stream);
         }
     }
     switch (v) {
         case FLEXQ_V(64, 2, 4, 4, 1024): return launch<64, 2, 2, 4, 4, 1024>(a, stream);
         case FLEXQ_V(32, 3, 3, 4, 576): return launch<64, 1, 3, 3, 4, 576>(a, stream);
-        default: return launch<64, 2, 2, 2, 4, 576>(a, stream);
+        case FLEXQ_V(64, 2, 2, 4, 576): return launch<64, 2, 2, 2, 4, 576>(a, stream);
+        default: return launch<64, 2, 2, 3, 4, 576>(a, stream);
     }
 }
 
