@@ -46,7 +46,8 @@ namespace flexq {
 namespace {
 
 constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
-constexpr int kMinSplitTokens = 64;
+constexpr int kMinSplitTokens = 128;  // smallest context split (two 64-token stages)
+constexpr int kUnitsPerWarp = 3;       // split (b, h) units until each resident warp gets ~3
 constexpr int kMinUnitTokens = 512;    // smallest per-warp score buffer of any variant (sizes the workspace)
 
 // UNR: unroll factor of the full-stage loops (code size vs. scheduling freedom:
@@ -316,12 +317,15 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
     // context split: only when (b, h) units cannot fill the resident warps
-    // context split: forced when a unit would exceed the score buffer, else only
-    // when (b, h) units cannot fill the resident warps
+    // context split: forced when a unit would exceed the score buffer; otherwise
+    // only when there are fewer than kUnitsPerWarp (b, h) units per resident warp
+    // (persistent warps pull units dynamically, so a few units each balance the
+    // tail), keeping >= kMinSplitTokens tokens per split.
     const int min_split = (a.cur_len + MAXT - 1) / MAXT;
     int nsplit = min_split;
-    if (int64_t(bh) * nsplit < warps_resident) {
-        nsplit = (warps_resident + bh - 1) / bh;
+    const int64_t target = int64_t(kUnitsPerWarp) * warps_resident;
+    if (int64_t(bh) * nsplit < target) {
+        nsplit = int((target + bh - 1) / bh);
         const int max_by_len = (a.cur_len + kMinSplitTokens - 1) / kMinSplitTokens;
         nsplit = min(nsplit, max_by_len);
         nsplit = int(std::min<int64_t>(nsplit, split_slots(bh, a.t_cap) / bh));
