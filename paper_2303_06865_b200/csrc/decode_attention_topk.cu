@@ -57,7 +57,7 @@ __device__ __forceinline__ uint32_t ldg_nc32(const void* p) {
     return r;
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int MAXT>
 __global__ void __launch_bounds__(WPC * 32)
 decode_attention_topk_kernel(const TopkParams P) {
     using C = Cfg<D, NCH>;
@@ -65,13 +65,11 @@ decode_attention_topk_kernel(const TopkParams P) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
-    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (kTopkMaxTokens * 6 + 256 * 4);
+    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (MAXT * 6 + 256 * 4);
     float* scores = reinterpret_cast<float*>(wsm);
-    uint16_t* kept = reinterpret_cast<uint16_t*>(wsm + kTopkMaxTokens * 4);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + kTopkMaxTokens * 6);
-    uint8_t* tail = smem + WPC * (S * C::STAGE + kTopkMaxTokens * 6 + 256 * 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tail) + warp * S;
-    Desc* desc = reinterpret_cast<Desc*>(tail + WPC * S * 8) + warp * S;
+    uint16_t* kept = reinterpret_cast<uint16_t*>(wsm + MAXT * 4);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + MAXT * 6);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 6 + 256 * 4)) + warp * S;
 
     const uint64_t policy = evict_first_policy();
     if (lane == 0) {
@@ -80,43 +78,36 @@ decode_attention_topk_kernel(const TopkParams P) {
     }
     __syncwarp();
 
-    // ---------------- producer: K stages of whole (b, h) units
-    int p_bh = -1, p_tok = 0;
+    // ---------------- producer: the K stages of whole (b, h) units (no split)
+    const int nst = (P.cur_len + C::CH - 1) / C::CH;
+    int p_bh = -1, p_stage = 0;
+    const uint8_t* p_k = nullptr;
+    int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
     auto next_unit = [&]() {
         int t = 0;
         if (lane == 0) t = int(atomicAdd(P.ctrl, 1u));
         t = __shfl_sync(0xffffffffu, t, 0);
         p_bh = t < P.bh_total ? t : -1;
-        p_tok = 0;
+        p_stage = 0;
+        if (p_bh >= 0) p_k = P.kc + int64_t(p_bh) * P.chunks * C::CHB;
+        if (fcount == 0) fq0 = p_bh; else if (fcount == 1) fq1 = p_bh; else fq2 = p_bh;
+        ++fcount;
     };
     auto issue = [&](int slot) {
+        if (p_bh < 0) {
+            if (lane == 0) mbar_expect_tx(&bars[slot], 0);
+            return;
+        }
         if (lane == 0) {
-            Desc d;
-            uint32_t bytes = 0;
-            if (p_bh >= 0) {
-                const int n = min(C::CH, P.cur_len - p_tok);
-                d.unit = p_bh;
-                d.bh = p_bh;
-                d.t0 = p_tok;
-                d.flags = (p_tok == 0 ? kFirst : 0) | (p_tok + C::CH >= P.cur_len ? kLastK : 0) | (n << 8);
-                bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
-            } else {
-                d.unit = -1; d.bh = 0; d.t0 = 0; d.flags = 0;
-            }
-            desc[slot] = d;
-            fence_proxy_async();
-            mbar_expect_tx(&bars[slot], bytes + ((d.flags & kFirst) ? 2 * D : 0));
-            if (p_bh >= 0) {
-                uint8_t* sb = ring + slot * C::STAGE;
-                const int64_t chunk = int64_t(p_bh) * P.chunks + (p_tok >> 5);
-                bulk_g2s(sb, P.kc + chunk * C::CHB, bytes, &bars[slot], policy);
-                if (d.flags & kFirst) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
-            }
+            const int n = min(C::CH, P.cur_len - p_stage * C::CH);
+            const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
+            const bool first = p_stage == 0;
+            uint8_t* sb = ring + slot * C::STAGE;
+            mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0));
+            bulk_g2s(sb, p_k + int64_t(p_stage) * (NCH * C::CHB), bytes, &bars[slot], policy);
+            if (first) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
         }
-        if (p_bh >= 0) {
-            p_tok += C::CH;
-            if (p_tok >= P.cur_len) next_unit();
-        }
+        if (++p_stage == nst) next_unit();
     };
     next_unit();
 #pragma unroll 1
@@ -133,45 +124,51 @@ decode_attention_topk_kernel(const TopkParams P) {
 
     int slot = 0;
     uint32_t parity = 0;
-#pragma unroll 1
-    for (;;) {
+    auto acquire = [&]() -> const uint8_t* {
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
-        Desc d = desc[slot];
-        if (d.unit < 0) break;
-        const int bh = d.bh;
-        const uint8_t* sb = ring + slot * C::STAGE;
+        return ring + slot * C::STAGE;
+    };
+    auto release = [&]() {
+        __syncwarp();
+        if (++slot == S) {
+            slot = 0;
+            parity ^= 1u;
+        }
+    };
+
+#pragma unroll 1
+    for (;;) {
+        const int bh = fq0;
+        fq0 = fq1;
+        fq1 = fq2;
+        --fcount;
+        if (bh < 0) break;
 
         // ------------------------------------------------ pass 1: all scores -> smem
         float M;
         {
+            const uint8_t* sb = acquire();
             KQuery kq;
             load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
 #pragma unroll 1
-            for (;;) {
-                const int n = d.flags >> 8;
+            for (int st = 0;;) {
+                const int t0 = st * C::CH;
+                const int n = min(C::CH, n_tok - t0);
                 if (n == C::CH) {
 #pragma unroll 4
                     for (int i = 0; i < C::ITERS; ++i)
-                        k_iter<D, NCH, true>(i, kq, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                        k_iter<D, NCH, true>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
                 } else {
-#pragma unroll 1
+#pragma unroll 4
                     for (int i = 0; i < C::ITERS; ++i)
                         if (i * C::TPI < n)
-                            k_iter<D, NCH, false>(i, kq, sb, scores, d.t0, tl, n, lc, lm, sg, magic, mx);
+                            k_iter<D, NCH, false>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
                 }
-                const bool last = d.flags & kLastK;
-                __syncwarp();
-                if (++slot == S) {
-                    slot = 0;
-                    parity ^= 1u;
-                }
-                if (last) break;
-                issue(slot == 0 ? S - 1 : slot - 1);
-                mbar_wait(&bars[slot], parity);
-                d = desc[slot];
-                sb = ring + slot * C::STAGE;
+                release();
+                if (++st == nst) break;
+                sb = acquire();
             }
 #pragma unroll
             for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -185,9 +182,15 @@ decode_attention_topk_kernel(const TopkParams P) {
         for (int shift = 24; shift >= 0; shift -= 8) {
             for (int b = lane; b < 256; b += 32) hist[b] = 0;
             __syncwarp();
-            for (int t = lane; t < n_tok; t += 32) {
-                const uint32_t k = order_key(scores[t]);
-                if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+#pragma unroll 1
+            for (int t0 = 0; t0 < n_tok; t0 += 32) {
+                const int t = t0 + lane;
+                const uint32_t k = t < n_tok ? order_key(scores[t]) : 0u;
+                const bool in = t < n_tok && (k & pmask) == prefix;
+                const uint32_t bin = in ? (k >> shift) & 255u : 256u;
+                // aggregate equal bins across the warp first: one smem atomic per distinct bin
+                const unsigned same = __match_any_sync(0xffffffffu, bin);
+                if (in && (same & lt_mask) == 0u) atomicAdd(&hist[bin], uint32_t(__popc(same)));
             }
             __syncwarp();
             int c[8], local = 0;                // lane owns bins 255-8*lane .. 248-8*lane (descending)
@@ -279,30 +282,31 @@ decode_attention_topk_kernel(const TopkParams P) {
             t = j < keep ? int(kept[j]) : 0;
             return j < keep;
         };
-        int t_cur;
-        bool v_cur = row_of(tl, t_cur);
-        uint4 r_cur[4] = {};
-        uint32_t m_cur = 0u;
-        if (v_cur) load_row(t_cur, r_cur, m_cur);
+        // three groups of rows in flight (the gather is latency-bound)
+        int ta, tb, tc;
+        bool va = row_of(tl, ta), vb = row_of(C::TPI + tl, tb), vc = row_of(2 * C::TPI + tl, tc);
+        uint4 ra[4] = {}, rb[4] = {}, rc[4] = {};
+        uint32_t ma = 0u, mb = 0u, mc = 0u;
+        if (va) load_row(ta, ra, ma);
+        if (vb) load_row(tb, rb, mb);
+        if (vc) load_row(tc, rc, mc);
 #pragma unroll 1
         for (int g = 0; g * C::TPI < keep; ++g) {
-            int t_nxt;
-            const bool v_nxt = row_of((g + 1) * C::TPI + tl, t_nxt);
-            uint4 r_nxt[4] = {};
-            uint32_t m_nxt = 0u;
-            if (v_nxt) load_row(t_nxt, r_nxt, m_nxt);   // prefetch the next group's rows
-            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&m_cur));
-            float p = ex2(scores[t_cur] - M);
-            if (!v_cur) {
+            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&ma));
+            float p = ex2(scores[ta] - M);
+            if (!va) {
                 p = 0.0f;
                 vm = make_float2(0.0f, 0.0f);
             }
-            v_accum(acc, l, bsum, row_bytes(t_cur, r_cur), vm, p, magic);
-            t_cur = t_nxt;
-            v_cur = v_nxt;
+            v_accum(acc, l, bsum, row_bytes(ta, ra), vm, p, magic);
+            // rotate and fetch group g + 3
+            ta = tb; va = vb; ma = mb;
+            tb = tc; vb = vc; mb = mc;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) r_cur[i] = r_nxt[i];
-            m_cur = m_nxt;
+            for (int i = 0; i < 4; ++i) { ra[i] = rb[i]; rb[i] = rc[i]; }
+            vc = row_of((g + 3) * C::TPI + tl, tc);
+            mc = 0u;
+            if (vc) load_row(tc, rc, mc);
         }
         float v[32];
         const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
@@ -321,16 +325,16 @@ decode_attention_topk_kernel(const TopkParams P) {
     }
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t topk_smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8 + sizeof(Desc)) + kTopkMaxTokens * 6 + 256 * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 6 + 256 * 4);
 }
 
-template <int D, int NCH, int S, int WPC>
+template <int D, int NCH, int S, int WPC, int MAXT>
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
     static int occ = -1;
-    auto k = decode_attention_topk_kernel<D, NCH, S, WPC>;
-    const size_t smem = topk_smem_bytes<D, NCH, S, WPC>();
+    auto k = decode_attention_topk_kernel<D, NCH, S, WPC, MAXT>;
+    const size_t smem = topk_smem_bytes<D, NCH, S, WPC, MAXT>();
     if (occ < 0) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int o = 0;
@@ -361,8 +365,11 @@ cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
-    if (a.head_dim == 128) return launch_topk<128, 2, 2, 4>(a, stream);
-    return launch_topk<64, 2, 2, 4>(a, stream);
+    if (a.head_dim == 128)
+        return a.cur_len <= 576 ? launch_topk<128, 2, 2, 3, 576>(a, stream)
+                                : launch_topk<128, 2, 2, 3, kTopkMaxTokens>(a, stream);
+    return a.cur_len <= 576 ? launch_topk<64, 2, 2, 3, 576>(a, stream)
+                            : launch_topk<64, 2, 2, 3, kTopkMaxTokens>(a, stream);
 }
 
 }  // namespace flexq
