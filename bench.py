@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default="opt-175b")
     ap.add_argument("--layers", type=int, default=0, help="override model depth (0 = full)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--step", default="fused", choices=["fused", "two"],
+                    help="per layer: one fused append+attention launch (NEXT-3) or append_kv then attention")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
@@ -265,11 +267,20 @@ def run_flexq(args):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     cache_bytes = sum(c.nbytes() for c in caches)
 
+    fused = args.step == "fused"
+
+    def layer_step(j, cur, q, k_new, v_new, out, st):
+        """One layer of decode step cur_len = cur: append the token, attend (one or two launches)."""
+        if fused:
+            fq.flexq_append_decode_attention(q, k_new, v_new, caches[j], cur, out=out, workspace=ws, stream=st)
+        else:
+            fq.flexq_append_kv(k_new, v_new, caches[j], pos=cur - 1, stream=st)
+            fq.flexq_decode_attention(q, caches[j], cur, out=out, workspace=ws, stream=st)
+
     def step_calls(i, st):
         cur = s + i
         for j in range(L):
-            fq.flexq_append_kv(kn[j], vn[j], caches[j], pos=cur - 1, stream=st)
-            fq.flexq_decode_attention(qs[j], caches[j], cur, out=outs[j], workspace=ws, stream=st)
+            layer_step(j, cur, qs[j], kn[j], vn[j], outs[j], st)
 
     # one CUDA graph per decode step i = 1..n-1
     log("prompt fill done; capturing graphs")
@@ -327,8 +338,13 @@ def run_flexq(args):
     with torch.cuda.graph(gapp, stream=stream):
         for j in range(L):
             fq.flexq_append_kv(kn[j], vn[j], caches[j], pos=cur_last - 1, stream=stream)
+    gfu = torch.cuda.CUDAGraph()          # fused append + attention (rewrites the same token: idempotent)
+    with torch.cuda.graph(gfu, stream=stream):
+        for j in range(L):
+            fq.flexq_append_decode_attention(qs[j], kn[j], vn[j], caches[j], cur_last, out=outs[j], workspace=ws,
+                                             stream=stream)
     reps = 5
-    for g in (ga, gapp):
+    for g in (ga, gapp, gfu):
         g.replay()
     torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -340,12 +356,19 @@ def run_flexq(args):
         for _ in range(reps):
             gapp.replay()
         e[2].record(stream)
+        for _ in range(reps):
+            gfu.replay()
+        e[3].record(stream)
     torch.cuda.synchronize()
     attn_us = e[0].elapsed_time(e[1]) * 1e3 / (reps * L)
     app_us = e[1].elapsed_time(e[2]) * 1e3 / (reps * L)
+    fused_us = e[2].elapsed_time(e[3]) * 1e3 / (reps * L)
     attn_bytes = wl.attention_bytes(B, h1, cur_last)
+    fused_bytes = attn_bytes + wl.append_bytes(B, h1)
     peak, peak_kind = peaks()
-    achieved = attn_bytes / (attn_us * 1e-6) / 1e9
+    # the dominant kernel is the one the step launches per layer
+    k_us, k_bytes = (fused_us, fused_bytes) if fused else (attn_us, attn_bytes)
+    achieved = k_bytes / (k_us * 1e-6) / 1e9
 
     # ---- NEXT-1: Top-K sparse attention (keep 10%) at the same shape
     topk = None
@@ -376,7 +399,7 @@ def run_flexq(args):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tp) and w.name == "opt-175b" and B == 144:
-        traffic = json.load(open(tp))["dram_bytes_per_launch"]
+        traffic = json.load(open(tp)).get("fused_dram_bytes_per_launch" if fused else "dram_bytes_per_launch")
 
     # ---- e2e: host buffers through the public API, H2D of the step's inputs and D2H of its outputs
     log("e2e")
@@ -390,31 +413,33 @@ def run_flexq(args):
         knd = [torch.empty_like(kn[0]) for _ in range(2)]
         vnd = [torch.empty_like(vn[0]) for _ in range(2)]
         od = [torch.empty_like(outs[0]) for _ in range(2)]
-        copy = torch.cuda.Stream(device=dev)
+        h2d = torch.cuda.Stream(device=dev)       # one stream per copy direction: both copy engines busy
+        d2h = torch.cuda.Stream(device=dev)
 
         def e2e_step(i):
             cur = s + i
             ready = [torch.cuda.Event() for _ in range(L)]
             done = [torch.cuda.Event() for _ in range(L)]
+            drained = [torch.cuda.Event() for _ in range(L)]
             for j in range(L):
                 b = j & 1
-                with torch.cuda.stream(copy):
+                with torch.cuda.stream(h2d):
                     if j >= 2:
-                        copy.wait_event(done[j - 2])
-                        outh[j - 2].copy_(od[b], non_blocking=True)
+                        h2d.wait_event(done[j - 2])         # buffer b free: layer j - 2 has consumed it
                     qd[b].copy_(qh[j], non_blocking=True)
                     knd[b].copy_(knh[j], non_blocking=True)
                     vnd[b].copy_(vnh[j], non_blocking=True)
-                    ready[j].record(copy)
+                    ready[j].record(h2d)
                 stream.wait_event(ready[j])
-                fq.flexq_append_kv(knd[b], vnd[b], caches[j], pos=cur - 1, stream=stream)
-                fq.flexq_decode_attention(qd[b], caches[j], cur, out=od[b], workspace=ws, stream=stream)
+                if j >= 2:
+                    stream.wait_event(drained[j - 2])      # od[b] copied out
+                layer_step(j, cur, qd[b], knd[b], vnd[b], od[b], stream)
                 done[j].record(stream)
-            with torch.cuda.stream(copy):
-                for j in range(max(0, L - 2), L):
-                    copy.wait_event(done[j])
-                    outh[j].copy_(od[j & 1], non_blocking=True)
-            stream.wait_stream(copy)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(done[j])
+                    outh[j].copy_(od[b], non_blocking=True)
+                    drained[j].record(d2h)
+            stream.wait_stream(d2h)
 
         for k in range(2):
             e2e_step(seq_of(k))
@@ -435,7 +460,8 @@ def run_flexq(args):
                "unit": "GB/s", "h2d_bytes_per_step": int(qh.nbytes + knh.nbytes + vnh.nbytes),
                "d2h_bytes_per_step": int(outh.nbytes), "ms_per_step": round(ems / ke, 3),
                "tokens_per_s": round(B_total * ke / (ems / 1e3), 2),
-               "how": "pinned host q/k_new/v_new per layer -> H2D on a copy stream (double-buffered), "
+               "how": "pinned host q/k_new/v_new per layer -> H2D on a copy stream, D2H of the output on another "
+                      "(double-buffered), "
                       "append+attention via the C ABI, D2H of every layer's output; CUDA events, max over ranks"}
 
     # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
@@ -486,18 +512,24 @@ def run_flexq(args):
             "tokens_per_s": round(tokens_per_s, 2),
             "attention_tokens_per_s_per_layer": round(tokens_per_s * L, 1),
             "config": {"workload": f"{w.name} decode step: batch {B} per GPU (global {B_total}), {H} heads x {D}, "
-                                   f"s={s}, n={n}, l={L} layers, append_kv + decode_attention per layer, "
+                                   f"s={s}, n={n}, l={L} layers, "
+                                   + ("fused append+attention (one launch) per layer, " if fused else
+                                      "append_kv + decode_attention per layer, ") +
                                    f"steps cycle cur_len {s + 1}..{s + n - 1}",
                        "global_batch": B_total, "seq_len": s + n, "parallelism": f"dp{world} (sequences)",
                        "l2": f"working set {cache_bytes / 1e9:.1f} GB per GPU >> {l2 / 1e6:.0f} MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "traffic_source": "profiles/attention_traffic.json (ncu --set full, same launch shape)",
-                         "kernel": "decode_attention_kernel<128>", "peak_kind": peak_kind,
-                         "bytes_per_launch": attn_bytes, "us_per_launch": round(attn_us, 2),
+                         "kernel": "decode_attention_kernel<128>" + (" (fused append)" if fused else ""),
+                         "peak_kind": peak_kind,
+                         "bytes_per_launch": k_bytes, "us_per_launch": round(k_us, 2),
+                         "share_of_step": round(k_us * L / (ms_step * 1e3), 4),
+                         "attention_only_us_per_launch": round(attn_us, 2),
+                         "attention_only_GBps": round(attn_bytes / (attn_us * 1e-6) / 1e9, 1),
                          "append_us_per_launch": round(app_us, 2),
-                         "attention_share_of_step": round(attn_us * L / (ms_step * 1e3), 4)},
-            "gpu_launches": args.steps * L * 2,
+                         "fused_us_per_launch": round(fused_us, 2)},
+            "gpu_launches": args.steps * L * (1 if fused else 2),
             "clocks": clk.result(),
             "e2e": e2e,
             "cpu_baseline": cpu,

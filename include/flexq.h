@@ -130,6 +130,22 @@ flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, cons
                                     int cur_len, int bits, int group_size, void *out_f16,
                                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* One decode step of one layer in a single launch:
+ * exactly flexq_append_kv(k_new, v_new, pos = cur_len - 1, n_new = 1)
+ * followed by flexq_decode_attention(q, ..., cur_len) -- the new token is
+ * quantized first and attends to itself (reading L).
+ * k_new_f16, v_new_f16: fp16 [batch][heads][head_dim] (the token's K and V).
+ * The cache bytes written for position cur_len - 1 are identical to those of
+ * flexq_append_kv; nothing else in the cache is touched; the output
+ * satisfies flexq_decode_attention's accuracy bound.  Arguments, workspace
+ * and errors as for flexq_decode_attention (+ FLEXQ_ERR_NULL / _ALIGN for
+ * k_new / v_new). */
+flexq_status flexq_append_decode_attention(const void *q_f16, const void *k_new_f16, const void *v_new_f16,
+                                           void *k_cache, void *v_cache, int batch, int heads,
+                                           int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
+                                           int group_size, void *out_f16, void *workspace,
+                                           size_t workspace_bytes, void *stream);
+
 /* Top-K sparse decode attention, FlexGen's "4-bit-S":
  * scores s_t = q . K^_t / sqrt(head_dim) for t in [0, cur_len); the `keep`
  * highest scores are kept (equal scores: lower token index first); out fp16

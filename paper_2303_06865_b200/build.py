@@ -81,3 +81,4 @@ if __name__ == "__main__":
     if "--ab" in sys.argv:   # A/B libraries for tuning
         print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=1",), tag="h16unpack"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=0",), tag="kffma2"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_MINB=5",), tag="topk5"))

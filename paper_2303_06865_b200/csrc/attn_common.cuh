@@ -24,7 +24,8 @@ struct Cfg {
     static constexpr int CHB = kChunk * (CB + MB);     // chunk bytes (18 D)
     static constexpr int OFF_M = kChunk * CB;          // meta inside a chunk
     static constexpr int OFF_Q = NCH * CHB;
-    static constexpr int STAGE = OFF_Q + 2 * D;        // + q (fp16) for the unit's first stage
+    static constexpr int OFF_NEW = OFF_Q + 2 * D;      // fused append: k_new, v_new rows (fp16)
+    static constexpr int STAGE = OFF_NEW + 4 * D;      // + q [+ k_new, v_new] for the unit's first stage
     static constexpr int CPL_WORDS = D / 64;           // V pass: column-pair words per lane per quad
     static_assert(STAGE % 16 == 0 && CHB % 16 == 0, "stage alignment");
     static_assert(kChunk % TPI == 0, "an iteration stays inside one chunk");
@@ -170,14 +171,6 @@ __host__ __device__ constexpr int pair_col(int p, int h) {
 #endif
 }
 
-struct Desc {        // per-slot descriptor (shared memory)
-    int unit;        // work unit id (-1: none)
-    int bh;          // (batch, head) index of the unit
-    int t0;          // first token of the stage, relative to the unit
-    int flags;       // kFirst | kV | kLastK | kLast, tokens in the stage << 8
-};
-constexpr int kFirst = 1, kV = 2, kLastK = 4, kLast = 8;
-
 struct Params {
     const __half* q;
     const uint8_t* kc;   // chunked K cache
@@ -189,6 +182,10 @@ struct Params {
     float2* ml;          // [unit] (m, l)
     int bh_total, chunks, cur_len, nsplit, split_len;
     float qscale;        // log2(e) / sqrt(D)
+    const __half* k_new; // fused append (NEXT-3): token cur_len - 1 of every (b, h), [B H][D];
+    const __half* v_new; //   nullptr = the cache already holds it
+    uint8_t* kc_w;       // writable aliases of kc / vc for the fused append
+    uint8_t* vc_w;
 };
 
 #ifndef FLEXQ_K_IDP4A
@@ -557,6 +554,103 @@ __device__ __forceinline__ void write_out(__half* dst, const float (&v)[32], flo
     } else {
         *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(v[0] * inv, v[1] * inv);
     }
+}
+
+// ---------------------------------------------------------------- fused append (NEXT-3)
+// Quantize the new token's K and V rows (D fp16 each, contiguous in shared
+// memory: [k_new | v_new]) with one warp: lanes 0-15 take the K row, lanes
+// 16-31 the V row, EL = D / 16 consecutive elements per lane, so a 64-element
+// group spans GL = 64 / EL lanes.  The result stays in registers (TokenQ) and
+// is stored in the chunked cache layout by store_token (once into the cache in
+// HBM, once into the stage image in shared memory, so the attention reads the
+// new token without a round trip).  Same quantizer as quant.cu, operation for
+// operation (readings A-D, P): a = RN(x - min), u = RN(a / r)
+// via the per-group reciprocal + Markstein correction, t = RN(15 u),
+// code = RNE(t); scale = f16(RN(r / 15)) with RN(r / 15) by the same Markstein
+// step on the constant reciprocal RN(1/15) (tests/test_division.py checks it
+// against IEEE division for every fp32 r in the operand range).  Only scalar
+// round-to-nearest intrinsics are used, which ptxas never contracts, so the
+// bytes match quant.cu (compiled -fmad=false) exactly.
+struct TokenQ {
+    uint32_t codes;   // the lane's EL nibbles, element 2k in the low nibble of byte k
+    uint32_t meta;    // half2 {scale, min} of the lane's group
+};
+template <int D>
+__device__ __forceinline__ TokenQ quantize_kv_token(const uint8_t* rows, int lane) {
+    constexpr int EL = D / 16;                 // elements per lane (8 or 4)
+    constexpr int GL = kGroup / EL;            // lanes per group (8 or 16)
+    __half2 h[EL / 2];
+    if constexpr (EL == 8) {
+        const uint4 w = *reinterpret_cast<const uint4*>(rows + lane * 16);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = *reinterpret_cast<const __half2*>(&ws[i]);
+    } else {
+        const uint2 w = *reinterpret_cast<const uint2*>(rows + lane * 8);
+        h[0] = *reinterpret_cast<const __half2*>(&w.x);
+        h[1] = *reinterpret_cast<const __half2*>(&w.y);
+    }
+    __half2 lo = h[0], hi = h[0];
+#pragma unroll
+    for (int i = 1; i < EL / 2; ++i) {
+        lo = __hmin2(lo, h[i]);
+        hi = __hmax2(hi, h[i]);
+    }
+    __half2 mm = __halves2half2(__hmin(__low2half(lo), __high2half(lo)), __hmax(__low2half(hi), __high2half(hi)));
+#pragma unroll
+    for (int o = 1; o < GL; o <<= 1) {
+        const uint32_t tu = __shfl_xor_sync(0xffffffffu, *reinterpret_cast<const uint32_t*>(&mm), o);
+        const __half2 t = *reinterpret_cast<const __half2*>(&tu);
+        mm = __halves2half2(__hmin(__low2half(mm), __low2half(t)), __hmax(__high2half(mm), __high2half(t)));
+    }
+    float mn = __low2float(mm);
+    const float mx = __high2float(mm);
+    mn = (mn == 0.0f) ? 0.0f : mn;             // reading P
+    const float r = __fsub_rn(mx, mn);
+    TokenQ t;
+    t.codes = 0u;
+    float sc = 0.0f;
+    if (r != 0.0f) {                           // reading C
+        constexpr float kInv15 = 0.0666666701436042785645f;   // RN(1/15)
+        const float s0 = __fmul_rn(r, kInv15);
+        sc = __fmaf_rn(__fmaf_rn(-s0, 15.0f, r), kInv15, s0);  // RN(r / 15)
+        const float y = __frcp_rn(r);
+#pragma unroll
+        for (int e = 0; e < EL; ++e) {
+            const float x = (e & 1) ? __high2float(h[e / 2]) : __low2float(h[e / 2]);
+            const float a = __fsub_rn(x, mn);
+            const float q0 = __fmul_rn(a, y);
+            const float er = __fmaf_rn(-q0, r, a);
+            const float u = __fmaf_rn(er, y, q0);
+            const float b = __fadd_rn(__fmul_rn(u, 15.0f), 8388608.0f);   // 2^23 + RNE(15 u)
+            t.codes |= (__float_as_uint(b) & 15u) << (4 * e);
+        }
+    }
+    const __half2 m = __halves2half2(__float2half_rn(sc), __float2half_rn(mn));
+    t.meta = *reinterpret_cast<const uint32_t*>(&m);
+    return t;
+}
+// Store the lane's part of the quantized token at `slot` (index inside its
+// 32-token chunk) of `chunk`: lanes 0-15 write into a K chunk (token-major code
+// rows), lanes 16-31 into a V chunk (byte slot % 4 of the words of its quad row).
+// Each lane is called with the chunk of its own half.
+template <int D>
+__device__ __forceinline__ void store_token(const TokenQ& t, int slot, uint8_t* chunk, int lane) {
+    constexpr int EL = D / 16, GL = kGroup / EL;
+    constexpr int CB = D / 2, MB = D / 16;
+    const int l16 = lane & 15;
+    if (lane < 16) {
+        const int off = slot * CB + l16 * (EL / 2);
+        if constexpr (EL == 8)
+            *reinterpret_cast<uint32_t*>(chunk + off) = t.codes;
+        else
+            *reinterpret_cast<uint16_t*>(chunk + off) = uint16_t(t.codes);
+    } else {
+        uint8_t* p = chunk + ((slot >> 2) * CB + l16 * (EL / 2)) * 4 + (slot & 3);
+#pragma unroll
+        for (int i = 0; i < EL / 2; ++i) p[4 * i] = uint8_t(t.codes >> (8 * i));
+    }
+    if (l16 % GL == 0) *reinterpret_cast<uint32_t*>(chunk + kChunk * CB + slot * MB + (l16 / GL) * 4) = t.meta;
 }
 
 }  // namespace

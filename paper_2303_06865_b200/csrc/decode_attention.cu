@@ -40,6 +40,13 @@
 #include <algorithm>
 
 #include "attn_common.cuh"
+
+#ifndef FLEXQ_AB_FENCE
+#define FLEXQ_AB_FENCE 1
+#endif
+#ifndef FLEXQ_AB_GSTORE
+#define FLEXQ_AB_GSTORE 1
+#endif
 #include "flexq_internal.h"
 
 namespace flexq {
@@ -95,6 +102,7 @@ decode_attention_kernel(const Params P) {
     const uint8_t* p_v = nullptr;   // first V chunk
     const __half* p_q = nullptr;
     int p_len = 0;
+    bool p_new = false;             // fused append: this unit holds token cur_len - 1
     int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
     auto next_unit = [&]() {
         int t = 0;
@@ -110,6 +118,7 @@ decode_attention_kernel(const Params P) {
             p_k = P.kc + c0 * C::CHB;
             p_v = P.vc + c0 * C::CHB;
             p_q = P.q + int64_t(bh) * D;
+            p_new = P.k_new != nullptr && first + p_len == P.cur_len;
         }
         if (fcount == 0) fq0 = p_unit; else if (fcount == 1) fq1 = p_unit; else fq2 = p_unit;
         ++fcount;
@@ -126,9 +135,15 @@ decode_attention_kernel(const Params P) {
             const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
             const bool first = p_stage == 0;
             uint8_t* sb = ring + slot * C::STAGE;
-            mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0));
+            const bool with_new = first && p_new;
+            mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0) + (with_new ? 4 * D : 0));
             bulk_g2s(sb, (vpass ? p_v : p_k) + int64_t(si) * (NCH * C::CHB), bytes, &bars[slot], policy);
             if (first) bulk_g2s(sb + C::OFF_Q, p_q, 2 * D, &bars[slot], policy);
+            if (with_new) {
+                const int64_t row = (p_q - P.q);   // (b, h) * D
+                bulk_g2s(sb + C::OFF_NEW, P.k_new + row, 2 * D, &bars[slot], policy);
+                bulk_g2s(sb + C::OFF_NEW + 2 * D, P.v_new + row, 2 * D, &bars[slot], policy);
+            }
         }
         if (++p_stage == 2 * p_nst) next_unit();
     };
@@ -170,10 +185,35 @@ decode_attention_kernel(const Params P) {
         geo(unit, bh, first, len);
         const int nst = (len + C::CH - 1) / C::CH;
 
+        // fused append: the unit holding token cur_len - 1 quantizes k_new / v_new (they
+        // arrive with its first stage), stores them to the cache at once, and patches
+        // the stage images of its last K and V stages before the math reads them
+        const bool owns_new = P.k_new != nullptr && first + len == P.cur_len;
+        const int new_idx = (P.cur_len - 1) - first - (nst - 1) * C::CH;   // inside the last stage
+        const int new_slot = (P.cur_len - 1) & (kChunk - 1);
+        TokenQ tq{};                       // lanes 0-15: the K row, 16-31: the V row
+        auto patch = [&](const uint8_t* sb, bool vpass) {
+            if (vpass == (lane >= 16))
+                store_token<D>(tq, new_slot, const_cast<uint8_t*>(sb) + (new_idx >> 5) * C::CHB, lane);
+#if FLEXQ_AB_FENCE
+            fence_proxy_async();   // generic smem writes before the slot's next bulk copy
+#endif
+            __syncwarp();
+        };
+
         // ------------------------------------------------ pass 1: scores -> smem
         float M;
         {
             const uint8_t* sb = acquire();
+            if (owns_new) {
+                tq = quantize_kv_token<D>(sb + C::OFF_NEW, lane);
+#if FLEXQ_AB_GSTORE
+                uint8_t* gchunk = (lane < 16 ? P.kc_w : P.vc_w) +
+                                  (int64_t(bh) * P.chunks + ((P.cur_len - 1) >> 5)) * C::CHB;
+                store_token<D>(tq, new_slot, gchunk, lane);
+#endif
+                if (nst == 1) patch(sb, false);
+            }
             KQuery kq;                        // the lane's q for pass 1
             load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
@@ -194,6 +234,7 @@ decode_attention_kernel(const Params P) {
                 release();
                 if (++st == nst) break;
                 sb = acquire();
+                if (owns_new && st == nst - 1) patch(sb, false);
             }
 #pragma unroll
             for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -208,6 +249,7 @@ decode_attention_kernel(const Params P) {
 #pragma unroll 1
         for (int st = 0; st < nst; ++st) {
             const uint8_t* sb = acquire();
+            if (owns_new && st == nst - 1) patch(sb, true);
             const int t0 = st * C::CH;
             const int n = min(C::CH, len - t0);
             v_stage<D, NCH>(va, sb, scores + t0, M, n, lane, limbs);
@@ -354,6 +396,10 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.nsplit = nsplit;
     P.split_len = split_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
+    P.k_new = static_cast<const __half*>(a.k_new);
+    P.v_new = static_cast<const __half*>(a.v_new);
+    P.kc_w = static_cast<uint8_t*>(const_cast<void*>(a.k_cache));
+    P.vc_w = static_cast<uint8_t*>(const_cast<void*>(a.v_cache));
     decode_attention_kernel<D, NCH, S, WPC, UNR, MAXT><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC, MAXT>(), stream>>>(P);
     return cudaGetLastError();
 }

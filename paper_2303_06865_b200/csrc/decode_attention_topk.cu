@@ -12,19 +12,24 @@
 //
 // Design: persistent warps, one warp = one (b, h) (no context split; the
 // per-warp score buffer holds kTopkMaxTokens).  Pass 1 is the dense kernel's
-// TMA-bulk-staged K pass (attn_common.cuh).  Selection is an exact 4-round
-// radix select (8-bit digits) on order-preserving 32-bit keys of the fp32
-// scores, a warp-local smem histogram per round; ties at the threshold key go
-// to the lowest token indices (ballot prefix counts), so the kept set is the
-// definition's.  Pass 2 gathers the kept V rows straight from HBM (the token's
-// quad row of the quad-interleaved V chunk, 64 B per lane in 128-bit loads,
-// its byte extracted with PRMT, software-prefetched one group ahead) into
+// TMA-bulk-staged K pass (attn_common.cuh).  Selection is an exact bitwise
+// select on order-preserving 32-bit keys of the fp32 scores held in registers
+// (one warp-wide REDUX count per bit, stopping once exactly `keep` keys lie
+// above the candidate); ties at the threshold key go to the lowest token
+// indices (ballot prefix counts), so the kept set is the definition's.
+// Pass 2 gathers the kept V rows straight from HBM (the token's quad row of
+// the quad-interleaved V chunk, 64 B per lane in 128-bit loads, its byte
+// extracted with PRMT, three groups of rows in flight) into
 // fp32 register accumulators.
 #include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "attn_common.cuh"
 #include "flexq_internal.h"
+
+#ifndef FLEXQ_TOPK_MINB
+#define FLEXQ_TOPK_MINB 4   // CTAs per SM the register budget is sized for
+#endif
 
 namespace flexq {
 namespace {
@@ -58,18 +63,17 @@ __device__ __forceinline__ uint32_t ldg_nc32(const void* p) {
 }
 
 template <int D, int NCH, int S, int WPC, int MAXT>
-__global__ void __launch_bounds__(WPC * 32)
+__global__ void __launch_bounds__(WPC * 32, FLEXQ_TOPK_MINB)
 decode_attention_topk_kernel(const TopkParams P) {
     using C = Cfg<D, NCH>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     uint8_t* ring = smem + warp * (S * C::STAGE);
-    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (MAXT * 6 + 256 * 4);
+    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (MAXT * 6);
     float* scores = reinterpret_cast<float*>(wsm);
     uint16_t* kept = reinterpret_cast<uint16_t*>(wsm + MAXT * 4);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + MAXT * 6);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 6 + 256 * 4)) + warp * S;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 6)) + warp * S;
 
     const uint64_t policy = evict_first_policy();
     if (lane == 0) {
@@ -175,73 +179,55 @@ decode_attention_topk_kernel(const TopkParams P) {
             M = mx;   // the largest score is always kept, so M is the kept set's max
         }
 
-        // ------------------------------------------------ select: key of rank `keep` (radix, 4 x 8 bits)
-        uint32_t prefix = 0, pmask = 0;
-        int krem = keep;                       // rank still to find among keys matching prefix
+        // ------------------------------------------------ select: key T of rank `keep`
+        // Keys live in registers (token j * 32 + lane); T is built bit by bit from the
+        // top: a bit is set when at least `keep` keys are >= the candidate.  The search
+        // stops as soon as exactly `keep` keys are >= the candidate (then every kept
+        // key is >= T and no tie needs breaking); otherwise T ends as the exact key of
+        // rank `keep`.  Padding slots hold key 0, below every candidate.
+        constexpr int KPL = MAXT / 32;
+        uint32_t key[KPL];
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            const int t = j * 32 + lane;
+            key[j] = t < n_tok ? order_key(scores[t]) : 0u;
+        }
+        uint32_t T = 0u;
+        bool exact = false;
 #pragma unroll 1
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int b = lane; b < 256; b += 32) hist[b] = 0;
-            __syncwarp();
-#pragma unroll 1
-            for (int t0 = 0; t0 < n_tok; t0 += 32) {
-                const int t = t0 + lane;
-                const uint32_t k = t < n_tok ? order_key(scores[t]) : 0u;
-                const bool in = t < n_tok && (k & pmask) == prefix;
-                const uint32_t bin = in ? (k >> shift) & 255u : 256u;
-                // aggregate equal bins across the warp first: one smem atomic per distinct bin
-                const unsigned same = __match_any_sync(0xffffffffu, bin);
-                if (in && (same & lt_mask) == 0u) atomicAdd(&hist[bin], uint32_t(__popc(same)));
-            }
-            __syncwarp();
-            int c[8], local = 0;                // lane owns bins 255-8*lane .. 248-8*lane (descending)
+        for (int bit = 31; bit >= 0; --bit) {
+            const uint32_t cand = T | (1u << bit);
+            int c = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                c[i] = int(hist[255 - (lane * 8 + i)]);
-                local += c[i];
-            }
-            int incl = local;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int excl = incl - local;
-            const unsigned hit = __ballot_sync(0xffffffffu, excl < krem && krem <= incl);
-            const int src = __ffs(hit) - 1;
-            int digit = 0, above = 0;
-            if (lane == src) {
-                int acc = excl;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (acc + c[i] >= krem) {
-                        digit = 255 - (lane * 8 + i);
-                        above = acc;
-                        break;
-                    }
-                    acc += c[i];
+            for (int j = 0; j < KPL; ++j) c += key[j] >= cand ? 1 : 0;
+            c = int(__reduce_add_sync(0xffffffffu, uint32_t(c)));
+            if (c >= keep) {
+                T = cand;
+                if (c == keep) {
+                    exact = true;
+                    break;
                 }
             }
-            digit = __shfl_sync(0xffffffffu, digit, src);
-            above = __shfl_sync(0xffffffffu, above, src);
-            krem -= above;
-            prefix |= uint32_t(digit) << shift;
-            pmask |= 255u << shift;
-            __syncwarp();
         }
         // kept: key > T, or key == T among the first krem such tokens by index
         {
+            int krem = keep;
+            if (!exact) {
+                int gt = 0;
+#pragma unroll
+                for (int j = 0; j < KPL; ++j) gt += key[j] > T ? 1 : 0;
+                krem = keep - int(__reduce_add_sync(0xffffffffu, uint32_t(gt)));
+            }
             int base = 0, ties = 0;
-#pragma unroll 1
-            for (int t0 = 0; t0 < n_tok; t0 += 32) {
-                const int t = t0 + lane;
-                const bool in = t < n_tok;
-                const uint32_t k = in ? order_key(scores[t]) : 0u;
-                const bool gt = in && k > prefix;
-                const bool eq = in && k == prefix;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                if (j * 32 >= n_tok) break;
+                const bool gt = key[j] > T;
+                const bool eq = key[j] == T;
                 const unsigned beq = __ballot_sync(0xffffffffu, eq);
                 const bool keepit = gt || (eq && ties + __popc(beq & lt_mask) < krem);
                 const unsigned bk = __ballot_sync(0xffffffffu, keepit);
-                if (keepit) kept[base + __popc(bk & lt_mask)] = uint16_t(t);
+                if (keepit) kept[base + __popc(bk & lt_mask)] = uint16_t(j * 32 + lane);
                 base += __popc(bk);
                 ties += __popc(beq);
             }
@@ -282,7 +268,9 @@ decode_attention_topk_kernel(const TopkParams P) {
             t = j < keep ? int(kept[j]) : 0;
             return j < keep;
         };
-        // three groups of rows in flight (the gather is latency-bound)
+        // three groups of rows in flight (the gather is latency-bound); the loop is
+        // unrolled over the three register slots so no slot is copied while its
+        // loads are outstanding
         int ta, tb, tc;
         bool va = row_of(tl, ta), vb = row_of(C::TPI + tl, tb), vc = row_of(2 * C::TPI + tl, tc);
         uint4 ra[4] = {}, rb[4] = {}, rc[4] = {};
@@ -290,23 +278,26 @@ decode_attention_topk_kernel(const TopkParams P) {
         if (va) load_row(ta, ra, ma);
         if (vb) load_row(tb, rb, mb);
         if (vc) load_row(tc, rc, mc);
-#pragma unroll 1
-        for (int g = 0; g * C::TPI < keep; ++g) {
-            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&ma));
-            float p = ex2(scores[ta] - M);
-            if (!va) {
+        auto step = [&](int g, int& t, bool& v, uint4 (&r)[4], uint32_t& m) {
+            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&m));
+            float p = ex2(scores[t] - M);
+            if (!v) {
                 p = 0.0f;
                 vm = make_float2(0.0f, 0.0f);
             }
-            v_accum(acc, l, bsum, row_bytes(ta, ra), vm, p, magic);
-            // rotate and fetch group g + 3
-            ta = tb; va = vb; ma = mb;
-            tb = tc; vb = vc; mb = mc;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { ra[i] = rb[i]; rb[i] = rc[i]; }
-            vc = row_of((g + 3) * C::TPI + tl, tc);
-            mc = 0u;
-            if (vc) load_row(tc, rc, mc);
+            v_accum(acc, l, bsum, row_bytes(t, r), vm, p, magic);
+            v = row_of((g + 3) * C::TPI + tl, t);   // refill the slot with group g + 3
+            m = 0u;
+            if (v) load_row(t, r, m);
+        };
+#pragma unroll 1
+        for (int g = 0;; g += 3) {
+            step(g, ta, va, ra, ma);
+            if ((g + 1) * C::TPI >= keep) break;
+            step(g + 1, tb, vb, rb, mb);
+            if ((g + 2) * C::TPI >= keep) break;
+            step(g + 2, tc, vc, rc, mc);
+            if ((g + 3) * C::TPI >= keep) break;
         }
         float v[32];
         const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
@@ -327,7 +318,7 @@ decode_attention_topk_kernel(const TopkParams P) {
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t topk_smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 6 + 256 * 4);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 6);
 }
 
 template <int D, int NCH, int S, int WPC, int MAXT>

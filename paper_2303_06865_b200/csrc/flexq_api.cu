@@ -132,6 +132,28 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, cons
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
+flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_f16, const void* v_new_f16,
+                                           void* k_cache, void* v_cache, int batch, int heads, int head_dim,
+                                           int prompt_len, int gen_len, int cur_len, int bits, int group_size,
+                                           void* out_f16, void* workspace, size_t workspace_bytes,
+                                           void* stream) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s == FLEXQ_ERR_ARG) return s;
+    const int t_cap = prompt_len + gen_len;
+    if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
+    if (s != FLEXQ_OK) return s;
+    if (!q_f16 || !k_new_f16 || !v_new_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(q_f16) || !aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_cache) ||
+        !aligned16(v_cache) || !aligned16(out_f16))
+        return FLEXQ_ERR_ALIGN;
+    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+        return FLEXQ_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
+    flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
+                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap, k_new_f16, v_new_f16};
+    return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
+}
+
 flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache, const void* v_cache,
                                          int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                          int cur_len, int keep, int bits, int group_size, void* out_f16,

@@ -38,6 +38,8 @@ struct AttnArgs {
     void* out;
     void* workspace;
     int batch, heads, head_dim, chunks, cur_len, t_cap;
+    const void* k_new = nullptr;   // fused append of token cur_len - 1 (NEXT-3), or nullptr
+    const void* v_new = nullptr;
 };
 
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);

@@ -52,8 +52,9 @@ def lib():
         L.flexq_decode_attention_workspace_size.restype = SZ
         L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 8 + [P, P, SZ, P]
         L.flexq_decode_attention_topk.argtypes = [P, P, P] + [I] * 9 + [P, P, P, SZ, P]
+        L.flexq_append_decode_attention.argtypes = [P] * 5 + [I] * 8 + [P, P, SZ, P]
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
-                  "flexq_decode_attention", "flexq_decode_attention_topk"):
+                  "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -214,6 +215,29 @@ def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=No
                                         cur_len, cache.bits, cache.group_size, out.data_ptr(),
                                         workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "flexq_decode_attention")
+    return out
+
+
+def flexq_append_decode_attention(q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache,
+                                  cur_len: int, out=None, workspace=None, stream=None) -> torch.Tensor:
+    """One layer's decode step in one launch (NEXT-3): append k_new / v_new fp16 [B][H][D] (or
+    [B][H][1][D]) at position cur_len - 1, then attend over [0, cur_len).  Same cache bytes as
+    flexq_append_kv, same output bound as flexq_decode_attention."""
+    _need(q, torch.float16, "q")
+    _need(k_new, torch.float16, "k_new")
+    _need(v_new, torch.float16, "v_new")
+    if k_new.numel() != q.numel() or v_new.numel() != q.numel():
+        raise ValueError("k_new / v_new must hold one token per (batch, head): [B][H][D]")
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = make_workspace(cache)
+    _check(lib().flexq_append_decode_attention(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), cache.k.data_ptr(),
+                                               cache.v.data_ptr(), cache.batch, cache.heads, cache.head_dim,
+                                               cache.prompt_len, cache.gen_len, cur_len, cache.bits,
+                                               cache.group_size, out.data_ptr(), workspace.data_ptr(),
+                                               workspace.numel(), _stream(stream)),
+           "flexq_append_decode_attention")
     return out
 
 

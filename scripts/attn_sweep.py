@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--fused", action="store_true", help="time flexq_append_decode_attention")
     a = ap.parse_args()
     w = wl.CONFIGS[a.config]
     B = a.batch or w.batch
@@ -41,13 +42,21 @@ def main():
     ws = fq.make_workspace(caches[0])
     cur = s + n - 1
     st = torch.cuda.current_stream()
+    kn = synth.fill(5, 4, (B, H, D), device=dev)
+    vn = synth.fill(5, 5, (B, H, D), device=dev)
+
+    def call(c):
+        if a.fused:
+            fq.flexq_append_decode_attention(q, kn, vn, c, cur, out=out, workspace=ws)
+        else:
+            fq.flexq_decode_attention(q, c, cur, out=out, workspace=ws)
     g = torch.cuda.CUDAGraph()
     for c in caches:
-        fq.flexq_decode_attention(q, c, cur, out=out, workspace=ws)
+        call(c)
     torch.cuda.synchronize()
     with torch.cuda.graph(g):
         for c in caches:
-            fq.flexq_decode_attention(q, c, cur, out=out, workspace=ws)
+            call(c)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -57,8 +66,9 @@ def main():
     e1.record(st)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (a.reps * a.layers)
-    nb = wl.attention_bytes(B, H * D, cur)
-    print(json.dumps({"cfg": os.environ.get("FLEXQ_ATTN_CFG", "default"), "config": a.config, "batch": B,
+    nb = wl.attention_bytes(B, H * D, cur) + (wl.append_bytes(B, H * D) if a.fused else 0)
+    print(json.dumps({"cfg": os.environ.get("FLEXQ_ATTN_CFG", "default"), "fused": a.fused, "config": a.config,
+                      "batch": B,
                       "cur_len": cur, "us": round(us, 2), "GBps": round(nb / us / 1e3, 1)}))
 
 

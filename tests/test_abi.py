@@ -119,3 +119,21 @@ def test_topk_validation(L):
     assert call(sel=U) == fq.FLEXQ_ERR_ALIGN
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
     assert fq.topk_keep(543) == 55 and fq.topk_keep(130) == 13 and fq.topk_keep(5) == 1
+
+
+def test_append_attention_validation(L):
+    f = L.flexq_append_decode_attention
+    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+
+    def call(cur=5, D=128, q=A, kn=A, vn=A, kv=A, out=A, w=A, wb=ws, g=64):
+        return f(q, kn, vn, kv, A, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
+    assert call(cur=0) == fq.FLEXQ_ERR_ARG
+    assert call(cur=13) == fq.FLEXQ_ERR_ARG
+    assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(g=32) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(kn=None) == fq.FLEXQ_ERR_NULL
+    assert call(vn=None) == fq.FLEXQ_ERR_NULL
+    assert call(kv=None) == fq.FLEXQ_ERR_NULL
+    assert call(vn=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
+    assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE

@@ -72,3 +72,41 @@ def test_markstein_division_equals_ieee():
         assert out.returncode == 0, out.stdout
         tested = int(out.stdout.split()[-3])
         assert tested > 10_000_000
+
+
+SRC15 = r"""
+#include <stdio.h>
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+int main(void) {
+  /* every fp32 r in [2^-24, 131008] (a superset of RN(max - min) over fp16 groups) */
+  const float y = 1.0f / 15.0f;
+  uint32_t lo, hi; float flo = ldexpf(1.0f, -24), fhi = 131008.0f;
+  memcpy(&lo, &flo, 4); memcpy(&hi, &fhi, 4);
+  long bad = 0, tested = 0;
+  for (uint32_t b = lo; b <= hi; b++) {
+    float r; memcpy(&r, &b, 4);
+    float u = r / 15.0f;
+    float s0 = r * y, s1 = fmaf(fmaf(-s0, 15.0f, r), y, s0);
+    tested++;
+    if (memcmp(&u, &s1, 4) != 0) { if (bad < 5) printf("MISMATCH r=%a ieee=%a markstein=%a\n", r, u, s1); bad++; }
+  }
+  printf("y=%a tested %ld bad %ld\n", y, tested, bad);
+  return bad != 0;
+}
+"""
+
+
+def test_scale_division_by_15_exhaustive():
+    """RN(r / 15) (the stored scale, O5) as s0 = RN(r * RN(1/15)), RN(s0 + fma(-s0, 15, r) * RN(1/15)):
+    equal to IEEE division for every fp32 r in the operand range (the fused append kernel's form)."""
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "div15.c")
+        exe = os.path.join(d, "div15")
+        open(c, "w").write(SRC15)
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-o", exe, c, "-lm"])
+        out = subprocess.run([exe], capture_output=True, text=True)
+        assert out.returncode == 0, out.stdout
+        assert "y=0x1.111112p-4" in out.stdout          # RN(1/15) = 0x3D888889, the kernel's constant
+        assert int(out.stdout.split()[-3]) > 300_000_000

@@ -277,3 +277,61 @@ def test_topk_attention_parity(orc, cuda, case):
     assert (mask != omask).sum() <= 2 * B * H          # differences only at near-ties
     ref, _, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, cur, keep, sel=mask)
     assert_attn_close(out.cpu().numpy(), ref, name)
+
+
+# ---------------------------------------------------------------- fused append + attention (NEXT-3)
+FUSED_CASES = [
+    # name, B, H, D, s, n, steps (fused decode steps after the prompt), outliers, qfactor
+    ("d128_split_ragged", 2, 3, 128, 100, 8, 3, False, 1),        # split-K, token in a ragged last stage
+    ("d128_first_token_of_chunk", 2, 4, 128, 95, 4, 2, True, 16),  # cur_len 96, 97: chunk boundary
+    ("d128_one_token", 3, 2, 128, 0, 2, 1, False, 1),             # cur_len = 1: the new token alone
+    ("d128_no_split", 24, 128, 128, 40, 2, 1, False, 4),          # B*H = 3072 units
+    ("d64_tiny", 4, 12, 64, 512, 1, 1, False, 1),                 # configs[0] with the fused step
+    ("d64_full_capacity", 2, 3, 64, 60, 3, 3, True, 16),          # last step: cur_len = T_cap
+]
+
+
+@pytest.mark.parametrize("case", FUSED_CASES, ids=[c[0] for c in FUSED_CASES])
+def test_append_attention_fused(orc, cuda, case):
+    """flexq_append_decode_attention == flexq_append_kv(pos = cur_len - 1) then attention:
+    the cache bytes bit-exact against the oracle's append, the output within reading Q."""
+    name, B, H, D, s, n, steps, outl, qf = case
+    cache, okc, ovc, _, cur = build_case(orc, cuda, B, H, D, s, n, 0, seed=45, outliers=outl)
+    ws = fq.make_workspace(cache)
+    for step in range(1, steps + 1):
+        kn = synth.fill(45, synth.tensor_id(1, synth.K_NEW, step), (B, H, D))
+        vn = synth.fill(45, synth.tensor_id(1, synth.V_NEW, step), (B, H, D))
+        if outl:
+            kn, vn = synth.with_outliers(kn), synth.with_outliers(vn)
+        q = synth.peaky(synth.fill(45, synth.tensor_id(1, synth.Q, step), (B, H, D)), qf)
+        cur = s + step
+        out = fq.flexq_append_decode_attention(q.to(cuda), kn.to(cuda), vn.to(cuda), cache, cur, workspace=ws)
+        orc.append_kv(kn.numpy()[:, :, None], vn.numpy()[:, :, None], okc, ovc, cur - 1)
+        torch.cuda.synchronize()
+        assert_attn_close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, cur), f"{name} step {step}")
+    T = s + n
+    assert np.array_equal(cache.k_codes()[:, :, :T].cpu().numpy(), orc.pack4(okc[0]))
+    assert np.array_equal(cache.v_codes()[:, :, :T].cpu().numpy(), orc.pack4(ovc[0]))
+    assert np.array_equal(cache.k_meta()[:, :, :T].cpu().numpy().view(np.uint16), okc[1])
+    assert np.array_equal(cache.v_meta()[:, :, :T].cpu().numpy().view(np.uint16), ovc[1])
+    assert int(ws[:256 + 4 * B * H].sum()) == 0
+
+
+def test_append_attention_fused_matches_two_launches(cuda):
+    """The fused step and the two-launch step (append, then attention) leave
+    byte-identical caches; outputs agree to reading Q (same kernel, same data)."""
+    B, H, D, s, n = 16, 12, 128, 300, 4
+    k = synth.fill(46, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D)).to(cuda)
+    v = synth.fill(46, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D)).to(cuda)
+    c1, c2 = fq.KVCache(B, H, D, s, n, device=cuda), fq.KVCache(B, H, D, s, n, device=cuda)
+    fq.flexq_append_kv(k, v, c1, pos=0)
+    fq.flexq_append_kv(k, v, c2, pos=0)
+    for step in range(1, n + 1):
+        kn = synth.fill(46, synth.tensor_id(1, synth.K_NEW, step), (B, H, D)).to(cuda)
+        vn = synth.fill(46, synth.tensor_id(1, synth.V_NEW, step), (B, H, D)).to(cuda)
+        q = synth.fill(46, synth.tensor_id(1, synth.Q, step), (B, H, D)).to(cuda)
+        o1 = fq.flexq_append_decode_attention(q, kn, vn, c1, s + step)
+        fq.flexq_append_kv(kn.view(B, H, 1, D), vn.view(B, H, 1, D), c2, pos=s + step - 1)
+        o2 = fq.flexq_decode_attention(q, c2, s + step)
+        assert torch.equal(o1, o2), f"step {step}"
+    assert torch.equal(c1.k, c2.k) and torch.equal(c1.v, c2.v)
