@@ -82,3 +82,5 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=1",), tag="h16unpack"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=0",), tag="kffma2"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_MINB=5",), tag="topk5"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_MMA=0",), tag="kidp"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_V_MMA=0",), tag="vidp"))

@@ -324,6 +324,171 @@ __device__ __forceinline__ void k_iter(int i, const KQuery& kq, const uint8_t* s
     }
 }
 
+// ---------------------------------------------------------------- pass 1 on the tensor cores
+// FLEXQ_K_MMA=1 (default): the scores of 16 tokens at a time as one integer
+// matrix product on IMMA (mma.sync m16n8k32, u8 codes x s8 q digits, exact
+// int32 accumulation):
+//   A (16 x 32, u8)  = the codes of 16 tokens (rows) x 32 elements (k), straight
+//                      from the smem stage: a code word's low nibbles (w & 0x0F0F0F0F)
+//                      and high nibbles ((w >> 4) & 0x0F0F0F0F) are 4 bytes of A each;
+//   B (32 x 8, s8)   = q as a 23-bit fixed-point integer per 64-element group
+//                      (scale 2^(22 - E_g), |q| < 2^E_g), split into three signed
+//                      base-256 digits; column n = (digit, group) (3 G columns used);
+//   C (16 x 8, s32)  = per token, the dot products of its codes with each digit
+//                      of each group's q.
+// The element order along k is any permutation applied to both operands alike
+// (a dot product does not care): k-step s, lane quad-index j covers the word
+// w = j KS + s of the token row, k positions 4j..4j+3 its even columns,
+// 16+4j..16+4j+3 its odd columns.  Epilogue per token (each lane holds two C
+// columns of two tokens; a 2-step quad reduction adds them up):
+//   score = sum_g scale_g * 2^(E_g - 22) qscale * (C_g0 + 2^8 C_g1 + 2^16 C_g2)
+//           + sum_g min_g * qscale * sum_{j in g} q_j              (log2 domain).
+// Column map: D = 128: n = 0..5 -> (d0,g0) (d1,g0) (d2,g0) (d2,g1) (d0,g1) (d1,g1);
+// D = 64: n = 0..2 -> d0, d1, d2.  So lane tig 0 and 2 combine their two columns
+// in int32 (C_d0 + 2^8 C_d1 < 2^31), tig 1 holds the two d2 columns, tig 3
+// (zero columns) adds the min term.
+#ifndef FLEXQ_K_MMA
+#define FLEXQ_K_MMA 1
+#endif
+
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int D>
+struct KFrag {
+    static constexpr int KS = D / 32;   // k-steps per token row
+    uint32_t b[KS][2];                  // B fragment (q digits of the lane's column)
+    int k256;                           // 256: combine the lane's two C columns in int32
+    float wA, wB, bA, bB;               // v = fma(x0, wA, bA) hA + fma(x1, wB, bB) hB
+    int offA, offB;                     // byte offsets of hA / hB in the token's meta
+};
+
+// q (fp16 [D] at qs, smem) -> the lane's KFrag.
+template <int D>
+__device__ __forceinline__ void load_q_mma(const uint8_t* qs, float qscale, int lane, KFrag<D>& kf) {
+    constexpr int KS = D / 32, G = D / 64, NE = 8 * KS;   // elements per lane
+    constexpr int JG = 4 / G;                             // quad lanes per group
+    const int n = lane >> 2, j = lane & 3;
+    const __half* qh = reinterpret_cast<const __half*>(qs) + NE * j;   // words j KS .. j KS + KS - 1
+    float q[NE], mx = 0.0f, sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        q[i] = __half2float(qh[i]);
+        mx = fmaxf(mx, fabsf(q[i]));
+        sum += q[i];
+    }
+#pragma unroll
+    for (int o = 1; o < JG; o <<= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    }
+    int e = 0;
+    frexpf(mx, &e);                                      // mx < 2^e (mx = 0 -> e = 0)
+    const float up = ldexpf(1.0f, 22 - e);   // |Q| < 2^22: the signed top digit stays in [-64, 64]
+    const int gl = j / JG;                               // the group of the lane's words
+    // column n of B: digit n % 3 of group n / 3 (D = 128: n = 3 is (d2, g1), 4 / 5 are d0 / d1 of g1)
+    int dig = -1, grp = -1;
+    if (G == 2) {
+        dig = n < 3 ? n : (n == 3 ? 2 : (n == 4 ? 0 : (n == 5 ? 1 : -1)));
+        grp = n < 3 ? 0 : (n < 6 ? 1 : -1);
+    } else if (n < 3) {
+        dig = n;
+        grp = 0;
+    }
+    const bool live = dig >= 0 && grp == gl;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+        uint32_t b0 = 0, b1 = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int Q0 = __float2int_rn(q[8 * s + 2 * i] * up);       // exact scaling, |Q| < 2^22
+            const int Q1 = __float2int_rn(q[8 * s + 2 * i + 1] * up);
+            // signed base-256 digits: Q = d0 + 2^8 d1 + 2^16 d2, each in [-128, 127]
+            const int a0 = (Q0 << 24) >> 24, r0 = (Q0 - a0) >> 8, a1 = (r0 << 24) >> 24, a2 = (r0 - a1) >> 8;
+            const int c0 = (Q1 << 24) >> 24, r1 = (Q1 - c0) >> 8, c1 = (r1 << 24) >> 24, c2 = (r1 - c1) >> 8;
+            const int x = dig == 0 ? a0 : (dig == 1 ? a1 : a2);
+            const int y = dig == 0 ? c0 : (dig == 1 ? c1 : c2);
+            b0 |= (uint32_t(x) & 0xFFu) << (8 * i);
+            b1 |= (uint32_t(y) & 0xFFu) << (8 * i);
+        }
+        kf.b[s][0] = live ? b0 : 0u;
+        kf.b[s][1] = live ? b1 : 0u;
+    }
+    // per-group weights from the quad lanes that own each group
+    const float w_l = qscale * ldexpf(1.0f, e - 22);   // this lane's group weight
+    const float s_l = sum * qscale;
+    const float w0 = __shfl_sync(0xffffffffu, w_l, lane & ~3);
+    const float s0 = __shfl_sync(0xffffffffu, s_l, lane & ~3);
+    const float w1 = __shfl_sync(0xffffffffu, w_l, (lane & ~3) | 2);
+    const float s1 = __shfl_sync(0xffffffffu, s_l, (lane & ~3) | 2);
+    kf.wA = kf.wB = kf.bA = kf.bB = 0.0f;
+    kf.k256 = 0;
+    kf.offA = 0;
+    kf.offB = 2;
+    if (G == 2) {
+        if (j == 0) { kf.k256 = 256; kf.wA = w0; kf.offA = 0; }
+        if (j == 1) { kf.wA = w0 * 65536.0f; kf.offA = 0; kf.wB = w1 * 65536.0f; kf.offB = 4; }
+        if (j == 2) { kf.k256 = 256; kf.wA = w1; kf.offA = 4; }
+        if (j == 3) { kf.bA = s0; kf.offA = 2; kf.bB = s1; kf.offB = 6; }
+    } else {
+        if (j == 0) { kf.k256 = 256; kf.wA = w0; kf.offA = 0; }
+        if (j == 1) { kf.wA = w0 * 65536.0f; kf.offA = 0; }
+        if (j == 3) { kf.bA = s0; kf.offA = 2; }
+    }
+}
+
+// Pass 1, one 16-token block `blk` of the stage (tokens 16 blk + [0, 16)): scores -> smem.
+template <int D, int NCH>
+__device__ __forceinline__ void k_block_mma(int blk, const KFrag<D>& kf, const uint8_t* sb, float* sc, int t0,
+                                            int n, int lane, float& mx) {
+    using C = Cfg<D, NCH>;
+    constexpr int KS = D / 32;
+    const int r = lane >> 2, j = lane & 3;
+    const int tok = blk * 16 + r;                       // stage-relative token of row r (row r + 8: tok + 8)
+    const uint8_t* ch = sb + (tok >> 5) * C::CHB;       // a 16-token block never straddles a chunk
+    const int slot = tok & 31;
+    const uint8_t* cr = ch + slot * C::CB + j * (4 * KS);
+    uint32_t w0[KS], w8[KS];
+    if constexpr (KS == 4) {
+        const uint4 x = lds128(cr), y = lds128(cr + 8 * C::CB);
+        w0[0] = x.x; w0[1] = x.y; w0[2] = x.z; w0[3] = x.w;
+        w8[0] = y.x; w8[1] = y.y; w8[2] = y.z; w8[3] = y.w;
+    } else {
+        const uint2 x = *reinterpret_cast<const uint2*>(cr), y = *reinterpret_cast<const uint2*>(cr + 8 * C::CB);
+        w0[0] = x.x; w0[1] = x.y;
+        w8[0] = y.x; w8[1] = y.y;
+    }
+    int c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < KS; ++s)
+        mma_u8s8(c, w0[s] & 0x0F0F0F0Fu, w8[s] & 0x0F0F0F0Fu, (w0[s] >> 4) & 0x0F0F0F0Fu,
+                 (w8[s] >> 4) & 0x0F0F0F0Fu, kf.b[s][0], kf.b[s][1]);
+    const uint8_t* mr = ch + C::OFF_M + slot * C::MB;
+    const float hA0 = __half2float(*reinterpret_cast<const __half*>(mr + kf.offA));
+    const float hB0 = __half2float(*reinterpret_cast<const __half*>(mr + kf.offB));
+    const float hA8 = __half2float(*reinterpret_cast<const __half*>(mr + 8 * C::MB + kf.offA));
+    const float hB8 = __half2float(*reinterpret_cast<const __half*>(mr + 8 * C::MB + kf.offB));
+    float v0 = fmaf(fmaf(float(c[0] + kf.k256 * c[1]), kf.wA, kf.bA), hA0, fmaf(float(c[1]), kf.wB, kf.bB) * hB0);
+    float v8 = fmaf(fmaf(float(c[2] + kf.k256 * c[3]), kf.wA, kf.bA), hA8, fmaf(float(c[3]), kf.wB, kf.bB) * hB8);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+    v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+    v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
+    if (tok < n) {
+        mx = fmaxf(mx, v0);
+        if (j == 0) sc[t0 + tok] = v0;
+    }
+    if (tok + 8 < n) {
+        mx = fmaxf(mx, v8);
+        if (j == 1) sc[t0 + tok + 8] = v8;
+    }
+}
+
 // acc_j += (p scale) c_j over the lane's 32 columns, bias += p min, l += p.
 __device__ __forceinline__ void v_accum(float2 (&acc)[16], float& l, float& bsum, uint4 vw, float2 vm, float p,
                                         uint32_t magic) {
@@ -409,9 +574,13 @@ struct VAcc {
     }
 };
 
+// Pass 2 stage pre-pass: weights a_tg = p_t scale_tg of the stage's tokens as
+// 24-bit fixed point (scale 2^(23 - e_g), a < 2^e_g per group) in the limb
+// table [group][quad][limb 0..2, pad][token byte]; l += p, bias_g += p min_g
+// on the lane's tokens; inv[g] = 2^(e_g - 23).
 template <int D, int NCH>
-__device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const float* sc, float M, int n, int lane,
-                                        uint32_t* limbs) {
+__device__ __forceinline__ void v_weights(float& l, float (&bsum)[D / 64], const uint8_t* sb, const float* sc, float M,
+                                          int n, int lane, uint32_t* limbs, float (&inv)[D / 64]) {
     using C = Cfg<D, NCH>;
     constexpr int G = D / 64;           // groups per token
     constexpr int Q = C::CH / 4;        // quads per stage
@@ -426,7 +595,7 @@ __device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const fl
         const int t = lane + 32 * i;
         const bool valid = t < n;
         const float p = valid ? ex2(sc[t] - M) : 0.0f;
-        va.l += p;
+        l += p;
         const uint8_t* mrow = sb + (t / kChunk) * C::CHB + C::OFF_M + (t % kChunk) * C::MB;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -434,11 +603,10 @@ __device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const fl
             sm.x = valid ? sm.x : 0.0f;
             sm.y = valid ? sm.y : 0.0f;
             a[i][g] = p * sm.x;
-            va.bsum[g] = fmaf(p, sm.y, va.bsum[g]);
+            bsum[g] = fmaf(p, sm.y, bsum[g]);
             amax[g] = fmaxf(amax[g], a[i][g]);
         }
     }
-    float inv[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -459,6 +627,16 @@ __device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const fl
         }
     }
     __syncwarp();
+}
+
+template <int D, int NCH>
+__device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const float* sc, float M, int n, int lane,
+                                        uint32_t* limbs) {
+    using C = Cfg<D, NCH>;
+    constexpr int G = D / 64;           // groups per token
+    constexpr int Q = C::CH / 4;        // quads per stage
+    float inv[G];
+    v_weights<D, NCH>(va.l, va.bsum, sb, sc, M, n, lane, limbs, inv);
     // ---- IDP.4A over quads: lane's CPL columns = CPL/2 column-pair words per quad
     constexpr int W = C::CPL_WORDS;
     const int g = (lane * (D / 32)) / 64;
@@ -497,6 +675,237 @@ __device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const fl
         va.acc[c] = fmaf(f, (G == 1 || g == 0) ? inv[0] : inv[G - 1], va.acc[c]);
     }
     __syncwarp();   // limb table reuse by the next stage
+}
+
+// ---------------------------------------------------------------- pass 2 on the tensor cores
+// FLEXQ_V_MMA=1 (default): P.V of each 32-token k-step as IMMA m16n8k32 (u8 x u8,
+// exact int32):
+//   A (16 x 32) = V codes: row r <-> column 2 p (low nibbles, w & 0x0F0F0F0F),
+//                 row r + 8 <-> column 2 p + 1 (high nibbles, w & 0xF0F0F0F0 = 16 c),
+//                 p = PPL r + u for tile u; k <-> tokens: positions 4j..4j+3 are the
+//                 4 tokens of quad 8s + j (one quad-interleaved word), 16+4j.. quad 8s+4+j;
+//   B (32 x 8)  = the weight limbs a_tg (v_weights' table, one word per quad and limb);
+//                 column n = (limb, group) as in pass 1's map;
+//   C (16 x 8)  = per column, per (limb, group) partial sums; only the column's own
+//                 group is kept.  Flushed to fp32 once per stage (the fixed-point scale
+//                 is per stage); limbs and nibble positions are combined at the end of
+//                 the unit, with a quad reduction.
+#ifndef FLEXQ_V_MMA
+#define FLEXQ_V_MMA 1
+#endif
+
+__device__ __forceinline__ void mma_u8u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int D>
+struct VAccM {
+    static constexpr int PPL = D / 16;   // tiles (column pairs per lane row)
+    float acc[PPL][4];                   // fp32 partials of C, per tile / C register
+    float l, bsum[D / 64];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int u = 0; u < PPL; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[u][i] = 0.0f;
+        l = 0.0f;
+#pragma unroll
+        for (int g = 0; g < D / 64; ++g) bsum[g] = 0.0f;
+    }
+};
+
+// pass 1's (limb, group) map of C column n (-1: unused)
+template <int D>
+__device__ __forceinline__ void col_role(int n, int& limb, int& grp) {
+    if (D == 128) {
+        limb = n < 3 ? n : (n == 3 ? 2 : (n == 4 ? 0 : (n == 5 ? 1 : -1)));
+        grp = n < 3 ? 0 : (n < 6 ? 1 : -1);
+    } else {
+        limb = n < 3 ? n : -1;
+        grp = n < 3 ? 0 : -1;
+    }
+}
+
+// Fixed-point scale for a block of non-negative weights with maximum bit
+// pattern mb: e = floor(log2(amax)) + 1 (amax < 2^e); up = 2^(23 - e),
+// inv = 2^(e - 23), built from the exponent field (no frexpf / ldexpf slow
+// paths).  amax < 2^-103 (or 0) gives up = inv = 0: such weights are below
+// 2^-100 of the unit's largest p (= 1) and drop out.
+__device__ __forceinline__ void fixed_scale(uint32_t mb, float& up, float& inv) {
+    const int eb = int((mb >> 23) & 0xFFu);
+    up = eb < 24 ? 0.0f : __int_as_float((276 - eb) << 23);
+    inv = eb < 24 ? 0.0f : __int_as_float((eb - 22) << 23);
+}
+
+// Weight pre-pass of the MMA pass 2 (same table as v_weights): lane (quad qd,
+// group g) computes the 4 weights of its quad, the per-group exponent comes
+// from one REDUX max on the float bits (a >= 0, so the bit patterns order like
+// the values), and the three limb words are assembled with PRMT and stored as
+// one 16-byte row [limb0, limb1, limb2, 0] of the table.
+template <int D, int NCH>
+__device__ __forceinline__ void v_weights_quad(float& l, float (&bsum)[D / 64], const uint8_t* sb, const float* sc,
+                                               float M, int n, int lane, uint32_t* limbs, float (&inv)[D / 64]) {
+    using C = Cfg<D, NCH>;
+    constexpr int G = D / 64, Q = C::CH / 4;
+    static_assert(Q * G <= 32, "one (quad, group) per lane");
+    const int qd = lane % Q, g = lane / Q;
+    const bool act = g < G;
+    const float4 s4 = *reinterpret_cast<const float4*>(sc + 4 * qd);
+    const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+    float a[4], amax = 0.0f, ps = 0.0f, bs = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int t = 4 * qd + k;
+        const bool valid = act && t < n;
+        const float p = valid ? ex2(sv[k] - M) : 0.0f;
+        const float2 sm = __half22float2(*reinterpret_cast<const __half2*>(
+            sb + (t / kChunk) * C::CHB + C::OFF_M + (t % kChunk) * C::MB + 4 * (act ? g : 0)));
+        a[k] = valid ? p * sm.x : 0.0f;
+        bs = valid ? fmaf(p, sm.y, bs) : bs;
+        ps += p;
+        amax = fmaxf(amax, a[k]);
+    }
+    if (g == 0) l += ps;                      // p is counted once (lanes of group 1 repeat the quad)
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) if (g == gg) bsum[gg] += bs;
+    float up = 0.0f;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+        const uint32_t mb = __reduce_max_sync(0xffffffffu, (g == gg) ? __float_as_uint(amax) : 0u);
+        float u;
+        fixed_scale(mb, u, inv[gg]);
+        up = (g == gg) ? u : up;
+    }
+    if (act) {
+        const uint32_t q0 = uint32_t(__float2int_rn(a[0] * up)), q1 = uint32_t(__float2int_rn(a[1] * up));
+        const uint32_t q2 = uint32_t(__float2int_rn(a[2] * up)), q3 = uint32_t(__float2int_rn(a[3] * up));
+        const uint32_t l01 = __byte_perm(q0, q1, 0x5140), l23 = __byte_perm(q2, q3, 0x5140);   // bytes 0, 1
+        const uint32_t h01 = __byte_perm(q0, q1, 0x7362), h23 = __byte_perm(q2, q3, 0x7362);   // bytes 2, 3
+        *reinterpret_cast<uint4*>(limbs + (g * Q + qd) * 4) =
+            make_uint4(__byte_perm(l01, l23, 0x5410), __byte_perm(l01, l23, 0x7632), __byte_perm(h01, h23, 0x5410), 0u);
+    }
+    __syncwarp();
+}
+
+// The lane's fixed roles in pass 2 (computed once per kernel).
+template <int D>
+struct VLane {
+    int tab;          // word offset of the lane's B column (limb, group) in a stage's limb table
+    bool live;        // the lane's B column is used
+    int g0, g1;       // group of the weights in C columns 2j, 2j+1 (-1: unused column)
+    float w0, w1;     // end-of-unit limb weights of those columns (0: other group / unused)
+    int gr;           // group of the lane row's output columns
+};
+template <int D, int NCH>
+__device__ __forceinline__ VLane<D> v_lane(int lane) {
+    constexpr int Q = Cfg<D, NCH>::CH / 4, PPL = D / 16;
+    const int r = lane >> 2, j = lane & 3;
+    VLane<D> v;
+    int limb, grp, l0, l1;
+    col_role<D>(r, limb, grp);
+    v.live = grp >= 0;
+    v.tab = v.live ? grp * Q * 4 + limb : 0;
+    col_role<D>(2 * j, l0, v.g0);
+    col_role<D>(2 * j + 1, l1, v.g1);
+    v.gr = (2 * PPL * r) / 64;
+    v.w0 = (v.g0 == v.gr) ? float(1 << (8 * l0)) : 0.0f;
+    v.w1 = (v.g1 == v.gr) ? float(1 << (8 * l1)) : 0.0f;
+    return v;
+}
+
+template <int D, int NCH>
+__device__ __forceinline__ void v_stage_mma(VAccM<D>& va, const VLane<D>& vl, const uint8_t* sb, const float* sc,
+                                            float M, int n, int lane, uint32_t* limbs) {
+    using C = Cfg<D, NCH>;
+    constexpr int G = D / 64, PPL = D / 16;
+    float inv[G];
+    v_weights_quad<D, NCH>(va.l, va.bsum, sb, sc, M, n, lane, limbs, inv);
+    const int r = lane >> 2, j = lane & 3;
+    const uint32_t* lt = limbs + vl.tab;
+    int c[PPL][4];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[u][i] = 0;
+#pragma unroll
+    for (int s = 0; s < C::CH / 32; ++s) {
+        if (32 * s >= n) break;
+        const uint32_t b0 = vl.live ? lt[(8 * s + j) * 4] : 0u;
+        const uint32_t b1 = vl.live ? lt[(8 * s + 4 + j) * 4] : 0u;
+        const uint8_t* ch = sb + s * C::CHB;      // quads 8s .. 8s + 7 = chunk s
+        const uint8_t* wa = ch + (j * C::CB + PPL * r) * 4;
+        const uint8_t* wb = ch + ((4 + j) * C::CB + PPL * r) * 4;
+        uint32_t xa[PPL], xb[PPL];
+#pragma unroll
+        for (int h = 0; h < PPL / 4; ++h) {
+            const uint4 ua = lds128(wa + 16 * h), ub = lds128(wb + 16 * h);
+            xa[4 * h] = ua.x; xa[4 * h + 1] = ua.y; xa[4 * h + 2] = ua.z; xa[4 * h + 3] = ua.w;
+            xb[4 * h] = ub.x; xb[4 * h + 1] = ub.y; xb[4 * h + 2] = ub.z; xb[4 * h + 3] = ub.w;
+        }
+#pragma unroll
+        for (int u = 0; u < PPL; ++u)
+            mma_u8u8(c[u], xa[u] & 0x0F0F0F0Fu, xa[u] & 0xF0F0F0F0u, xb[u] & 0x0F0F0F0Fu, xb[u] & 0xF0F0F0F0u, b0,
+                     b1);
+    }
+    // flush: C column n = 2j + {0, 1} holds weights of group g0 / g1
+    const float i0 = vl.g0 < 0 ? 0.0f : (vl.g0 == 0 ? inv[0] : inv[G - 1]);
+    const float i1 = vl.g1 < 0 ? 0.0f : (vl.g1 == 0 ? inv[0] : inv[G - 1]);
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+        va.acc[u][0] = fmaf(float(c[u][0]), i0, va.acc[u][0]);
+        va.acc[u][1] = fmaf(float(c[u][1]), i1, va.acc[u][1]);
+        va.acc[u][2] = fmaf(float(c[u][2]), i0, va.acc[u][2]);
+        va.acc[u][3] = fmaf(float(c[u][3]), i1, va.acc[u][3]);
+    }
+    __syncwarp();   // limb table reuse by the next stage
+}
+
+// End of a unit (MMA pass 2): combine limbs / nibble positions, quad-reduce, add the
+// bias, normalise and write.  Lane (r, j) writes tiles u = j, j + 4, ... (columns
+// 2 (PPL r + u), +1).
+template <int D>
+__device__ __forceinline__ void v_finish_mma(VAccM<D>& va, const VLane<D>& vl, int lane, __half* out_bh, float& lsum,
+                                             float* v_part /* nullptr: normalise + write fp16 */) {
+    constexpr int G = D / 64, PPL = D / 16;
+    const int r = lane >> 2, j = lane & 3;
+    float b[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) b[g] = va.bsum[g];
+    float l = va.l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+        for (int g = 0; g < G; ++g) b[g] += __shfl_xor_sync(0xffffffffu, b[g], o);
+    }
+    lsum = l;
+    const float w0 = vl.w0, w1 = vl.w1;
+    const float bias = vl.gr == 0 ? b[0] : b[G - 1];
+    const float inv_l = 1.0f / l;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+        float ev = fmaf(va.acc[u][0], w0, va.acc[u][1] * w1);                    // column 2p
+        float od = fmaf(va.acc[u][2], w0, va.acc[u][3] * w1) * 0.0625f;         // column 2p+1 (16 c)
+        ev += __shfl_xor_sync(0xffffffffu, ev, 1);
+        od += __shfl_xor_sync(0xffffffffu, od, 1);
+        ev += __shfl_xor_sync(0xffffffffu, ev, 2);
+        od += __shfl_xor_sync(0xffffffffu, od, 2);
+        if ((u & 3) == j) {
+            const int col = 2 * (PPL * r + u);
+            ev += bias;
+            od += bias;
+            if (v_part) {
+                v_part[col] = ev;
+                v_part[col + 1] = od;
+            } else {
+                *reinterpret_cast<__half2*>(out_bh + col) = __floats2half2_rn(ev * inv_l, od * inv_l);
+            }
+        }
+    }
 }
 
 // End of a unit: remove the 16^k factors, reduce (acc, l, bsum) over the token

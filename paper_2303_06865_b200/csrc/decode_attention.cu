@@ -158,6 +158,9 @@ decode_attention_kernel(const Params P) {
     const int lc = tl * C::CB + sg * 16;  // lane's codes offset inside an iteration's rows
     const int lm = tl * C::MB + (sg >> 1) * 4;   // lane's meta (group of the segment) offset
     const uint32_t magic = magic_reg();
+#if FLEXQ_V_MMA
+    const VLane<D> vlane = v_lane<D, NCH>(lane);
+#endif
 
     int slot = 0;
     uint32_t parity = 0;
@@ -214,6 +217,28 @@ decode_attention_kernel(const Params P) {
 #endif
                 if (nst == 1) patch(sb, false);
             }
+#if FLEXQ_K_MMA
+            KFrag<D> kf;                      // the lane's q digits + epilogue weights for pass 1
+            load_q_mma<D>(sb + C::OFF_Q, P.qscale, lane, kf);
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int st = 0;;) {
+                const int t0 = st * C::CH;
+                const int n = min(C::CH, len - t0);
+                if (n == C::CH) {
+#pragma unroll
+                    for (int b = 0; b < C::CH / 16; ++b) k_block_mma<D, NCH>(b, kf, sb, scores, t0, C::CH, lane, mx);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < C::CH / 16; ++b)
+                        if (b * 16 < n) k_block_mma<D, NCH>(b, kf, sb, scores, t0, n, lane, mx);
+                }
+                release();
+                if (++st == nst) break;
+                sb = acquire();
+                if (owns_new && st == nst - 1) patch(sb, false);
+            }
+#else
             KQuery kq;                        // the lane's q for pass 1
             load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
@@ -236,6 +261,7 @@ decode_attention_kernel(const Params P) {
                 sb = acquire();
                 if (owns_new && st == nst - 1) patch(sb, false);
             }
+#endif
 #pragma unroll
             for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             M = mx;
@@ -244,6 +270,26 @@ decode_attention_kernel(const Params P) {
         // ------------------------------------------------ pass 2: P.V with p = 2^(s - M)
         // V codes are quad-interleaved (include/flexq.h): lanes own columns, IDP.4A over
         // 4 tokens at a time against per-stage fixed-point weights a_t = p_t scale_tg.
+#if FLEXQ_V_MMA
+        VAccM<D> va;
+        va.init();
+#pragma unroll 1
+        for (int st = 0; st < nst; ++st) {
+            const uint8_t* sb = acquire();
+            if (owns_new && st == nst - 1) patch(sb, true);
+            const int t0 = st * C::CH;
+            const int n = min(C::CH, len - t0);
+            v_stage_mma<D, NCH>(va, vlane, sb, scores + t0, M, n, lane, limbs);
+            release();
+        }
+
+        // ------------------------------------------------ end of unit: combine, reduce, write
+        float l;
+        if (P.nsplit == 1) {
+            v_finish_mma<D>(va, vlane, lane, P.out + int64_t(bh) * D, l, nullptr);
+        } else {
+            v_finish_mma<D>(va, vlane, lane, nullptr, l, P.part + int64_t(unit) * D);
+#else
         VAcc<D> va;
         va.init();
 #pragma unroll 1
@@ -265,6 +311,7 @@ decode_attention_kernel(const Params P) {
             float* dst = P.part + int64_t(unit) * D + col0;
 #pragma unroll
             for (int k = 0; k < D / 32; ++k) dst[k] = v[k];
+#endif
             if (lane == 0) P.ml[unit] = make_float2(M, l);
             __threadfence();
             __syncwarp();

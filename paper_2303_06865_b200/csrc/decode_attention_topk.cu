@@ -153,6 +153,27 @@ decode_attention_topk_kernel(const TopkParams P) {
         float M;
         {
             const uint8_t* sb = acquire();
+#if FLEXQ_K_MMA
+            KFrag<D> kf;                      // the lane's q digits + epilogue weights for pass 1
+            load_q_mma<D>(sb + C::OFF_Q, P.qscale, lane, kf);
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int st = 0;;) {
+                const int t0 = st * C::CH;
+                const int n = min(C::CH, n_tok - t0);
+                if (n == C::CH) {
+#pragma unroll
+                    for (int b = 0; b < C::CH / 16; ++b) k_block_mma<D, NCH>(b, kf, sb, scores, t0, C::CH, lane, mx);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < C::CH / 16; ++b)
+                        if (b * 16 < n) k_block_mma<D, NCH>(b, kf, sb, scores, t0, n, lane, mx);
+                }
+                release();
+                if (++st == nst) break;
+                sb = acquire();
+            }
+#else
             KQuery kq;
             load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
             float mx = -INFINITY;
@@ -174,6 +195,7 @@ decode_attention_topk_kernel(const TopkParams P) {
                 if (++st == nst) break;
                 sb = acquire();
             }
+#endif
 #pragma unroll
             for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             M = mx;   // the largest score is always kept, so M is the kept set's max
