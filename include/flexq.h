@@ -85,9 +85,11 @@ flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t
  * along D).  Codes: two codes per byte, column 2i in the low nibble
  * (S:520), and
  *   K: token-major -- byte i of the token's row at s*CB + i;
- *   V: quad-interleaved -- byte k of the 32-bit word at ((s/4)*CB + i)*4 is
- *      token 4*(s/4) + k's byte i (so one word holds 4 tokens of a column
- *      pair, the shape the PV integer dot product consumes).
+ *   V: quad-interleaved and swizzled -- byte k of the 32-bit word at
+ *      ((s/4)*CB + (i ^ (((s/4) & 3) << 3)))*4 is token 4*(s/4) + k's byte i
+ *      (one word holds 4 tokens of a column pair, the shape the P.V integer
+ *      matrix product consumes; the XOR spreads the four quads a tensor-core
+ *      fragment reads at once over distinct shared-memory banks).
  * The chunks of one head are contiguous, so the attention kernel streams any
  * run of them with one 1-D TMA bulk copy.  Tokens [T_cap, T_stride) are
  * padding the library never writes.

@@ -647,7 +647,7 @@ __device__ __forceinline__ void v_stage(VAcc<D>& va, const uint8_t* sb, const fl
 #pragma unroll 4
     for (int qd = 0; qd < Q; ++qd) {
         const uint4 lm = *reinterpret_cast<const uint4*>(lt + qd * 4);       // limbs 0..2 (+ pad)
-        const uint8_t* crow = sb + (qd / 8) * C::CHB + ((qd % 8) * C::CB + lane * W) * 4;
+        const uint8_t* crow = sb + (qd / 8) * C::CHB + ((qd % 8) * C::CB + ((lane * W) ^ ((qd & 3) << 3))) * 4;
         uint32_t wv[W];
         if constexpr (W == 2) {
             const uint2 x = *reinterpret_cast<const uint2*>(crow);
@@ -799,6 +799,7 @@ struct VLane {
     int g0, g1;       // group of the weights in C columns 2j, 2j+1 (-1: unused column)
     float w0, w1;     // end-of-unit limb weights of those columns (0: other group / unused)
     int gr;           // group of the lane row's output columns
+    int hx;           // D = 128: byte XOR of the half-block order (16 for odd rows)
 };
 template <int D, int NCH>
 __device__ __forceinline__ VLane<D> v_lane(int lane) {
@@ -814,6 +815,7 @@ __device__ __forceinline__ VLane<D> v_lane(int lane) {
     v.gr = (2 * PPL * r) / 64;
     v.w0 = (v.g0 == v.gr) ? float(1 << (8 * l0)) : 0.0f;
     v.w1 = (v.g1 == v.gr) ? float(1 << (8 * l1)) : 0.0f;
+    v.hx = (D == 128 && (r & 1)) ? 16 : 0;
     return v;
 }
 
@@ -837,12 +839,18 @@ __device__ __forceinline__ void v_stage_mma(VAccM<D>& va, const VLane<D>& vl, co
         const uint32_t b0 = vl.live ? lt[(8 * s + j) * 4] : 0u;
         const uint32_t b1 = vl.live ? lt[(8 * s + 4 + j) * 4] : 0u;
         const uint8_t* ch = sb + s * C::CHB;      // quads 8s .. 8s + 7 = chunk s
-        const uint8_t* wa = ch + (j * C::CB + PPL * r) * 4;
-        const uint8_t* wb = ch + ((4 + j) * C::CB + PPL * r) * 4;
+        // the swizzled layout puts pair p of quad q at p ^ ((q & 3) << 3): quads j and 4 + j
+        // share the swizzle j.  D = 128: the lane's 8 pairs (two 16-B halves) start at
+        // 8 (r ^ j); odd rows read their upper half first (vl.hx = 16) so the 8 lanes of an
+        // LDS.128 phase hit 8 distinct 16-B bank groups.  D = 64: 4 pairs at 4 (r ^ 2j).
+        const int blk = D == 128 ? PPL * (r ^ j) : PPL * (r ^ (2 * j));
+        const uint8_t* wa = ch + (j * C::CB + blk) * 4;
+        const uint8_t* wb = ch + ((4 + j) * C::CB + blk) * 4;
         uint32_t xa[PPL], xb[PPL];
 #pragma unroll
         for (int h = 0; h < PPL / 4; ++h) {
-            const uint4 ua = lds128(wa + 16 * h), ub = lds128(wb + 16 * h);
+            const int off = (16 * h) ^ vl.hx;
+            const uint4 ua = lds128(wa + off), ub = lds128(wb + off);
             xa[4 * h] = ua.x; xa[4 * h + 1] = ua.y; xa[4 * h + 2] = ua.z; xa[4 * h + 3] = ua.w;
             xb[4 * h] = ub.x; xb[4 * h + 1] = ub.y; xb[4 * h + 2] = ub.z; xb[4 * h + 3] = ub.w;
         }
@@ -895,7 +903,7 @@ __device__ __forceinline__ void v_finish_mma(VAccM<D>& va, const VLane<D>& vl, i
         ev += __shfl_xor_sync(0xffffffffu, ev, 2);
         od += __shfl_xor_sync(0xffffffffu, od, 2);
         if ((u & 3) == j) {
-            const int col = 2 * (PPL * r + u);
+            const int col = 2 * (PPL * r + (u ^ (vl.hx >> 2)));   // tile u holds pair PPL r + (u ^ 4) on odd rows (D = 128)
             ev += bias;
             od += bias;
             if (v_part) {
@@ -1055,7 +1063,7 @@ __device__ __forceinline__ void store_token(const TokenQ& t, int slot, uint8_t* 
         else
             *reinterpret_cast<uint16_t*>(chunk + off) = uint16_t(t.codes);
     } else {
-        uint8_t* p = chunk + ((slot >> 2) * CB + l16 * (EL / 2)) * 4 + (slot & 3);
+        uint8_t* p = chunk + ((slot >> 2) * CB + ((l16 * (EL / 2)) ^ (((slot >> 2) & 3) << 3))) * 4 + (slot & 3);
 #pragma unroll
         for (int i = 0; i < EL / 2; ++i) p[4 * i] = uint8_t(t.codes >> (8 * i));
     }

@@ -265,13 +265,19 @@ decode_attention_topk_kernel(const TopkParams P) {
         float l = 0.0f, bsum = 0.0f;
         const uint8_t* vbase = P.vc + int64_t(bh) * P.chunks * C::CHB;
         // V codes are quad-interleaved (include/flexq.h): token t's 16 B segment sg
-        // (column pairs 16 sg .. 16 sg + 15) is byte t % 4 of 16 consecutive words
-        // of its quad row; load the 64 B and gather that byte with PRMT.
+        // (column pairs 16 sg .. 16 sg + 15) is byte t % 4 of 16 words of its quad
+        // row (two swizzled 8-pair blocks); load the 64 B and gather that byte with PRMT.
         auto load_row = [&](int t, uint4 (&raw)[4], uint32_t& meta) {
             const uint8_t* cb = vbase + (t >> 5) * C::CHB;
-            const uint8_t* q = cb + ((((t & 31) >> 2) * C::CB) + 16 * sg) * 4;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) raw[i] = ldg_nc128(q + 16 * i);
+            const int quad = (t & 31) >> 2;
+            const uint8_t* q = cb + quad * C::CB * 4;
+            // swizzled layout: 8-pair block b of the quad row sits at block b ^ (quad & 3)
+            const uint8_t* b0 = q + ((2 * sg) ^ (quad & 3)) * 32;
+            const uint8_t* b1 = q + ((2 * sg + 1) ^ (quad & 3)) * 32;
+            raw[0] = ldg_nc128(b0);
+            raw[1] = ldg_nc128(b0 + 16);
+            raw[2] = ldg_nc128(b1);
+            raw[3] = ldg_nc128(b1 + 16);
             meta = ldg_nc32(cb + C::OFF_M + (t & 31) * C::MB + (sg >> 1) * 4);
         };
         auto row_bytes = [&](int t, const uint4 (&raw)[4]) -> uint4 {

@@ -79,16 +79,17 @@ struct KvChunkDst {
         const int64_t base = chunk * (kChunk * (cb + mb));                // kv_chunk_bytes(2 cb)
         if (kv == 0)
             codes_off = base + slot * cb + k * (kGroup / 2);
-        else
-            codes_off = base + ((slot >> 2) * cb + k * (kGroup / 2)) * 4 + (slot & 3);
+        else   // word (quad, first pair of group k), plus the token's byte lane; + the quad's swizzle
+            codes_off = (base + ((slot >> 2) * cb + k * (kGroup / 2)) * 4 + (slot & 3)) * 4 + ((slot >> 2) & 3);
         meta_off = base + kChunk * cb + slot * mb + k * 4;
     }
     __device__ __forceinline__ void store_codes(uint8_t* base, int64_t co, int part, int kv, uint32_t lo,
                                                 uint32_t hi) const {
         if (kv == 0) {
             *reinterpret_cast<uint2*>(base + co + part * 8) = make_uint2(lo, hi);
-        } else {   // V: byte i (column pair part*8 + i of the group) -> word (quad, pair), byte t % 4
-            uint8_t* p = base + co + part * 32;
+        } else {   // V: byte i (column pair part*8 + i of the group) -> word (quad, pair ^ (swz << 3)), byte t % 4
+            const int swz = int(co & 3);   // V offsets carry the swizzle (quad & 3) in 2 low bits (operator())
+            uint8_t* p = base + (co >> 2) + (part ^ swz) * 32;
 #pragma unroll
             for (int i = 0; i < 4; ++i) p[4 * i] = uint8_t(lo >> (8 * i));
 #pragma unroll

@@ -159,9 +159,14 @@ class KVCache:
 
     def v_codes(self):
         """V codes as token-major rows.  In memory each chunk's V codes are
-        quad-interleaved: word (quad, column pair) holds token 4 quad + k in byte k."""
+        quad-interleaved and swizzled: word (quad, column pair i ^ ((quad & 3) << 3)) holds
+        token 4 quad + k in byte k (include/flexq.h)."""
         B, H, NC, cb = self.batch, self.heads, self.chunks, self.head_dim // 2
         x = self.v[..., :CHUNK * cb].reshape(B, H, NC, CHUNK // 4, cb, 4)
+        quad = torch.arange(CHUNK // 4, device=x.device).view(-1, 1)
+        pair = torch.arange(cb, device=x.device).view(1, -1)
+        src = pair ^ ((quad & 3) << 3)                                  # [quad][logical pair] -> stored pair
+        x = torch.gather(x, 4, src.view(1, 1, 1, CHUNK // 4, cb, 1).expand(B, H, NC, CHUNK // 4, cb, 4))
         return x.permute(0, 1, 2, 3, 5, 4).reshape(B, H, NC * CHUNK, cb)
 
     def k_meta(self):
