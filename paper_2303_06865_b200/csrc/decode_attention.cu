@@ -54,7 +54,8 @@ namespace {
 
 constexpr int kMaxSplitUnits = 8192;   // partial slots in the workspace
 constexpr int kMinSplitTokens = 128;  // smallest context split (two 64-token stages)
-constexpr int kUnitsPerWarp = 3;       // split (b, h) units until each resident warp gets ~3
+constexpr int kUnitsPerWarp = 0;       // occupancy splits off by default (B200 sweep):
+                                       // split only where a context exceeds the score buffer
 constexpr int kMinUnitTokens = 512;    // smallest per-warp score buffer of any variant (sizes the workspace)
 
 // UNR: unroll factor of the full-stage loops (code size vs. scheduling freedom:
@@ -379,6 +380,17 @@ int ctas_per_sm() {
     return occ;
 }
 
+// Split target in units per resident warp (FLEXQ_UNITS_PER_WARP overrides, tuning only).
+int units_per_warp() {
+    static int u = -1;
+    if (u < 0) {
+        const char* e = getenv("FLEXQ_UNITS_PER_WARP");
+        u = e ? atoi(e) : kUnitsPerWarp;
+        if (u < 0) u = 0;   // 0: split only where the score buffer forces it
+    }
+    return u;
+}
+
 struct WsLayout {
     size_t ctrl, tickets, part, ml, total;
 };
@@ -405,15 +417,15 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int occ = ctas_per_sm<D, NCH, S, WPC, UNR, MAXT>();
     const int ctas_resident = sm_count() * occ;
     const int warps_resident = ctas_resident * WPC;
-    // context split: only when (b, h) units cannot fill the resident warps
     // context split: forced when a unit would exceed the score buffer; otherwise
-    // only when there are fewer than kUnitsPerWarp (b, h) units per resident warp
-    // (persistent warps pull units dynamically, so a few units each balance the
-    // tail), keeping >= kMinSplitTokens tokens per split.
+    // (FLEXQ_UNITS_PER_WARP = u > 0, tuning) when there are fewer than u (b, h)
+    // units per resident warp, keeping >= kMinSplitTokens tokens per split.  The
+    // B200 sweep found occupancy splits slower at every BASELINE shape (the
+    // partial write + merge costs more than the idle warps), so u = 0.
     const int min_split = (a.cur_len + MAXT - 1) / MAXT;
     int nsplit = min_split;
-    const int64_t target = int64_t(kUnitsPerWarp) * warps_resident;
-    if (int64_t(bh) * nsplit < target) {
+    const int64_t target = int64_t(units_per_warp()) * warps_resident;
+    if (target > 0 && int64_t(bh) * nsplit < target) {
         nsplit = int((target + bh - 1) / bh);
         const int max_by_len = (a.cur_len + kMinSplitTokens - 1) / kMinSplitTokens;
         nsplit = min(nsplit, max_by_len);
@@ -491,7 +503,10 @@ cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
             case FLEXQ_V(32, 4, 2, 4, 576): return launch<128, 1, 4, 2, 4, 576>(a, stream);
             case FLEXQ_V(64, 2, 2, 4, 576): return launch<128, 2, 2, 2, 4, 576>(a, stream);
             case FLEXQ_V(64, 2, 3, 4, 1088): return launch<128, 2, 2, 3, 4, 1088>(a, stream);
-            default: return launch<128, 2, 2, 3, 4, 576>(a, stream);
+            case FLEXQ_V(64, 2, 2, 4, 1088): return launch<128, 2, 2, 2, 4, 1088>(a, stream);
+            default:   // B200 sweep: 2 warps / CTA; score buffer sized to the context
+                return a.cur_len <= 576 ? launch<128, 2, 2, 2, 4, 576>(a, stream)
+                                        : launch<128, 2, 2, 2, 4, 1088>(a, stream);
         }
     }
     switch (v) {
