@@ -47,6 +47,12 @@
 #ifndef FLEXQ_AB_GSTORE
 #define FLEXQ_AB_GSTORE 1
 #endif
+#ifndef FLEXQ_AB_QUANT
+#define FLEXQ_AB_QUANT 1
+#endif
+#ifndef FLEXQ_AB_NEWCOPY
+#define FLEXQ_AB_NEWCOPY 1
+#endif
 #include "flexq_internal.h"
 
 namespace flexq {
@@ -136,7 +142,7 @@ decode_attention_kernel(const Params P) {
             const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
             const bool first = p_stage == 0;
             uint8_t* sb = ring + slot * C::STAGE;
-            const bool with_new = first && p_new;
+            const bool with_new = FLEXQ_AB_NEWCOPY && first && p_new;
             mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0) + (with_new ? 4 * D : 0));
             bulk_g2s(sb, (vpass ? p_v : p_k) + int64_t(si) * (NCH * C::CHB), bytes, &bars[slot], policy);
             if (first) bulk_g2s(sb + C::OFF_Q, p_q, 2 * D, &bars[slot], policy);
@@ -196,9 +202,29 @@ decode_attention_kernel(const Params P) {
         const int new_idx = (P.cur_len - 1) - first - (nst - 1) * C::CH;   // inside the last stage
         const int new_slot = (P.cur_len - 1) & (kChunk - 1);
         TokenQ tq{};                       // lanes 0-15: the K row, 16-31: the V row
+        // Patch the stage image, then write the patched bytes to the cache as whole
+        // 16-B pieces: the token's K code row (or, for V, the whole 4-token quad row
+        // the swizzled layout spreads it over) and the 32-B sector of the quad's
+        // metadata.  Rewriting neighbours' unchanged bytes is harmless (no other
+        // writer), and full-sector stores avoid partial-sector read-modify-writes.
         auto patch = [&](const uint8_t* sb, bool vpass) {
-            if (vpass == (lane >= 16))
-                store_token<D>(tq, new_slot, const_cast<uint8_t*>(sb) + (new_idx >> 5) * C::CHB, lane);
+            uint8_t* s_chunk = const_cast<uint8_t*>(sb) + (new_idx >> 5) * C::CHB;
+            if (vpass == (lane >= 16)) store_token<D>(tq, new_slot, s_chunk, lane);
+            __syncwarp();
+#if FLEXQ_AB_GSTORE
+            fence_proxy_async();   // the patch (generic writes) before the TMA store reads it
+            __syncwarp();
+            if (lane == 0) {
+                uint8_t* g_chunk = (vpass ? P.vc_w : P.kc_w) +
+                                   (int64_t(bh) * P.chunks + ((P.cur_len - 1) >> 5)) * C::CHB;
+                const int rows = vpass ? (new_slot >> 2) * 4 * C::CB : new_slot * C::CB;   // byte offset
+                const int moff = C::OFF_M + (new_slot & ~3) * C::MB;                     // quad's meta
+                bulk_s2g(g_chunk + rows, s_chunk + rows, vpass ? 4 * C::CB : C::CB);
+                bulk_s2g(g_chunk + moff, s_chunk + moff, 4 * C::MB);
+                bulk_commit();
+                bulk_wait_read0();   // the slot is refilled after release
+            }
+#endif
 #if FLEXQ_AB_FENCE
             fence_proxy_async();   // generic smem writes before the slot's next bulk copy
 #endif
@@ -210,11 +236,8 @@ decode_attention_kernel(const Params P) {
         {
             const uint8_t* sb = acquire();
             if (owns_new) {
+#if FLEXQ_AB_QUANT
                 tq = quantize_kv_token<D>(sb + C::OFF_NEW, lane);
-#if FLEXQ_AB_GSTORE
-                uint8_t* gchunk = (lane < 16 ? P.kc_w : P.vc_w) +
-                                  (int64_t(bh) * P.chunks + ((P.cur_len - 1) >> 5)) * C::CHB;
-                store_token<D>(tq, new_slot, gchunk, lane);
 #endif
                 if (nst == 1) patch(sb, false);
             }
