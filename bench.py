@@ -474,26 +474,37 @@ def run_flexq(args):
             codes = torch.empty(r, c // 2, dtype=torch.uint8, device=dev)
             meta = torch.empty(r, c // 64, 2, dtype=torch.float16, device=dev)
             y = torch.empty_like(x)
+            # each op as a CUDA graph of 10 launches (no host launch gaps inside the timing)
+            def graph_of(fn):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(10):
+                        fn()
+                return g
             with torch.cuda.stream(stream):
                 fq.flexq_quantize(x, codes, meta, stream=stream)
                 fq.flexq_dequantize(codes, meta, y, stream=stream)
-                tq, td = [], []
-                for _ in range(10):
+            torch.cuda.synchronize()
+            gq = graph_of(lambda: fq.flexq_quantize(x, codes, meta, stream=stream))
+            gd = graph_of(lambda: fq.flexq_dequantize(codes, meta, y, stream=stream))
+            tq, td = [], []
+            with torch.cuda.stream(stream):
+                for _ in range(5):
                     a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                     a0.record(stream)
-                    fq.flexq_quantize(x, codes, meta, stream=stream)
+                    gq.replay()
                     a1.record(stream)
-                    fq.flexq_dequantize(codes, meta, y, stream=stream)
+                    gd.replay()
                     a2.record(stream)
                     a2.synchronize()
-                    tq.append(a0.elapsed_time(a1))
-                    td.append(a1.elapsed_time(a2))
+                    tq.append(a0.elapsed_time(a1) / 10)
+                    td.append(a1.elapsed_time(a2) / 10)
             nb = r * c * 2 + r * c // 2 + r * c // 64 * 4
             sweep[f"{r}x{c}"] = {"quantize_us": round(statistics.median(tq) * 1e3, 1),
                                  "quantize_gbs": round(nb / (statistics.median(tq) * 1e-3) / 1e9, 1),
                                  "dequantize_us": round(statistics.median(td) * 1e3, 1),
                                  "dequantize_gbs": round(nb / (statistics.median(td) * 1e-3) / 1e9, 1)}
-            del x, codes, meta, y
+            del x, codes, meta, y, gq, gd
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     log("cpu baseline")
