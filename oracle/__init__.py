@@ -51,6 +51,7 @@ def lib():
         L.oracle_attention_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P]
         L.oracle_attention_f32.argtypes = [P] * 5 + [i32] * 7 + [P]
         L.oracle_attention_topk_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P, P, P]
+        L.oracle_dequant_gemm_f64.argtypes = [P, P, P, i64, i64, i64, i32, i32, P]
         _lib = L
     return _lib
 
@@ -176,3 +177,18 @@ def attention_topk_f64(q, k_cache, v_cache, cur_len: int, keep: int, group: int 
                                            group, keep, _p(sel_arr) if sel_arr is not None else None,
                                            _p(mask), _p(scores), _p(out)), "attention_topk_f64")
     return out, mask, scores
+
+
+def dequant_gemm_f64(x, codes, meta, bits: int = 4, group: int = 64) -> np.ndarray:
+    """Decode linear layer over a quantized weight.
+    x: fp16 [M][K]; codes u8 [K][N] unpacked; meta u16 [K][N/group][2] -> float64 [M][N]."""
+    x = _h(x)
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    meta = _h(meta)
+    M, K = x.shape
+    K2, N = codes.shape
+    assert K2 == K
+    out = np.zeros((M, N), np.float64)
+    _check(lib().oracle_dequant_gemm_f64(_p(x), _p(codes), _p(meta), M, K, N, bits, group, _p(out)),
+           "dequant_gemm_f64")
+    return out

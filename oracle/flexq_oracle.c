@@ -27,6 +27,8 @@
  *   O8  decode attention softmax(q K^T / sqrt(D)) V over the dequantized cache
  *         (P:271-274), K^ and V^ = fmaf(code, scale, min) in fp32   (reading M)
  *   A4  KV update x_K <- Concat(x_K, t w_K): append quantized rows
+ *   G1  decode linear layer y = t . w^ over a 4-bit weight grouped along the
+ *         output channel, w^ = O7 fp16 (NEXT-2)
  *
  * Parity pins: see tests/test_oracle_*.py (each function is pinned there to
  * something other than itself: exact rational arithmetic, brute-force search,
@@ -375,5 +377,46 @@ int oracle_attention_topk_f64(const uint16_t *q, const uint8_t *k_codes, const u
         }
     free(s);
     free(kept);
+    return OK;
+}
+
+/* ------------------------------------------------------------------ G1 */
+/* Decode-step linear layer over a group-wise 4-bit weight:
+ * y = t . w with w in R^{h1 x h2}, stored quantized
+ * ("compress both [weights and KV cache] to 4 bits with a group
+ * size of 64"), grouped "along the output channel dimension" (reading
+ * J: contiguous groups along the last axis of the [in][out] matrix), and
+ * "converted back to FP16 before computation": the operand is
+ * O7's fp16 value, exactly what oracle_dequantize returns.
+ *
+ *   x     fp16 [M][K]            (M = batch b, K = in features)
+ *   codes u8   [K][N] unpacked   (N = out features)
+ *   meta  u16  [K][N/group][2]   ({scale, min} fp16 bit patterns)
+ *   out   f64  [M][N] = sum_k x[m][k] * w^[k][n], summed in double, k ascending.
+ * The plain definition of a matrix product (no blocking, no reordering). */
+int oracle_dequant_gemm_f64(const uint16_t *x, const uint8_t *codes, const uint16_t *meta,
+                            int64_t M, int64_t K, int64_t N, int bits, int group, double *out)
+{
+    if (M < 0 || K < 0 || N < 0 || bits < 1 || bits > 8 || group < 1) return ERR_ARG;
+    if (N % group != 0) return ERR_UNSUPPORTED;
+    int64_t ng = N / group;
+    /* O7 per weight element, then the product. */
+    double *w = (double *)malloc(sizeof(double) * (size_t)(K * N > 0 ? K * N : 1));
+    if (!w) return ERR_ARG;
+    for (int64_t k = 0; k < K; ++k)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t mo = (k * ng + n / group) * 2;
+            float v = dequant_f32(codes[k * N + n], meta[mo], meta[mo + 1]);
+            v = fminf(fmaxf(v, -65504.0f), 65504.0f);
+            w[k * N + n] = (double)oracle_f16_to_f32(oracle_f32_to_f16(v));
+        }
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k)
+                acc += (double)oracle_f16_to_f32(x[m * K + k]) * w[k * N + n];
+            out[m * N + n] = acc;
+        }
+    free(w);
     return OK;
 }
