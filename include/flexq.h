@@ -164,6 +164,42 @@ flexq_status flexq_decode_attention_topk(const void *q_f16, const void *k_cache,
                                          void *sel_i32, void *workspace, size_t workspace_bytes,
                                          void *stream);
 
+/* Decode-step linear layer over a group-wise 4-bit weight:
+ *   y[m][n] = sum_k x[m][k] * w^[k][n],   y = t . w,
+ * w in R^{h1 x h2} row-major [k][n], quantized by flexq_quantize with groups of group_size
+ * contiguous elements along the output channel n (reading J), and "converted back to
+ * FP16 before computation" inside the kernel: w^ = min(RN16(c*scale + min),
+ * 65504), one fp16 FMA -- equal to flexq_dequantize's output except where RN32 of the exact
+ * value lands on an fp16 tie (reading G2; at most 1 fp16 ulp).  Products are
+ * exact and accumulate in fp32 on the tensor cores; y is rounded once to fp16.
+ *
+ * Built: bits = 4, group_size = 64, n % 256 == 0, k % 64 == 0 (else FLEXQ_ERR_UNSUPPORTED).
+ *
+ * flexq_pack_weight: one-time re-layout (no arithmetic) of flexq_quantize's output for a
+ * [k][n] weight -- codes_u8 u8 [k][n/2], meta_h2 half2 [k][n/group_size] -- into
+ * flexq_gemm_panel_bytes(k, n) bytes of "panels" (one 9 KB panel per 256 columns x 64 k:
+ * codes column-major along k, then that block's (scale, min) pairs), the operand format of
+ * flexq_dequant_gemm.  Same total size as codes + meta.  Writes only `panels`.
+ *
+ * flexq_dequant_gemm:
+ *   x_f16   fp16 [m][k] row-major (m = decode batch b, k = in features); any m >= 1
+ *           (rows are processed 160 at a time)
+ *   panels  flexq_pack_weight's output for the [k][n] weight
+ *   y_f16   fp16 [m][n] row-major; every element is written.
+ *   m == 0 or n == 0: FLEXQ_OK, nothing written; k == 0: FLEXQ_ERR_UNSUPPORTED.
+ *   workspace: >= flexq_dequant_gemm_workspace_size(...) bytes, 16-byte aligned, ZEROED by
+ *   the caller before its first use.  It holds per-tile tickets (first n/256 * 4 bytes,
+ *   rounded up to 256) and split-k fp32 partial sums (scratch); every call leaves the
+ *   tickets zero again, so the workspace may be reused across calls on one stream but not
+ *   shared by calls that can run concurrently. */
+size_t flexq_gemm_panel_bytes(int64_t k, int64_t n, int bits, int group_size);
+flexq_status flexq_pack_weight(const void *codes_u8, const void *meta_h2, int64_t k, int64_t n, int bits,
+                               int group_size, void *panels, void *stream);
+size_t flexq_dequant_gemm_workspace_size(int64_t m, int64_t k, int64_t n, int bits, int group_size);
+flexq_status flexq_dequant_gemm(const void *x_f16, const void *panels, int64_t m, int64_t k, int64_t n, int bits,
+                                int group_size, void *y_f16, void *workspace, size_t workspace_bytes,
+                                void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ SOURCES = {
     "quant.cu": ["-fmad=false", "-prec-div=true", "-ftz=false"],
     "decode_attention.cu": [],
     "decode_attention_topk.cu": [],
+    "dequant_gemm.cu": [],
 }
 
 
@@ -84,3 +85,6 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_MINB=5",), tag="topk5"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_K_MMA=0",), tag="kidp"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_V_MMA=0",), tag="vidp"))
+    if "--gemm-ab" in sys.argv:
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_L2PROMO=CU_TENSOR_MAP_L2_PROMOTION_NONE",),
+                    tag="promo0"))

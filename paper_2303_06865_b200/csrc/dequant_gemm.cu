@@ -1,0 +1,686 @@
+// dequant_gemm.cu -- decode-step linear layer over a group-wise 4-bit weight.
+//
+//   y[m][n] = sum_k x[m][k] * w^[k][n]          (t . w)
+// with the weight quantized by flexq_quantize -- codes u4 [K][N/2] and half2 {scale, min}
+// [K][N/64], groups of 64 "along the output channel dimension" (reading J) -- and
+// "converted back to FP16 before computation" inside the kernel:
+//   w^[k][n] = min(RN16(c * scale + min), 65504)   (one fp16 FMA; reading G2 in DESIGN.md)
+//
+// The decode batch (M = 144 at OPT-175B) is small against the weight (K x N = 12288 x
+// 49152), so the MMA is "swapped": the tensor core's M dimension runs over 128 weight
+// columns n, its N dimension over the batch rows m (<= 160), K over k:
+//
+//     D[n][m] (TMEM fp32) += A[n][k] (TMEM f16) * B[m][k] (smem f16, K-major, TMA SW128)
+//
+//   * A never touches shared memory.  flexq_pack_weight re-lays the quantized weight once
+//     into 9 KB "panels" (256 columns x 64 k: codes column-major along k + the (scale, min)
+//     pairs of those k), one contiguous bulk copy each.  Dequant warps own one TMEM lane
+//     (= one weight column n) each: two 16-byte shared loads give the lane's 64 codes, four
+//     LOP3/HADD2/HFMA2/HMNMX2 steps per 8 codes give 8 fp16 values already paired along k,
+//     and tcgen05.st writes them straight into the A operand columns.  (In the first,
+//     shared-memory-A version the dequant stores plus the MMA's A and B reads needed more
+//     than the 128 B/clk of shared-memory bandwidth.)
+//   * One elected thread issues tcgen05.mma (kind::f16, A from TMEM, M = 128, N = Mpad,
+//     K = 16) into two TMEM accumulators -- 256 weight columns per tile, so every x block
+//     fetched from L2 feeds two MMAs.
+//   * Schedule: data-parallel full tiles plus a split-k remainder (Sched below); a tile
+//     split along k writes fp32 partials to the workspace and the last of its contributors
+//     (ticket) sums them in contributor order -- deterministic -- and stores fp16.
+//
+// Warp roles (16 warps): 0 panel bulk copies, 1 MMA issuer, 2 x TMA, 3 TMEM allocator,
+// 4-7 epilogue (TMEM lanes 32*(w%4) ..), 8-15 dequant (lanes 32*(w%4) .., A half (w-8)/4).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "flexq_internal.h"
+
+namespace flexq {
+namespace {
+
+constexpr int kBN = kGemmTileN;        // 256 weight columns per tile (two 128-row A operands)
+constexpr int kBK = kGemmTileK;        // 64 k per stage (one 128-byte swizzle row of x)
+constexpr int kThreads = 512;
+constexpr int kPanelStages = 8;
+constexpr int kPanelCodes = kBN * kBK / 2;      // 8 KB: [k half (2)][column (256)][16 B = 32 codes]
+constexpr int kPanelBytes = kGemmPanelBytes;    // + 1 KB: [group (4)][k pair (32)][{scale pair, min pair}]
+constexpr int kAStages = 3;
+constexpr int kDequantWarps = 8;
+constexpr int kEpiWarps = 4;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAccStride = 160;            // accumulator h at TMEM column h * 160 (Mpad <= 160)
+constexpr uint32_t kACol = 320;                 // A stage s, half h at column 320 + 64 s + 32 h
+constexpr int kSmemLimit = 232448;              // 227 KB opt-in
+constexpr uint32_t kEpiScratch = kEpiWarps * 16 * 32 * 2;   // per warp: 16 rows (m) x 32 columns (n) fp16
+static_assert(kGemmMaxRows <= int(kAccStride), "two accumulators must fit below the A columns");
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory"); }
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((addr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            addr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(su32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, __half v) {
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(__half_as_ushort(v)) : "memory");
+}
+
+// ------------------------------------------------------------------ dequant
+// A panel code word holds 8 codes of one column for k0 .. k0+7 with nibble positions
+// (0, 4) = (k0, k0+1), (1, 5) = (k0+2, k0+3), (2, 6) = (k0+4, k0+5), (3, 7) = (k0+6, k0+7):
+// one shift and one LOP3 put a k pair into the mantissas of fp16 1024 + c (exact), HADD2
+// removes the 1024 (exact), HFMA2 applies the pair's (scale, min) with one rounding, and
+// HMNMX2 clamps at 65504 (reading R; c * scale + min >= min >= -65504 needs no lower clamp).
+// The result is the tcgen05 A column word for that k pair (low half = even k).
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t mp) {
+    uint32_t m;
+    asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));   // (t & mask) | magic
+    const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));                      // c (exact)
+    const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
+    return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));                                 // <= 65504
+}
+__device__ __forceinline__ void deq_word(uint32_t w, uint4 meta_lo, uint4 meta_hi, uint32_t* o) {
+    // meta_lo = {s01, m01, s23, m23}, meta_hi = {s45, m45, s67, m67}
+    o[0] = deq_pair(w, meta_lo.x, meta_lo.y);
+    o[1] = deq_pair(w >> 4, meta_lo.z, meta_lo.w);
+    o[2] = deq_pair(w >> 8, meta_hi.x, meta_hi.y);
+    o[3] = deq_pair(w >> 12, meta_hi.z, meta_hi.w);
+}
+
+// Store 16 rows (m0 .. m0+15) x 32 columns (n0 .. n0+31) of y from one warp: lane j holds
+// column n0 + j's 16 values; a per-warp smem transpose turns them into 16-byte row pieces.
+__device__ __forceinline__ void store_rows16(const float (&v)[16], uint32_t scratch, int lane, __half* y, int64_t ldy,
+                                             int m0, int M, int n0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sts16(scratch + uint32_t(i * 64 + lane * 2), __float2half_rn(v[i]));
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int j = lane + 32 * r, row = j >> 2, piece = j & 3;
+        const uint4 d = lds128(scratch + uint32_t(row * 64 + piece * 16));
+        if (m0 + row < M) *reinterpret_cast<uint4*>(y + int64_t(m0 + row) * ldy + n0 + piece * 8) = d;
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ work schedule
+// Data-parallel waves plus a split-k remainder.  CTA c owns the full tiles c, c + G, ...
+// (dp_waves of them).  The T mod G remainder tiles are cut along k into S parts of L
+// k-blocks; CTA c < R*S takes part c / R of remainder tile c % R -- FIRST, so that the
+// fixup by the last of the S contributors overlaps that CTA's data-parallel tiles.
+struct Sched {
+    int KB;          // k-blocks per tile
+    int G;           // CTAs
+    int dp_waves;    // full tiles per CTA
+    int R, S, L;     // remainder tiles, parts per remainder tile, k-blocks per part
+    __device__ __forceinline__ bool has_rem(int c) const { return c < R * S; }
+    __device__ __forceinline__ int units(int c) const { return dp_waves + (has_rem(c) ? 1 : 0); }
+    // unit u of CTA c -> tile, first k-block, k-block count, remainder part (-1: full tile)
+    __device__ __forceinline__ void unit(int c, int u, int& tile, int& kb0, int& nk, int& part) const {
+        if (has_rem(c) && u == 0) {
+            part = c / R;
+            tile = dp_waves * G + c % R;
+            kb0 = part * L;
+            nk = KB - kb0 < L ? KB - kb0 : L;
+        } else {
+            part = -1;
+            tile = (u - (has_rem(c) ? 1 : 0)) * G + c;
+            kb0 = 0;
+            nk = KB;
+        }
+    }
+};
+
+struct GemmParams {
+    const uint8_t* panels;   // [tiles][KB][9216 B]
+    __half* y;               // [M][N]
+    float* partials;         // [grid][256 (n)][mpad (m)]
+    uint32_t* tickets;       // [remainder tiles]
+    int M, N, mpad;
+    Sched sc;
+};
+
+struct Smem {
+    uint32_t panel, b, epi, bars, b_stages, total;
+};
+__host__ __device__ inline Smem smem_plan(int mpad) {
+    Smem s;
+    const uint32_t bstage = uint32_t(mpad) * 128u;
+    const uint32_t budget = uint32_t(kSmemLimit) - 1024u /* alignment slack */;
+    s.panel = 0;
+    s.b = s.panel + kPanelStages * kPanelBytes;      // 1024-aligned (8 * 9 KB)
+    const uint32_t fixed = s.b + kEpiScratch + 1024u /* bars */;
+    uint32_t bs = (budget - fixed) / bstage;
+    if (bs > 6) bs = 6;
+    s.b_stages = bs;
+    s.epi = s.b + bs * bstage;
+    s.bars = s.epi + kEpiScratch;
+    s.total = s.bars + 1024u + 1024u;
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
+    const Smem L = smem_plan(p.mpad);
+    const uint32_t s_panel = su32(smem + L.panel);
+    const uint32_t s_b = su32(smem + L.b);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* panel_full = bars;
+    uint64_t* panel_empty = panel_full + kPanelStages;
+    uint64_t* a_full = panel_empty + kPanelStages;
+    uint64_t* a_empty = a_full + kAStages;
+    uint64_t* b_full = a_empty + kAStages;
+    uint64_t* b_empty = b_full + 6;
+    uint64_t* tmem_full = b_empty + 6;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint32_t* epi_flag = tmem_slot + 1;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int BS = int(L.b_stages);
+    const uint32_t bstage = uint32_t(p.mpad) * 128u;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPanelStages; ++i) {
+            mbar_init(panel_full + i, 1);
+            mbar_init(panel_empty + i, kDequantWarps);
+        }
+        for (int i = 0; i < kAStages; ++i) {
+            mbar_init(a_full + i, kDequantWarps);
+            mbar_init(a_empty + i, 1);
+        }
+        for (int i = 0; i < BS; ++i) {
+            mbar_init(b_full + i, 1);
+            mbar_init(b_empty + i, 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, kEpiWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 3) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (warp == 2 && lane == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const Sched& S = p.sc;
+    const int c = blockIdx.x;
+    const int nunits = S.units(c);
+    const int KB = S.KB;
+
+    if (warp == 0) {
+        // ---------------- weight panels: one contiguous 9 KB bulk copy per (tile, k-block), evict-first
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int u = 0; u < nunits; ++u) {
+                int tile, kb0, nk, part;
+                S.unit(c, u, tile, kb0, nk, part);
+                const uint8_t* src = p.panels + (int64_t(tile) * KB + kb0) * kPanelBytes;
+                for (int j = 0; j < nk; ++j, src += kPanelBytes) {
+                    mbar_wait(panel_empty + s, ph ^ 1);
+                    mbar_expect_tx(panel_full + s, kPanelBytes);
+                    bulk_g2s(s_panel + uint32_t(s * kPanelBytes), src, kPanelBytes, panel_full + s, pol);
+                    if (++s == kPanelStages) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------- x producer (L2-resident, evict-last)
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int u = 0; u < nunits; ++u) {
+                int tile, kb0, nk, part;
+                S.unit(c, u, tile, kb0, nk, part);
+                for (int kb = kb0; kb < kb0 + nk; ++kb) {
+                    mbar_wait(b_empty + s, ph ^ 1);
+                    mbar_expect_tx(b_full + s, bstage);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s_b + uint32_t(s) * bstage),
+                        "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kBK), "r"(0), "r"(su32(b_full + s)),
+                        "l"(pol)
+                        : "memory");
+                    if (++s == BS) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4)                        // D fp32; A, B fp16, both K-major
+                                   | (uint32_t(p.mpad >> 3) << 17)  // N
+                                   | (uint32_t(128 >> 4) << 24);    // M
+            int as = 0, bs = 0;
+            uint32_t aph = 0, bph = 0;
+            for (int seg = 0; seg < nunits; ++seg) {
+                int tile, kb0, nk, part;
+                S.unit(c, seg, tile, kb0, nk, part);
+                mbar_wait(tmem_empty, (uint32_t(seg) & 1u) ^ 1u);
+                tc_fence_after();
+                for (int j = 0; j < nk; ++j) {
+                    mbar_wait(a_full + as, aph);
+                    mbar_wait(b_full + bs, bph);
+                    tc_fence_after();
+                    const uint32_t b0 = s_b + uint32_t(bs) * bstage;
+                    const uint32_t a0 = tmem_base + kACol + uint32_t(as) * 64u;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t bd = smem_desc(b0 + kk * 32, 16, 1024);
+                        const uint32_t accf = (j > 0 || kk > 0) ? 1u : 0u;
+                        umma_ts(tmem_base, a0 + kk * 8, bd, idesc, accf);
+                        umma_ts(tmem_base + kAccStride, a0 + 32 + kk * 8, bd, idesc, accf);
+                    }
+                    umma_commit(a_empty + as);
+                    umma_commit(b_empty + bs);
+                    if (++as == kAStages) { as = 0; aph ^= 1; }
+                    if (++bs == BS) { bs = 0; bph ^= 1; }
+                }
+                umma_commit(tmem_full);
+            }
+        }
+    } else if (warp >= 8) {
+        // ---------------- dequant warps: panel (smem) -> fp16 A operand (TMEM lane = weight column)
+        const int q = warp & 3, h = (warp - 8) >> 2;
+        const int nl = h * 128 + q * 32 + lane;             // column within the 256-column tile
+        const uint32_t codes_off = uint32_t(nl) * 16u;
+        const uint32_t meta_off = uint32_t(kPanelCodes) + uint32_t(nl >> 6) * 256u;
+        const uint32_t a_lane = tmem_base + (uint32_t(q * 32) << 16) + kACol + uint32_t(h) * 32u;
+        int total = 0;
+        for (int u = 0; u < nunits; ++u) {
+            int tile, kb0, nk, part;
+            S.unit(c, u, tile, kb0, nk, part);
+            total += nk;
+        }
+        int ps = 0, as = 0;
+        uint32_t pph = 0, aph = 0;
+        for (int it = 0; it < total; ++it) {
+            mbar_wait(panel_full + ps, pph);
+            const uint32_t pb = s_panel + uint32_t(ps * kPanelBytes);
+            const uint4 cw0 = lds128(pb + codes_off);            // k 0..31 of this column
+            const uint4 cw1 = lds128(pb + 4096u + codes_off);    // k 32..63
+            mbar_wait(a_empty + as, aph ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int hk = 0; hk < 2; ++hk) {
+                const uint4 cw = hk ? cw1 : cw0;
+                const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+                uint32_t o[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t mo = pb + meta_off + uint32_t((16 * hk + 4 * j) * 8);
+                    deq_word(words[j], lds128(mo), lds128(mo + 16), o + 4 * j);
+                }
+                tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(panel_empty + ps);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full + as);
+            if (++ps == kPanelStages) { ps = 0; pph ^= 1; }
+            if (++as == kAStages) { as = 0; aph ^= 1; }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> fp16 y (or fp32 partials + split-k fixup)
+        const int q = warp & 3;                 // TMEM lanes 32q .. 32q+31
+        const int nl = q * 32 + lane;           // column within a 128-column half
+        const uint32_t scratch = su32(smem + L.epi) + uint32_t(q * 1024);
+        const int mp = p.mpad;
+        for (int seg = 0; seg < nunits; ++seg) {
+            int tile, kb0, nk, part;
+            S.unit(c, seg, tile, kb0, nk, part);
+            const bool full = part < 0;
+            mbar_wait(tmem_full, uint32_t(seg) & 1u);
+            tc_fence_after();
+            float* slot = p.partials + int64_t(c) * mp * kBN;    // [256 n][mpad m]
+            for (int h = 0; h < 2; ++h) {
+                const int n0 = tile * kBN + h * 128 + q * 32;
+                for (int m0 = 0; m0 < mp; m0 += 16) {
+                    float v[16];
+                    tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(h) * kAccStride + uint32_t(m0), v);
+                    if (full) {
+                        store_rows16(v, scratch, lane, p.y, p.N, m0, p.M, n0);
+                    } else {
+                        float4* dst = reinterpret_cast<float4*>(slot + int64_t(h * 128 + nl) * mp + m0);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            __stcg(dst + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_empty);
+            if (!full) {
+                // Split-k fixup: the last of the tile's S contributors (CTAs r + R p) sums their
+                // partials in p order (deterministic) and stores fp16.
+                const int r = c % S.R;
+                __threadfence();
+                epi_bar();
+                if (q == 0 && lane == 0) {
+                    const uint32_t old = atomicAdd(p.tickets + r, 1u);
+                    const bool last = old == uint32_t(S.S - 1);
+                    if (last) p.tickets[r] = 0u;
+                    *epi_flag = last ? 1u : 0u;
+                }
+                epi_bar();
+                if (*epi_flag) {
+                    __threadfence();
+                    for (int h = 0; h < 2; ++h) {
+                        const int n0 = tile * kBN + h * 128 + q * 32;
+                        const int64_t col = int64_t(h * 128 + nl) * mp;
+                        for (int m0 = 0; m0 < mp; m0 += 16) {
+                            float v[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+                            for (int pp = 0; pp < S.S; pp += 2) {
+                                // two contributors per round: 8 independent 16-byte loads in flight
+                                float4 a[8];
+#pragma unroll
+                                for (int u = 0; u < 2; ++u) {
+                                    const int k = r + S.R * (pp + u < S.S ? pp + u : pp);
+                                    const float4* src =
+                                        reinterpret_cast<const float4*>(p.partials + int64_t(k) * mp * kBN + col + m0);
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) a[4 * u + i] = __ldcg(src + i);
+                                }
+#pragma unroll
+                                for (int u = 0; u < 2; ++u) {
+                                    if (pp + u >= S.S) break;
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) {
+                                        v[4 * i] += a[4 * u + i].x;
+                                        v[4 * i + 1] += a[4 * u + i].y;
+                                        v[4 * i + 2] += a[4 * u + i].z;
+                                        v[4 * i + 3] += a[4 * u + i].w;
+                                    }
+                                }
+                            }
+                            store_rows16(v, scratch, lane, p.y, p.N, m0, p.M, n0);
+                        }
+                    }
+                }
+                epi_bar();
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 3) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ weight panels
+// Pure re-layout of flexq_quantize's output (no arithmetic): panel (t, kb) holds columns
+// [256 t, 256 t + 256) and k [64 kb, 64 kb + 64):
+//   codes [hk (2)][column (256)][4 words]; word j of (hk, column) holds the codes of
+//     k = 32 hk + 8 j + {0..7} at nibble positions {0, 4, 1, 5, 2, 6, 3, 7}
+//   meta  [group (4)][k pair (32)][scale pair (half2), min pair (half2)].
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, uint8_t* __restrict__ panels, int64_t K,
+                                  int64_t N) {
+    const int64_t KB = K / kBK;
+    const int64_t total = (N / kBN) * KB * 2 * kBN;      // one thread per (panel, hk, column)
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int col = int(i % kBN);
+        const int hk = int((i / kBN) % 2);
+        const int64_t panel = i / (2 * kBN);
+        const int64_t tile = panel / KB, kb = panel % KB;
+        const int64_t n = tile * kBN + col;
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (int kl = 0; kl < 32; ++kl) {
+            const int64_t k = kb * kBK + hk * 32 + kl;
+            const uint32_t byte = codes[k * (N / 2) + n / 2];
+            const uint32_t c = (n & 1) ? (byte >> 4) : (byte & 15u);
+            const int j = kl >> 3, e = kl & 7;
+            const int pos = (e & 1) ? 4 + (e >> 1) : (e >> 1);
+            w[j] |= c << (4 * pos);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(panels + panel * kPanelBytes + hk * 4096 + col * 16);
+        *dst = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void pack_meta_kernel(const __half2* __restrict__ meta, uint8_t* __restrict__ panels, int64_t K,
+                                 int64_t N) {
+    const int64_t KB = K / kBK;
+    const int64_t G = N / kGroup;
+    const int64_t total = (N / kBN) * KB * 4 * 32;       // one thread per (panel, group, k pair)
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int kp = int(i % 32);
+        const int g = int((i / 32) % 4);
+        const int64_t panel = i / 128;
+        const int64_t tile = panel / KB, kb = panel % KB;
+        const int64_t gg = tile * 4 + g;
+        const int64_t k = kb * kBK + 2 * kp;
+        const __half2 a = meta[k * G + gg], b = meta[(k + 1) * G + gg];
+        const __half2 sp = __halves2half2(__low2half(a), __low2half(b));    // scales of k, k+1
+        const __half2 mp = __halves2half2(__high2half(a), __high2half(b));  // mins of k, k+1
+        uint2* dst = reinterpret_cast<uint2*>(panels + panel * kPanelBytes + kPanelCodes + (g * 32 + kp) * 8);
+        *dst = make_uint2(h2u(sp), h2u(mp));
+    }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(f);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+              uint64_t stride1_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
+              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+    EncodeTiled enc = encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {d0, d1};
+    const cuuint64_t strides[1] = {stride1_bytes};
+    const cuuint32_t box[2] = {b0, b1};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+               promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+inline int mpad_of(int64_t m) {
+    const int64_t r = m < kGemmMaxRows ? m : kGemmMaxRows;
+    return int((r + 15) / 16 * 16);
+}
+
+}  // namespace
+
+size_t gemm_panel_bytes(int64_t k, int64_t n) { return size_t(n / kBN) * size_t(k / kBK) * kPanelBytes; }
+
+cudaError_t launch_pack_weight(const void* codes, const void* meta, int64_t K, int64_t N, void* panels,
+                               cudaStream_t stream) {
+    const int blocks = sm_count() * 8;
+    pack_codes_kernel<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(codes), static_cast<uint8_t*>(panels),
+                                                  K, N);
+    pack_meta_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __half2*>(meta), static_cast<uint8_t*>(panels), K,
+                                                 N);
+    return cudaGetLastError();
+}
+
+// Host-only arithmetic (no CUDA call): one partial slot per CTA for at most kGemmMaxGrid CTAs.
+size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n) {
+    (void)k;
+    const int64_t tiles = n / kBN;
+    const size_t tickets = size_t((tiles * 4 + 255) / 256 * 256);
+    return tickets + size_t(kGemmMaxGrid) * size_t(mpad_of(m)) * kBN * sizeof(float);
+}
+
+cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, int64_t K, int64_t N, void* y,
+                                void* workspace, cudaStream_t stream) {
+    const int64_t tiles = N / kBN;
+    const int kb = int(K / kBK);
+    const int G = sm_count() < kGemmMaxGrid ? sm_count() : kGemmMaxGrid;
+    Sched sc;
+    sc.KB = kb;
+    sc.dp_waves = int(tiles / G);
+    sc.R = int(tiles % G);
+    sc.S = 1;
+    sc.L = kb;
+    if (sc.R > 0) {
+        int parts = G / sc.R;
+        if (parts > kb) parts = kb;
+        if (parts < 1) parts = 1;
+        sc.L = (kb + parts - 1) / parts;
+        sc.S = (kb + sc.L - 1) / sc.L;
+    }
+    sc.G = G;
+    const int grid = sc.dp_waves > 0 ? G : sc.R * sc.S;
+    const size_t tick_bytes = size_t((tiles * 4 + 255) / 256 * 256);
+    uint32_t* tickets = static_cast<uint32_t*>(workspace);
+    float* partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + tick_bytes);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(dequant_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    for (int64_t m0 = 0; m0 < M; m0 += kGemmMaxRows) {
+        const int mrows = int(M - m0 < kGemmMaxRows ? M - m0 : kGemmMaxRows);
+        const int mpad = (mrows + 15) / 16 * 16;
+        CUtensorMap mx;
+        if (!make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, static_cast<const __half*>(x) + m0 * K, uint64_t(K),
+                      uint64_t(mrows), uint64_t(K * 2), kBK, uint32_t(mpad), CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+        GemmParams p;
+        p.panels = static_cast<const uint8_t*>(panels);
+        p.y = static_cast<__half*>(y) + m0 * N;
+        p.partials = partials;
+        p.tickets = tickets;
+        p.M = mrows;
+        p.N = int(N);
+        p.mpad = mpad;
+        p.sc = sc;
+        const Smem L = smem_plan(mpad);
+        dequant_gemm_kernel<<<grid, kThreads, L.total, stream>>>(mx, p);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace flexq

@@ -176,4 +176,52 @@ flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache,
     return from_cuda(flexq::launch_decode_attention_topk(a, static_cast<cudaStream_t>(stream)));
 }
 
+// Shared checks for the decode linear layer's weight shape (NEXT-2).
+static flexq_status check_gemm_weight(int64_t k, int64_t n, int bits, int group_size) {
+    if (k < 0 || n < 0) return FLEXQ_ERR_ARG;
+    flexq_status s = check_bits_group(bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (n % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
+    if (k == 0 || n == 0) return FLEXQ_OK;
+    if (n % flexq::kGemmTileN != 0 || k % flexq::kGemmTileK != 0) return FLEXQ_ERR_UNSUPPORTED;
+    if (k > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return FLEXQ_ERR_ARG;
+    return FLEXQ_OK;
+}
+
+size_t flexq_gemm_panel_bytes(int64_t k, int64_t n, int bits, int group_size) {
+    if (check_gemm_weight(k, n, bits, group_size) != FLEXQ_OK) return 0;
+    return flexq::gemm_panel_bytes(k, n);
+}
+
+flexq_status flexq_pack_weight(const void* codes_u8, const void* meta_h2, int64_t k, int64_t n, int bits,
+                               int group_size, void* panels, void* stream) {
+    flexq_status s = check_gemm_weight(k, n, bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (k == 0 || n == 0) return FLEXQ_OK;
+    if (!codes_u8 || !meta_h2 || !panels) return FLEXQ_ERR_NULL;
+    if (!aligned16(codes_u8) || !aligned16(meta_h2) || !aligned16(panels)) return FLEXQ_ERR_ALIGN;
+    return from_cuda(flexq::launch_pack_weight(codes_u8, meta_h2, k, n, panels, static_cast<cudaStream_t>(stream)));
+}
+
+size_t flexq_dequant_gemm_workspace_size(int64_t m, int64_t k, int64_t n, int bits, int group_size) {
+    if (m < 1 || k < 1 || n < 1 || check_gemm_weight(k, n, bits, group_size) != FLEXQ_OK) return 0;
+    return flexq::dequant_gemm_workspace_bytes(m, k, n);
+}
+
+flexq_status flexq_dequant_gemm(const void* x_f16, const void* panels, int64_t m, int64_t k, int64_t n, int bits,
+                                int group_size, void* y_f16, void* workspace, size_t workspace_bytes, void* stream) {
+    if (m < 0) return FLEXQ_ERR_ARG;
+    flexq_status s = check_gemm_weight(k, n, bits, group_size);
+    if (s != FLEXQ_OK) return s;
+    if (m == 0 || n == 0) return FLEXQ_OK;
+    if (k == 0) return FLEXQ_ERR_UNSUPPORTED;     // an empty sum would need a zero fill, not built
+    if (m * n >= (int64_t(1) << 40)) return FLEXQ_ERR_ARG;
+    if (!x_f16 || !panels || !y_f16) return FLEXQ_ERR_NULL;
+    if (!aligned16(x_f16) || !aligned16(panels) || !aligned16(y_f16)) return FLEXQ_ERR_ALIGN;
+    if (!workspace || workspace_bytes < flexq::dequant_gemm_workspace_bytes(m, k, n)) return FLEXQ_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
+    return from_cuda(flexq::launch_dequant_gemm(x_f16, panels, m, k, n, y_f16, workspace,
+                                                static_cast<cudaStream_t>(stream)));
+}
+
 }  // extern "C"

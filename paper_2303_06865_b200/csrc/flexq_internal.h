@@ -59,4 +59,19 @@ struct TopkArgs {
 };
 cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream);
 
+// Decode linear layer over a 4-bit weight (NEXT-2, dequant_gemm.cu): y [M][N] = x [M][K] . w^ [K][N].
+// The quantized weight is re-laid out once into panels of 256 columns x 64 k (9 KB each);
+// rows are processed in chunks of kGemmMaxRows (the MMA N dimension); N % 256 == 0, K % 64 == 0.
+constexpr int kGemmMaxRows = 160;
+constexpr int kGemmTileN = 256;
+constexpr int kGemmTileK = 64;
+constexpr int kGemmPanelBytes = kGemmTileN * kGemmTileK / 2 + 4 * 32 * 8;   // 9216
+constexpr int kGemmMaxGrid = 160;   // persistent CTAs (one per SM, B200: 148)
+size_t gemm_panel_bytes(int64_t k, int64_t n);
+cudaError_t launch_pack_weight(const void* codes, const void* meta, int64_t k, int64_t n, void* panels,
+                               cudaStream_t stream);
+size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n);
+cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t m, int64_t k, int64_t n, void* y,
+                                void* workspace, cudaStream_t stream);
+
 }  // namespace flexq

@@ -53,8 +53,15 @@ def lib():
         L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 8 + [P, P, SZ, P]
         L.flexq_decode_attention_topk.argtypes = [P, P, P] + [I] * 9 + [P, P, P, SZ, P]
         L.flexq_append_decode_attention.argtypes = [P] * 5 + [I] * 8 + [P, P, SZ, P]
+        L.flexq_dequant_gemm_workspace_size.argtypes = [I64, I64, I64, I, I]
+        L.flexq_dequant_gemm_workspace_size.restype = SZ
+        L.flexq_dequant_gemm.argtypes = [P, P, I64, I64, I64, I, I, P, P, SZ, P]
+        L.flexq_gemm_panel_bytes.argtypes = [I64, I64, I, I]
+        L.flexq_gemm_panel_bytes.restype = SZ
+        L.flexq_pack_weight.argtypes = [P, P, I64, I64, I, I, P, P]
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
-                  "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention"):
+                  "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention",
+                  "flexq_dequant_gemm", "flexq_pack_weight"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -266,4 +273,46 @@ def flexq_decode_attention_topk(q: torch.Tensor, cache: KVCache, cur_len: int, k
                                              cur_len, keep, cache.bits, cache.group_size, out.data_ptr(),
                                              _ptr(sel), workspace.data_ptr(), workspace.numel(), _stream(stream)),
            "flexq_decode_attention_topk")
+    return out
+
+
+# ---------------------------------------------------------------- decode linear layer (NEXT-2)
+def flexq_gemm_panel_bytes(k: int, n: int, bits: int = BITS, group_size: int = GROUP) -> int:
+    return int(lib().flexq_gemm_panel_bytes(k, n, bits, group_size))
+
+
+def flexq_pack_weight(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: int = BITS, group_size: int = GROUP,
+                      stream=None) -> torch.Tensor:
+    """One-time re-layout of a quantized [k][n] weight (codes u8 [k][n/2], meta [k][n/g][2])
+    into the GEMM's panel format (u8, same total size)."""
+    k, half_n = codes.shape
+    n = half_n * 2
+    if out is None:
+        out = torch.empty(max(flexq_gemm_panel_bytes(k, n, bits, group_size), 16), dtype=torch.uint8,
+                          device=codes.device)
+    _check(lib().flexq_pack_weight(codes.data_ptr(), meta.data_ptr(), k, n, bits, group_size, out.data_ptr(),
+                                   _stream(stream)), "flexq_pack_weight")
+    return out
+
+
+def flexq_dequant_gemm_workspace_size(m: int, k: int, n: int, bits: int = BITS, group_size: int = GROUP) -> int:
+    return int(lib().flexq_dequant_gemm_workspace_size(m, k, n, bits, group_size))
+
+
+def make_gemm_workspace(m: int, k: int, n: int, device) -> torch.Tensor:
+    """Zeroed workspace for flexq_dequant_gemm (every call leaves its tickets zeroed)."""
+    return torch.zeros(max(flexq_dequant_gemm_workspace_size(m, k, n), 16), dtype=torch.uint8, device=device)
+
+
+def flexq_dequant_gemm(x: torch.Tensor, panels: torch.Tensor, n: int, out=None, workspace=None, bits: int = BITS,
+                       group_size: int = GROUP, stream=None) -> torch.Tensor:
+    """y fp16 [m][n] = x fp16 [m][k] . w^; panels = flexq_pack_weight(codes, meta)."""
+    _need(x, torch.float16, "x")
+    m, k = x.shape
+    if out is None:
+        out = torch.empty(m, n, dtype=torch.float16, device=x.device)
+    if workspace is None:
+        workspace = make_gemm_workspace(m, k, n, x.device)
+    _check(lib().flexq_dequant_gemm(x.data_ptr(), panels.data_ptr(), m, k, n, bits, group_size, out.data_ptr(),
+                                    workspace.data_ptr(), workspace.numel(), _stream(stream)), "flexq_dequant_gemm")
     return out

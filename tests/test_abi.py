@@ -137,3 +137,39 @@ def test_append_attention_validation(L):
     assert call(vn=U) == fq.FLEXQ_ERR_ALIGN
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
     assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
+
+
+def test_dequant_gemm_validation(L):
+    f = L.flexq_dequant_gemm
+    ws = L.flexq_dequant_gemm_workspace_size(144, 12288, 49152, 4, 64)
+    assert ws > 0
+    assert L.flexq_dequant_gemm_workspace_size(144, 12288, 49152, 4, 32) == 0
+    assert L.flexq_dequant_gemm_workspace_size(144, 100, 49152, 4, 64) == 0
+    # panels are a re-layout: exactly the bytes of codes + meta
+    assert L.flexq_gemm_panel_bytes(12288, 49152, 4, 64) == 12288 * 49152 // 2 + 12288 * 49152 // 64 * 4
+    assert L.flexq_gemm_panel_bytes(12288, 100, 4, 64) == 0
+
+    def call(m=144, k=12288, n=49152, x=A, pn=A, y=A, w=A, wb=ws, b=4, g=64):
+        return f(x, pn, m, k, n, b, g, y, w, wb, None)
+    assert call(m=-1) == fq.FLEXQ_ERR_ARG
+    assert call(k=-1) == fq.FLEXQ_ERR_ARG
+    assert call(b=9) == fq.FLEXQ_ERR_ARG
+    assert call(g=0) == fq.FLEXQ_ERR_ARG
+    assert call(b=3) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(g=128) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(n=100) == fq.FLEXQ_ERR_UNSUPPORTED      # partial group (reading I)
+    assert call(n=192) == fq.FLEXQ_ERR_UNSUPPORTED      # n % 256 != 0: not built
+    assert call(k=96) == fq.FLEXQ_ERR_UNSUPPORTED       # k % 64 != 0: not built
+    assert call(k=0) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(x=None) == fq.FLEXQ_ERR_NULL
+    assert call(pn=None) == fq.FLEXQ_ERR_NULL
+    assert call(y=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
+    assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
+    assert call(m=0, x=None, pn=None, y=None, w=None) == fq.FLEXQ_OK   # empty: no-op
+    pk = L.flexq_pack_weight
+    assert pk(A, A, 128, 100, 4, 64, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert pk(A, A, 128, 256, 4, 32, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert pk(A, None, 128, 256, 4, 64, A, None) == fq.FLEXQ_ERR_NULL
+    assert pk(A, A, 128, 256, 4, 64, U, None) == fq.FLEXQ_ERR_ALIGN
+    assert pk(A, A, 0, 256, 4, 64, None, None) == fq.FLEXQ_OK
