@@ -67,6 +67,14 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+def bf16_peak_tflops() -> float:
+    """Measured dense bf16 (= fp16) tensor peak, burst (MEASURED_PEAKS.json), else the guide's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["bf16_tflops"])
+    return 1590.0
+
+
 class ClockSampler:
     """NVML SM clock / throttle-reason sampling during the timed region."""
 
@@ -466,9 +474,10 @@ def run_flexq(args):
 
     # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
     log("sweep")
-    sweep = None
+    sweep = gemm = None
     if rank == 0 and not args.no_sweep:
-        sweep = {}
+        sweep, gemm = {}, {}
+        bf16_peak = bf16_peak_tflops()
         for (r, c) in ((12288, 49152), (12288, 12288)):
             x = synth.fill(seed, synth.tensor_id(0, synth.WEIGHT, c), (r, c), device=dev)
             codes = torch.empty(r, c // 2, dtype=torch.uint8, device=dev)
@@ -499,6 +508,45 @@ def run_flexq(args):
                     a2.synchronize()
                     tq.append(a0.elapsed_time(a1) / 10)
                     td.append(a1.elapsed_time(a2) / 10)
+            # NEXT-2: the decode linear layer y = t . w^ over this 4-bit weight at the decode batch
+            # (M = 144), through flexq_pack_weight + flexq_dequant_gemm (tcgen05 kernel),
+            # beside two library baselines: flexq_dequantize + cuBLAS, and cuBLAS on the fp16 weight.
+            M = 144
+            panels = fq.flexq_pack_weight(codes, meta)
+            xt = synth.fill(seed, synth.tensor_id(0, synth.WEIGHT, c + 1), (M, r), device=dev)
+            yt = torch.empty(M, c, dtype=torch.float16, device=dev)
+            wsg = fq.make_gemm_workspace(M, r, c, dev)
+            with torch.cuda.stream(stream):
+                fq.flexq_dequant_gemm(xt, panels, c, out=yt, workspace=wsg, stream=stream)
+                torch.matmul(xt, y, out=yt)
+            torch.cuda.synchronize()
+            gg = graph_of(lambda: fq.flexq_dequant_gemm(xt, panels, c, out=yt, workspace=wsg, stream=stream))
+            gb1 = graph_of(lambda: (fq.flexq_dequantize(codes, meta, y, stream=stream), torch.matmul(xt, y, out=yt)))
+            gb2 = graph_of(lambda: torch.matmul(xt, x, out=yt))
+            tg, tb1, tb2 = [], [], []
+            with torch.cuda.stream(stream):
+                for _ in range(5):
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    ev[0].record(stream)
+                    gg.replay()
+                    ev[1].record(stream)
+                    gb1.replay()
+                    ev[2].record(stream)
+                    gb2.replay()
+                    ev[3].record(stream)
+                    ev[3].synchronize()
+                    tg.append(ev[0].elapsed_time(ev[1]) / 10)
+                    tb1.append(ev[1].elapsed_time(ev[2]) / 10)
+                    tb2.append(ev[2].elapsed_time(ev[3]) / 10)
+            fl = 2.0 * M * r * c
+            tgm = statistics.median(tg) * 1e-3
+            gemm[f"{M}x{r}x{c}"] = {
+                "us": round(tgm * 1e6, 1), "tflops": round(fl / tgm / 1e12, 1),
+                "tensor_frac_of_measured_bf16": round(fl / tgm / 1e12 / bf16_peak, 4),
+                "weight_gbs": round((r * c // 2 + r * c // 64 * 4) / tgm / 1e9, 1),
+                "dequantize_then_cublas_us": round(statistics.median(tb1) * 1e3, 1),
+                "cublas_fp16_weight_us": round(statistics.median(tb2) * 1e3, 1)}
+            del panels, xt, yt, wsg, gg, gb1, gb2
             nb = r * c * 2 + r * c // 2 + r * c // 64 * 4
             sweep[f"{r}x{c}"] = {"quantize_us": round(statistics.median(tq) * 1e3, 1),
                                  "quantize_gbs": round(nb / (statistics.median(tq) * 1e-3) / 1e9, 1),
@@ -546,6 +594,7 @@ def run_flexq(args):
             "cpu_baseline": cpu,
             "weight_sweep": sweep,
             "topk_sparse": topk,
+            "dequant_gemm": gemm,
         }
         print(json.dumps(line), flush=True)
     if pg:

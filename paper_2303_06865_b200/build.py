@@ -86,5 +86,9 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_K_MMA=0",), tag="kidp"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_V_MMA=0",), tag="vidp"))
     if "--gemm-ab" in sys.argv:
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_L2PROMO=CU_TENSOR_MAP_L2_PROMOTION_NONE",),
-                    tag="promo0"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1",), tag="deqskip"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1", "FLEXQ_GEMM_NO_MMA=1"),
+                    tag="nomma"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_TRACE=1",), tag="trace"))
+

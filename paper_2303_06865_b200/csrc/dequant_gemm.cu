@@ -41,19 +41,41 @@ namespace {
 
 constexpr int kBN = kGemmTileN;        // 256 weight columns per tile (two 128-row A operands)
 constexpr int kBK = kGemmTileK;        // 64 k per stage (one 128-byte swizzle row of x)
-constexpr int kThreads = 512;
-constexpr int kPanelStages = 8;
+#ifndef FLEXQ_GEMM_DEQ_SKIP
+#define FLEXQ_GEMM_DEQ_SKIP 0   // tuning only: skip the dequant arithmetic (wrong results)
+#endif
+#ifndef FLEXQ_GEMM_DQW
+#define FLEXQ_GEMM_DQW 16
+#endif
+constexpr int kDequantWarps = FLEXQ_GEMM_DQW;   // 8: each warp converts all 64 k of its column;
+                                                // 16: two warps per column, one per 32-k half
+constexpr int kThreads = (8 + kDequantWarps) * 32;
+#ifndef FLEXQ_GEMM_PANEL_STAGES
+#define FLEXQ_GEMM_PANEL_STAGES 8
+#endif
+#ifndef FLEXQ_GEMM_TRACE
+#define FLEXQ_GEMM_TRACE 0      // tuning only: clock64 stamps of CTA 0's pipeline into the workspace
+#endif
+#define TRACE(slot, j) \
+    do { if (FLEXQ_GEMM_TRACE && blockIdx.x == 0 && (j) < 256) { \
+        long long t_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)); \
+        reinterpret_cast<long long*>(p.partials)[(slot) * 256 + (j)] = t_; } } while (0)
+#ifndef FLEXQ_GEMM_NO_MMA
+#define FLEXQ_GEMM_NO_MMA 0     // tuning only: stream panels and x without MMAs (wrong results)
+#endif
+constexpr int kPanelStages = FLEXQ_GEMM_PANEL_STAGES;
 constexpr int kPanelCodes = kBN * kBK / 2;      // 8 KB: [k half (2)][column (256)][16 B = 32 codes]
 constexpr int kPanelBytes = kGemmPanelBytes;    // + 1 KB: [group (4)][k pair (32)][{scale pair, min pair}]
-constexpr int kAStages = 3;
-constexpr int kDequantWarps = 8;
+constexpr int kMaxAStages = 6;                 // A operand stages in TMEM (64 columns each)
+constexpr int kBStages = 6;                    // x stages in smem
+constexpr int kDoneSlots = 6;                  // ring of commit barriers, one per group of stages
 constexpr int kEpiWarps = 4;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccStride = 160;            // accumulator h at TMEM column h * 160 (Mpad <= 160)
-constexpr uint32_t kACol = 320;                 // A stage s, half h at column 320 + 64 s + 32 h
+// TMEM columns: accumulator h at h * acc_stride (acc_stride = Mpad rounded up to 32), then
+// n_a A stages of 64 columns (half h of stage s at a_col + 64 s + 32 h).
 constexpr int kSmemLimit = 232448;              // 227 KB opt-in
 constexpr uint32_t kEpiScratch = kEpiWarps * 16 * 32 * 2;   // per warp: 16 rows (m) x 32 columns (n) fp16
-static_assert(kGemmMaxRows <= int(kAccStride), "two accumulators must fit below the A columns");
+static_assert(2 * ((kGemmMaxRows + 31) / 32 * 32) + 3 * 64 <= int(kTmemCols), "2 accumulators + 3 A stages");
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -100,6 +122,20 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                  : "memory");
 }
+// Polling wait with a sleep between polls, for roles that wait long (the epilogue waits a whole
+// tile): spinning try_wait loops compete with the MMA issuer's own barrier and UTCHMMA issue.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t ns) {
+    uint32_t ok = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     uint32_t r[16];
     asm volatile(
@@ -112,12 +148,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Issued by a whole, converged warp: elect.sync picks the one lane that issues.  (Issuing from
+// a lone lane makes ptxas wrap every tcgen05 op in an ELECT/BRA.U.ANY loop: ~45 cycles per
+// MMA against ~16 this way -- the issuing warp's latency chain bounds the MMA rate at small N.)
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
         "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(su32(bar))
         : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
@@ -186,6 +232,27 @@ __device__ __forceinline__ void store_rows16(const float (&v)[16], uint32_t scra
     __syncwarp();
 }
 
+// Ring position without divisions (the issuing thread's instruction count is on the critical path).
+struct Ring {
+    int slot = 0, n;
+    uint32_t phase = 0;
+    __device__ explicit Ring(int n_) : n(n_) {}
+    __device__ __forceinline__ void next() {
+        if (++slot == n) { slot = 0; phase ^= 1u; }
+    }
+};
+// Tracks which commit barrier covers a stage: stage groups of G consecutive stages, one
+// done[] slot per group, 6 slots.
+struct GroupRing {
+    int pos = 0, G;
+    Ring q{kDoneSlots};
+    __device__ explicit GroupRing(int g) : G(g) {}
+    __device__ __forceinline__ bool last_in_group() const { return pos == G - 1; }
+    __device__ __forceinline__ void next() {
+        if (++pos == G) { pos = 0; q.next(); }
+    }
+};
+
 // ------------------------------------------------------------------ work schedule
 // Data-parallel waves plus a split-k remainder.  CTA c owns the full tiles c, c + G, ...
 // (dp_waves of them).  The T mod G remainder tiles are cut along k into S parts of L
@@ -220,6 +287,11 @@ struct GemmParams {
     float* partials;         // [grid][256 (n)][mpad (m)]
     uint32_t* tickets;       // [remainder tiles]
     int M, N, mpad;
+    // Pipeline shape (host-chosen from Mpad): n_a A stages in TMEM, one tcgen05.commit per group
+    // of `group` stages (a commit costs the issuing thread ~250 cycles of tensor-pipe time, so
+    // small batches, whose accumulators leave room for 6 A stages, commit every 3 stages).
+    int n_a, group;
+    uint32_t acc_stride, a_col;
     Sched sc;
 };
 
@@ -233,8 +305,8 @@ __host__ __device__ inline Smem smem_plan(int mpad) {
     s.panel = 0;
     s.b = s.panel + kPanelStages * kPanelBytes;      // 1024-aligned (8 * 9 KB)
     const uint32_t fixed = s.b + kEpiScratch + 1024u /* bars */;
-    uint32_t bs = (budget - fixed) / bstage;
-    if (bs > 6) bs = 6;
+    (void)budget;
+    const uint32_t bs = kBStages;   // fixed-size plan: 8 * 9 KB + 6 * Mpad * 128 B + 4 KB + bars <= 227 KB
     s.b_stages = bs;
     s.epi = s.b + bs * bstage;
     s.bars = s.epi + kEpiScratch;
@@ -253,31 +325,27 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     uint64_t* panel_full = bars;
     uint64_t* panel_empty = panel_full + kPanelStages;
     uint64_t* a_full = panel_empty + kPanelStages;
-    uint64_t* a_empty = a_full + kAStages;
-    uint64_t* b_full = a_empty + kAStages;
-    uint64_t* b_empty = b_full + 6;
-    uint64_t* tmem_full = b_empty + 6;
+    uint64_t* b_full = a_full + kMaxAStages;
+    // done[q % 6] completes when the MMAs of stage group q (stages q*G .. q*G+G-1) have finished
+    // reading A (TMEM) and B (smem): one commit frees both rings for the whole group.
+    uint64_t* done = b_full + kBStages;
+    uint64_t* tmem_full = done + kDoneSlots;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
     uint32_t* epi_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int BS = int(L.b_stages);
     const uint32_t bstage = uint32_t(p.mpad) * 128u;
+    const int NA = p.n_a, GR = p.group;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPanelStages; ++i) {
             mbar_init(panel_full + i, 1);
             mbar_init(panel_empty + i, kDequantWarps);
         }
-        for (int i = 0; i < kAStages; ++i) {
-            mbar_init(a_full + i, kDequantWarps);
-            mbar_init(a_empty + i, 1);
-        }
-        for (int i = 0; i < BS; ++i) {
-            mbar_init(b_full + i, 1);
-            mbar_init(b_empty + i, 1);
-        }
+        for (int i = 0; i < kMaxAStages; ++i) mbar_init(a_full + i, kDequantWarps);
+        for (int i = 0; i < kBStages; ++i) mbar_init(b_full + i, 1);
+        for (int i = 0; i < kDoneSlots; ++i) mbar_init(done + i, 1);
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -322,13 +390,19 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
         // ---------------- x producer (L2-resident, evict-last)
         if (lane == 0) {
             const uint64_t pol = policy_evict_last();
-            int s = 0;
-            uint32_t ph = 0;
+            int g = 0;     // global stage index
+            Ring rb(kBStages);
+            GroupRing prev(GR);   // commit group of stage g - 6
             for (int u = 0; u < nunits; ++u) {
                 int tile, kb0, nk, part;
                 S.unit(c, u, tile, kb0, nk, part);
-                for (int kb = kb0; kb < kb0 + nk; ++kb) {
-                    mbar_wait(b_empty + s, ph ^ 1);
+                for (int kb = kb0; kb < kb0 + nk; ++kb, ++g) {
+                    const int s = rb.slot;
+                    if (g >= kBStages) {      // the slot's previous stage (g - 6) has been consumed
+                        mbar_wait(done + prev.q.slot, prev.q.phase);
+                        prev.next();
+                    }
+                    rb.next();
                     mbar_expect_tx(b_full + s, bstage);
                     asm volatile(
                         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
@@ -336,75 +410,111 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                         "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kBK), "r"(0), "r"(su32(b_full + s)),
                         "l"(pol)
                         : "memory");
-                    if (++s == BS) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
+        // ---------------- MMA issuer (the whole warp runs the loop; elect.sync issues)
+        {
             const uint32_t idesc = (1u << 4)                        // D fp32; A, B fp16, both K-major
                                    | (uint32_t(p.mpad >> 3) << 17)  // N
                                    | (uint32_t(128 >> 4) << 24);    // M
-            int as = 0, bs = 0;
-            uint32_t aph = 0, bph = 0;
+            // Lean issue loop (the single issuing thread's own instruction count bounds the MMA
+            // rate at small N): descriptors are a precomputed base plus an add on the start-address
+            // field (addr >> 4 < 2^14, so the add never carries into the next field).
+            const uint64_t bdesc0 = smem_desc(s_b, 16, 1024);
+            const uint32_t bstage16 = bstage >> 4;
+            Ring ra(NA), rb(kBStages);
+            GroupRing grp(GR);
             for (int seg = 0; seg < nunits; ++seg) {
                 int tile, kb0, nk, part;
                 S.unit(c, seg, tile, kb0, nk, part);
                 mbar_wait(tmem_empty, (uint32_t(seg) & 1u) ^ 1u);
-                tc_fence_after();
+#if !FLEXQ_GEMM_NO_MMA
+                mbar_wait(a_full + ra.slot, ra.phase);
+                mbar_wait(b_full + rb.slot, rb.phase);
+#endif
                 for (int j = 0; j < nk; ++j) {
-                    mbar_wait(a_full + as, aph);
-                    mbar_wait(b_full + bs, bph);
+#if FLEXQ_GEMM_NO_MMA
+                    mbar_wait(b_full + rb.slot, rb.phase);
+                    rb.next();
+                    if (grp.last_in_group()) umma_commit_warp(done + grp.q.slot);
+                    grp.next();
+                    continue;
+#endif
                     tc_fence_after();
-                    const uint32_t b0 = s_b + uint32_t(bs) * bstage;
-                    const uint32_t a0 = tmem_base + kACol + uint32_t(as) * 64u;
+                    const uint64_t bd0 = bdesc0 + uint64_t(uint32_t(rb.slot) * bstage16);
+                    const uint32_t a0 = tmem_base + p.a_col + uint32_t(ra.slot) * 64u;
+                    ra.next();
+                    rb.next();
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t bd = smem_desc(b0 + kk * 32, 16, 1024);
+                        const uint64_t bd = bd0 + uint64_t(kk * 2);
                         const uint32_t accf = (j > 0 || kk > 0) ? 1u : 0u;
                         umma_ts(tmem_base, a0 + kk * 8, bd, idesc, accf);
-                        umma_ts(tmem_base + kAccStride, a0 + 32 + kk * 8, bd, idesc, accf);
+                        umma_ts(tmem_base + p.acc_stride, a0 + 32 + kk * 8, bd, idesc, accf);
+                        if (kk == 1 && j + 1 < nk) {
+                            // stage g + 1's barriers, waited while stage g's MMAs are still queued
+                            mbar_wait(a_full + ra.slot, ra.phase);
+                            mbar_wait(b_full + rb.slot, rb.phase);
+                        }
                     }
-                    umma_commit(a_empty + as);
-                    umma_commit(b_empty + bs);
-                    if (++as == kAStages) { as = 0; aph ^= 1; }
-                    if (++bs == BS) { bs = 0; bph ^= 1; }
+                    if (grp.last_in_group()) umma_commit_warp(done + grp.q.slot);
+                    grp.next();
                 }
-                umma_commit(tmem_full);
+                umma_commit_warp(tmem_full);
             }
+            if (grp.pos != 0) umma_commit_warp(done + grp.q.slot);   // a final partial group
         }
     } else if (warp >= 8) {
         // ---------------- dequant warps: panel (smem) -> fp16 A operand (TMEM lane = weight column)
-        const int q = warp & 3, h = (warp - 8) >> 2;
+        const int d = warp - 8;
+        const int q = warp & 3, h = (d >> 2) & 1;
+        constexpr int kHalves = kDequantWarps == 16 ? 1 : 2;   // 32-k halves converted by this warp
+        const int hk0 = kDequantWarps == 16 ? (d >> 3) : 0;
         const int nl = h * 128 + q * 32 + lane;             // column within the 256-column tile
         const uint32_t codes_off = uint32_t(nl) * 16u;
         const uint32_t meta_off = uint32_t(kPanelCodes) + uint32_t(nl >> 6) * 256u;
-        const uint32_t a_lane = tmem_base + (uint32_t(q * 32) << 16) + kACol + uint32_t(h) * 32u;
+        const uint32_t a_lane = tmem_base + (uint32_t(q * 32) << 16) + p.a_col + uint32_t(h) * 32u;
         int total = 0;
         for (int u = 0; u < nunits; ++u) {
             int tile, kb0, nk, part;
             S.unit(c, u, tile, kb0, nk, part);
             total += nk;
         }
-        int ps = 0, as = 0;
-        uint32_t pph = 0, aph = 0;
+        int ps = 0;
+        uint32_t pph = 0;
+        Ring ra(NA);
+        GroupRing prev(GR);   // commit group of stage it - NA
         for (int it = 0; it < total; ++it) {
+            const int as = ra.slot;
+            ra.next();
+            if (warp == 8 && lane == 0) TRACE(4, it);
             mbar_wait(panel_full + ps, pph);
+            if (warp == 8 && lane == 0) TRACE(5, it);
             const uint32_t pb = s_panel + uint32_t(ps * kPanelBytes);
-            const uint4 cw0 = lds128(pb + codes_off);            // k 0..31 of this column
-            const uint4 cw1 = lds128(pb + 4096u + codes_off);    // k 32..63
-            mbar_wait(a_empty + as, aph ^ 1);
+            uint4 cw[kHalves];
+#pragma unroll
+            for (int i = 0; i < kHalves; ++i) cw[i] = lds128(pb + uint32_t(hk0 + i) * 4096u + codes_off);
+            if (!FLEXQ_GEMM_NO_MMA && it >= NA) {     // the A slot's previous stage (it - NA) is done
+                mbar_wait(done + prev.q.slot, prev.q.phase);
+                prev.next();
+            }
+            if (warp == 8 && lane == 0) TRACE(6, it);
             tc_fence_after();
 #pragma unroll
-            for (int hk = 0; hk < 2; ++hk) {
-                const uint4 cw = hk ? cw1 : cw0;
-                const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+            for (int i = 0; i < kHalves; ++i) {
+                const int hk = hk0 + i;
+                const uint32_t words[4] = {cw[i].x, cw[i].y, cw[i].z, cw[i].w};
                 uint32_t o[16];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t mo = pb + meta_off + uint32_t((16 * hk + 4 * j) * 8);
+#if FLEXQ_GEMM_DEQ_SKIP
+                    o[4 * j] = words[j]; o[4 * j + 1] = words[j] >> 4; o[4 * j + 2] = lds128(mo).x; o[4 * j + 3] = 0;
+#else
                     deq_word(words[j], lds128(mo), lds128(mo + 16), o + 4 * j);
+#endif
                 }
                 tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
             }
@@ -413,9 +523,9 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(a_full + as);
+            if (lane == 0 && !FLEXQ_GEMM_NO_MMA) mbar_arrive(a_full + as);
+            if (warp == 8 && lane == 0) TRACE(7, it);
             if (++ps == kPanelStages) { ps = 0; pph ^= 1; }
-            if (++as == kAStages) { as = 0; aph ^= 1; }
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> fp16 y (or fp32 partials + split-k fixup)
@@ -427,14 +537,14 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             int tile, kb0, nk, part;
             S.unit(c, seg, tile, kb0, nk, part);
             const bool full = part < 0;
-            mbar_wait(tmem_full, uint32_t(seg) & 1u);
+            mbar_wait_sleep(tmem_full, uint32_t(seg) & 1u, 2000);
             tc_fence_after();
             float* slot = p.partials + int64_t(c) * mp * kBN;    // [256 n][mpad m]
             for (int h = 0; h < 2; ++h) {
                 const int n0 = tile * kBN + h * 128 + q * 32;
                 for (int m0 = 0; m0 < mp; m0 += 16) {
                     float v[16];
-                    tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(h) * kAccStride + uint32_t(m0), v);
+                    tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(h) * p.acc_stride + uint32_t(m0), v);
                     if (full) {
                         store_rows16(v, scratch, lane, p.y, p.N, m0, p.M, n0);
                     } else {
@@ -674,6 +784,11 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
         p.M = mrows;
         p.N = int(N);
         p.mpad = mpad;
+        p.acc_stride = uint32_t((mpad + 31) / 32 * 32);
+        p.a_col = 2u * p.acc_stride;
+        const int fit = int((kTmemCols - p.a_col) / 64u);
+        p.n_a = fit >= 6 ? 6 : (fit >= 4 ? 4 : 3);
+        p.group = p.n_a == 6 ? 3 : (p.n_a == 4 ? 2 : 1);
         p.sc = sc;
         const Smem L = smem_plan(mpad);
         dequant_gemm_kernel<<<grid, kThreads, L.total, stream>>>(mx, p);

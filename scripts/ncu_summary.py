@@ -20,6 +20,8 @@ FULL_METRICS = [
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "smsp__average_warp_latency_issue_stalled_long_scoreboard", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "sm__cycles_elapsed.avg.per_second",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
