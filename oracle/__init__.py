@@ -46,6 +46,8 @@ def lib():
         L.oracle_quantize.argtypes = [P, i64, i64, i32, i32, P, P]
         L.oracle_pack4.argtypes = [P, i64, P]
         L.oracle_unpack4.argtypes = [P, i64, P]
+        L.oracle_pack_bits.argtypes = [P, i64, i32, P]
+        L.oracle_unpack_bits.argtypes = [P, i64, i32, P]
         L.oracle_dequantize.argtypes = [P, P, i64, i64, i32, i32, P]
         L.oracle_append_kv.argtypes = [P, P] + [i32] * 8 + [P, P, P, P]
         L.oracle_attention_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P]
@@ -105,6 +107,31 @@ def unpack4(packed: np.ndarray) -> np.ndarray:
     out = np.zeros(packed.shape[:-1] + (packed.shape[-1] * 2,), np.uint8)
     _check(lib().oracle_unpack4(_p(packed), out.size, _p(out)), "unpack4")
     return out
+
+
+def pack_bits(codes: np.ndarray, bits: int) -> np.ndarray:
+    """Little-endian bit stream of each row's codes: [..][n] -> [..][n * bits / 8] bytes."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    n = codes.shape[-1]
+    out = np.zeros(codes.shape[:-1] + (n * bits // 8,), np.uint8)
+    rows = codes.reshape(-1, n)
+    o = out.reshape(-1, n * bits // 8)
+    for i in range(rows.shape[0]):
+        r, oi = np.ascontiguousarray(rows[i]), np.zeros(n * bits // 8, np.uint8)
+        _check(lib().oracle_pack_bits(_p(r), n, bits, _p(oi)), "pack_bits")
+        o[i] = oi
+    return out
+
+
+def unpack_bits(packed: np.ndarray, n: int, bits: int) -> np.ndarray:
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    rows = packed.reshape(-1, packed.shape[-1])
+    out = np.zeros((rows.shape[0], n), np.uint8)
+    for i in range(rows.shape[0]):
+        r, oi = np.ascontiguousarray(rows[i]), np.zeros(n, np.uint8)
+        _check(lib().oracle_unpack_bits(_p(r), n, bits, _p(oi)), "unpack_bits")
+        out[i] = oi
+    return out.reshape(packed.shape[:-1] + (n,))
 
 
 def dequantize(codes, meta, bits: int = 4, group: int = 64) -> np.ndarray:

@@ -22,7 +22,8 @@
  *         fp32, literal operand order, IEEE division, round-half-even  (readings A, B)
  *         degenerate max == min -> codes 0                          (reading C)
  *   O5  metadata (scale, min) as fp16, scale = (max-min)/(2^b-1)   (reading E)
- *   O6  pack two 4-bit codes per byte, even element in low nibble  (reading H)
+ *   O6  pack two 4-bit codes per byte, even element in low nibble  (reading H);
+ *         any b: a little-endian bit stream per row (NEXT-3 variants)
  *   O7  dequantize: f16(clamp(fmaf(code, scale, min), +-65504))    (readings R)
  *   O8  decode attention softmax(q K^T / sqrt(D)) V over the dequantized cache
  *         (P:271-274), K^ and V^ = fmaf(code, scale, min) in fp32   (reading M)
@@ -159,6 +160,37 @@ int oracle_unpack4(const uint8_t *packed, int64_t n, uint8_t *codes)
     for (int64_t k = 0; k < n / 2; ++k) {
         codes[2 * k] = packed[k] & 0xf;
         codes[2 * k + 1] = packed[k] >> 4;
+    }
+    return OK;
+}
+
+/* O6 for any bit width b in [1, 8] (NEXT-3 variants): the codes of n elements form a
+ * little-endian bit stream, "codes packed little-endian bit-order within bytes":
+ * bit i of code j is stream bit j*b + i, stream bit s is bit s % 8 of byte s / 8.
+ * For b = 4 this is oracle_pack4's byte k = code[2k] | code[2k+1] << 4.
+ * n * b must be a multiple of 8 (whole bytes). */
+int oracle_pack_bits(const uint8_t *codes, int64_t n, int bits, uint8_t *packed)
+{
+    if (n < 0 || bits < 1 || bits > 8 || (n * bits) % 8 != 0) return ERR_ARG;
+    for (int64_t k = 0; k < n * bits / 8; ++k) packed[k] = 0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int i = 0; i < bits; ++i) {
+            int64_t sbit = j * bits + i;
+            if ((codes[j] >> i) & 1) packed[sbit / 8] |= (uint8_t)(1u << (sbit % 8));
+        }
+    return OK;
+}
+
+int oracle_unpack_bits(const uint8_t *packed, int64_t n, int bits, uint8_t *codes)
+{
+    if (n < 0 || bits < 1 || bits > 8 || (n * bits) % 8 != 0) return ERR_ARG;
+    for (int64_t j = 0; j < n; ++j) {
+        unsigned c = 0;
+        for (int i = 0; i < bits; ++i) {
+            int64_t sbit = j * bits + i;
+            c |= (unsigned)((packed[sbit / 8] >> (sbit % 8)) & 1) << i;
+        }
+        codes[j] = (uint8_t)c;
     }
     return OK;
 }

@@ -202,3 +202,34 @@ def test_unsupported_and_bad_args(orc):
         orc.quantize(np.zeros((2, 100), np.float16), 4, 64)     # partial group (reading I)
     with pytest.raises(ValueError):
         orc.quantize(np.zeros((2, 64), np.float16), 9, 64)      # bits out of [1, 8]
+
+
+# ---------------------------------------------------------------- O6 for any b (NEXT-3 variants)
+def test_pack_bits_golden_bytes(orc):
+    """Hand-worked little-endian bit streams."""
+    # b = 2: codes [1, 2, 3, 0] -> bits 10 01 11 00 (LSB first) -> 0b00111001 = 0x39
+    assert orc.pack_bits(np.array([1, 2, 3, 0], np.uint8), 2).tolist() == [0x39]
+    # b = 3: codes [5, 3, 7, 1, 0, 2, 6, 4] -> stream (LSB of each code first)
+    #   101 110 111 100 000 010 011 001
+    #   byte 0 = stream bits 0..7   = 1,0,1,1,1,0,1,1 -> 0xDD
+    #   byte 1 = stream bits 8..15  = 1,1,0,0,0,0,0,0 -> 0x03
+    #   byte 2 = stream bits 16..23 = 1,0,0,1,1,0,0,1 -> 0x99
+    assert orc.pack_bits(np.array([5, 3, 7, 1, 0, 2, 6, 4], np.uint8), 3).tolist() == [0xDD, 0x03, 0x99]
+    # b = 8: identity; b = 4: oracle_pack4's nibble order
+    c = np.arange(16, dtype=np.uint8)
+    assert np.array_equal(orc.pack_bits(c, 8), c)
+    c4 = np.random.default_rng(3).integers(0, 16, 64).astype(np.uint8)
+    assert np.array_equal(orc.pack_bits(c4, 4), orc.pack4(c4))
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 4, 5, 7, 8])
+def test_pack_bits_round_trip_and_numpy(orc, bits):
+    rng = np.random.default_rng(bits)
+    c = rng.integers(0, 1 << bits, size=(3, 64)).astype(np.uint8)
+    p = orc.pack_bits(c, bits)
+    assert p.shape == (3, 64 * bits // 8)
+    assert np.array_equal(orc.unpack_bits(p, 64, bits), c)
+    # independent numpy bit stream: unpackbits (little) of each code's b low bits, concatenated
+    ref = np.packbits(np.unpackbits(c[..., None], axis=-1, bitorder="little")[..., :bits].reshape(3, -1),
+                      axis=-1, bitorder="little")
+    assert np.array_equal(p, ref)
