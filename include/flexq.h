@@ -43,9 +43,11 @@ typedef enum {
                                   pos + n_new > prompt_len + gen_len, cur_len not in
                                   [1, prompt_len + gen_len]                                  */
     FLEXQ_ERR_ALIGN = 3,       /* a tensor pointer is not 16-byte aligned                     */
-    FLEXQ_ERR_UNSUPPORTED = 4, /* legal per the paper but not built: bits != 4, group_size
-                                  != 64 (P:846 fixes b = 4, g = 64), head_dim not in
-                                  {64, 128}, cols % group_size != 0 (reading I)             */
+    FLEXQ_ERR_UNSUPPORTED = 4, /* legal per the paper but not built: (bits, group_size) other
+                                  than (4, 64) -- except flexq_quantize /
+                                  flexq_dequantize, which also build bits in {2, 3, 8} and
+                                  group_size in {32, 128}; head_dim not in {64, 128},
+                                  cols % group_size != 0 (reading I)                          */
     FLEXQ_ERR_WORKSPACE = 5,   /* workspace NULL or smaller than the size query              */
     FLEXQ_ERR_CUDA = 6         /* a CUDA launch / attribute call failed                       */
 } flexq_status;
@@ -59,17 +61,22 @@ const char *flexq_status_string(int status);
 /* Group-wise quantize (reading B): x fp16 [rows][cols] row-major;
  * groups are runs of group_size contiguous elements along cols (for weights,
  * the output-channel axis of the paper's x.w orientation).
- * Per group: min, max; code = RNE(RN32(RN32(RN32(x-min) / RN32(max-min)) * 15));
+ * Per group: min, max; code = RNE(RN32(RN32(RN32(x-min) / RN32(max-min)) * (2^bits - 1)));
  * max == min -> codes 0, scale 0 (reading C).
- *   codes_u8 [rows][cols/2]: element 2k in the low nibble of byte k.
- *   meta_h2  [rows][cols/group_size] half2 {scale = f16((max-min)/15), min}.
- * Supported: bits == 4, group_size == 64, rows * cols / 64 < 2^31 (else
- * FLEXQ_ERR_ARG).  rows == 0 or cols == 0 is a no-op. */
+ *   codes_u8 [rows][cols*bits/8]: each row's codes as a little-endian bit stream, "codes
+ *            packed little-endian bit-order within bytes": bit i of element j is
+ *            stream bit j*bits + i = bit (j*bits + i) % 8 of byte (j*bits + i) / 8.  For
+ *            bits = 4: element 2k in the low nibble of byte k.
+ *   meta_h2  [rows][cols/group_size] half2 {scale = f16((max-min)/(2^bits - 1)), min}.
+ * Built: bits in {2, 3, 4, 8} x group_size in {32, 64, 128} (P:846's b = 4, g = 64 plus the
+ * NEXT-3 variants; other legal values -> FLEXQ_ERR_UNSUPPORTED); rows * cols / group_size
+ * < 2^31 (else FLEXQ_ERR_ARG).  rows == 0 or cols == 0 is a no-op. */
 flexq_status flexq_quantize(const void *x_f16, int64_t rows, int64_t cols, int bits, int group_size,
                             void *codes_u8, void *meta_h2, void *stream);
 
 /* Inverse of flexq_quantize: out fp16 [rows][cols] =
- * f16_RNE(clamp(fmaf(code, scale, min), -65504, 65504)) (reading R). */
+ * f16_RNE(clamp(fmaf(code, scale, min), -65504, 65504)) (reading R).  Same layouts and
+ * built (bits, group_size) set as flexq_quantize. */
 flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t rows, int64_t cols,
                               int bits, int group_size, void *out_f16, void *stream);
 

@@ -49,29 +49,38 @@ const char* flexq_status_string(int s) {
     }
 }
 
+// Quantize / dequantize also build the NEXT-3 variants: b in {2, 3, 8}, g in {32, 128}.
+static flexq_status check_quant_variant(int bits, int group_size) {
+    if (bits < 1 || bits > 8 || group_size < 1) return FLEXQ_ERR_ARG;
+    if (!flexq::quant_variant_built(bits, group_size)) return FLEXQ_ERR_UNSUPPORTED;
+    return FLEXQ_OK;
+}
+
 flexq_status flexq_quantize(const void* x_f16, int64_t rows, int64_t cols, int bits, int group_size,
                             void* codes_u8, void* meta_h2, void* stream) {
     if (rows < 0 || cols < 0) return FLEXQ_ERR_ARG;
-    flexq_status s = check_bits_group(bits, group_size);
+    flexq_status s = check_quant_variant(bits, group_size);
     if (s != FLEXQ_OK) return s;
     if (cols % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
     if (rows == 0 || cols == 0) return FLEXQ_OK;
     if (rows > (int64_t(1) << 31) / (cols / group_size)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     if (!x_f16 || !codes_u8 || !meta_h2) return FLEXQ_ERR_NULL;
     if (!aligned16(x_f16) || !aligned16(codes_u8) || !aligned16(meta_h2)) return FLEXQ_ERR_ALIGN;
-    return from_cuda(flexq::launch_quantize(x_f16, rows, cols, codes_u8, meta_h2, static_cast<cudaStream_t>(stream)));
+    return from_cuda(flexq::launch_quantize(x_f16, rows, cols, bits, group_size, codes_u8, meta_h2,
+                                            static_cast<cudaStream_t>(stream)));
 }
 
 flexq_status flexq_dequantize(const void* codes_u8, const void* meta_h2, int64_t rows, int64_t cols,
                               int bits, int group_size, void* out_f16, void* stream) {
     if (rows < 0 || cols < 0) return FLEXQ_ERR_ARG;
-    flexq_status s = check_bits_group(bits, group_size);
+    flexq_status s = check_quant_variant(bits, group_size);
     if (s != FLEXQ_OK) return s;
     if (cols % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
     if (rows == 0 || cols == 0) return FLEXQ_OK;
+    if (rows > (int64_t(1) << 31) / (cols / group_size)) return FLEXQ_ERR_ARG;
     if (!codes_u8 || !meta_h2 || !out_f16) return FLEXQ_ERR_NULL;
     if (!aligned16(codes_u8) || !aligned16(meta_h2) || !aligned16(out_f16)) return FLEXQ_ERR_ALIGN;
-    return from_cuda(flexq::launch_dequantize(codes_u8, meta_h2, rows, cols, out_f16,
+    return from_cuda(flexq::launch_dequantize(codes_u8, meta_h2, rows, cols, bits, group_size, out_f16,
                                               static_cast<cudaStream_t>(stream)));
 }
 

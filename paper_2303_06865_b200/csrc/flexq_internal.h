@@ -24,11 +24,16 @@ struct KvDst {
     int64_t chunks;   // chunks per (batch, head) = token stride / kChunk
 };
 
-cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* codes, void* meta,
+// bits in {2, 3, 4, 8}, group in {32, 64, 128} (b = 4, g = 64 is the tuned kernel; the others
+// are NEXT-3 variants).  Codes are a little-endian bit stream per row.
+inline bool quant_variant_built(int bits, int group) {
+    return (bits == 2 || bits == 3 || bits == 4 || bits == 8) && (group == 32 || group == 64 || group == 128);
+}
+cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits, int group, void* codes, void* meta,
                             cudaStream_t stream);
 cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
                              void* v_cache, KvDst dst, cudaStream_t stream);
-cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols,
+cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols, int bits, int group,
                               void* out, cudaStream_t stream);
 
 struct AttnArgs {

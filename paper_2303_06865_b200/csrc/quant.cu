@@ -270,6 +270,138 @@ dequantize_kernel(const uint8_t* __restrict__ codes, const __half2* __restrict__
     }
 }
 
+// ------------------------------------------------------------------ other (b, g): NEXT-3 variants
+// Same fp32 sequence as the b = 4, g = 64 kernel with 2^b - 1 levels (reading B), for
+// b in {2, 3, 8} (and 4) and g in {32, 64, 128}.  G / 16 lanes per group, 16 elements per
+// lane; codes are a little-endian bit stream per row, so a lane's 16 codes are the
+// 2b bytes at (16 * element index) * b / 8 -- byte aligned for every b.
+template <int B>
+__device__ __forceinline__ void store_bits(uint8_t* p, uint64_t lo, uint64_t hi) {
+    if constexpr (B == 2) {
+        *reinterpret_cast<uint32_t*>(p) = uint32_t(lo);
+    } else if constexpr (B == 3) {                      // 6 bytes at a 2-byte aligned offset
+        uint16_t* q = reinterpret_cast<uint16_t*>(p);
+        q[0] = uint16_t(lo);
+        q[1] = uint16_t(lo >> 16);
+        q[2] = uint16_t(lo >> 32);
+    } else if constexpr (B == 4) {
+        *reinterpret_cast<uint64_t*>(p) = lo;
+    } else {
+        *reinterpret_cast<uint4*>(p) = make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi), uint32_t(hi >> 32));
+    }
+}
+
+template <int B, int G>
+__global__ void __launch_bounds__(kThreads)
+quantize_generic_kernel(const __half* __restrict__ x, uint8_t* __restrict__ codes, uint8_t* __restrict__ meta,
+                        int64_t groups) {
+    constexpr int L = G / 16;                     // lanes per group
+    constexpr float kLevels = float((1 << B) - 1);
+    const int lane = threadIdx.x & 31;
+    const int part = lane & (L - 1);
+    const int64_t warp0 = (int64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * kThreads) >> 5;
+    for (int64_t wg = warp0 * (32 / L); wg < groups; wg += nwarps * (32 / L)) {   // warp-uniform loop
+        const int64_t g = wg + lane / L;
+        const bool valid = g < groups;
+        uint4 va = make_uint4(0, 0, 0, 0), vb = va;
+        if (valid) {
+            const __half* p = x + g * G + part * 16;
+            va = ld_stream(p);
+            vb = ld_stream(p + 8);
+        }
+        const __half2 h[8] = {u2h(va.x), u2h(va.y), u2h(va.z), u2h(va.w),
+                              u2h(vb.x), u2h(vb.y), u2h(vb.z), u2h(vb.w)};
+        __half2 lo2 = __hmin2(__hmin2(__hmin2(h[0], h[1]), __hmin2(h[2], h[3])),
+                              __hmin2(__hmin2(h[4], h[5]), __hmin2(h[6], h[7])));
+        __half2 hi2 = __hmax2(__hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])),
+                              __hmax2(__hmax2(h[4], h[5]), __hmax2(h[6], h[7])));
+        __half2 mm = __halves2half2(__hmin(__low2half(lo2), __high2half(lo2)),
+                                    __hmax(__low2half(hi2), __high2half(hi2)));   // (min, max), exact
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) {
+            const __half2 t = u2h(__shfl_xor_sync(0xffffffffu, h2u(mm), o));
+            mm = __halves2half2(__hmin(__low2half(mm), __low2half(t)), __hmax(__high2half(mm), __high2half(t)));
+        }
+        if (!valid) continue;
+        float mn = __low2float(mm);
+        const float mx = __high2float(mm);
+        mn = (mn == 0.0f) ? 0.0f : mn;            // reading P
+        const float r = __fsub_rn(mx, mn);        // RN32(max - min)
+        uint64_t plo = 0, phi = 0;
+        __half scale16 = __float2half_rn(0.0f);
+        if (r != 0.0f) {                          // reading C
+            scale16 = __float2half_rn(__fdiv_rn(r, kLevels));
+            const float y = __frcp_rn(r);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float2 f = __half22float2(h[j]);
+                const float xs[2] = {f.x, f.y};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float a = __fsub_rn(xs[e], mn);                     // RN(x - min)
+                    const float q0 = __fmul_rn(a, y);
+                    const float er = __fmaf_rn(-q0, r, a);                   // exact
+                    const float u = __fmaf_rn(er, y, q0);                    // RN(a / r)  (Markstein)
+                    const float t = __fmul_rn(u, kLevels);                   // RN(u (2^b - 1))
+                    const uint32_t c = __float_as_uint(__fadd_rn(t, 8388608.0f)) & 0xFFu;   // RNE(t)
+                    const int idx = 2 * j + e;
+                    if (B * idx < 64)
+                        plo |= uint64_t(c) << (B * idx);
+                    else
+                        phi |= uint64_t(c) << (B * idx - 64);
+                }
+            }
+        }
+        store_bits<B>(codes + (g * G + part * 16) * B / 8, plo, phi);
+        if (part == 0) *reinterpret_cast<__half2*>(meta + g * 4) = __halves2half2(scale16, __float2half_rn(mn));
+    }
+}
+
+// out = f16(clamp(fmaf(code, scale, min), +-65504))   (O7, any b)
+template <int B, int G>
+__global__ void __launch_bounds__(kThreads)
+dequantize_generic_kernel(const uint8_t* __restrict__ codes, const __half2* __restrict__ meta,
+                          __half* __restrict__ out, int64_t groups) {
+    constexpr int L = G / 16;
+    const int64_t nthr = int64_t(gridDim.x) * kThreads;
+    for (int64_t t = int64_t(blockIdx.x) * kThreads + threadIdx.x; t < groups * L; t += nthr) {
+        const int64_t g = t / L;
+        const int part = int(t % L);
+        const uint8_t* p = codes + (g * G + part * 16) * B / 8;
+        uint64_t lo = 0, hi = 0;
+        if constexpr (B == 2) {
+            lo = *reinterpret_cast<const uint32_t*>(p);
+        } else if constexpr (B == 3) {
+            const uint16_t* q = reinterpret_cast<const uint16_t*>(p);
+            lo = uint64_t(q[0]) | (uint64_t(q[1]) << 16) | (uint64_t(q[2]) << 32);
+        } else if constexpr (B == 4) {
+            lo = *reinterpret_cast<const uint64_t*>(p);
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(p);
+            lo = uint64_t(v.x) | (uint64_t(v.y) << 32);
+            hi = uint64_t(v.z) | (uint64_t(v.w) << 32);
+        }
+        const float2 sm = __half22float2(meta[g]);
+        uint32_t o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float v[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int idx = 2 * j + e;
+                const uint32_t c = uint32_t((B * idx < 64 ? (lo >> (B * idx)) : (hi >> (B * idx - 64))) &
+                                            ((1u << B) - 1u));
+                v[e] = __fmaf_rn(float(c), sm.x, sm.y);
+            }
+            o[j] = sat_pack(v[0], v[1]);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + g * G + part * 16);
+        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
 int num_sms() {
     static int sms = 0;
     if (sms == 0) {
@@ -283,8 +415,44 @@ int num_sms() {
 
 }  // namespace
 
-cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, void* codes, void* meta,
+template <int B, int G>
+cudaError_t launch_quantize_bg(const void* x, int64_t groups, void* codes, void* meta, cudaStream_t stream) {
+    int64_t blocks = (groups * (G / 16) + kThreads - 1) / kThreads;
+    const int64_t cap = int64_t(num_sms()) * 8;
+    if (blocks > cap) blocks = cap;
+    quantize_generic_kernel<B, G><<<unsigned(blocks), kThreads, 0, stream>>>(
+        static_cast<const __half*>(x), static_cast<uint8_t*>(codes), static_cast<uint8_t*>(meta), groups);
+    return cudaGetLastError();
+}
+template <int B, int G>
+cudaError_t launch_dequantize_bg(const void* codes, const void* meta, int64_t groups, void* out,
+                                 cudaStream_t stream) {
+    int64_t blocks = (groups * (G / 16) + kThreads - 1) / kThreads;
+    const int64_t cap = int64_t(num_sms()) * 8;
+    if (blocks > cap) blocks = cap;
+    dequantize_generic_kernel<B, G><<<unsigned(blocks), kThreads, 0, stream>>>(
+        static_cast<const uint8_t*>(codes), static_cast<const __half2*>(meta), static_cast<__half*>(out), groups);
+    return cudaGetLastError();
+}
+
+#define FLEXQ_BG_SWITCH(bits, group, CALL)                                                         \
+    switch (bits * 1000 + group) {                                                                 \
+        case 2032: return CALL(2, 32); case 2064: return CALL(2, 64); case 2128: return CALL(2, 128); \
+        case 3032: return CALL(3, 32); case 3064: return CALL(3, 64); case 3128: return CALL(3, 128); \
+        case 4032: return CALL(4, 32); case 4128: return CALL(4, 128);                             \
+        case 8032: return CALL(8, 32); case 8064: return CALL(8, 64); case 8128: return CALL(8, 128); \
+        default: return cudaErrorInvalidValue;                                                     \
+    }
+
+cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits, int group, void* codes, void* meta,
                             cudaStream_t stream) {
+    if (bits != kBits || group != kGroup) {
+        const int64_t groups = rows * (cols / group);
+        if (groups == 0) return cudaSuccess;
+#define Q_CALL(b, g) launch_quantize_bg<b, g>(x, groups, codes, meta, stream)
+        FLEXQ_BG_SWITCH(bits, group, Q_CALL)
+#undef Q_CALL
+    }
     const int64_t groups = rows * (cols / kGroup);
     if (groups == 0) return cudaSuccess;
     int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;
@@ -311,8 +479,15 @@ cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int hea
     return cudaGetLastError();
 }
 
-cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols,
+cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols, int bits, int group,
                               void* out, cudaStream_t stream) {
+    if (bits != kBits || group != kGroup) {
+        const int64_t groups = rows * (cols / group);
+        if (groups == 0) return cudaSuccess;
+#define D_CALL(b, g) launch_dequantize_bg<b, g>(codes, meta, groups, out, stream)
+        FLEXQ_BG_SWITCH(bits, group, D_CALL)
+#undef D_CALL
+    }
     const int64_t groups = rows * (cols / kGroup);
     if (groups == 0) return cudaSuccess;
     int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;

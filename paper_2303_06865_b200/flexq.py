@@ -96,11 +96,12 @@ def _need(t: torch.Tensor, dtype, name: str):
 # ---------------------------------------------------------------- quantizer
 def flexq_quantize(x: torch.Tensor, codes=None, meta=None, bits: int = BITS, group_size: int = GROUP,
                    stream=None):
-    """x fp16 [rows][cols] -> (codes u8 [rows][cols/2], meta fp16 [rows][cols/g][2] = (scale, min))."""
+    """x fp16 [rows][cols] -> (codes u8 [rows][cols*bits/8] (bit stream),
+    meta fp16 [rows][cols/g][2] = (scale, min))."""
     _need(x, torch.float16, "x")
     rows, cols = x.shape
     if codes is None:
-        codes = torch.empty(rows, cols // 2, dtype=torch.uint8, device=x.device)
+        codes = torch.empty(rows, cols * bits // 8, dtype=torch.uint8, device=x.device)
     if meta is None:
         meta = torch.empty(rows, cols // group_size, 2, dtype=torch.float16, device=x.device)
     _check(lib().flexq_quantize(x.data_ptr(), rows, cols, bits, group_size, codes.data_ptr(),
@@ -110,8 +111,8 @@ def flexq_quantize(x: torch.Tensor, codes=None, meta=None, bits: int = BITS, gro
 
 def flexq_dequantize(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: int = BITS,
                      group_size: int = GROUP, stream=None) -> torch.Tensor:
-    rows, half_cols = codes.shape
-    cols = half_cols * 2
+    rows, nbytes = codes.shape
+    cols = nbytes * 8 // bits
     if out is None:
         out = torch.empty(rows, cols, dtype=torch.float16, device=codes.device)
     _check(lib().flexq_dequantize(codes.data_ptr(), meta.data_ptr(), rows, cols, bits, group_size,

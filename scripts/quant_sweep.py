@@ -42,5 +42,26 @@ def main():
                           "dequantize_us": round(td, 1), "dequantize_gbs": round(nb / td / 1e3, 1)}))
 
 
+def variants():
+    """NEXT-3 variants on the OPT-175B w_Q-class matrix (12288 x 12288)."""
+    dev = torch.device("cuda:0")
+    r, c = 12288, 12288
+    x = synth.fill(7, 1, (r, c), device=dev)
+    y = torch.empty_like(x)
+    for b in (2, 3, 4, 8):
+        for g in (32, 64, 128):
+            codes = torch.empty(r, c * b // 8, dtype=torch.uint8, device=dev)
+            meta = torch.empty(r, c // g, 2, dtype=torch.float16, device=dev)
+            nb = r * c * 2 + r * c * b // 8 + r * c // g * 4
+            tq = timed(lambda: fq.flexq_quantize(x, codes, meta, bits=b, group_size=g))
+            td = timed(lambda: fq.flexq_dequantize(codes, meta, y, bits=b, group_size=g))
+            print(json.dumps({"shape": f"{r}x{c}", "bits": b, "group": g, "quantize_us": round(tq, 1),
+                              "quantize_gbs": round(nb / tq / 1e3, 1), "dequantize_us": round(td, 1),
+                              "dequantize_gbs": round(nb / td / 1e3, 1)}))
+
+
 if __name__ == "__main__":
-    main()
+    if "--variants" in sys.argv:
+        variants()
+    else:
+        main()

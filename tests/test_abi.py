@@ -37,8 +37,11 @@ def test_quantize_validation(L):
     assert q(A, 4, 128, 0, 64, A, A, None) == fq.FLEXQ_ERR_ARG      # bits < 1
     assert q(A, 4, 128, 9, 64, A, A, None) == fq.FLEXQ_ERR_ARG      # bits > 8
     assert q(A, 4, 128, 4, 0, A, A, None) == fq.FLEXQ_ERR_ARG
-    assert q(A, 4, 128, 3, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
-    assert q(A, 4, 128, 4, 32, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert q(A, 4, 128, 5, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED   # b = 5: legal, not built
+    assert q(A, 4, 128, 1, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert q(A, 4, 128, 4, 16, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED   # g = 16: legal, not built
+    assert q(A, 4, 96, 4, 48, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert q(A, 4, 96, 3, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED    # partial group (reading I)
     assert q(A, 4, 100, 4, 64, A, A, None) == fq.FLEXQ_ERR_UNSUPPORTED   # partial group (reading I)
     assert q(None, 4, 128, 4, 64, A, A, None) == fq.FLEXQ_ERR_NULL
     assert q(A, 4, 128, 4, 64, None, A, None) == fq.FLEXQ_ERR_NULL
@@ -50,6 +53,8 @@ def test_quantize_validation(L):
 def test_dequantize_validation(L):
     d = L.flexq_dequantize
     assert d(A, A, 4, 128, 4, 65, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert d(A, A, 4, 128, 6, 64, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert d(A, A, 4, 96, 8, 64, A, None) == fq.FLEXQ_ERR_UNSUPPORTED
     assert d(A, A, 4, 128, 10, 64, A, None) == fq.FLEXQ_ERR_ARG
     assert d(A, None, 4, 128, 4, 64, A, None) == fq.FLEXQ_ERR_NULL
     assert d(A, A, 4, 128, 4, 64, U, None) == fq.FLEXQ_ERR_ALIGN
