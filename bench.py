@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-offload", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--same-device", action="store_true",
                     help="all ranks on cuda:0 with gloo (functional test of the N > 1 path on one GPU)")
@@ -554,6 +555,19 @@ def run_flexq(args):
                                  "dequantize_gbs": round(nb / (statistics.median(td) * 1e-3) / 1e9, 1)}
             del x, codes, meta, y, gq, gd
 
+    # ---- NEXT-4: host-offloaded compressed KV, Alg. 1 overlap (rank 0): 2 OPT-175B layers of
+    # batch 144 in pinned host memory, streamed through a 2-slot device ring
+    log("offload")
+    offload = None
+    if rank == 0 and not args.no_offload and w.name == "opt-175b":
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import offload_bench
+        offload = offload_bench.run(layers=2, gpu_batches=1, B=B, H=H, D=D, s=s, n=n, steps=3, dev=str(dev))
+        offload["bound"] = "pcie"
+        offload["how"] = ("per (layer, GPU batch) in Alg. 1 order: H2D of the whole compressed block on a load "
+                          "stream, fused append+attention on the compute stream, D2H of the new token's chunk "
+                          "on a store stream; value = H2D bytes / device time, vs a pinned 1 GiB H2D copy")
+
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     log("cpu baseline")
     cpu = None
@@ -595,6 +609,7 @@ def run_flexq(args):
             "weight_sweep": sweep,
             "topk_sparse": topk,
             "dequant_gemm": gemm,
+            "offload": offload,
         }
         print(json.dumps(line), flush=True)
     if pg:
