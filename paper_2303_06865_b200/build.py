@@ -88,6 +88,7 @@ if __name__ == "__main__":
     if "--gemm-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1",), tag="deqskip"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEFER=1",), tag="defer"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1", "FLEXQ_GEMM_NO_MMA=1"),
                     tag="nomma"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_TRACE=1",), tag="trace"))

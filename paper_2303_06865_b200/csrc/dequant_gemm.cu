@@ -53,6 +53,9 @@ constexpr int kThreads = (8 + kDequantWarps) * 32;
 #ifndef FLEXQ_GEMM_PANEL_STAGES
 #define FLEXQ_GEMM_PANEL_STAGES 8
 #endif
+#ifndef FLEXQ_GEMM_DEFER
+#define FLEXQ_GEMM_DEFER 0      // defer each group commit behind the next stage's first MMAs
+#endif
 #ifndef FLEXQ_GEMM_TRACE
 #define FLEXQ_GEMM_TRACE 0      // tuning only: clock64 stamps of CTA 0's pipeline into the workspace
 #endif
@@ -426,6 +429,8 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             const uint32_t bstage16 = bstage >> 4;
             Ring ra(NA), rb(kBStages);
             GroupRing grp(GR);
+            int gt = 0;   // stage counter (trace only)
+            int prev_q = 0;
             for (int seg = 0; seg < nunits; ++seg) {
                 int tile, kb0, nk, part;
                 S.unit(c, seg, tile, kb0, nk, part);
@@ -433,7 +438,9 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
 #if !FLEXQ_GEMM_NO_MMA
                 mbar_wait(a_full + ra.slot, ra.phase);
                 mbar_wait(b_full + rb.slot, rb.phase);
+                tc_fence_after();
 #endif
+                bool pending = false;      // a group commit deferred behind the next stage's first MMAs
                 for (int j = 0; j < nk; ++j) {
 #if FLEXQ_GEMM_NO_MMA
                     mbar_wait(b_full + rb.slot, rb.phase);
@@ -442,7 +449,7 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                     grp.next();
                     continue;
 #endif
-                    tc_fence_after();
+                    if (lane == 0) TRACE(0, gt);
                     const uint64_t bd0 = bdesc0 + uint64_t(uint32_t(rb.slot) * bstage16);
                     const uint32_t a0 = tmem_base + p.a_col + uint32_t(ra.slot) * 64u;
                     ra.next();
@@ -453,13 +460,33 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                         const uint32_t accf = (j > 0 || kk > 0) ? 1u : 0u;
                         umma_ts(tmem_base, a0 + kk * 8, bd, idesc, accf);
                         umma_ts(tmem_base + p.acc_stride, a0 + 32 + kk * 8, bd, idesc, accf);
-                        if (kk == 1 && j + 1 < nk) {
-                            // stage g + 1's barriers, waited while stage g's MMAs are still queued
-                            mbar_wait(a_full + ra.slot, ra.phase);
-                            mbar_wait(b_full + rb.slot, rb.phase);
+                        if (kk == 0) {
+                            if (FLEXQ_GEMM_DEFER && pending) {
+                                // the previous stage group's commit, issued behind this stage's first
+                                // MMAs so the commit's wait does not find the tensor pipe empty
+                                umma_commit_warp(done + prev_q);
+                                pending = false;
+                            }
+                            if (j + 1 < nk) {
+                                // stage g + 1's barriers, waited while stage g's MMAs are still queued
+                                if (lane == 0) TRACE(1, gt);
+                                mbar_wait(a_full + ra.slot, ra.phase);
+                                mbar_wait(b_full + rb.slot, rb.phase);
+                                tc_fence_after();
+                                if (lane == 0) TRACE(2, gt);
+                            }
                         }
                     }
-                    if (grp.last_in_group()) umma_commit_warp(done + grp.q.slot);
+                    if (grp.last_in_group()) {
+                        if (FLEXQ_GEMM_DEFER && j + 1 < nk) {
+                            pending = true;
+                            prev_q = grp.q.slot;
+                        } else {
+                            umma_commit_warp(done + grp.q.slot);
+                        }
+                    }
+                    if (lane == 0) TRACE(3, gt);
+                    ++gt;
                     grp.next();
                 }
                 umma_commit_warp(tmem_full);

@@ -23,7 +23,7 @@ for M in [int(a) for a in sys.argv[1:]] or [1, 144]:
     tick = (N // 256 * 4 + 255) // 256 * 256
     t = ws[tick:tick + 8 * 256 * 8].view(torch.int64).view(8, 256).cpu().numpy().astype(np.int64)
     t = t - t[0, 0]
-    names = ["mma_top", "mma_2issued", "mma_waited", "mma_commit", "dq_pre", "dq_pfull", "dq_aempty", "dq_afull"]
+    names = ["mma_top", "mma_2iss", "mma_waited", "mma_commit", "dq_pre", "dq_pfull", "dq_aempty", "dq_afull"]
     print(f"M={M}: stages 100..110 (cycles from MMA start)")
     print("      " + " ".join(f"{n:>10s}" for n in names))
     for j in range(100, 106):
