@@ -242,31 +242,56 @@ __device__ __forceinline__ void deq8(uint32_t w, uint32_t magic, const float2 (&
     y = __ffma2_rn(f3, s[3], m2); o[3] = sat_pack(y.x, y.y);
 }
 
+#ifndef FLEXQ_DEQ_UNROLL
+#define FLEXQ_DEQ_UNROLL 4      // group-parts per thread per iteration: loads issued together
+#endif
+#ifndef FLEXQ_DEQ_CS
+#define FLEXQ_DEQ_CS 1          // streaming (evict-first) stores of the fp16 output
+#endif
+__device__ __forceinline__ void st_out(uint4* p, uint4 v) {
+#if FLEXQ_DEQ_CS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 __global__ void __launch_bounds__(kThreads)
 dequantize_kernel(const uint8_t* __restrict__ codes, const __half2* __restrict__ meta,
                   __half* __restrict__ out, int64_t rows, int64_t cols) {
-    const int lane = threadIdx.x & 31;
-    const int part = lane & 3;
-    const int64_t total = rows * (cols / kGroup);
+    constexpr int U = FLEXQ_DEQ_UNROLL;
+    const int64_t total = rows * (cols / kGroup) * 4;       // group parts (16 elements each)
     const int64_t t0 = int64_t(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nthr = int64_t(gridDim.x) * kThreads;
     const uint32_t magic = magic_reg();
-    for (int64_t t = t0; t < total * 4; t += nthr) {
-        const int64_t g = t >> 2;
-        const uint2 c = *reinterpret_cast<const uint2*>(codes + g * (kGroup / 2) + part * 8);
-        const float2 sm = __half22float2(meta[g]);
-        // scale * 16^-k for the nibble positions used by deq8: (0,0), (8,8), (16,16), (8,8)
-        const float2 s[4] = {make_float2(sm.x, sm.x),
-                             make_float2(sm.x * 0.00390625f, sm.x * 0.00390625f),
-                             make_float2(sm.x * 1.52587890625e-05f, sm.x * 1.52587890625e-05f),
-                             make_float2(sm.x * 0.00390625f, sm.x * 0.00390625f)};
-        const float2 m2 = make_float2(sm.y, sm.y);
-        uint32_t o[8];
-        deq8(c.x, magic, s, m2, o);
-        deq8(c.y, magic, s, m2, o + 4);
-        uint4* dst = reinterpret_cast<uint4*>(out + g * kGroup + part * 16);
-        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    for (int64_t tb = t0; tb < total; tb += nthr * U) {
+        uint2 c[U];
+        float2 sm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {          // all loads of the U parts first (memory-level parallelism)
+            const int64_t t = tb + int64_t(u) * nthr;
+            if (t < total) {
+                c[u] = __ldcs(reinterpret_cast<const uint2*>(codes + (t >> 2) * (kGroup / 2) + (t & 3) * 8));
+                sm[u] = __half22float2(meta[t >> 2]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = tb + int64_t(u) * nthr;
+            if (t >= total) break;
+            // scale * 16^-k for the nibble positions used by deq8: (0,0), (8,8), (16,16), (8,8)
+            const float2 s[4] = {make_float2(sm[u].x, sm[u].x),
+                                 make_float2(sm[u].x * 0.00390625f, sm[u].x * 0.00390625f),
+                                 make_float2(sm[u].x * 1.52587890625e-05f, sm[u].x * 1.52587890625e-05f),
+                                 make_float2(sm[u].x * 0.00390625f, sm[u].x * 0.00390625f)};
+            const float2 m2 = make_float2(sm[u].y, sm[u].y);
+            uint32_t o[8];
+            deq8(c[u].x, magic, s, m2, o);
+            deq8(c[u].y, magic, s, m2, o + 4);
+            uint4* dst = reinterpret_cast<uint4*>(out + (t >> 2) * kGroup + (t & 3) * 16);
+            st_out(dst, make_uint4(o[0], o[1], o[2], o[3]));
+            st_out(dst + 1, make_uint4(o[4], o[5], o[6], o[7]));
+        }
     }
 }
 
