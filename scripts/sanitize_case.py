@@ -2,10 +2,11 @@
 
     compute-sanitizer --tool memcheck python scripts/sanitize_case.py
 
-Covers: quantize/dequantize with a ragged row count, prompt fill + 1-token
-append, attention with split-K (few heads) and without, and a cache whose
-capacity is not a multiple of the token stride (cur_len = T_cap, last head:
-the metadata bulk copy rounds up into the stride padding).
+Covers: quantize/dequantize with a ragged row count (and the b/g variants),
+prompt fill + 1-token append, attention with split-K (few heads) and without,
+Top-K, the fused append + attention, a cache whose capacity is not a multiple
+of the token stride (cur_len = T_cap, last head: the metadata bulk copy rounds
+up into the stride padding), weight packing and the tcgen05 dequant-GEMM.
 """
 import os
 import sys
@@ -37,6 +38,20 @@ def main():
         ws = fq.make_workspace(cache)
         for cur in (1, s, s + n):
             fq.flexq_decode_attention(q, cache, cur, workspace=ws)
+        # NEXT-1 Top-K and NEXT-3 fused append + attention on the same cache
+        fq.flexq_decode_attention_topk(q, cache, s, keep=fq.topk_keep(s), workspace=ws)
+        fq.flexq_append_decode_attention(q, q, q, cache, s + n, workspace=ws)
+    # NEXT-3 quantizer variants
+    for b, g in ((2, 32), (3, 128), (8, 64)):
+        c, m = fq.flexq_quantize(x[:, :128].contiguous(), bits=b, group_size=g)
+        fq.flexq_dequantize(c, m, bits=b, group_size=g)
+    # NEXT-2 decode linear layer: a full tile and split-k remainder tiles, two row chunks
+    K, N = 256, 512
+    w = synth.fill(3, 1, (K, N), device=dev)
+    c, m = fq.flexq_quantize(w)
+    panels = fq.flexq_pack_weight(c, m)
+    for M in (20, 170):
+        fq.flexq_dequant_gemm(synth.fill(3, 2 + M, (M, K), device=dev), panels, N)
     torch.cuda.synchronize()
     print("sanitize case ok")
 
