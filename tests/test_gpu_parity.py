@@ -126,6 +126,9 @@ ATTN_CASES = [
     ("d128_many_heads_nosplit", 24, 128, 128, 40, 2, 1, False, 1),  # B*H = 3072: no split
     ("d128_full_capacity_odd", 3, 5, 128, 100, 3, 3, False, 4),      # cur_len = T_cap = 103 (stride 104)
     ("d64_full_capacity_odd", 2, 3, 64, 60, 1, 1, True, 16),         # cur_len = T_cap = 61 (stride 64)
+    ("d128_opt30b_len", 2, 4, 128, 1024, 32, 31, False, 1),          # cur_len 1055: the 1088-token buffer
+    ("d128_beyond_buffer", 1, 3, 128, 1500, 8, 2, True, 16),         # cur_len 1502 > 1088: context split
+    ("d64_beyond_buffer", 1, 2, 64, 2000, 1, 1, False, 4),           # cur_len 2001
 ]
 
 
@@ -200,12 +203,14 @@ def test_attention_cuda_graph_replay(orc, cuda):
 
 
 # ---------------------------------------------------------------- full size, sampled
-def test_opt175b_full_size_sampled(orc, cuda):
-    """BASELINE configs[3] at full size on one GPU (B=144, H=96, D=128, s=512,
-    step 31 -> cur_len 543), the launch configuration bench.py times; the
-    oracle recomputes 12 sampled (b, h) heads from host-regenerated inputs."""
-    B, H, D, s, n = 144, 96, 128, 512, 32
-    seed = synth.BASE_SEED + 3
+@pytest.mark.parametrize("cfg", [("opt175b", 144, 96, 128, 512, 32, 3), ("opt30b", 144, 56, 128, 1024, 32, 2)],
+                         ids=["opt175b", "opt30b"])
+def test_full_size_sampled(orc, cuda, cfg):
+    """BASELINE configs[3] (OPT-175B: B=144, H=96, s=512) and configs[2] (OPT-30B: B=144, H=56,
+    s=1024) at full size on one GPU, step 31 (cur_len 543 / 1055), the launch configuration
+    bench.py times; the oracle recomputes 12 sampled (b, h) heads from host-regenerated inputs."""
+    _, B, H, D, s, n, cfg_index = cfg
+    seed = synth.BASE_SEED + cfg_index
     cache = fq.KVCache(B, H, D, s, n, device=cuda)
     k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=cuda)
     v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), device=cuda)
