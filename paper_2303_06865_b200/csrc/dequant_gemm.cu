@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "flexq_internal.h"
 
@@ -209,7 +210,11 @@ __device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t m
     asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));   // (t & mask) | magic
     const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));                      // c (exact)
     const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
+#if FLEXQ_GEMM_NOCLAMP
+    return h2u(v);
+#else
     return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));                                 // <= 65504
+#endif
 }
 __device__ __forceinline__ void deq_word(uint32_t w, uint4 meta_lo, uint4 meta_hi, uint32_t* o) {
     // meta_lo = {s01, m01, s23, m23}, meta_hi = {s45, m45, s67, m67}
@@ -233,6 +238,63 @@ __device__ __forceinline__ void store_rows16(const float (&v)[16], uint32_t scra
         if (m0 + row < M) *reinterpret_cast<uint4*>(y + int64_t(m0 + row) * ldy + n0 + piece * 8) = d;
     }
     __syncwarp();
+}
+
+// ------------------------------------------------------------------ CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p`'s counterpart in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(p)), "r"(rank));
+    return r;
+}
+// wait with cluster-scope acquire (the phase was completed by arrivals from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WC_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+#ifndef FLEXQ_GEMM_NOCLAMP
+#define FLEXQ_GEMM_NOCLAMP 0
+#endif
+#ifndef FLEXQ_PAIR_FWD
+#define FLEXQ_PAIR_FWD 3   // 1: forwarder, release.cluster; 2: forwarder, relaxed; 3: each warp, relaxed
+#endif
+__device__ __forceinline__ void umma_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(
+            su32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
 }
 
 // Ring position without divisions (the issuing thread's instruction count is on the critical path).
@@ -301,9 +363,9 @@ struct GemmParams {
 struct Smem {
     uint32_t panel, b, epi, bars, b_stages, total;
 };
-__host__ __device__ inline Smem smem_plan(int mpad) {
+__host__ __device__ inline Smem smem_plan(int mpad, bool pair) {
     Smem s;
-    const uint32_t bstage = uint32_t(mpad) * 128u;
+    const uint32_t bstage = uint32_t(pair ? mpad / 2 : mpad) * 128u;   // x rows held by this CTA
     const uint32_t budget = uint32_t(kSmemLimit) - 1024u /* alignment slack */;
     s.panel = 0;
     s.b = s.panel + kPanelStages * kPanelBytes;      // 1024-aligned (8 * 9 KB)
@@ -317,11 +379,16 @@ __host__ __device__ inline Smem smem_plan(int mpad) {
     return s;
 }
 
+// PAIR: a cluster of two CTAs on one TPC runs cta_group::2 MMAs with M = 256 (each CTA holds the A
+// operand of its own 256 weight columns in its TMEM, and half of the x rows in its shared memory);
+// the leader (rank 0) issues for both.  Per CTA that halves the MMA instructions, the commits and
+// the tensor core's shared-memory reads of x, which together bounded the single-CTA version.
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
 dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
-    const Smem L = smem_plan(p.mpad);
+    const Smem L = smem_plan(p.mpad, PAIR);
     const uint32_t s_panel = su32(smem + L.panel);
     const uint32_t s_b = su32(smem + L.b);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -338,36 +405,57 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     uint32_t* epi_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t bstage = uint32_t(p.mpad) * 128u;
+    const uint32_t bstage = uint32_t(PAIR ? p.mpad / 2 : p.mpad) * 128u;   // this CTA's x rows per stage
     const int NA = p.n_a, GR = p.group;
+    const uint32_t rank = PAIR ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    (void)leader;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPanelStages; ++i) {
             mbar_init(panel_full + i, 1);
             mbar_init(panel_empty + i, kDequantWarps);
         }
-        for (int i = 0; i < kMaxAStages; ++i) mbar_init(a_full + i, kDequantWarps);
+        // in a pair, the peer's dequant warps arrive on the peer's own a_full, and the peer's idle MMA
+        // warp forwards one cluster-scope arrive per stage to the leader's (one release.cluster per
+        // stage instead of one per warp: each costs ~1000 cycles)
+        for (int i = 0; i < kMaxAStages; ++i)
+            mbar_init(a_full + i, !PAIR ? kDequantWarps
+                                        : FLEXQ_PAIR_FWD == 3 ? (leader ? 2 * kDequantWarps : 1)
+                                                              : kDequantWarps + (leader ? 1 : 0));
         for (int i = 0; i < kBStages; ++i) mbar_init(b_full + i, 1);
         for (int i = 0; i < kDoneSlots; ++i) mbar_init(done + i, 1);
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, kEpiWarps);
+        mbar_init(tmem_empty, (PAIR ? 2 : 1) * kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 3) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "n"(kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                         "n"(kTmemCols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                         "n"(kTmemCols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     if (warp == 2 && lane == 0)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();      // the peer's barriers exist before anyone arrives remotely
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // barriers the leader waits on, as seen from this CTA (local in the leader, remote in the peer)
+    const uint32_t a_full_l = PAIR ? peer_addr(a_full, 0) : su32(a_full);
+    const uint32_t b_full_l = PAIR ? peer_addr(b_full, 0) : su32(b_full);
+    const uint32_t tmem_empty_l = PAIR ? peer_addr(tmem_empty, 0) : su32(tmem_empty);
 
     const Sched& S = p.sc;
-    const int c = blockIdx.x;
+    const int c = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);   // schedule index: the pair, or the CTA
     const int nunits = S.units(c);
     const int KB = S.KB;
 
@@ -380,7 +468,8 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             for (int u = 0; u < nunits; ++u) {
                 int tile, kb0, nk, part;
                 S.unit(c, u, tile, kb0, nk, part);
-                const uint8_t* src = p.panels + (int64_t(tile) * KB + kb0) * kPanelBytes;
+                const int t256 = PAIR ? 2 * tile + int(rank) : tile;   // this CTA's 256-column tile
+                const uint8_t* src = p.panels + (int64_t(t256) * KB + kb0) * kPanelBytes;
                 for (int j = 0; j < nk; ++j, src += kPanelBytes) {
                     mbar_wait(panel_empty + s, ph ^ 1);
                     mbar_expect_tx(panel_full + s, kPanelBytes);
@@ -406,27 +495,69 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                         prev.next();
                     }
                     rb.next();
-                    mbar_expect_tx(b_full + s, bstage);
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-                        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s_b + uint32_t(s) * bstage),
-                        "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kBK), "r"(0), "r"(su32(b_full + s)),
-                        "l"(pol)
-                        : "memory");
+                    if constexpr (PAIR) {
+                        // both halves complete on the leader's barrier; the leader expects both
+                        if (leader) mbar_expect_tx(b_full + s, 2u * bstage);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s_b + uint32_t(s) * bstage),
+                            "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kBK), "r"(int(rank) * p.mpad / 2),
+                            "r"(b_full_l + uint32_t(s) * 8u), "l"(pol)
+                            : "memory");
+                    } else {
+                        mbar_expect_tx(b_full + s, bstage);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                            " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s_b + uint32_t(s) * bstage),
+                            "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kBK), "r"(0), "r"(su32(b_full + s)),
+                            "l"(pol)
+                            : "memory");
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (the whole warp runs the loop; elect.sync issues)
-        {
+        // ---------------- MMA issuer (the whole warp runs the loop; elect.sync issues); in a pair,
+        // only the leader's warp issues, for both CTAs
+        if (PAIR && !leader && FLEXQ_PAIR_FWD != 3) {
+            // peer: forward "this CTA's A stage is written" to the leader, one arrive per stage
+            int total = 0;
+            for (int u = 0; u < nunits; ++u) {
+                int tile, kb0, nk, part;
+                S.unit(c, u, tile, kb0, nk, part);
+                total += nk;
+            }
+            Ring ra(NA);
+            for (int it = 0; it < total; ++it) {
+                mbar_wait(a_full + ra.slot, ra.phase);
+                tc_fence_after();
+                tc_fence_before();
+                if (lane == 0) {
+                    if (FLEXQ_PAIR_FWD == 2) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(ra.slot) * 8u);
+                    else mbar_arrive_cluster(a_full_l + uint32_t(ra.slot) * 8u);
+                }
+                __syncwarp();
+                ra.next();
+            }
+        }
+        if (!PAIR || leader) {
             const uint32_t idesc = (1u << 4)                        // D fp32; A, B fp16, both K-major
                                    | (uint32_t(p.mpad >> 3) << 17)  // N
-                                   | (uint32_t(128 >> 4) << 24);    // M
+                                   | (uint32_t((PAIR ? 256 : 128) >> 4) << 24);    // M
             // Lean issue loop (the single issuing thread's own instruction count bounds the MMA
             // rate at small N): descriptors are a precomputed base plus an add on the start-address
             // field (addr >> 4 < 2^14, so the add never carries into the next field).
             const uint64_t bdesc0 = smem_desc(s_b, 16, 1024);
             const uint32_t bstage16 = bstage >> 4;
+            auto mma_ = [](uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+                if constexpr (PAIR) umma_ts_pair(d, a, b, id, acc); else umma_ts(d, a, b, id, acc);
+            };
+            auto wait_a_ = [](uint64_t* bar, uint32_t par) {
+                if constexpr (PAIR) mbar_wait_cluster(bar, par); else mbar_wait(bar, par);
+            };
+            auto commit_ = [](uint64_t* bar) {
+                if constexpr (PAIR) umma_commit_pair(bar); else umma_commit_warp(bar);
+            };
             Ring ra(NA), rb(kBStages);
             GroupRing grp(GR);
             int gt = 0;   // stage counter (trace only)
@@ -434,9 +565,9 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             for (int seg = 0; seg < nunits; ++seg) {
                 int tile, kb0, nk, part;
                 S.unit(c, seg, tile, kb0, nk, part);
-                mbar_wait(tmem_empty, (uint32_t(seg) & 1u) ^ 1u);
+                wait_a_(tmem_empty, (uint32_t(seg) & 1u) ^ 1u);
 #if !FLEXQ_GEMM_NO_MMA
-                mbar_wait(a_full + ra.slot, ra.phase);
+                wait_a_(a_full + ra.slot, ra.phase);
                 mbar_wait(b_full + rb.slot, rb.phase);
                 tc_fence_after();
 #endif
@@ -445,7 +576,7 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
 #if FLEXQ_GEMM_NO_MMA
                     mbar_wait(b_full + rb.slot, rb.phase);
                     rb.next();
-                    if (grp.last_in_group()) umma_commit_warp(done + grp.q.slot);
+                    if (grp.last_in_group()) commit_(done + grp.q.slot);
                     grp.next();
                     continue;
 #endif
@@ -458,19 +589,19 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint64_t bd = bd0 + uint64_t(kk * 2);
                         const uint32_t accf = (j > 0 || kk > 0) ? 1u : 0u;
-                        umma_ts(tmem_base, a0 + kk * 8, bd, idesc, accf);
-                        umma_ts(tmem_base + p.acc_stride, a0 + 32 + kk * 8, bd, idesc, accf);
+                        mma_(tmem_base, a0 + kk * 8, bd, idesc, accf);
+                        mma_(tmem_base + p.acc_stride, a0 + 32 + kk * 8, bd, idesc, accf);
                         if (kk == 0) {
                             if (FLEXQ_GEMM_DEFER && pending) {
                                 // the previous stage group's commit, issued behind this stage's first
                                 // MMAs so the commit's wait does not find the tensor pipe empty
-                                umma_commit_warp(done + prev_q);
+                                commit_(done + prev_q);
                                 pending = false;
                             }
                             if (j + 1 < nk) {
                                 // stage g + 1's barriers, waited while stage g's MMAs are still queued
                                 if (lane == 0) TRACE(1, gt);
-                                mbar_wait(a_full + ra.slot, ra.phase);
+                                wait_a_(a_full + ra.slot, ra.phase);
                                 mbar_wait(b_full + rb.slot, rb.phase);
                                 tc_fence_after();
                                 if (lane == 0) TRACE(2, gt);
@@ -482,16 +613,16 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                             pending = true;
                             prev_q = grp.q.slot;
                         } else {
-                            umma_commit_warp(done + grp.q.slot);
+                            commit_(done + grp.q.slot);
                         }
                     }
                     if (lane == 0) TRACE(3, gt);
                     ++gt;
                     grp.next();
                 }
-                umma_commit_warp(tmem_full);
+                commit_(tmem_full);
             }
-            if (grp.pos != 0) umma_commit_warp(done + grp.q.slot);   // a final partial group
+            if (grp.pos != 0) commit_(done + grp.q.slot);   // a final partial group
         }
     } else if (warp >= 8) {
         // ---------------- dequant warps: panel (smem) -> fp16 A operand (TMEM lane = weight column)
@@ -550,7 +681,10 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0 && !FLEXQ_GEMM_NO_MMA) mbar_arrive(a_full + as);
+            if (lane == 0 && !FLEXQ_GEMM_NO_MMA) {
+                if (PAIR && FLEXQ_PAIR_FWD == 3) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(as) * 8u);
+                else mbar_arrive(a_full + as);
+            }
             if (warp == 8 && lane == 0) TRACE(7, it);
             if (++ps == kPanelStages) { ps = 0; pph ^= 1; }
         }
@@ -566,9 +700,10 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             const bool full = part < 0;
             mbar_wait_sleep(tmem_full, uint32_t(seg) & 1u, 2000);
             tc_fence_after();
-            float* slot = p.partials + int64_t(c) * mp * kBN;    // [256 n][mpad m]
+            const int t256 = PAIR ? 2 * tile + int(rank) : tile;     // this CTA's 256-column tile
+            float* slot = p.partials + int64_t(blockIdx.x) * mp * kBN;    // [256 n][mpad m]
             for (int h = 0; h < 2; ++h) {
-                const int n0 = tile * kBN + h * 128 + q * 32;
+                const int n0 = t256 * kBN + h * 128 + q * 32;
                 for (int m0 = 0; m0 < mp; m0 += 16) {
                     float v[16];
                     tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(h) * p.acc_stride + uint32_t(m0), v);
@@ -584,24 +719,28 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tmem_empty);
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_cluster(tmem_empty_l);   // the leader's MMA waits on both CTAs
+                else mbar_arrive(tmem_empty);
+            }
             if (!full) {
                 // Split-k fixup: the last of the tile's S contributors (CTAs r + R p) sums their
                 // partials in p order (deterministic) and stores fp16.
-                const int r = c % S.R;
+                const int r = c % S.R;                                  // remainder tile (pair tile)
+                const int tk = PAIR ? 2 * r + int(rank) : r;             // ticket of this CTA's half
                 __threadfence();
                 epi_bar();
                 if (q == 0 && lane == 0) {
-                    const uint32_t old = atomicAdd(p.tickets + r, 1u);
+                    const uint32_t old = atomicAdd(p.tickets + tk, 1u);
                     const bool last = old == uint32_t(S.S - 1);
-                    if (last) p.tickets[r] = 0u;
+                    if (last) p.tickets[tk] = 0u;
                     *epi_flag = last ? 1u : 0u;
                 }
                 epi_bar();
                 if (*epi_flag) {
                     __threadfence();
                     for (int h = 0; h < 2; ++h) {
-                        const int n0 = tile * kBN + h * 128 + q * 32;
+                        const int n0 = t256 * kBN + h * 128 + q * 32;
                         const int64_t col = int64_t(h * 128 + nl) * mp;
                         for (int m0 = 0; m0 < mp; m0 += 16) {
                             float v[16];
@@ -612,7 +751,8 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                                 float4 a[8];
 #pragma unroll
                                 for (int u = 0; u < 2; ++u) {
-                                    const int k = r + S.R * (pp + u < S.S ? pp + u : pp);
+                                    const int kp = r + S.R * (pp + u < S.S ? pp + u : pp);   // contributor
+                                    const int k = PAIR ? 2 * kp + int(rank) : kp;            // its slot
                                     const float4* src =
                                         reinterpret_cast<const float4*>(p.partials + int64_t(k) * mp * kBN + col + m0);
 #pragma unroll
@@ -641,10 +781,15 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
 
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();      // neither CTA frees TMEM the pair's MMAs may still use
     tc_fence_after();
     if (warp == 3) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
-                     : "memory");
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols)
+                         : "memory");
     }
 }
 
@@ -768,31 +913,44 @@ size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n) {
 
 cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, int64_t K, int64_t N, void* y,
                                 void* workspace, cudaStream_t stream) {
-    const int64_t tiles = N / kBN;
     const int kb = int(K / kBK);
     const int G = sm_count() < kGemmMaxGrid ? sm_count() : kGemmMaxGrid;
+    // CTA pairs (cta_group::2, 512-column pair tiles) are opt-in (FLEXQ_GEMM_PAIR=1): measured within 3 %
+    // of the single-CTA kernel (165 vs 170 us at 144 x 12288 x 49152), whose bound is the dequant
+    // warps' ALU work and the per-stage issue chain rather than the MMA count.
+    static const bool pair_ok = [] {
+        const char* e = getenv("FLEXQ_GEMM_PAIR");
+        return e && e[0] == '1';
+    }();
+    const bool pair = pair_ok && N % (2 * kBN) == 0 && G >= 2;
+    const int64_t tiles = N / (pair ? 2 * kBN : kBN);   // schedule units: pair tiles or CTA tiles
+    const int Gs = pair ? G / 2 : G;
     Sched sc;
     sc.KB = kb;
-    sc.dp_waves = int(tiles / G);
-    sc.R = int(tiles % G);
+    sc.dp_waves = int(tiles / Gs);
+    sc.R = int(tiles % Gs);
     sc.S = 1;
     sc.L = kb;
     if (sc.R > 0) {
-        int parts = G / sc.R;
+        int parts = Gs / sc.R;
         if (parts > kb) parts = kb;
         if (parts < 1) parts = 1;
         sc.L = (kb + parts - 1) / parts;
         sc.S = (kb + sc.L - 1) / sc.L;
     }
-    sc.G = G;
-    const int grid = sc.dp_waves > 0 ? G : sc.R * sc.S;
-    const size_t tick_bytes = size_t((tiles * 4 + 255) / 256 * 256);
+    sc.G = Gs;
+    const int units = sc.dp_waves > 0 ? Gs : sc.R * sc.S;
+    const int grid = pair ? 2 * units : units;
+    const size_t tick_bytes = size_t((N / kBN * 4 + 255) / 256 * 256);
     uint32_t* tickets = static_cast<uint32_t*>(workspace);
     float* partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + tick_bytes);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e =
-            cudaFuncSetAttribute(dequant_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+            cudaFuncSetAttribute(dequant_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(dequant_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemLimit);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -801,7 +959,8 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
         const int mpad = (mrows + 15) / 16 * 16;
         CUtensorMap mx;
         if (!make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, static_cast<const __half*>(x) + m0 * K, uint64_t(K),
-                      uint64_t(mrows), uint64_t(K * 2), kBK, uint32_t(mpad), CU_TENSOR_MAP_SWIZZLE_128B))
+                      uint64_t(mrows), uint64_t(K * 2), kBK, uint32_t(pair ? mpad / 2 : mpad),
+                      CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         GemmParams p;
         p.panels = static_cast<const uint8_t*>(panels);
@@ -817,9 +976,26 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
         p.n_a = fit >= 6 ? 6 : (fit >= 4 ? 4 : 3);
         p.group = p.n_a == 6 ? 3 : (p.n_a == 4 ? 2 : 1);
         p.sc = sc;
-        const Smem L = smem_plan(mpad);
-        dequant_gemm_kernel<<<grid, kThreads, L.total, stream>>>(mx, p);
-        cudaError_t e = cudaGetLastError();
+        const Smem L = smem_plan(mpad, pair);
+        cudaError_t e;
+        if (pair) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned(grid));
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = L.total;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, dequant_gemm_kernel<true>, mx, p);
+        } else {
+            dequant_gemm_kernel<false><<<grid, kThreads, L.total, stream>>>(mx, p);
+            e = cudaGetLastError();
+        }
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

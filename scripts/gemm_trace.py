@@ -10,7 +10,7 @@ from paper_2303_06865_b200 import flexq as fq  # noqa: E402
 from paper_2303_06865_b200 import synth  # noqa: E402
 
 dev = torch.device("cuda:0")
-K, N = 12288, 256 * 148
+K, N = 12288, 256 * 148 * int(os.environ.get('TRACE_NMUL', '1'))
 w = synth.fill(7, 1, (K, N), device=dev)
 codes, meta = fq.flexq_quantize(w)
 panels = fq.flexq_pack_weight(codes, meta)

@@ -194,3 +194,36 @@ def test_opt175b_weight_full_size_sampled(orc, cuda, N):
         wb = synth.gather(seed, 10 + N // 12288, (K, N), [slice(None), slice(64 * b, 64 * b + 64)])
         oc, om = orc.quantize(wb.numpy(), 4, 64)
         check_gemm(y[:, 64 * b:64 * b + 64], x.numpy(), oc, om, orc, f"N={N} block {b}")
+
+
+def test_pair_kernel_matches_single(cuda, tmp_path):
+    """The opt-in CTA-pair kernel (cta_group::2, FLEXQ_GEMM_PAIR=1) splits the MMA's M across two
+    SMs without changing any sum: its output must equal the single-CTA kernel's bit for bit, at
+    a full tile wave, a split-k remainder and two row chunks."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "pair_case.py"
+    script.write_text(
+        "import sys, torch\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_2303_06865_b200 import flexq as fq, synth\n"
+        "dev = torch.device('cuda:0')\n"
+        "out = []\n"
+        "for M, K, N in ((144, 640, 512), (16, 256, 256 * 150), (300, 256, 1024)):\n"
+        "    w = synth.fill(4300 + N, 1, (K, N), device=dev)\n"
+        "    c, m = fq.flexq_quantize(w)\n"
+        "    p = fq.flexq_pack_weight(c, m)\n"
+        "    y = fq.flexq_dequant_gemm(synth.fill(4300 + N, 2, (M, K), device=dev), p, N)\n"
+        "    out.append(y.cpu())\n"
+        "torch.save(out, sys.argv[1])\n")
+    res = {}
+    for mode in ("0", "1"):
+        f = tmp_path / f"y{mode}.pt"
+        env = dict(os.environ, FLEXQ_GEMM_PAIR=mode)
+        r = subprocess.run([sys.executable, str(script), str(f)], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = torch.load(f)
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)
