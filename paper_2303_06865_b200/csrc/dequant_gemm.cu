@@ -271,6 +271,9 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+#ifndef FLEXQ_GEMM_DQBAR
+#define FLEXQ_GEMM_DQBAR 0      // dequant warps: one warp waits / arrives, a named barrier syncs the rest
+#endif
 #ifndef FLEXQ_GEMM_NOCLAMP
 #define FLEXQ_GEMM_NOCLAMP 0
 #endif
@@ -414,15 +417,16 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPanelStages; ++i) {
             mbar_init(panel_full + i, 1);
-            mbar_init(panel_empty + i, kDequantWarps);
+            mbar_init(panel_empty + i, FLEXQ_GEMM_DQBAR ? 1 : kDequantWarps);
         }
         // in a pair, the peer's dequant warps arrive on the peer's own a_full, and the peer's idle MMA
         // warp forwards one cluster-scope arrive per stage to the leader's (one release.cluster per
         // stage instead of one per warp: each costs ~1000 cycles)
         for (int i = 0; i < kMaxAStages; ++i)
-            mbar_init(a_full + i, !PAIR ? kDequantWarps
-                                        : FLEXQ_PAIR_FWD == 3 ? (leader ? 2 * kDequantWarps : 1)
-                                                              : kDequantWarps + (leader ? 1 : 0));
+            mbar_init(a_full + i, FLEXQ_GEMM_DQBAR ? (PAIR && leader ? 2 : 1)
+                                  : !PAIR ? kDequantWarps
+                                  : FLEXQ_PAIR_FWD == 3 ? (leader ? 2 * kDequantWarps : 1)
+                                                        : kDequantWarps + (leader ? 1 : 0));
         for (int i = 0; i < kBStages; ++i) mbar_init(b_full + i, 1);
         for (int i = 0; i < kDoneSlots; ++i) mbar_init(done + i, 1);
         mbar_init(tmem_full, 1);
@@ -648,16 +652,21 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             const int as = ra.slot;
             ra.next();
             if (warp == 8 && lane == 0) TRACE(4, it);
-            mbar_wait(panel_full + ps, pph);
-            if (warp == 8 && lane == 0) TRACE(5, it);
+            // FLEXQ_GEMM_DQBAR: the mbarrier traffic of 16 warps per stage (~64 SYNCS operations)
+            // becomes one waiting warp + two named-barrier syncs of the dequant warps
+            if (!FLEXQ_GEMM_DQBAR || d == 0) {
+                mbar_wait(panel_full + ps, pph);
+                if (warp == 8 && lane == 0) TRACE(5, it);
+                if (!FLEXQ_GEMM_NO_MMA && it >= NA) {     // the A slot's previous stage (it - NA) is done
+                    mbar_wait(done + prev.q.slot, prev.q.phase);
+                    prev.next();
+                }
+            }
+            if (FLEXQ_GEMM_DQBAR) asm volatile("bar.sync 2, %0;" ::"n"(kDequantWarps * 32) : "memory");
             const uint32_t pb = s_panel + uint32_t(ps * kPanelBytes);
             uint4 cw[kHalves];
 #pragma unroll
             for (int i = 0; i < kHalves; ++i) cw[i] = lds128(pb + uint32_t(hk0 + i) * 4096u + codes_off);
-            if (!FLEXQ_GEMM_NO_MMA && it >= NA) {     // the A slot's previous stage (it - NA) is done
-                mbar_wait(done + prev.q.slot, prev.q.phase);
-                prev.next();
-            }
             if (warp == 8 && lane == 0) TRACE(6, it);
             tc_fence_after();
 #pragma unroll
@@ -676,14 +685,16 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                 }
                 tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(panel_empty + ps);
             tmem_wait_st();
             tc_fence_before();
-            __syncwarp();
-            if (lane == 0 && !FLEXQ_GEMM_NO_MMA) {
-                if (PAIR && FLEXQ_PAIR_FWD == 3) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(as) * 8u);
-                else mbar_arrive(a_full + as);
+            if (FLEXQ_GEMM_DQBAR) asm volatile("bar.sync 2, %0;" ::"n"(kDequantWarps * 32) : "memory");
+            else __syncwarp();
+            if (lane == 0 && (!FLEXQ_GEMM_DQBAR || d == 0)) {
+                mbar_arrive(panel_empty + ps);
+                if (!FLEXQ_GEMM_NO_MMA) {
+                    if (PAIR && FLEXQ_PAIR_FWD == 3) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(as) * 8u);
+                    else mbar_arrive(a_full + as);
+                }
             }
             if (warp == 8 && lane == 0) TRACE(7, it);
             if (++ps == kPanelStages) { ps = 0; pph ^= 1; }
