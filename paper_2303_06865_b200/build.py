@@ -89,13 +89,6 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=1", "FLEXQ_DEQ_CS=0"), tag="deq1"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=4", "FLEXQ_DEQ_CS=0"), tag="deq4n"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=2",), tag="deq2"))
-    if "--pair-ab" in sys.argv:
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQBAR=1",), tag="dqbar"))
     if "--gemm-ab" in sys.argv:
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1",), tag="deqskip"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEFER=1",), tag="defer"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DEQ_SKIP=1", "FLEXQ_GEMM_NO_MMA=1"),
-                    tag="nomma"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_TRACE=1",), tag="trace"))
-

@@ -42,9 +42,6 @@ namespace {
 
 constexpr int kBN = kGemmTileN;        // 256 weight columns per tile (two 128-row A operands)
 constexpr int kBK = kGemmTileK;        // 64 k per stage (one 128-byte swizzle row of x)
-#ifndef FLEXQ_GEMM_DEQ_SKIP
-#define FLEXQ_GEMM_DEQ_SKIP 0   // tuning only: skip the dequant arithmetic (wrong results)
-#endif
 #ifndef FLEXQ_GEMM_DQW
 #define FLEXQ_GEMM_DQW 16
 #endif
@@ -54,9 +51,6 @@ constexpr int kThreads = (8 + kDequantWarps) * 32;
 #ifndef FLEXQ_GEMM_PANEL_STAGES
 #define FLEXQ_GEMM_PANEL_STAGES 8
 #endif
-#ifndef FLEXQ_GEMM_DEFER
-#define FLEXQ_GEMM_DEFER 0      // defer each group commit behind the next stage's first MMAs
-#endif
 #ifndef FLEXQ_GEMM_TRACE
 #define FLEXQ_GEMM_TRACE 0      // tuning only: clock64 stamps of CTA 0's pipeline into the workspace
 #endif
@@ -64,9 +58,6 @@ constexpr int kThreads = (8 + kDequantWarps) * 32;
     do { if (FLEXQ_GEMM_TRACE && blockIdx.x == 0 && (j) < 256) { \
         long long t_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)); \
         reinterpret_cast<long long*>(p.partials)[(slot) * 256 + (j)] = t_; } } while (0)
-#ifndef FLEXQ_GEMM_NO_MMA
-#define FLEXQ_GEMM_NO_MMA 0     // tuning only: stream panels and x without MMAs (wrong results)
-#endif
 constexpr int kPanelStages = FLEXQ_GEMM_PANEL_STAGES;
 constexpr int kPanelCodes = kBN * kBK / 2;      // 8 KB: [k half (2)][column (256)][16 B = 32 codes]
 constexpr int kPanelBytes = kGemmPanelBytes;    // + 1 KB: [group (4)][k pair (32)][{scale pair, min pair}]
@@ -121,10 +112,6 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     return uint64_t((addr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
            (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-                 : "memory");
 }
 // Polling wait with a sleep between polls, for roles that wait long (the epilogue waits a whole
 // tile): spinning try_wait loops compete with the MMA issuer's own barrier and UTCHMMA issue.
@@ -210,11 +197,7 @@ __device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t m
     asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));   // (t & mask) | magic
     const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));                      // c (exact)
     const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
-#if FLEXQ_GEMM_NOCLAMP
-    return h2u(v);
-#else
     return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));                                 // <= 65504
-#endif
 }
 __device__ __forceinline__ void deq_word(uint32_t w, uint4 meta_lo, uint4 meta_hi, uint32_t* o) {
     // meta_lo = {s01, m01, s23, m23}, meta_hi = {s45, m45, s67, m67}
@@ -271,15 +254,6 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-#ifndef FLEXQ_GEMM_DQBAR
-#define FLEXQ_GEMM_DQBAR 0      // dequant warps: one warp waits / arrives, a named barrier syncs the rest
-#endif
-#ifndef FLEXQ_GEMM_NOCLAMP
-#define FLEXQ_GEMM_NOCLAMP 0
-#endif
-#ifndef FLEXQ_PAIR_FWD
-#define FLEXQ_PAIR_FWD 3   // 1: forwarder, release.cluster; 2: forwarder, relaxed; 3: each warp, relaxed
-#endif
 __device__ __forceinline__ void umma_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                              uint32_t acc) {
     asm volatile(
@@ -369,11 +343,8 @@ struct Smem {
 __host__ __device__ inline Smem smem_plan(int mpad, bool pair) {
     Smem s;
     const uint32_t bstage = uint32_t(pair ? mpad / 2 : mpad) * 128u;   // x rows held by this CTA
-    const uint32_t budget = uint32_t(kSmemLimit) - 1024u /* alignment slack */;
     s.panel = 0;
     s.b = s.panel + kPanelStages * kPanelBytes;      // 1024-aligned (8 * 9 KB)
-    const uint32_t fixed = s.b + kEpiScratch + 1024u /* bars */;
-    (void)budget;
     const uint32_t bs = kBStages;   // fixed-size plan: 8 * 9 KB + 6 * Mpad * 128 B + 4 KB + bars <= 227 KB
     s.b_stages = bs;
     s.epi = s.b + bs * bstage;
@@ -417,16 +388,12 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPanelStages; ++i) {
             mbar_init(panel_full + i, 1);
-            mbar_init(panel_empty + i, FLEXQ_GEMM_DQBAR ? 1 : kDequantWarps);
+            mbar_init(panel_empty + i, kDequantWarps);
         }
-        // in a pair, the peer's dequant warps arrive on the peer's own a_full, and the peer's idle MMA
-        // warp forwards one cluster-scope arrive per stage to the leader's (one release.cluster per
-        // stage instead of one per warp: each costs ~1000 cycles)
+        // in a pair, the peer's dequant warps arrive on the leader's a_full as well (relaxed cluster-scope
+        // arrives after tcgen05.wait::st: a release.cluster arrive per warp costs ~1000 cycles)
         for (int i = 0; i < kMaxAStages; ++i)
-            mbar_init(a_full + i, FLEXQ_GEMM_DQBAR ? (PAIR && leader ? 2 : 1)
-                                  : !PAIR ? kDequantWarps
-                                  : FLEXQ_PAIR_FWD == 3 ? (leader ? 2 * kDequantWarps : 1)
-                                                        : kDequantWarps + (leader ? 1 : 0));
+            mbar_init(a_full + i, PAIR && leader ? 2 * kDequantWarps : kDequantWarps);
         for (int i = 0; i < kBStages; ++i) mbar_init(b_full + i, 1);
         for (int i = 0; i < kDoneSlots; ++i) mbar_init(done + i, 1);
         mbar_init(tmem_full, 1);
@@ -523,27 +490,6 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     } else if (warp == 1) {
         // ---------------- MMA issuer (the whole warp runs the loop; elect.sync issues); in a pair,
         // only the leader's warp issues, for both CTAs
-        if (PAIR && !leader && FLEXQ_PAIR_FWD != 3) {
-            // peer: forward "this CTA's A stage is written" to the leader, one arrive per stage
-            int total = 0;
-            for (int u = 0; u < nunits; ++u) {
-                int tile, kb0, nk, part;
-                S.unit(c, u, tile, kb0, nk, part);
-                total += nk;
-            }
-            Ring ra(NA);
-            for (int it = 0; it < total; ++it) {
-                mbar_wait(a_full + ra.slot, ra.phase);
-                tc_fence_after();
-                tc_fence_before();
-                if (lane == 0) {
-                    if (FLEXQ_PAIR_FWD == 2) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(ra.slot) * 8u);
-                    else mbar_arrive_cluster(a_full_l + uint32_t(ra.slot) * 8u);
-                }
-                __syncwarp();
-                ra.next();
-            }
-        }
         if (!PAIR || leader) {
             const uint32_t idesc = (1u << 4)                        // D fp32; A, B fp16, both K-major
                                    | (uint32_t(p.mpad >> 3) << 17)  // N
@@ -565,25 +511,14 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             Ring ra(NA), rb(kBStages);
             GroupRing grp(GR);
             int gt = 0;   // stage counter (trace only)
-            int prev_q = 0;
             for (int seg = 0; seg < nunits; ++seg) {
                 int tile, kb0, nk, part;
                 S.unit(c, seg, tile, kb0, nk, part);
                 wait_a_(tmem_empty, (uint32_t(seg) & 1u) ^ 1u);
-#if !FLEXQ_GEMM_NO_MMA
                 wait_a_(a_full + ra.slot, ra.phase);
                 mbar_wait(b_full + rb.slot, rb.phase);
                 tc_fence_after();
-#endif
-                bool pending = false;      // a group commit deferred behind the next stage's first MMAs
                 for (int j = 0; j < nk; ++j) {
-#if FLEXQ_GEMM_NO_MMA
-                    mbar_wait(b_full + rb.slot, rb.phase);
-                    rb.next();
-                    if (grp.last_in_group()) commit_(done + grp.q.slot);
-                    grp.next();
-                    continue;
-#endif
                     if (lane == 0) TRACE(0, gt);
                     const uint64_t bd0 = bdesc0 + uint64_t(uint32_t(rb.slot) * bstage16);
                     const uint32_t a0 = tmem_base + p.a_col + uint32_t(ra.slot) * 64u;
@@ -596,12 +531,6 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                         mma_(tmem_base, a0 + kk * 8, bd, idesc, accf);
                         mma_(tmem_base + p.acc_stride, a0 + 32 + kk * 8, bd, idesc, accf);
                         if (kk == 0) {
-                            if (FLEXQ_GEMM_DEFER && pending) {
-                                // the previous stage group's commit, issued behind this stage's first
-                                // MMAs so the commit's wait does not find the tensor pipe empty
-                                commit_(done + prev_q);
-                                pending = false;
-                            }
                             if (j + 1 < nk) {
                                 // stage g + 1's barriers, waited while stage g's MMAs are still queued
                                 if (lane == 0) TRACE(1, gt);
@@ -612,14 +541,7 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                             }
                         }
                     }
-                    if (grp.last_in_group()) {
-                        if (FLEXQ_GEMM_DEFER && j + 1 < nk) {
-                            pending = true;
-                            prev_q = grp.q.slot;
-                        } else {
-                            commit_(done + grp.q.slot);
-                        }
-                    }
+                    if (grp.last_in_group()) commit_(done + grp.q.slot);
                     if (lane == 0) TRACE(3, gt);
                     ++gt;
                     grp.next();
@@ -652,17 +574,12 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
             const int as = ra.slot;
             ra.next();
             if (warp == 8 && lane == 0) TRACE(4, it);
-            // FLEXQ_GEMM_DQBAR: the mbarrier traffic of 16 warps per stage (~64 SYNCS operations)
-            // becomes one waiting warp + two named-barrier syncs of the dequant warps
-            if (!FLEXQ_GEMM_DQBAR || d == 0) {
-                mbar_wait(panel_full + ps, pph);
-                if (warp == 8 && lane == 0) TRACE(5, it);
-                if (!FLEXQ_GEMM_NO_MMA && it >= NA) {     // the A slot's previous stage (it - NA) is done
-                    mbar_wait(done + prev.q.slot, prev.q.phase);
-                    prev.next();
-                }
+            mbar_wait(panel_full + ps, pph);
+            if (warp == 8 && lane == 0) TRACE(5, it);
+            if (it >= NA) {     // the A slot's previous stage (it - NA) is done
+                mbar_wait(done + prev.q.slot, prev.q.phase);
+                prev.next();
             }
-            if (FLEXQ_GEMM_DQBAR) asm volatile("bar.sync 2, %0;" ::"n"(kDequantWarps * 32) : "memory");
             const uint32_t pb = s_panel + uint32_t(ps * kPanelBytes);
             uint4 cw[kHalves];
 #pragma unroll
@@ -677,24 +594,17 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t mo = pb + meta_off + uint32_t((16 * hk + 4 * j) * 8);
-#if FLEXQ_GEMM_DEQ_SKIP
-                    o[4 * j] = words[j]; o[4 * j + 1] = words[j] >> 4; o[4 * j + 2] = lds128(mo).x; o[4 * j + 3] = 0;
-#else
                     deq_word(words[j], lds128(mo), lds128(mo + 16), o + 4 * j);
-#endif
                 }
                 tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
             }
             tmem_wait_st();
             tc_fence_before();
-            if (FLEXQ_GEMM_DQBAR) asm volatile("bar.sync 2, %0;" ::"n"(kDequantWarps * 32) : "memory");
-            else __syncwarp();
-            if (lane == 0 && (!FLEXQ_GEMM_DQBAR || d == 0)) {
+            __syncwarp();
+            if (lane == 0) {
                 mbar_arrive(panel_empty + ps);
-                if (!FLEXQ_GEMM_NO_MMA) {
-                    if (PAIR && FLEXQ_PAIR_FWD == 3) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(as) * 8u);
-                    else mbar_arrive(a_full + as);
-                }
+                if constexpr (PAIR) mbar_arrive_cluster_relaxed(a_full_l + uint32_t(as) * 8u);   // leader's
+                else mbar_arrive(a_full + as);
             }
             if (warp == 8 && lane == 0) TRACE(7, it);
             if (++ps == kPanelStages) { ps = 0; pph ^= 1; }
