@@ -19,12 +19,15 @@ def h2d_gbs(dev, nbytes=1 << 30):
     dst.copy_(src, non_blocking=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(3):
-        dst.copy_(src, non_blocking=True)
-    e1.record()
-    torch.cuda.synchronize()
-    return 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    best = 0.0
+    for _ in range(3):                    # best of 3 trials of 4 back-to-back 1 GiB copies
+        e0.record()
+        for _ in range(4):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 4 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
 
 
 def run(layers=2, gpu_batches=1, B=144, H=96, D=128, s=512, n=32, steps=3, dev="cuda:0"):
