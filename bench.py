@@ -336,6 +336,31 @@ def run_flexq(args):
     value_gbs = job_bytes / (ms / 1e3) / 1e9
     tokens_per_s = B_total * args.steps / (ms / 1e3)
 
+    # ---- N > 1: gather every rank's outputs of one layer-step (NCCL all-gather),
+    # outside the timed data path and timed on its own; checked against each rank's own block
+    allgather = None
+    if world > 1 and not args.same_device:
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        G_out = B_total if args.scaling == "strong" else B * world
+        per = (G_out + world - 1) // world
+        full = fd.gather_outputs(outs[L - 1], G_out)
+        ok = bool(torch.equal(full[rank * per: rank * per + B], outs[L - 1]))
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        g0.record()
+        for _ in range(20):
+            fd.gather_outputs(outs[L - 1], G_out)
+        g1.record()
+        torch.cuda.synchronize()
+        ag_us = fd.max_over_ranks(g0.elapsed_time(g1) / 20 * 1e3, device=dev)
+        ok_all = fd.max_over_ranks(0.0 if ok else 1.0, device=dev) == 0.0
+        allgather = {"what": "all_gather_into_tensor of one layer-step's fp16 outputs [B][H][D] per rank",
+                     "bytes_per_rank": int(outs[L - 1].numel() * 2), "us": round(ag_us, 1),
+                     "matches_rank_blocks": ok_all, "in_timed_region": False}
+        del full
+        _ = dist
+
     # ---- dominant kernel: attention alone, one graph of L launches at cur_len = s + n - 1
     log("timed; per-kernel pass")
     cur_last = s + n - 1
@@ -610,6 +635,7 @@ def run_flexq(args):
             "topk_sparse": topk,
             "dequant_gemm": gemm,
             "offload": offload,
+            "allgather": allgather,
         }
         print(json.dumps(line), flush=True)
     if pg:
