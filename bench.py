@@ -339,27 +339,30 @@ def run_flexq(args):
     # ---- N > 1: gather every rank's outputs of one layer-step (NCCL all-gather),
     # outside the timed data path and timed on its own; checked against each rank's own block
     allgather = None
-    if world > 1 and not args.same_device:
-        import torch.distributed as dist
+    if world > 1:
         torch.cuda.synchronize()
+        # same-device functional runs use gloo, which gathers host tensors
+        src = outs[L - 1].cpu() if args.same_device else outs[L - 1]
         G_out = B_total if args.scaling == "strong" else B * world
         per = (G_out + world - 1) // world
-        full = fd.gather_outputs(outs[L - 1], G_out)
-        ok = bool(torch.equal(full[rank * per: rank * per + B], outs[L - 1]))
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        full = fd.gather_outputs(src, G_out)
+        ok = bool(torch.equal(full[rank * per: rank * per + B], src))
         barrier()
+        t0 = time.perf_counter()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record()
         for _ in range(20):
-            fd.gather_outputs(outs[L - 1], G_out)
+            fd.gather_outputs(src, G_out)
         g1.record()
         torch.cuda.synchronize()
-        ag_us = fd.max_over_ranks(g0.elapsed_time(g1) / 20 * 1e3, device=dev)
+        ag_us = (g0.elapsed_time(g1) if not args.same_device else (time.perf_counter() - t0) * 1e3) / 20 * 1e3
+        ag_us = fd.max_over_ranks(ag_us, device=dev)
         ok_all = fd.max_over_ranks(0.0 if ok else 1.0, device=dev) == 0.0
         allgather = {"what": "all_gather_into_tensor of one layer-step's fp16 outputs [B][H][D] per rank",
-                     "bytes_per_rank": int(outs[L - 1].numel() * 2), "us": round(ag_us, 1),
-                     "matches_rank_blocks": ok_all, "in_timed_region": False}
+                     "bytes_per_rank": int(src.numel() * 2), "us": round(ag_us, 1),
+                     "matches_rank_blocks": ok_all, "in_timed_region": False,
+                     "backend": "gloo (same-device functional run)" if args.same_device else "nccl"}
         del full
-        _ = dist
 
     # ---- dominant kernel: attention alone, one graph of L launches at cur_len = s + n - 1
     log("timed; per-kernel pass")
