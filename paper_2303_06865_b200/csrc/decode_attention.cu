@@ -83,11 +83,17 @@ decode_attention_kernel(const Params P) {
 
     const int units = P.bh_total * P.nsplit;
     const uint64_t policy = evict_first_policy();
+    // Programmatic dependent launch (NEXT-3 multi-layer decode): let the next layer's launch be
+    // scheduled now (its CTAs become resident as this grid's retire) and, before touching any
+    // global memory, wait for the previous grid in the stream to complete (a no-op when the
+    // launch carried no programmatic dependency).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_proxy_async();
     }
     __syncwarp();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // Unit geometry: unit u = (b, h, split); tokens [first, first + len), nst stages per pass.
     auto geo = [&](int u, int& bh, int& first, int& len) {
@@ -482,8 +488,21 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.v_new = static_cast<const __half*>(a.v_new);
     P.kc_w = static_cast<uint8_t*>(const_cast<void*>(a.k_cache));
     P.vc_w = static_cast<uint8_t*>(const_cast<void*>(a.v_cache));
-    decode_attention_kernel<D, NCH, S, WPC, UNR, MAXT><<<ctas, WPC * 32, smem_bytes<D, NCH, S, WPC, MAXT>(), stream>>>(P);
-    return cudaGetLastError();
+    static const bool pdl = [] {
+        const char* e = getenv("FLEXQ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(ctas));
+    cfg.blockDim = dim3(WPC * 32);
+    cfg.dynamicSmemBytes = smem_bytes<D, NCH, S, WPC, MAXT>();
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<D, NCH, S, WPC, UNR, MAXT>, P);
 }
 
 // Stage geometry (tokens per stage CH, ring depth S, warps per CTA).  The
