@@ -583,6 +583,44 @@ def run_flexq(args):
                                  "dequantize_gbs": round(nb / (statistics.median(td) * 1e-3) / 1e9, 1)}
             del x, codes, meta, y, gq, gd
 
+    # ---- the other BASELINE configs (OPT-6.7B, OPT-30B shapes): decode attention alone at the last
+    # step's context, 4 layers of fresh caches, one CUDA graph -- per-launch time and GB/s (rank 0)
+    other = None
+    if rank == 0 and not args.no_sweep and w.name == "opt-175b":
+        other = {}
+        for cname in ("opt-6.7b", "opt-30b"):
+            cw = wl.CONFIGS[cname]
+            cl, cB = 4, cw.batch
+            ccaches = [fq.KVCache(cB, cw.heads, cw.head_dim, cw.prompt_len, cw.gen_len, device=dev) for _ in range(cl)]
+            for j in range(cl):
+                kp = synth.fill(seed + 7, synth.tensor_id(j, synth.K_PROMPT), (cB, cw.heads, cw.prompt_len, cw.head_dim),
+                                device=dev)
+                fq.flexq_append_kv(kp, kp, ccaches[j], pos=0)
+                del kp
+            ccur = cw.prompt_len + cw.gen_len - 1
+            cq = synth.fill(seed + 7, synth.tensor_id(0, synth.Q), (cB, cw.heads, cw.head_dim), device=dev)
+            cout = torch.empty_like(cq)
+            cws = fq.make_workspace(ccaches[0])
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=stream):
+                for j in range(cl):
+                    fq.flexq_decode_attention(cq, ccaches[j], ccur, out=cout, workspace=cws, stream=stream)
+            gc.replay()
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                c0.record(stream)
+                for _ in range(10):
+                    gc.replay()
+                c1.record(stream)
+            torch.cuda.synchronize()
+            cus = c0.elapsed_time(c1) * 1e3 / (10 * cl)
+            cbytes = wl.attention_bytes(cB, cw.h1, ccur)
+            other[cname] = {"batch": cB, "heads": cw.heads, "cur_len": ccur, "us_per_launch": round(cus, 2),
+                            "bytes_per_launch": cbytes, "GBps": round(cbytes / (cus * 1e-6) / 1e9, 1),
+                            "frac_of_measured_hbm": round(cbytes / (cus * 1e-6) / 1e9 / peak, 4)}
+            del ccaches, cq, cout, cws, gc
+
     # ---- NEXT-4: host-offloaded compressed KV, Alg. 1 overlap (rank 0): 2 OPT-175B layers of
     # batch 144 in pinned host memory, streamed through a 2-slot device ring
     log("offload")
@@ -639,6 +677,7 @@ def run_flexq(args):
             "dequant_gemm": gemm,
             "offload": offload,
             "allgather": allgather,
+            "other_configs": other,
         }
         print(json.dumps(line), flush=True)
     if pg:
