@@ -283,7 +283,7 @@ def run_flexq(args):
         if fused:
             fq.flexq_append_decode_attention(q, k_new, v_new, caches[j], cur, out=out, workspace=ws, stream=st)
         else:
-            fq.flexq_append_kv(k_new, v_new, caches[j], pos=cur - 1, stream=st)
+            fq.flexq_append_kv(k_new.view(B, H, 1, D), v_new.view(B, H, 1, D), caches[j], pos=cur - 1, stream=st)
             fq.flexq_decode_attention(q, caches[j], cur, out=out, workspace=ws, stream=st)
 
     def step_calls(i, st):
@@ -442,41 +442,39 @@ def run_flexq(args):
     log("e2e")
     e2e = None
     if not args.no_e2e:
-        qh = qs.cpu().pin_memory()
-        knh = kn.cpu().pin_memory()
-        vnh = vn.cpu().pin_memory()
+        # one pinned block per layer holding (q, k_new, v_new): one H2D copy per layer
+        hin = torch.stack([qs, kn.view(qs.shape), vn.view(qs.shape)], dim=1).cpu().pin_memory()   # [L][3][B][H][D]
         outh = torch.empty(outs.shape, dtype=outs.dtype).pin_memory()
-        qd = [torch.empty_like(qs[0]) for _ in range(2)]
-        knd = [torch.empty_like(kn[0]) for _ in range(2)]
-        vnd = [torch.empty_like(vn[0]) for _ in range(2)]
-        od = [torch.empty_like(outs[0]) for _ in range(2)]
+        NB = 6                                     # device slots: H2D runs up to NB layers ahead
+        din = [torch.empty_like(hin[0], device=dev) for _ in range(NB)]
+        dout = [torch.empty_like(outs[0]) for _ in range(NB)]
         h2d = torch.cuda.Stream(device=dev)       # one stream per copy direction: both copy engines busy
         d2h = torch.cuda.Stream(device=dev)
+        ready = [torch.cuda.Event() for _ in range(NB)]
+        consumed = [torch.cuda.Event() for _ in range(NB)]
+        drained = [torch.cuda.Event() for _ in range(NB)]
+        gl = [0]                                   # global layer counter (slot = gl % NB)
 
         def e2e_step(i):
             cur = s + i
-            ready = [torch.cuda.Event() for _ in range(L)]
-            done = [torch.cuda.Event() for _ in range(L)]
-            drained = [torch.cuda.Event() for _ in range(L)]
             for j in range(L):
-                b = j & 1
+                g = gl[0]
+                gl[0] += 1
+                b = g % NB
                 with torch.cuda.stream(h2d):
-                    if j >= 2:
-                        h2d.wait_event(done[j - 2])         # buffer b free: layer j - 2 has consumed it
-                    qd[b].copy_(qh[j], non_blocking=True)
-                    knd[b].copy_(knh[j], non_blocking=True)
-                    vnd[b].copy_(vnh[j], non_blocking=True)
-                    ready[j].record(h2d)
-                stream.wait_event(ready[j])
-                if j >= 2:
-                    stream.wait_event(drained[j - 2])      # od[b] copied out
-                layer_step(j, cur, qd[b], knd[b], vnd[b], od[b], stream)
-                done[j].record(stream)
+                    if g >= NB:
+                        h2d.wait_event(consumed[b])        # slot b's inputs consumed by layer g - NB
+                    din[b].copy_(hin[j], non_blocking=True)
+                    ready[b].record(h2d)
+                stream.wait_event(ready[b])
+                if g >= NB:
+                    stream.wait_event(drained[b])          # slot b's output copied out
+                layer_step(j, cur, din[b][0], din[b][1], din[b][2], dout[b], stream)
+                consumed[b].record(stream)
                 with torch.cuda.stream(d2h):
-                    d2h.wait_event(done[j])
-                    outh[j].copy_(od[b], non_blocking=True)
-                    drained[j].record(d2h)
-            stream.wait_stream(d2h)
+                    d2h.wait_event(consumed[b])
+                    outh[j].copy_(dout[b], non_blocking=True)
+                    drained[b].record(d2h)
 
         for k in range(2):
             e2e_step(seq_of(k))
@@ -489,17 +487,18 @@ def run_flexq(args):
             i = seq_of(k)
             e2e_step(i)
             e2e_bytes += step_bytes[i]
+        stream.wait_stream(d2h)                    # the last outputs are home
         x1.record(stream)
         barrier()
         ems = fd.max_over_ranks(x0.elapsed_time(x1), device=dev)
         e2e_job = e2e_bytes * (B_total / B if B else 0)
         e2e = {"value": round(e2e_job / (ems / 1e3) / 1e9, 2),
-               "unit": "GB/s", "h2d_bytes_per_step": int(qh.nbytes + knh.nbytes + vnh.nbytes),
+               "unit": "GB/s", "h2d_bytes_per_step": int(hin.nbytes),
                "d2h_bytes_per_step": int(outh.nbytes), "ms_per_step": round(ems / ke, 3),
                "tokens_per_s": round(B_total * ke / (ems / 1e3), 2),
-               "how": "pinned host q/k_new/v_new per layer -> H2D on a copy stream, D2H of the output on another "
-                      "(double-buffered), "
-                      "append+attention via the C ABI, D2H of every layer's output; CUDA events, max over ranks"}
+               "how": "pinned host (q, k_new, v_new) block per layer -> one H2D copy on a copy stream, D2H of the "
+                      "output on another, 6 device slots so copies run ahead of compute; append+attention via the "
+                      "C ABI, D2H of every layer's output; CUDA events, max over ranks"}
 
     # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
     log("sweep")
