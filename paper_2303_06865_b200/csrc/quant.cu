@@ -188,7 +188,12 @@ quantize_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, ui
         uint32_t wlo = 0, whi = 0;
         __half scale16 = __float2half_rn(0.0f);
         if (r != 0.0f) {                          // reading C: degenerate group -> codes 0
-            scale16 = __float2half_rn(__fdiv_rn(r, 15.0f));
+            // RN(r / 15) by one Markstein step on RN(1/15): equal to the IEEE quotient for every
+            // fp32 r in the operand range (tests/test_division.py, exhaustive), ~15 instructions
+            // cheaper than __fdiv_rn
+            constexpr float kInv15 = 0.0666666701436042785645f;   // RN(1/15) = 0x3D888889
+            const float s0 = __fmul_rn(r, kInv15);
+            scale16 = __float2half_rn(__fmaf_rn(__fmaf_rn(-s0, 15.0f, r), kInv15, s0));
             const float y = __frcp_rn(r);
             float2 f[4];
 #pragma unroll
