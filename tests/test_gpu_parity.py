@@ -340,3 +340,32 @@ def test_append_attention_fused_matches_two_launches(cuda):
         o2 = fq.flexq_decode_attention(q, c2, s + step)
         assert torch.equal(o1, o2), f"step {step}"
     assert torch.equal(c1.k, c2.k) and torch.equal(c1.v, c2.v)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_attention_extreme_cache(orc, cuda, D):
+    """Pathological KV groups (synth.extreme: constant groups -> scale 0, +-65504 mixes, subnormal
+    groups, any finite pattern), scaled by powers of two so the softmax stays finite: the
+    fixed-point q and weight paths must still land within reading Q of the f64 oracle."""
+    B, H, s, n = 2, 3, 150, 4
+    rows = B * H * s
+    k = (synth.extreme(4401, 1, rows, D).float() * 2.0 ** -10).half().view(B, H, s, D)
+    v = (synth.extreme(4401, 2, rows, D).float() * 2.0 ** -4).half().view(B, H, s, D)
+    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    okc, ovc = orc.empty_cache(B, H, s + n, D), orc.empty_cache(B, H, s + n, D)
+    fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+    orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+    for qf in (1, 16):
+        q = synth.peaky(synth.fill(4401, 3 + qf, (B, H, D)), qf)
+        out = fq.flexq_decode_attention(q.to(cuda), cache, s)
+        ref = orc.attention_f64(q.numpy(), okc, ovc, s)
+        assert_attn_close(out.cpu().numpy(), ref, f"extreme D={D} q x{qf}")
+    # and one fused append + attention step with a pathological new token
+    kn = (synth.extreme(4401, 10, B * H, D).float() * 2.0 ** -10).half().view(B, H, D)
+    vn = (synth.extreme(4401, 20, B * H, D).float() * 2.0 ** -4).half().view(B, H, D)
+    q = synth.fill(4401, 30, (B, H, D))
+    out = fq.flexq_append_decode_attention(q.to(cuda), kn.to(cuda), vn.to(cuda), cache, s + 1)
+    orc.append_kv(kn.view(B, H, 1, D).numpy(), vn.view(B, H, 1, D).numpy(), okc, ovc, s)
+    ref = orc.attention_f64(q.numpy(), okc, ovc, s + 1)
+    assert_attn_close(out.cpu().numpy(), ref, f"extreme fused D={D}")
+    assert np.array_equal(cache.k_codes()[:, :, :s + 1].cpu().numpy(), orc.pack4(okc[0][:, :, :s + 1]))
