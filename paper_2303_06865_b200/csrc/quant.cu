@@ -361,19 +361,26 @@ quantize_generic_kernel(const __half* __restrict__ x, uint8_t* __restrict__ code
         uint64_t plo = 0, phi = 0;
         __half scale16 = __float2half_rn(0.0f);
         if (r != 0.0f) {                          // reading C
-            scale16 = __float2half_rn(__fdiv_rn(r, kLevels));
+            // RN(r / (2^b - 1)) by one Markstein step on RN(1 / (2^b - 1)): equal to the IEEE quotient
+            // for every fp32 r in the operand range and b in {2, 3, 4, 8} (tests/test_division.py)
+            constexpr float kInvLevels = 1.0f / kLevels;
+            const float s0 = __fmul_rn(r, kInvLevels);
+            scale16 = __float2half_rn(__fmaf_rn(__fmaf_rn(-s0, kLevels, r), kInvLevels, s0));
             const float y = __frcp_rn(r);
+            const float2 nmn = make_float2(-mn, -mn), yy = make_float2(y, y), nr = make_float2(-r, -r);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const float2 f = __half22float2(h[j]);
-                const float xs[2] = {f.x, f.y};
+                // the b = 4 kernel's packed sequence: a, q0, e, u two elements at a time (each a single
+                // rounding, no two of them contractible); t and the magic add stay scalar (a packed
+                // mul + add pair is contracted into one FFMA2 by ptxas, see codes8)
+                const float2 a = __fadd2_rn(__half22float2(h[j]), nmn);   // RN(x - min)
+                const float2 q0 = __fmul2_rn(a, yy);
+                const float2 er = __ffma2_rn(q0, nr, a);                  // exact
+                const float2 u = __ffma2_rn(er, yy, q0);                  // RN(a / r)  (Markstein)
+                const float us[2] = {u.x, u.y};
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const float a = __fsub_rn(xs[e], mn);                     // RN(x - min)
-                    const float q0 = __fmul_rn(a, y);
-                    const float er = __fmaf_rn(-q0, r, a);                   // exact
-                    const float u = __fmaf_rn(er, y, q0);                    // RN(a / r)  (Markstein)
-                    const float t = __fmul_rn(u, kLevels);                   // RN(u (2^b - 1))
+                    const float t = __fmul_rn(us[e], kLevels);                  // RN(u (2^b - 1))
                     const uint32_t c = __float_as_uint(__fadd_rn(t, 8388608.0f)) & 0xFFu;   // RNE(t)
                     const int idx = 2 * j + e;
                     if (B * idx < 64)

@@ -11,6 +11,8 @@ r = 30 m 2^e.  Written in C (gcc -ffp-contract=off); shares no code with
 csrc/ or oracle/.
 """
 import os
+
+import pytest
 import subprocess
 import tempfile
 
@@ -78,17 +80,19 @@ SRC15 = r"""
 #include <stdio.h>
 #include <stdint.h>
 #include <string.h>
+#include <stdlib.h>
 #include <math.h>
-int main(void) {
+int main(int argc, char **argv) {
   /* every fp32 r in [2^-24, 131008] (a superset of RN(max - min) over fp16 groups) */
-  const float y = 1.0f / 15.0f;
+  const float L = argc > 1 ? (float)atoi(argv[1]) : 15.0f;   /* 2^b - 1 */
+  const float y = 1.0f / L;
   uint32_t lo, hi; float flo = ldexpf(1.0f, -24), fhi = 131008.0f;
   memcpy(&lo, &flo, 4); memcpy(&hi, &fhi, 4);
   long bad = 0, tested = 0;
   for (uint32_t b = lo; b <= hi; b++) {
     float r; memcpy(&r, &b, 4);
-    float u = r / 15.0f;
-    float s0 = r * y, s1 = fmaf(fmaf(-s0, 15.0f, r), y, s0);
+    float u = r / L;
+    float s0 = r * y, s1 = fmaf(fmaf(-s0, L, r), y, s0);
     tested++;
     if (memcmp(&u, &s1, 4) != 0) { if (bad < 5) printf("MISMATCH r=%a ieee=%a markstein=%a\n", r, u, s1); bad++; }
   }
@@ -98,15 +102,18 @@ int main(void) {
 """
 
 
-def test_scale_division_by_15_exhaustive():
-    """RN(r / 15) (the stored scale, O5) as s0 = RN(r * RN(1/15)), RN(s0 + fma(-s0, 15, r) * RN(1/15)):
-    equal to IEEE division for every fp32 r in the operand range (the fused append kernel's form)."""
+@pytest.mark.parametrize("levels,recip", [(15, "0x1.111112p-4"), (3, "0x1.555556p-2"), (7, "0x1.24924ap-3"),
+                                          (255, "0x1.010102p-8")])
+def test_scale_division_exhaustive(levels, recip):
+    """RN(r / L) (the stored scale, O5, L = 2^b - 1) as s0 = RN(r * RN(1/L)), RN(s0 + fma(-s0, L, r) * RN(1/L)):
+    equal to IEEE division for every fp32 r in the operand range (the quantize and fused append kernels'
+    form), for b = 4 and the NEXT-3 variants b = 2, 3, 8."""
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "div15.c")
         exe = os.path.join(d, "div15")
         open(c, "w").write(SRC15)
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-o", exe, c, "-lm"])
-        out = subprocess.run([exe], capture_output=True, text=True)
+        out = subprocess.run([exe, str(levels)], capture_output=True, text=True)
         assert out.returncode == 0, out.stdout
-        assert "y=0x1.111112p-4" in out.stdout          # RN(1/15) = 0x3D888889, the kernel's constant
+        assert f"y={recip}" in out.stdout                # RN(1/L), the kernels' constant
         assert int(out.stdout.split()[-3]) > 300_000_000
