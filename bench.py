@@ -55,9 +55,22 @@ def parse():
 _T0 = time.time()
 
 
+_NVTX = [False]
+
+
 def log(msg: str):
+    """Progress line on stderr; also an NVTX range per bench phase (visible in nsys / ncu --nvtx)."""
     sys.stderr.write(f"[bench {time.time() - _T0:7.1f}s] {msg}\n")
     sys.stderr.flush()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            if _NVTX[0]:
+                torch.cuda.nvtx.range_pop()
+            torch.cuda.nvtx.range_push(f"bench:{msg}")
+            _NVTX[0] = True
+    except Exception:  # noqa: BLE001 -- tracing is best effort
+        pass
 
 
 def peaks():
