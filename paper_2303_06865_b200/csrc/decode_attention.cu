@@ -45,7 +45,7 @@
 #define FLEXQ_AB_FENCE 1
 #endif
 #ifndef FLEXQ_AB_GSTORE
-#define FLEXQ_AB_GSTORE 1
+#define FLEXQ_AB_GSTORE 2   // fused append write-back: 2 lane stores (default), 1 TMA bulk store, 0 none (A/B)
 #endif
 #ifndef FLEXQ_AB_QUANT
 #define FLEXQ_AB_QUANT 1
@@ -136,7 +136,15 @@ decode_attention_kernel(const Params P) {
         if (fcount == 0) fq0 = p_unit; else if (fcount == 1) fq1 = p_unit; else fq2 = p_unit;
         ++fcount;
     };
+    bool store_pending = false;     // a fused-append TMA store may still be reading a stage slot
     auto issue = [&](int slot) {
+        if (lane == 0 && store_pending) {
+            // the patched slot is refilled only after the bulk store has read it; waiting here
+            // (one stage of math after the store was issued) instead of right after issuing it
+            // takes the wait off the critical path
+            bulk_wait_read0();
+            store_pending = false;
+        }
         if (p_unit < 0) {
             if (lane == 0) mbar_expect_tx(&bars[slot], 0);   // keeps the phase sequence; nothing to load
             return;
@@ -217,7 +225,21 @@ decode_attention_kernel(const Params P) {
             uint8_t* s_chunk = const_cast<uint8_t*>(sb) + (new_idx >> 5) * C::CHB;
             if (vpass == (lane >= 16)) store_token<D>(tq, new_slot, s_chunk, lane);
             __syncwarp();
-#if FLEXQ_AB_GSTORE
+#if FLEXQ_AB_GSTORE == 2
+            {   // lanes copy the patched 16-byte pieces to the cache with plain stores
+                uint8_t* g_chunk = (vpass ? P.vc_w : P.kc_w) +
+                                   (int64_t(bh) * P.chunks + ((P.cur_len - 1) >> 5)) * C::CHB;
+                const int rows = vpass ? (new_slot >> 2) * 4 * C::CB : new_slot * C::CB;   // byte offset
+                const int moff = C::OFF_M + (new_slot & ~3) * C::MB;                     // quad's meta
+                const int nrow = (vpass ? 4 * C::CB : C::CB) / 16, nmeta = (4 * C::MB) / 16;
+                if (lane < nrow)
+                    *reinterpret_cast<uint4*>(g_chunk + rows + 16 * lane) =
+                        *reinterpret_cast<const uint4*>(s_chunk + rows + 16 * lane);
+                else if (lane < nrow + nmeta)
+                    *reinterpret_cast<uint4*>(g_chunk + moff + 16 * (lane - nrow)) =
+                        *reinterpret_cast<const uint4*>(s_chunk + moff + 16 * (lane - nrow));
+            }
+#elif FLEXQ_AB_GSTORE
             fence_proxy_async();   // the patch (generic writes) before the TMA store reads it
             __syncwarp();
             if (lane == 0) {
@@ -228,7 +250,7 @@ decode_attention_kernel(const Params P) {
                 bulk_s2g(g_chunk + rows, s_chunk + rows, vpass ? 4 * C::CB : C::CB);
                 bulk_s2g(g_chunk + moff, s_chunk + moff, 4 * C::MB);
                 bulk_commit();
-                bulk_wait_read0();   // the slot is refilled after release
+                store_pending = true;   // waited for before the slot's next bulk copy (issue)
             }
 #endif
 #if FLEXQ_AB_FENCE
@@ -370,6 +392,7 @@ decode_attention_kernel(const Params P) {
 
     // retire: the last warp out resets the ticket counter for the next call
     if (lane == 0) {
+        if (store_pending) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // before smem goes away
         __threadfence();
         const uint32_t total = gridDim.x * WPC;
         if (atomicAdd(P.ctrl + 1, 1u) == total - 1) {
