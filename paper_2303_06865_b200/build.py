@@ -90,7 +90,8 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=4", "FLEXQ_DEQ_CS=0"), tag="deq4n"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=2",), tag="deq2"))
     if "--fuse-ab" in sys.argv:
-        for d, t in (("FLEXQ_AB_GSTORE=0", "abg0"), ("FLEXQ_AB_GSTORE=1", "abg1")):
+        for d, t in (("FLEXQ_AB_GSTORE=0", "abg0"), ("FLEXQ_AB_GSTORE=1", "abg1"), ("FLEXQ_AB_STPOL=1", "stp1"),
+                     ("FLEXQ_AB_STPOL=2", "stp2")):
             print(build(force="--force" in sys.argv, defines=(d,), tag=t))
     if "--gemm-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))

@@ -47,6 +47,9 @@
 #ifndef FLEXQ_AB_GSTORE
 #define FLEXQ_AB_GSTORE 2   // fused append write-back: 2 lane stores (default), 1 TMA bulk store, 0 none (A/B)
 #endif
+#ifndef FLEXQ_AB_STPOL
+#define FLEXQ_AB_STPOL 0    // write-back cache policy (A/B): 0 default, 1 L2 evict-last, 2 streaming
+#endif
 #ifndef FLEXQ_AB_QUANT
 #define FLEXQ_AB_QUANT 1
 #endif
@@ -232,12 +235,27 @@ decode_attention_kernel(const Params P) {
                 const int rows = vpass ? (new_slot >> 2) * 4 * C::CB : new_slot * C::CB;   // byte offset
                 const int moff = C::OFF_M + (new_slot & ~3) * C::MB;                     // quad's meta
                 const int nrow = (vpass ? 4 * C::CB : C::CB) / 16, nmeta = (4 * C::MB) / 16;
-                if (lane < nrow)
-                    *reinterpret_cast<uint4*>(g_chunk + rows + 16 * lane) =
-                        *reinterpret_cast<const uint4*>(s_chunk + rows + 16 * lane);
-                else if (lane < nrow + nmeta)
-                    *reinterpret_cast<uint4*>(g_chunk + moff + 16 * (lane - nrow)) =
-                        *reinterpret_cast<const uint4*>(s_chunk + moff + 16 * (lane - nrow));
+                uint8_t* gdst = nullptr;
+                const uint8_t* ssrc = nullptr;
+                if (lane < nrow) {
+                    gdst = g_chunk + rows + 16 * lane;
+                    ssrc = s_chunk + rows + 16 * lane;
+                } else if (lane < nrow + nmeta) {
+                    gdst = g_chunk + moff + 16 * (lane - nrow);
+                    ssrc = s_chunk + moff + 16 * (lane - nrow);
+                }
+                if (gdst) {
+                    const uint4 d = *reinterpret_cast<const uint4*>(ssrc);
+#if FLEXQ_AB_STPOL == 1
+                    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(gdst), "r"(d.x),
+                                 "r"(d.y), "r"(d.z), "r"(d.w), "l"(evict_last_policy())
+                                 : "memory");
+#elif FLEXQ_AB_STPOL == 2
+                    __stcs(reinterpret_cast<uint4*>(gdst), d);
+#else
+                    *reinterpret_cast<uint4*>(gdst) = d;
+#endif
+                }
             }
 #elif FLEXQ_AB_GSTORE
             fence_proxy_async();   // the patch (generic writes) before the TMA store reads it
