@@ -184,9 +184,11 @@ flexq_status flexq_decode_attention_topk(const void *q_f16, const void *k_cache,
  *
  * flexq_pack_weight: one-time re-layout (no arithmetic) of flexq_quantize's output for a
  * [k][n] weight -- codes_u8 u8 [k][n/2], meta_h2 half2 [k][n/group_size] -- into
- * flexq_gemm_panel_bytes(k, n) bytes of "panels" (one 9 KB panel per 256 columns x 64 k:
- * codes column-major along k, then that block's (scale, min) pairs), the operand format of
- * flexq_dequant_gemm.  Same total size as codes + meta.  Writes only `panels`.
+ * flexq_gemm_panel_bytes(k, n) bytes of "panels" (one 9216-byte panel per 256 columns x 64 k:
+ * codes column-major along k, then that block's (scale, min) pairs; after all panels, one
+ * 16-byte flag per panel whose first word is 1 when some code of the panel can reconstruct above
+ * 65504 -- the kernel then applies reading R's clamp), the operand format of
+ * flexq_dequant_gemm: the bytes of codes + meta plus 16 per panel.  Writes only `panels`.
  *
  * flexq_dequant_gemm:
  *   x_f16   fp16 [m][k] row-major (m = decode batch b, k = in features); any m >= 1

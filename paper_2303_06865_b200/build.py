@@ -96,3 +96,5 @@ if __name__ == "__main__":
     if "--gemm-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_TRACE=1",), tag="trace"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_PROBE=1",), tag="nostt"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_PROBE=2",), tag="nomath"))

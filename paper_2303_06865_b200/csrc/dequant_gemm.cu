@@ -51,6 +51,9 @@ constexpr int kThreads = (8 + kDequantWarps) * 32;
 #ifndef FLEXQ_GEMM_PANEL_STAGES
 #define FLEXQ_GEMM_PANEL_STAGES 8
 #endif
+#ifndef FLEXQ_GEMM_PROBE
+#define FLEXQ_GEMM_PROBE 0   // tuning only: 1 skip the A stores to TMEM, 2 skip the dequant arithmetic
+#endif
 #ifndef FLEXQ_GEMM_TRACE
 #define FLEXQ_GEMM_TRACE 0      // tuning only: clock64 stamps of CTA 0's pipeline into the workspace
 #endif
@@ -60,7 +63,10 @@ constexpr int kThreads = (8 + kDequantWarps) * 32;
         reinterpret_cast<long long*>(p.partials)[(slot) * 256 + (j)] = t_; } } while (0)
 constexpr int kPanelStages = FLEXQ_GEMM_PANEL_STAGES;
 constexpr int kPanelCodes = kBN * kBK / 2;      // 8 KB: [k half (2)][column (256)][16 B = 32 codes]
-constexpr int kPanelBytes = kGemmPanelBytes;    // + 1 KB: [group (4)][k pair (32)][{scale pair, min pair}]
+constexpr int kPanelData = kPanelCodes + 1024;  // + 1 KB: [group (4)][k pair (32)][{scale pair, min pair}]
+constexpr int kPanelBytes = kGemmPanelBytes;    // per panel in the buffer and per smem stage: data + 16 B flag
+constexpr int kPanelFlag = kPanelData;          // smem stage offset of the flag; in global memory the flags
+                                                // follow all panels (panel data stays 1 KB-aligned)
 constexpr int kMaxAStages = 6;                 // A operand stages in TMEM (64 columns each)
 constexpr int kBStages = 6;                    // x stages in smem
 constexpr int kDoneSlots = 6;                  // ring of commit barriers, one per group of stages
@@ -174,6 +180,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(su32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -192,19 +203,22 @@ __device__ __forceinline__ void sts16(uint32_t a, __half v) {
 // The result is the tcgen05 A column word for that k pair (low half = even k).
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+template <bool CLAMP>
 __device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t mp) {
     uint32_t m;
     asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));   // (t & mask) | magic
     const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));                      // c (exact)
     const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
-    return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));                                 // <= 65504
+    if constexpr (CLAMP) return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));           // <= 65504
+    else return h2u(v);   // the panel's flag says no code can exceed 65504 (flexq_pack_weight)
 }
+template <bool CLAMP>
 __device__ __forceinline__ void deq_word(uint32_t w, uint4 meta_lo, uint4 meta_hi, uint32_t* o) {
     // meta_lo = {s01, m01, s23, m23}, meta_hi = {s45, m45, s67, m67}
-    o[0] = deq_pair(w, meta_lo.x, meta_lo.y);
-    o[1] = deq_pair(w >> 4, meta_lo.z, meta_lo.w);
-    o[2] = deq_pair(w >> 8, meta_hi.x, meta_hi.y);
-    o[3] = deq_pair(w >> 12, meta_hi.z, meta_hi.w);
+    o[0] = deq_pair<CLAMP>(w, meta_lo.x, meta_lo.y);
+    o[1] = deq_pair<CLAMP>(w >> 4, meta_lo.z, meta_lo.w);
+    o[2] = deq_pair<CLAMP>(w >> 8, meta_hi.x, meta_hi.y);
+    o[3] = deq_pair<CLAMP>(w >> 12, meta_hi.z, meta_hi.w);
 }
 
 // Store 16 rows (m0 .. m0+15) x 32 columns (n0 .. n0+31) of y from one warp: lane j holds
@@ -274,6 +288,11 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+template <bool B>
+struct BoolTag {
+    static constexpr bool value = B;
+};
+
 // Ring position without divisions (the issuing thread's instruction count is on the critical path).
 struct Ring {
     int slot = 0, n;
@@ -324,7 +343,8 @@ struct Sched {
 };
 
 struct GemmParams {
-    const uint8_t* panels;   // [tiles][KB][9216 B]
+    const uint8_t* panels;   // [tiles][KB][9216 B] panel data, then [tiles][KB][16 B] flags
+    int64_t n_panels;
     __half* y;               // [M][N]
     float* partials;         // [grid][256 (n)][mpad (m)]
     uint32_t* tickets;       // [remainder tiles]
@@ -344,7 +364,7 @@ __host__ __device__ inline Smem smem_plan(int mpad, bool pair) {
     Smem s;
     const uint32_t bstage = uint32_t(pair ? mpad / 2 : mpad) * 128u;   // x rows held by this CTA
     s.panel = 0;
-    s.b = s.panel + kPanelStages * kPanelBytes;      // 1024-aligned (8 * 9 KB)
+    s.b = (s.panel + kPanelStages * kPanelBytes + 1023u) / 1024u * 1024u;   // x stages: 1024-aligned (SW128)
     const uint32_t bs = kBStages;   // fixed-size plan: 8 * 9 KB + 6 * Mpad * 128 B + 4 KB + bars <= 227 KB
     s.b_stages = bs;
     s.epi = s.b + bs * bstage;
@@ -440,11 +460,14 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                 int tile, kb0, nk, part;
                 S.unit(c, u, tile, kb0, nk, part);
                 const int t256 = PAIR ? 2 * tile + int(rank) : tile;   // this CTA's 256-column tile
-                const uint8_t* src = p.panels + (int64_t(t256) * KB + kb0) * kPanelBytes;
-                for (int j = 0; j < nk; ++j, src += kPanelBytes) {
+                const int64_t pi0 = int64_t(t256) * KB + kb0;
+                const uint8_t* src = p.panels + pi0 * kPanelData;
+                const uint8_t* fsrc = p.panels + p.n_panels * kPanelData + pi0 * 16;
+                for (int j = 0; j < nk; ++j, src += kPanelData, fsrc += 16) {
                     mbar_wait(panel_empty + s, ph ^ 1);
                     mbar_expect_tx(panel_full + s, kPanelBytes);
-                    bulk_g2s(s_panel + uint32_t(s * kPanelBytes), src, kPanelBytes, panel_full + s, pol);
+                    bulk_g2s(s_panel + uint32_t(s * kPanelBytes), src, kPanelData, panel_full + s, pol);
+                    bulk_g2s(s_panel + uint32_t(s * kPanelBytes + kPanelFlag), fsrc, 16, panel_full + s, pol);
                     if (++s == kPanelStages) { s = 0; ph ^= 1; }
                 }
             }
@@ -581,23 +604,38 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                 prev.next();
             }
             const uint32_t pb = s_panel + uint32_t(ps * kPanelBytes);
+            const uint32_t clampf = lds32(pb + uint32_t(kPanelFlag));   // warp-uniform
             uint4 cw[kHalves];
 #pragma unroll
             for (int i = 0; i < kHalves; ++i) cw[i] = lds128(pb + uint32_t(hk0 + i) * 4096u + codes_off);
             if (warp == 8 && lane == 0) TRACE(6, it);
             tc_fence_after();
+            // the panel's clamp flag selects one of two fully unrolled copies of the conversion
+            auto convert = [&](auto clamp_tag) {
+                constexpr bool kClamp = decltype(clamp_tag)::value;
 #pragma unroll
-            for (int i = 0; i < kHalves; ++i) {
-                const int hk = hk0 + i;
-                const uint32_t words[4] = {cw[i].x, cw[i].y, cw[i].z, cw[i].w};
-                uint32_t o[16];
+                for (int i = 0; i < kHalves; ++i) {
+                    const int hk = hk0 + i;
+                    const uint32_t words[4] = {cw[i].x, cw[i].y, cw[i].z, cw[i].w};
+                    uint32_t o[16];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t mo = pb + meta_off + uint32_t((16 * hk + 4 * j) * 8);
-                    deq_word(words[j], lds128(mo), lds128(mo + 16), o + 4 * j);
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t mo = pb + meta_off + uint32_t((16 * hk + 4 * j) * 8);
+#if FLEXQ_GEMM_PROBE == 2     // tuning only (wrong results): no dequant arithmetic, no meta loads
+                        o[4 * j] = words[j]; o[4 * j + 1] = words[j] >> 8; o[4 * j + 2] = words[j] >> 16;
+                        o[4 * j + 3] = mo;
+#else
+                        deq_word<kClamp>(words[j], lds128(mo), lds128(mo + 16), o + 4 * j);
+#endif
+                    }
+#if FLEXQ_GEMM_PROBE == 1     // tuning only (wrong results): no TMEM writes
+                    if (o[0] == 0x12345678u && o[15] == 0x9abcdef0u)
+#endif
+                    tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
                 }
-                tmem_st16(a_lane + uint32_t(as) * 64u + uint32_t(hk) * 16u, o);
-            }
+            };
+            if (clampf) convert(BoolTag<true>{});
+            else convert(BoolTag<false>{});
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -739,8 +777,10 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, uint8_t* __
             const int pos = (e & 1) ? 4 + (e >> 1) : (e >> 1);
             w[j] |= c << (4 * pos);
         }
-        uint4* dst = reinterpret_cast<uint4*>(panels + panel * kPanelBytes + hk * 4096 + col * 16);
+        uint4* dst = reinterpret_cast<uint4*>(panels + panel * kPanelData + hk * 4096 + col * 16);
         *dst = make_uint4(w[0], w[1], w[2], w[3]);
+        if (hk == 0 && col == 0)   // the panel's flag; pack_meta_kernel (next in the stream) ORs into it
+            *reinterpret_cast<uint4*>(panels + (N / kBN) * KB * kPanelData + panel * 16) = make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -759,8 +799,14 @@ __global__ void pack_meta_kernel(const __half2* __restrict__ meta, uint8_t* __re
         const __half2 a = meta[k * G + gg], b = meta[(k + 1) * G + gg];
         const __half2 sp = __halves2half2(__low2half(a), __low2half(b));    // scales of k, k+1
         const __half2 mp = __halves2half2(__high2half(a), __high2half(b));  // mins of k, k+1
-        uint2* dst = reinterpret_cast<uint2*>(panels + panel * kPanelBytes + kPanelCodes + (g * 32 + kp) * 8);
+        uint2* dst = reinterpret_cast<uint2*>(panels + panel * kPanelData + kPanelCodes + (g * 32 + kp) * 8);
         *dst = make_uint2(h2u(sp), h2u(mp));
+        // clamp flag: some code of this panel may reconstruct above 65504 (c = 15 is the largest
+        // value, 15 * scale + min, exact in double), so its fp16 FMA needs the clamp of reading R
+        const double top0 = 15.0 * double(__low2float(a)) + double(__high2float(a));
+        const double top1 = 15.0 * double(__low2float(b)) + double(__high2float(b));
+        if (top0 > 65504.0 || top1 > 65504.0)
+            atomicOr(reinterpret_cast<unsigned int*>(panels + (N / kBN) * KB * kPanelData + panel * 16), 1u);
     }
 }
 
@@ -885,6 +931,7 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
             return cudaErrorInvalidValue;
         GemmParams p;
         p.panels = static_cast<const uint8_t*>(panels);
+        p.n_panels = int64_t(N / kBN) * kb;
         p.y = static_cast<__half*>(y) + m0 * N;
         p.partials = partials;
         p.tickets = tickets;

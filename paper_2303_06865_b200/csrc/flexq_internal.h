@@ -70,7 +70,7 @@ cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream)
 constexpr int kGemmMaxRows = 160;
 constexpr int kGemmTileN = 256;
 constexpr int kGemmTileK = 64;
-constexpr int kGemmPanelBytes = kGemmTileN * kGemmTileK / 2 + 4 * 32 * 8;   // 9216
+constexpr int kGemmPanelBytes = kGemmTileN * kGemmTileK / 2 + 4 * 32 * 8 + 16;   // 9232: codes, meta, flag
 constexpr int kGemmMaxGrid = 160;   // persistent CTAs (one per SM, B200: 148)
 size_t gemm_panel_bytes(int64_t k, int64_t n);
 cudaError_t launch_pack_weight(const void* codes, const void* meta, int64_t k, int64_t n, void* panels,

@@ -150,8 +150,9 @@ def test_dequant_gemm_validation(L):
     assert ws > 0
     assert L.flexq_dequant_gemm_workspace_size(144, 12288, 49152, 4, 32) == 0
     assert L.flexq_dequant_gemm_workspace_size(144, 100, 49152, 4, 64) == 0
-    # panels are a re-layout: exactly the bytes of codes + meta
-    assert L.flexq_gemm_panel_bytes(12288, 49152, 4, 64) == 12288 * 49152 // 2 + 12288 * 49152 // 64 * 4
+    # panels are a re-layout: the bytes of codes + meta, plus a 16-byte flag trailer per panel
+    assert L.flexq_gemm_panel_bytes(12288, 49152, 4, 64) == (12288 * 49152 // 2 + 12288 * 49152 // 64 * 4
+                                                             + 16 * (49152 // 256) * (12288 // 64))
     assert L.flexq_gemm_panel_bytes(12288, 100, 4, 64) == 0
 
     def call(m=144, k=12288, n=49152, x=A, pn=A, y=A, w=A, wb=ws, b=4, g=64):

@@ -120,10 +120,12 @@ def test_dequant_gemm_one_hot_rows_are_dequantize(cuda):
     assert int((ulps > 0).sum()) <= K * N // 10000
 
 
-def test_pack_weight_layout(cuda):
-    """flexq_pack_weight is a pure re-layout: rebuild it in numpy from the documented layout."""
+@pytest.mark.parametrize("kind", ["normal", "extreme"])
+def test_pack_weight_layout(cuda, kind):
+    """flexq_pack_weight is a pure re-layout (plus the clamp-flag trailer): rebuild it in numpy from
+    the documented layout, for ordinary weights (flag 0) and +-65504 groups (flag 1 where needed)."""
     K, N = 128, 512
-    w = weights(4205, K, N)
+    w = weights(4205, K, N) if kind == "normal" else synth.extreme(4205, 9, K, N)
     panels, codes, meta = quantized(w, cuda)
     P = panels.cpu().numpy()
     c = codes.cpu().numpy()
@@ -135,7 +137,14 @@ def test_pack_weight_layout(cuda):
     pos_of = [0, 4, 1, 5, 2, 6, 3, 7]                  # nibble position of k offset e in a word
     for t in range(N // 256):
         for kb in range(KB):
-            blob = P[(t * KB + kb) * 9216:(t * KB + kb + 1) * 9216]
+            pi = t * KB + kb
+            blob = P[pi * 9216:(pi + 1) * 9216]
+            # flag (after all panels): some code may reconstruct above 65504 (15 * scale + min > 65504)
+            flag = P[(N // 256) * KB * 9216 + pi * 16:(N // 256) * KB * 9216 + (pi + 1) * 16]
+            sc = mt[kb * 64:(kb + 1) * 64, t * 4:(t + 1) * 4, 0].view(np.float16).astype(np.float64)
+            mn = mt[kb * 64:(kb + 1) * 64, t * 4:(t + 1) * 4, 1].view(np.float16).astype(np.float64)
+            assert flag[:4].view(np.uint32)[0] == int((15 * sc + mn > 65504).any())
+            assert not flag[4:].any()
             words = blob[:8192].view(np.uint32).reshape(2, 256, 4)
             for hk in range(2):
                 for j in range(4):
@@ -144,7 +153,7 @@ def test_pack_weight_layout(cuda):
                     for e in range(8):
                         ref |= full[k0 + e, t * 256:(t + 1) * 256].astype(np.uint32) << (4 * pos_of[e])
                     assert np.array_equal(words[hk, :, j], ref)
-            mb = blob[8192:].view(np.uint16).reshape(4, 32, 2, 2)   # [g][kp][scale|min pair][k, k+1]
+            mb = blob[8192:9216].view(np.uint16).reshape(4, 32, 2, 2)   # [g][kp][scale|min pair][k, k+1]
             for g in range(4):
                 for kp in range(32):
                     k = kb * 64 + 2 * kp
