@@ -28,6 +28,7 @@ SOURCES = {
     "quant.cu": ["-fmad=false", "-prec-div=true", "-ftz=false"],
     "decode_attention.cu": [],
     "decode_attention_topk.cu": [],
+    "decode_attention_variants.cu": [],
     "dequant_gemm.cu": [],
 }
 

@@ -1,0 +1,295 @@
+// decode_attention_variants.cu -- decode attention over the b in {2, 3, 4, 8} x g in {32, 64, 128}
+// KV caches (SURVEY 8(f) NEXT-3 variants; the b = 4, g = 64 cache has its own tensor-core kernel,
+// decode_attention.cu).
+//
+// The method is the same (P:271-274 with the cache dequantized as in P:845, reading M):
+//   out = softmax(q . K^[0:cur_len]^T / sqrt(D)) . V^[0:cur_len],  K^, V^ = fmaf(c, scale, min)
+// Cache layout (include/flexq.h): 32-token chunks [codes 32 x CB][meta 32 x MB] per (b, h), CB =
+// D b / 8 (each token's row a little-endian bit stream, K and V alike), MB = 4 D / g.
+//
+// Mapping: one 128-thread CTA per (head, split); a split is a run of 128-token tiles (4 chunks).
+// Per tile:
+//   K pass  -- thread i owns token t0 + i: its code row and meta come straight from global memory
+//              (a warp reads 32 consecutive rows, so the lines are fully used through L1), and
+//              score = sum_g (scale_g sum_{d in g} q_d c_d + min_g sum_{d in g} q_d) in fp32, q from
+//              shared memory (broadcast reads); the per-group factoring is the exact identity of
+//              sum_d q_d (c_d s_g + m_g) (reordered fp32 rounding, within reading Q).
+//   softmax -- block max, p = 2^(score - max) (log2 domain), running (max, sum) per CTA.
+//   V pass  -- the V tile (4 chunks, contiguous) was staged into shared memory with cp.async while
+//              the K pass ran; warp w takes chunk w's 32 tokens, lane l the D / 32 dims at bit
+//              l (D / 32) b of the row (one funnel shift out of two words), and accumulates
+//              acc_d += (p s_g) c_d and acc_m += p m_g (the same identity).
+// Splits > 1 write (max, sum, acc[D]) partials to the workspace and a combine kernel merges them.
+// CUDA cores only: these variants are HBM-bound like the b = 4 path but are not the headline
+// configuration, so they trade the tensor-core passes for one generic kernel per (b, g, D).
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "flexq_internal.h"
+
+namespace flexq {
+namespace {
+
+constexpr int kVThreads = 128;
+
+struct VarParams {
+    const __half* q;
+    const uint8_t* kc;
+    const uint8_t* vc;
+    __half* out;
+    float* part;          // [bh][splits][D + 2] (splits > 1)
+    int64_t chunks;       // chunks per (b, h)
+    int cur_len, tiles_per_split, splits;
+    float scale_log2;     // log2(e) / sqrt(D)
+};
+
+__device__ __forceinline__ float code_f(uint32_t c) {   // exact: 2^23 + c - 2^23
+    return __fsub_rn(__uint_as_float(c | 0x4B000000u), 8388608.0f);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int B, int G, int D>
+__global__ void __launch_bounds__(kVThreads)
+attention_variant_kernel(VarParams p) {
+    constexpr int CB = D * B / 8, MB = 4 * D / G, NG = D / G, CHB = kChunk * (CB + MB);
+    constexpr int NWR = CB / 4;                   // code words per token row
+    constexpr uint32_t kMask = (1u << B) - 1u;
+    constexpr int DPL = D / 32;                   // V pass: dims per lane
+    static_assert(DPL * B <= 32, "a lane's V codes fit one funnel-shifted word");
+
+    __shared__ __align__(16) float q_s[D];
+    __shared__ float qg_s[NG];
+    __shared__ float p_s[kVarTile];
+    __shared__ float red_s[kVThreads / 32];
+    __shared__ __align__(16) uint8_t vbuf[4 * CHB];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t bh = blockIdx.x;
+    const int split = blockIdx.y;
+    const int n_tiles = (p.cur_len + kVarTile - 1) / kVarTile;
+    const int tile_a = split * p.tiles_per_split;
+    const int tile_b = min(tile_a + p.tiles_per_split, n_tiles);
+
+    for (int d = tid; d < D; d += kVThreads) q_s[d] = __half2float(p.q[bh * D + d]);
+    __syncthreads();
+    if (tid < NG) {
+        float s = 0.0f;
+        for (int d = 0; d < G; ++d) s += q_s[tid * G + d];
+        qg_s[tid] = s;
+    }
+    __syncthreads();
+
+    const uint8_t* kbase = p.kc + bh * p.chunks * CHB;
+    const uint8_t* vbase = p.vc + bh * p.chunks * CHB;
+    const int vbit = lane * DPL * B, vwi = vbit >> 5, vsh = vbit & 31, vgi = lane * DPL / G;
+
+    float m_run = -INFINITY, l_part = 0.0f, acc[DPL], acc_m = 0.0f;
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[e] = 0.0f;
+
+    for (int tile = tile_a; tile < tile_b; ++tile) {
+        const int t0 = tile * kVarTile;
+        const int tcount = min(kVarTile, p.cur_len - t0);
+        // stage the V tile (whole chunks holding valid tokens) while the K pass runs
+        {
+            const int nch = (tcount + kChunk - 1) / kChunk;
+            const uint8_t* src = vbase + int64_t(t0 / kChunk) * CHB;
+            for (int i = tid; i < nch * CHB / 16; i += kVThreads) cp_async16(vbuf + 16 * i, src + 16 * i);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // K pass: thread tid owns token t0 + tid
+        float score = -INFINITY;
+        if (tid < tcount) {
+            const int t = t0 + tid;
+            const uint8_t* chunk = kbase + int64_t(t / kChunk) * CHB;
+            const int slot = t & (kChunk - 1);
+            uint32_t w[NWR + 1];
+            const uint8_t* row = chunk + slot * CB;
+            if constexpr (CB % 16 == 0) {
+#pragma unroll
+                for (int i = 0; i < CB / 16; ++i) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(row + 16 * i);
+                    w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < CB / 8; ++i) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(row + 8 * i);
+                    w[2 * i] = v.x; w[2 * i + 1] = v.y;
+                }
+            }
+            w[NWR] = 0;
+            const __half2* meta = reinterpret_cast<const __half2*>(chunk + kChunk * CB + slot * MB);
+            float s = 0.0f;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                float dot[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int dd = 0; dd < G; dd += 4) {
+                    const float4 qq = *reinterpret_cast<const float4*>(&q_s[gi * G + dd]);
+                    const float qv[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int bit = (gi * G + dd + e) * B, wi = bit >> 5, sh = bit & 31;
+                        uint32_t c = w[wi] >> sh;
+                        if (sh + B > 32) c |= w[wi + 1] << (32 - sh);
+                        dot[e] = fmaf(qv[e], code_f(c & kMask), dot[e]);
+                    }
+                }
+                const float2 sm = __half22float2(meta[gi]);
+                s = fmaf(sm.x, (dot[0] + dot[1]) + (dot[2] + dot[3]), fmaf(sm.y, qg_s[gi], s));
+            }
+            score = s * p.scale_log2;
+        }
+        // block max -> running max, probabilities
+        float mx = score;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) red_s[warp] = mx;
+        __syncthreads();
+        mx = fmaxf(fmaxf(red_s[0], red_s[1]), fmaxf(red_s[2], red_s[3]));
+        const float m_new = fmaxf(m_run, mx);
+        const float alpha = exp2f(m_run - m_new);
+        const float pt = (tid < tcount) ? exp2f(score - m_new) : 0.0f;
+        p_s[tid] = pt;
+        l_part = fmaf(l_part, alpha, pt);
+        m_run = m_new;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] *= alpha;
+        acc_m *= alpha;
+        cp_async_wait_all();
+        __syncthreads();
+        // V pass: warp w takes chunk w of the tile
+        const int nj = min(kChunk, tcount - warp * kChunk);
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(vbuf + warp * CHB);
+        const __half2* mw = reinterpret_cast<const __half2*>(vbuf + warp * CHB + kChunk * CB);
+        for (int j = 0; j < nj; ++j) {
+            uint32_t x = cw[j * NWR + vwi];
+            if constexpr ((DPL * B) % 32 != 0) x = __funnelshift_r(x, cw[j * NWR + vwi + 1], vsh);
+            const float pj = p_s[warp * kChunk + j];
+            const float2 sm = __half22float2(mw[j * NG + vgi]);
+            const float ps = pj * sm.x;
+            acc_m = fmaf(pj, sm.y, acc_m);
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) acc[e] = fmaf(ps, code_f((x >> (e * B)) & kMask), acc[e]);
+        }
+        __syncthreads();   // vbuf / p_s are rewritten by the next tile
+    }
+
+    // combine the 4 warps' partial sums (all share m_run)
+    float* comb = reinterpret_cast<float*>(vbuf);
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) comb[warp * D + lane * DPL + e] = acc[e] + acc_m;
+    float l = l_part;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) red_s[warp] = l;
+    __syncthreads();
+    l = (red_s[0] + red_s[1]) + (red_s[2] + red_s[3]);
+    for (int d = tid; d < D; d += kVThreads) {
+        const float o = (comb[d] + comb[D + d]) + (comb[2 * D + d] + comb[3 * D + d]);
+        if (p.splits == 1) {
+            p.out[bh * D + d] = __float2half_rn(o / l);
+        } else {
+            float* part = p.part + (bh * p.splits + split) * (D + 2);
+            if (d == 0) {
+                part[0] = m_run;
+                part[1] = l;
+            }
+            part[2 + d] = o;
+        }
+    }
+}
+
+// out = sum_i 2^(m_i - m) acc_i / sum_i 2^(m_i - m) l_i over the splits of one head
+template <int D>
+__global__ void __launch_bounds__(D)
+attention_variant_combine(const float* __restrict__ part, __half* __restrict__ out, int splits) {
+    const int64_t bh = blockIdx.x;
+    const int d = threadIdx.x;
+    const float* pp = part + bh * splits * (D + 2);
+    float m = -INFINITY;
+    for (int i = 0; i < splits; ++i) m = fmaxf(m, pp[i * (D + 2)]);
+    float num = 0.0f, den = 0.0f;
+    for (int i = 0; i < splits; ++i) {
+        const float w = exp2f(pp[i * (D + 2)] - m);
+        den = fmaf(w, pp[i * (D + 2) + 1], den);
+        num = fmaf(w, pp[i * (D + 2) + 2 + d], num);
+    }
+    out[bh * D + d] = __float2half_rn(num / den);
+}
+
+int sm_count() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <int B, int G, int D>
+cudaError_t launch_var(const AttnArgs& a, cudaStream_t stream) {
+    const int64_t bhs = int64_t(a.batch) * a.heads;
+    const int n_tiles = (a.cur_len + kVarTile - 1) / kVarTile;
+    const int64_t target = int64_t(sm_count()) * 8;                   // CTAs to fill the GPU
+    int want = int((target + bhs - 1) / bhs);
+    if (want > n_tiles) want = n_tiles;
+    if (want < 1) want = 1;
+    const int tps = (n_tiles + want - 1) / want;
+    const int splits = (n_tiles + tps - 1) / tps;
+    VarParams p;
+    p.q = static_cast<const __half*>(a.q);
+    p.kc = static_cast<const uint8_t*>(a.k_cache);
+    p.vc = static_cast<const uint8_t*>(a.v_cache);
+    p.out = static_cast<__half*>(a.out);
+    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + 256);
+    p.chunks = a.chunks;
+    p.cur_len = a.cur_len;
+    p.tiles_per_split = tps;
+    p.splits = splits;
+    p.scale_log2 = 1.4426950408889634f / sqrtf(float(D));
+    attention_variant_kernel<B, G, D><<<dim3(unsigned(bhs), unsigned(splits)), kVThreads, 0, stream>>>(p);
+    if (splits > 1) attention_variant_combine<D><<<unsigned(bhs), D, 0, stream>>>(p.part, p.out, splits);
+    return cudaGetLastError();
+}
+
+template <int B, int G>
+cudaError_t launch_var_d(const AttnArgs& a, cudaStream_t stream) {
+    if (a.head_dim == 128) return launch_var<B, G, 128>(a, stream);
+    if constexpr (G <= 64) return launch_var<B, G, 64>(a, stream);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+size_t attention_variant_workspace_bytes(int batch, int heads, int head_dim, int t_cap) {
+    const size_t tiles = size_t((t_cap + kVarTile - 1) / kVarTile);
+    return 256 + (size_t(batch) * heads * tiles * size_t(head_dim + 2) * 4 + 15) / 16 * 16;
+}
+
+cudaError_t launch_decode_attention_variant(const AttnArgs& a, int bits, int group, cudaStream_t stream) {
+    switch (bits * 1000 + group) {
+        case 2032: return launch_var_d<2, 32>(a, stream);
+        case 2064: return launch_var_d<2, 64>(a, stream);
+        case 2128: return launch_var_d<2, 128>(a, stream);
+        case 3032: return launch_var_d<3, 32>(a, stream);
+        case 3064: return launch_var_d<3, 64>(a, stream);
+        case 3128: return launch_var_d<3, 128>(a, stream);
+        case 4032: return launch_var_d<4, 32>(a, stream);
+        case 4128: return launch_var_d<4, 128>(a, stream);
+        case 8032: return launch_var_d<8, 32>(a, stream);
+        case 8064: return launch_var_d<8, 64>(a, stream);
+        case 8128: return launch_var_d<8, 128>(a, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace flexq

@@ -22,10 +22,19 @@ flexq_status check_kv_dims(int batch, int heads, int head_dim, int prompt_len, i
     if (batch < 1 || heads < 1 || head_dim < 1 || prompt_len < 0 || gen_len < 0 ||
         int64_t(prompt_len) + gen_len < 1 || int64_t(prompt_len) + gen_len > INT32_MAX - flexq::kChunk)
         return FLEXQ_ERR_ARG;
-    flexq_status s = check_bits_group(bits, group_size);
-    if (s != FLEXQ_OK) return s;
+    if (bits < 1 || bits > 8 || group_size < 1) return FLEXQ_ERR_ARG;
+    if (!flexq::quant_variant_built(bits, group_size)) return FLEXQ_ERR_UNSUPPORTED;
     if (head_dim != 64 && head_dim != 128) return FLEXQ_ERR_UNSUPPORTED;
+    if (head_dim % group_size != 0) return FLEXQ_ERR_UNSUPPORTED;
     return FLEXQ_OK;
+}
+
+// b = 4, g = 64 runs the tensor-core kernels; the other built (b, g) the variant kernels
+bool is_variant(int bits, int group_size) { return bits != flexq::kBits || group_size != flexq::kGroup; }
+
+size_t attn_ws_bytes(int batch, int heads, int head_dim, int t_cap, int bits, int group_size) {
+    return is_variant(bits, group_size) ? flexq::attention_variant_workspace_bytes(batch, heads, head_dim, t_cap)
+                                        : flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap);
 }
 
 flexq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FLEXQ_OK : FLEXQ_ERR_CUDA; }
@@ -91,7 +100,7 @@ flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt
     if (s != FLEXQ_OK) return s;
     const int64_t stride = flexq::kv_token_stride(int64_t(prompt_len) + gen_len);
     if (cache_bytes)
-        *cache_bytes = size_t(batch) * heads * size_t(stride / flexq::kChunk) * size_t(flexq::kv_chunk_bytes(head_dim));
+        *cache_bytes = size_t(batch) * heads * size_t(stride / flexq::kChunk) * size_t(flexq::kv_chunk_bytes(head_dim, bits, group_size));
     if (token_stride) *token_stride = int(stride);
     return FLEXQ_OK;
 }
@@ -110,14 +119,14 @@ flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int b
     const int64_t rows = int64_t(batch) * heads * n_new;
     if (rows * (head_dim / group_size) >= (int64_t(1) << 31)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     const flexq::KvDst d{n_new, pos, flexq::kv_token_stride(t_cap) / flexq::kChunk};
-    return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, k_cache, v_cache, d,
+    return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, bits, group_size, k_cache, v_cache, d,
                                              static_cast<cudaStream_t>(stream)));
 }
 
 size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
                                              int gen_len, int bits, int group_size) {
     if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
-    return flexq::attention_workspace_bytes(batch, heads, head_dim, prompt_len + gen_len);
+    return attn_ws_bytes(batch, heads, head_dim, prompt_len + gen_len, bits, group_size);
 }
 
 flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, const void* v_cache, int batch,
@@ -133,11 +142,13 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, cons
     if (!q_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
     if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap};
+    if (is_variant(bits, group_size))
+        return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
@@ -155,11 +166,19 @@ flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_
     if (!aligned16(q_f16) || !aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_cache) ||
         !aligned16(v_cache) || !aligned16(out_f16))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap, k_new_f16, v_new_f16};
+    if (is_variant(bits, group_size)) {   // variants: the append kernel, then the attention kernel
+        const flexq::KvDst d{1, cur_len - 1, a.chunks};
+        cudaError_t e = flexq::launch_append_kv(k_new_f16, v_new_f16, int64_t(batch) * heads, head_dim, bits,
+                                                group_size, k_cache, v_cache, d, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return FLEXQ_ERR_CUDA;
+        a.k_new = a.v_new = nullptr;
+        return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
+    }
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
@@ -172,12 +191,13 @@ flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache,
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap || keep < 1 || keep > cur_len) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
+    if (is_variant(bits, group_size)) return FLEXQ_ERR_UNSUPPORTED;   // Top-K: b = 4, g = 64 only
     if (cur_len > flexq::kTopkMaxTokens) return FLEXQ_ERR_UNSUPPORTED;
     if (!q_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
     if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16) ||
         (sel_i32 && !aligned16(sel_i32)))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap))
+    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::TopkArgs a{q_f16, k_cache, v_cache, out_f16, sel_i32, workspace, batch, heads, head_dim,

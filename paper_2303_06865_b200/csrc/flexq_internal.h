@@ -14,7 +14,9 @@ constexpr int kGroup = 64;
 // head), a run of chunks of kChunk tokens; chunk = [codes kChunk x D/2][meta kChunk x D/16].
 constexpr int kChunk = 32;
 inline int64_t kv_token_stride(int64_t t_cap) { return (t_cap + kChunk - 1) / kChunk * kChunk; }
-inline int64_t kv_chunk_bytes(int64_t d) { return int64_t(kChunk) * (d / 2 + d / 16); }   // 18 d
+inline int64_t kv_chunk_bytes(int64_t d, int bits = kBits, int group = kGroup) {   // 18 d at b = 4, g = 64
+    return int64_t(kChunk) * (d * bits / 8 + 4 * d / group);
+}
 
 // Destination of a KV append: source rows are (bh, t) with t in [0, n_new),
 // written at token pos + t of head bh.
@@ -31,8 +33,8 @@ inline bool quant_variant_built(int bits, int group) {
 }
 cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits, int group, void* codes, void* meta,
                             cudaStream_t stream);
-cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
-                             void* v_cache, KvDst dst, cudaStream_t stream);
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, int bits, int group,
+                             void* k_cache, void* v_cache, KvDst dst, cudaStream_t stream);
 cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols, int bits, int group,
                               void* out, cudaStream_t stream);
 
@@ -49,6 +51,12 @@ struct AttnArgs {
 
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
+
+// Decode attention over the (b, g) variant caches (NEXT-3; decode_attention_variants.cu):
+// token-major bit-stream rows for K and V, CUDA-core arithmetic, split-K over 128-token tiles.
+constexpr int kVarTile = 128;
+size_t attention_variant_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
+cudaError_t launch_decode_attention_variant(const AttnArgs& a, int bits, int group, cudaStream_t stream);
 
 // Top-K sparse attention: one warp per (b, h), so the context is
 // bounded by the per-warp score buffer.

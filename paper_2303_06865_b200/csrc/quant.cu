@@ -321,10 +321,45 @@ __device__ __forceinline__ void store_bits(uint8_t* p, uint64_t lo, uint64_t hi)
     }
 }
 
+// Destination of group g's codes (lane `part`'s 2b bytes) and half2 meta.  Plain tensors:
+// [rows][cols * b / 8] bit-stream rows and [rows][cols / g] meta.
 template <int B, int G>
+struct PlainBitsDst {
+    __device__ __forceinline__ void operator()(int64_t g, int part, int64_t& co, int64_t& mo) const {
+        co = (g * G + part * 16) * B / 8;
+        mo = g * 4;
+    }
+};
+// KV append of the variants: the chunked cache layout of include/flexq.h with CB = D b / 8 code
+// bytes (the token's row as a little-endian bit stream, K and V alike) and MB = 4 D / g meta
+// bytes per token; chunk = [codes 32 x CB][meta 32 x MB].  Source row r = bh * n_new + t goes to
+// token pos + t of head bh.
+template <int B, int G>
+struct KvBitsDst {
+    int64_t pos, chunks;
+    FastDiv nnew;
+    int gpr_log2, cb, mb;
+    __device__ __forceinline__ void operator()(int64_t g, int part, int64_t& co, int64_t& mo) const {
+        const uint32_t row = uint32_t(g >> gpr_log2), k = uint32_t(g) & ((1u << gpr_log2) - 1u);
+        const uint32_t bh = nnew.div(row);
+        const int64_t t = pos + (row - bh * nnew.d);
+        const int64_t base = (int64_t(bh) * chunks + (t >> 5)) * (kChunk * (cb + mb));
+        const int slot = int(t & (kChunk - 1));
+        co = base + slot * cb + (int64_t(k) * G + part * 16) * B / 8;
+        mo = base + kChunk * cb + slot * mb + k * 4;
+    }
+};
+
+// blockIdx.y selects source x0 -> (codes0, meta0) or x1 -> (codes1, meta1) (byte bases)
+template <int B, int G, class Dst>
 __global__ void __launch_bounds__(kThreads)
-quantize_generic_kernel(const __half* __restrict__ x, uint8_t* __restrict__ codes, uint8_t* __restrict__ meta,
-                        int64_t groups) {
+quantize_generic_kernel(const __half* __restrict__ x0, const __half* __restrict__ x1, uint8_t* __restrict__ codes0,
+                        uint8_t* __restrict__ meta0, uint8_t* __restrict__ codes1, uint8_t* __restrict__ meta1,
+                        int64_t groups, Dst dst) {
+    const int kv = blockIdx.y;
+    const __half* x = kv ? x1 : x0;
+    uint8_t* codes = kv ? codes1 : codes0;
+    uint8_t* meta = kv ? meta1 : meta0;
     constexpr int L = G / 16;                     // lanes per group
     constexpr float kLevels = float((1 << B) - 1);
     const int lane = threadIdx.x & 31;
@@ -390,8 +425,10 @@ quantize_generic_kernel(const __half* __restrict__ x, uint8_t* __restrict__ code
                 }
             }
         }
-        store_bits<B>(codes + (g * G + part * 16) * B / 8, plo, phi);
-        if (part == 0) *reinterpret_cast<__half2*>(meta + g * 4) = __halves2half2(scale16, __float2half_rn(mn));
+        int64_t co, mo;
+        dst(g, part, co, mo);
+        store_bits<B>(codes + co, plo, phi);
+        if (part == 0) *reinterpret_cast<__half2*>(meta + mo) = __halves2half2(scale16, __float2half_rn(mn));
     }
 }
 
@@ -457,8 +494,27 @@ cudaError_t launch_quantize_bg(const void* x, int64_t groups, void* codes, void*
     int64_t blocks = (groups * (G / 16) + kThreads - 1) / kThreads;
     const int64_t cap = int64_t(num_sms()) * 8;
     if (blocks > cap) blocks = cap;
-    quantize_generic_kernel<B, G><<<unsigned(blocks), kThreads, 0, stream>>>(
-        static_cast<const __half*>(x), static_cast<uint8_t*>(codes), static_cast<uint8_t*>(meta), groups);
+    uint8_t* c = static_cast<uint8_t*>(codes);
+    uint8_t* m = static_cast<uint8_t*>(meta);
+    quantize_generic_kernel<B, G, PlainBitsDst<B, G>><<<unsigned(blocks), kThreads, 0, stream>>>(
+        static_cast<const __half*>(x), nullptr, c, m, nullptr, nullptr, groups, PlainBitsDst<B, G>{});
+    return cudaGetLastError();
+}
+template <int B, int G>
+cudaError_t launch_append_kv_bg(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
+                                void* v_cache, KvDst d, cudaStream_t stream) {
+    const int64_t groups = rows * (head_dim / G);
+    int64_t blocks = (groups * (G / 16) + kThreads - 1) / kThreads;
+    const int64_t cap = int64_t(num_sms()) * 8;
+    if (blocks > cap) blocks = cap;
+    int gl = 0;
+    while ((G << gl) < head_dim) ++gl;
+    const KvBitsDst<B, G> dst{d.pos, d.chunks, FastDiv::make(uint32_t(d.n_new)), gl, head_dim * B / 8,
+                              4 * head_dim / G};
+    uint8_t* kc = static_cast<uint8_t*>(k_cache);
+    uint8_t* vc = static_cast<uint8_t*>(v_cache);
+    quantize_generic_kernel<B, G, KvBitsDst<B, G>><<<dim3(unsigned(blocks), 2u), kThreads, 0, stream>>>(
+        static_cast<const __half*>(k), static_cast<const __half*>(v), kc, kc, vc, vc, groups, dst);
     return cudaGetLastError();
 }
 template <int B, int G>
@@ -501,10 +557,15 @@ cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits,
     return cudaGetLastError();
 }
 
-cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, void* k_cache,
-                             void* v_cache, KvDst d, cudaStream_t stream) {
+cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, int bits, int group,
+                             void* k_cache, void* v_cache, KvDst d, cudaStream_t stream) {
+    if (rows == 0) return cudaSuccess;
+    if (bits != kBits || group != kGroup) {
+#define A_CALL(b, g) launch_append_kv_bg<b, g>(k, v, rows, head_dim, k_cache, v_cache, d, stream)
+        FLEXQ_BG_SWITCH(bits, group, A_CALL)
+#undef A_CALL
+    }
     const int64_t groups = rows * (head_dim / kGroup);
-    if (groups == 0) return cudaSuccess;
     int64_t blocks = (groups * 4 + kThreads - 1) / kThreads;
     const int64_t cap = int64_t(num_sms()) * 8;
     if (blocks > cap) blocks = cap;

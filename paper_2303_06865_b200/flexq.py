@@ -131,7 +131,8 @@ def token_stride(t_cap: int) -> int:
 
 class KVCache:
     """One layer's compressed KV cache in the chunked layout of include/flexq.h:
-    `k` and `v` are u8 [B][H][T_stride/32][18*D], chunk = [codes 32 x D/2][meta 32 x D/16]
+    `k` and `v` are u8 [B][H][T_stride/32][32*(CB+MB)], chunk = [codes 32 x CB][meta 32 x MB], CB = D*bits/8,
+    MB = 4*D/group (18*D per chunk at bits 4, group 64)
     (K codes token-major, V codes quad-interleaved).
     The *_codes() / *_meta() accessors are layout views (copies) for tests and
     inspection, over tokens [0, T_stride)."""
@@ -144,7 +145,10 @@ class KVCache:
         self.t_cap = prompt_len + gen_len
         self.t_stride = token_stride(self.t_cap)
         self.chunks = self.t_stride // CHUNK
-        self.k = torch.zeros(batch, heads, self.chunks, 18 * head_dim, dtype=torch.uint8, device=device)
+        self.code_bytes = head_dim * bits // 8          # CB: one token's codes (bit stream)
+        self.meta_bytes = 4 * head_dim // group_size     # MB: one token's half2 (scale, min) per group
+        self.k = torch.zeros(batch, heads, self.chunks, CHUNK * (self.code_bytes + self.meta_bytes),
+                             dtype=torch.uint8, device=device)
         self.v = torch.zeros_like(self.k)
 
     def nbytes(self) -> int:
@@ -155,11 +159,15 @@ class KVCache:
         x = buf[..., offset:offset + CHUNK * per_token].reshape(B, H, NC, CHUNK, per_token)
         return x.reshape(B, H, NC * CHUNK, per_token)
 
-    def _codes(self, buf) -> torch.Tensor:        # u8 [B][H][T_stride][D/2]
-        return self._part(buf, 0, self.head_dim // 2)
+    def variant(self) -> bool:
+        """(bits, group) other than P:846's (4, 64): token-major K and V rows, variant kernels."""
+        return (self.bits, self.group_size) != (BITS, GROUP)
 
-    def _meta(self, buf) -> torch.Tensor:         # fp16 [B][H][T_stride][D/64][2] = (scale, min)
-        m = self._part(buf, CHUNK * self.head_dim // 2, self.head_dim // 16)
+    def _codes(self, buf) -> torch.Tensor:        # u8 [B][H][T_stride][D*bits/8]
+        return self._part(buf, 0, self.code_bytes)
+
+    def _meta(self, buf) -> torch.Tensor:         # fp16 [B][H][T_stride][D/g][2] = (scale, min)
+        m = self._part(buf, CHUNK * self.code_bytes, self.meta_bytes)
         return m.contiguous().view(torch.float16).view(self.batch, self.heads, self.t_stride, -1, 2)
 
     def k_codes(self):
@@ -169,6 +177,8 @@ class KVCache:
         """V codes as token-major rows.  In memory each chunk's V codes are
         quad-interleaved and swizzled: word (quad, column pair i ^ ((quad & 3) << 3)) holds
         token 4 quad + k in byte k (include/flexq.h)."""
+        if self.variant():
+            return self._codes(self.v)
         B, H, NC, cb = self.batch, self.heads, self.chunks, self.head_dim // 2
         x = self.v[..., :CHUNK * cb].reshape(B, H, NC, CHUNK // 4, cb, 4)
         quad = torch.arange(CHUNK // 4, device=x.device).view(-1, 1)

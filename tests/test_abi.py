@@ -72,7 +72,11 @@ def test_append_validation(L):
     assert call(pos=10, nn=3) == fq.FLEXQ_ERR_ARG
     assert call(nn=0) == fq.FLEXQ_ERR_ARG
     assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
-    assert call(bits=2) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(bits=5) == fq.FLEXQ_ERR_UNSUPPORTED       # legal, not built
+    assert call(g=16) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(D=64, bits=2, g=128) == fq.FLEXQ_ERR_UNSUPPORTED   # head_dim % group != 0
+    assert call(bits=9) == fq.FLEXQ_ERR_ARG
+    assert call(bits=3, g=32, k=None) == fq.FLEXQ_ERR_NULL          # a built variant gets to the pointer checks
     assert call(k=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=U) == fq.FLEXQ_ERR_ALIGN
@@ -89,10 +93,17 @@ def test_attention_validation(L):
     assert call(cur=0) == fq.FLEXQ_ERR_ARG
     assert call(cur=13) == fq.FLEXQ_ERR_ARG             # cur_len > s + n
     assert call(D=32) == fq.FLEXQ_ERR_UNSUPPORTED
-    assert call(g=128) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(g=16) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(D=64, g=128) == fq.FLEXQ_ERR_UNSUPPORTED
     assert call(q=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=None) == fq.FLEXQ_ERR_NULL
     assert call(out=U) == fq.FLEXQ_ERR_ALIGN
+    # variants (NEXT-3): their own workspace size, 256 B + (D + 2) floats per (b, h, 128-token tile)
+    wv = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 3, 32)
+    assert wv == 256 + (6 * 1 * 130 * 4 + 15) // 16 * 16
+    assert L.flexq_decode_attention_workspace_size(2, 3, 128, 300, 0, 8, 128) == 256 + 6 * 3 * 130 * 4
+    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 3, 32, A, A, wv - 1, None) == fq.FLEXQ_ERR_WORKSPACE
+    assert f(None, A, A, 2, 3, 128, 8, 4, 5, 3, 32, A, A, wv, None) == fq.FLEXQ_ERR_NULL
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
     assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
 
@@ -104,6 +115,13 @@ def test_kv_cache_bytes(L):
     assert c * 8 == 144 * 96 * 544 * 128 * 4.5        # 4.5 bits per element
     c, t = fq.flexq_kv_cache_bytes(4, 12, 64, 512, 1)
     assert t == 544 and c == 4 * 12 * 17 * 18 * 64
+    # variants: chunk = 32 x (D b / 8 code bytes + 4 D / g meta bytes)
+    c, t = fq.flexq_kv_cache_bytes(144, 96, 128, 512, 32, bits=3, group_size=32)
+    assert c == 144 * 96 * 17 * 32 * (48 + 16)
+    c, _ = fq.flexq_kv_cache_bytes(2, 2, 64, 40, 0, bits=8, group_size=64)
+    assert c == 2 * 2 * 2 * 32 * (64 + 4)
+    c, _ = fq.flexq_kv_cache_bytes(2, 2, 128, 40, 0, bits=2, group_size=128)
+    assert c == 2 * 2 * 2 * 32 * (32 + 4)
     assert fq.token_stride(513) == 544 and fq.token_stride(1) == 32 and fq.token_stride(32) == 32
     with __import__("pytest").raises(fq.FlexqError):
         fq.flexq_kv_cache_bytes(1, 1, 96, 8, 8)
@@ -120,6 +138,7 @@ def test_topk_validation(L):
     assert call(cur=13) == fq.FLEXQ_ERR_ARG
     assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
     assert call(cur=1153, keep=5, s=1200, n=0) == fq.FLEXQ_ERR_UNSUPPORTED   # beyond the score buffer
+    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 2, 3, 32, A, None, A, ws, None) == fq.FLEXQ_ERR_UNSUPPORTED   # b = 4, g = 64 only
     assert call(q=None) == fq.FLEXQ_ERR_NULL
     assert call(sel=U) == fq.FLEXQ_ERR_ALIGN
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
@@ -135,7 +154,7 @@ def test_append_attention_validation(L):
     assert call(cur=0) == fq.FLEXQ_ERR_ARG
     assert call(cur=13) == fq.FLEXQ_ERR_ARG
     assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
-    assert call(g=32) == fq.FLEXQ_ERR_UNSUPPORTED
+    assert call(g=16) == fq.FLEXQ_ERR_UNSUPPORTED
     assert call(kn=None) == fq.FLEXQ_ERR_NULL
     assert call(vn=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=None) == fq.FLEXQ_ERR_NULL
