@@ -43,9 +43,34 @@ struct VarParams {
     float scale_log2;     // log2(e) / sqrt(D)
 };
 
-__device__ __forceinline__ float code_f(uint32_t c) {   // exact: 2^23 + c - 2^23
-    return __fsub_rn(__uint_as_float(c | 0x4B000000u), 8388608.0f);
+// Codes become floats without a conversion instruction: (word & (mask << sh)) | 0x4B000000 is the
+// float 2^23 + c 2^sh (one LOP3, exact while sh + b <= 23), and one packed FADD2 of -2^23 per pair
+// leaves c 2^sh exactly.  The 2^sh factors are folded into q (K pass: qsc_d = q_d 2^-sh_d, exact)
+// or removed from the accumulators at the end (V pass), so every product is the exact q_d c_d /
+// p s c_d of the plain formula.
+//
+// Where element d of a token's bit stream is read from (K pass): bit P = d b of word i = P / 32 at
+// s = P % 32; s + b > 32 (b = 3 only) -> funnel shift of words i, i + 1 (shift 0); s + b <= 23 ->
+// word i at shift s; else the word's upper half w >> 16 at shift s - 16 (<= 16 - b).
+template <int B>
+struct ElemSrc {
+    int word, kind, sh;   // kind 0: word, 1: word >> 16, 2: funnel(word, word + 1)
+};
+template <int B>
+__host__ __device__ constexpr ElemSrc<B> elem_src(int d) {
+    const int P = d * B, i = P >> 5, s = P & 31;
+    return (s + B > 32) ? ElemSrc<B>{i, 2, 0} : (s + B <= 23) ? ElemSrc<B>{i, 0, s} : ElemSrc<B>{i, 1, s - 16};
 }
+constexpr uint32_t kMagic = 0x4B000000u;
+// w | 2^23's bit pattern, opaque to the compiler: (w | M) & (K | M) == (w & K) | M is then ONE
+// LOP3 with an immediate per element (given as (w & K) | M, ptxas emits two).
+__device__ __forceinline__ uint32_t or_magic(uint32_t w) {
+    uint32_t r;
+    asm("or.b32 %0, %1, 0x4B000000;" : "=r"(r) : "r"(w));
+    return r;
+}
+// (w >> 16) | M in one PRMT: bytes (w.2, w.3, 0, 0x4B)
+__device__ __forceinline__ uint32_t hi_magic(uint32_t w) { return __byte_perm(w, kMagic, 0x7432); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -62,9 +87,9 @@ attention_variant_kernel(VarParams p) {
     constexpr int DPL = D / 32;                   // V pass: dims per lane
     static_assert(DPL * B <= 32, "a lane's V codes fit one funnel-shifted word");
 
-    __shared__ __align__(16) float q_s[D];
+    __shared__ __align__(16) float q_s[D];     // q_d 2^-sh_d (K pass source shift)
     __shared__ float qg_s[NG];
-    __shared__ float p_s[kVarTile];
+    __shared__ float2 psm_s[kVarTile * NG];      // V side per (token, group): (p scale, p min)
     __shared__ float red_s[kVThreads / 32];
     __shared__ __align__(16) uint8_t vbuf[4 * CHB];
 
@@ -75,13 +100,13 @@ attention_variant_kernel(VarParams p) {
     const int tile_a = split * p.tiles_per_split;
     const int tile_b = min(tile_a + p.tiles_per_split, n_tiles);
 
-    for (int d = tid; d < D; d += kVThreads) q_s[d] = __half2float(p.q[bh * D + d]);
-    __syncthreads();
     if (tid < NG) {
         float s = 0.0f;
-        for (int d = 0; d < G; ++d) s += q_s[tid * G + d];
+        for (int d = 0; d < G; ++d) s += __half2float(p.q[bh * D + tid * G + d]);
         qg_s[tid] = s;
     }
+    for (int d = tid; d < D; d += kVThreads)
+        q_s[d] = ldexpf(__half2float(p.q[bh * D + d]), -elem_src<B>(d).sh);
     __syncthreads();
 
     const uint8_t* kbase = p.kc + bh * p.chunks * CHB;
@@ -125,24 +150,37 @@ attention_variant_kernel(VarParams p) {
             }
             w[NWR] = 0;
             const __half2* meta = reinterpret_cast<const __half2*>(chunk + kChunk * CB + slot * MB);
+            uint32_t wm[NWR], hm[NWR];
+#pragma unroll
+            for (int i = 0; i < NWR; ++i) {
+                wm[i] = or_magic(w[i]);
+                hm[i] = hi_magic(w[i]);
+            }
+            const float2 nbias = make_float2(-8388608.0f, -8388608.0f);
             float s = 0.0f;
 #pragma unroll
             for (int gi = 0; gi < NG; ++gi) {
-                float dot[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                float2 dot[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 #pragma unroll
                 for (int dd = 0; dd < G; dd += 4) {
                     const float4 qq = *reinterpret_cast<const float4*>(&q_s[gi * G + dd]);
-                    const float qv[4] = {qq.x, qq.y, qq.z, qq.w};
+                    float f[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int bit = (gi * G + dd + e) * B, wi = bit >> 5, sh = bit & 31;
-                        uint32_t c = w[wi] >> sh;
-                        if (sh + B > 32) c |= w[wi + 1] << (32 - sh);
-                        dot[e] = fmaf(qv[e], code_f(c & kMask), dot[e]);
+                        const ElemSrc<B> es = elem_src<B>(gi * G + dd + e);
+                        const uint32_t src =
+                            es.kind == 0   ? wm[es.word]
+                            : es.kind == 1 ? hm[es.word]
+                                           : or_magic(__funnelshift_r(w[es.word], w[es.word + 1], (gi * G + dd + e) * B & 31));
+                        f[e] = __uint_as_float(src & ((kMask << es.sh) | kMagic));
                     }
+                    const float2 c01 = __fadd2_rn(make_float2(f[0], f[1]), nbias);
+                    const float2 c23 = __fadd2_rn(make_float2(f[2], f[3]), nbias);
+                    dot[0] = __ffma2_rn(make_float2(qq.x, qq.y), c01, dot[0]);
+                    dot[1] = __ffma2_rn(make_float2(qq.z, qq.w), c23, dot[1]);
                 }
                 const float2 sm = __half22float2(meta[gi]);
-                s = fmaf(sm.x, (dot[0] + dot[1]) + (dot[2] + dot[3]), fmaf(sm.y, qg_s[gi], s));
+                s = fmaf(sm.x, (dot[0].x + dot[0].y) + (dot[1].x + dot[1].y), fmaf(sm.y, qg_s[gi], s));
             }
             score = s * p.scale_log2;
         }
@@ -156,7 +194,6 @@ attention_variant_kernel(VarParams p) {
         const float m_new = fmaxf(m_run, mx);
         const float alpha = exp2f(m_run - m_new);
         const float pt = (tid < tcount) ? exp2f(score - m_new) : 0.0f;
-        p_s[tid] = pt;
         l_part = fmaf(l_part, alpha, pt);
         m_run = m_new;
 #pragma unroll
@@ -164,27 +201,54 @@ attention_variant_kernel(VarParams p) {
         acc_m *= alpha;
         cp_async_wait_all();
         __syncthreads();
+        // the V meta of token tid, times its probability, once per (token, group)
+        if (tid < tcount) {
+            const __half2* vm = reinterpret_cast<const __half2*>(vbuf + (tid >> 5) * CHB + kChunk * CB +
+                                                                 (tid & (kChunk - 1)) * MB);
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                const float2 sm = __half22float2(vm[gi]);
+                psm_s[tid * NG + gi] = make_float2(pt * sm.x, pt * sm.y);
+            }
+        }
+        __syncthreads();
         // V pass: warp w takes chunk w of the tile
         const int nj = min(kChunk, tcount - warp * kChunk);
         const uint32_t* cw = reinterpret_cast<const uint32_t*>(vbuf + warp * CHB);
-        const __half2* mw = reinterpret_cast<const __half2*>(vbuf + warp * CHB + kChunk * CB);
+        const float2* pw = psm_s + warp * kChunk * NG + vgi;
+#pragma unroll 2
         for (int j = 0; j < nj; ++j) {
             uint32_t x = cw[j * NWR + vwi];
             if constexpr ((DPL * B) % 32 != 0) x = __funnelshift_r(x, cw[j * NWR + vwi + 1], vsh);
-            const float pj = p_s[warp * kChunk + j];
-            const float2 sm = __half22float2(mw[j * NG + vgi]);
-            const float ps = pj * sm.x;
-            acc_m = fmaf(pj, sm.y, acc_m);
+            const uint32_t xm = or_magic(x), xh = hi_magic(x);
+            const float2 pp = pw[j * NG];
+            const float ps = pp.x;
+            acc_m += pp.y;
+            float f[DPL];
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) acc[e] = fmaf(ps, code_f((x >> (e * B)) & kMask), acc[e]);
+            for (int e = 0; e < DPL; ++e) {   // element e at bit e b of x: 2^23 + c 2^vsh_e
+                const int sh = e * B;
+                f[e] = __uint_as_float(sh + B <= 23 ? (xm & ((kMask << sh) | kMagic))
+                                                    : (xh & ((kMask << (sh - 16)) | kMagic)));
+            }
+#pragma unroll
+            for (int e = 0; e < DPL; e += 2) {
+                const float2 c = __fadd2_rn(make_float2(f[e], f[e + 1]), make_float2(-8388608.0f, -8388608.0f));
+                const float2 r = __ffma2_rn(make_float2(ps, ps), c, make_float2(acc[e], acc[e + 1]));
+                acc[e] = r.x;
+                acc[e + 1] = r.y;
+            }
         }
-        __syncthreads();   // vbuf / p_s are rewritten by the next tile
+        __syncthreads();   // vbuf / psm_s are rewritten by the next tile
     }
 
     // combine the 4 warps' partial sums (all share m_run)
     float* comb = reinterpret_cast<float*>(vbuf);
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) comb[warp * D + lane * DPL + e] = acc[e] + acc_m;
+    for (int e = 0; e < DPL; ++e) {   // remove the 2^sh factor of element e (exact)
+        const int sh = e * B + B <= 23 ? e * B : e * B - 16;
+        comb[warp * D + lane * DPL + e] = ldexpf(acc[e], -sh) + acc_m;
+    }
     float l = l_part;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
