@@ -100,9 +100,17 @@ flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t
  * The chunks of one head are contiguous, so the attention kernel streams any
  * run of them with one 1-D TMA bulk copy.  Tokens [T_cap, T_stride) are
  * padding the library never writes.
+ *
+ * Variants: bits in {2, 3, 4, 8} x group_size in {32, 64, 128} other than
+ * (4, 64), with head_dim % group_size == 0.  Same 32-token chunks with CB = D*bits/8 code bytes
+ * and MB = 4*D/group_size meta bytes per token, chunk = 32*(CB + MB) bytes:
+ *     [codes 32 x CB][meta 32 x MB]
+ * K and V alike token-major: token s's codes at s*CB as a little-endian bit stream (bit i of
+ * column j is stream bit j*bits + i), its D/group_size half2 {scale, min} at 32*CB + s*MB.
+ *
  * *cache_bytes (may be NULL) receives the size of ONE buffer (K or V),
- * *token_stride (may be NULL) T_stride.  Supported: bits == 4,
- * group_size == 64, head_dim in {64, 128}. */
+ * *token_stride (may be NULL) T_stride.  Supported: head_dim in {64, 128}; (bits, group_size)
+ * = (4, 64) or a variant above (other legal values -> FLEXQ_ERR_UNSUPPORTED). */
 flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                   int bits, int group_size, size_t *cache_bytes, int *token_stride);
 
@@ -118,8 +126,9 @@ flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
                              void *k_cache, void *v_cache, void *stream);
 
 /* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
- * arguments).  Layout: 256 B of scheduler counters, 4 B per (batch, head) of
- * split tickets, then split-K partials.  The workspace must be zero-filled
+ * arguments).  Layout (b = 4, g = 64): 256 B of scheduler counters, 4 B per (batch, head) of
+ * split tickets, then split-K partials; variants: 256 B (unused), then (D + 2) floats per
+ * (batch, head, 128-token tile) of split-K partials.  The workspace must be zero-filled
  * ONCE after allocation; every call restores the counters and tickets to
  * zero before it completes (the partials are scratch), so one buffer serves
  * any number of stream-ordered calls (not concurrent ones). */
@@ -133,7 +142,8 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
  * M); q fp16 [batch][heads][head_dim].  Cache layout as above; tokens at
  * positions >= cur_len do not influence the result (the kernel may stream the
  * rest of the last 32-token chunk into shared memory and discard it).  Accuracy: |out - exact| <=
- * max(2e-3, 1e-2 |exact|) per element (reading Q). */
+ * max(2e-3, 1e-2 |exact|) per element (reading Q).  (4, 64) runs the tensor-core kernel; the
+ * variants a CUDA-core split-K kernel (+ a combine launch when a head is split). */
 flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, const void *v_cache,
                                     int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                     int cur_len, int bits, int group_size, void *out_f16,
@@ -148,7 +158,7 @@ flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, cons
  * flexq_append_kv; nothing else in the cache is touched; the output
  * satisfies flexq_decode_attention's accuracy bound.  Arguments, workspace
  * and errors as for flexq_decode_attention (+ FLEXQ_ERR_NULL / _ALIGN for
- * k_new / v_new). */
+ * k_new / v_new).  Variants: the append kernel, then the attention kernel (two launches). */
 flexq_status flexq_append_decode_attention(const void *q_f16, const void *k_new_f16, const void *v_new_f16,
                                            void *k_cache, void *v_cache, int batch, int heads,
                                            int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
@@ -163,7 +173,7 @@ flexq_status flexq_append_decode_attention(const void *q_f16, const void *k_new_
  * (P:856).  The paper keeps the top 10%: keep = ceil(0.1 * cur_len).
  * sel_i32 (optional, may be NULL): int32 [batch][heads][keep] receives the
  * kept token indices in ascending order.  Workspace as for
- * flexq_decode_attention.  Supported: cur_len <= 1152 (else
+ * flexq_decode_attention.  Supported: bits = 4, group_size = 64, cur_len <= 1152 (else
  * FLEXQ_ERR_UNSUPPORTED); 1 <= keep <= cur_len (else FLEXQ_ERR_ARG). */
 flexq_status flexq_decode_attention_topk(const void *q_f16, const void *k_cache, const void *v_cache,
                                          int batch, int heads, int head_dim, int prompt_len, int gen_len,
