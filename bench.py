@@ -633,6 +633,42 @@ def run_flexq(args):
                             "frac_of_measured_hbm": round(cbytes / (cus * 1e-6) / 1e9 / peak, 4)}
             del ccaches, cq, cout, cws, gc
 
+    # ---- NEXT-3 variants of the KV cache (rank 0): decode attention on the OPT-175B shape at the
+    # last step's context for three (b, g), 2 layers of fresh caches each, one CUDA graph
+    kv_variants = None
+    if rank == 0 and not args.no_sweep and w.name == "opt-175b":
+        kv_variants = {}
+        vcur = s + n - 1
+        vk = synth.fill(seed + 9, synth.tensor_id(0, synth.K_PROMPT), (B, H, vcur, D), device=dev)
+        vq = synth.fill(seed + 9, synth.tensor_id(0, synth.Q), (B, H, D), device=dev)
+        vout = torch.empty_like(vq)
+        for vb, vg in ((2, 32), (3, 64), (8, 128)):
+            vcaches = [fq.KVCache(B, H, D, s, n, device=dev, bits=vb, group_size=vg) for _ in range(2)]
+            for vc in vcaches:
+                fq.flexq_append_kv(vk, vk, vc, pos=0)
+            vws = fq.make_workspace(vcaches[0])
+            gv = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gv, stream=stream):
+                for vc in vcaches:
+                    fq.flexq_decode_attention(vq, vc, vcur, out=vout, workspace=vws, stream=stream)
+            gv.replay()
+            torch.cuda.synchronize()
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                v0.record(stream)
+                for _ in range(10):
+                    gv.replay()
+                v1.record(stream)
+            torch.cuda.synchronize()
+            vus = v0.elapsed_time(v1) * 1e3 / (10 * len(vcaches))
+            vbytes = 2 * B * H * vcur * (D * vb // 8 + 4 * D // vg) + 2 * B * H * D * 2
+            kv_variants[f"b{vb}g{vg}"] = {"cur_len": vcur, "us_per_launch": round(vus, 2), "bytes_per_launch": vbytes,
+                                          "GBps": round(vbytes / (vus * 1e-6) / 1e9, 1),
+                                          "frac_of_measured_hbm": round(vbytes / (vus * 1e-6) / 1e9 / peak, 4),
+                                          "kernel": "attention_variant_kernel (CUDA cores)"}
+            del vcaches, vws, gv
+        del vk, vq, vout
+
     # ---- NEXT-4: host-offloaded compressed KV, Alg. 1 overlap (rank 0): 2 OPT-175B layers of
     # batch 144 in pinned host memory, streamed through a 2-slot device ring
     log("offload")
@@ -690,6 +726,7 @@ def run_flexq(args):
             "offload": offload,
             "allgather": allgather,
             "other_configs": other,
+            "kv_variants": kv_variants,
         }
         print(json.dumps(line), flush=True)
     if pg:

@@ -92,6 +92,15 @@ attention_variant_kernel(VarParams p) {
     __shared__ float2 psm_s[kVarTile * NG];      // V side per (token, group): (p scale, p min)
     __shared__ float red_s[kVThreads / 32];
     __shared__ __align__(16) uint8_t vbuf[4 * CHB];
+    // b = 8: K codes of the tile staged in shared memory, one row per token, padded so that
+    // lane-per-row LDS.128 reads of 8 consecutive rows hit 8 distinct 16-B bank groups.  With
+    // 128-B rows read straight from global memory, a warp's LDG.128 touches 32 lines and the
+    // small L1 left beside the shared memory re-fetches them from L2 (ncu: 1.8x the DRAM bytes
+    // through L2; 433-576 -> 398-433 us).  b <= 4 reads its rows from global memory (the extra
+    // copy and barrier cost more than they save there: 295 -> 307 us at b = 2).
+    constexpr bool KSM = B == 8;
+    constexpr int KRS = CB + (((CB / 16) % 2 == 0) ? 16 : 32);
+    __shared__ __align__(16) uint8_t kbuf[KSM ? kVarTile * KRS : 16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t bh = blockIdx.x;
@@ -120,12 +129,25 @@ attention_variant_kernel(VarParams p) {
     for (int tile = tile_a; tile < tile_b; ++tile) {
         const int t0 = tile * kVarTile;
         const int tcount = min(kVarTile, p.cur_len - t0);
-        // stage the V tile (whole chunks holding valid tokens) while the K pass runs
+        // stage the tile: K codes (padded rows) as one cp.async group, then the V chunks as a second
+        // group that lands while the K pass runs
         {
             const int nch = (tcount + kChunk - 1) / kChunk;
+            if constexpr (KSM) {
+                const uint8_t* ksrc = kbase + int64_t(t0 / kChunk) * CHB;
+                for (int i = tid; i < nch * kChunk * (CB / 16); i += kVThreads) {
+                    const int r = i / (CB / 16), c = i % (CB / 16);
+                    cp_async16(kbuf + r * KRS + 16 * c, ksrc + (r / kChunk) * CHB + (r % kChunk) * CB + 16 * c);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             const uint8_t* src = vbase + int64_t(t0 / kChunk) * CHB;
             for (int i = tid; i < nch * CHB / 16; i += kVThreads) cp_async16(vbuf + 16 * i, src + 16 * i);
             asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        if constexpr (KSM) {
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // the K group
+            __syncthreads();
         }
         // K pass: thread tid owns token t0 + tid
         float score = -INFINITY;
@@ -134,7 +156,7 @@ attention_variant_kernel(VarParams p) {
             const uint8_t* chunk = kbase + int64_t(t / kChunk) * CHB;
             const int slot = t & (kChunk - 1);
             uint32_t w[NWR + 1];
-            const uint8_t* row = chunk + slot * CB;
+            const uint8_t* row = KSM ? kbuf + tid * KRS : chunk + slot * CB;
             if constexpr (CB % 16 == 0) {
 #pragma unroll
                 for (int i = 0; i < CB / 16; ++i) {
