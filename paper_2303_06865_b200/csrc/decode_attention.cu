@@ -501,6 +501,15 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         nsplit = min(nsplit, max_by_len);
         nsplit = int(std::min<int64_t>(nsplit, split_slots(bh, a.t_cap) / bh));
         nsplit = max(nsplit, min_split);
+    } else if (target == 0 && int64_t(bh) * nsplit * 8 <= warps_resident) {
+        // a small problem (>= 8 resident warps per unit, e.g. the tiny config's 48 heads) is
+        // latency-bound on each warp's serial context walk: split the context down to one stage
+        // per split (tiny: 14.95 -> 9.95 us at two stages per split).  Problems near one unit per warp
+        // (OPT-6.7B's 2048 heads) stay unsplit: the partial write + merge costs more there.
+        const int max_by_len = (a.cur_len + Cfg<D, NCH>::CH - 1) / Cfg<D, NCH>::CH;   // one stage per split
+        nsplit = int(std::min<int64_t>({int64_t(max_by_len), split_slots(bh, a.t_cap) / bh,
+                                        int64_t(warps_resident) / bh}));
+        nsplit = max(nsplit, min_split);
     }
     int split_len = (a.cur_len + nsplit - 1) / nsplit;
     split_len = (split_len + Cfg<D, NCH>::CH - 1) / Cfg<D, NCH>::CH * Cfg<D, NCH>::CH;
