@@ -16,8 +16,9 @@
 //              sum_d q_d (c_d s_g + m_g) (reordered fp32 rounding, within reading Q).
 //   softmax -- block max, p = 2^(score - max) (log2 domain), running (max, sum) per CTA.
 //   V pass  -- the V tile (4 chunks, contiguous) was staged into shared memory with cp.async while
-//              the K pass ran; warp w takes chunk w's 32 tokens, lane l the D / 32 dims at bit
-//              l (D / 32) b of the row (one funnel shift out of two words), and accumulates
+//              the K pass ran; warp w takes chunk w's 32 tokens, half-warp h the tokens h, h + 2, ...,
+//              lane l of it the D / 16 dims at bit l (D / 16) b of the row (one funnel shift out
+//              of two words, or two words at b = 8, D = 128), and accumulates
 //              acc_d += (p s_g) c_d and acc_m += p m_g (the same identity).
 // Splits > 1 write (max, sum, acc[D]) partials to the workspace and a combine kernel merges them.
 // CUDA cores only: these variants are HBM-bound like the b = 4 path but are not the headline
@@ -84,8 +85,9 @@ attention_variant_kernel(VarParams p) {
     constexpr int CB = D * B / 8, MB = 4 * D / G, NG = D / G, CHB = kChunk * (CB + MB);
     constexpr int NWR = CB / 4;                   // code words per token row
     constexpr uint32_t kMask = (1u << B) - 1u;
-    constexpr int DPL = D / 32;                   // V pass: dims per lane
-    static_assert(DPL * B <= 32, "a lane's V codes fit one funnel-shifted word");
+    constexpr int DPL = D / 16;                   // V pass: dims per lane (16 lanes per token)
+    constexpr int NWIN = DPL * B > 32 ? 2 : 1;    // words of a lane's V codes (2: b = 8, D = 128)
+    static_assert(DPL * B <= 64 && (NWIN == 1 || DPL * B == 64), "a lane's V codes: one funnel-shifted word or two words");
 
     __shared__ __align__(16) float q_s[D];     // q_d 2^-sh_d (K pass source shift)
     __shared__ float qg_s[NG];
@@ -120,7 +122,8 @@ attention_variant_kernel(VarParams p) {
 
     const uint8_t* kbase = p.kc + bh * p.chunks * CHB;
     const uint8_t* vbase = p.vc + bh * p.chunks * CHB;
-    const int vbit = lane * DPL * B, vwi = vbit >> 5, vsh = vbit & 31, vgi = lane * DPL / G;
+    const int half = lane >> 4, l16 = lane & 15;
+    const int vbit = l16 * DPL * B, vwi = vbit >> 5, vsh = vbit & 31, vgi = l16 * DPL / G;
 
     float m_run = -INFINITY, l_part = 0.0f, acc[DPL], acc_m = 0.0f;
 #pragma unroll
@@ -239,19 +242,26 @@ attention_variant_kernel(VarParams p) {
         const uint32_t* cw = reinterpret_cast<const uint32_t*>(vbuf + warp * CHB);
         const float2* pw = psm_s + warp * kChunk * NG + vgi;
 #pragma unroll 2
-        for (int j = 0; j < nj; ++j) {
-            uint32_t x = cw[j * NWR + vwi];
-            if constexpr ((DPL * B) % 32 != 0) x = __funnelshift_r(x, cw[j * NWR + vwi + 1], vsh);
-            const uint32_t xm = or_magic(x), xh = hi_magic(x);
+        for (int j = half; j < nj; j += 2) {   // half-warp h takes tokens h, h + 2, ...
+            uint32_t x[NWIN];
+            x[0] = cw[j * NWR + vwi];
+            if constexpr ((DPL * B) % 32 != 0) x[0] = __funnelshift_r(x[0], cw[j * NWR + vwi + 1], vsh);
+            if constexpr (NWIN == 2) x[1] = cw[j * NWR + vwi + 1];
+            uint32_t xm[NWIN], xh[NWIN];
+#pragma unroll
+            for (int i = 0; i < NWIN; ++i) {
+                xm[i] = or_magic(x[i]);
+                xh[i] = hi_magic(x[i]);
+            }
             const float2 pp = pw[j * NG];
             const float ps = pp.x;
             acc_m += pp.y;
             float f[DPL];
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) {   // element e at bit e b of x: 2^23 + c 2^vsh_e
-                const int sh = e * B;
-                f[e] = __uint_as_float(sh + B <= 23 ? (xm & ((kMask << sh) | kMagic))
-                                                    : (xh & ((kMask << (sh - 16)) | kMagic)));
+            for (int e = 0; e < DPL; ++e) {   // element e at bit e b of the window: 2^23 + c 2^sh_e
+                const int wi = e * B / 32, sh = e * B % 32;
+                f[e] = __uint_as_float(sh + B <= 23 ? (xm[wi] & ((kMask << sh) | kMagic))
+                                                    : (xh[wi] & ((kMask << (sh - 16)) | kMagic)));
             }
 #pragma unroll
             for (int e = 0; e < DPL; e += 2) {
@@ -264,12 +274,13 @@ attention_variant_kernel(VarParams p) {
         __syncthreads();   // vbuf / psm_s are rewritten by the next tile
     }
 
-    // combine the 4 warps' partial sums (all share m_run)
-    float* comb = reinterpret_cast<float*>(vbuf);
+    // combine the 8 half-warps' partial sums (all share m_run)
+    float* comb = reinterpret_cast<float*>(vbuf);   // [8][D]: fits every variant's 4 staged chunks
+    static_assert(8 * D * 4 <= 4 * CHB, "combine buffer");
 #pragma unroll
     for (int e = 0; e < DPL; ++e) {   // remove the 2^sh factor of element e (exact)
-        const int sh = e * B + B <= 23 ? e * B : e * B - 16;
-        comb[warp * D + lane * DPL + e] = ldexpf(acc[e], -sh) + acc_m;
+        const int s0 = e * B % 32, sh = s0 + B <= 23 ? s0 : s0 - 16;
+        comb[(warp * 2 + half) * D + l16 * DPL + e] = ldexpf(acc[e], -sh) + acc_m;
     }
     float l = l_part;
 #pragma unroll
@@ -278,7 +289,9 @@ attention_variant_kernel(VarParams p) {
     __syncthreads();
     l = (red_s[0] + red_s[1]) + (red_s[2] + red_s[3]);
     for (int d = tid; d < D; d += kVThreads) {
-        const float o = (comb[d] + comb[D + d]) + (comb[2 * D + d] + comb[3 * D + d]);
+        float o = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o += comb[i * D + d];
         if (p.splits == 1) {
             p.out[bh * D + d] = __float2half_rn(o / l);
         } else {
