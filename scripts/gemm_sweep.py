@@ -38,9 +38,10 @@ def main():
     ap.add_argument("--m", type=int, nargs="*", default=[144])
     ap.add_argument("--only", action="store_true", help="flexq kernel only (for ncu)")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--shapes", nargs="*", default=["12288x49152", "12288x12288"], help="KxN")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    for (K, N) in ((12288, 49152), (12288, 12288)):
+    for (K, N) in [tuple(int(v) for v in sh.split("x")) for sh in a.shapes]:
         w = synth.fill(7, 1, (K, N), device=dev)
         codes, meta = fq.flexq_quantize(w)
         panels = fq.flexq_pack_weight(codes, meta)
