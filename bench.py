@@ -711,7 +711,11 @@ def run_flexq(args):
                          "kernel": "decode_attention_kernel<128>" + (" (fused append)" if fused else ""),
                          "peak_kind": peak_kind,
                          "bytes_per_launch": k_bytes, "us_per_launch": round(k_us, 2),
-                         "share_of_step": round(k_us * L / (ms_step * 1e3), 4),
+                         # the step's algorithmic bytes at this kernel's measured rate, over the step time
+                         # (the per-launch pass runs at the longest context, cur_len = s + n - 1, so
+                         # k_us * L would overstate a step whose contexts run s + 1 .. s + n - 1)
+                         "share_of_step": round(value_gbs / (achieved * world) if fused else
+                                                attn_us * L / (ms_step * 1e3), 4),
                          "attention_only_us_per_launch": round(attn_us, 2),
                          "attention_only_GBps": round(attn_bytes / (attn_us * 1e-6) / 1e9, 1),
                          "append_us_per_launch": round(app_us, 2),
