@@ -94,6 +94,10 @@ if __name__ == "__main__":
         for d, t in (("FLEXQ_AB_GSTORE=0", "abg0"), ("FLEXQ_AB_GSTORE=1", "abg1"), ("FLEXQ_AB_STPOL=1", "stp1"),
                      ("FLEXQ_AB_STPOL=2", "stp2")):
             print(build(force="--force" in sys.argv, defines=(d,), tag=t))
+    if "--topk-ab" in sys.argv:
+        for w, m in ((2, 8), (4, 4), (2, 6), (3, 5)):
+            print(build(force="--force" in sys.argv, defines=(f"FLEXQ_TOPK_WPC={w}", f"FLEXQ_TOPK_MINB={m}"),
+                        tag=f"topk_w{w}m{m}"))
     if "--gemm-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_DQW=8",), tag="dqw8"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMM_TRACE=1",), tag="trace"))

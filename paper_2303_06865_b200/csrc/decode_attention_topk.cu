@@ -30,6 +30,9 @@
 #ifndef FLEXQ_TOPK_MINB
 #define FLEXQ_TOPK_MINB 4   // CTAs per SM the register budget is sized for
 #endif
+#ifndef FLEXQ_TOPK_WPC
+#define FLEXQ_TOPK_WPC 3    // warps (= (b, h) units in flight) per CTA
+#endif
 
 namespace flexq {
 namespace {
@@ -384,11 +387,12 @@ cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
+    constexpr int W = FLEXQ_TOPK_WPC;
     if (a.head_dim == 128)
-        return a.cur_len <= 576 ? launch_topk<128, 2, 2, 3, 576>(a, stream)
-                                : launch_topk<128, 2, 2, 3, kTopkMaxTokens>(a, stream);
-    return a.cur_len <= 576 ? launch_topk<64, 2, 2, 3, 576>(a, stream)
-                            : launch_topk<64, 2, 2, 3, kTopkMaxTokens>(a, stream);
+        return a.cur_len <= 576 ? launch_topk<128, 2, 2, W, 576>(a, stream)
+                                : launch_topk<128, 2, 2, W, kTopkMaxTokens>(a, stream);
+    return a.cur_len <= 576 ? launch_topk<64, 2, 2, W, 576>(a, stream)
+                            : launch_topk<64, 2, 2, W, kTopkMaxTokens>(a, stream);
 }
 
 }  // namespace flexq
