@@ -6,7 +6,7 @@ Covers: quantize/dequantize with a ragged row count (and the b/g variants),
 prompt fill + 1-token append, attention with split-K (few heads) and without,
 Top-K, the fused append + attention, a cache whose capacity is not a multiple
 of the token stride (cur_len = T_cap, last head: the metadata bulk copy rounds
-up into the stride padding), weight packing and the tcgen05 dequant-GEMM.
+up into the stride padding), the KV-cache variants, weight packing and the tcgen05 dequant-GEMM.
 """
 import os
 import sys
@@ -45,6 +45,17 @@ def main():
     for b, g in ((2, 32), (3, 128), (8, 64)):
         c, m = fq.flexq_quantize(x[:, :128].contiguous(), bits=b, group_size=g)
         fq.flexq_dequantize(c, m, bits=b, group_size=g)
+    # NEXT-3 KV-cache variants: append, attention with and without splits (cur_len up to T_cap,
+    # last head: the staged chunks end at the buffer end), the one-call decode step; b = 8 stages K
+    for (b, g, D, B, H, s, n) in ((3, 32, 128, 1, 3, 300, 3), (8, 128, 128, 2, 2, 160, 1), (2, 64, 64, 8, 40, 61, 2)):
+        cache = fq.KVCache(B, H, D, s, n, device=dev, bits=b, group_size=g)
+        k = synth.fill(4, b, (B, H, s, D), device=dev)
+        fq.flexq_append_kv(k, k, cache, pos=0)
+        q = synth.fill(4, 9, (B, H, D), device=dev)
+        ws = fq.make_workspace(cache)
+        for cur in (1, s):
+            fq.flexq_decode_attention(q, cache, cur, workspace=ws)
+        fq.flexq_append_decode_attention(q, q, q, cache, s + n, workspace=ws)
     # NEXT-2 decode linear layer: a full tile and split-k remainder tiles, two row chunks
     K, N = 256, 512
     w = synth.fill(3, 1, (K, N), device=dev)

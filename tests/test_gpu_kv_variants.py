@@ -140,3 +140,30 @@ def test_variant_full_size_sampled(orc, cuda):
         orc.append_kv(kp.reshape(1, 1, s, D).numpy(), vp.reshape(1, 1, s, D).numpy(), okc, ovc, 0, bits, group)
         ref = orc.attention_f64(q[b:b + 1, h:h + 1].numpy(), okc, ovc, s, group)
         close(out[b:b + 1, h:h + 1], ref, f"head ({b}, {h})")
+
+
+@pytest.mark.parametrize("bits,group", [(2, 32), (3, 128), (8, 32), (4, 128)])
+def test_attention_variant_extreme_cache(orc, cuda, bits, group):
+    """Pathological KV groups (synth.extreme, per group of the variant: constant groups -> scale 0,
+    +-65504 mixes, subnormal groups, any finite pattern) scaled by powers of two so the softmax stays
+    finite; cache bytes identical to the oracle's, output within reading Q, plus one pathological
+    one-call decode step."""
+    B, H, D, s, n = 2, 3, 128, 150, 4
+    rows = B * H * s
+    k = (synth.extreme(4402, 1, rows, D, group).float() * 2.0 ** -10).half().view(B, H, s, D)
+    v = (synth.extreme(4402, 2, rows, D, group).float() * 2.0 ** -4).half().view(B, H, s, D)
+    cache = fq.KVCache(B, H, D, s, n, device=cuda, bits=bits, group_size=group)
+    okc, ovc = orc.empty_cache(B, H, s + n, D, group), orc.empty_cache(B, H, s + n, D, group)
+    fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+    orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0, bits, group)
+    for qf in (1, 16):
+        q = synth.peaky(synth.fill(4402, 3 + qf, (B, H, D)), qf)
+        out = fq.flexq_decode_attention(q.to(cuda), cache, s)
+        close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, s, group), f"extreme q x{qf}")
+    kn = (synth.extreme(4402, 10, B * H, D, group).float() * 2.0 ** -10).half().view(B, H, D)
+    vn = (synth.extreme(4402, 20, B * H, D, group).float() * 2.0 ** -4).half().view(B, H, D)
+    q = synth.fill(4402, 30, (B, H, D))
+    out = fq.flexq_append_decode_attention(q.to(cuda), kn.to(cuda), vn.to(cuda), cache, s + 1)
+    orc.append_kv(kn.view(B, H, 1, D).numpy(), vn.view(B, H, 1, D).numpy(), okc, ovc, s, bits, group)
+    close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, s + 1, group), "extreme fused")
+    check_cache(orc, cache, okc, ovc, s + 1, bits)
