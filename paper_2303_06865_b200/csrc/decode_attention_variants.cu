@@ -9,8 +9,9 @@
 //
 // Mapping: one 128-thread CTA per (head, split); a split is a run of 128-token tiles (4 chunks).
 // Per tile:
-//   K pass  -- thread i owns token t0 + i: its code row and meta come straight from global memory
-//              (a warp reads 32 consecutive rows, so the lines are fully used through L1), and
+//   K pass  -- thread i owns token t0 + i: its code row comes straight from global memory (a warp
+//              reads 32 consecutive rows, so the lines are fully used through L1; b = 8 stages the
+//              rows in shared memory first, see KSM), its meta from global memory, and
 //              score = sum_g (scale_g sum_{d in g} q_d c_d + min_g sum_{d in g} q_d) in fp32, q from
 //              shared memory (broadcast reads); the per-group factoring is the exact identity of
 //              sum_d q_d (c_d s_g + m_g) (reordered fp32 rounding, within reading Q).
@@ -21,8 +22,8 @@
 //              of two words, or two words at b = 8, D = 128), and accumulates
 //              acc_d += (p s_g) c_d and acc_m += p m_g (the same identity).
 // Splits > 1 write (max, sum, acc[D]) partials to the workspace and a combine kernel merges them.
-// CUDA cores only: these variants are HBM-bound like the b = 4 path but are not the headline
-// configuration, so they trade the tensor-core passes for one generic kernel per (b, g, D).
+// CUDA cores only: one generic kernel per (b, g, D) instead of the b = 4, g = 64 kernel's
+// tensor-core passes; it is instruction-issue-bound at about two instructions per code.
 #include <cuda_fp16.h>
 #include <stdint.h>
 
