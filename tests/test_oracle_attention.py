@@ -210,3 +210,26 @@ def test_topk_converges_to_dense(orc):
             for f in (0.1, 0.25, 0.5, 1.0)]
     assert all(devs[i + 1] <= devs[i] + 1e-15 for i in range(3)), devs
     assert devs[-1] < 1e-12
+
+
+@pytest.mark.parametrize("bits,group", [(2, 32), (3, 128), (8, 64), (4, 32)])
+def test_variant_cache_append_and_attention(orc, bits, group):
+    """NEXT-3 variants (reading V): append writes quantize(rows, bits, group) per token row, and the
+    attention dequantizes with the row's (D / group) meta pairs -- checked against an independent
+    numpy dequant (exact in f64) + scipy softmax, and the closed form of cur_len = 1."""
+    B, H, D, T = 2, 2, 128, 40
+    k = synth.with_outliers(synth.fill(26, 1, (B, H, T, D))).numpy()
+    v = synth.fill(26, 2, (B, H, T, D)).numpy()
+    kc, vc = orc.empty_cache(B, H, T, D, group), orc.empty_cache(B, H, T, D, group)
+    orc.append_kv(k, v, kc, vc, 0, bits, group)
+    c, m = orc.quantize(k.reshape(-1, D), bits, group)
+    assert np.array_equal(kc[0].reshape(-1, D), c) and np.array_equal(kc[1].reshape(-1, D // group, 2), m)
+    assert kc[0].max() <= 2 ** bits - 1
+    q = synth.fill(26, 3, (B, H, D)).numpy()
+    K = deq_f32(orc, kc).astype(np.float64)
+    V = deq_f32(orc, vc).astype(np.float64)
+    s = np.einsum("bhd,bhtd->bht", q.astype(np.float64), K) / np.sqrt(D)
+    ref = np.einsum("bht,bhtd->bhd", scipy.special.softmax(s, axis=-1), V)
+    got = orc.attention_f64(q, kc, vc, T, group)
+    assert np.abs(got - ref).max() <= 1e-10 * max(1.0, np.abs(V).max())
+    assert np.array_equal(orc.attention_f64(q, kc, vc, 1, group), V[:, :, 0, :])
