@@ -14,7 +14,8 @@
 //              rows in shared memory first, see KSM), its meta from global memory, and
 //              score = sum_g (scale_g sum_{d in g} q_d c_d + min_g sum_{d in g} q_d) in fp32, q from
 //              shared memory (broadcast reads); the per-group factoring is the exact identity of
-//              sum_d q_d (c_d s_g + m_g) (reordered fp32 rounding, within reading Q).
+//              sum_d q_d (c_d s_g + m_g) (reordered fp32 rounding, within reading Q).  b in
+//              {2, 4, 8} forms sum q_d c_d with IDP.4A on a 22-bit fixed-point q (see IDP).
 //   softmax -- block max, p = 2^(score - max) (log2 domain), running (max, sum) per CTA.
 //   V pass  -- the V tile (4 chunks, contiguous) was staged into shared memory with cp.async while
 //              the K pass ran; warp w takes chunk w's 32 tokens, half-warp h the tokens h, h + 2, ...,
@@ -74,6 +75,13 @@ __device__ __forceinline__ uint32_t or_magic(uint32_t w) {
 // (w >> 16) | M in one PRMT: bytes (w.2, w.3, 0, 0x4B)
 __device__ __forceinline__ uint32_t hi_magic(uint32_t w) { return __byte_perm(w, kMagic, 0x7432); }
 
+// sum_i a.u8[i] * b.s8[i] + c (exact int32)
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
@@ -119,6 +127,37 @@ attention_variant_kernel(VarParams p) {
     }
     for (int d = tid; d < D; d += kVThreads)
         q_s[d] = ldexpf(__half2float(p.q[bh * D + d]), -elem_src<B>(d).sh);
+    // b in {2, 4, 8}: K pass on IDP.4A.  q in 22-bit fixed point relative to the head's max |q|,
+    // Q_d = RN(q_d 2^(21 - e)) (|q| < 2^e, error <= 2^-22 of max |q|), as three signed 8-bit digits
+    // Q = d0 + 2^8 d1 + 2^16 d2 (|d2| <= 32).  The codes of one 32-bit word become byte vectors with
+    // one mask: (w >> b k) & (2^b - 1) * 0x01010101 holds elements 8 i / b + k (i = 0..3) of the
+    // word, so digit words are stored in that order.  dp4a(u8 codes, s8 digits) sums are exact.
+    constexpr bool IDP = B != 3;
+    constexpr int EPW = 32 / B, KPW = 8 / B;            // elements per word, byte vectors per word
+    __shared__ __align__(16) uint32_t qd_s[IDP ? 3 * (D / 4) : 4];
+    float qfix = 0.0f;                                  // 2^(e - 21)
+    if constexpr (IDP) {
+        float a = 0.0f;
+        for (int d = tid; d < D; d += kVThreads) a = fmaxf(a, fabsf(__half2float(p.q[bh * D + d])));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+        if (lane == 0) red_s[warp] = a;
+        __syncthreads();
+        a = fmaxf(fmaxf(red_s[0], red_s[1]), fmaxf(red_s[2], red_s[3]));
+        int e = 0;
+        if (a > 0.0f) frexpf(a, &e);                    // a = f 2^e, f in [0.5, 1)
+        qfix = ldexpf(1.0f, e - 21);
+        int8_t* qb = reinterpret_cast<int8_t*>(qd_s);
+        for (int d = tid; d < D; d += kVThreads) {
+            const int Q = __float2int_rn(ldexpf(__half2float(p.q[bh * D + d]), 21 - e));
+            const int d0 = (Q << 24) >> 24, r1 = (Q - d0) >> 8, d1 = (r1 << 24) >> 24, d2 = (r1 - d1) >> 8;
+            const int W = d / EPW, ew = d % EPW, k = ew % KPW, i = ew / KPW;
+            const int byte = (W * KPW + k) * 4 + i;
+            qb[byte] = int8_t(d0);
+            qb[D + byte] = int8_t(d1);
+            qb[2 * D + byte] = int8_t(d2);
+        }
+    }
     __syncthreads();
 
     const uint8_t* kbase = p.kc + bh * p.chunks * CHB;
@@ -176,6 +215,30 @@ attention_variant_kernel(VarParams p) {
             }
             w[NWR] = 0;
             const __half2* meta = reinterpret_cast<const __half2*>(chunk + kChunk * CB + slot * MB);
+            float s = 0.0f;
+            if constexpr (IDP) {
+                constexpr uint32_t kByteMask = kMask * 0x01010101u;
+                int acc[3][NG];
+#pragma unroll
+                for (int gi = 0; gi < NG; ++gi) acc[0][gi] = acc[1][gi] = acc[2][gi] = 0;
+#pragma unroll
+                for (int W = 0; W < NWR; ++W) {
+                    const int gi = W * EPW / G;
+#pragma unroll
+                    for (int k = 0; k < KPW; ++k) {
+                        const uint32_t v = B == 8 ? w[W] : (w[W] >> (B * k)) & kByteMask;
+                        const int idx = W * KPW + k;
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) acc[j][gi] = dp4a_us(v, qd_s[j * (D / 4) + idx], acc[j][gi]);
+                    }
+                }
+#pragma unroll
+                for (int gi = 0; gi < NG; ++gi) {
+                    const float dot = fmaf(65536.0f, float(acc[2][gi]), fmaf(256.0f, float(acc[1][gi]), float(acc[0][gi])));
+                    const float2 sm = __half22float2(meta[gi]);
+                    s = fmaf(sm.x * qfix, dot, fmaf(sm.y, qg_s[gi], s));
+                }
+            } else {
             uint32_t wm[NWR], hm[NWR];
 #pragma unroll
             for (int i = 0; i < NWR; ++i) {
@@ -183,7 +246,6 @@ attention_variant_kernel(VarParams p) {
                 hm[i] = hi_magic(w[i]);
             }
             const float2 nbias = make_float2(-8388608.0f, -8388608.0f);
-            float s = 0.0f;
 #pragma unroll
             for (int gi = 0; gi < NG; ++gi) {
                 float2 dot[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
@@ -207,6 +269,7 @@ attention_variant_kernel(VarParams p) {
                 }
                 const float2 sm = __half22float2(meta[gi]);
                 s = fmaf(sm.x, (dot[0].x + dot[0].y) + (dot[1].x + dot[1].y), fmaf(sm.y, qg_s[gi], s));
+            }
             }
             score = s * p.scale_log2;
         }

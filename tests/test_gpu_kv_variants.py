@@ -167,3 +167,16 @@ def test_attention_variant_extreme_cache(orc, cuda, bits, group):
     orc.append_kv(kn.view(B, H, 1, D).numpy(), vn.view(B, H, 1, D).numpy(), okc, ovc, s, bits, group)
     close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, s + 1, group), "extreme fused")
     check_cache(orc, cache, okc, ovc, s + 1, bits)
+
+
+@pytest.mark.parametrize("bits,group", [(2, 32), (8, 128), (4, 128)])
+def test_attention_variant_q_wide_dynamic_range(orc, cuda, bits, group):
+    """q with one channel per head at 2^12 x the rest: the IDP.4A K pass holds q in 22-bit fixed point
+    relative to the head's max |q| (the small channels to 2^-22 of that max); still within reading Q."""
+    B, H, D, s, n = 2, 4, 128, 200, 4
+    cache, okc, ovc, q, cur = build(orc, cuda, B, H, D, s, n, 2, bits, group, seed=65)
+    q = q.clone()
+    q[..., 5] = torch.where(q[..., 5] >= 0, 1.0, -1.0).to(torch.float16) * 4096
+    q = (q.float() * 0.001).to(torch.float16)
+    out = fq.flexq_decode_attention(q.to(cuda), cache, cur)
+    close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, cur, group), f"wide-range q b{bits} g{group}")
