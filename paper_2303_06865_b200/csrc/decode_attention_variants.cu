@@ -18,9 +18,9 @@
 //              {2, 4, 8} forms sum q_d c_d with IDP.4A on a 22-bit fixed-point q (see IDP).
 //   softmax -- block max, p = 2^(score - max) (log2 domain), running (max, sum) per CTA.
 //   V pass  -- the V tile (4 chunks, contiguous) was staged into shared memory with cp.async while
-//              the K pass ran; warp w takes chunk w's 32 tokens, half-warp h the tokens h, h + 2, ...,
-//              lane l of it the D / 16 dims at bit l (D / 16) b of the row (one funnel shift out
-//              of two words, or two words at b = 8, D = 128), and accumulates
+//              the K pass ran; warp w takes chunk w's 32 tokens, lane group h (LPT lanes) the tokens
+//              h, h + 32 / LPT, ..., lane l of it the D / LPT dims at bit l (D / LPT) b of the row
+//              (whole words, or one funnel shift out of two words), and accumulates
 //              acc_d += (p s_g) c_d and acc_m += p m_g (the same identity).
 // Splits > 1 write (max, sum, acc[D]) partials to the workspace and a combine kernel merges them.
 // CUDA cores only: one generic kernel per (b, g, D) instead of the b = 4, g = 64 kernel's
@@ -94,9 +94,14 @@ attention_variant_kernel(VarParams p) {
     constexpr int CB = D * B / 8, MB = 4 * D / G, NG = D / G, CHB = kChunk * (CB + MB);
     constexpr int NWR = CB / 4;                   // code words per token row
     constexpr uint32_t kMask = (1u << B) - 1u;
-    constexpr int DPL = D / 16;                   // V pass: dims per lane (16 lanes per token)
-    constexpr int NWIN = DPL * B > 32 ? 2 : 1;    // words of a lane's V codes (2: b = 8, D = 128)
-    static_assert(DPL * B <= 64 && (NWIN == 1 || DPL * B == 64), "a lane's V codes: one funnel-shifted word or two words");
+    // V pass: LPT lanes per token, DPL dims per lane.  b = 8, D = 128: 8 lanes (16 dims, 4 whole
+    // words; 396 -> 359 us at g = 64); else 16 lanes (one funnel-shifted word, or two words at
+    // b = 8, D = 64) -- 8 lanes measured slower at b = 2 and 4 (251 -> 270 us at b = 2, g = 32)
+    constexpr int LPT = (B == 8 && D == 128) ? 8 : 16;
+    constexpr int TPS = 32 / LPT;                 // tokens per warp step
+    constexpr int DPL = D / LPT;
+    constexpr int NWIN = (DPL * B + 31) / 32;     // words of a lane's V codes
+    static_assert((DPL * B) % 32 == 0 || NWIN == 1, "a lane's V codes: whole words or one funnel-shifted word");
 
     __shared__ __align__(16) float q_s[D];     // q_d 2^-sh_d (K pass source shift)
     __shared__ float qg_s[NG];
@@ -162,8 +167,8 @@ attention_variant_kernel(VarParams p) {
 
     const uint8_t* kbase = p.kc + bh * p.chunks * CHB;
     const uint8_t* vbase = p.vc + bh * p.chunks * CHB;
-    const int half = lane >> 4, l16 = lane & 15;
-    const int vbit = l16 * DPL * B, vwi = vbit >> 5, vsh = vbit & 31, vgi = l16 * DPL / G;
+    const int tsub = lane / LPT, lsub = lane % LPT;
+    const int vbit = lsub * DPL * B, vwi = vbit >> 5, vsh = vbit & 31, vgi = lsub * DPL / G;
 
     float m_run = -INFINITY, l_part = 0.0f, acc[DPL], acc_m = 0.0f;
 #pragma unroll
@@ -306,11 +311,14 @@ attention_variant_kernel(VarParams p) {
         const uint32_t* cw = reinterpret_cast<const uint32_t*>(vbuf + warp * CHB);
         const float2* pw = psm_s + warp * kChunk * NG + vgi;
 #pragma unroll 2
-        for (int j = half; j < nj; j += 2) {   // half-warp h takes tokens h, h + 2, ...
+        for (int j = tsub; j < nj; j += TPS) {   // lane group h takes tokens h, h + TPS, ...
             uint32_t x[NWIN];
-            x[0] = cw[j * NWR + vwi];
-            if constexpr ((DPL * B) % 32 != 0) x[0] = __funnelshift_r(x[0], cw[j * NWR + vwi + 1], vsh);
-            if constexpr (NWIN == 2) x[1] = cw[j * NWR + vwi + 1];
+            if constexpr ((DPL * B) % 32 != 0) {
+                x[0] = __funnelshift_r(cw[j * NWR + vwi], cw[j * NWR + vwi + 1], vsh);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NWIN; ++i) x[i] = cw[j * NWR + vwi + i];
+            }
             uint32_t xm[NWIN], xh[NWIN];
 #pragma unroll
             for (int i = 0; i < NWIN; ++i) {
@@ -338,13 +346,21 @@ attention_variant_kernel(VarParams p) {
         __syncthreads();   // vbuf / psm_s are rewritten by the next tile
     }
 
-    // combine the 8 half-warps' partial sums (all share m_run)
-    float* comb = reinterpret_cast<float*>(vbuf);   // [8][D]: fits every variant's 4 staged chunks
-    static_assert(8 * D * 4 <= 4 * CHB, "combine buffer");
+    // combine: the warp's lane groups by shuffles, then the 4 warps (all share m_run)
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) {   // remove the 2^sh factor of element e (exact)
-        const int s0 = e * B % 32, sh = s0 + B <= 23 ? s0 : s0 - 16;
-        comb[(warp * 2 + half) * D + l16 * DPL + e] = ldexpf(acc[e], -sh) + acc_m;
+    for (int o = LPT; o < 32; o <<= 1) {
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+        acc_m += __shfl_xor_sync(0xffffffffu, acc_m, o);
+    }
+    float* comb = reinterpret_cast<float*>(vbuf);   // [4][D]: fits every variant's 4 staged chunks
+    static_assert(4 * D * 4 <= 4 * CHB, "combine buffer");
+    if (tsub == 0) {
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) {   // remove the 2^sh factor of element e (exact)
+            const int s0 = e * B % 32, sh = s0 + B <= 23 ? s0 : s0 - 16;
+            comb[warp * D + lsub * DPL + e] = ldexpf(acc[e], -sh) + acc_m;
+        }
     }
     float l = l_part;
 #pragma unroll
@@ -353,9 +369,7 @@ attention_variant_kernel(VarParams p) {
     __syncthreads();
     l = (red_s[0] + red_s[1]) + (red_s[2] + red_s[3]);
     for (int d = tid; d < D; d += kVThreads) {
-        float o = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o += comb[i * D + d];
+        const float o = (comb[d] + comb[D + d]) + (comb[2 * D + d] + comb[3 * D + d]);
         if (p.splits == 1) {
             p.out[bh * D + d] = __float2half_rn(o / l);
         } else {
