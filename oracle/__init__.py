@@ -50,8 +50,8 @@ def lib():
         L.oracle_unpack_bits.argtypes = [P, i64, i32, P]
         L.oracle_dequantize.argtypes = [P, P, i64, i64, i32, i32, P]
         L.oracle_append_kv.argtypes = [P, P] + [i32] * 8 + [P, P, P, P]
-        L.oracle_attention_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P]
-        L.oracle_attention_f32.argtypes = [P] * 5 + [i32] * 7 + [P]
+        L.oracle_attention_f64.argtypes = [P] * 5 + [i32] * 6 + [P, P]
+        L.oracle_attention_f32.argtypes = [P] * 5 + [i32] * 6 + [P]
         L.oracle_attention_topk_f64.argtypes = [P] * 5 + [i32] * 7 + [P, P, P, P]
         L.oracle_dequant_gemm_f64.argtypes = [P, P, P, i64, i64, i64, i32, i32, P]
         _lib = L
@@ -159,7 +159,7 @@ def append_kv(k_new, v_new, k_cache, v_cache, pos: int, bits: int = 4, group: in
                                   _p(kc), _p(km), _p(vc), _p(vm)), "append_kv")
 
 
-def attention_f64(q, k_cache, v_cache, cur_len: int, group: int = 64, kv_f16: bool = False,
+def attention_f64(q, k_cache, v_cache, cur_len: int, group: int = 64,
                   want_probs: bool = False):
     """q: fp16 [B][H][D] -> out float64 [B][H][D] (and probs [B][H][cur_len] if asked)."""
     q = _h(q)
@@ -170,12 +170,12 @@ def attention_f64(q, k_cache, v_cache, cur_len: int, group: int = 64, kv_f16: bo
     out = np.zeros((B, H, D), np.float64)
     probs = np.zeros((B, H, cur_len), np.float64) if want_probs else None
     _check(lib().oracle_attention_f64(_p(q), _p(kc), _p(km), _p(vc), _p(vm), B, H, D, T_cap, cur_len,
-                                      group, int(kv_f16), _p(out),
+                                      group, _p(out),
                                       _p(probs) if want_probs else None), "attention_f64")
     return (out, probs) if want_probs else out
 
 
-def attention_f32(q, k_cache, v_cache, cur_len: int, group: int = 64, kv_f16: bool = False):
+def attention_f32(q, k_cache, v_cache, cur_len: int, group: int = 64):
     q = _h(q)
     B, H, D = q.shape
     kc, km = k_cache
@@ -183,7 +183,7 @@ def attention_f32(q, k_cache, v_cache, cur_len: int, group: int = 64, kv_f16: bo
     T_cap = kc.shape[2]
     out = np.zeros((B, H, D), np.float32)
     _check(lib().oracle_attention_f32(_p(q), _p(kc), _p(km), _p(vc), _p(vm), B, H, D, T_cap, cur_len,
-                                      group, int(kv_f16), _p(out)), "attention_f32")
+                                      group, _p(out)), "attention_f32")
     return out
 
 

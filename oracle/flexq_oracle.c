@@ -249,16 +249,12 @@ int oracle_append_kv(const uint16_t *k_new, const uint16_t *v_new,
 }
 
 /* ------------------------------------------------------------------ O8 */
-/* Dequantized cache element of head (b,h), token t, column j, as fp32 (reading M),
- * or rounded to fp16 first when kv_f16 != 0 (the paper's literal "converted back
- * to FP16 before computation"; diagnostic only). */
-static float cache_elem(const uint8_t *codes, const uint16_t *meta, int64_t row, int D, int group,
-                        int j, int kv_f16)
+/* Dequantized cache element of head (b,h), token t, column j, as fp32 (reading M:
+ * fmaf(code, scale, min), never rounded to fp16). */
+static float cache_elem(const uint8_t *codes, const uint16_t *meta, int64_t row, int D, int group, int j)
 {
     int64_t mo = (row * (D / group) + j / group) * 2;
-    float v = dequant_f32(codes[row * D + j], meta[mo], meta[mo + 1]);
-    if (kv_f16) v = oracle_f16_to_f32(oracle_f32_to_f16(fminf(fmaxf(v, -65504.0f), 65504.0f)));
-    return v;
+    return dequant_f32(codes[row * D + j], meta[mo], meta[mo + 1]);
 }
 
 /* Textbook decode attention in double (reading K: sqrt(head_dim)):
@@ -268,7 +264,7 @@ static float cache_elem(const uint8_t *codes, const uint16_t *meta, int64_t row,
  * probs (optional, may be NULL): double [B][H][cur_len] softmax weights. */
 int oracle_attention_f64(const uint16_t *q, const uint8_t *k_codes, const uint16_t *k_meta,
                          const uint8_t *v_codes, const uint16_t *v_meta,
-                         int B, int H, int D, int T_cap, int cur_len, int group, int kv_f16,
+                         int B, int H, int D, int T_cap, int cur_len, int group,
                          double *out, double *probs)
 {
     if (B < 1 || H < 1 || D < 1 || T_cap < 1 || group < 1) return ERR_ARG;
@@ -286,7 +282,7 @@ int oracle_attention_f64(const uint16_t *q, const uint8_t *k_codes, const uint16
                 double acc = 0.0;
                 for (int j = 0; j < D; ++j)
                     acc += (double)oracle_f16_to_f32(qh[j]) *
-                           (double)cache_elem(k_codes, k_meta, row, D, group, j, kv_f16);
+                           (double)cache_elem(k_codes, k_meta, row, D, group, j);
                 s[t] = acc / sqrt((double)D);
                 if (s[t] > mx) mx = s[t];
             }
@@ -299,7 +295,7 @@ int oracle_attention_f64(const uint16_t *q, const uint8_t *k_codes, const uint16
             for (int j = 0; j < D; ++j) {
                 double o = 0.0;
                 for (int t = 0; t < cur_len; ++t)
-                    o += s[t] * (double)cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j, kv_f16);
+                    o += s[t] * (double)cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j);
                 out[bh * D + j] = o;
             }
         }
@@ -311,7 +307,7 @@ int oracle_attention_f64(const uint16_t *q, const uint8_t *k_codes, const uint16
  * s_t = sigma * sum_{j asc} q_j K^_tj, e_t = expf(s_t - M), o_j = (sum_t e_t V^_tj) / Z. */
 int oracle_attention_f32(const uint16_t *q, const uint8_t *k_codes, const uint16_t *k_meta,
                          const uint8_t *v_codes, const uint16_t *v_meta,
-                         int B, int H, int D, int T_cap, int cur_len, int group, int kv_f16,
+                         int B, int H, int D, int T_cap, int cur_len, int group,
                          float *out)
 {
     if (B < 1 || H < 1 || D < 1 || T_cap < 1 || group < 1) return ERR_ARG;
@@ -329,7 +325,7 @@ int oracle_attention_f32(const uint16_t *q, const uint8_t *k_codes, const uint16
                 int64_t row = bh * T_cap + t;
                 float acc = 0.0f;
                 for (int j = 0; j < D; ++j)
-                    acc += oracle_f16_to_f32(qh[j]) * cache_elem(k_codes, k_meta, row, D, group, j, kv_f16);
+                    acc += oracle_f16_to_f32(qh[j]) * cache_elem(k_codes, k_meta, row, D, group, j);
                 e[t] = sigma * acc;
                 if (e[t] > mx) mx = e[t];
             }
@@ -338,7 +334,7 @@ int oracle_attention_f32(const uint16_t *q, const uint8_t *k_codes, const uint16
             for (int j = 0; j < D; ++j) {
                 float o = 0.0f;
                 for (int t = 0; t < cur_len; ++t)
-                    o += e[t] * cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j, kv_f16);
+                    o += e[t] * cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j);
                 out[bh * D + j] = o / z;
             }
         }
@@ -377,7 +373,7 @@ int oracle_attention_topk_f64(const uint16_t *q, const uint8_t *k_codes, const u
                 double acc = 0.0;
                 for (int j = 0; j < D; ++j)
                     acc += (double)oracle_f16_to_f32(qh[j]) *
-                           (double)cache_elem(k_codes, k_meta, row, D, group, j, 0);
+                           (double)cache_elem(k_codes, k_meta, row, D, group, j);
                 s[t] = acc / sqrt((double)D);
                 if (scores_out) scores_out[bh * cur_len + t] = s[t];
             }
@@ -403,7 +399,7 @@ int oracle_attention_topk_f64(const uint16_t *q, const uint8_t *k_codes, const u
                 for (int t = 0; t < cur_len; ++t)
                     if (kept[t])
                         o += exp(s[t] - mx) / z *
-                             (double)cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j, 0);
+                             (double)cache_elem(v_codes, v_meta, bh * T_cap + t, D, group, j);
                 out[bh * D + j] = o;
             }
         }

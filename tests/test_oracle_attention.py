@@ -178,6 +178,53 @@ def test_topk_selection_is_top_scores(orc):
             assert mask[b, h].sum() == keep
 
 
+def tied_topk_case(orc, B=1, H=2, D=64, T=40, seed=57):
+    """K rows drawn from 3 distinct rows (token t gets row t % 3, reversed in head 1), so the
+    scores take 3 values with exact ties (identical codes and meta give bit-identical sums)."""
+    base = synth.fill(seed, 1, (B, H, 3, D)).numpy()
+    k = np.empty((B, H, T, D), np.float16)
+    for h in range(H):
+        cls = np.arange(T) % 3 if h == 0 else (2 - np.arange(T) % 3)
+        k[:, h] = base[:, h][:, cls]
+    v = synth.fill(seed, 2, (B, H, T, D)).numpy()
+    kc, vc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
+    orc.append_kv(k, v, kc, vc, 0)
+    q = synth.fill(seed, 3, (B, H, D)).numpy()
+    return q, kc, vc, base
+
+
+def test_topk_exact_ties_keep_lowest_index(orc):
+    """Selection is index work: on exactly tied scores the kept set is
+    the definition's -- score descending, then token index ascending (flexq.h).  The class
+    order comes from an independent numpy evaluation of the 3 distinct rows; the expected
+    set is then built by counting, not from the oracle's own ranking."""
+    B, H, D, T = 1, 2, 64, 40
+    q, kc, vc, _ = tied_topk_case(orc, B, H, D, T)
+    K = deq_f32(orc, kc).astype(np.float64)
+    for keep in (1, 5, 14, 20, 27, 39):
+        _, mask, scores = orc.attention_topk_f64(q, kc, vc, T, keep=keep)
+        for h in range(H):
+            cls_of = np.arange(T) % 3 if h == 0 else (2 - np.arange(T) % 3)
+            s_cls = np.array([q[0, h].astype(np.float64) @ K[0, h, list(cls_of).index(c)] for c in range(3)])
+            assert len(set(s_cls.tolist())) == 3                          # three distinct values
+            for c in range(3):                                            # ties are exact
+                assert len(set(scores[0, h, cls_of == c].tolist())) == 1
+            want = np.zeros(T, np.uint8)
+            left = keep
+            for c in np.argsort(-s_cls):                                   # best class first
+                idx = np.flatnonzero(cls_of == c)                          # ascending token index
+                take = idx[:left]
+                want[take] = 1
+                left -= len(take)
+            assert np.array_equal(mask[0, h], want), (keep, h)
+    # all-identical keys: the kept set is the first `keep` tokens
+    k = np.repeat(synth.fill(58, 1, (1, 1, 1, D)).numpy(), T, axis=2)
+    kc1, vc1 = orc.empty_cache(1, 1, T, D), orc.empty_cache(1, 1, T, D)
+    orc.append_kv(k, synth.fill(58, 2, (1, 1, T, D)).numpy(), kc1, vc1, 0)
+    _, mask, _ = orc.attention_topk_f64(synth.fill(58, 3, (1, 1, D)).numpy(), kc1, vc1, T, keep=9)
+    assert mask[0, 0].tolist() == [1] * 9 + [0] * (T - 9)
+
+
 def test_topk_renormalised_and_dominant_key(orc):
     """one dominant key and keep = 1 -> output = that key's V^ row; weights
     renormalised over the kept set sum to 1 (checked through V = constant rows)."""

@@ -58,11 +58,11 @@ int main(void) {
     double *o = ALLOC(double, B * H * D), *pr = ALLOC(double, B * H * cur), *sc = ALLOC(double, B * H * cur);
     float *of = ALLOC(float, B * H * D);
     uint8_t *sel = ALLOC(uint8_t, B * H * cur);
-    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, cur, grp, 0, o, pr) != 0;
-    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, cur, grp, 1, o, NULL) != 0;
-    fails += oracle_attention_f32(q, kc, km, vc, vm, B, H, D, T, cur, grp, 0, of) != 0;
+    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, cur, grp, o, pr) != 0;
+    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, cur, grp, o, NULL) != 0;
+    fails += oracle_attention_f32(q, kc, km, vc, vm, B, H, D, T, cur, grp, of) != 0;
     fails += oracle_attention_topk_f64(q, kc, km, vc, vm, B, H, D, T, cur, grp, 4, NULL, sel, sc, o) != 0;
-    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, T + 1, grp, 0, o, NULL) == 0;   /* rejected */
+    fails += oracle_attention_f64(q, kc, km, vc, vm, B, H, D, T, T + 1, grp, o, NULL) == 0;   /* rejected */
     /* decode linear layer */
     const int M = 3, K = 16, N = 128;
     uint16_t *xw = ALLOC(uint16_t, M * K), *w = ALLOC(uint16_t, K * N), *wm = ALLOC(uint16_t, K * N / 64 * 2);
