@@ -80,20 +80,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "")
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
-    if "--ab" in sys.argv:   # A/B libraries for tuning
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_H16_UNPACK=1",), tag="h16unpack"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_IDP4A=0",), tag="kffma2"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_MINB=5",), tag="topk5"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_K_MMA=0",), tag="kidp"))
-        print(build(force="--force" in sys.argv, defines=("FLEXQ_V_MMA=0",), tag="vidp"))
     if "--deq-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=1", "FLEXQ_DEQ_CS=0"), tag="deq1"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=4", "FLEXQ_DEQ_CS=0"), tag="deq4n"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=2",), tag="deq2"))
-    if "--fuse-ab" in sys.argv:
-        for d, t in (("FLEXQ_AB_GSTORE=0", "abg0"), ("FLEXQ_AB_GSTORE=1", "abg1"), ("FLEXQ_AB_STPOL=1", "stp1"),
-                     ("FLEXQ_AB_STPOL=2", "stp2")):
-            print(build(force="--force" in sys.argv, defines=(d,), tag=t))
+    if "--trace" in sys.argv:
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_ATTN_TRACE=1",), tag="trace"))
     if "--topk-ab" in sys.argv:
         for w, m in ((2, 8), (4, 4), (2, 6), (3, 5)):
             print(build(force="--force" in sys.argv, defines=(f"FLEXQ_TOPK_WPC={w}", f"FLEXQ_TOPK_MINB={m}"),

@@ -24,6 +24,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "attn_common.cuh"
 #include "flexq_internal.h"
 
@@ -36,6 +38,118 @@
 
 namespace flexq {
 namespace {
+
+// ---------------------------------------------------------------- V-row gather helpers
+// Nibble -> float conversion of one 32-bit code word (8 codes, columns e = 0..7):
+// (w & 0xF<<4e) | 0x4B000000 = 2^23 + c_e 16^e (one LOP3 per code, e = 5..7 from
+// w >> 12), one FADD2 removes 2^23 per pair.  Pairs: f[0] = (c0, 16 c1),
+// f[1] = (256 c2, 4096 c3), f[2] = (65536 c4, 256 c5), f[3] = (4096 c6, 65536 c7).
+// The value is exact; the power-of-two factor is removed once per unit
+// (inv_shift).  The magic constant lives in a register so that (w & mask) | magic
+// is a single LOP3.
+__device__ __forceinline__ uint32_t magic_reg() {
+    uint32_t m;
+    asm volatile("mov.b32 %0, 0x4B000000;" : "=r"(m));
+    return m;
+}
+template <uint32_t M>
+__device__ __forceinline__ uint32_t lop_and_or(uint32_t w, uint32_t magic) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(M), "r"(magic));  // (a & b) | c
+    return r;
+}
+__device__ __forceinline__ void unpack8(uint32_t w, uint32_t magic, float2 (&f)[4]) {
+    const uint32_t w12 = w >> 12;
+    const float2 bias = make_float2(-8388608.0f, -8388608.0f);
+    f[0] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x0000Fu>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x000F0u>(w, magic))), bias);
+    f[1] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x00F00u>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x0F000u>(w, magic))), bias);
+    f[2] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0xF0000u>(w, magic)),
+                                  __uint_as_float(lop_and_or<0x00F00u>(w12, magic))), bias);
+    f[3] = __fadd2_rn(make_float2(__uint_as_float(lop_and_or<0x0F000u>(w12, magic)),
+                                  __uint_as_float(lop_and_or<0xF0000u>(w12, magic))), bias);
+}
+// 2^-k of the two codes of pair p (order of unpack8).
+__device__ __forceinline__ float2 inv_shift(int pair) {
+    switch (pair) {
+        case 0: return make_float2(1.0f, 0.0625f);
+        case 1: return make_float2(0.00390625f, 0.000244140625f);
+        case 2: return make_float2(1.52587890625e-05f, 0.00390625f);
+        default: return make_float2(0.000244140625f, 1.52587890625e-05f);
+    }
+}
+// acc_j += (p scale) c_j over the lane's 32 columns, bias += p min, l += p.
+__device__ __forceinline__ void v_accum(float2 (&acc)[16], float& l, float& bsum, uint4 vw, float2 vm, float p,
+                                        uint32_t magic) {
+    l += p;
+    const float a = p * vm.x;
+    bsum = fmaf(p, vm.y, bsum);
+    const float2 a2 = make_float2(a, a);
+    const uint32_t wv[4] = {vw.x, vw.y, vw.z, vw.w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        float2 f[4];
+        unpack8(wv[w], magic, f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[4 * w + k] = __ffma2_rn(a2, f[k], acc[4 * w + k]);
+    }
+}
+// End of a unit: remove the 16^k factors, reduce (acc, l, bsum) over the token
+// lanes (reduce-scatter for acc: lane keeps D/32 columns), and return the
+// lane's column offset col0; v[0 .. D/32) = sum_t (p scale) c + bias (unnormalised).
+template <int D>
+__device__ __forceinline__ int reduce_unit(float2 (&acc)[16], float& l, float& bsum, int lane, int sg,
+                                           float (&v)[32]) {
+    constexpr int LPT = D / 32;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = __fmul2_rn(acc[k], inv_shift(k & 3));
+#pragma unroll
+    for (int o = LPT; o < 32; o <<= 1) {
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+        bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {   // natural column order: v[col] (static register renaming)
+        v[8 * (k / 4) + 2 * (k & 3)] = acc[k].x;
+        v[8 * (k / 4) + 2 * (k & 3) + 1] = acc[k].y;
+    }
+    int width = 32;   // live entries
+    int base = 0;     // column offset (within the 32-column segment) of v[0]
+#pragma unroll
+    for (int o = 16; o >= LPT; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+        const int half = width >> 1;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (k < half) {
+                const float send = upper ? v[k] : v[k + half];
+                const float keep = upper ? v[k + half] : v[k];
+                v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        if (upper) base += half;
+        width = half;
+    }
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) v[k] += bsum;
+    return sg * 32 + base;
+}
+// out[col0 .. col0 + D/32) = v / l as fp16.
+template <int D>
+__device__ __forceinline__ void write_out(__half* dst, const float (&v)[32], float l) {
+    const float inv = 1.0f / l;
+    if constexpr (D == 128) {
+        __half2 h0 = __floats2half2_rn(v[0] * inv, v[1] * inv);
+        __half2 h1 = __floats2half2_rn(v[2] * inv, v[3] * inv);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(dst) = w;
+    } else {
+        *reinterpret_cast<__half2*>(dst) = __floats2half2_rn(v[0] * inv, v[1] * inv);
+    }
+}
 
 struct TopkParams {
     const __half* q;
@@ -72,11 +186,12 @@ decode_attention_topk_kernel(const TopkParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    uint8_t* ring = smem + warp * (S * C::STAGE);
-    uint8_t* wsm = smem + WPC * S * C::STAGE + warp * (MAXT * 6);
-    float* scores = reinterpret_cast<float*>(wsm);
-    uint16_t* kept = reinterpret_cast<uint16_t*>(wsm + MAXT * 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * (S * C::STAGE + MAXT * 6)) + warp * S;
+    constexpr int PW = S * C::STG + 2 * D + MAXT * 6;   // per warp: ring, q, scores, kept list
+    uint8_t* ring = smem + warp * PW;
+    uint8_t* qsm = ring + S * C::STG;
+    float* scores = reinterpret_cast<float*>(qsm + 2 * D);
+    uint16_t* kept = reinterpret_cast<uint16_t*>(qsm + 2 * D + MAXT * 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * S;
 
     const uint64_t policy = evict_first_policy();
     if (lane == 0) {
@@ -100,30 +215,29 @@ decode_attention_topk_kernel(const TopkParams P) {
         if (fcount == 0) fq0 = p_bh; else if (fcount == 1) fq1 = p_bh; else fq2 = p_bh;
         ++fcount;
     };
-    auto issue = [&](int slot) {
+    auto issue = [&](int slot) {   // warp-collective (elect.sync issues)
         if (p_bh < 0) {
-            if (lane == 0) mbar_expect_tx(&bars[slot], 0);
+            mbar_expect_tx_elect(&bars[slot], 0);
             return;
         }
-        if (lane == 0) {
-            const int n = min(C::CH, P.cur_len - p_stage * C::CH);
-            const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
-            const bool first = p_stage == 0;
-            uint8_t* sb = ring + slot * C::STAGE;
-            mbar_expect_tx(&bars[slot], bytes + (first ? 2 * D : 0));
-            bulk_g2s(sb, p_k + int64_t(p_stage) * (NCH * C::CHB), bytes, &bars[slot], policy);
-            if (first) bulk_g2s(sb + C::OFF_Q, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
-        }
+        const int n = min(C::CH, P.cur_len - p_stage * C::CH);
+        const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
+        const bool first = p_stage == 0;
+        uint8_t* sb = ring + slot * C::STG;
+        mbar_expect_tx_elect(&bars[slot], bytes + (first ? 2 * D : 0));
+        bulk_g2s_elect(sb, p_k + int64_t(p_stage) * C::STG, bytes, &bars[slot], policy);
+        // q of the unit (read at its first stage, before the next unit's q is issued: S = 2)
+        if (first) bulk_g2s_elect(qsm, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
         if (++p_stage == nst) next_unit();
     };
     next_unit();
 #pragma unroll 1
     for (int s = 0; s < S - 1; ++s) issue(s);
 
-    const int tl = lane / C::LPT;
-    const int sg = lane % C::LPT;
-    const int lc = tl * C::CB + sg * 16;
-    const int lm = tl * C::MB + (sg >> 1) * 4;
+    constexpr int LPT = D / 32;   // V gather: lanes per token
+    constexpr int TPI = 32 / LPT; //   tokens per warp iteration
+    const int tl = lane / LPT;
+    const int sg = lane % LPT;
     const uint32_t magic = magic_reg();
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n_tok = P.cur_len;
@@ -134,7 +248,7 @@ decode_attention_topk_kernel(const TopkParams P) {
     auto acquire = [&]() -> const uint8_t* {
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
-        return ring + slot * C::STAGE;
+        return ring + slot * C::STG;
     };
     auto release = [&]() {
         __syncwarp();
@@ -156,9 +270,8 @@ decode_attention_topk_kernel(const TopkParams P) {
         float M;
         {
             const uint8_t* sb = acquire();
-#if FLEXQ_K_MMA
             KFrag<D> kf;                      // the lane's q digits + epilogue weights for pass 1
-            load_q_mma<D>(sb + C::OFF_Q, P.qscale, lane, kf);
+            load_q_mma<D>(qsm, P.qscale, lane, kf);
             float mx = -INFINITY;
 #pragma unroll 1
             for (int st = 0;;) {
@@ -176,31 +289,8 @@ decode_attention_topk_kernel(const TopkParams P) {
                 if (++st == nst) break;
                 sb = acquire();
             }
-#else
-            KQuery kq;
-            load_q(sb + C::OFF_Q + sg * 64, P.qscale, kq);
-            float mx = -INFINITY;
-#pragma unroll 1
-            for (int st = 0;;) {
-                const int t0 = st * C::CH;
-                const int n = min(C::CH, n_tok - t0);
-                if (n == C::CH) {
-#pragma unroll 4
-                    for (int i = 0; i < C::ITERS; ++i)
-                        k_iter<D, NCH, true>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
-                } else {
-#pragma unroll 4
-                    for (int i = 0; i < C::ITERS; ++i)
-                        if (i * C::TPI < n)
-                            k_iter<D, NCH, false>(i, kq, sb, scores, t0, tl, n, lc, lm, sg, magic, mx);
-                }
-                release();
-                if (++st == nst) break;
-                sb = acquire();
-            }
-#endif
 #pragma unroll
-            for (int o = C::LPT; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             M = mx;   // the largest score is always kept, so M is the kept set's max
         }
 
@@ -303,7 +393,7 @@ decode_attention_topk_kernel(const TopkParams P) {
         // unrolled over the three register slots so no slot is copied while its
         // loads are outstanding
         int ta, tb, tc;
-        bool va = row_of(tl, ta), vb = row_of(C::TPI + tl, tb), vc = row_of(2 * C::TPI + tl, tc);
+        bool va = row_of(tl, ta), vb = row_of(TPI + tl, tb), vc = row_of(2 * TPI + tl, tc);
         uint4 ra[4] = {}, rb[4] = {}, rc[4] = {};
         uint32_t ma = 0u, mb = 0u, mc = 0u;
         if (va) load_row(ta, ra, ma);
@@ -317,18 +407,18 @@ decode_attention_topk_kernel(const TopkParams P) {
                 vm = make_float2(0.0f, 0.0f);
             }
             v_accum(acc, l, bsum, row_bytes(t, r), vm, p, magic);
-            v = row_of((g + 3) * C::TPI + tl, t);   // refill the slot with group g + 3
+            v = row_of((g + 3) * TPI + tl, t);   // refill the slot with group g + 3
             m = 0u;
             if (v) load_row(t, r, m);
         };
 #pragma unroll 1
         for (int g = 0;; g += 3) {
             step(g, ta, va, ra, ma);
-            if ((g + 1) * C::TPI >= keep) break;
+            if ((g + 1) * TPI >= keep) break;
             step(g + 1, tb, vb, rb, mb);
-            if ((g + 2) * C::TPI >= keep) break;
+            if ((g + 2) * TPI >= keep) break;
             step(g + 2, tc, vc, rc, mc);
-            if ((g + 3) * C::TPI >= keep) break;
+            if ((g + 3) * TPI >= keep) break;
         }
         float v[32];
         const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
@@ -349,23 +439,29 @@ decode_attention_topk_kernel(const TopkParams P) {
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t topk_smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STAGE + 8) + MAXT * 6);
+    return size_t(WPC) * (S * (Cfg<D, NCH>::STG + 8) + 2 * D + MAXT * 6);
 }
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
-    static int occ = -1;
     auto k = decode_attention_topk_kernel<D, NCH, S, WPC, MAXT>;
     const size_t smem = topk_smem_bytes<D, NCH, S, WPC, MAXT>();
-    if (occ < 0) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem);
-        occ = o > 0 ? o : 1;
-    }
-    int sms = 0, dev = 0;
+    // per-device launch facts, computed once per device under a lock
+    constexpr int kMaxDev = 64;
+    static int occs[kMaxDev], smss[kMaxDev];
+    static std::once_flag once[kMaxDev];
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    std::call_once(once[dev], [&] {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int o = 0, n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, WPC * 32, smem);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        occs[dev] = o > 0 ? o : 1;
+        smss[dev] = n > 0 ? n : 148;
+    });
+    const int occ = occs[dev], sms = smss[dev];
     const int bh = a.batch * a.heads;
     const int ctas = min(sms * occ, (bh + WPC - 1) / WPC);
     TopkParams P;

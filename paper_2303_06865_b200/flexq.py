@@ -63,6 +63,9 @@ def lib():
                   "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention",
                   "flexq_dequant_gemm", "flexq_pack_weight"):
             getattr(L, f).restype = I
+        if hasattr(L, "flexq_debug_attn_trace"):   # tuning build only
+            L.flexq_debug_attn_trace.argtypes = [P, I]
+            L.flexq_debug_attn_trace.restype = I
         _lib = L
     return _lib
 

@@ -245,7 +245,86 @@ def test_full_size_sampled(orc, cuda, cfg):
         assert_attn_close(out[b:b + 1, h:h + 1], ref, f"(b={b}, h={h})")
 
 
+def test_full_size_fused_sampled(orc, cuda):
+    """The launch bench.py times: OPT-175B (B=144, H=96, D=128, s=512, n=32) at full size, every
+    decode step i = 1..31 through flexq_append_decode_attention (cur_len 513..543, one fused launch
+    per step).  For 12 sampled heads the oracle replays prompt fill + the 31 appends and
+    recomputes the outputs of steps 1 (cur_len 513) and 31 (cur_len 543); K codes, K meta, V codes
+    and V meta of those heads must be byte-identical over all 543 tokens."""
+    B, H, D, s, n = 144, 96, 128, 512, 32
+    seed = synth.BASE_SEED + 3
+    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=cuda)
+    v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), device=cuda)
+    fq.flexq_append_kv(k, v, cache, pos=0)
+    del k, v
+    ws = fq.make_workspace(cache)
+    outs = {}
+    steps = n - 1
+    for step in range(1, steps + 1):
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW, step), (B, H, D), device=cuda)
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, D), device=cuda)
+        q = synth.fill(seed, synth.tensor_id(0, synth.Q, step), (B, H, D), device=cuda)
+        o = fq.flexq_append_decode_attention(q, kn, vn, cache, s + step, workspace=ws)
+        if step in (1, steps):
+            outs[step] = o.cpu().numpy()
+    T = s + steps
+    kc_all, vc_all = cache.k_codes().cpu().numpy(), cache.v_codes().cpu().numpy()
+    km_all = cache.k_meta().cpu().numpy().view(np.uint16)
+    vm_all = cache.v_meta().cpu().numpy().view(np.uint16)
+    assert int(ws[:256 + 4 * B * H].sum()) == 0
+    rng = np.random.default_rng(11)
+    samples = [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(10)]
+    sl = lambda b, h, *rest: [b, h, *rest]   # noqa: E731
+    for b, h in samples:
+        okc, ovc = orc.empty_cache(1, 1, s + n, D), orc.empty_cache(1, 1, s + n, D)
+        kp = synth.gather(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), sl(b, h, slice(None), slice(None)))
+        vp = synth.gather(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), sl(b, h, slice(None), slice(None)))
+        orc.append_kv(kp.numpy(), vp.numpy(), okc, ovc, 0)
+        for step in range(1, steps + 1):
+            kn = synth.gather(seed, synth.tensor_id(0, synth.K_NEW, step), (B, H, D), sl(b, h, slice(None)))
+            vn = synth.gather(seed, synth.tensor_id(0, synth.V_NEW, step), (B, H, D), sl(b, h, slice(None)))
+            orc.append_kv(kn.numpy().reshape(1, 1, 1, D), vn.numpy().reshape(1, 1, 1, D), okc, ovc, s + step - 1)
+            if step in outs:
+                qh = synth.gather(seed, synth.tensor_id(0, synth.Q, step), (B, H, D), sl(b, h, slice(None)))
+                ref = orc.attention_f64(qh.numpy().reshape(1, 1, D), okc, ovc, s + step)
+                assert_attn_close(outs[step][b:b + 1, h:h + 1], ref, f"step {step} (b={b}, h={h})")
+        assert np.array_equal(kc_all[b, h, :T], orc.pack4(okc[0][0, 0, :T])), (b, h)
+        assert np.array_equal(vc_all[b, h, :T], orc.pack4(ovc[0][0, 0, :T])), (b, h)
+        assert np.array_equal(km_all[b, h, :T], okc[1][0, 0, :T]), (b, h)
+        assert np.array_equal(vm_all[b, h, :T], ovc[1][0, 0, :T]), (b, h)
+
+
 # ---------------------------------------------------------------- NEXT-1: Top-K sparse attention
+@pytest.mark.parametrize("D", [64, 128])
+def test_topk_exact_ties_bit_exact(orc, cuda, D):
+    """Selection is index work: on exactly tied scores (K rows drawn from 3
+    distinct rows, so identical codes + meta give identical scores on both sides) the GPU's
+    kept set must equal the oracle's -- score descending, then lowest token index -- with zero
+    mismatches; the output is then within reading Q of the oracle on that set."""
+    B, H, T = 2, 3, 150
+    base = synth.fill(59, 1, (B, H, 3, D))
+    cls = torch.stack([torch.arange(T) % 3, 2 - torch.arange(T) % 3, (torch.arange(T) // 7) % 3])
+    k = torch.stack([torch.stack([base[b, h][cls[h]] for h in range(H)]) for b in range(B)])
+    v = synth.fill(59, 2, (B, H, T, D))
+    cache = fq.KVCache(B, H, D, T, 1, device=cuda)
+    fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+    okc, ovc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
+    orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+    q = synth.fill(59, 3, (B, H, D))
+    for keep in (1, 15, 50, 73, 149):
+        sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
+        out = fq.flexq_decode_attention_topk(q.to(cuda), cache, T, keep, sel=sel)
+        torch.cuda.synchronize()
+        ref, omask, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, T, keep)
+        mask = np.zeros((B, H, T), np.uint8)
+        for b in range(B):
+            for h in range(H):
+                mask[b, h, sel.cpu().numpy()[b, h]] = 1
+        assert int((mask != omask).sum()) == 0, f"keep={keep}: kept sets differ"
+        assert_attn_close(out.cpu().numpy(), ref, f"ties keep={keep}")
+
+
 TOPK_CASES = [
     # name, B, H, D, s, n, steps, outliers, qfactor, keep fraction
     ("d128_10pct", 3, 8, 128, 300, 4, 3, False, 4, 0.1),
