@@ -283,11 +283,13 @@ __device__ __forceinline__ void k_block_mma(int blk, const KFrag<D>& kf, const u
 //                 byte limbs (table [group][quad][limb], built per stage); column n =
 //                 (limb, group) as in pass 1's map;
 //   C (16 x 8)  = per column, per (limb, group) int32 sums over the whole work unit.
-// The fixed-point scale of a group is a running one: 2^(23 - e_g) with e_g the exponent
-// of the largest weight seen so far in the unit (p <= 1, the unit's exact max is known
-// from pass 1).  When a stage raises e_g the int32 sums of that group are shifted right
-// (rounded) by the difference; int32 cannot overflow (<= 1088 tokens x 255 x 240).
-// Limbs and nibble positions are combined in fp32 once, at the end of the unit.
+// The fixed-point scale of a group is a running one: 2^(23 - e_g) with 2^(e_g - kVHead)
+// above the largest weight seen so far in the unit (p <= 1, the unit's exact max is known
+// from pass 1).  When a stage's weights reach 2^e_g, the int32 sums of that group are first
+// flushed into fp32 (exact conversion of the limb sums at the old scale, then zeroed) and
+// e_g is raised; otherwise the sums simply keep accumulating in int32 (no overflow:
+// <= 1088 tokens x 255 x 240).  Limbs and nibble positions are combined per lane row at
+// the flush and at the end of the unit.
 template <int D, int NCH>
 constexpr int kLimbWords = (D / 64) * (NCH * kChunk / 4) * 4;   // [group][quad][4 words]
 
@@ -303,13 +305,17 @@ template <int D>
 struct VAccM {
     static constexpr int PPL = D / 16;   // tiles (column pairs per lane row)
     int c[PPL][4];                       // int32 sums of C, per tile / C register
+    float ev[PPL], od[PPL];              // flushed fp32 parts of the lane row's even / odd column (x 16)
     int e[D / 64];                       // running exponent per group (weights < 2^e)
     float l, bsum[D / 64];
     __device__ __forceinline__ void init() {
 #pragma unroll
-        for (int u = 0; u < PPL; ++u)
+        for (int u = 0; u < PPL; ++u) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) c[u][i] = 0;
+            ev[u] = 0.0f;
+            od[u] = 0.0f;
+        }
         l = 0.0f;
 #pragma unroll
         for (int g = 0; g < D / 64; ++g) {
@@ -359,11 +365,14 @@ __device__ __forceinline__ VLane<D> v_lane(int lane) {
     return v;
 }
 
-// Rounded arithmetic shift right by k >= 0 (k >= 31 gives 0 or -1 -> 0 after rounding).
-__device__ __forceinline__ int rshift_rn(int x, int k) {
-    if (k == 0) return x;
-    if (k > 30) return 0;
-    return (x + (1 << (k - 1))) >> k;
+// Headroom of the running fixed-point scale: a group's scale is set 2^kVHead above the
+// largest weight seen so far, so later stages rarely raise it (each raise flushes the
+// group's int32 sums to fp32); weights keep >= 19 significant bits against the running bound.
+constexpr int kVHead = 4;
+
+// 2^(e - 23): the value of one unit of a limb-0 sum at running exponent e (0: no weights yet).
+__device__ __forceinline__ float unit_of(int e) {
+    return e < -100 ? 0.0f : __int_as_float((127 + e - 23) << 23);
 }
 
 // One stage of pass 2: weight pre-pass (lane (quad qd, group g) computes the 4 weights
@@ -397,20 +406,24 @@ __device__ __forceinline__ void v_stage_mma(VAccM<D>& va, const VLane<D>& vl, co
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) if (g == gg) va.bsum[gg] += bs;
         float up = 0.0f;
-        const int ci0 = vl.g0, ci1 = vl.g1;       // groups of the lane's C columns
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
             const uint32_t mb = __reduce_max_sync(0xffffffffu, (g == gg) ? __float_as_uint(amax) : 0u);
             // weights < 2^es with es = exponent field - 126 (0 -> tiny, dropped below)
             const int es = int((mb >> 23) & 0xFFu) - 126;
             if (es > va.e[gg]) {                  // warp-uniform: the running scale grows
-                const int k = es - va.e[gg];
+                if (vl.gr == gg) {                // flush the lane row's sums of this group (exact)
+                    const float f = unit_of(va.e[gg]);
+                    const float w0 = vl.w0 * f, w1 = vl.w1 * f;
 #pragma unroll
-                for (int u = 0; u < PPL; ++u) {
-                    if (ci0 == gg) { va.c[u][0] = rshift_rn(va.c[u][0], k); va.c[u][2] = rshift_rn(va.c[u][2], k); }
-                    if (ci1 == gg) { va.c[u][1] = rshift_rn(va.c[u][1], k); va.c[u][3] = rshift_rn(va.c[u][3], k); }
+                    for (int u = 0; u < PPL; ++u) {
+                        va.ev[u] = fmaf(float(va.c[u][0]), w0, fmaf(float(va.c[u][1]), w1, va.ev[u]));
+                        va.od[u] = fmaf(float(va.c[u][2]), w0, fmaf(float(va.c[u][3]), w1, va.od[u]));
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) va.c[u][i] = 0;
+                    }
                 }
-                va.e[gg] = es;
+                va.e[gg] = es + kVHead;
             }
             const int eg = va.e[gg];              // weights < 2^eg; fixed point 2^(23 - eg)
             const float u = eg < -100 ? 0.0f : __int_as_float((127 + 23 - eg) << 23);
@@ -478,18 +491,16 @@ __device__ __forceinline__ void v_finish_mma(const VAccM<D>& va, const VLane<D>&
         for (int g = 0; g < G; ++g) b[g] += __shfl_xor_sync(0xffffffffu, b[g], o);
     }
     lsum = l;
-    // column weights: limb weight x 2^(e_g - 23) of the column's group (0 for unused columns)
-    auto inv = [&](int g) {   // g in {-1, 0, G - 1}: selects, no dynamic register indexing
-        const int e = g == 0 ? va.e[0] : va.e[G - 1];
-        return g < 0 || e < -100 ? 0.0f : __int_as_float((127 + e - 23) << 23);
-    };
-    const float w0 = vl.w0 * inv(vl.g0), w1 = vl.w1 * inv(vl.g1);
+    // column weights: limb weight x 2^(e_g - 23) of the lane row's group (vl.w0 / w1 are 0 for
+    // columns of the other group and unused columns)
+    const float f = unit_of(vl.gr == 0 ? va.e[0] : va.e[G - 1]);
+    const float w0 = vl.w0 * f, w1 = vl.w1 * f;
     const float bias = vl.gr == 0 ? b[0] : b[G - 1];
     const float inv_l = 1.0f / l;
 #pragma unroll
     for (int u = 0; u < PPL; ++u) {
-        float ev = fmaf(float(va.c[u][0]), w0, float(va.c[u][1]) * w1);                 // column 2p
-        float od = fmaf(float(va.c[u][2]), w0, float(va.c[u][3]) * w1) * 0.0625f;       // column 2p+1 (16 c)
+        float ev = fmaf(float(va.c[u][0]), w0, fmaf(float(va.c[u][1]), w1, va.ev[u]));             // column 2p
+        float od = fmaf(float(va.c[u][2]), w0, fmaf(float(va.c[u][3]), w1, va.od[u])) * 0.0625f;   // 2p+1 (16 c)
         ev += __shfl_xor_sync(0xffffffffu, ev, 1);
         od += __shfl_xor_sync(0xffffffffu, od, 1);
         ev += __shfl_xor_sync(0xffffffffu, ev, 2);

@@ -6,28 +6,25 @@
 //   K^_tj = fmaf(c_tj, scale_tg, min_tg) in fp32 (never rounded to fp16).
 //
 // Design ("decode_attention_kernel"):
-//  * Persistent kernel, one warp per CTA, every warp resident.  The work is the
-//    B*H*nck 32-token chunks of the context (nck = ceil(cur_len / 32)), laid out
-//    head after head; warp w owns the contiguous range [w T / W, (w+1) T / W)
-//    ("stream-K"): every warp streams the same number of bytes whatever B*H is,
-//    so there is no tail of idle warps at small batch and no wave quantisation.
-//  * A warp's range is cut into pieces at head boundaries and at MAXT tokens
-//    (the score buffer).  A piece that is a whole head writes its fp16 output;
-//    the others write (acc, m, l) partials and count their tokens on a per-head
-//    ticket -- the piece that completes the count merges the head's partials in
-//    token order with the log-sum-exp rule (online-softmax combine) and resets
-//    the ticket.  The piece layout is a pure function of (B*H, nck, W), so the
-//    merger finds every partial by index: results are deterministic.
+//  * Persistent kernel, one warp per CTA, every warp resident.  Work items are
+//    handed out by an atomic ticket (fetched one item ahead, so its latency hides
+//    behind the current item): first whole (b, h) heads, then -- for the last
+//    heads, about one per warp -- pieces of a head (a contiguous run of its
+//    32-token chunks).  Fast SMs take more items, and the end of the launch is cut
+//    into small pieces, so no SM idles while another finishes a whole head (the
+//    per-SM streaming rate differs by up to ~6-15 % on B200).
+//  * A piece writes (acc, m, l) partials; the last piece of its head to finish (a
+//    per-head ticket) merges them in piece order with the log-sum-exp rule
+//    (online-softmax combine) and resets the ticket: results are deterministic.
+//    Contexts longer than the score buffer (MAXT tokens) are split the same way.
 //  * Each warp owns a 2-stage shared-memory ring.  A stage is 2 consecutive
 //    32-token chunks of the K cache (pass 1) or of the V cache (pass 2) -- codes
 //    + fp16 (scale, min), one contiguous run in HBM -- loaded with a single 1-D
 //    TMA bulk copy (cp.async.bulk -> mbarrier complete_tx); q (and, for the fused
-//    append, the new token's k and v rows) rides with a piece's first stage into
-//    the warp's extra area.  Loads run one stage ahead of the math, across pieces.
-//    All of the copy-issue code is warp-uniform (one warp per CTA: every value
-//    derives from blockIdx and the parameters) and elect.sync picks the lane
-//    that issues.
-//  * Two passes per piece, no online rescaling: pass 1 streams the K stages and
+//    append, the new token's k and v rows) rides with an item's first stage into
+//    the warp's extra area.  Loads run one stage ahead of the math, across items;
+//    elect.sync picks the lane that issues.
+//  * Two passes per item, no online rescaling: pass 1 streams the K stages and
 //    writes every score (log2 domain) to the warp's smem score buffer; pass 2
 //    takes the exact max, streams the V stages and accumulates p_t = 2^(s_t - M).
 //    Both passes run on the tensor cores as exact integer MMAs (attn_common.cuh).
@@ -46,9 +43,9 @@ namespace flexq {
 namespace {
 
 constexpr int kNch = 2;             // chunks per stage (64 tokens)
-constexpr int kMaxWarps = 4096;     // grid cap (bounds the partial slots per head)
-constexpr int kMinPieceChunks = 2;  // fewest chunks per warp when the problem is small
-constexpr int kMinMaxT = 576;       // smallest score buffer of any variant (sizes the workspace)
+constexpr int kMaxWarps = 4096;     // grid cap
+constexpr int kMaxPieces = 32;      // pieces per head (partial slots per head)
+constexpr int kMinPieceChunks = 2;  // smallest piece
 constexpr int kCtasPerSm = 16;      // one-warp CTAs resident per SM (register / smem budget)
 
 #ifndef FLEXQ_ATTN_TRACE
@@ -68,14 +65,18 @@ struct Params {
     const uint8_t* kc;     // chunked K cache
     const uint8_t* vc;     // chunked V cache
     __half* out;
-    uint32_t* tickets;     // per (b, h): tokens of finished partial pieces (self-resetting)
-    float* part;           // [bh][pmax][D] unnormalised partial outputs
-    float2* ml;            // [bh][pmax] (m, l) of each partial
-    int total;             // bh * nck chunks of work
+    uint32_t* ctrl;        // [0] next item ticket, [1] retired warps (self-resetting)
+    uint32_t* tickets;     // per (b, h): finished pieces (self-resetting)
+    float* part;           // [bh][kMaxPieces][D] unnormalised partial outputs
+    float2* ml;            // [bh][kMaxPieces] (m, l) of each partial
     int nck;               // chunks per head
-    int maxch;             // most chunks per piece (score buffer)
-    int pmax;              // partial slots per head
-    int wq, wr;            // total = wq W + wr (W = gridDim.x warps)
+    int na, ka;            // phase A: heads [0, na), ka pieces each (ka > 1 only past the score buffer)
+    int kb;                // phase B: heads [na, bh), kb pieces each
+    int items;             // na ka + (bh - na) kb
+    int dynamic;           // 1: ticket items (above); 0: static stream-K ranges (below)
+    int total;             // static: bh nck chunks, warp w owns [w total / W, (w+1) total / W)
+    int wq, wr;            // static: total = wq W + wr
+    int maxch;             // static: most chunks per piece (score buffer)
     int64_t chunks;        // chunk stride per (b, h) in the cache
     int cur_len;
     float qscale;          // log2(e) / sqrt(D)
@@ -85,31 +86,45 @@ struct Params {
     uint8_t* vc_w;
 };
 
-// First chunk of warp w's range: floor(w total / W) without 64-bit arithmetic.
+// Work item t: piece k of np of head bh = chunks [o, o + nch) (np = 1: the whole head).
+struct Piece {
+    int bh, o, nch, k, np;
+};
+__device__ __forceinline__ bool decode_item(const Params& P, int t, Piece& p) {
+    if (t >= P.items) return false;
+    const int ta = P.na * P.ka;
+    if (t < ta) {
+        p.np = P.ka;
+        p.bh = t / P.ka;
+        p.k = t - p.bh * P.ka;
+    } else {
+        const int t2 = t - ta;
+        p.np = P.kb;
+        const int hb = t2 / P.kb;
+        p.k = t2 - hb * P.kb;
+        p.bh = P.na + hb;
+    }
+    p.o = p.k * P.nck / p.np;
+    p.nch = (p.k + 1) * P.nck / p.np - p.o;
+    return true;
+}
+
+// Static mode: first chunk of warp w's range, floor(w total / W) without 64-bit arithmetic.
 __device__ __forceinline__ int range_start(const Params& P, int w, int W) {
     return w * P.wq + (w * P.wr) / W;
 }
-
-// A piece: chunks [o, o + nch) of head bh.
-struct Piece {
-    int bh, o, nch;
-};
-struct PieceIter {
-    int cur, end;
-    __device__ __forceinline__ bool next(const Params& P, Piece& p) {
-        if (cur >= end) return false;
-        p.bh = cur / P.nck;
-        p.o = cur - p.bh * P.nck;
-        const int e = min(min(end, (p.bh + 1) * P.nck), cur + P.maxch);
-        p.nch = e - cur;
-        cur = e;
-        return true;
-    }
-};
-
-// Index of the piece of head bh that starts at chunk offset o (o < 0: none), and the
-// head's piece count: the pieces are the warp segments of the head, each cut every
-// maxch chunks from its start (the same cuts PieceIter makes).
+// Static mode: the piece starting at global chunk c of a warp whose range ends at r1 --
+// cut at the head's end and every maxch chunks.
+__device__ __forceinline__ void static_piece(const Params& P, int c, int r1, Piece& p) {
+    p.bh = c / P.nck;
+    p.o = c - p.bh * P.nck;
+    p.nch = min(min(r1, (p.bh + 1) * P.nck), c + P.maxch) - c;
+    p.k = 0;
+    p.np = (p.o == 0 && p.nch == P.nck) ? 1 : 0;   // 0: a piece; index / count by head_pieces
+}
+// Static mode: index of the piece of head bh that starts at chunk offset o, and the head's
+// piece count -- the warp segments of the head, each cut every maxch chunks from its start
+// (the cuts static_piece makes).  A pure function of the launch: the merge order is fixed.
 __device__ int head_pieces(const Params& P, int W, int bh, int o, int& count) {
     const int h0 = bh * P.nck, h1 = h0 + P.nck;
     int w = int((int64_t(h0 + 1) * W - 1) / P.total);   // the warp owning chunk h0
@@ -117,7 +132,7 @@ __device__ int head_pieces(const Params& P, int W, int bh, int o, int& count) {
     for (;;) {
         const int s = max(range_start(P, w, W), h0), e = min(range_start(P, w + 1, W), h1);
         if (e > s) {
-            if (found < 0 && o >= 0 && h0 + o >= s && h0 + o < e) found = idx + (h0 + o - s) / P.maxch;
+            if (found < 0 && h0 + o >= s && h0 + o < e) found = idx + (h0 + o - s) / P.maxch;
             idx += (e - s + P.maxch - 1) / P.maxch;
         }
         if (e >= h1) break;
@@ -159,18 +174,36 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     int n_pieces = 0;
 #endif
 
+    // ---------------- producer (warp-uniform): per item nst K stages, then nst V stages.
+    // The next ticket is fetched one item ahead (lane 0 holds the raw atomic result
+    // until it is needed); item ids go through a 3-entry FIFO to the consumer, which
+    // lags by at most one stage.
     const int W = gridDim.x;
-    const int r0 = range_start(P, blockIdx.x, W), r1 = range_start(P, blockIdx.x + 1, W);
-
-    // ---------------- producer (warp-uniform): per piece nst K stages, then nst V stages
-    PieceIter pit{r0, r1};
-    Piece pp{0, 0, 0};
+    const int r0 = P.dynamic ? 0 : range_start(P, blockIdx.x, W);
+    const int r1 = P.dynamic ? 0 : range_start(P, blockIdx.x + 1, W);
+    int p_cur = r0;                        // static mode: the producer's next chunk
+    uint32_t tk_raw = 0;
+    if (P.dynamic && lane == 0) tk_raw = atomicAdd(P.ctrl, 1u);
+    Piece pp{0, 0, 0, 0, 1};
     bool p_valid = false, p_new = false;
     int p_stage = 0, p_nst = 0, p_last = 0;
     const uint8_t* p_k = nullptr;
     const uint8_t* p_v = nullptr;
+    int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
     auto p_next = [&]() {
-        p_valid = pit.next(P, pp);
+        int t;
+        if (P.dynamic) {
+            t = int(__shfl_sync(0xffffffffu, tk_raw, 0));
+            p_valid = decode_item(P, t, pp);
+            if (lane == 0 && p_valid) tk_raw = atomicAdd(P.ctrl, 1u);   // prefetch the following ticket
+        } else {
+            t = p_cur;
+            p_valid = p_cur < r1;
+            if (p_valid) {
+                static_piece(P, p_cur, r1, pp);
+                p_cur += pp.nch;
+            }
+        }
         p_stage = 0;
         if (p_valid) {
             p_nst = (pp.nch + kNch - 1) / kNch;
@@ -180,6 +213,9 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
             p_v = P.vc + c0 * C::CHB;
             p_new = P.k_new != nullptr && pp.o + pp.nch == P.nck;
         }
+        const int id = p_valid ? t : -1;
+        if (fcount == 0) fq0 = id; else if (fcount == 1) fq1 = id; else fq2 = id;
+        ++fcount;
     };
     auto issue = [&](int slot) {
         if (!p_valid) {
@@ -205,7 +241,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     p_next();
     issue(0);
 
-    // ---------------- consumer: the same piece sequence, one stage behind
+    // ---------------- consumer: the same item sequence, one stage behind
     const VLane<D> vlane = v_lane<D, kNch>(lane);
     int slot = 0;
     uint32_t parity = 0;
@@ -220,10 +256,16 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         parity ^= uint32_t(slot == 0);
     };
 
-    PieceIter cit{r0, r1};
     Piece pc;
 #pragma unroll 1
-    while (cit.next(P, pc)) {
+    for (;;) {
+        const int item = fq0;              // pop the consumer's next item
+        fq0 = fq1;
+        fq1 = fq2;
+        --fcount;
+        if (item < 0) break;
+        if (P.dynamic) decode_item(P, item, pc);
+        else static_piece(P, item, r1, pc);
 #if FLEXQ_ATTN_TRACE
         ++n_pieces;
 #endif
@@ -231,7 +273,6 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         const int first = pc.o * kChunk;
         const int len = min(P.cur_len - first, pc.nch * kChunk);
         const int nst = (pc.nch + kNch - 1) / kNch;
-        const bool whole = pc.o == 0 && pc.nch == P.nck;
 
         // fused append: the piece holding token cur_len - 1 quantizes k_new / v_new (they
         // arrive with its first stage), and patches the stage images of its last K and V
@@ -306,41 +347,82 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
             release();
         }
 
-        // ------------------------------------------------ end of piece
+        // ------------------------------------------------ end of item
         float l;
-        if (whole) {
+        if (pc.np == 1) {
             v_finish_mma<D>(va, vlane, lane, P.out + int64_t(bh) * D, l, nullptr);
             continue;
         }
-        int np = 0;
-        const int k = head_pieces(P, W, bh, pc.o, np);
-        const int64_t slot0 = int64_t(bh) * P.pmax;
+        // a piece: store the partial, then count its tokens on the head's ticket (release: the
+        // partial stores of every lane happen before the increment, through the warp barrier);
+        // the piece that completes the count merges all of them in piece order (deterministic)
+        int np = pc.np, k = pc.k;
+        if (np == 0) k = head_pieces(P, W, bh, pc.o, np);
+        const int64_t slot0 = int64_t(bh) * kMaxPieces;
         v_finish_mma<D>(va, vlane, lane, nullptr, l, P.part + (slot0 + k) * D);
         if (lane == 0) P.ml[slot0 + k] = make_float2(M, l);
-        __threadfence();
         __syncwarp();
         uint32_t done = 0;
-        if (lane == 0) done = atomicAdd(&P.tickets[bh], uint32_t(len)) + uint32_t(len);
+        if (lane == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            done = atomicAdd(&P.tickets[bh], uint32_t(len)) + uint32_t(len);
+            if (done == uint32_t(P.cur_len)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
         done = __shfl_sync(0xffffffffu, done, 0);
-        if (done == uint32_t(P.cur_len)) {   // the last piece of this (b, h) to finish: merge in token order
-            __threadfence();
-            float Mx = -INFINITY;
-            for (int i = 0; i < np; ++i) Mx = fmaxf(Mx, __ldcg(&P.ml[slot0 + i].x));
-            float num[D / 32], den = 0.0f;
+        if (done == uint32_t(P.cur_len)) {   // every piece of this (b, h) is in: merge
+            // all loads are independent (no serial round trips): lane i < np holds piece i's
+            // (m, l); lane c owns columns 4c .. 4c + 3 (D = 128) or 2c, 2c + 1 (D = 64)
+            constexpr int CPL = D / 32;
+            const float2 mli = lane < np ? __ldcg(&P.ml[slot0 + lane]) : make_float2(-INFINITY, 0.0f);
+            float Mx = mli.x;
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) num[c] = 0.0f;
+            for (int o = 16; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+            const float wi = lane < np ? ex2(mli.x - Mx) : 0.0f;
+            float den = wi * mli.y;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+            float num[CPL];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) num[c] = 0.0f;
+#pragma unroll 4
             for (int i = 0; i < np; ++i) {
-                const float2 mlv = __ldcg(&P.ml[slot0 + i]);
-                const float w = ex2(mlv.x - Mx);
-                const float* pr = P.part + (slot0 + i) * D;
-#pragma unroll
-                for (int c = 0; c < D / 32; ++c) num[c] = fmaf(w, __ldcg(pr + lane + 32 * c), num[c]);
-                den = fmaf(w, mlv.y, den);
+                const float w = __shfl_sync(0xffffffffu, wi, i);
+                const float* pr = P.part + (slot0 + i) * D + CPL * lane;
+                if constexpr (CPL == 4) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(pr));
+                    num[0] = fmaf(w, v.x, num[0]);
+                    num[1] = fmaf(w, v.y, num[1]);
+                    num[2] = fmaf(w, v.z, num[2]);
+                    num[3] = fmaf(w, v.w, num[3]);
+                } else {
+                    const float2 v = __ldcg(reinterpret_cast<const float2*>(pr));
+                    num[0] = fmaf(w, v.x, num[0]);
+                    num[1] = fmaf(w, v.y, num[1]);
+                }
             }
             const float inv = 1.0f / den;
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) P.out[int64_t(bh) * D + lane + 32 * c] = __float2half_rn(num[c] * inv);
+            __half* o = P.out + int64_t(bh) * D + CPL * lane;
+            if constexpr (CPL == 4) {
+                const __half2 h0 = __floats2half2_rn(num[0] * inv, num[1] * inv);
+                const __half2 h1 = __floats2half2_rn(num[2] * inv, num[3] * inv);
+                uint2 u;
+                u.x = *reinterpret_cast<const uint32_t*>(&h0);
+                u.y = *reinterpret_cast<const uint32_t*>(&h1);
+                *reinterpret_cast<uint2*>(o) = u;
+            } else {
+                *reinterpret_cast<__half2*>(o) = __floats2half2_rn(num[0] * inv, num[1] * inv);
+            }
             if (lane == 0) P.tickets[bh] = 0u;   // leave the workspace zeroed
+        }
+    }
+
+    // retire: the last warp out resets the item ticket for the next call
+    if (P.dynamic && lane == 0) {
+        __threadfence();
+        if (atomicAdd(P.ctrl + 1, 1u) == gridDim.x - 1) {
+            P.ctrl[0] = 0u;
+            P.ctrl[1] = 0u;
+            __threadfence();
         }
     }
 #if FLEXQ_ATTN_TRACE
@@ -386,51 +468,84 @@ DevInfo dev_info() {
     return info[dev];
 }
 
-// Partial slots per head for a launch over W warps (a bound on head_pieces' count).
-int pieces_bound(int bh, int nck, int W, int maxch) {
-    const int64_t b = int64_t(nck) / maxch + 1 + (int64_t(W) + bh - 1) / bh;
-    return int(std::min<int64_t>(nck, b));
-}
-
 struct WsLayout {
-    size_t tickets, part, ml, total;
-    int pmax;
+    size_t ctrl, tickets, part, ml, total;
 };
-WsLayout ws_layout(int bh, int d, int t_cap) {
-    const int nck = int((t_cap + kChunk - 1) / kChunk);
+WsLayout ws_layout(int bh, int d) {
     WsLayout w;
-    w.pmax = pieces_bound(bh, nck, kMaxWarps, kMinMaxT / kChunk);
+    w.ctrl = 0;
     w.tickets = 256;
     w.part = (w.tickets + size_t(bh) * 4 + 255) / 256 * 256;
-    w.ml = w.part + size_t(bh) * w.pmax * d * 4;
-    w.total = w.ml + size_t(bh) * w.pmax * 8;
+    w.ml = w.part + size_t(bh) * kMaxPieces * d * 4;
+    w.total = w.ml + size_t(bh) * kMaxPieces * 8;
     return w;
+}
+
+// Scheduler choice and tail split (tuning only):
+// FLEXQ_ATTN_SPLIT="<min heads per warp x 100 for dynamic>,<tail heads per warp x 100>,<pieces per tail head>".
+constexpr int kDynHeadsPerWarpX100 = 150;   // B200 sweep: dynamic wins from ~1.5 heads per warp
+void tune_split(int& dyn_min_x100, int& nb_per_warp_x100, int& kb) {
+    static int v0 = -1, v1 = -1, v2 = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* e = getenv("FLEXQ_ATTN_SPLIT");
+        if (e) sscanf(e, "%d,%d,%d", &v0, &v1, &v2);
+    });
+    if (v0 >= 0) dyn_min_x100 = v0;
+    if (v1 >= 0) nb_per_warp_x100 = v1;
+    if (v2 > 0) kb = v2;
 }
 
 template <int D, int MAXT>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
     const DevInfo di = dev_info<D, MAXT>();
+    const int Wres = std::min(di.sms * di.occ, kMaxWarps);
     const int nck = (a.cur_len + kChunk - 1) / kChunk;
-    const int total = bh * nck;
-    const int W = std::max(1, std::min({di.sms * di.occ, kMaxWarps, total / kMinPieceChunks}));
     const int maxch = MAXT / kChunk;
-    const WsLayout w = ws_layout(bh, D, a.t_cap);
+    const int ka = (nck + maxch - 1) / maxch;
+    if (ka > kMaxPieces / 2) return cudaErrorInvalidValue;   // context beyond 16 score buffers
+    // Scheduler (B200 sweep): with many heads per warp, dynamic tickets over whole
+    // heads balance the per-SM rate differences and leave a short tail; with few, static
+    // stream-K ranges keep every warp streaming (a whole-head ticket would idle warps).
+    int dyn_min_x100 = kDynHeadsPerWarpX100, nb_x100 = 0, kb = 0;
+    tune_split(dyn_min_x100, nb_x100, kb);
+    const bool dynamic = int64_t(bh) * 100 >= int64_t(dyn_min_x100) * Wres;
+    int W, na = bh, nb = 0;
+    if (dynamic) {
+        W = Wres;
+        nb = int(std::min<int64_t>(bh, (int64_t(W) * nb_x100 + 99) / 100));
+        if (kb <= 0) kb = 2;
+        kb = std::max(ka, std::min({kb, std::max(1, nck / kMinPieceChunks), kMaxPieces}));
+        if (kb <= 1) nb = 0;
+        na = bh - nb;
+    } else {
+        // >= kMinPieceChunks chunks per warp and <= 16 warps per head keep a head's pieces
+        // within kMaxPieces (head_pieces <= 1 + ceil(W / bh) + ceil(nck / maxch))
+        W = std::max(1, std::min({Wres, bh * nck / kMinPieceChunks, bh * 15}));
+        kb = 1;
+    }
+    const WsLayout w = ws_layout(bh, D);
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     Params P;
     P.q = static_cast<const __half*>(a.q);
     P.kc = static_cast<const uint8_t*>(a.k_cache);
     P.vc = static_cast<const uint8_t*>(a.v_cache);
     P.out = static_cast<__half*>(a.out);
+    P.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
     P.tickets = reinterpret_cast<uint32_t*>(ws + w.tickets);
     P.part = reinterpret_cast<float*>(ws + w.part);
     P.ml = reinterpret_cast<float2*>(ws + w.ml);
-    P.total = total;
     P.nck = nck;
+    P.na = na;
+    P.ka = ka;
+    P.kb = kb;
+    P.items = na * ka + nb * kb;
+    P.dynamic = dynamic ? 1 : 0;
+    P.total = bh * nck;
+    P.wq = P.total / W;
+    P.wr = P.total % W;
     P.maxch = maxch;
-    P.pmax = w.pmax;   // >= pieces_bound(bh, nck, W, maxch): nck <= the capacity's, W <= kMaxWarps
-    P.wq = total / W;
-    P.wr = total % W;
     P.chunks = a.chunks;
     P.cur_len = a.cur_len;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
@@ -443,7 +558,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         return !(e && e[0] == '0');
     }();
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(W));
+    cfg.gridDim = dim3(unsigned(dynamic ? std::max(1, std::min(W, P.items)) : W));
     cfg.blockDim = dim3(32);
     cfg.dynamicSmemBytes = smem_bytes<D, MAXT>();
     cfg.stream = stream;
@@ -458,7 +573,8 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
 }  // namespace
 
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) {
-    return ws_layout(batch * heads, head_dim, t_cap).total;
+    (void)t_cap;
+    return ws_layout(batch * heads, head_dim).total;
 }
 
 // Score buffer sized to the context: 576 tokens covers every prompt-512 step in one piece
