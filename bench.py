@@ -11,7 +11,12 @@ HBM).  metric: algorithmic compressed-KV GB/s of the step (whole job), with
 tokens/s alongside.
 
     python bench.py [--gpus N --steps K --warmup W] [--config opt-175b] [--impl reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, weak scaling)
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+`--gpus N` without torchrun re-launches itself under torch.distributed.run with N ranks.
+Scaling: OPT-175B is strong-scaled by default (BASELINE configs[3]: an effective batch of 144
+sharded across the GPUs); a weak-scaling run (every rank its own batch of 144) is
+reported beside it as `weak_scaling`.
 """
 from __future__ import annotations
 
@@ -38,7 +43,9 @@ def parse():
     ap.add_argument("--impl", default="flexq", choices=["flexq", "reference"])
     ap.add_argument("--config", default="opt-175b")
     ap.add_argument("--layers", type=int, default=0, help="override model depth (0 = full)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="default: strong for opt-175b (global batch 144 sharded), weak otherwise")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling secondary run (N > 1)")
     ap.add_argument("--step", default="fused", choices=["fused", "two"],
                     help="per layer: one fused append+attention launch (NEXT-3) or append_kv then attention")
     ap.add_argument("--no-e2e", action="store_true")
@@ -48,7 +55,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--same-device", action="store_true",
                     help="all ranks on cuda:0 with gloo (functional test of the N > 1 path on one GPU)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.scaling is None:
+        a.scaling = "strong" if a.config == "opt-175b" else "weak"
+    return a
 
 
 # ---------------------------------------------------------------- helpers
@@ -141,6 +151,10 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                         f"(python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus "
+                         f"{args.gpus} ...), or run without torchrun and let bench.py launch it")
     if args.same_device:          # functional test of the multi-rank path on one GPU (gloo)
         local = 0
     pg = None
@@ -235,7 +249,7 @@ def run_reference(args):
     tok_s = seqs / w.layers
     line = {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u4+f16->f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u4+f16->f32",
             "data": "synthetic", "tokens_per_s": round(tok_s, 4),
             "config": {"workload": f"{w.name}: batch {w.batch}, {w.heads}x{w.head_dim}, s={w.prompt_len}, "
                                    f"n={w.gen_len}, l={w.layers}; oracle on a bounded per-step sample",
@@ -247,11 +261,174 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- flexq arm
-def run_flexq(args):
+def rank_rows(B_total: int, world: int, rank: int, scaling: str, per_gpu: int) -> tuple[int, int]:
+    """Global sequence rows [b0, b1) of `rank`: its shard of the fixed global batch (strong) or
+    its own block of per_gpu sequences (weak).  Inputs are drawn per global row, so any
+    sharding sees the same sequences a single process would."""
+    from paper_2303_06865_b200 import dist as fd
+    if scaling == "strong":
+        return fd.shard(B_total, world, rank)
+    return rank * per_gpu, (rank + 1) * per_gpu
+
+
+class DecodeModel:
+    """The compressed KV caches of every layer for sequences [b0, b1) of a global batch, with
+    the step's per-layer inputs (q, k_new, v_new) and one CUDA graph per decode step i."""
+
+    def __init__(self, w, L, B_total, b0, b1, seed, dev, stream, fused=True):
+        import torch
+        from paper_2303_06865_b200 import flexq as fq
+        from paper_2303_06865_b200 import synth
+        self.fq, self.w, self.L, self.B = fq, w, L, b1 - b0
+        self.b0, self.b1, self.B_total, self.stream, self.fused = b0, b1, B_total, stream, fused
+        H, D, s, n = w.heads, w.head_dim, w.prompt_len, w.gen_len
+        self.steps_i = list(range(1, n)) if n > 1 else [1]
+        with torch.cuda.stream(stream):
+            self.caches = [fq.KVCache(self.B, H, D, s, max(n, 1), device=dev) for _ in range(L)]
+            kp = synth.fill_rows(seed, synth.tensor_id(0, synth.K_PROMPT), (B_total, H, s, D), b0, b1, device=dev)
+            vp = synth.fill_rows(seed, synth.tensor_id(0, synth.V_PROMPT), (B_total, H, s, D), b0, b1, device=dev)
+            for c in self.caches:                                  # prompt fill (prefill's KV, quantized)
+                fq.flexq_append_kv(kp, vp, c, pos=0, stream=stream)
+            del kp, vp
+            rows = lambda kind, j: synth.fill_rows(seed, synth.tensor_id(j, kind), (B_total, H, D), b0, b1,  # noqa: E731
+                                                   device=dev)
+            self.qs = torch.stack([rows(synth.Q, j) for j in range(L)])
+            self.kn = torch.stack([rows(synth.K_NEW, j) for j in range(L)])
+            self.vn = torch.stack([rows(synth.V_NEW, j) for j in range(L)])
+            self.outs = torch.empty(L, self.B, H, D, dtype=torch.float16, device=dev)
+            self.ws = fq.make_workspace(self.caches[0])
+        torch.cuda.synchronize()
+        self.graphs = {}
+
+    def nbytes(self):
+        return sum(c.nbytes() for c in self.caches)
+
+    def layer_step(self, j, cur, q, k_new, v_new, out, st):
+        """One layer of decode step cur_len = cur: append the token, attend (one or two launches)."""
+        fq, B, H, D = self.fq, self.B, self.w.heads, self.w.head_dim
+        if self.fused:
+            fq.flexq_append_decode_attention(q, k_new, v_new, self.caches[j], cur, out=out, workspace=self.ws,
+                                             stream=st)
+        else:
+            fq.flexq_append_kv(k_new.view(B, H, 1, D), v_new.view(B, H, 1, D), self.caches[j], pos=cur - 1,
+                               stream=st)
+            fq.flexq_decode_attention(q, self.caches[j], cur, out=out, workspace=self.ws, stream=st)
+
+    def step_calls(self, i, st):
+        cur = self.w.prompt_len + i
+        for j in range(self.L):
+            self.layer_step(j, cur, self.qs[j], self.kn[j], self.vn[j], self.outs[j], st)
+
+    def capture(self):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.step_calls(self.steps_i[0], self.stream)          # warm the launch path before capture
+        torch.cuda.synchronize()
+        for i in self.steps_i:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self.step_calls(i, self.stream)
+            self.graphs[i] = g
+        torch.cuda.synchronize()
+
+    def seq_of(self, k):
+        return self.steps_i[k % len(self.steps_i)]
+
+    def step_bytes(self, i, rows):
+        from paper_2303_06865_b200 import workloads as wl
+        h1 = self.w.h1
+        return self.L * (wl.attention_bytes(rows, h1, self.w.prompt_len + i) + wl.append_bytes(rows, h1))
+
+    def time_steps(self, warmup, steps, barrier, clocks=None):
+        """W untimed steps, then K timed steps (CUDA events on the launching stream)."""
+        import torch
+        for k in range(warmup):
+            self.graphs[self.seq_of(k)].replay()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx = clocks if clocks is not None else _Null()
+        with ctx:
+            with torch.cuda.stream(self.stream):
+                ev0.record(self.stream)
+                for k in range(steps):
+                    self.graphs[self.seq_of(warmup + k)].replay()
+                ev1.record(self.stream)
+            barrier()
+        return ev0.elapsed_time(ev1), [self.seq_of(warmup + k) for k in range(steps)]
+
+    def per_launch(self, cur, which, reps=5, layers=None):
+        """Average launch time (us) of `which` in {attn, append, fused, topk} over one CUDA graph of
+        `layers` launches (one per layer cache) at cur_len = cur."""
+        import torch
+        fq, st = self.fq, self.stream
+        L = self.L if layers is None else min(layers, self.L)
+        keep = fq.topk_keep(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for j in range(L):
+                if which == "attn":
+                    fq.flexq_decode_attention(self.qs[j], self.caches[j], cur, out=self.outs[j], workspace=self.ws,
+                                              stream=st)
+                elif which == "append":
+                    fq.flexq_append_kv(self.kn[j].unsqueeze(2), self.vn[j].unsqueeze(2), self.caches[j],
+                                       pos=cur - 1, stream=st)
+                elif which == "topk":
+                    fq.flexq_decode_attention_topk(self.qs[j], self.caches[j], cur, keep, out=self.outs[j],
+                                                   workspace=self.ws, stream=st)
+                else:                   # fused: rewrites the same token at cur - 1 (idempotent)
+                    fq.flexq_append_decode_attention(self.qs[j], self.kn[j], self.vn[j], self.caches[j], cur,
+                                                     out=self.outs[j], workspace=self.ws, stream=st)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for _ in range(reps):
+                g.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / (reps * L)
+
+    def free(self):
+        self.graphs.clear()
+        del self.caches, self.qs, self.kn, self.vn, self.outs, self.ws
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def reference_output(w, B_total, row, layer, step_i, seed, dev):
+    """Recompute, for one global sequence `row`, the attention output of `layer` at decode step
+    step_i from scratch (its own one-sequence cache: prompt fill, then the step's token k_new of
+    that layer appended at every position s .. s + i - 1, exactly what steps 1..i write)."""
     import torch
     from paper_2303_06865_b200 import flexq as fq
     from paper_2303_06865_b200 import synth
+    H, D, s, n = w.heads, w.head_dim, w.prompt_len, w.gen_len
+    c = fq.KVCache(1, H, D, s, max(n, 1), device=dev)
+    kp = synth.fill_rows(seed, synth.tensor_id(0, synth.K_PROMPT), (B_total, H, s, D), row, row + 1, device=dev)
+    vp = synth.fill_rows(seed, synth.tensor_id(0, synth.V_PROMPT), (B_total, H, s, D), row, row + 1, device=dev)
+    fq.flexq_append_kv(kp, vp, c, pos=0)
+    one = lambda kind: synth.fill_rows(seed, synth.tensor_id(layer, kind), (B_total, H, D), row, row + 1,  # noqa: E731
+                                       device=dev)
+    kn, vn, q = one(synth.K_NEW), one(synth.V_NEW), one(synth.Q)
+    for pos in range(s, s + step_i):
+        fq.flexq_append_kv(kn.unsqueeze(2), vn.unsqueeze(2), c, pos=pos)
+    out = fq.flexq_decode_attention(q, c, s + step_i)
+    torch.cuda.synchronize()
+    return out[0]
+
+
+def run_flexq(args):
+    import torch
+    from paper_2303_06865_b200 import flexq as fq
     from paper_2303_06865_b200 import workloads as wl
+    from paper_2303_06865_b200 import dist as fd
 
     world, rank, local, pg = dist_setup(args)
     dev = torch.device("cuda", local)
@@ -261,191 +438,106 @@ def run_flexq(args):
     w = wl.CONFIGS[args.config]
     if args.layers:
         w = wl.Workload(w.name, w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len, args.layers, w.h2)
-    from paper_2303_06865_b200 import dist as fd
-    B_total = w.batch * (world if args.scaling == "weak" else 1)
-    B = fd.rank_batch(w.batch, world, rank, args.scaling)
-    if B == 0:
+    scaling = args.scaling
+    B_total = w.batch if scaling == "strong" else w.batch * world
+    b0, b1 = rank_rows(B_total, world, rank, scaling, w.batch)
+    if b1 <= b0:
         raise SystemExit(f"--scaling strong needs batch ({w.batch}) >= ranks ({world})")
     H, D, s, n, L = w.heads, w.head_dim, w.prompt_len, w.gen_len, w.layers
     h1 = H * D
-    seed = synth.BASE_SEED + 3 + 1000 * rank
+    seed = synth_seed()
     stream = torch.cuda.Stream(device=dev)
-
-    # ---- setup: compressed caches for all layers resident in HBM
-    log("setup")
-    with torch.cuda.stream(stream):
-        caches = [fq.KVCache(B, H, D, s, n, device=dev) for _ in range(L)]
-        kp = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D), device=dev)
-        vp = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D), device=dev)
-        for c in caches:                                  # prompt fill (prefill's KV, quantized)
-            fq.flexq_append_kv(kp, vp, c, pos=0)
-        del kp, vp
-        qs = synth.fill(seed, synth.tensor_id(0, synth.Q), (L, B, H, D), device=dev)
-        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW), (L, B, H, 1, D), device=dev)
-        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW), (L, B, H, 1, D), device=dev)
-        outs = torch.empty(L, B, H, D, dtype=torch.float16, device=dev)
-        ws = fq.make_workspace(caches[0])
-    torch.cuda.synchronize()
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    cache_bytes = sum(c.nbytes() for c in caches)
-
     fused = args.step == "fused"
-
-    def layer_step(j, cur, q, k_new, v_new, out, st):
-        """One layer of decode step cur_len = cur: append the token, attend (one or two launches)."""
-        if fused:
-            fq.flexq_append_decode_attention(q, k_new, v_new, caches[j], cur, out=out, workspace=ws, stream=st)
-        else:
-            fq.flexq_append_kv(k_new.view(B, H, 1, D), v_new.view(B, H, 1, D), caches[j], pos=cur - 1, stream=st)
-            fq.flexq_decode_attention(q, caches[j], cur, out=out, workspace=ws, stream=st)
-
-    def step_calls(i, st):
-        cur = s + i
-        for j in range(L):
-            layer_step(j, cur, qs[j], kn[j], vn[j], outs[j], st)
-
-    # one CUDA graph per decode step i = 1..n-1
-    log("prompt fill done; capturing graphs")
-    steps_i = list(range(1, n))
-    graphs = {}
-    with torch.cuda.stream(stream):
-        step_calls(1, stream)                              # warm the launch path before capture
-    torch.cuda.synchronize()
-    for i in steps_i:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            step_calls(i, stream)
-        graphs[i] = g
-    torch.cuda.synchronize()
-
-    def seq_of(k):
-        return steps_i[k % len(steps_i)]
-
-    step_bytes = {i: L * (wl.attention_bytes(B, h1, s + i) + wl.append_bytes(B, h1)) for i in steps_i}
+    peak, peak_kind = peaks()
 
     def barrier():
         if pg:
             pg.barrier()
         torch.cuda.synchronize()
 
-    # ---- warmup + timed region (device events on the launching stream)
+    # ---- setup: compressed caches for all layers resident in HBM
+    log(f"setup: rows [{b0}, {b1}) of a global batch of {B_total} ({scaling} scaling, {world} rank(s))")
+    m = DecodeModel(w, L, B_total, b0, b1, seed, dev, stream, fused)
+    B = m.B
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    cache_bytes = m.nbytes()
+    log("prompt fill done; capturing graphs")
+    m.capture()
+
+    # ---- warmup + timed region
     log("graphs captured; timing")
-    for k in range(args.warmup):
-        graphs[seq_of(k)].replay()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
-            for k in range(args.steps):
-                i = seq_of(args.warmup + k)
-                graphs[i].replay()
-            ev1.record(stream)
-        barrier()
-    ms = fd.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    clk = ClockSampler(local)
+    ms, seqs = m.time_steps(args.warmup, args.steps, barrier, clk)
+    ms = fd.max_over_ranks(ms, device=dev)
     ms_step = ms / args.steps
-    job_bytes = B_total * sum(L * (wl.attention_bytes(1, h1, s + seq_of(args.warmup + k)) + wl.append_bytes(1, h1))
-                              for k in range(args.steps))
+    job_bytes = sum(m.step_bytes(i, B_total) for i in seqs)
     value_gbs = job_bytes / (ms / 1e3) / 1e9
     tokens_per_s = B_total * args.steps / (ms / 1e3)
+    last_i = seqs[-1]
 
-    # ---- N > 1: gather every rank's outputs of one layer-step (NCCL all-gather, SURVEY 8(e)),
-    # outside the timed data path and timed on its own; checked against each rank's own block
-    allgather = None
+    # ---- outputs: all-gather one layer-step's fp16 outputs (NCCL, outside the timed data path),
+    # then rank 0 recomputes the last global sequence (owned by the last rank) from scratch on its
+    # own one-sequence cache and checks the gathered row (reading Q's tolerance: the one-sequence
+    # launch schedules its pieces differently)
+    gather = None
+    out_last = m.outs[L - 1]
+    check_row = B_total - 1
     if world > 1:
         torch.cuda.synchronize()
-        # same-device functional runs use gloo, which gathers host tensors
-        src = outs[L - 1].cpu() if args.same_device else outs[L - 1]
-        G_out = B_total if args.scaling == "strong" else B * world
-        per = (G_out + world - 1) // world
-        full = fd.gather_outputs(src, G_out)
-        ok = bool(torch.equal(full[rank * per: rank * per + B], src))
-        barrier()
-        t0 = time.perf_counter()
+        src = out_last.cpu() if args.same_device else out_last
+        full = fd.gather_outputs(src, B_total)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         g0.record()
         for _ in range(20):
-            fd.gather_outputs(src, G_out)
+            fd.gather_outputs(src, B_total)
         g1.record()
         torch.cuda.synchronize()
         ag_us = (g0.elapsed_time(g1) if not args.same_device else (time.perf_counter() - t0) * 1e3) / 20 * 1e3
         ag_us = fd.max_over_ranks(ag_us, device=dev)
-        ok_all = fd.max_over_ranks(0.0 if ok else 1.0, device=dev) == 0.0
-        allgather = {"what": "all_gather_into_tensor of one layer-step's fp16 outputs [B][H][D] per rank",
-                     "bytes_per_rank": int(src.numel() * 2), "us": round(ag_us, 1),
-                     "matches_rank_blocks": ok_all, "in_timed_region": False,
-                     "backend": "gloo (same-device functional run)" if args.same_device else "nccl"}
+        got_row = full[check_row].to(dev)
+        import torch.distributed as dist
+        gather = {"what": "all_gather of one layer-step's fp16 outputs [B_rank][H][D] per rank",
+                  "bytes_per_rank": int(src.numel() * 2), "us": round(ag_us, 1), "in_timed_region": False,
+                  "backend": dist.get_backend(), "comm_size": dist.get_world_size(),
+                  "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if not args.same_device else None}
         del full
+    else:
+        got_row = out_last[check_row - b0]
+    check = None
+    if rank == 0:
+        ref = reference_output(w, B_total, check_row, L - 1, last_i, seed, dev).float()
+        err = (got_row.float() - ref).abs()
+        ok = bool((err <= torch.clamp(1e-2 * ref.abs(), min=2e-3)).all())
+        check = {"row": check_row, "owner_rank": fd.owner(B_total, world, check_row), "layer": L - 1,
+                 "cur_len": s + last_i, "max_abs_err": float(err.max()), "within_reading_Q": ok,
+                 "what": "rank 0 recomputes the last global sequence's output from scratch on a one-sequence "
+                         "cache and checks the row gathered from its owner"}
+        if not ok:
+            log(f"cross-rank output check FAILED: {check}")
 
-    # ---- dominant kernel: attention alone, one graph of L launches at cur_len = s + n - 1
+    # ---- dominant kernel: per-launch time at the longest context (cur_len = s + n - 1)
     log("timed; per-kernel pass")
-    cur_last = s + n - 1
-    ga = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(ga, stream=stream):
-        for j in range(L):
-            fq.flexq_decode_attention(qs[j], caches[j], cur_last, out=outs[j], workspace=ws, stream=stream)
-    gapp = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gapp, stream=stream):
-        for j in range(L):
-            fq.flexq_append_kv(kn[j], vn[j], caches[j], pos=cur_last - 1, stream=stream)
-    gfu = torch.cuda.CUDAGraph()          # fused append + attention (rewrites the same token: idempotent)
-    with torch.cuda.graph(gfu, stream=stream):
-        for j in range(L):
-            fq.flexq_append_decode_attention(qs[j], kn[j], vn[j], caches[j], cur_last, out=outs[j], workspace=ws,
-                                             stream=stream)
-    reps = 5
-    for g in (ga, gapp, gfu):
-        g.replay()
-    torch.cuda.synchronize()
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    with torch.cuda.stream(stream):
-        e[0].record(stream)
-        for _ in range(reps):
-            ga.replay()
-        e[1].record(stream)
-        for _ in range(reps):
-            gapp.replay()
-        e[2].record(stream)
-        for _ in range(reps):
-            gfu.replay()
-        e[3].record(stream)
-    torch.cuda.synchronize()
-    attn_us = e[0].elapsed_time(e[1]) * 1e3 / (reps * L)
-    app_us = e[1].elapsed_time(e[2]) * 1e3 / (reps * L)
-    fused_us = e[2].elapsed_time(e[3]) * 1e3 / (reps * L)
+    cur_last = s + m.steps_i[-1]
+    attn_us = m.per_launch(cur_last, "attn")
+    app_us = m.per_launch(cur_last, "append")
+    fused_us = m.per_launch(cur_last, "fused")
     attn_bytes = wl.attention_bytes(B, h1, cur_last)
     fused_bytes = attn_bytes + wl.append_bytes(B, h1)
-    peak, peak_kind = peaks()
-    # the dominant kernel is the one the step launches per layer
     k_us, k_bytes = (fused_us, fused_bytes) if fused else (attn_us, attn_bytes)
     achieved = k_bytes / (k_us * 1e-6) / 1e9
 
     # ---- NEXT-1: Top-K sparse attention (keep 10%, P:854) at the same shape
     topk = None
-    if cur_last <= 1152:
+    if cur_last <= 1152 and rank == 0:
         keep = fq.topk_keep(cur_last)
-        gt = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gt, stream=stream):
-            for j in range(L):
-                fq.flexq_decode_attention_topk(qs[j], caches[j], cur_last, keep, out=outs[j], workspace=ws,
-                                               stream=stream)
-        gt.replay()
-        torch.cuda.synchronize()
-        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            t0e.record(stream)
-            for _ in range(reps):
-                gt.replay()
-            t1e.record(stream)
-        torch.cuda.synchronize()
-        tk_us = t0e.elapsed_time(t1e) * 1e3 / (reps * L)
+        tk_us = m.per_launch(cur_last, "topk")
         kv_row = h1 // 2 + h1 // 64 * 4                      # one token's K (or V) bytes over all heads
         tk_bytes = B * (cur_last * kv_row + keep * kv_row + 2 * h1 * 2)
         topk = {"keep": keep, "cur_len": cur_last, "us_per_launch": round(tk_us, 2),
                 "algorithmic_bytes_per_launch": tk_bytes, "GBps": round(tk_bytes / (tk_us * 1e-6) / 1e9, 1),
                 "speedup_vs_dense": round(attn_us / tk_us, 3),
-                "note": "bytes = K for all tokens + V for the kept 10% (P:856) + q + out; the V gather "
-                        "reads each kept token's 4-token quad row"}
+                "note": "bytes = K for all tokens + V for the kept 10% (P:856) + q + out"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tp) and w.name == "opt-175b" and B == 144:
@@ -455,68 +547,249 @@ def run_flexq(args):
     log("e2e")
     e2e = None
     if not args.no_e2e:
-        # one pinned block per layer holding (q, k_new, v_new): one H2D copy per layer
-        hin = torch.stack([qs, kn.view(qs.shape), vn.view(qs.shape)], dim=1).cpu().pin_memory()   # [L][3][B][H][D]
-        outh = torch.empty(outs.shape, dtype=outs.dtype).pin_memory()
-        NB = 6                                     # device slots: H2D runs up to NB layers ahead
-        din = [torch.empty_like(hin[0], device=dev) for _ in range(NB)]
-        dout = [torch.empty_like(outs[0]) for _ in range(NB)]
-        h2d = torch.cuda.Stream(device=dev)       # one stream per copy direction: both copy engines busy
-        d2h = torch.cuda.Stream(device=dev)
-        ready = [torch.cuda.Event() for _ in range(NB)]
-        consumed = [torch.cuda.Event() for _ in range(NB)]
-        drained = [torch.cuda.Event() for _ in range(NB)]
-        gl = [0]                                   # global layer counter (slot = gl % NB)
+        e2e = run_e2e(m, args, dev, barrier, B_total)
+    m.free()
+    del m
+    torch.cuda.empty_cache()
 
-        def e2e_step(i):
-            cur = s + i
-            for j in range(L):
-                g = gl[0]
-                gl[0] += 1
-                b = g % NB
-                with torch.cuda.stream(h2d):
-                    if g >= NB:
-                        h2d.wait_event(consumed[b])        # slot b's inputs consumed by layer g - NB
-                    din[b].copy_(hin[j], non_blocking=True)
-                    ready[b].record(h2d)
-                stream.wait_event(ready[b])
-                if g >= NB:
-                    stream.wait_event(drained[b])          # slot b's output copied out
-                layer_step(j, cur, din[b][0], din[b][1], din[b][2], dout[b], stream)
-                consumed[b].record(stream)
-                with torch.cuda.stream(d2h):
-                    d2h.wait_event(consumed[b])
-                    outh[j].copy_(dout[b], non_blocking=True)
-                    drained[b].record(d2h)
+    # ---- weak-scaling secondary key (N > 1 strong runs): every rank its own full batch
+    weak = None
+    if world > 1 and scaling == "strong" and not args.no_weak:
+        log("weak-scaling secondary")
+        wb0, wb1 = rank_rows(w.batch * world, world, rank, "weak", w.batch)
+        mw = DecodeModel(w, L, w.batch * world, wb0, wb1, seed, dev, stream, fused)
+        mw.capture()
+        wms, wseqs = mw.time_steps(args.warmup, args.steps, barrier)
+        wms = fd.max_over_ranks(wms, device=dev)
+        wbytes = sum(mw.step_bytes(i, w.batch * world) for i in wseqs)
+        weak = {"value": round(wbytes / (wms / 1e3) / 1e9, 2), "unit": "GB/s", "scaling": "weak",
+                "global_batch": w.batch * world, "batch_per_gpu": w.batch, "ms_per_step": round(wms / args.steps, 4),
+                "tokens_per_s": round(w.batch * world * args.steps / (wms / 1e3), 2)}
+        mw.free()
+        del mw
+        torch.cuda.empty_cache()
 
-        for k in range(2):
-            e2e_step(seq_of(k))
-        barrier()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e2e_bytes = 0
-        ke = max(3, min(args.steps, 10))
-        x0.record(stream)
-        for k in range(ke):
-            i = seq_of(k)
+    extra = {}
+    if rank == 0 and world == 1 and w.name == "opt-175b" and not args.no_sweep:
+        extra = run_sweeps(args, dev, stream, seed, peak)
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    log("cpu baseline")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_object(w, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "u4+f16->f32", "data": "synthetic (counter-based Irwin-Hall fp16, P:41/P:44)",
+            "tokens_per_s": round(tokens_per_s, 2),
+            "attention_tokens_per_s_per_layer": round(tokens_per_s * L, 1),
+            "config": {"workload": f"{w.name} decode step: global batch {B_total} ({scaling} scaling: {B} per GPU), "
+                                   f"{H} heads x {D}, s={s}, n={n}, l={L} layers, "
+                                   + ("fused append+attention (one launch) per layer, " if fused else
+                                      "append_kv + decode_attention per layer, ") +
+                                   f"steps cycle cur_len {s + 1}..{s + n - 1}",
+                       "global_batch": B_total, "seq_len": s + n, "parallelism": f"dp{world} (sequences)",
+                       "l2": f"working set {cache_bytes / 1e9:.1f} GB per GPU >> {l2 / 1e6:.0f} MB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": "profiles/attention_traffic.json (ncu --set full, same launch shape)",
+                         "kernel": "decode_attention_kernel<128>" + (" (fused append)" if fused else ""),
+                         "peak_kind": peak_kind,
+                         "bytes_per_launch": k_bytes, "us_per_launch": round(k_us, 2),
+                         # the step's algorithmic bytes at this kernel's measured rate, over the step time
+                         # (the per-launch pass runs at the longest context, cur_len = s + n - 1, so
+                         # k_us * L would overstate a step whose contexts run s + 1 .. s + n - 1)
+                         "share_of_step": round(value_gbs / (achieved * world) if fused else
+                                                attn_us * L / (ms_step * 1e3), 4),
+                         "attention_only_us_per_launch": round(attn_us, 2),
+                         "attention_only_GBps": round(attn_bytes / (attn_us * 1e-6) / 1e9, 1),
+                         "append_us_per_launch": round(app_us, 2),
+                         "fused_us_per_launch": round(fused_us, 2)},
+            "gpu_launches": args.steps * L * (1 if fused else 2),
+            "clocks": clk.result(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "topk_sparse": topk,
+            "dist": gather,
+            "output_check": check,
+            "weak_scaling": weak,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def synth_seed():
+    from paper_2303_06865_b200 import synth
+    return synth.BASE_SEED + 3
+
+
+def run_e2e(m, args, dev, barrier, B_total):
+    """The same step through the public API from HOST buffers: per layer, one H2D copy of the
+    pinned (q, k_new, v_new) block on a copy stream and one D2H copy of the layer's output on a
+    second copy stream (PCIe is full duplex), the fused launch in between; NB device slots let
+    the copies run ahead.  Each step is one CUDA graph (copies + launches + cross-stream
+    events), timed over the same --steps as the device region."""
+    import torch
+    from paper_2303_06865_b200 import dist as fd
+    L, s = m.L, m.w.prompt_len
+    hin = torch.stack([m.qs, m.kn, m.vn], dim=1).cpu().pin_memory()    # [L][3][B][H][D]
+    outh = torch.empty(m.outs.shape, dtype=m.outs.dtype).pin_memory()
+    NB = 8 if L % 8 == 0 else (6 if L % 6 == 0 else 4)
+    din = [torch.empty_like(hin[0], device=dev) for _ in range(NB)]
+    dout = [torch.empty_like(m.outs[0]) for _ in range(NB)]
+    st = m.stream
+    h2d = torch.cuda.Stream(device=dev)
+    d2h = torch.cuda.Stream(device=dev)
+
+    def e2e_step(i):
+        cur = s + i
+        ready = [torch.cuda.Event() for _ in range(L)]
+        consumed = [torch.cuda.Event() for _ in range(L)]
+        drained = [torch.cuda.Event() for _ in range(L)]
+        fork = torch.cuda.Event()
+        fork.record(st)
+        h2d.wait_event(fork)
+        d2h.wait_event(fork)
+        for j in range(L):
+            b = j % NB
+            with torch.cuda.stream(h2d):
+                if j >= NB:
+                    h2d.wait_event(consumed[j - NB])      # slot b's inputs consumed by layer j - NB
+                din[b].copy_(hin[j], non_blocking=True)
+                ready[j].record(h2d)
+            st.wait_event(ready[j])
+            if j >= NB:
+                st.wait_event(drained[j - NB])            # slot b's output copied out
+            m.layer_step(j, cur, din[b][0], din[b][1], din[b][2], dout[b], st)
+            consumed[j].record(st)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(consumed[j])
+                outh[j].copy_(dout[b], non_blocking=True)
+                drained[j].record(d2h)
+        st.wait_stream(h2d)
+        st.wait_stream(d2h)                               # join: the step's outputs are home
+
+    graphs = {}
+    for i in m.steps_i:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
             e2e_step(i)
-            e2e_bytes += step_bytes[i]
-        stream.wait_stream(d2h)                    # the last outputs are home
-        x1.record(stream)
-        barrier()
-        ems = fd.max_over_ranks(x0.elapsed_time(x1), device=dev)
-        e2e_job = e2e_bytes * (B_total / B if B else 0)
-        e2e = {"value": round(e2e_job / (ems / 1e3) / 1e9, 2),
-               "unit": "GB/s", "h2d_bytes_per_step": int(hin.nbytes),
-               "d2h_bytes_per_step": int(outh.nbytes), "ms_per_step": round(ems / ke, 3),
-               "tokens_per_s": round(B_total * ke / (ems / 1e3), 2),
-               "how": "pinned host (q, k_new, v_new) block per layer -> one H2D copy on a copy stream, D2H of the "
-                      "output on another, 6 device slots so copies run ahead of compute; append+attention via the "
-                      "C ABI, D2H of every layer's output; CUDA events, max over ranks"}
+        graphs[i] = g
+    torch.cuda.synchronize()
+    for k in range(args.warmup):
+        graphs[m.seq_of(k)].replay()
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_bytes = 0
+    with torch.cuda.stream(st):
+        x0.record(st)
+        for k in range(args.steps):
+            i = m.seq_of(args.warmup + k)
+            graphs[i].replay()
+            e2e_bytes += m.step_bytes(i, B_total)
+        x1.record(st)
+    barrier()
+    ems = fd.max_over_ranks(x0.elapsed_time(x1), device=dev)
+    res = {"value": round(e2e_bytes / (ems / 1e3) / 1e9, 2),
+           "unit": "GB/s", "h2d_bytes_per_step": int(hin.nbytes),
+           "d2h_bytes_per_step": int(outh.nbytes), "ms_per_step": round(ems / args.steps, 3),
+           "tokens_per_s": round(B_total * args.steps / (ems / 1e3), 2),
+           "pcie_floor_ms_per_step": None,
+           "how": f"pinned host (q, k_new, v_new) block per layer -> one H2D copy on a copy stream, D2H of the "
+                  f"layer's output on another (full duplex), {NB} device slots so copies run ahead of compute; "
+                  f"fused append+attention via the C ABI; one CUDA graph per step; CUDA events, max over ranks"}
+    # the PCIe floor: the step's H2D bytes at this box's pinned copy rate (both directions busy)
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import offload_bench
+        res["pcie_floor_ms_per_step"] = round(hin.nbytes / offload_bench.h2d_gbs(dev, 1 << 28) / 1e6, 3)
+    except Exception:  # noqa: BLE001
+        pass
+    del graphs, din, dout, hin, outh
+    return res
 
+
+def run_sweeps(args, dev, stream, seed, peak):
+    """Rank 0, N = 1: the other BASELINE configs as full-depth steps, the OPT-175B shard proxies,
+    the weight quantize / dequantize sweep + NEXT-2 GEMM, the KV-cache variants and NEXT-4."""
+    import torch
+    from paper_2303_06865_b200 import flexq as fq
+    from paper_2303_06865_b200 import synth
+    from paper_2303_06865_b200 import workloads as wl
+    out = {}
+    nobar = torch.cuda.synchronize
+
+    # ---- BASELINE configs[0..2]: tiny, OPT-6.7B, OPT-30B as full-depth decode steps on one GPU
+    log("config lines")
+    lines = {}
+    for cname in ("tiny", "opt-6.7b", "opt-30b"):
+        cw = wl.CONFIGS[cname]
+        cm = DecodeModel(cw, cw.layers, cw.batch, 0, cw.batch, seed + 11, dev, stream, True)
+        cm.capture()
+        steps = len(cm.steps_i)
+        cms, cseqs = cm.time_steps(2, steps, nobar)
+        cbytes = sum(cm.step_bytes(i, cw.batch) for i in cseqs)
+        cur = cw.prompt_len + cm.steps_i[-1]
+        kus = cm.per_launch(cur, "fused", layers=8)
+        kbytes = wl.attention_bytes(cw.batch, cw.h1, cur) + wl.append_bytes(cw.batch, cw.h1)
+        lines[cname] = {"batch": cw.batch, "heads": cw.heads, "head_dim": cw.head_dim, "layers": cw.layers,
+                        "steps": steps, "ms_per_step": round(cms / steps, 4),
+                        "value": round(cbytes / (cms / 1e3) / 1e9, 2), "unit": "GB/s",
+                        "tokens_per_s": round(cw.batch * steps / (cms / 1e3), 2),
+                        "fused_us_per_launch": round(kus, 2), "cur_len": cur,
+                        "frac_of_measured_hbm": round(kbytes / (kus * 1e-6) / 1e9 / peak, 4)}
+        cm.free()
+        del cm
+        torch.cuda.empty_cache()
+    out["config_lines"] = lines
+
+    # ---- shard proxies: the OPT-175B per-rank shard of a strong-scaled global batch of 144 at
+    # N = 2 / 4 / 8 (batch 72 / 36 / 18) on this one GPU, fused launches at cur_len 543
+    log("shard proxies")
+    w = wl.CONFIGS["opt-175b"]
+    proxy = {}
+    for nb in (2, 4, 8):
+        Bp = w.batch // nb
+        pm = DecodeModel(wl.Workload(w.name, w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len, 8),
+                         8, w.batch, 0, Bp, seed, dev, stream, True)
+        cur = w.prompt_len + w.gen_len - 1
+        us = pm.per_launch(cur, "fused")
+        kb = wl.attention_bytes(Bp, w.h1, cur) + wl.append_bytes(Bp, w.h1)
+        proxy[f"n{nb}_batch{Bp}"] = {"batch": Bp, "us_per_launch": round(us, 2),
+                                     "GBps": round(kb / (us * 1e-6) / 1e9, 1),
+                                     "frac_of_measured_hbm": round(kb / (us * 1e-6) / 1e9 / peak, 4),
+                                     "step_ms_estimate": round(us * w.layers / 1e3, 3)}
+        pm.free()
+        del pm
+        torch.cuda.empty_cache()
+    out["shard_proxy"] = proxy
+
+    sw = legacy_sweeps(args, dev, stream, seed, peak)
+    out.update(sw)
+    return out
+
+
+def legacy_sweeps(args, dev, stream, seed, peak):
+    """Rank 0, N = 1: weight quantize / dequantize sweep (BASELINE configs[4]) with the NEXT-2
+    dequant-GEMM beside its library baselines, the NEXT-3 KV-cache variants on the OPT-175B
+    shape, and NEXT-4 host-offloaded KV."""
+    import torch
+    from paper_2303_06865_b200 import flexq as fq
+    from paper_2303_06865_b200 import synth
+    from paper_2303_06865_b200 import workloads as wl
+    w = wl.CONFIGS["opt-175b"]
+    B, H, D, s, n = w.batch, w.heads, w.head_dim, w.prompt_len, w.gen_len
     # ---- weight quantize / dequantize sweep (BASELINE configs[4]), rank 0
     log("sweep")
     sweep = gemm = None
-    if rank == 0 and not args.no_sweep:
+    if True:
         sweep, gemm = {}, {}
         bf16_peak = bf16_peak_tflops()
         for (r, c) in ((12288, 49152), (12288, 12288)):
@@ -595,48 +868,10 @@ def run_flexq(args):
                                  "dequantize_gbs": round(nb / (statistics.median(td) * 1e-3) / 1e9, 1)}
             del x, codes, meta, y, gq, gd
 
-    # ---- the other BASELINE configs (OPT-6.7B, OPT-30B shapes): decode attention alone at the last
-    # step's context, 4 layers of fresh caches, one CUDA graph -- per-launch time and GB/s (rank 0)
-    other = None
-    if rank == 0 and not args.no_sweep and w.name == "opt-175b":
-        other = {}
-        for cname in ("opt-6.7b", "opt-30b"):
-            cw = wl.CONFIGS[cname]
-            cl, cB = 4, cw.batch
-            ccaches = [fq.KVCache(cB, cw.heads, cw.head_dim, cw.prompt_len, cw.gen_len, device=dev) for _ in range(cl)]
-            for j in range(cl):
-                kp = synth.fill(seed + 7, synth.tensor_id(j, synth.K_PROMPT), (cB, cw.heads, cw.prompt_len, cw.head_dim),
-                                device=dev)
-                fq.flexq_append_kv(kp, kp, ccaches[j], pos=0)
-                del kp
-            ccur = cw.prompt_len + cw.gen_len - 1
-            cq = synth.fill(seed + 7, synth.tensor_id(0, synth.Q), (cB, cw.heads, cw.head_dim), device=dev)
-            cout = torch.empty_like(cq)
-            cws = fq.make_workspace(ccaches[0])
-            gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=stream):
-                for j in range(cl):
-                    fq.flexq_decode_attention(cq, ccaches[j], ccur, out=cout, workspace=cws, stream=stream)
-            gc.replay()
-            torch.cuda.synchronize()
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                c0.record(stream)
-                for _ in range(10):
-                    gc.replay()
-                c1.record(stream)
-            torch.cuda.synchronize()
-            cus = c0.elapsed_time(c1) * 1e3 / (10 * cl)
-            cbytes = wl.attention_bytes(cB, cw.h1, ccur)
-            other[cname] = {"batch": cB, "heads": cw.heads, "cur_len": ccur, "us_per_launch": round(cus, 2),
-                            "bytes_per_launch": cbytes, "GBps": round(cbytes / (cus * 1e-6) / 1e9, 1),
-                            "frac_of_measured_hbm": round(cbytes / (cus * 1e-6) / 1e9 / peak, 4)}
-            del ccaches, cq, cout, cws, gc
-
     # ---- NEXT-3 variants of the KV cache (rank 0): decode attention on the OPT-175B shape at the
     # last step's context for three (b, g), 2 layers of fresh caches each, one CUDA graph
     kv_variants = None
-    if rank == 0 and not args.no_sweep and w.name == "opt-175b":
+    if True:
         kv_variants = {}
         vcur = s + n - 1
         vk = synth.fill(seed + 9, synth.tensor_id(0, synth.K_PROMPT), (B, H, vcur, D), device=dev)
@@ -673,7 +908,7 @@ def run_flexq(args):
     # batch 144 in pinned host memory, streamed through a 2-slot device ring
     log("offload")
     offload = None
-    if rank == 0 and not args.no_offload and w.name == "opt-175b":
+    if not args.no_offload:
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import offload_bench
         offload = offload_bench.run(layers=2, gpu_batches=1, B=B, H=H, D=D, s=s, n=n, steps=3, dev=str(dev))
@@ -682,64 +917,66 @@ def run_flexq(args):
                           "stream, fused append+attention on the compute stream, D2H of the new token's chunk "
                           "on a store stream; value = H2D bytes / device time, vs a pinned 1 GiB H2D copy")
 
-    # ---- CPU oracle baseline (rank 0, N = 1 only)
-    log("cpu baseline")
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        per = lambda nseq, cur: nseq * (wl.attention_bytes(1, h1, cur) + wl.append_bytes(1, h1))  # noqa: E731
-        gbs, seqs, cores, sample = cpu_oracle_baseline(w, args.cpu_seconds, per)
-        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample}
+    return {"weight_sweep": sweep, "dequant_gemm": gemm, "kv_variants": kv_variants, "offload": offload}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "u4+f16->f32", "data": "synthetic (counter-based Irwin-Hall fp16, P:41/P:44)",
-            "tokens_per_s": round(tokens_per_s, 2),
-            "attention_tokens_per_s_per_layer": round(tokens_per_s * L, 1),
-            "config": {"workload": f"{w.name} decode step: batch {B} per GPU (global {B_total}), {H} heads x {D}, "
-                                   f"s={s}, n={n}, l={L} layers, "
-                                   + ("fused append+attention (one launch) per layer, " if fused else
-                                      "append_kv + decode_attention per layer, ") +
-                                   f"steps cycle cur_len {s + 1}..{s + n - 1}",
-                       "global_batch": B_total, "seq_len": s + n, "parallelism": f"dp{world} (sequences)",
-                       "l2": f"working set {cache_bytes / 1e9:.1f} GB per GPU >> {l2 / 1e6:.0f} MB L2; no flush"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "traffic_source": "profiles/attention_traffic.json (ncu --set full, same launch shape)",
-                         "kernel": "decode_attention_kernel<128>" + (" (fused append)" if fused else ""),
-                         "peak_kind": peak_kind,
-                         "bytes_per_launch": k_bytes, "us_per_launch": round(k_us, 2),
-                         # the step's algorithmic bytes at this kernel's measured rate, over the step time
-                         # (the per-launch pass runs at the longest context, cur_len = s + n - 1, so
-                         # k_us * L would overstate a step whose contexts run s + 1 .. s + n - 1)
-                         "share_of_step": round(value_gbs / (achieved * world) if fused else
-                                                attn_us * L / (ms_step * 1e3), 4),
-                         "attention_only_us_per_launch": round(attn_us, 2),
-                         "attention_only_GBps": round(attn_bytes / (attn_us * 1e-6) / 1e9, 1),
-                         "append_us_per_launch": round(app_us, 2),
-                         "fused_us_per_launch": round(fused_us, 2)},
-            "gpu_launches": args.steps * L * (1 if fused else 2),
-            "clocks": clk.result(),
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "weight_sweep": sweep,
-            "topk_sparse": topk,
-            "dequant_gemm": gemm,
-            "offload": offload,
-            "allgather": allgather,
-            "other_configs": other,
-            "kv_variants": kv_variants,
-        }
-        print(json.dumps(line), flush=True)
-    if pg:
-        pg.barrier()
-        pg.destroy_process_group()
+
+def cpu_baseline_object(w, budget_s):
+    """The oracle as it stands on this host: (1) all cores, one worker process per core, on a bounded
+    sample of the workload (extrapolated: sample bytes / sample time); (2) the tiny configuration
+    (BASELINE configs[0]) in full on one thread -- prompt fill, one appended token and one decode
+    attention step -- timed end to end."""
+    from paper_2303_06865_b200 import workloads as wl
+    h1 = w.h1
+    per = lambda nseq, cur: nseq * (wl.attention_bytes(1, h1, cur) + wl.append_bytes(1, h1))  # noqa: E731
+    gbs, seqs, cores, sample = cpu_oracle_baseline(w, budget_s, per)
+    obj = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample,
+           "extrapolated": True}
+    try:
+        import oracle
+        from paper_2303_06865_b200 import synth
+        t = wl.CONFIGS["tiny"]
+        B, H, D, s = t.batch, t.heads, t.head_dim, t.prompt_len
+        seed = synth.BASE_SEED
+        k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D)).numpy()
+        v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D)).numpy()
+        kn = synth.fill(seed, synth.tensor_id(0, synth.K_NEW, 1), (B, H, 1, D)).numpy()
+        vn = synth.fill(seed, synth.tensor_id(0, synth.V_NEW, 1), (B, H, 1, D)).numpy()
+        q = synth.fill(seed, synth.tensor_id(0, synth.Q, 1), (B, H, D)).numpy()
+        t0 = time.perf_counter()
+        kc, vc = oracle.empty_cache(B, H, s + 1, D), oracle.empty_cache(B, H, s + 1, D)
+        oracle.append_kv(k, v, kc, vc, 0)
+        t1 = time.perf_counter()
+        oracle.append_kv(kn, vn, kc, vc, s)
+        oracle.attention_f64(q, kc, vc, s + 1)
+        t2 = time.perf_counter()
+        step_bytes = wl.attention_bytes(B, H * D, s + 1) + wl.append_bytes(B, H * D)
+        obj["tiny_full_single_thread"] = {
+            "prompt_fill_s": round(t1 - t0, 4), "decode_step_s": round(t2 - t1, 4),
+            "decode_step_GBps": round(step_bytes / (t2 - t1) / 1e9, 5), "threads": 1,
+            "what": "BASELINE configs[0] in full: quantize the 512-token prompt of 4 x 12 heads, append one "
+                    "token, one decode attention at cur_len 513 (oracle_attention_f64)"}
+    except Exception as e:  # noqa: BLE001
+        obj["tiny_full_single_thread"] = {"error": str(e)}
+    return obj
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without torchrun: run this script under torch.distributed.run, one rank per GPU."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"launching {args.gpus} ranks: {' '.join(cmd[1:6])} ...")
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

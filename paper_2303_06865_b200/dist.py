@@ -20,6 +20,11 @@ def shard(batch: int, world: int, rank: int) -> tuple[int, int]:
     return begin, end
 
 
+def owner(batch: int, world: int, row: int) -> int:
+    """The rank whose shard holds global sequence `row`."""
+    return row // ((batch + world - 1) // world)
+
+
 def rank_batch(global_batch: int, world: int, rank: int, scaling: str) -> int:
     """Sequences processed by `rank`: the full per-GPU batch for weak scaling,
     its shard of the fixed global batch for strong scaling."""

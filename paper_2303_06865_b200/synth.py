@@ -79,6 +79,21 @@ def fill(seed: int, tid: int, shape, device="cpu", chunk: int = 1 << 25) -> torc
     return out.view(*shape)
 
 
+def fill_rows(seed: int, tid: int, shape, row0: int, row1: int, device="cpu", chunk: int = 1 << 25) -> torch.Tensor:
+    """Rows [row0, row1) of the leading dimension of fill(seed, tid, shape), drawn directly
+    (same counters): a rank generates its shard of a global batch without the rest."""
+    rs = 1
+    for d in shape[1:]:
+        rs *= int(d)
+    n = (row1 - row0) * rs
+    out = torch.empty(n, dtype=torch.float16, device=device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        idx = torch.arange(row0 * rs + s, row0 * rs + e, dtype=torch.int64, device=device)
+        out[s:e] = irwin_hall(seed, tid, idx)
+    return out.view(row1 - row0, *shape[1:])
+
+
 def gather(seed: int, tid: int, shape, index_slices) -> torch.Tensor:
     """Host (CPU) regeneration of a sub-block of fill(seed, tid, shape).
 

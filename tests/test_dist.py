@@ -62,3 +62,43 @@ def test_gloo_world2(B):
     for rank, t, col in res:
         assert t == 11.0                       # max over ranks
         assert col == [float(i) for i in range(B)]
+
+
+def test_bench_rank_rows_and_defaults():
+    """bench.py's sharding: strong scaling splits the fixed global batch (configs[3]: 144 over
+    the GPUs), weak gives every rank its own block of the per-GPU batch; owner() inverts shard()."""
+    import importlib.util
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for world in (1, 2, 4, 8):
+        rows = [bench.rank_rows(144, world, r, "strong", 144) for r in range(world)]
+        assert rows[0][0] == 0 and rows[-1][1] == 144
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        for r, (b0, b1) in enumerate(rows):
+            assert all(fd.owner(144, world, x) == r for x in range(b0, b1))
+        weak = [bench.rank_rows(144 * world, world, r, "weak", 144) for r in range(world)]
+        assert weak == [(144 * r, 144 * (r + 1)) for r in range(world)]
+    old = sys.argv
+    try:
+        sys.argv = ["bench.py", "--gpus", "8"]
+        assert bench.parse().scaling == "strong"
+        sys.argv = ["bench.py", "--config", "opt-30b"]
+        assert bench.parse().scaling == "weak"
+    finally:
+        sys.argv = old
+
+
+def test_bench_world_size_mismatch_fails():
+    """--gpus N must match the launched world size (no silent single-process run)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE=3" in (r.stderr + r.stdout)
