@@ -21,7 +21,9 @@
  *    the caller's next synchronization.
  *  - Inputs must be finite; NaN / Inf inputs give unspecified codes.
  *  - fp16 = IEEE binary16 (`half`); half2 meta = {.x = scale, .y = min}.
- *  - The library keeps no mutable global state: calls are reentrant.
+ *  - The library keeps no mutable global state beyond per-device launch facts (SM count,
+ *    kernel occupancy, the shared-memory attribute), computed once per device under a lock:
+ *    calls are reentrant and may target several devices.
  */
 #ifndef FLEXQ_H
 #define FLEXQ_H
@@ -125,9 +127,34 @@ flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
                              int pos, int n_new, int bits, int group_size,
                              void *k_cache, void *v_cache, void *stream);
 
+/* Conversion between the plain quantized KV layout and the cache layout above.  The paper
+ * keeps the KV cache "in the quantized format" without fixing a layout; the plain one
+ * is flexq_quantize's output for the token rows of each head, four arrays per layer:
+ *     k_codes_u8, v_codes_u8  u8    [batch][heads][plain_tokens][head_dim*bits/8]
+ *                             (each token row a little-endian bit stream; bits = 4:
+ *                              column 2i in the low nibble of byte i)
+ *     k_meta_h2, v_meta_h2    half2 [batch][heads][plain_tokens][head_dim/group_size]
+ *                             {scale, min} (groups along head_dim)
+ * flexq_kv_import copies tokens [t0, t0 + n_tok) of the plain arrays into the same positions
+ * of k_cache / v_cache and touches no other cache byte; flexq_kv_export copies those tokens of
+ * the caches into the plain arrays and touches nothing else there.  Bytes are moved, never
+ * recomputed: import of flexq_quantize's rows gives exactly flexq_append_kv's cache bytes.
+ * Requires 0 <= t0, t0 + n_tok <= min(plain_tokens, prompt_len + gen_len) (else
+ * FLEXQ_ERR_ARG); n_tok == 0 is a no-op.  Same (bits, group_size, head_dim) support as the
+ * cache; every pointer 16-byte aligned. */
+flexq_status flexq_kv_import(const void *k_codes_u8, const void *k_meta_h2, const void *v_codes_u8,
+                             const void *v_meta_h2, int batch, int heads, int head_dim, int prompt_len,
+                             int gen_len, int plain_tokens, int t0, int n_tok, int bits, int group_size,
+                             void *k_cache, void *v_cache, void *stream);
+flexq_status flexq_kv_export(const void *k_cache, const void *v_cache, int batch, int heads, int head_dim,
+                             int prompt_len, int gen_len, int plain_tokens, int t0, int n_tok, int bits,
+                             int group_size, void *k_codes_u8, void *k_meta_h2, void *v_codes_u8,
+                             void *v_meta_h2, void *stream);
+
 /* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
- * arguments).  Layout (b = 4, g = 64): 256 B of scheduler counters, 4 B per (batch, head) of
- * split tickets, then split-K partials; variants: 256 B (unused), then (D + 2) floats per
+ * arguments).  Layout (b = 4, g = 64): 256 B of scheduler counters (the item ticket), 4 B per
+ * (batch, head) of merge tickets, then per (batch, head) 32 slots of split-K partials (D
+ * floats each) and 32 (m, l) float pairs; variants: 256 B (unused), then (D + 2) floats per
  * (batch, head, 128-token tile) of split-K partials.  The workspace must be zero-filled
  * ONCE after allocation; every call restores the counters and tickets to
  * zero before it completes (the partials are scratch), so one buffer serves
@@ -142,8 +169,9 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
  * M); q fp16 [batch][heads][head_dim].  Cache layout as above; tokens at
  * positions >= cur_len do not influence the result (the kernel may stream the
  * rest of the last 32-token chunk into shared memory and discard it).  Accuracy: |out - exact| <=
- * max(2e-3, 1e-2 |exact|) per element (reading Q).  (4, 64) runs the tensor-core kernel; the
- * variants a CUDA-core split-K kernel (+ a combine launch when a head is split). */
+ * max(2e-3, 1e-2 |exact|) per element (reading Q).  (4, 64) runs the tensor-core kernel
+ * (cur_len <= 17408, else FLEXQ_ERR_UNSUPPORTED); the variants a CUDA-core split-K kernel
+ * (+ a combine launch when a head is split). */
 flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, const void *v_cache,
                                     int batch, int heads, int head_dim, int prompt_len, int gen_len,
                                     int cur_len, int bits, int group_size, void *out_f16,

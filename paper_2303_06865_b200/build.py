@@ -30,6 +30,8 @@ SOURCES = {
     "decode_attention_topk.cu": [],
     "decode_attention_variants.cu": [],
     "dequant_gemm.cu": [],
+    "kv_interop.cu": [],
+    "device_info.cu": [],
 }
 
 

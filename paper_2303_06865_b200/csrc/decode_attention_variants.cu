@@ -28,6 +28,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "flexq_internal.h"
 
 namespace flexq {
@@ -401,16 +403,7 @@ attention_variant_combine(const float* __restrict__ part, __half* __restrict__ o
     out[bh * D + d] = __float2half_rn(num / den);
 }
 
-int sm_count() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+int sm_count() { return device_sm_count(); }
 
 template <int B, int G, int D>
 cudaError_t launch_var(const AttnArgs& a, cudaStream_t stream) {

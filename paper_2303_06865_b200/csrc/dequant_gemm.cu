@@ -33,6 +33,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <mutex>
 #include <stdlib.h>
 
 #include "flexq_internal.h"
@@ -817,13 +819,14 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
 
 EncodeTiled encode_fn() {
     static EncodeTiled fn = nullptr;
-    if (!fn) {
+    static std::once_flag once;
+    std::call_once(once, [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = reinterpret_cast<EncodeTiled>(f);
-    }
+    });
     return fn;
 }
 
@@ -840,16 +843,7 @@ bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
                promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int sm_count() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+int sm_count() { return device_sm_count(); }
 
 inline int mpad_of(int64_t m) {
     const int64_t r = m < kGemmMaxRows ? m : kGemmMaxRows;
@@ -911,15 +905,19 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
     const size_t tick_bytes = size_t((N / kBN * 4 + 255) / 256 * 256);
     uint32_t* tickets = static_cast<uint32_t*>(workspace);
     float* partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + tick_bytes);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(dequant_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(dequant_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemLimit);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
+    {   // the shared-memory attribute, once per device (under a lock)
+        static cudaError_t attr_err[kMaxDevices];
+        static std::once_flag attr_once[kMaxDevices];
+        const int dev = current_device();
+        std::call_once(attr_once[dev], [dev] {
+            cudaError_t e = cudaFuncSetAttribute(dequant_gemm_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(dequant_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemLimit);
+            attr_err[dev] = e;
+        });
+        if (attr_err[dev] != cudaSuccess) return attr_err[dev];
     }
     for (int64_t m0 = 0; m0 < M; m0 += kGemmMaxRows) {
         const int mrows = int(M - m0 < kGemmMaxRows ? M - m0 : kGemmMaxRows);

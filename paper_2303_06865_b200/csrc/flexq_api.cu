@@ -149,6 +149,7 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, cons
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap};
     if (is_variant(bits, group_size))
         return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
+    if (cur_len > flexq::kDenseMaxTokens) return FLEXQ_ERR_UNSUPPORTED;
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
@@ -179,6 +180,7 @@ flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_
         a.k_new = a.v_new = nullptr;
         return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
     }
+    if (cur_len > flexq::kDenseMaxTokens) return FLEXQ_ERR_UNSUPPORTED;
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
@@ -203,6 +205,44 @@ flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache,
     flexq::TopkArgs a{q_f16, k_cache, v_cache, out_f16, sel_i32, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, keep};
     return from_cuda(flexq::launch_decode_attention_topk(a, static_cast<cudaStream_t>(stream)));
+}
+
+static flexq_status kv_interop(bool import_, void* k_codes, void* k_meta, void* v_codes, void* v_meta, int batch,
+                               int heads, int head_dim, int prompt_len, int gen_len, int plain_tokens, int t0,
+                               int n_tok, int bits, int group_size, void* k_cache, void* v_cache, void* stream) {
+    flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
+    if (s == FLEXQ_ERR_ARG) return s;
+    const int64_t t_cap = int64_t(prompt_len) + gen_len;
+    if (plain_tokens < 1 || t0 < 0 || n_tok < 0 || int64_t(t0) + n_tok > t_cap || t0 + n_tok > plain_tokens)
+        return FLEXQ_ERR_ARG;
+    if (s != FLEXQ_OK) return s;
+    if (n_tok == 0) return FLEXQ_OK;
+    if (!k_codes || !k_meta || !v_codes || !v_meta || !k_cache || !v_cache) return FLEXQ_ERR_NULL;
+    if (!aligned16(k_codes) || !aligned16(k_meta) || !aligned16(v_codes) || !aligned16(v_meta) ||
+        !aligned16(k_cache) || !aligned16(v_cache))
+        return FLEXQ_ERR_ALIGN;
+    flexq::KvInterop x{k_codes, k_meta, v_codes, v_meta, k_cache, v_cache, int64_t(batch) * heads,
+                       flexq::kv_token_stride(t_cap) / flexq::kChunk, plain_tokens, t0, n_tok, head_dim, bits,
+                       group_size};
+    return from_cuda(flexq::launch_kv_interop(import_, x, static_cast<cudaStream_t>(stream)));
+}
+
+flexq_status flexq_kv_import(const void* k_codes_u8, const void* k_meta_h2, const void* v_codes_u8,
+                             const void* v_meta_h2, int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                             int plain_tokens, int t0, int n_tok, int bits, int group_size, void* k_cache,
+                             void* v_cache, void* stream) {
+    return kv_interop(true, const_cast<void*>(k_codes_u8), const_cast<void*>(k_meta_h2), const_cast<void*>(v_codes_u8),
+                      const_cast<void*>(v_meta_h2), batch, heads, head_dim, prompt_len, gen_len, plain_tokens, t0,
+                      n_tok, bits, group_size, k_cache, v_cache, stream);
+}
+
+flexq_status flexq_kv_export(const void* k_cache, const void* v_cache, int batch, int heads, int head_dim,
+                             int prompt_len, int gen_len, int plain_tokens, int t0, int n_tok, int bits,
+                             int group_size, void* k_codes_u8, void* k_meta_h2, void* v_codes_u8, void* v_meta_h2,
+                             void* stream) {
+    return kv_interop(false, k_codes_u8, k_meta_h2, v_codes_u8, v_meta_h2, batch, heads, head_dim, prompt_len,
+                      gen_len, plain_tokens, t0, n_tok, bits, group_size, const_cast<void*>(k_cache),
+                      const_cast<void*>(v_cache), stream);
 }
 
 // Shared checks for the decode linear layer's weight shape (NEXT-2).

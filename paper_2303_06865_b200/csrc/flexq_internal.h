@@ -6,6 +6,11 @@
 
 namespace flexq {
 
+// Per-device launch facts (device_info.cu), computed once per device under a lock.
+constexpr int kMaxDevices = 64;
+int current_device();
+int device_sm_count();
+
 // Fixed by the paper's configuration: 4-bit codes, groups of 64.
 constexpr int kBits = 4;
 constexpr int kGroup = 64;
@@ -38,6 +43,20 @@ cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int hea
 cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols, int bits, int group,
                               void* out, cudaStream_t stream);
 
+// Plain quantized KV layout <-> chunked cache (kv_interop.cu): byte moves only.
+struct KvInterop {
+    void* k_codes;        // plain u8 [rows][plain_tokens][D*bits/8]
+    void* k_meta;         // plain half2 [rows][plain_tokens][D/group]
+    void* v_codes;
+    void* v_meta;
+    void* k_cache;        // chunked caches (include/flexq.h)
+    void* v_cache;
+    int64_t rows;         // batch * heads
+    int64_t chunks;       // chunks per (b, h)
+    int plain_tokens, t0, n, head_dim, bits, group;
+};
+cudaError_t launch_kv_interop(bool import_, const KvInterop& x, cudaStream_t stream);
+
 struct AttnArgs {
     const void* q;
     const void* k_cache;
@@ -50,6 +69,8 @@ struct AttnArgs {
 };
 
 size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
+// Longest context of the (4, 64) tensor-core kernel: 16 pieces of its 1088-token score buffer.
+constexpr int kDenseMaxTokens = 16 * 1088;
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
 
 // Decode attention over the (b, g) variant caches (NEXT-3; decode_attention_variants.cu):

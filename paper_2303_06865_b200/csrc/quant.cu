@@ -15,6 +15,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "flexq_internal.h"
 
 namespace flexq {
@@ -476,16 +478,7 @@ dequantize_generic_kernel(const uint8_t* __restrict__ codes, const __half2* __re
     }
 }
 
-int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
+int num_sms() { return device_sm_count(); }
 
 }  // namespace
 

@@ -59,9 +59,11 @@ def lib():
         L.flexq_gemm_panel_bytes.argtypes = [I64, I64, I, I]
         L.flexq_gemm_panel_bytes.restype = SZ
         L.flexq_pack_weight.argtypes = [P, P, I64, I64, I, I, P, P]
+        L.flexq_kv_import.argtypes = [P] * 4 + [I] * 10 + [P, P, P]
+        L.flexq_kv_export.argtypes = [P, P] + [I] * 10 + [P] * 5
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
                   "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention",
-                  "flexq_dequant_gemm", "flexq_pack_weight"):
+                  "flexq_dequant_gemm", "flexq_pack_weight", "flexq_kv_import", "flexq_kv_export"):
             getattr(L, f).restype = I
         if hasattr(L, "flexq_debug_attn_trace"):   # tuning build only
             L.flexq_debug_attn_trace.argtypes = [P, I]
@@ -85,15 +87,23 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def _stream(stream) -> int:
+def _stream(stream, device=None) -> int:
+    """The cudaStream_t to pass: the given stream, else torch's current stream of `device`
+    (the tensors' device, not necessarily the current one)."""
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _need(t: torch.Tensor, dtype, name: str):
-    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+def _need(t: torch.Tensor, dtype, name: str, shape=None, device=None):
+    """A contiguous CUDA tensor of `dtype` (and `shape` / on `device` when given); the C ABI
+    takes raw pointers, so a mismatch must be caught here, not as an illegal address."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous CUDA {dtype} tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
 
 
 # ---------------------------------------------------------------- quantizer
@@ -107,19 +117,27 @@ def flexq_quantize(x: torch.Tensor, codes=None, meta=None, bits: int = BITS, gro
         codes = torch.empty(rows, cols * bits // 8, dtype=torch.uint8, device=x.device)
     if meta is None:
         meta = torch.empty(rows, cols // group_size, 2, dtype=torch.float16, device=x.device)
-    _check(lib().flexq_quantize(x.data_ptr(), rows, cols, bits, group_size, codes.data_ptr(),
-                                meta.data_ptr(), _stream(stream)), "flexq_quantize")
+    _need(codes, torch.uint8, "codes", (rows, cols * bits // 8), x.device)
+    _need(meta, torch.float16, "meta", (rows, cols // group_size, 2), x.device)
+    with torch.cuda.device(x.device):
+        _check(lib().flexq_quantize(x.data_ptr(), rows, cols, bits, group_size, codes.data_ptr(),
+                                    meta.data_ptr(), _stream(stream, x.device)), "flexq_quantize")
     return codes, meta
 
 
 def flexq_dequantize(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: int = BITS,
                      group_size: int = GROUP, stream=None) -> torch.Tensor:
+    _need(codes, torch.uint8, "codes")
     rows, nbytes = codes.shape
     cols = nbytes * 8 // bits
+    dev = codes.device
+    _need(meta, torch.float16, "meta", (rows, cols // group_size, 2), dev)
     if out is None:
-        out = torch.empty(rows, cols, dtype=torch.float16, device=codes.device)
-    _check(lib().flexq_dequantize(codes.data_ptr(), meta.data_ptr(), rows, cols, bits, group_size,
-                                  out.data_ptr(), _stream(stream)), "flexq_dequantize")
+        out = torch.empty(rows, cols, dtype=torch.float16, device=dev)
+    _need(out, torch.float16, "out", (rows, cols), dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_dequantize(codes.data_ptr(), meta.data_ptr(), rows, cols, bits, group_size,
+                                      out.data_ptr(), _stream(stream, dev)), "flexq_dequantize")
     return out
 
 
@@ -197,6 +215,49 @@ class KVCache:
         return self._meta(self.v)
 
 
+def _plain_shapes(cache: "KVCache", plain_tokens: int):
+    B, H, D = cache.batch, cache.heads, cache.head_dim
+    return (B, H, plain_tokens, D * cache.bits // 8), (B, H, plain_tokens, D // cache.group_size, 2)
+
+
+def flexq_kv_import(cache: "KVCache", k_codes, k_meta, v_codes, v_meta, t0: int = 0, n_tok=None, stream=None):
+    """Plain quantized KV (flexq_quantize's rows per head: codes u8 [B][H][T][D*bits/8], meta fp16
+    [B][H][T][D/g][2]) -> cache tokens [t0, t0 + n_tok) (include/flexq.h)."""
+    T = k_codes.shape[2]
+    n_tok = T - t0 if n_tok is None else n_tok
+    cs, ms = _plain_shapes(cache, T)
+    for t, name, dt, shp in ((k_codes, "k_codes", torch.uint8, cs), (v_codes, "v_codes", torch.uint8, cs),
+                             (k_meta, "k_meta", torch.float16, ms), (v_meta, "v_meta", torch.float16, ms)):
+        _need(t, dt, name)
+        if tuple(t.shape) != shp:
+            raise ValueError(f"{name} must have shape {shp}, got {tuple(t.shape)}")
+    dev = cache.k.device
+    for t in (k_codes, k_meta, v_codes, v_meta):
+        if t.device != dev:
+            raise ValueError(f"plain arrays must be on {dev}")
+    with torch.cuda.device(dev):
+        _check(lib().flexq_kv_import(_ptr(k_codes), _ptr(k_meta), _ptr(v_codes), _ptr(v_meta), cache.batch, cache.heads,
+                                 cache.head_dim, cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits,
+                                     cache.group_size, _ptr(cache.k), _ptr(cache.v), _stream(stream, dev)),
+               "flexq_kv_import")
+
+
+def flexq_kv_export(cache: "KVCache", t0: int = 0, n_tok=None, plain_tokens=None, stream=None):
+    """Cache tokens [t0, t0 + n_tok) -> plain (k_codes, k_meta, v_codes, v_meta) arrays with
+    plain_tokens (default t0 + n_tok) token rows; rows outside the range are zero."""
+    n_tok = cache.t_cap - t0 if n_tok is None else n_tok
+    T = t0 + n_tok if plain_tokens is None else plain_tokens
+    cs, ms = _plain_shapes(cache, T)
+    dev = cache.k.device
+    kc, vc = torch.zeros(cs, dtype=torch.uint8, device=dev), torch.zeros(cs, dtype=torch.uint8, device=dev)
+    km, vm = torch.zeros(ms, dtype=torch.float16, device=dev), torch.zeros(ms, dtype=torch.float16, device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_kv_export(_ptr(cache.k), _ptr(cache.v), cache.batch, cache.heads, cache.head_dim,
+                                     cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits, cache.group_size,
+                                     _ptr(kc), _ptr(km), _ptr(vc), _ptr(vm), _stream(stream, dev)), "flexq_kv_export")
+    return kc, km, vc, vm
+
+
 def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS, group_size=GROUP):
     """-> (bytes of one cache buffer (K or V) of one layer, token stride)."""
     c, t = ctypes.c_size_t(), ctypes.c_int()
@@ -207,12 +268,18 @@ def flexq_kv_cache_bytes(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
 
 def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, pos: int, stream=None):
     """k_new, v_new fp16 [B][H][n_new][D] -> cache tokens [pos, pos + n_new)."""
-    _need(k_new, torch.float16, "k_new")
-    _need(v_new, torch.float16, "v_new")
+    dev = cache.k.device
+    _need(k_new, torch.float16, "k_new", device=dev)
+    if k_new.dim() != 4 or (k_new.shape[0], k_new.shape[1], k_new.shape[3]) != (cache.batch, cache.heads,
+                                                                                cache.head_dim):
+        raise ValueError(f"k_new must be [B={cache.batch}][H={cache.heads}][n_new][D={cache.head_dim}], "
+                         f"got {tuple(k_new.shape)}")
+    _need(v_new, torch.float16, "v_new", k_new.shape, dev)
     B, H, n_new, D = k_new.shape
-    _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
-                                 cache.gen_len, pos, n_new, cache.bits, cache.group_size,
-                                 cache.k.data_ptr(), cache.v.data_ptr(), _stream(stream)), "flexq_append_kv")
+    with torch.cuda.device(dev):
+        _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
+                                     cache.gen_len, pos, n_new, cache.bits, cache.group_size,
+                                     cache.k.data_ptr(), cache.v.data_ptr(), _stream(stream, dev)), "flexq_append_kv")
 
 
 def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
@@ -230,17 +297,20 @@ def make_workspace(cache: KVCache) -> torch.Tensor:
 def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=None, workspace=None,
                            stream=None) -> torch.Tensor:
     """q fp16 [B][H][D] -> out fp16 [B][H][D] over cache tokens [0, cur_len)."""
-    _need(q, torch.float16, "q")
+    dev, shp = cache.k.device, (cache.batch, cache.heads, cache.head_dim)
+    _need(q, torch.float16, "q", shp, dev)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = make_workspace(cache)
-    _check(lib().flexq_decode_attention(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
-                                        cache.heads,
-                                        cache.head_dim, cache.prompt_len, cache.gen_len,
-                                        cur_len, cache.bits, cache.group_size, out.data_ptr(),
-                                        workspace.data_ptr(), workspace.numel(), _stream(stream)),
-           "flexq_decode_attention")
+    _need(out, torch.float16, "out", shp, dev)
+    _need(workspace, torch.uint8, "workspace", device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_decode_attention(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
+                                            cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
+                                            cur_len, cache.bits, cache.group_size, out.data_ptr(),
+                                            workspace.data_ptr(), workspace.numel(), _stream(stream, dev)),
+               "flexq_decode_attention")
     return out
 
 
@@ -249,21 +319,25 @@ def flexq_append_decode_attention(q: torch.Tensor, k_new: torch.Tensor, v_new: t
     """One layer's decode step in one launch (NEXT-3): append k_new / v_new fp16 [B][H][D] (or
     [B][H][1][D]) at position cur_len - 1, then attend over [0, cur_len).  Same cache bytes as
     flexq_append_kv, same output bound as flexq_decode_attention."""
-    _need(q, torch.float16, "q")
-    _need(k_new, torch.float16, "k_new")
-    _need(v_new, torch.float16, "v_new")
+    dev, shp = cache.k.device, (cache.batch, cache.heads, cache.head_dim)
+    _need(q, torch.float16, "q", shp, dev)
+    _need(k_new, torch.float16, "k_new", device=dev)
+    _need(v_new, torch.float16, "v_new", device=dev)
     if k_new.numel() != q.numel() or v_new.numel() != q.numel():
         raise ValueError("k_new / v_new must hold one token per (batch, head): [B][H][D]")
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = make_workspace(cache)
-    _check(lib().flexq_append_decode_attention(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), cache.k.data_ptr(),
-                                               cache.v.data_ptr(), cache.batch, cache.heads, cache.head_dim,
-                                               cache.prompt_len, cache.gen_len, cur_len, cache.bits,
-                                               cache.group_size, out.data_ptr(), workspace.data_ptr(),
-                                               workspace.numel(), _stream(stream)),
-           "flexq_append_decode_attention")
+    _need(out, torch.float16, "out", shp, dev)
+    _need(workspace, torch.uint8, "workspace", device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_append_decode_attention(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                                                   cache.k.data_ptr(), cache.v.data_ptr(), cache.batch, cache.heads,
+                                                   cache.head_dim, cache.prompt_len, cache.gen_len, cur_len,
+                                                   cache.bits, cache.group_size, out.data_ptr(),
+                                                   workspace.data_ptr(), workspace.numel(), _stream(stream, dev)),
+               "flexq_append_decode_attention")
     return out
 
 
@@ -277,16 +351,23 @@ def flexq_decode_attention_topk(q: torch.Tensor, cache: KVCache, cur_len: int, k
                                 workspace=None, stream=None) -> torch.Tensor:
     """Top-K sparse decode attention.  sel: optional int32 [B][H][keep] output
     receiving the kept token indices (ascending)."""
-    _need(q, torch.float16, "q")
+    dev, shp = cache.k.device, (cache.batch, cache.heads, cache.head_dim)
+    _need(q, torch.float16, "q", shp, dev)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = make_workspace(cache)
-    _check(lib().flexq_decode_attention_topk(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
-                                             cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
-                                             cur_len, keep, cache.bits, cache.group_size, out.data_ptr(),
-                                             _ptr(sel), workspace.data_ptr(), workspace.numel(), _stream(stream)),
-           "flexq_decode_attention_topk")
+    _need(out, torch.float16, "out", shp, dev)
+    _need(workspace, torch.uint8, "workspace", device=dev)
+    if sel is not None:
+        _need(sel, torch.int32, "sel", (cache.batch, cache.heads, keep), dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_decode_attention_topk(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
+                                                 cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
+                                                 cur_len, keep, cache.bits, cache.group_size, out.data_ptr(),
+                                                 _ptr(sel), workspace.data_ptr(), workspace.numel(),
+                                                 _stream(stream, dev)),
+               "flexq_decode_attention_topk")
     return out
 
 
@@ -299,13 +380,19 @@ def flexq_pack_weight(codes: torch.Tensor, meta: torch.Tensor, out=None, bits: i
                       stream=None) -> torch.Tensor:
     """One-time re-layout of a quantized [k][n] weight (codes u8 [k][n/2], meta [k][n/g][2])
     into the GEMM's panel format (u8, same total size)."""
+    _need(codes, torch.uint8, "codes")
     k, half_n = codes.shape
     n = half_n * 2
+    dev = codes.device
+    _need(meta, torch.float16, "meta", (k, n // group_size, 2), dev)
     if out is None:
-        out = torch.empty(max(flexq_gemm_panel_bytes(k, n, bits, group_size), 16), dtype=torch.uint8,
-                          device=codes.device)
-    _check(lib().flexq_pack_weight(codes.data_ptr(), meta.data_ptr(), k, n, bits, group_size, out.data_ptr(),
-                                   _stream(stream)), "flexq_pack_weight")
+        out = torch.empty(max(flexq_gemm_panel_bytes(k, n, bits, group_size), 16), dtype=torch.uint8, device=dev)
+    _need(out, torch.uint8, "panels", device=dev)
+    if out.numel() < flexq_gemm_panel_bytes(k, n, bits, group_size):
+        raise ValueError("panels buffer smaller than flexq_gemm_panel_bytes(k, n)")
+    with torch.cuda.device(dev):
+        _check(lib().flexq_pack_weight(codes.data_ptr(), meta.data_ptr(), k, n, bits, group_size, out.data_ptr(),
+                                       _stream(stream, dev)), "flexq_pack_weight")
     return out
 
 
@@ -323,10 +410,18 @@ def flexq_dequant_gemm(x: torch.Tensor, panels: torch.Tensor, n: int, out=None, 
     """y fp16 [m][n] = x fp16 [m][k] . w^; panels = flexq_pack_weight(codes, meta)."""
     _need(x, torch.float16, "x")
     m, k = x.shape
+    dev = x.device
+    _need(panels, torch.uint8, "panels", device=dev)
+    if panels.numel() < flexq_gemm_panel_bytes(k, n, bits, group_size):
+        raise ValueError("panels smaller than flexq_gemm_panel_bytes(k, n): packed for another shape?")
     if out is None:
-        out = torch.empty(m, n, dtype=torch.float16, device=x.device)
+        out = torch.empty(m, n, dtype=torch.float16, device=dev)
     if workspace is None:
-        workspace = make_gemm_workspace(m, k, n, x.device)
-    _check(lib().flexq_dequant_gemm(x.data_ptr(), panels.data_ptr(), m, k, n, bits, group_size, out.data_ptr(),
-                                    workspace.data_ptr(), workspace.numel(), _stream(stream)), "flexq_dequant_gemm")
+        workspace = make_gemm_workspace(m, k, n, dev)
+    _need(out, torch.float16, "out", (m, n), dev)
+    _need(workspace, torch.uint8, "workspace", device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().flexq_dequant_gemm(x.data_ptr(), panels.data_ptr(), m, k, n, bits, group_size, out.data_ptr(),
+                                        workspace.data_ptr(), workspace.numel(), _stream(stream, dev)),
+               "flexq_dequant_gemm")
     return out

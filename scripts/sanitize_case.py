@@ -41,6 +41,9 @@ def main():
         # NEXT-1 Top-K and NEXT-3 fused append + attention on the same cache
         fq.flexq_decode_attention_topk(q, cache, s, keep=fq.topk_keep(s), workspace=ws)
         fq.flexq_append_decode_attention(q, q, q, cache, s + n, workspace=ws)
+        # interop: export the cache to the plain layout, import a token range back
+        kc, km, vc, vm = fq.flexq_kv_export(cache)
+        fq.flexq_kv_import(cache, kc, km, vc, vm, t0=min(5, s), n_tok=min(37, s + n - min(5, s)))
     # NEXT-3 quantizer variants
     for b, g in ((2, 32), (3, 128), (8, 64)):
         c, m = fq.flexq_quantize(x[:, :128].contiguous(), bits=b, group_size=g)

@@ -1,4 +1,6 @@
-"""compute-sanitizer memcheck / racecheck / synccheck over every kernel."""
+"""compute-sanitizer memcheck / racecheck / synccheck / initcheck over every kernel,
+under the default attention schedule and with every launch forced onto the dynamic
+whole-head ticket schedule (FLEXQ_ATTN_SPLIT=0,0,0)."""
 import os
 import shutil
 import subprocess
@@ -10,14 +12,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
-def test_compute_sanitizer(cuda, tool):
+@pytest.mark.parametrize("tool,sched", [("memcheck", "default"), ("racecheck", "default"), ("synccheck", "default"),
+                                        ("initcheck", "default"), ("memcheck", "dynamic"), ("racecheck", "dynamic")])
+def test_compute_sanitizer(cuda, tool, sched):
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not available")
+    env = dict(os.environ)
+    if sched == "dynamic":
+        env["FLEXQ_ATTN_SPLIT"] = "0,0,0"
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", "--kernel-name", "kns=flexq",
                         sys.executable, os.path.join(ROOT, "scripts", "sanitize_case.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "sanitize case ok" in out
