@@ -372,9 +372,10 @@ class DecodeModel:
                 elif which == "append":
                     fq.flexq_append_kv(self.kn[j].unsqueeze(2), self.vn[j].unsqueeze(2), self.caches[j],
                                        pos=cur - 1, stream=st)
-                elif which == "topk":
-                    fq.flexq_decode_attention_topk(self.qs[j], self.caches[j], cur, keep, out=self.outs[j],
-                                                   workspace=self.ws, stream=st)
+                elif which in ("topk", "topk_tm"):
+                    c = self.caches[j] if which == "topk" else self.tm_cache(j)
+                    fq.flexq_decode_attention_topk(self.qs[j], c, cur, keep, out=self.outs[j],
+                                                   workspace=self.topk_ws(), stream=st)
                 else:                   # fused: rewrites the same token at cur - 1 (idempotent)
                     fq.flexq_append_decode_attention(self.qs[j], self.kn[j], self.vn[j], self.caches[j], cur,
                                                      out=self.outs[j], workspace=self.ws, stream=st)
@@ -389,8 +390,28 @@ class DecodeModel:
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e3 / (reps * L)
 
+    def topk_ws(self):
+        if getattr(self, "tws", None) is None:
+            self.tws = self.fq.make_topk_workspace(self.caches[0])
+        return self.tws
+
+    def tm_cache(self, j):
+        """Layer j's cache in the token-major layout (Top-K's): the same bytes moved with
+        flexq_kv_export / flexq_kv_import (no requantization)."""
+        self.tm = getattr(self, "tm", {})
+        if j not in self.tm:
+            fq, c = self.fq, self.caches[j]
+            t = fq.KVCache(c.batch, c.heads, c.head_dim, c.prompt_len, c.gen_len, device=c.k.device,
+                           layout="token_major")
+            plain = fq.flexq_kv_export(c, stream=self.stream)
+            fq.flexq_kv_import(t, *plain, stream=self.stream)
+            del plain
+            self.tm[j] = t
+        return self.tm[j]
+
     def free(self):
         self.graphs.clear()
+        self.tm, self.tws = {}, None
         del self.caches, self.qs, self.kn, self.vn, self.outs, self.ws
 
 
@@ -531,13 +552,18 @@ def run_flexq(args):
     topk = None
     if cur_last <= 1152 and rank == 0:
         keep = fq.topk_keep(cur_last)
-        tk_us = m.per_launch(cur_last, "topk")
         kv_row = h1 // 2 + h1 // 64 * 4                      # one token's K (or V) bytes over all heads
         tk_bytes = B * (cur_last * kv_row + keep * kv_row + 2 * h1 * 2)
-        topk = {"keep": keep, "cur_len": cur_last, "us_per_launch": round(tk_us, 2),
+        tk_us = m.per_launch(cur_last, "topk_tm", layers=4)
+        tk_us_dense = m.per_launch(cur_last, "topk", layers=4)
+        attn4_us = m.per_launch(cur_last, "attn", layers=4)
+        topk = {"keep": keep, "cur_len": cur_last, "layout": "token_major", "us_per_launch": round(tk_us, 2),
                 "algorithmic_bytes_per_launch": tk_bytes, "GBps": round(tk_bytes / (tk_us * 1e-6) / 1e9, 1),
-                "speedup_vs_dense": round(attn_us / tk_us, 3),
-                "note": "bytes = K for all tokens + V for the kept 10% (P:856) + q + out"}
+                "frac_of_measured_hbm": round(tk_bytes / (tk_us * 1e-6) / 1e9 / peak, 4),
+                "speedup_vs_dense": round(attn4_us / tk_us, 3), "dense_attention_us_same_graph": round(attn4_us, 2),
+                "dense_layout_us_per_launch": round(tk_us_dense, 2),
+                "note": "bytes = K for all tokens + V for the kept 10% (P:856) + q + out; two launches (select, "
+                        "gather), graph of 4 layers; the dense layout gathers whole 4-token quad rows"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "attention_traffic.json")
     if os.path.exists(tp) and w.name == "opt-175b" and B == 144:

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FLEXQ_ABI_VERSION 1
+#define FLEXQ_ABI_VERSION 2   /* 2: the kv_layout argument of the KV-cache calls */
 
 typedef enum {
     FLEXQ_OK = 0,
@@ -56,6 +56,17 @@ typedef enum {
 
 /* = FLEXQ_ABI_VERSION. */
 int flexq_abi_version(void);
+
+/* KV cache layouts: the `kv_layout` argument of every call that reads or writes a KV cache
+ * (layouts below, at "KV cache layout").  Any other value -> FLEXQ_ERR_ARG.
+ *   FLEXQ_KV_DENSE        the default.  (4, 64): K token-major, V quad-interleaved and swizzled
+ *                         (the operand order of the tensor-core decode kernel); the variants:
+ *                         K and V token-major.
+ *   FLEXQ_KV_TOKEN_MAJOR  K and V token-major for every built (bits, group_size).  At (4, 64) it is
+ *                         the layout of Top-K sparse attention (one kept token = one contiguous
+ *                         V row); dense decode attention over it runs the CUDA-core kernel
+ *                         of the variants.  For the variants it equals FLEXQ_KV_DENSE. */
+typedef enum { FLEXQ_KV_DENSE = 0, FLEXQ_KV_TOKEN_MAJOR = 1 } flexq_kv_layout;
 
 /* Static, never-NULL description of a status code (unknown codes included). */
 const char *flexq_status_string(int status);
@@ -109,6 +120,8 @@ flexq_status flexq_dequantize(const void *codes_u8, const void *meta_h2, int64_t
  *     [codes 32 x CB][meta 32 x MB]
  * K and V alike token-major: token s's codes at s*CB as a little-endian bit stream (bit i of
  * column j is stream bit j*bits + i), its D/group_size half2 {scale, min} at 32*CB + s*MB.
+ * FLEXQ_KV_TOKEN_MAJOR at (4, 64) is this layout too (V laid out exactly like K); the buffer
+ * sizes do not depend on the layout.
  *
  * *cache_bytes (may be NULL) receives the size of ONE buffer (K or V),
  * *token_stride (may be NULL) T_stride.  Supported: head_dim in {64, 128}; (bits, group_size)
@@ -124,7 +137,7 @@ flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt
  * position. */
 flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
                              int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                             int pos, int n_new, int bits, int group_size,
+                             int pos, int n_new, int bits, int group_size, int kv_layout,
                              void *k_cache, void *v_cache, void *stream);
 
 /* Conversion between the plain quantized KV layout and the cache layout above.  The paper
@@ -145,14 +158,14 @@ flexq_status flexq_append_kv(const void *k_new_f16, const void *v_new_f16,
 flexq_status flexq_kv_import(const void *k_codes_u8, const void *k_meta_h2, const void *v_codes_u8,
                              const void *v_meta_h2, int batch, int heads, int head_dim, int prompt_len,
                              int gen_len, int plain_tokens, int t0, int n_tok, int bits, int group_size,
-                             void *k_cache, void *v_cache, void *stream);
+                             int kv_layout, void *k_cache, void *v_cache, void *stream);
 flexq_status flexq_kv_export(const void *k_cache, const void *v_cache, int batch, int heads, int head_dim,
                              int prompt_len, int gen_len, int plain_tokens, int t0, int n_tok, int bits,
-                             int group_size, void *k_codes_u8, void *k_meta_h2, void *v_codes_u8,
+                             int group_size, int kv_layout, void *k_codes_u8, void *k_meta_h2, void *v_codes_u8,
                              void *v_meta_h2, void *stream);
 
 /* Workspace bytes flexq_decode_attention needs for these dimensions (0 on bad
- * arguments).  Layout (b = 4, g = 64): 256 B of scheduler counters (the item ticket), 4 B per
+ * arguments).  Layout (b = 4, g = 64): 2 KB of scheduler counters (item tickets), 4 B per
  * (batch, head) of merge tickets, then per (batch, head) 32 slots of split-K partials (D
  * floats each) and 32 (m, l) float pairs; variants: 256 B (unused), then (D + 2) floats per
  * (batch, head, 128-token tile) of split-K partials.  The workspace must be zero-filled
@@ -160,7 +173,7 @@ flexq_status flexq_kv_export(const void *k_cache, const void *v_cache, int batch
  * zero before it completes (the partials are scratch), so one buffer serves
  * any number of stream-ordered calls (not concurrent ones). */
 size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
-                                             int gen_len, int bits, int group_size);
+                                             int gen_len, int bits, int group_size, int kv_layout);
 
 /* Decode-step attention over the compressed cache (reading K):
  *   out fp16 [batch][heads][head_dim] =
@@ -174,7 +187,7 @@ size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim,
  * (+ a combine launch when a head is split). */
 flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, const void *v_cache,
                                     int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                    int cur_len, int bits, int group_size, void *out_f16,
+                                    int cur_len, int bits, int group_size, int kv_layout, void *out_f16,
                                     void *workspace, size_t workspace_bytes, void *stream);
 
 /* One decode step of one layer in a single launch:
@@ -190,8 +203,16 @@ flexq_status flexq_decode_attention(const void *q_f16, const void *k_cache, cons
 flexq_status flexq_append_decode_attention(const void *q_f16, const void *k_new_f16, const void *v_new_f16,
                                            void *k_cache, void *v_cache, int batch, int heads,
                                            int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
-                                           int group_size, void *out_f16, void *workspace,
+                                           int group_size, int kv_layout, void *out_f16, void *workspace,
                                            size_t workspace_bytes, void *stream);
+
+/* Workspace bytes flexq_decode_attention_topk needs (0 on bad arguments or a configuration
+ * Top-K does not build): 2 KB of scheduler counters, then the kept lists -- an int32 token
+ * index and an fp32 weight per (batch, head, kept token), sized for keep <= prompt_len +
+ * gen_len (8 B per cached token position: 60 MB at OPT-175B's 144 x 96 heads x 544 tokens).
+ * Zero-filled once after allocation; every call leaves the counters zero again. */
+size_t flexq_decode_attention_topk_workspace_size(int batch, int heads, int head_dim, int prompt_len,
+                                                  int gen_len, int bits, int group_size, int kv_layout);
 
 /* Top-K sparse decode attention, FlexGen's "4-bit-S":
  * scores s_t = q . K^_t / sqrt(head_dim) for t in [0, cur_len); the `keep`
@@ -200,13 +221,16 @@ flexq_status flexq_append_decode_attention(const void *q_f16, const void *k_new_
  * renormalised over the kept set.  Only the kept V rows are read
  * (P:856).  The paper keeps the top 10%: keep = ceil(0.1 * cur_len).
  * sel_i32 (optional, may be NULL): int32 [batch][heads][keep] receives the
- * kept token indices in ascending order.  Workspace as for
- * flexq_decode_attention.  Supported: bits = 4, group_size = 64, cur_len <= 1152 (else
- * FLEXQ_ERR_UNSUPPORTED); 1 <= keep <= cur_len (else FLEXQ_ERR_ARG). */
+ * kept token indices in ascending order.  Workspace: >=
+ * flexq_decode_attention_topk_workspace_size(...) bytes.  Two launches (select, then gather
+ * of the kept V rows).  Both layouts are read; FLEXQ_KV_TOKEN_MAJOR makes a kept token one
+ * contiguous V row (the dense layout spreads it over its 4-token quad row).  Supported:
+ * bits = 4, group_size = 64, cur_len <= 1152 (else FLEXQ_ERR_UNSUPPORTED);
+ * 1 <= keep <= cur_len (else FLEXQ_ERR_ARG). */
 flexq_status flexq_decode_attention_topk(const void *q_f16, const void *k_cache, const void *v_cache,
                                          int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                         int cur_len, int keep, int bits, int group_size, void *out_f16,
-                                         void *sel_i32, void *workspace, size_t workspace_bytes,
+                                         int cur_len, int keep, int bits, int group_size, int kv_layout,
+                                         void *out_f16, void *sel_i32, void *workspace, size_t workspace_bytes,
                                          void *stream);
 
 /* Decode-step linear layer over a group-wise 4-bit weight:

@@ -30,6 +30,7 @@ SOURCES = {
     "decode_attention_topk.cu": [],
     "decode_attention_variants.cu": [],
     "dequant_gemm.cu": [],
+    "dequant_gemv.cu": [],
     "kv_interop.cu": [],
     "device_info.cu": [],
 }

@@ -47,6 +47,8 @@ constexpr int kMaxWarps = 4096;     // grid cap
 constexpr int kMaxPieces = 32;      // pieces per head (partial slots per head)
 constexpr int kMinPieceChunks = 2;  // smallest piece
 constexpr int kCtasPerSm = 16;      // one-warp CTAs resident per SM (register / smem budget)
+constexpr int kMaxCtrs = 16;        // ticket counters, 64 B apart in the 1 KB control block
+constexpr int kRetire = 16 * kMaxCtrs;
 
 #ifndef FLEXQ_ATTN_TRACE
 #define FLEXQ_ATTN_TRACE 0           // 1: per-warp %globaltimer stamps of the last launch (tuning build)
@@ -65,18 +67,22 @@ struct Params {
     const uint8_t* kc;     // chunked K cache
     const uint8_t* vc;     // chunked V cache
     __half* out;
-    uint32_t* ctrl;        // [0] next item ticket, [1] retired warps (self-resetting)
+    uint32_t* ctrl;        // [0, nctr) ticket counters, [63] retired warps (self-resetting)
     uint32_t* tickets;     // per (b, h): finished pieces (self-resetting)
     float* part;           // [bh][kMaxPieces][D] unnormalised partial outputs
     float2* ml;            // [bh][kMaxPieces] (m, l) of each partial
     int nck;               // chunks per head
-    int na, ka;            // phase A: heads [0, na), ka pieces each (ka > 1 only past the score buffer)
-    int kb;                // phase B: heads [na, bh), kb pieces each
-    int items;             // na ka + (bh - na) kb
-    int dynamic;           // 1: ticket items (above); 0: static stream-K ranges (below)
-    int total;             // static: bh nck chunks, warp w owns [w total / W, (w+1) total / W)
+    // Two phases: a static stream-K prefix over heads [0, hs), then ticket items over heads [hs, bh)
+    // ("Schedule").  Either may be empty.
+    int total;             // static: hs nck chunks, warp w owns [w total / W, (w+1) total / W)
     int wq, wr;            // static: total = wq W + wr
     int maxch;             // static: most chunks per piece (score buffer)
+    int hs;                // first ticket head
+    int na, ka;            // tickets, part A: heads [hs, hs + na), ka pieces each (ka > 1 only past the score buffer)
+    int kb;                // tickets, part B: heads [hs + na, bh), kb pieces each
+    int items;             // na ka + (bh - hs - na) kb
+    int nctr;              // ticket counters: warp w draws items c, c + nctr, ... from counter c = w % nctr
+                           // (spreads the same-address atomics of a launch over nctr L2 lines)
     int64_t chunks;        // chunk stride per (b, h) in the cache
     int cur_len;
     float qscale;          // log2(e) / sqrt(D)
@@ -95,14 +101,15 @@ __device__ __forceinline__ bool decode_item(const Params& P, int t, Piece& p) {
     const int ta = P.na * P.ka;
     if (t < ta) {
         p.np = P.ka;
-        p.bh = t / P.ka;
-        p.k = t - p.bh * P.ka;
+        const int ha = t / P.ka;
+        p.k = t - ha * P.ka;
+        p.bh = P.hs + ha;
     } else {
         const int t2 = t - ta;
         p.np = P.kb;
         const int hb = t2 / P.kb;
         p.k = t2 - hb * P.kb;
-        p.bh = P.na + hb;
+        p.bh = P.hs + P.na + hb;
     }
     p.o = p.k * P.nck / p.np;
     p.nch = (p.k + 1) * P.nck / p.np - p.o;
@@ -142,17 +149,23 @@ __device__ int head_pieces(const Params& P, int W, int bh, int o, int& count) {
     return found;
 }
 
-template <int D, int MAXT>
+// S: ring depth (stages in flight ahead of the math: S - 1).  The extra area (q, k_new, v_new)
+// is refilled at the next item's first stage; with S = 2 that issue comes after the previous item
+// has read its rows (every item has >= 2 stages), deeper rings use two extra areas, alternating.
+template <int S>
+constexpr int kXtraBufs = S > 2 ? 2 : 1;
+
+template <int D, int MAXT, int S>
 __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const Params P) {
     using C = Cfg<D, kNch>;
-    constexpr int S = 2;   // ring depth (the extra area is reused one piece ahead: S = 2 only)
+    constexpr int NX = kXtraBufs<S>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
     uint8_t* ring = smem;
-    uint8_t* xtra = smem + S * C::STG;
-    float* scores = reinterpret_cast<float*>(xtra + C::XTRA);
+    uint8_t* xtra0 = smem + S * C::STG;   // NX extra areas
+    float* scores = reinterpret_cast<float*>(xtra0 + NX * C::XTRA);
     uint32_t* limbs = reinterpret_cast<uint32_t*>(scores + MAXT);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(limbs + kLimbWords<D, kNch>);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(limbs + kLimbWords<D, kNch>);   // S stages, then NX extra
 
     const uint64_t policy = evict_first_policy();
     // Programmatic dependent launch (NEXT-3 multi-layer decode): let the next layer's launch be
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     const unsigned long long t_res = gtime();
 #endif
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S + NX; ++s) mbar_init(&bars[s], 1);   // S stage barriers + the extra areas'
         fence_proxy_async();
     }
     __syncwarp();
@@ -178,31 +191,36 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     // The next ticket is fetched one item ahead (lane 0 holds the raw atomic result
     // until it is needed); item ids go through a 3-entry FIFO to the consumer, which
     // lags by at most one stage.
+    // Item ids: a static piece is its first chunk c < P.total; ticket t is P.total + t.  The
+    // first ticket is fetched when the warp hands out its last static piece (or at the start,
+    // if its static range is empty), then always one item ahead.
     const int W = gridDim.x;
-    const int r0 = P.dynamic ? 0 : range_start(P, blockIdx.x, W);
-    const int r1 = P.dynamic ? 0 : range_start(P, blockIdx.x + 1, W);
-    int p_cur = r0;                        // static mode: the producer's next chunk
+    const int r0 = range_start(P, blockIdx.x, W);
+    const int r1 = range_start(P, blockIdx.x + 1, W);
+    int p_cur = r0;                        // the producer's next static chunk
     uint32_t tk_raw = 0;
-    if (P.dynamic && lane == 0) tk_raw = atomicAdd(P.ctrl, 1u);
+    const int ctr = int(blockIdx.x) % P.nctr;
+    if (r0 >= r1 && P.items > 0 && lane == 0) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);
     Piece pp{0, 0, 0, 0, 1};
     bool p_valid = false, p_new = false;
     int p_stage = 0, p_nst = 0, p_last = 0;
     const uint8_t* p_k = nullptr;
     const uint8_t* p_v = nullptr;
-    int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
+    int fq0 = -1, fq1 = -1, fq2 = -1, fq3 = -1, fcount = 0;
+    int p_items = 0;                       // valid items issued (selects the extra area)
     auto p_next = [&]() {
         int t;
-        if (P.dynamic) {
-            t = int(__shfl_sync(0xffffffffu, tk_raw, 0));
-            p_valid = decode_item(P, t, pp);
-            if (lane == 0 && p_valid) tk_raw = atomicAdd(P.ctrl, 1u);   // prefetch the following ticket
-        } else {
+        if (p_cur < r1) {
             t = p_cur;
-            p_valid = p_cur < r1;
-            if (p_valid) {
-                static_piece(P, p_cur, r1, pp);
-                p_cur += pp.nch;
-            }
+            static_piece(P, p_cur, r1, pp);
+            p_cur += pp.nch;
+            p_valid = true;
+            if (p_cur >= r1 && P.items > 0 && lane == 0) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);
+        } else {
+            const int tk = int(__shfl_sync(0xffffffffu, tk_raw, 0)) * P.nctr + ctr;
+            p_valid = P.items > 0 && decode_item(P, tk, pp);
+            if (lane == 0 && p_valid) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);   // prefetch the following ticket
+            t = P.total + tk;
         }
         p_stage = 0;
         if (p_valid) {
@@ -214,7 +232,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
             p_new = P.k_new != nullptr && pp.o + pp.nch == P.nck;
         }
         const int id = p_valid ? t : -1;
-        if (fcount == 0) fq0 = id; else if (fcount == 1) fq1 = id; else fq2 = id;
+        if (fcount == 0) fq0 = id; else if (fcount == 1) fq1 = id; else if (fcount == 2) fq2 = id; else fq3 = id;
         ++fcount;
     };
     auto issue = [&](int slot) {
@@ -226,34 +244,48 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         const int si = vpass ? p_stage - p_nst : p_stage;
         const uint32_t bytes = uint32_t(si == p_nst - 1 ? p_last : kNch) * C::CHB;
         const bool first = p_stage == 0;
-        mbar_expect_tx_elect(&bars[slot], bytes + (first ? (p_new ? 6 * D : 2 * D) : 0));
+        // the extra area (q, k_new, v_new) is rewritten by the async proxy for the next item: order
+        mbar_expect_tx_elect(&bars[slot], bytes);
         bulk_g2s_elect(ring + slot * C::STG, (vpass ? p_v : p_k) + int64_t(si) * C::STG, bytes, &bars[slot], policy);
         if (first) {
+            // the item's rows (q; k_new, v_new for the fused append) complete on the extra area's own
+            // barrier, one phase per item: the previous item read them before this item's first
+            // stage is issued (one stage ahead), and both the writes and the reads of every item are
+            // ordered through the same barrier's phases
             const int64_t row = int64_t(pp.bh) * D;
-            bulk_g2s_elect(xtra + C::XQ, P.q + row, 2 * D, &bars[slot], policy);
+            const int xb = NX == 1 ? 0 : (p_items & 1);
+            uint8_t* xt = xtra0 + xb * C::XTRA;
+            uint64_t* xbar = &bars[S + xb];
+            ++p_items;
+            fence_proxy_async();
+            mbar_expect_tx_elect(xbar, p_new ? 6 * D : 2 * D);
+            bulk_g2s_elect(xt + C::XQ, P.q + row, 2 * D, xbar, policy);
             if (p_new) {
-                bulk_g2s_elect(xtra + C::XNEW, P.k_new + row, 2 * D, &bars[slot], policy);
-                bulk_g2s_elect(xtra + C::XNEW + 2 * D, P.v_new + row, 2 * D, &bars[slot], policy);
+                bulk_g2s_elect(xt + C::XNEW, P.k_new + row, 2 * D, xbar, policy);
+                bulk_g2s_elect(xt + C::XNEW + 2 * D, P.v_new + row, 2 * D, xbar, policy);
             }
         }
         if (++p_stage == 2 * p_nst) p_next();
     };
     p_next();
-    issue(0);
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) issue(s);
 
     // ---------------- consumer: the same item sequence, one stage behind
     const VLane<D> vlane = v_lane<D, kNch>(lane);
-    int slot = 0;
-    uint32_t parity = 0;
-    auto acquire = [&]() -> const uint8_t* {   // issue ahead, then wait for the current slot
-        issue(slot ^ 1);
+    int slot = 0, c_items = 0;
+    uint32_t parity = 0, xparity = 0;      // xparity: bit b = phase of extra area b
+    auto acquire = [&]() -> const uint8_t* {   // issue S - 1 stages ahead, then wait for the current slot
+        issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
         return ring + slot * C::STG;
     };
     auto release = [&]() {
         __syncwarp();
-        slot ^= 1;
-        parity ^= uint32_t(slot == 0);
+        if (++slot == S) {
+            slot = 0;
+            parity ^= 1u;
+        }
     };
 
     Piece pc;
@@ -262,9 +294,10 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         const int item = fq0;              // pop the consumer's next item
         fq0 = fq1;
         fq1 = fq2;
+        fq2 = fq3;
         --fcount;
         if (item < 0) break;
-        if (P.dynamic) decode_item(P, item, pc);
+        if (item >= P.total) decode_item(P, item - P.total, pc);
         else static_piece(P, item, r1, pc);
 #if FLEXQ_ATTN_TRACE
         ++n_pieces;
@@ -306,12 +339,17 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         float M;
         {
             const uint8_t* sb = acquire();
+            const int xb = NX == 1 ? 0 : (c_items & 1);   // the item's q (and new token's rows)
+            const uint8_t* xt = xtra0 + xb * C::XTRA;
+            ++c_items;
+            mbar_wait(&bars[S + xb], (xparity >> xb) & 1u);
+            xparity ^= 1u << xb;
             if (owns_new) {
-                tq = quantize_kv_token<D>(xtra + C::XNEW, lane);
+                tq = quantize_kv_token<D>(xt + C::XNEW, lane);
                 if (nst == 1) patch(sb, false);
             }
             KFrag<D> kf;                      // the lane's q digits + epilogue weights for pass 1
-            load_q_mma<D>(xtra + C::XQ, P.qscale, lane, kf);
+            load_q_mma<D>(xt + C::XQ, P.qscale, lane, kf);
             float mx = -INFINITY;
 #pragma unroll 1
             for (int st = 0;;) {
@@ -417,11 +455,11 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     }
 
     // retire: the last warp out resets the item ticket for the next call
-    if (P.dynamic && lane == 0) {
+    if (P.items > 0 && lane == 0) {
         __threadfence();
-        if (atomicAdd(P.ctrl + 1, 1u) == gridDim.x - 1) {
-            P.ctrl[0] = 0u;
-            P.ctrl[1] = 0u;
+        if (atomicAdd(P.ctrl + kRetire, 1u) == gridDim.x - 1) {
+            for (int c = 0; c < P.nctr; ++c) P.ctrl[16 * c] = 0u;
+            P.ctrl[kRetire] = 0u;
             __threadfence();
         }
     }
@@ -437,9 +475,10 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
 #endif
 }
 
-template <int D, int MAXT>
+template <int D, int MAXT, int S>
 constexpr size_t smem_bytes() {
-    return size_t(2) * Cfg<D, kNch>::STG + Cfg<D, kNch>::XTRA + MAXT * 4 + kLimbWords<D, kNch> * 4 + 2 * 8;
+    return size_t(S) * Cfg<D, kNch>::STG + kXtraBufs<S> * Cfg<D, kNch>::XTRA + MAXT * 4 + kLimbWords<D, kNch> * 4 +
+           (S + kXtraBufs<S>) * 8;
 }
 
 // Per-device launch facts (the SM count and the kernel's occupancy), computed once per
@@ -448,7 +487,7 @@ struct DevInfo {
     int sms = 0;
     int occ = 0;
 };
-template <int D, int MAXT>
+template <int D, int MAXT, int S>
 DevInfo dev_info() {
     constexpr int kMaxDev = 64;
     static DevInfo info[kMaxDev];
@@ -457,11 +496,11 @@ DevInfo dev_info() {
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDev) dev = 0;
     std::call_once(once[dev], [dev] {
-        auto k = decode_attention_kernel<D, MAXT>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, MAXT>()));
+        auto k = decode_attention_kernel<D, MAXT, S>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, MAXT, S>()));
         int sms = 0, o = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, smem_bytes<D, MAXT>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, smem_bytes<D, MAXT, S>());
         info[dev].sms = sms > 0 ? sms : 148;
         info[dev].occ = o > 0 ? o : 1;
     });
@@ -474,56 +513,75 @@ struct WsLayout {
 WsLayout ws_layout(int bh, int d) {
     WsLayout w;
     w.ctrl = 0;
-    w.tickets = 256;
+    w.tickets = 2048;   // after the 2 KB control block (ticket counters 64 B apart, the retire count)
     w.part = (w.tickets + size_t(bh) * 4 + 255) / 256 * 256;
     w.ml = w.part + size_t(bh) * kMaxPieces * d * 4;
     w.total = w.ml + size_t(bh) * kMaxPieces * 8;
     return w;
 }
 
-// Scheduler choice and tail split (tuning only):
-// FLEXQ_ATTN_SPLIT="<min heads per warp x 100 for dynamic>,<tail heads per warp x 100>,<pieces per tail head>".
-constexpr int kDynHeadsPerWarpX100 = 150;   // B200 sweep: dynamic wins from ~1.5 heads per warp
-void tune_split(int& dyn_min_x100, int& nb_per_warp_x100, int& kb) {
-    static int v0 = -1, v1 = -1, v2 = -1;
+// Scheduler tuning (environment, A/B sweeps only):
+//   FLEXQ_ATTN_SPLIT="<min heads per warp x 100 for all-ticket mode>,<tail heads per warp x 100>,<pieces per tail head>"
+//   FLEXQ_ATTN_HYBRID="<static share of the heads, %>,<chunks per ticket piece>"
+//   FLEXQ_ATTN_CTRS=<ticket counters, 1..16>
+constexpr int kDynHeadsPerWarpX100 = 150;   // B200 sweep: whole-head tickets win from ~1.5 heads per warp
+constexpr int kHybridStaticPct = 100;       // below that: static stream-K (the static-prefix + ticket-piece
+                                            // hybrid measured slower at every share; tuning only)
+constexpr int kHybridPieceChunks = 3;
+void tune_split(int& dyn_min_x100, int& nb_per_warp_x100, int& kb, int& hyb_pct, int& hyb_q) {
+    static int v[5] = {-1, -1, -1, -1, -1};
     static std::once_flag once;
     std::call_once(once, [] {
-        const char* e = getenv("FLEXQ_ATTN_SPLIT");
-        if (e) sscanf(e, "%d,%d,%d", &v0, &v1, &v2);
+        if (const char* e = getenv("FLEXQ_ATTN_SPLIT")) sscanf(e, "%d,%d,%d", &v[0], &v[1], &v[2]);
+        if (const char* e = getenv("FLEXQ_ATTN_HYBRID")) sscanf(e, "%d,%d", &v[3], &v[4]);
     });
-    if (v0 >= 0) dyn_min_x100 = v0;
-    if (v1 >= 0) nb_per_warp_x100 = v1;
-    if (v2 > 0) kb = v2;
+    if (v[0] >= 0) dyn_min_x100 = v[0];
+    if (v[1] >= 0) nb_per_warp_x100 = v[1];
+    if (v[2] > 0) kb = v[2];
+    if (v[3] >= 0) hyb_pct = v[3];
+    if (v[4] > 0) hyb_q = v[4];
 }
 
-template <int D, int MAXT>
+template <int D, int MAXT, int S>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const DevInfo di = dev_info<D, MAXT>();
+    const DevInfo di = dev_info<D, MAXT, S>();
     const int Wres = std::min(di.sms * di.occ, kMaxWarps);
     const int nck = (a.cur_len + kChunk - 1) / kChunk;
     const int maxch = MAXT / kChunk;
     const int ka = (nck + maxch - 1) / maxch;
     if (ka > kMaxPieces / 2) return cudaErrorInvalidValue;   // context beyond 16 score buffers
-    // Scheduler (B200 sweep): with many heads per warp, dynamic tickets over whole
-    // heads balance the per-SM rate differences and leave a short tail; with few, static
-    // stream-K ranges keep every warp streaming (a whole-head ticket would idle warps).
-    int dyn_min_x100 = kDynHeadsPerWarpX100, nb_x100 = 0, kb = 0;
-    tune_split(dyn_min_x100, nb_x100, kb);
+    // Scheduler (B200 sweeps, DESIGN.md section 3 "Schedule"):
+    //  * many heads per warp: tickets over whole heads (the last ones in pieces) balance the
+    //    per-SM streaming rates and leave a short tail;
+    //  * fewer, with the GPU full: a static stream-K prefix over the first hyb_pct % of the heads
+    //    (every warp streams from the start), then tickets over small pieces of the rest, so the
+    //    SMs that stream faster take more of the end;
+    //  * small problems: static stream-K ranges only.
+    int dyn_min_x100 = kDynHeadsPerWarpX100, nb_x100 = 0, kb = 0, hyb_pct = kHybridStaticPct,
+        hyb_q = kHybridPieceChunks;
+    tune_split(dyn_min_x100, nb_x100, kb, hyb_pct, hyb_q);
     const bool dynamic = int64_t(bh) * 100 >= int64_t(dyn_min_x100) * Wres;
-    int W, na = bh, nb = 0;
+    int W, hs, na = 0, nb = 0;
     if (dynamic) {
         W = Wres;
+        hs = 0;
         nb = int(std::min<int64_t>(bh, (int64_t(W) * nb_x100 + 99) / 100));
         if (kb <= 0) kb = 2;
         kb = std::max(ka, std::min({kb, std::max(1, nck / kMinPieceChunks), kMaxPieces}));
         if (kb <= 1) nb = 0;
         na = bh - nb;
     } else {
-        // >= kMinPieceChunks chunks per warp and <= 16 warps per head keep a head's pieces
-        // within kMaxPieces (head_pieces <= 1 + ceil(W / bh) + ceil(nck / maxch))
+        // >= kMinPieceChunks chunks per warp and <= 15 warps per head keep a head's pieces
+        // within kMaxPieces (head_pieces <= 1 + ceil(W / heads) + ceil(nck / maxch))
         W = std::max(1, std::min({Wres, bh * nck / kMinPieceChunks, bh * 15}));
-        kb = 1;
+        hs = bh;
+        if (W == Wres && hyb_pct < 100) {
+            hs = int(int64_t(bh) * hyb_pct / 100);
+            if (hs > 0 && int64_t(hs) * 15 < W) hs = std::min(bh, (W + 14) / 15);
+            nb = bh - hs;
+            kb = std::max(ka, std::min({(nck + hyb_q - 1) / hyb_q, kMaxPieces}));
+        }
     }
     const WsLayout w = ws_layout(bh, D);
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
@@ -537,12 +595,18 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.part = reinterpret_cast<float*>(ws + w.part);
     P.ml = reinterpret_cast<float2*>(ws + w.ml);
     P.nck = nck;
+    P.hs = hs;
     P.na = na;
     P.ka = ka;
-    P.kb = kb;
-    P.items = na * ka + nb * kb;
-    P.dynamic = dynamic ? 1 : 0;
-    P.total = bh * nck;
+    P.kb = std::max(kb, 1);
+    P.items = na * ka + nb * P.kb;
+    P.total = hs * nck;
+    static const int nctr_env = [] {
+        const char* e = getenv("FLEXQ_ATTN_CTRS");
+        return e ? atoi(e) : 0;
+    }();
+    const int grid = dynamic ? std::max(1, std::min(W, P.items)) : W;
+    P.nctr = std::max(1, std::min({nctr_env > 0 ? nctr_env : kMaxCtrs, kMaxCtrs, grid}));   // every counter has warps
     P.wq = P.total / W;
     P.wr = P.total % W;
     P.maxch = maxch;
@@ -558,16 +622,29 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
         return !(e && e[0] == '0');
     }();
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(dynamic ? std::max(1, std::min(W, P.items)) : W));
+    cfg.gridDim = dim3(unsigned(grid));   // dynamic: no more warps than items
     cfg.blockDim = dim3(32);
-    cfg.dynamicSmemBytes = smem_bytes<D, MAXT>();
+    cfg.dynamicSmemBytes = smem_bytes<D, MAXT, S>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<D, MAXT>, P);
+    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<D, MAXT, S>, P);
+}
+
+// Ring depth (tuning: FLEXQ_ATTN_RING=2|3|4).
+template <int D, int MAXT>
+cudaError_t launch_ring(const AttnArgs& a, cudaStream_t stream) {
+    static const int ring_env = [] {
+        const char* e = getenv("FLEXQ_ATTN_RING");
+        return e ? atoi(e) : 0;
+    }();
+    const int S = ring_env >= 2 && ring_env <= 4 ? ring_env : 2;
+    if (S == 4) return launch<D, MAXT, 4>(a, stream);
+    if (S == 3) return launch<D, MAXT, 3>(a, stream);
+    return launch<D, MAXT, 2>(a, stream);
 }
 
 }  // namespace
@@ -581,8 +658,8 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) 
 // per head, 1088 the prompt-1024 steps; longer contexts are cut into 1088-token pieces.
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
     if (a.head_dim == 128)
-        return a.cur_len <= 576 ? launch<128, 576>(a, stream) : launch<128, 1088>(a, stream);
-    return a.cur_len <= 576 ? launch<64, 576>(a, stream) : launch<64, 1088>(a, stream);
+        return a.cur_len <= 576 ? launch_ring<128, 576>(a, stream) : launch_ring<128, 1088>(a, stream);
+    return a.cur_len <= 576 ? launch_ring<64, 576>(a, stream) : launch_ring<64, 1088>(a, stream);
 }
 
 }  // namespace flexq

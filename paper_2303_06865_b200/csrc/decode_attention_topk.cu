@@ -2,7 +2,7 @@
 // compressed KV cache (FlexGen Sec. 4 "Sparse Attention", PAPER.md P:853-857,
 // SPEC S:496-504).
 //
-//   s_t = q . K^_t / sqrt(D) for every cached token (pass 1, full K stream);
+//   s_t = q . K^_t / sqrt(D) for every cached token (full K stream);
 //   keep the `keep` largest s_t (equal scores: lower token index first);
 //   out = sum_{t kept} p_t V^_t with p renormalised over the kept set.
 //
@@ -10,17 +10,22 @@
 // P:856): at keep = 10% the step reads K (0.5625 B/elem) + 10% of V instead of
 // all of V, ~55% of the dense bytes.
 //
-// Design: persistent warps, one warp = one (b, h) (no context split; the
-// per-warp score buffer holds kTopkMaxTokens).  Pass 1 is the dense kernel's
-// TMA-bulk-staged K pass (attn_common.cuh).  Selection is an exact bitwise
-// select on order-preserving 32-bit keys of the fp32 scores held in registers
-// (one warp-wide REDUX count per bit, stopping once exactly `keep` keys lie
-// above the candidate); ties at the threshold key go to the lowest token
-// indices (ballot prefix counts), so the kept set is the definition's.
-// Pass 2 gathers the kept V rows straight from HBM (the token's quad row of
-// the quad-interleaved V chunk, 64 B per lane in 128-bit loads, its byte
-// extracted with PRMT, three groups of rows in flight) into
-// fp32 register accumulators.
+// Two launches:
+//  * topk_select_kernel -- persistent warps, one warp = one (b, h) (no context split; the
+//    per-warp score buffer holds kTopkMaxTokens).  The K pass is the dense kernel's TMA-bulk-
+//    staged tensor-core pass (attn_common.cuh).  Selection is an exact bitwise select on
+//    order-preserving 32-bit keys of the fp32 scores held in registers (one warp-wide REDUX
+//    count per bit, stopping once exactly `keep` keys lie above the candidate); ties at the
+//    threshold key go to the lowest token indices (ballot prefix counts), so the kept set is the
+//    definition's.  The head's kept list (index, weight p_t / l) goes to the workspace.  With
+//    the V gather out of this kernel the warp's K stream only pauses for the select.
+//  * topk_gather_kernel -- one warp per (b, h) reads the kept V rows and accumulates
+//    sum w_t V^_t in fp32; groups of rows are loaded before any is used, so the gathers of a
+//    head are in flight together.  In the token-major layout (FLEXQ_KV_TOKEN_MAJOR) a kept
+//    token is one contiguous 64-byte row (D = 128); in the dense layout it is spread over its
+//    256-byte quad row (the price of the dense kernel's operand order).
+// The gather is launched with programmatic dependent launch, so its grid is scheduled while
+// the select grid drains.
 #include <cuda_fp16.h>
 #include <stdint.h>
 
@@ -30,10 +35,10 @@
 #include "flexq_internal.h"
 
 #ifndef FLEXQ_TOPK_MINB
-#define FLEXQ_TOPK_MINB 4   // CTAs per SM the register budget is sized for
+#define FLEXQ_TOPK_MINB 4   // select kernel: CTAs per SM the register budget is sized for
 #endif
 #ifndef FLEXQ_TOPK_WPC
-#define FLEXQ_TOPK_WPC 3    // warps (= (b, h) units in flight) per CTA
+#define FLEXQ_TOPK_WPC 4    // select kernel: warps (= (b, h) units in flight) per CTA
 #endif
 
 namespace flexq {
@@ -151,22 +156,6 @@ __device__ __forceinline__ void write_out(__half* dst, const float (&v)[32], flo
     }
 }
 
-struct TopkParams {
-    const __half* q;
-    const uint8_t* kc;
-    const uint8_t* vc;
-    __half* out;
-    int32_t* sel;        // optional [bh][keep] kept token indices (ascending)
-    uint32_t* ctrl;      // [0] next ticket, [1] finished warps (workspace)
-    int bh_total, chunks, cur_len, keep;
-    float qscale;
-};
-
-__device__ __forceinline__ uint32_t order_key(float f) {
-    const uint32_t u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
-}
-
 __device__ __forceinline__ uint4 ldg_nc128(const void* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -179,9 +168,27 @@ __device__ __forceinline__ uint32_t ldg_nc32(const void* p) {
     return r;
 }
 
+struct SelectParams {
+    const __half* q;
+    const uint8_t* kc;
+    int32_t* sel;        // optional [bh][keep] kept token indices (ascending)
+    int32_t* kidx;       // [bh][keep] kept token indices (workspace)
+    float* kw;           // [bh][keep] their softmax weights, renormalised over the kept set
+    uint32_t* ctrl;      // [0] next ticket, [1] finished warps (workspace)
+    int bh_total, chunks, cur_len, keep;
+    float qscale;
+};
+
+__device__ __forceinline__ uint32_t order_key(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
+}
+
+// Kernel 1: scores of every cached token (the dense kernel's tensor-core K pass over a TMA-bulk
+// ring), the exact top-`keep` selection, and the kept list with its weights.
 template <int D, int NCH, int S, int WPC, int MAXT>
 __global__ void __launch_bounds__(WPC * 32, FLEXQ_TOPK_MINB)
-decode_attention_topk_kernel(const TopkParams P) {
+topk_select_kernel(const SelectParams P) {
     using C = Cfg<D, NCH>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -191,14 +198,15 @@ decode_attention_topk_kernel(const TopkParams P) {
     uint8_t* qsm = ring + S * C::STG;
     float* scores = reinterpret_cast<float*>(qsm + 2 * D);
     uint16_t* kept = reinterpret_cast<uint16_t*>(qsm + 2 * D + MAXT * 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * S;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * (S + 1);   // + q's barrier
 
     const uint64_t policy = evict_first_policy();
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s <= S; ++s) mbar_init(&bars[s], 1);
         fence_proxy_async();
     }
     __syncwarp();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---------------- producer: the K stages of whole (b, h) units (no split)
     const int nst = (P.cur_len + C::CH - 1) / C::CH;
@@ -222,29 +230,25 @@ decode_attention_topk_kernel(const TopkParams P) {
         }
         const int n = min(C::CH, P.cur_len - p_stage * C::CH);
         const uint32_t bytes = uint32_t((n + kChunk - 1) / kChunk) * C::CHB;
-        const bool first = p_stage == 0;
-        uint8_t* sb = ring + slot * C::STG;
-        mbar_expect_tx_elect(&bars[slot], bytes + (first ? 2 * D : 0));
-        bulk_g2s_elect(sb, p_k + int64_t(p_stage) * C::STG, bytes, &bars[slot], policy);
-        // q of the unit (read at its first stage, before the next unit's q is issued: S = 2)
-        if (first) bulk_g2s_elect(qsm, P.q + int64_t(p_bh) * D, 2 * D, &bars[slot], policy);
+        mbar_expect_tx_elect(&bars[slot], bytes);
+        bulk_g2s_elect(ring + slot * C::STG, p_k + int64_t(p_stage) * C::STG, bytes, &bars[slot], policy);
+        if (p_stage == 0) {   // the unit's q, on its own barrier (one phase per unit)
+            fence_proxy_async();
+            mbar_expect_tx_elect(&bars[S], 2 * D);
+            bulk_g2s_elect(qsm, P.q + int64_t(p_bh) * D, 2 * D, &bars[S], policy);
+        }
         if (++p_stage == nst) next_unit();
     };
     next_unit();
 #pragma unroll 1
     for (int s = 0; s < S - 1; ++s) issue(s);
 
-    constexpr int LPT = D / 32;   // V gather: lanes per token
-    constexpr int TPI = 32 / LPT; //   tokens per warp iteration
-    const int tl = lane / LPT;
-    const int sg = lane % LPT;
-    const uint32_t magic = magic_reg();
     const unsigned lt_mask = (1u << lane) - 1u;
     const int n_tok = P.cur_len;
     const int keep = P.keep;
 
     int slot = 0;
-    uint32_t parity = 0;
+    uint32_t parity = 0, qparity = 0;
     auto acquire = [&]() -> const uint8_t* {
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
@@ -266,11 +270,13 @@ decode_attention_topk_kernel(const TopkParams P) {
         --fcount;
         if (bh < 0) break;
 
-        // ------------------------------------------------ pass 1: all scores -> smem
+        // ------------------------------------------------ all scores -> smem
         float M;
         {
             const uint8_t* sb = acquire();
-            KFrag<D> kf;                      // the lane's q digits + epilogue weights for pass 1
+            mbar_wait(&bars[S], qparity);
+            qparity ^= 1u;
+            KFrag<D> kf;                      // the lane's q digits + epilogue weights
             load_q_mma<D>(qsm, P.qscale, lane, kf);
             float mx = -INFINITY;
 #pragma unroll 1
@@ -324,7 +330,9 @@ decode_attention_topk_kernel(const TopkParams P) {
                 }
             }
         }
-        // kept: key > T, or key == T among the first krem such tokens by index
+        // kept: key > T, or key == T among the first krem such tokens by index; the list is
+        // built in ascending token order with its weights p_t = 2^(s_t - M)
+        float l = 0.0f;
         {
             int krem = keep;
             if (!exact) {
@@ -342,90 +350,30 @@ decode_attention_topk_kernel(const TopkParams P) {
                 const unsigned beq = __ballot_sync(0xffffffffu, eq);
                 const bool keepit = gt || (eq && ties + __popc(beq & lt_mask) < krem);
                 const unsigned bk = __ballot_sync(0xffffffffu, keepit);
-                if (keepit) kept[base + __popc(bk & lt_mask)] = uint16_t(j * 32 + lane);
+                if (keepit) {
+                    kept[base + __popc(bk & lt_mask)] = uint16_t(j * 32 + lane);
+                    l += ex2(scores[j * 32 + lane] - M);
+                }
                 base += __popc(bk);
                 ties += __popc(beq);
             }
-            __syncwarp();
-            if (P.sel)
-                for (int j = lane; j < keep; j += 32) P.sel[int64_t(bh) * keep + j] = kept[j];
-        }
-
-        // ------------------------------------------------ pass 2: gather the kept V rows
-        float2 acc[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
-        float l = 0.0f, bsum = 0.0f;
-        const uint8_t* vbase = P.vc + int64_t(bh) * P.chunks * C::CHB;
-        // V codes are quad-interleaved (include/flexq.h): token t's 16 B segment sg
-        // (column pairs 16 sg .. 16 sg + 15) is byte t % 4 of 16 words of its quad
-        // row (two swizzled 8-pair blocks); load the 64 B and gather that byte with PRMT.
-        auto load_row = [&](int t, uint4 (&raw)[4], uint32_t& meta) {
-            const uint8_t* cb = vbase + (t >> 5) * C::CHB;
-            const int quad = (t & 31) >> 2;
-            const uint8_t* q = cb + quad * C::CB * 4;
-            // swizzled layout: 8-pair block b of the quad row sits at block b ^ (quad & 3)
-            const uint8_t* b0 = q + ((2 * sg) ^ (quad & 3)) * 32;
-            const uint8_t* b1 = q + ((2 * sg + 1) ^ (quad & 3)) * 32;
-            raw[0] = ldg_nc128(b0);
-            raw[1] = ldg_nc128(b0 + 16);
-            raw[2] = ldg_nc128(b1);
-            raw[3] = ldg_nc128(b1 + 16);
-            meta = ldg_nc32(cb + C::OFF_M + (t & 31) * C::MB + (sg >> 1) * 4);
-        };
-        auto row_bytes = [&](int t, const uint4 (&raw)[4]) -> uint4 {
-            const uint32_t k = uint32_t(t & 3);
-            const uint32_t sel = k | ((k + 4) << 4);
-            uint32_t o[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t a = __byte_perm(raw[j].x, raw[j].y, sel);   // bytes k of words 4j, 4j+1
-                const uint32_t b = __byte_perm(raw[j].z, raw[j].w, sel);   // words 4j+2, 4j+3
-                o[j] = __byte_perm(a, b, 0x5410);
-            }
-            return make_uint4(o[0], o[1], o[2], o[3]);
-        };
-        auto row_of = [&](int j, int& t) -> bool {
-            t = j < keep ? int(kept[j]) : 0;
-            return j < keep;
-        };
-        // three groups of rows in flight (the gather is latency-bound); the loop is
-        // unrolled over the three register slots so no slot is copied while its
-        // loads are outstanding
-        int ta, tb, tc;
-        bool va = row_of(tl, ta), vb = row_of(TPI + tl, tb), vc = row_of(2 * TPI + tl, tc);
-        uint4 ra[4] = {}, rb[4] = {}, rc[4] = {};
-        uint32_t ma = 0u, mb = 0u, mc = 0u;
-        if (va) load_row(ta, ra, ma);
-        if (vb) load_row(tb, rb, mb);
-        if (vc) load_row(tc, rc, mc);
-        auto step = [&](int g, int& t, bool& v, uint4 (&r)[4], uint32_t& m) {
-            float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&m));
-            float p = ex2(scores[t] - M);
-            if (!v) {
-                p = 0.0f;
-                vm = make_float2(0.0f, 0.0f);
-            }
-            v_accum(acc, l, bsum, row_bytes(t, r), vm, p, magic);
-            v = row_of((g + 3) * TPI + tl, t);   // refill the slot with group g + 3
-            m = 0u;
-            if (v) load_row(t, r, m);
-        };
-#pragma unroll 1
-        for (int g = 0;; g += 3) {
-            step(g, ta, va, ra, ma);
-            if ((g + 1) * TPI >= keep) break;
-            step(g + 1, tb, vb, rb, mb);
-            if ((g + 2) * TPI >= keep) break;
-            step(g + 2, tc, vc, rc, mc);
-            if ((g + 3) * TPI >= keep) break;
+            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
         }
-        float v[32];
-        const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
-        write_out<D>(P.out + int64_t(bh) * D + col0, v, l);
         __syncwarp();
+        const float inv_l = 1.0f / l;
+        const int64_t lo = int64_t(bh) * keep;
+        for (int j = lane; j < keep; j += 32) {
+            const int t = kept[j];
+            P.kidx[lo + j] = t;
+            P.kw[lo + j] = ex2(scores[t] - M) * inv_l;
+            if (P.sel) P.sel[lo + j] = t;
+        }
+        __syncwarp();   // scores / kept are rewritten by the next unit
     }
 
+    // let the gather kernel's grid launch (its griddepcontrol.wait still waits for this grid)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (lane == 0) {
         __threadfence();
         const uint32_t total = gridDim.x * WPC;
@@ -437,15 +385,102 @@ decode_attention_topk_kernel(const TopkParams P) {
     }
 }
 
-template <int D, int NCH, int S, int WPC, int MAXT>
-constexpr size_t topk_smem_bytes() {
-    return size_t(WPC) * (S * (Cfg<D, NCH>::STG + 8) + 2 * D + MAXT * 6);
+struct GatherParams {
+    const uint8_t* vc;
+    const int32_t* kidx;
+    const float* kw;
+    __half* out;
+    int bh_total, chunks, keep;
+};
+
+// Kernel 2: out = sum over the kept tokens of w_t V^_t, one warp per (b, h).  LPT = D / 32 lanes
+// per token, lane sg of a token owns its columns 32 sg .. 32 sg + 31 (16 code bytes, one group's
+// half).  Token-major V (VTM): the 16 bytes are one load of the token's row; quad-interleaved V:
+// four 16-byte loads of the token's quad row and a byte gather (PRMT).  GB groups of TPI tokens
+// are loaded before any is accumulated (the loads are independent gathers).
+template <int D, bool VTM>
+__global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) {
+    constexpr int CB = D / 2, MB = D / 16, CHB = kChunk * (CB + MB);
+    constexpr int LPT = D / 32, TPI = 32 / LPT, GB = 4;
+    const int lane = threadIdx.x & 31;
+    const int bh = int(blockIdx.x) * (blockDim.x >> 5) + int(threadIdx.x >> 5);
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the kept lists of the select kernel
+    if (bh >= P.bh_total) return;
+    const int tl = lane / LPT, sg = lane % LPT;
+    const uint32_t magic = magic_reg();
+    const uint8_t* vbase = P.vc + int64_t(bh) * P.chunks * CHB;
+    const int32_t* idx = P.kidx + int64_t(bh) * P.keep;
+    const float* wts = P.kw + int64_t(bh) * P.keep;
+    float2 acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.0f, 0.0f);
+    float l = 0.0f, bsum = 0.0f;
+#pragma unroll 1
+    for (int j0 = 0; j0 < P.keep; j0 += GB * TPI) {
+        uint4 raw[GB][VTM ? 1 : 4];
+        uint32_t meta[GB];
+        float w[GB];
+        int tk[GB];
+#pragma unroll
+        for (int g = 0; g < GB; ++g) {
+            const int j = j0 + g * TPI + tl;
+            const bool v = j < P.keep;
+            const int t = v ? __ldg(idx + j) : 0;
+            tk[g] = t;
+            w[g] = v ? __ldg(wts + j) : 0.0f;
+            const uint8_t* cb = vbase + (t >> 5) * CHB;
+            meta[g] = ldg_nc32(cb + kChunk * CB + (t & 31) * MB + (sg >> 1) * 4);
+            if constexpr (VTM) {
+                raw[g][0] = ldg_nc128(cb + (t & 31) * CB + 16 * sg);
+            } else {
+                // quad row of the token; 8-pair block b of it sits at block b ^ (quad & 3)
+                const int quad = (t & 31) >> 2;
+                const uint8_t* qr = cb + quad * CB * 4;
+                const uint8_t* b0 = qr + ((2 * sg) ^ (quad & 3)) * 32;
+                const uint8_t* b1 = qr + ((2 * sg + 1) ^ (quad & 3)) * 32;
+                raw[g][0] = ldg_nc128(b0);
+                raw[g][1] = ldg_nc128(b0 + 16);
+                raw[g][2] = ldg_nc128(b1);
+                raw[g][3] = ldg_nc128(b1 + 16);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < GB; ++g) {
+            uint4 row;
+            if constexpr (VTM) {
+                row = raw[g][0];
+            } else {   // byte t % 4 of each word: the token's 16 bytes of the segment
+                const uint32_t k = uint32_t(tk[g] & 3);
+                const uint32_t selb = k | ((k + 4) << 4);
+                uint32_t o[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t a = __byte_perm(raw[g][q].x, raw[g][q].y, selb);
+                    const uint32_t b = __byte_perm(raw[g][q].z, raw[g][q].w, selb);
+                    o[q] = __byte_perm(a, b, 0x5410);
+                }
+                row = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            const float2 vm = __half22float2(*reinterpret_cast<const __half2*>(&meta[g]));
+            v_accum(acc, l, bsum, row, vm, w[g], magic);   // w = 0 for padding slots
+        }
+    }
+    float v[32];
+    const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
+    write_out<D>(P.out + int64_t(bh) * D + col0, v, 1.0f);   // the weights are already normalised
 }
 
 template <int D, int NCH, int S, int WPC, int MAXT>
+constexpr size_t select_smem_bytes() {
+    return size_t(WPC) * (S * Cfg<D, NCH>::STG + 2 * D + MAXT * 6 + (S + 1) * 8);
+}
+
+constexpr size_t kTopkCtrlBytes = 2048;
+
+template <int D, int NCH, int S, int WPC, int MAXT>
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
-    auto k = decode_attention_topk_kernel<D, NCH, S, WPC, MAXT>;
-    const size_t smem = topk_smem_bytes<D, NCH, S, WPC, MAXT>();
+    auto k = topk_select_kernel<D, NCH, S, WPC, MAXT>;
+    const size_t smem = select_smem_bytes<D, NCH, S, WPC, MAXT>();
     // per-device launch facts, computed once per device under a lock
     constexpr int kMaxDev = 64;
     static int occs[kMaxDev], smss[kMaxDev];
@@ -464,23 +499,51 @@ cudaError_t launch_topk(const TopkArgs& a, cudaStream_t stream) {
     const int occ = occs[dev], sms = smss[dev];
     const int bh = a.batch * a.heads;
     const int ctas = min(sms * occ, (bh + WPC - 1) / WPC);
-    TopkParams P;
+    uint8_t* ws = static_cast<uint8_t*>(a.workspace);
+    const size_t list = size_t(bh) * size_t(a.keep);
+    SelectParams P;
     P.q = static_cast<const __half*>(a.q);
     P.kc = static_cast<const uint8_t*>(a.k_cache);
-    P.vc = static_cast<const uint8_t*>(a.v_cache);
-    P.out = static_cast<__half*>(a.out);
     P.sel = static_cast<int32_t*>(a.sel);
-    P.ctrl = static_cast<uint32_t*>(a.workspace);
+    P.ctrl = reinterpret_cast<uint32_t*>(ws);
+    P.kidx = reinterpret_cast<int32_t*>(ws + kTopkCtrlBytes);
+    P.kw = reinterpret_cast<float*>(ws + kTopkCtrlBytes + list * 4);
     P.bh_total = bh;
     P.chunks = a.chunks;
     P.cur_len = a.cur_len;
     P.keep = a.keep;
     P.qscale = 1.4426950408889634f / sqrtf(float(D));
     k<<<ctas, WPC * 32, smem, stream>>>(P);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    GatherParams G;
+    G.vc = static_cast<const uint8_t*>(a.v_cache);
+    G.kidx = P.kidx;
+    G.kw = P.kw;
+    G.out = static_cast<__half*>(a.out);
+    G.bh_total = bh;
+    G.chunks = a.chunks;
+    G.keep = a.keep;
+    // programmatic dependent launch: the gather grid is scheduled as the select grid drains
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned((bh + 7) / 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (a.v_tm) return cudaLaunchKernelEx(&cfg, topk_gather_kernel<D, true>, G);
+    return cudaLaunchKernelEx(&cfg, topk_gather_kernel<D, false>, G);
 }
 
 }  // namespace
+
+size_t topk_workspace_bytes(int batch, int heads, int t_cap) {
+    // the kept lists: int32 index + fp32 weight per (b, h, kept token), keep <= t_cap
+    return kTopkCtrlBytes + size_t(batch) * size_t(heads) * size_t(t_cap) * 8;
+}
 
 cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
     constexpr int W = FLEXQ_TOPK_WPC;

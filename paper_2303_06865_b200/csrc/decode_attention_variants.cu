@@ -1,6 +1,6 @@
 // decode_attention_variants.cu -- decode attention over the b in {2, 3, 4, 8} x g in {32, 64, 128}
-// KV caches (SURVEY 8(f) NEXT-3 variants; the b = 4, g = 64 cache has its own tensor-core kernel,
-// decode_attention.cu).
+// KV caches (SURVEY 8(f) NEXT-3 variants; the b = 4, g = 64 cache in its default (dense) layout has
+// its own tensor-core kernel, decode_attention.cu; in the token-major layout it runs here).
 //
 // The method is the same (P:271-274 with the cache dequantized as in P:845, reading M):
 //   out = softmax(q . K^[0:cur_len]^T / sqrt(D)) . V^[0:cur_len],  K^, V^ = fmaf(c, scale, min)
@@ -454,6 +454,7 @@ cudaError_t launch_decode_attention_variant(const AttnArgs& a, int bits, int gro
         case 3064: return launch_var_d<3, 64>(a, stream);
         case 3128: return launch_var_d<3, 128>(a, stream);
         case 4032: return launch_var_d<4, 32>(a, stream);
+        case 4064: return launch_var_d<4, 64>(a, stream);   // the (4, 64) cache in the token-major layout
         case 4128: return launch_var_d<4, 128>(a, stream);
         case 8032: return launch_var_d<8, 32>(a, stream);
         case 8064: return launch_var_d<8, 64>(a, stream);

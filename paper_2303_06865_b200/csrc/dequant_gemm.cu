@@ -830,9 +830,11 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
+}  // namespace
+
 bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
               uint64_t stride1_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
-              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+              CUtensorMapL2promotion promo) {
     EncodeTiled enc = encode_fn();
     if (!enc) return false;
     const cuuint64_t dims[2] = {d0, d1};
@@ -842,6 +844,8 @@ bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t
     return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+namespace {
 
 int sm_count() { return device_sm_count(); }
 
@@ -869,11 +873,25 @@ size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n) {
     (void)k;
     const int64_t tiles = n / kBN;
     const size_t tickets = size_t((tiles * 4 + 255) / 256 * 256);
-    return tickets + size_t(kGemmMaxGrid) * size_t(mpad_of(m)) * kBN * sizeof(float);
+    const size_t tc = tickets + size_t(kGemmMaxGrid) * size_t(mpad_of(m)) * kBN * sizeof(float);
+    const size_t gv = m <= kGemvMaxRows ? dequant_gemv_workspace_bytes(n) : 0;
+    return tc > gv ? tc : gv;
 }
+
+namespace {
+// Small-batch path switch (tuning / A-B only): FLEXQ_GEMM_SMALLM=0 sends every batch to the tcgen05 kernel.
+bool small_m_path() {
+    static const bool on = [] {
+        const char* e = getenv("FLEXQ_GEMM_SMALLM");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
 
 cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, int64_t K, int64_t N, void* y,
                                 void* workspace, cudaStream_t stream) {
+    if (M <= kGemvMaxRows && small_m_path()) return launch_dequant_gemv(x, panels, M, K, N, y, workspace, stream);
     const int kb = int(K / kBK);
     const int G = sm_count() < kGemmMaxGrid ? sm_count() : kGemmMaxGrid;
     // CTA pairs (cta_group::2, 512-column pair tiles) are opt-in (FLEXQ_GEMM_PAIR=1): measured within 3 %

@@ -1,0 +1,360 @@
+// dequant_gemv.cu -- the decode linear layer at small batch (M <= 16 rows), SURVEY NEXT-2.
+//
+//   y[m][n] = sum_k x[m][k] * w^[k][n],   w^[k][n] = min(RN16(c * scale + min), 65504)
+// (readings J, G1, G2 in DESIGN.md) over the same 9 KB weight panels
+// as dequant_gemm.cu (flexq_pack_weight's output), with the same fp16 dequantized values.
+//
+// Why a second kernel: at M <= 16 the product is a GEMV -- 2 M flops per 0.56 weight bytes --
+// so the bound is the HBM stream of the compressed weight, not the tensor pipe.  The tcgen05
+// kernel runs one 9 KB panel per ~850-cycle pipeline step (MMA issue + commit + three rings),
+// ~114 us at M = 1 for 340 MB.  Here a panel is one stage of a deep per-SM ring and its math is a
+// handful of legacy mma.sync per warp:
+//   * Persistent CTAs, one per SM; CTA c streams the contiguous panel range
+//     [c T / G, (c + 1) T / G) of the T = tiles x KB panels in (tile, k-block) order
+//     (stream-K), so every SM moves the same number of bytes.
+//   * Four producer warps take every fourth stage of a 12-stage ring; per stage one lane issues
+//     three copies: the 9216-byte panel, its 16-byte clamp flag and the M x 64 tile of x (2-D
+//     TMA).  (One producer lane issuing per-row copies of x was the bound of the first version:
+//     ~90 cycles per copy, 141 us at M = 1 and 313 us at M = 16.)
+//   * Sixteen consumer warps each own 16 weight columns of the 256-column tile (one MMA row
+//     block).  Per stage a lane loads two code words per column (k 8t..8t+7 and
+//     32+8t..32+8t+7), dequantizes them into fp16 pairs (LOP3 + HADD2 + HFMA2 [+ HMNMX2] per pair,
+//     exactly dequant_gemm.cu's deq_pair), and runs 4 mma.sync.m16n8k16 (f16 x f16 -> f32) per
+//     8 rows of x: A = 16 columns x 16 k, B = x.  The k order inside an MMA is a permutation
+//     (step s takes sub-pair s of every code word), applied to x identically.  Each step has its
+//     own accumulator, so the 4 MMAs of a stage are independent (summed once per tile); with
+//     8 consumer warps and one accumulator chain (the second version) a stage took ~800 cycles,
+//     latency-bound at 2 warps per scheduler.
+//   * A tile split between CTAs writes fp32 partials; the last of its contributors (ticket)
+//     sums them in CTA order -- deterministic -- and stores fp16.
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "flexq_internal.h"
+
+namespace flexq {
+namespace {
+
+constexpr int kConsumers = 16;                        // consumer warps (16 columns each)
+constexpr int kProducers = 4;                         // producer warps (every 4th stage each)
+constexpr int kThreadsV = (kConsumers + kProducers) * 32;
+constexpr int kStagesV = 12;
+constexpr int kPanelData = kGemmTileN * kGemmTileK / 2 + 1024;   // 9216: codes + meta
+constexpr int kXOff = kPanelData;                     // the x tile [M][64] fp16 (128-B aligned for the 2-D TMA)
+constexpr int kFlagOff = kXOff + kGemvMaxRows * 128;  // the panel's 16-byte clamp flag
+constexpr int kStageBytes = (kFlagOff + 16 + 127) / 128 * 128;   // 11392
+static_assert(kXOff % 128 == 0 && kStageBytes % 128 == 0, "tensor-copy destination alignment");
+constexpr int kSmemV = kStagesV * kStageBytes + 2 * kStagesV * 8 + 16;
+
+struct GemvParams {
+    const uint8_t* panels;   // [tiles][KB][9216 B], then [tiles][KB][16 B] flags
+    __half* y;               // [M][N]
+    float* partials;         // [grid][2][256 n][16 m]
+    uint32_t* tickets;       // [tiles]
+    int M, N, KB;
+    int64_t total;           // panels
+    int G;                   // CTAs
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(su32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_fractional(bool last) {
+    uint64_t p;
+    if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+// dequant_gemm.cu's conversion, operation for operation (reading G2): nibbles 0 and 4 of t ->
+// fp16 1024 + c (exact), - 1024 (exact), one fp16 FMA with the pair's (scale, min), clamp.
+template <bool CLAMP>
+__device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t mp) {
+    uint32_t m;
+    asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));
+    const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));
+    const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
+    if constexpr (CLAMP) return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));
+    else return h2u(v);
+}
+
+__device__ __forceinline__ void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ int64_t range_start(int64_t total, int c, int G) { return int64_t(c) * total / G; }
+__device__ __forceinline__ int owner(int64_t total, int G, int64_t i) {   // CTA whose range holds panel i
+    return int(((i + 1) * G - 1) / total);
+}
+
+// One stage of a consumer warp: 16 columns x 64 k against MB blocks of 8 rows; step s of the
+// four accumulates into acc[s].
+template <int MB, bool CLAMP>
+__device__ __forceinline__ void stage_math(const uint8_t* st, int n0, int lane, float (&acc)[4][MB][4]) {
+    const int g = lane >> 2, t = lane & 3;
+    // code words: column n0 + g (A rows 0..7) and n0 + g + 8 (rows 8..15); hk0 word t, hk1 word t
+    const uint8_t* cw = st + (n0 + g) * 16 + 4 * t;
+    const uint32_t w00 = *reinterpret_cast<const uint32_t*>(cw);
+    const uint32_t w01 = *reinterpret_cast<const uint32_t*>(cw + 4096);
+    const uint32_t w10 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16);
+    const uint32_t w11 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16 + 4096);
+    // meta {scale pair, min pair} of k pairs 4t + s (hk0 word t) and 16 + 4t + s (hk1 word t)
+    const uint8_t* me = st + kGemmTileN * kGemmTileK / 2 + (n0 >> 6) * 256 + 32 * t;
+    const uint4 ma0 = *reinterpret_cast<const uint4*>(me);            // pairs 4t, 4t + 1
+    const uint4 ma1 = *reinterpret_cast<const uint4*>(me + 16);       // 4t + 2, 4t + 3
+    const uint4 mb0 = *reinterpret_cast<const uint4*>(me + 128);      // 16 + 4t, ..
+    const uint4 mb1 = *reinterpret_cast<const uint4*>(me + 144);
+    const uint32_t slo[4] = {ma0.x, ma0.z, ma1.x, ma1.z}, mlo[4] = {ma0.y, ma0.w, ma1.y, ma1.w};
+    const uint32_t shi[4] = {mb0.x, mb0.z, mb1.x, mb1.z}, mhi[4] = {mb0.y, mb0.w, mb1.y, mb1.w};
+    // x: row 8 mb + g, k 8t .. 8t+7 (b0 of steps 0..3) and 32 + 8t .. (b1)
+    uint4 xa[MB], xb[MB];
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+        const uint8_t* xr = st + kXOff + (8 * mb + g) * 128 + 16 * t;
+        xa[mb] = *reinterpret_cast<const uint4*>(xr);
+        xb[mb] = *reinterpret_cast<const uint4*>(xr + 64);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const uint32_t a0 = deq_pair<CLAMP>(w00 >> (4 * s), slo[s], mlo[s]);
+        const uint32_t a1 = deq_pair<CLAMP>(w10 >> (4 * s), slo[s], mlo[s]);
+        const uint32_t a2 = deq_pair<CLAMP>(w01 >> (4 * s), shi[s], mhi[s]);
+        const uint32_t a3 = deq_pair<CLAMP>(w11 >> (4 * s), shi[s], mhi[s]);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const uint32_t b0 = s == 0 ? xa[mb].x : s == 1 ? xa[mb].y : s == 2 ? xa[mb].z : xa[mb].w;
+            const uint32_t b1 = s == 0 ? xb[mb].x : s == 1 ? xb[mb].y : s == 2 ? xb[mb].z : xb[mb].w;
+            mma_f16(acc[s][mb], a0, a1, a2, a3, b0, b1);
+        }
+    }
+}
+
+// y (fp16) of the lane's fragment values: v[mb] = (column col0 + n0 + g, rows 8 mb + 2t, +1) and
+// (column + 8, same rows)
+template <int MB>
+__device__ __forceinline__ void store_y(const GemvParams& p, int col0, int n0, int lane, const float (&v)[MB][4]) {
+    const int g = lane >> 2, t = lane & 3;
+    const int col = col0 + n0 + g;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+        const int m = 8 * mb + 2 * t;
+        if (m < p.M) {
+            p.y[int64_t(m) * p.N + col] = __float2half_rn(v[mb][0]);
+            p.y[int64_t(m) * p.N + col + 8] = __float2half_rn(v[mb][2]);
+        }
+        if (m + 1 < p.M) {
+            p.y[int64_t(m + 1) * p.N + col] = __float2half_rn(v[mb][1]);
+            p.y[int64_t(m + 1) * p.N + col + 8] = __float2half_rn(v[mb][3]);
+        }
+    }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(kThreadsV, 1)
+dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesV * kStageBytes);
+    uint64_t* empty = full + kStagesV;
+    uint32_t* flag = reinterpret_cast<uint32_t*>(empty + kStagesV);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x;
+    const int64_t i0 = range_start(p.total, c, p.G), i1 = range_start(p.total, c + 1, p.G);
+    const int n = int(i1 - i0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesV; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp >= kConsumers) {
+        // ---------------- producers: warp kConsumers + r issues stages j = r, r + 4, ... (lane 0)
+        if (lane == 0) {
+            const int r = warp - kConsumers;
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+            const uint64_t pol_w = policy_fractional(false), pol_x = policy_fractional(true);
+            const uint8_t* flags = p.panels + p.total * kPanelData;
+            const uint32_t bytes = uint32_t(kPanelData + 16 + p.M * 128);
+            int64_t i = i0 + r;
+            int kb = int(i % p.KB);
+            for (int j = r; j < n; j += kProducers, i += kProducers) {
+                const int s = j % kStagesV;
+                mbar_wait(empty + s, ((j / kStagesV) & 1) ^ 1);
+                const uint32_t dst = su32(smem + s * kStageBytes);
+                mbar_expect_tx(full + s, bytes);
+                bulk_g2s(dst, p.panels + i * kPanelData, kPanelData, full + s, pol_w);
+                bulk_g2s(dst + kFlagOff, flags + i * 16, 16, full + s, pol_w);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                    " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst + kXOff),
+                    "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kGemmTileK), "r"(0), "r"(su32(full + s)),
+                    "l"(pol_x)
+                    : "memory");
+                kb += kProducers;
+                while (kb >= p.KB) kb -= p.KB;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warp owns columns n0 .. n0 + 15 of the tile
+    const int n0 = warp * 16;
+    const int t = lane & 3, g = lane >> 2;
+    float acc[4][MB][4];
+    int j = 0;
+    int64_t i = i0;
+    const int64_t first_tile = i0 / p.KB;
+    while (i < i1) {
+        const int64_t tile = i / p.KB;
+        const int64_t seg_end = min(i1, (tile + 1) * p.KB);
+        const bool whole = (i == tile * p.KB) && (seg_end == (tile + 1) * p.KB);
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) acc[s][mb][0] = acc[s][mb][1] = acc[s][mb][2] = acc[s][mb][3] = 0.0f;
+        for (; i < seg_end; ++i, ++j) {
+            const int s = j % kStagesV;
+            mbar_wait(full + s, (j / kStagesV) & 1);
+            const uint8_t* st = smem + s * kStageBytes;
+            if (*reinterpret_cast<const uint32_t*>(st + kFlagOff)) stage_math<MB, true>(st, n0, lane, acc);
+            else stage_math<MB, false>(st, n0, lane, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        float v[MB][4];   // the four step accumulators, summed in a fixed order
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) v[mb][r] = (acc[0][mb][r] + acc[1][mb][r]) + (acc[2][mb][r] + acc[3][mb][r]);
+        const int col0 = int(tile) * kGemmTileN;
+        if (whole) {
+            store_y<MB>(p, col0, n0, lane, v);
+            continue;
+        }
+        // a split tile: partial [256 n][16 m] in this CTA's slot (0: its first tile, 1: its last)
+        const int slot = tile == first_tile ? 0 : 1;
+        float* part = p.partials + (int64_t(c) * 2 + slot) * kGemmTileN * 16;
+        const int cl0 = n0 + g;
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+            const int m = 8 * mb + 2 * t;
+            __stcg(reinterpret_cast<float2*>(part + cl0 * 16 + m), make_float2(v[mb][0], v[mb][1]));
+            __stcg(reinterpret_cast<float2*>(part + (cl0 + 8) * 16 + m), make_float2(v[mb][2], v[mb][3]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+        const int cf = owner(p.total, p.G, tile * p.KB), cl = owner(p.total, p.G, (tile + 1) * p.KB - 1);
+        if (threadIdx.x == 0) {
+            const uint32_t old = atomicAdd(p.tickets + tile, 1u);
+            const bool last = old == uint32_t(cl - cf);
+            if (last) p.tickets[tile] = 0u;
+            *flag = last ? 1u : 0u;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+        if (*flag) {
+            __threadfence();
+            float y[MB][4];
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) y[mb][0] = y[mb][1] = y[mb][2] = y[mb][3] = 0.0f;
+            for (int cc = cf; cc <= cl; ++cc) {   // contributors in CTA order: deterministic
+                const int sl = (tile == range_start(p.total, cc, p.G) / p.KB) ? 0 : 1;
+                const float* pp = p.partials + (int64_t(cc) * 2 + sl) * kGemmTileN * 16;
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    const int m = 8 * mb + 2 * t;
+                    const float2 a = __ldcg(reinterpret_cast<const float2*>(pp + cl0 * 16 + m));
+                    const float2 b = __ldcg(reinterpret_cast<const float2*>(pp + (cl0 + 8) * 16 + m));
+                    y[mb][0] += a.x;
+                    y[mb][1] += a.y;
+                    y[mb][2] += b.x;
+                    y[mb][3] += b.y;
+                }
+            }
+            store_y<MB>(p, col0, n0, lane, y);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");   // *flag reuse
+    }
+}
+
+}  // namespace
+
+size_t dequant_gemv_workspace_bytes(int64_t n) {
+    const size_t tickets = size_t((n / kGemmTileN * 4 + 255) / 256 * 256);
+    return tickets + size_t(kGemmMaxGrid) * 2 * kGemmTileN * 16 * sizeof(float);
+}
+
+cudaError_t launch_dequant_gemv(const void* x, const void* panels, int64_t M, int64_t K, int64_t N, void* y,
+                                void* workspace, cudaStream_t stream) {
+    const int KB = int(K / kGemmTileK);
+    const int64_t total = (N / kGemmTileN) * KB;
+    const int sms = device_sm_count();
+    const int G = int(total < sms ? total : (sms < kGemmMaxGrid ? sms : kGemmMaxGrid));
+    {   // the shared-memory attribute, once per device (under a lock)
+        static cudaError_t attr_err[kMaxDevices];
+        static std::once_flag attr_once[kMaxDevices];
+        const int dev = current_device();
+        std::call_once(attr_once[dev], [dev] {
+            cudaError_t e = cudaFuncSetAttribute(dequant_gemv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kSmemV);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(dequant_gemv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV);
+            attr_err[dev] = e;
+        });
+        if (attr_err[dev] != cudaSuccess) return attr_err[dev];
+    }
+    GemvParams p;
+    p.panels = static_cast<const uint8_t*>(panels);
+    p.y = static_cast<__half*>(y);
+    p.tickets = static_cast<uint32_t*>(workspace);
+    p.partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) +
+                                          (N / kGemmTileN * 4 + 255) / 256 * 256);
+    p.M = int(M);
+    p.N = int(N);
+    p.KB = KB;
+    p.total = total;
+    p.G = G;
+    CUtensorMap mx;   // x [M][K] fp16, box 64 k x M rows, rows 128 B apart in the stage
+    if (!make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, uint64_t(K), uint64_t(M), uint64_t(K * 2),
+                  uint32_t(kGemmTileK), uint32_t(M), CU_TENSOR_MAP_SWIZZLE_NONE))
+        return cudaErrorInvalidValue;
+    if (M <= 8) dequant_gemv_kernel<1><<<G, kThreadsV, kSmemV, stream>>>(mx, p);
+    else dequant_gemv_kernel<2><<<G, kThreadsV, kSmemV, stream>>>(mx, p);
+    return cudaGetLastError();
+}
+
+}  // namespace flexq

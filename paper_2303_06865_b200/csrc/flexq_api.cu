@@ -29,12 +29,20 @@ flexq_status check_kv_dims(int batch, int heads, int head_dim, int prompt_len, i
     return FLEXQ_OK;
 }
 
-// b = 4, g = 64 runs the tensor-core kernels; the other built (b, g) the variant kernels
+// b = 4, g = 64 in the dense layout runs the tensor-core kernels; the other built (b, g),
+// and (4, 64) in the token-major layout, the CUDA-core variant kernels over token-major rows
 bool is_variant(int bits, int group_size) { return bits != flexq::kBits || group_size != flexq::kGroup; }
+bool token_major(int bits, int group_size, int kv_layout) {
+    return is_variant(bits, group_size) || kv_layout == FLEXQ_KV_TOKEN_MAJOR;
+}
+bool layout_ok(int kv_layout) { return kv_layout == FLEXQ_KV_DENSE || kv_layout == FLEXQ_KV_TOKEN_MAJOR; }
 
-size_t attn_ws_bytes(int batch, int heads, int head_dim, int t_cap, int bits, int group_size) {
-    return is_variant(bits, group_size) ? flexq::attention_variant_workspace_bytes(batch, heads, head_dim, t_cap)
-                                        : flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap);
+size_t attn_ws_bytes(int batch, int heads, int head_dim, int t_cap, int bits, int group_size, int kv_layout) {
+    const size_t var = flexq::attention_variant_workspace_bytes(batch, heads, head_dim, t_cap);
+    const size_t dense = flexq::attention_workspace_bytes(batch, heads, head_dim, t_cap);
+    if (is_variant(bits, group_size)) return var;
+    // (4, 64) token-major: the variant attention kernel, or Top-K (the dense kernel's workspace)
+    return kv_layout == FLEXQ_KV_TOKEN_MAJOR ? (var > dense ? var : dense) : dense;
 }
 
 flexq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? FLEXQ_OK : FLEXQ_ERR_CUDA; }
@@ -107,9 +115,9 @@ flexq_status flexq_kv_cache_bytes(int batch, int heads, int head_dim, int prompt
 
 flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int batch, int heads,
                              int head_dim, int prompt_len, int gen_len, int pos, int n_new, int bits,
-                             int group_size, void* k_cache, void* v_cache, void* stream) {
+                             int group_size, int kv_layout, void* k_cache, void* v_cache, void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
-    if (s == FLEXQ_ERR_ARG) return s;
+    if (s == FLEXQ_ERR_ARG || !layout_ok(kv_layout)) return FLEXQ_ERR_ARG;
     const int64_t t_cap = int64_t(prompt_len) + gen_len;
     if (pos < 0 || n_new < 1 || int64_t(pos) + n_new > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
@@ -120,34 +128,36 @@ flexq_status flexq_append_kv(const void* k_new_f16, const void* v_new_f16, int b
     if (rows * (head_dim / group_size) >= (int64_t(1) << 31)) return FLEXQ_ERR_ARG;   // < 2^31 groups
     const flexq::KvDst d{n_new, pos, flexq::kv_token_stride(t_cap) / flexq::kChunk};
     return from_cuda(flexq::launch_append_kv(k_new_f16, v_new_f16, rows, head_dim, bits, group_size, k_cache, v_cache, d,
-                                             static_cast<cudaStream_t>(stream)));
+                                             static_cast<cudaStream_t>(stream),
+                                             kv_layout == FLEXQ_KV_TOKEN_MAJOR));
 }
 
 size_t flexq_decode_attention_workspace_size(int batch, int heads, int head_dim, int prompt_len,
-                                             int gen_len, int bits, int group_size) {
+                                             int gen_len, int bits, int group_size, int kv_layout) {
     if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
-    return attn_ws_bytes(batch, heads, head_dim, prompt_len + gen_len, bits, group_size);
+    if (!layout_ok(kv_layout)) return 0;
+    return attn_ws_bytes(batch, heads, head_dim, prompt_len + gen_len, bits, group_size, kv_layout);
 }
 
 flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, const void* v_cache, int batch,
                                     int heads,
                                     int head_dim, int prompt_len, int gen_len, int cur_len, int bits,
-                                    int group_size, void* out_f16, void* workspace,
+                                    int group_size, int kv_layout, void* out_f16, void* workspace,
                                     size_t workspace_bytes, void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
-    if (s == FLEXQ_ERR_ARG) return s;
+    if (s == FLEXQ_ERR_ARG || !layout_ok(kv_layout)) return FLEXQ_ERR_ARG;
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
     if (!q_f16 || !k_cache || !v_cache || !out_f16) return FLEXQ_ERR_NULL;
     if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
+    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size, kv_layout))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap};
-    if (is_variant(bits, group_size))
+    if (token_major(bits, group_size, kv_layout))
         return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
     if (cur_len > flexq::kDenseMaxTokens) return FLEXQ_ERR_UNSUPPORTED;
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
@@ -156,10 +166,10 @@ flexq_status flexq_decode_attention(const void* q_f16, const void* k_cache, cons
 flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_f16, const void* v_new_f16,
                                            void* k_cache, void* v_cache, int batch, int heads, int head_dim,
                                            int prompt_len, int gen_len, int cur_len, int bits, int group_size,
-                                           void* out_f16, void* workspace, size_t workspace_bytes,
+                                           int kv_layout, void* out_f16, void* workspace, size_t workspace_bytes,
                                            void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
-    if (s == FLEXQ_ERR_ARG) return s;
+    if (s == FLEXQ_ERR_ARG || !layout_ok(kv_layout)) return FLEXQ_ERR_ARG;
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
@@ -167,15 +177,16 @@ flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_
     if (!aligned16(q_f16) || !aligned16(k_new_f16) || !aligned16(v_new_f16) || !aligned16(k_cache) ||
         !aligned16(v_cache) || !aligned16(out_f16))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
+    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size, kv_layout))
         return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::AttnArgs a{q_f16, k_cache, v_cache, out_f16, workspace, batch, heads, head_dim,
                       int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, t_cap, k_new_f16, v_new_f16};
-    if (is_variant(bits, group_size)) {   // variants: the append kernel, then the attention kernel
+    if (token_major(bits, group_size, kv_layout)) {   // token-major rows: the append kernel, then the attention kernel
         const flexq::KvDst d{1, cur_len - 1, a.chunks};
         cudaError_t e = flexq::launch_append_kv(k_new_f16, v_new_f16, int64_t(batch) * heads, head_dim, bits,
-                                                group_size, k_cache, v_cache, d, static_cast<cudaStream_t>(stream));
+                                                group_size, k_cache, v_cache, d, static_cast<cudaStream_t>(stream),
+                                                kv_layout == FLEXQ_KV_TOKEN_MAJOR);
         if (e != cudaSuccess) return FLEXQ_ERR_CUDA;
         a.k_new = a.v_new = nullptr;
         return from_cuda(flexq::launch_decode_attention_variant(a, bits, group_size, static_cast<cudaStream_t>(stream)));
@@ -184,12 +195,20 @@ flexq_status flexq_append_decode_attention(const void* q_f16, const void* k_new_
     return from_cuda(flexq::launch_decode_attention(a, static_cast<cudaStream_t>(stream)));
 }
 
+size_t flexq_decode_attention_topk_workspace_size(int batch, int heads, int head_dim, int prompt_len, int gen_len,
+                                                  int bits, int group_size, int kv_layout) {
+    if (check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size) != FLEXQ_OK) return 0;
+    if (!layout_ok(kv_layout) || is_variant(bits, group_size)) return 0;
+    return flexq::topk_workspace_bytes(batch, heads, prompt_len + gen_len);
+}
+
 flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache, const void* v_cache,
                                          int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                                         int cur_len, int keep, int bits, int group_size, void* out_f16,
-                                         void* sel_i32, void* workspace, size_t workspace_bytes, void* stream) {
+                                         int cur_len, int keep, int bits, int group_size, int kv_layout,
+                                         void* out_f16, void* sel_i32, void* workspace, size_t workspace_bytes,
+                                         void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
-    if (s == FLEXQ_ERR_ARG) return s;
+    if (s == FLEXQ_ERR_ARG || !layout_ok(kv_layout)) return FLEXQ_ERR_ARG;
     const int t_cap = prompt_len + gen_len;
     if (cur_len < 1 || cur_len > t_cap || keep < 1 || keep > cur_len) return FLEXQ_ERR_ARG;
     if (s != FLEXQ_OK) return s;
@@ -199,19 +218,20 @@ flexq_status flexq_decode_attention_topk(const void* q_f16, const void* k_cache,
     if (!aligned16(q_f16) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out_f16) ||
         (sel_i32 && !aligned16(sel_i32)))
         return FLEXQ_ERR_ALIGN;
-    if (!workspace || workspace_bytes < attn_ws_bytes(batch, heads, head_dim, t_cap, bits, group_size))
-        return FLEXQ_ERR_WORKSPACE;
+    if (!workspace || workspace_bytes < flexq::topk_workspace_bytes(batch, heads, t_cap)) return FLEXQ_ERR_WORKSPACE;
     if (!aligned16(workspace)) return FLEXQ_ERR_ALIGN;
     flexq::TopkArgs a{q_f16, k_cache, v_cache, out_f16, sel_i32, workspace, batch, heads, head_dim,
-                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, keep};
+                      int(flexq::kv_token_stride(t_cap) / flexq::kChunk), cur_len, keep,
+                      kv_layout == FLEXQ_KV_TOKEN_MAJOR ? 1 : 0};
     return from_cuda(flexq::launch_decode_attention_topk(a, static_cast<cudaStream_t>(stream)));
 }
 
 static flexq_status kv_interop(bool import_, void* k_codes, void* k_meta, void* v_codes, void* v_meta, int batch,
                                int heads, int head_dim, int prompt_len, int gen_len, int plain_tokens, int t0,
-                               int n_tok, int bits, int group_size, void* k_cache, void* v_cache, void* stream) {
+                               int n_tok, int bits, int group_size, int kv_layout, void* k_cache, void* v_cache,
+                               void* stream) {
     flexq_status s = check_kv_dims(batch, heads, head_dim, prompt_len, gen_len, bits, group_size);
-    if (s == FLEXQ_ERR_ARG) return s;
+    if (s == FLEXQ_ERR_ARG || !layout_ok(kv_layout)) return FLEXQ_ERR_ARG;
     const int64_t t_cap = int64_t(prompt_len) + gen_len;
     if (plain_tokens < 1 || t0 < 0 || n_tok < 0 || int64_t(t0) + n_tok > t_cap || t0 + n_tok > plain_tokens)
         return FLEXQ_ERR_ARG;
@@ -223,25 +243,25 @@ static flexq_status kv_interop(bool import_, void* k_codes, void* k_meta, void* 
         return FLEXQ_ERR_ALIGN;
     flexq::KvInterop x{k_codes, k_meta, v_codes, v_meta, k_cache, v_cache, int64_t(batch) * heads,
                        flexq::kv_token_stride(t_cap) / flexq::kChunk, plain_tokens, t0, n_tok, head_dim, bits,
-                       group_size};
+                       group_size, kv_layout == FLEXQ_KV_TOKEN_MAJOR ? 1 : 0};
     return from_cuda(flexq::launch_kv_interop(import_, x, static_cast<cudaStream_t>(stream)));
 }
 
 flexq_status flexq_kv_import(const void* k_codes_u8, const void* k_meta_h2, const void* v_codes_u8,
                              const void* v_meta_h2, int batch, int heads, int head_dim, int prompt_len, int gen_len,
-                             int plain_tokens, int t0, int n_tok, int bits, int group_size, void* k_cache,
-                             void* v_cache, void* stream) {
+                             int plain_tokens, int t0, int n_tok, int bits, int group_size, int kv_layout,
+                             void* k_cache, void* v_cache, void* stream) {
     return kv_interop(true, const_cast<void*>(k_codes_u8), const_cast<void*>(k_meta_h2), const_cast<void*>(v_codes_u8),
                       const_cast<void*>(v_meta_h2), batch, heads, head_dim, prompt_len, gen_len, plain_tokens, t0,
-                      n_tok, bits, group_size, k_cache, v_cache, stream);
+                      n_tok, bits, group_size, kv_layout, k_cache, v_cache, stream);
 }
 
 flexq_status flexq_kv_export(const void* k_cache, const void* v_cache, int batch, int heads, int head_dim,
                              int prompt_len, int gen_len, int plain_tokens, int t0, int n_tok, int bits,
-                             int group_size, void* k_codes_u8, void* k_meta_h2, void* v_codes_u8, void* v_meta_h2,
-                             void* stream) {
+                             int group_size, int kv_layout, void* k_codes_u8, void* k_meta_h2, void* v_codes_u8,
+                             void* v_meta_h2, void* stream) {
     return kv_interop(false, k_codes_u8, k_meta_h2, v_codes_u8, v_meta_h2, batch, heads, head_dim, prompt_len,
-                      gen_len, plain_tokens, t0, n_tok, bits, group_size, const_cast<void*>(k_cache),
+                      gen_len, plain_tokens, t0, n_tok, bits, group_size, kv_layout, const_cast<void*>(k_cache),
                       const_cast<void*>(v_cache), stream);
 }
 

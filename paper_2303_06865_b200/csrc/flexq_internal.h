@@ -1,6 +1,7 @@
 // flexq_internal.h -- launchers shared between the C-ABI layer and the kernels.
 // Internal to paper_2303_06865_b200/csrc (the oracle shares nothing with it).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -38,8 +39,9 @@ inline bool quant_variant_built(int bits, int group) {
 }
 cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits, int group, void* codes, void* meta,
                             cudaStream_t stream);
+// v_tm: the (4, 64) cache's V rows token-major (FLEXQ_KV_TOKEN_MAJOR) instead of quad-interleaved
 cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, int bits, int group,
-                             void* k_cache, void* v_cache, KvDst dst, cudaStream_t stream);
+                             void* k_cache, void* v_cache, KvDst dst, cudaStream_t stream, bool v_tm = false);
 cudaError_t launch_dequantize(const void* codes, const void* meta, int64_t rows, int64_t cols, int bits, int group,
                               void* out, cudaStream_t stream);
 
@@ -54,6 +56,7 @@ struct KvInterop {
     int64_t rows;         // batch * heads
     int64_t chunks;       // chunks per (b, h)
     int plain_tokens, t0, n, head_dim, bits, group;
+    int v_tm = 0;         // 1: the (4, 64) cache's V rows are token-major (FLEXQ_KV_TOKEN_MAJOR)
 };
 cudaError_t launch_kv_interop(bool import_, const KvInterop& x, cudaStream_t stream);
 
@@ -79,8 +82,9 @@ constexpr int kVarTile = 128;
 size_t attention_variant_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
 cudaError_t launch_decode_attention_variant(const AttnArgs& a, int bits, int group, cudaStream_t stream);
 
-// Top-K sparse attention: one warp per (b, h), so the context is
-// bounded by the per-warp score buffer.
+// Top-K sparse attention, two launches: a select kernel (one warp per (b, h), so
+// the context is bounded by the per-warp score buffer) writes each head's kept list, a gather
+// kernel reads only the kept V rows.
 constexpr int kTopkMaxTokens = 1152;
 struct TopkArgs {
     const void* q;
@@ -88,9 +92,11 @@ struct TopkArgs {
     const void* v_cache;
     void* out;
     void* sel;          // optional int32 [batch*heads][keep]
-    void* workspace;    // scheduler counters (same workspace as the dense kernel)
+    void* workspace;    // topk_workspace_bytes: 2 KB of scheduler counters, then the kept lists
     int batch, heads, head_dim, chunks, cur_len, keep;
+    int v_tm = 0;       // 1: V rows token-major (FLEXQ_KV_TOKEN_MAJOR): one contiguous row per kept token
 };
+size_t topk_workspace_bytes(int batch, int heads, int t_cap);
 cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream);
 
 // Decode linear layer over a 4-bit weight (NEXT-2, dequant_gemm.cu): y [M][N] = x [M][K] . w^ [K][N].
@@ -106,6 +112,16 @@ cudaError_t launch_pack_weight(const void* codes, const void* meta, int64_t k, i
                                cudaStream_t stream);
 size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n);
 cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t m, int64_t k, int64_t n, void* y,
+                                void* workspace, cudaStream_t stream);
+// Small batches (m <= kGemvMaxRows) take the HBM-streaming kernel over the same panels
+// (dequant_gemv.cu: CUDA-core dequant + mma.sync, stream-K over panels).
+constexpr int kGemvMaxRows = 16;
+size_t dequant_gemv_workspace_bytes(int64_t n);
+// 2-D TMA descriptor (dequant_gemm.cu; the driver entry point is looked up once)
+bool make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0, uint64_t d1,
+              uint64_t stride1_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
+              CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+cudaError_t launch_dequant_gemv(const void* x, const void* panels, int64_t m, int64_t k, int64_t n, void* y,
                                 void* workspace, cudaStream_t stream);
 
 }  // namespace flexq

@@ -95,7 +95,7 @@ cudaError_t launch_kv_interop(bool import_, const KvInterop& x, cudaStream_t str
     a.n = x.n;
     a.cb = x.head_dim * x.bits / 8;
     a.mb = 4 * x.head_dim / x.group;
-    a.swz = x.bits == kBits && x.group == kGroup;
+    a.swz = x.bits == kBits && x.group == kGroup && !x.v_tm;   // only the dense (4, 64) V is quad-swizzled
     const int64_t warps = a.rows * a.n;
     const int64_t blocks = (warps * 32 + 255) / 256;
     if (blocks > INT32_MAX) return cudaErrorInvalidValue;

@@ -67,8 +67,9 @@ struct KvChunkDst {
     FastDiv nnew;   // divisor n_new
     int gpr_log2;   // log2(groups per row) (head_dim / 64 = 1 or 2)
     int cb;         // code bytes per token (D/2)
-    // codes_off: K -> byte offset of the token's codes of group k (token-major rows);
-    //            V -> byte offset of the first column-pair word of group k in the token's
+    int v_tm;       // 1: V token-major like K (FLEXQ_KV_TOKEN_MAJOR); 0: V quad-interleaved (FLEXQ_KV_DENSE)
+    // codes_off: K (and token-major V) -> byte offset of the token's codes of group k;
+    //            quad V -> byte offset of the first column-pair word of group k in the token's
     //               quad, plus the token's byte lane (t % 4)   (include/flexq.h layout).
     __device__ __forceinline__ void operator()(uint32_t g, uint32_t /*gpr*/, int kv, int64_t& codes_off,
                                                int64_t& meta_off) const {
@@ -79,7 +80,7 @@ struct KvChunkDst {
         const int slot = int(t & (kChunk - 1));
         const int mb = cb / 8;                                            // meta bytes per token
         const int64_t base = chunk * (kChunk * (cb + mb));                // kv_chunk_bytes(2 cb)
-        if (kv == 0)
+        if (kv == 0 || v_tm)
             codes_off = base + slot * cb + k * (kGroup / 2);
         else   // word (quad, first pair of group k), plus the token's byte lane; + the quad's swizzle
             codes_off = (base + ((slot >> 2) * cb + k * (kGroup / 2)) * 4 + (slot & 3)) * 4 + ((slot >> 2) & 3);
@@ -87,7 +88,7 @@ struct KvChunkDst {
     }
     __device__ __forceinline__ void store_codes(uint8_t* base, int64_t co, int part, int kv, uint32_t lo,
                                                 uint32_t hi) const {
-        if (kv == 0) {
+        if (kv == 0 || v_tm) {
             *reinterpret_cast<uint2*>(base + co + part * 8) = make_uint2(lo, hi);
         } else {   // V: byte i (column pair part*8 + i of the group) -> word (quad, pair ^ (swz << 3)), byte t % 4
             const int swz = int(co & 3);   // V offsets carry the swizzle (quad & 3) in 2 low bits (operator())
@@ -551,7 +552,7 @@ cudaError_t launch_quantize(const void* x, int64_t rows, int64_t cols, int bits,
 }
 
 cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int head_dim, int bits, int group,
-                             void* k_cache, void* v_cache, KvDst d, cudaStream_t stream) {
+                             void* k_cache, void* v_cache, KvDst d, cudaStream_t stream, bool v_tm) {
     if (rows == 0) return cudaSuccess;
     if (bits != kBits || group != kGroup) {
 #define A_CALL(b, g) launch_append_kv_bg<b, g>(k, v, rows, head_dim, k_cache, v_cache, d, stream)
@@ -566,7 +567,7 @@ cudaError_t launch_append_kv(const void* k, const void* v, int64_t rows, int hea
     quantize_kernel<KvChunkDst><<<grid, kThreads, 0, stream>>>(
         static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<uint8_t*>(k_cache),
         static_cast<uint8_t*>(k_cache), static_cast<uint8_t*>(v_cache), static_cast<uint8_t*>(v_cache), rows,
-        head_dim, KvChunkDst{d, FastDiv::make(uint32_t(d.n_new)), head_dim == 128 ? 1 : 0, head_dim / 2});
+        head_dim, KvChunkDst{d, FastDiv::make(uint32_t(d.n_new)), head_dim == 128 ? 1 : 0, head_dim / 2, v_tm ? 1 : 0});
     return cudaGetLastError();
 }
 

@@ -21,6 +21,8 @@ HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))
 FLEXQ_OK, FLEXQ_ERR_NULL, FLEXQ_ERR_ARG, FLEXQ_ERR_ALIGN, FLEXQ_ERR_UNSUPPORTED, FLEXQ_ERR_WORKSPACE, \
     FLEXQ_ERR_CUDA = range(7)
 BITS, GROUP = 4, 64
+KV_DENSE, KV_TOKEN_MAJOR = 0, 1   # flexq_kv_layout (include/flexq.h)
+LAYOUTS = {"dense": KV_DENSE, "token_major": KV_TOKEN_MAJOR}
 
 
 class FlexqError(RuntimeError):
@@ -47,20 +49,22 @@ def lib():
         L.flexq_quantize.argtypes = [P, I64, I64, I, I, P, P, P]
         L.flexq_dequantize.argtypes = [P, P, I64, I64, I, I, P, P]
         L.flexq_kv_cache_bytes.argtypes = [I] * 7 + [ctypes.POINTER(SZ), ctypes.POINTER(I)]
-        L.flexq_append_kv.argtypes = [P, P] + [I] * 9 + [P, P, P]
-        L.flexq_decode_attention_workspace_size.argtypes = [I] * 7
+        L.flexq_append_kv.argtypes = [P, P] + [I] * 10 + [P, P, P]
+        L.flexq_decode_attention_workspace_size.argtypes = [I] * 8
         L.flexq_decode_attention_workspace_size.restype = SZ
-        L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 8 + [P, P, SZ, P]
-        L.flexq_decode_attention_topk.argtypes = [P, P, P] + [I] * 9 + [P, P, P, SZ, P]
-        L.flexq_append_decode_attention.argtypes = [P] * 5 + [I] * 8 + [P, P, SZ, P]
+        L.flexq_decode_attention_topk_workspace_size.argtypes = [I] * 8
+        L.flexq_decode_attention_topk_workspace_size.restype = SZ
+        L.flexq_decode_attention.argtypes = [P, P, P] + [I] * 9 + [P, P, SZ, P]
+        L.flexq_decode_attention_topk.argtypes = [P, P, P] + [I] * 10 + [P, P, P, SZ, P]
+        L.flexq_append_decode_attention.argtypes = [P] * 5 + [I] * 9 + [P, P, SZ, P]
         L.flexq_dequant_gemm_workspace_size.argtypes = [I64, I64, I64, I, I]
         L.flexq_dequant_gemm_workspace_size.restype = SZ
         L.flexq_dequant_gemm.argtypes = [P, P, I64, I64, I64, I, I, P, P, SZ, P]
         L.flexq_gemm_panel_bytes.argtypes = [I64, I64, I, I]
         L.flexq_gemm_panel_bytes.restype = SZ
         L.flexq_pack_weight.argtypes = [P, P, I64, I64, I, I, P, P]
-        L.flexq_kv_import.argtypes = [P] * 4 + [I] * 10 + [P, P, P]
-        L.flexq_kv_export.argtypes = [P, P] + [I] * 10 + [P] * 5
+        L.flexq_kv_import.argtypes = [P] * 4 + [I] * 11 + [P, P, P]
+        L.flexq_kv_export.argtypes = [P, P] + [I] * 11 + [P] * 5
         for f in ("flexq_quantize", "flexq_dequantize", "flexq_kv_cache_bytes", "flexq_append_kv",
                   "flexq_decode_attention", "flexq_decode_attention_topk", "flexq_append_decode_attention",
                   "flexq_dequant_gemm", "flexq_pack_weight", "flexq_kv_import", "flexq_kv_export"):
@@ -154,12 +158,17 @@ class KVCache:
     """One layer's compressed KV cache in the chunked layout of include/flexq.h:
     `k` and `v` are u8 [B][H][T_stride/32][32*(CB+MB)], chunk = [codes 32 x CB][meta 32 x MB], CB = D*bits/8,
     MB = 4*D/group (18*D per chunk at bits 4, group 64)
-    (K codes token-major, V codes quad-interleaved).
+    (K codes token-major; V codes quad-interleaved at (4, 64) in the default "dense" layout,
+    token-major like K in the "token_major" layout -- Top-K's -- and for the variants).
     The *_codes() / *_meta() accessors are layout views (copies) for tests and
     inspection, over tokens [0, T_stride)."""
 
     def __init__(self, batch: int, heads: int, head_dim: int, prompt_len: int, gen_len: int,
-                 device="cuda", bits: int = BITS, group_size: int = GROUP):
+                 device="cuda", bits: int = BITS, group_size: int = GROUP, layout: str = "dense"):
+        if layout not in LAYOUTS:
+            raise ValueError(f"layout must be one of {sorted(LAYOUTS)}")
+        self.layout = layout
+        self.kv_layout = LAYOUTS[layout]
         self.batch, self.heads, self.head_dim = batch, heads, head_dim
         self.prompt_len, self.gen_len = prompt_len, gen_len
         self.bits, self.group_size = bits, group_size
@@ -198,7 +207,7 @@ class KVCache:
         """V codes as token-major rows.  In memory each chunk's V codes are
         quad-interleaved and swizzled: word (quad, column pair i ^ ((quad & 3) << 3)) holds
         token 4 quad + k in byte k (include/flexq.h)."""
-        if self.variant():
+        if self.variant() or self.kv_layout == KV_TOKEN_MAJOR:
             return self._codes(self.v)
         B, H, NC, cb = self.batch, self.heads, self.chunks, self.head_dim // 2
         x = self.v[..., :CHUNK * cb].reshape(B, H, NC, CHUNK // 4, cb, 4)
@@ -237,8 +246,9 @@ def flexq_kv_import(cache: "KVCache", k_codes, k_meta, v_codes, v_meta, t0: int 
             raise ValueError(f"plain arrays must be on {dev}")
     with torch.cuda.device(dev):
         _check(lib().flexq_kv_import(_ptr(k_codes), _ptr(k_meta), _ptr(v_codes), _ptr(v_meta), cache.batch, cache.heads,
-                                 cache.head_dim, cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits,
-                                     cache.group_size, _ptr(cache.k), _ptr(cache.v), _stream(stream, dev)),
+                                     cache.head_dim, cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits,
+                                     cache.group_size, cache.kv_layout, _ptr(cache.k), _ptr(cache.v),
+                                     _stream(stream, dev)),
                "flexq_kv_import")
 
 
@@ -254,7 +264,8 @@ def flexq_kv_export(cache: "KVCache", t0: int = 0, n_tok=None, plain_tokens=None
     with torch.cuda.device(dev):
         _check(lib().flexq_kv_export(_ptr(cache.k), _ptr(cache.v), cache.batch, cache.heads, cache.head_dim,
                                      cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits, cache.group_size,
-                                     _ptr(kc), _ptr(km), _ptr(vc), _ptr(vm), _stream(stream, dev)), "flexq_kv_export")
+                                     cache.kv_layout, _ptr(kc), _ptr(km), _ptr(vc), _ptr(vm), _stream(stream, dev)),
+               "flexq_kv_export")
     return kc, km, vc, vm
 
 
@@ -278,19 +289,19 @@ def flexq_append_kv(k_new: torch.Tensor, v_new: torch.Tensor, cache: KVCache, po
     B, H, n_new, D = k_new.shape
     with torch.cuda.device(dev):
         _check(lib().flexq_append_kv(k_new.data_ptr(), v_new.data_ptr(), B, H, D, cache.prompt_len,
-                                     cache.gen_len, pos, n_new, cache.bits, cache.group_size,
+                                     cache.gen_len, pos, n_new, cache.bits, cache.group_size, cache.kv_layout,
                                      cache.k.data_ptr(), cache.v.data_ptr(), _stream(stream, dev)), "flexq_append_kv")
 
 
 def flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len, bits=BITS,
-                                          group_size=GROUP) -> int:
+                                          group_size=GROUP, kv_layout=KV_DENSE) -> int:
     return int(lib().flexq_decode_attention_workspace_size(batch, heads, head_dim, prompt_len, gen_len,
-                                                           bits, group_size))
+                                                           bits, group_size, kv_layout))
 
 
 def make_workspace(cache: KVCache) -> torch.Tensor:
     n = flexq_decode_attention_workspace_size(cache.batch, cache.heads, cache.head_dim, cache.prompt_len,
-                                              cache.gen_len, cache.bits, cache.group_size)
+                                              cache.gen_len, cache.bits, cache.group_size, cache.kv_layout)
     return torch.zeros(n, dtype=torch.uint8, device=cache.k.device)
 
 
@@ -308,7 +319,7 @@ def flexq_decode_attention(q: torch.Tensor, cache: KVCache, cur_len: int, out=No
     with torch.cuda.device(dev):
         _check(lib().flexq_decode_attention(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
                                             cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
-                                            cur_len, cache.bits, cache.group_size, out.data_ptr(),
+                                            cur_len, cache.bits, cache.group_size, cache.kv_layout, out.data_ptr(),
                                             workspace.data_ptr(), workspace.numel(), _stream(stream, dev)),
                "flexq_decode_attention")
     return out
@@ -335,7 +346,7 @@ def flexq_append_decode_attention(q: torch.Tensor, k_new: torch.Tensor, v_new: t
         _check(lib().flexq_append_decode_attention(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
                                                    cache.k.data_ptr(), cache.v.data_ptr(), cache.batch, cache.heads,
                                                    cache.head_dim, cache.prompt_len, cache.gen_len, cur_len,
-                                                   cache.bits, cache.group_size, out.data_ptr(),
+                                                   cache.bits, cache.group_size, cache.kv_layout, out.data_ptr(),
                                                    workspace.data_ptr(), workspace.numel(), _stream(stream, dev)),
                "flexq_append_decode_attention")
     return out
@@ -347,16 +358,25 @@ def topk_keep(cur_len: int, fraction: float = 0.1) -> int:
     return max(1, min(cur_len, math.ceil(fraction * cur_len - 1e-9)))
 
 
+def make_topk_workspace(cache: KVCache) -> torch.Tensor:
+    n = int(lib().flexq_decode_attention_topk_workspace_size(cache.batch, cache.heads, cache.head_dim,
+                                                             cache.prompt_len, cache.gen_len, cache.bits,
+                                                             cache.group_size, cache.kv_layout))
+    if n == 0:
+        raise FlexqError(FLEXQ_ERR_UNSUPPORTED, "flexq_decode_attention_topk_workspace_size")
+    return torch.zeros(n, dtype=torch.uint8, device=cache.k.device)
+
+
 def flexq_decode_attention_topk(q: torch.Tensor, cache: KVCache, cur_len: int, keep: int, out=None, sel=None,
                                 workspace=None, stream=None) -> torch.Tensor:
     """Top-K sparse decode attention.  sel: optional int32 [B][H][keep] output
-    receiving the kept token indices (ascending)."""
+    receiving the kept token indices (ascending).  workspace: make_topk_workspace(cache)."""
     dev, shp = cache.k.device, (cache.batch, cache.heads, cache.head_dim)
     _need(q, torch.float16, "q", shp, dev)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
-        workspace = make_workspace(cache)
+        workspace = make_topk_workspace(cache)
     _need(out, torch.float16, "out", shp, dev)
     _need(workspace, torch.uint8, "workspace", device=dev)
     if sel is not None:
@@ -364,7 +384,8 @@ def flexq_decode_attention_topk(q: torch.Tensor, cache: KVCache, cur_len: int, k
     with torch.cuda.device(dev):
         _check(lib().flexq_decode_attention_topk(q.data_ptr(), cache.k.data_ptr(), cache.v.data_ptr(), cache.batch,
                                                  cache.heads, cache.head_dim, cache.prompt_len, cache.gen_len,
-                                                 cur_len, keep, cache.bits, cache.group_size, out.data_ptr(),
+                                                 cur_len, keep, cache.bits, cache.group_size, cache.kv_layout,
+                                                 out.data_ptr(),
                                                  _ptr(sel), workspace.data_ptr(), workspace.numel(),
                                                  _stream(stream, dev)),
                "flexq_decode_attention_topk")

@@ -6,7 +6,7 @@ Covers: quantize/dequantize with a ragged row count (and the b/g variants),
 prompt fill + 1-token append, attention with split-K (few heads) and without,
 Top-K, the fused append + attention, a cache whose capacity is not a multiple
 of the token stride (cur_len = T_cap, last head: the metadata bulk copy rounds
-up into the stride padding), the KV-cache variants, weight packing and the tcgen05 dequant-GEMM.
+up into the stride padding), the KV-cache variants, weight packing, the tcgen05 dequant-GEMM and the small-batch dequant-GEMV.
 """
 import os
 import sys
@@ -39,7 +39,12 @@ def main():
         for cur in (1, s, s + n):
             fq.flexq_decode_attention(q, cache, cur, workspace=ws)
         # NEXT-1 Top-K and NEXT-3 fused append + attention on the same cache
-        fq.flexq_decode_attention_topk(q, cache, s, keep=fq.topk_keep(s), workspace=ws)
+        fq.flexq_decode_attention_topk(q, cache, s, keep=fq.topk_keep(s))
+        # the token-major layout (Top-K's): append, Top-K gather of contiguous rows, dense attention
+        tm = fq.KVCache(B, H, D, s, n, device=dev, layout="token_major")
+        fq.flexq_append_kv(k, v, tm, pos=0)
+        fq.flexq_decode_attention_topk(q, tm, s, keep=fq.topk_keep(s))
+        fq.flexq_append_decode_attention(q, q, q, tm, s + n)
         fq.flexq_append_decode_attention(q, q, q, cache, s + n, workspace=ws)
         # interop: export the cache to the plain layout, import a token range back
         kc, km, vc, vm = fq.flexq_kv_export(cache)
@@ -64,7 +69,7 @@ def main():
     w = synth.fill(3, 1, (K, N), device=dev)
     c, m = fq.flexq_quantize(w)
     panels = fq.flexq_pack_weight(c, m)
-    for M in (20, 170):
+    for M in (5, 12, 20, 170):   # 5, 12: the small-batch panel-streaming kernel (8 panels, 8 CTAs)
         fq.flexq_dequant_gemm(synth.fill(3, 2 + M, (M, K), device=dev), panels, N)
     torch.cuda.synchronize()
     print("sanitize case ok")

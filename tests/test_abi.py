@@ -26,7 +26,7 @@ def test_exports_every_header_symbol(L):
 
 
 def test_version_and_status_strings(L):
-    assert L.flexq_abi_version() == 1
+    assert L.flexq_abi_version() == 2
     for s in range(-2, 10):
         assert L.flexq_status_string(s)            # never NULL
 
@@ -64,8 +64,8 @@ def test_dequantize_validation(L):
 def test_append_validation(L):
     f = L.flexq_append_kv
 
-    def call(B=2, H=3, D=128, s=8, n=4, pos=0, nn=1, bits=4, g=64, k=A, kv=A):
-        return f(k, A, B, H, D, s, n, pos, nn, bits, g, A, kv, None)
+    def call(B=2, H=3, D=128, s=8, n=4, pos=0, nn=1, bits=4, g=64, k=A, kv=A, lay=0):
+        return f(k, A, B, H, D, s, n, pos, nn, bits, g, lay, A, kv, None)
     assert call(B=0) == fq.FLEXQ_ERR_ARG
     assert call(pos=-1) == fq.FLEXQ_ERR_ARG
     assert call(pos=12) == fq.FLEXQ_ERR_ARG            # pos + n_new > s + n
@@ -80,16 +80,23 @@ def test_append_validation(L):
     assert call(k=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(lay=2) == fq.FLEXQ_ERR_ARG           # flexq_kv_layout: 0 dense, 1 token-major
+    assert call(lay=-1) == fq.FLEXQ_ERR_ARG
+    assert call(lay=1, k=None) == fq.FLEXQ_ERR_NULL
 
 
 def test_attention_validation(L):
     f = L.flexq_decode_attention
-    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64, 0)
     assert ws > 0
-    assert L.flexq_decode_attention_workspace_size(0, 3, 128, 8, 4, 4, 64) == 0
+    assert L.flexq_decode_attention_workspace_size(0, 3, 128, 8, 4, 4, 64, 0) == 0
+    assert L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64, 7) == 0   # no such layout
+    # (4, 64) token-major: the variant kernel's workspace or the dense one, whichever is larger
+    wt = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64, 1)
+    assert wt == max(ws, 256 + (6 * 1 * 130 * 4 + 15) // 16 * 16)
 
-    def call(cur=5, D=128, q=A, kv=A, out=A, w=A, wb=ws, g=64):
-        return f(q, A, kv, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
+    def call(cur=5, D=128, q=A, kv=A, out=A, w=A, wb=ws, g=64, lay=0):
+        return f(q, A, kv, 2, 3, D, 8, 4, cur, 4, g, lay, out, w, wb, None)
     assert call(cur=0) == fq.FLEXQ_ERR_ARG
     assert call(cur=13) == fq.FLEXQ_ERR_ARG             # cur_len > s + n
     assert call(D=32) == fq.FLEXQ_ERR_UNSUPPORTED
@@ -98,12 +105,15 @@ def test_attention_validation(L):
     assert call(q=None) == fq.FLEXQ_ERR_NULL
     assert call(kv=None) == fq.FLEXQ_ERR_NULL
     assert call(out=U) == fq.FLEXQ_ERR_ALIGN
+    assert call(lay=3) == fq.FLEXQ_ERR_ARG
+    assert call(lay=1, wb=wt - 1) == fq.FLEXQ_ERR_WORKSPACE
     # variants (NEXT-3): their own workspace size, 256 B + (D + 2) floats per (b, h, 128-token tile)
-    wv = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 3, 32)
+    wv = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 3, 32, 0)
     assert wv == 256 + (6 * 1 * 130 * 4 + 15) // 16 * 16
-    assert L.flexq_decode_attention_workspace_size(2, 3, 128, 300, 0, 8, 128) == 256 + 6 * 3 * 130 * 4
-    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 3, 32, A, A, wv - 1, None) == fq.FLEXQ_ERR_WORKSPACE
-    assert f(None, A, A, 2, 3, 128, 8, 4, 5, 3, 32, A, A, wv, None) == fq.FLEXQ_ERR_NULL
+    assert L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 3, 32, 1) == wv   # same layout
+    assert L.flexq_decode_attention_workspace_size(2, 3, 128, 300, 0, 8, 128, 0) == 256 + 6 * 3 * 130 * 4
+    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 3, 32, 0, A, A, wv - 1, None) == fq.FLEXQ_ERR_WORKSPACE
+    assert f(None, A, A, 2, 3, 128, 8, 4, 5, 3, 32, 0, A, A, wv, None) == fq.FLEXQ_ERR_NULL
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
     assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
 
@@ -129,28 +139,35 @@ def test_kv_cache_bytes(L):
 
 def test_topk_validation(L):
     f = L.flexq_decode_attention_topk
-    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+    L.flexq_decode_attention_topk_workspace_size.restype = ctypes.c_size_t
+    ws = L.flexq_decode_attention_topk_workspace_size(2, 3, 128, 8, 4, 4, 64, 1)
+    assert ws == 2048 + 2 * 3 * 12 * 8          # counters + (index, weight) per (b, h, token)
+    assert L.flexq_decode_attention_topk_workspace_size(2, 3, 128, 8, 4, 4, 64, 0) == ws
+    assert L.flexq_decode_attention_topk_workspace_size(2, 3, 128, 8, 4, 3, 32, 0) == 0   # b = 4, g = 64 only
 
-    def call(cur=5, keep=2, D=128, q=A, out=A, sel=None, w=A, s=8, n=4):
-        return f(q, A, A, 2, 3, D, s, n, cur, keep, 4, 64, out, sel, w, ws, None)
+    def call(cur=5, keep=2, D=128, q=A, out=A, sel=None, w=A, s=8, n=4, lay=1):
+        return f(q, A, A, 2, 3, D, s, n, cur, keep, 4, 64, lay, out, sel, w, ws, None)
     assert call(keep=0) == fq.FLEXQ_ERR_ARG
     assert call(keep=6) == fq.FLEXQ_ERR_ARG          # keep > cur_len
     assert call(cur=13) == fq.FLEXQ_ERR_ARG
     assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
     assert call(cur=1153, keep=5, s=1200, n=0) == fq.FLEXQ_ERR_UNSUPPORTED   # beyond the score buffer
-    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 2, 3, 32, A, None, A, ws, None) == fq.FLEXQ_ERR_UNSUPPORTED   # b = 4, g = 64 only
+    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 2, 3, 32, 0, A, None, A, ws, None) == fq.FLEXQ_ERR_UNSUPPORTED   # b = 4, g = 64 only
+    assert call(lay=2) == fq.FLEXQ_ERR_ARG
+    assert call(lay=0, q=None) == fq.FLEXQ_ERR_NULL    # the dense layout is accepted too
     assert call(q=None) == fq.FLEXQ_ERR_NULL
     assert call(sel=U) == fq.FLEXQ_ERR_ALIGN
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
+    assert f(A, A, A, 2, 3, 128, 8, 4, 5, 2, 4, 64, 1, A, None, A, ws - 1, None) == fq.FLEXQ_ERR_WORKSPACE
     assert fq.topk_keep(543) == 55 and fq.topk_keep(130) == 13 and fq.topk_keep(5) == 1
 
 
 def test_append_attention_validation(L):
     f = L.flexq_append_decode_attention
-    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64)
+    ws = L.flexq_decode_attention_workspace_size(2, 3, 128, 8, 4, 4, 64, 0)
 
-    def call(cur=5, D=128, q=A, kn=A, vn=A, kv=A, out=A, w=A, wb=ws, g=64):
-        return f(q, kn, vn, kv, A, 2, 3, D, 8, 4, cur, 4, g, out, w, wb, None)
+    def call(cur=5, D=128, q=A, kn=A, vn=A, kv=A, out=A, w=A, wb=ws, g=64, lay=0):
+        return f(q, kn, vn, kv, A, 2, 3, D, 8, 4, cur, 4, g, lay, out, w, wb, None)
     assert call(cur=0) == fq.FLEXQ_ERR_ARG
     assert call(cur=13) == fq.FLEXQ_ERR_ARG
     assert call(D=96) == fq.FLEXQ_ERR_UNSUPPORTED
@@ -161,6 +178,7 @@ def test_append_attention_validation(L):
     assert call(vn=U) == fq.FLEXQ_ERR_ALIGN
     assert call(w=None) == fq.FLEXQ_ERR_WORKSPACE
     assert call(wb=ws - 1) == fq.FLEXQ_ERR_WORKSPACE
+    assert call(lay=5) == fq.FLEXQ_ERR_ARG
 
 
 def test_dequant_gemm_validation(L):

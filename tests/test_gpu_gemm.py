@@ -64,6 +64,12 @@ GEMM_CASES = [
     ("m256_two_row_chunks", 256, 128, 256),
     ("m300_two_row_chunks", 300, 256, 512),
     ("m16_remainder_split", 16, 256, 256 * 150),   # one full wave + 2 remainder tiles split 4 ways
+    # small batches (M <= 16) take the panel-streaming kernel (dequant_gemv.cu): stream-K ranges
+    # that start and end inside tiles, one- and two-block rows (M <= 8, 9..16)
+    ("m9_two_row_blocks", 9, 320, 768),
+    ("m1_stream_k_split", 1, 2048, 512),        # 64 panels < 148 CTAs: one panel per CTA
+    ("m3_ranges_cut_tiles", 3, 640, 256 * 160),  # 1600 panels over 148 CTAs: ranges cut tiles
+    ("m17_first_tcgen05_row", 17, 256, 512),
 ]
 
 
@@ -203,6 +209,27 @@ def test_opt175b_weight_full_size_sampled(orc, cuda, N):
         wb = synth.gather(seed, 10 + N // 12288, (K, N), [slice(None), slice(64 * b, 64 * b + 64)])
         oc, om = orc.quantize(wb.numpy(), 4, 64)
         check_gemm(y[:, 64 * b:64 * b + 64], x.numpy(), oc, om, orc, f"N={N} block {b}")
+
+
+@pytest.mark.parametrize("M", [1, 16])
+def test_small_batch_full_size_sampled(orc, cuda, M):
+    """Batch-1 / batch-16 decode (the panel-streaming kernel) on the OPT-175B w1 matrix
+    (12288 x 49152, BASELINE configs[4]); sampled 64-column blocks against the oracle."""
+    K, N = 12288, 49152
+    seed = synth.BASE_SEED + 5
+    w = synth.fill(seed, 12, (K, N), device=cuda)
+    codes, meta = fq.flexq_quantize(w)
+    del w
+    panels = fq.flexq_pack_weight(codes, meta)
+    del codes, meta
+    x = synth.fill(seed, 21 + M, (M, K))
+    y = fq.flexq_dequant_gemm(x.to(cuda), panels, N).cpu().numpy()
+    rng = np.random.default_rng(12 + M)
+    blocks = sorted({0, N // 64 - 1, *[int(b) for b in rng.integers(0, N // 64, size=3)]})
+    for b in blocks:
+        wb = synth.gather(seed, 12, (K, N), [slice(None), slice(64 * b, 64 * b + 64)])
+        oc, om = orc.quantize(wb.numpy(), 4, 64)
+        check_gemm(y[:, 64 * b:64 * b + 64], x.numpy(), oc, om, orc, f"M={M} block {b}")
 
 
 def test_pair_kernel_matches_single(cuda, tmp_path):

@@ -93,14 +93,14 @@ def test_append_kv_bit_exact(orc, cuda, D):
 
 
 # ---------------------------------------------------------------- attention
-def build_case(orc, cuda, B, H, D, s, n, n_steps, seed, outliers=False, qfactor=1):
+def build_case(orc, cuda, B, H, D, s, n, n_steps, seed, outliers=False, qfactor=1, layout="dense"):
     """Prompt fill + n_steps single-token appends on both sides; returns the
-    GPU cache, the oracle caches, q (fp16) and cur_len = s + n_steps."""
+    GPU cache (in `layout`), the oracle caches, q (fp16) and cur_len = s + n_steps."""
     k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, s, D))
     v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, s, D))
     if outliers:
         k, v = synth.with_outliers(k), synth.with_outliers(v)
-    cache = fq.KVCache(B, H, D, s, n, device=cuda)
+    cache = fq.KVCache(B, H, D, s, n, device=cuda, layout=layout)
     okc, ovc = orc.empty_cache(B, H, s + n, D), orc.empty_cache(B, H, s + n, D)
     if s > 0:
         fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
@@ -296,8 +296,9 @@ def test_full_size_fused_sampled(orc, cuda):
 
 
 # ---------------------------------------------------------------- NEXT-1: Top-K sparse attention
+@pytest.mark.parametrize("layout", ["dense", "token_major"])
 @pytest.mark.parametrize("D", [64, 128])
-def test_topk_exact_ties_bit_exact(orc, cuda, D):
+def test_topk_exact_ties_bit_exact(orc, cuda, D, layout):
     """Selection is index work: on exactly tied scores (K rows drawn from 3
     distinct rows, so identical codes + meta give identical scores on both sides) the GPU's
     kept set must equal the oracle's -- score descending, then lowest token index -- with zero
@@ -307,7 +308,7 @@ def test_topk_exact_ties_bit_exact(orc, cuda, D):
     cls = torch.stack([torch.arange(T) % 3, 2 - torch.arange(T) % 3, (torch.arange(T) // 7) % 3])
     k = torch.stack([torch.stack([base[b, h][cls[h]] for h in range(H)]) for b in range(B)])
     v = synth.fill(59, 2, (B, H, T, D))
-    cache = fq.KVCache(B, H, D, T, 1, device=cuda)
+    cache = fq.KVCache(B, H, D, T, 1, device=cuda, layout=layout)
     fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
     okc, ovc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
     orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
@@ -335,13 +336,20 @@ TOPK_CASES = [
 ]
 
 
+@pytest.mark.parametrize("layout", ["dense", "token_major"])
 @pytest.mark.parametrize("case", TOPK_CASES, ids=[c[0] for c in TOPK_CASES])
-def test_topk_attention_parity(orc, cuda, case):
+def test_topk_attention_parity(orc, cuda, case, layout):
     """The GPU's kept set must be a valid top-`keep` set of the oracle's scores
     (several sets are correct when scores tie within rounding), and the output
     must match the oracle evaluated on that set within reading Q's tolerance."""
     name, B, H, D, s, n, steps, outl, qf, frac = case
-    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, steps, seed=60, outliers=outl, qfactor=qf)
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, steps, seed=60, outliers=outl, qfactor=qf,
+                                         layout=layout)
+    if layout == "token_major":   # the cache bytes of the token-major layout: V rows like K rows
+        T = cur
+        assert np.array_equal(cache.v_codes()[:, :, :T].cpu().numpy(), orc.pack4(ovc[0][:, :, :T]))
+        assert np.array_equal(cache.v_meta()[:, :, :T].cpu().numpy().view(np.uint16), ovc[1][:, :, :T])
+        assert np.array_equal(cache.k_codes()[:, :, :T].cpu().numpy(), orc.pack4(okc[0][:, :, :T]))
     keep = fq.topk_keep(cur, frac) if frac > 0 else 1
     sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
     out = fq.flexq_decode_attention_topk(q.to(cuda), cache, cur, keep, sel=sel)
@@ -448,3 +456,37 @@ def test_attention_extreme_cache(orc, cuda, D):
     ref = orc.attention_f64(q.numpy(), okc, ovc, s + 1)
     assert_attn_close(out.cpu().numpy(), ref, f"extreme fused D={D}")
     assert np.array_equal(cache.k_codes()[:, :, :s + 1].cpu().numpy(), orc.pack4(okc[0][:, :, :s + 1]))
+
+
+# ---------------------------------------------------------------- the token-major (4, 64) layout
+@pytest.mark.parametrize("D", [64, 128])
+def test_token_major_layout(orc, cuda, D):
+    """FLEXQ_KV_TOKEN_MAJOR at (4, 64): V rows are laid out like K rows (byte-exact against the
+    oracle's append), dense decode attention over it (the CUDA-core kernel) and the one-call
+    decode step are within reading Q, and export / import move the same plain bytes as for the
+    dense layout."""
+    B, H, s, n = 2, 5, 200, 4
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, 2, seed=61, outliers=True, qfactor=4,
+                                         layout="token_major")
+    T = cur
+    assert np.array_equal(cache.k_codes()[:, :, :T].cpu().numpy(), orc.pack4(okc[0][:, :, :T]))
+    assert np.array_equal(cache.v_codes()[:, :, :T].cpu().numpy(), orc.pack4(ovc[0][:, :, :T]))
+    assert np.array_equal(cache.v_meta()[:, :, :T].cpu().numpy().view(np.uint16), ovc[1][:, :, :T])
+    # raw V bytes equal raw K-layout bytes of the same rows: token-major like K
+    vchunk = cache.v[..., :16 * D].reshape(B, H, -1, D // 2)      # each chunk's [codes 32 x D/2]
+    assert torch.equal(vchunk[:, :, :T].cpu(), cache.v_codes()[:, :, :T].cpu())
+    out = fq.flexq_decode_attention(q.to(cuda), cache, cur)
+    torch.cuda.synchronize()
+    assert_attn_close(out.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, cur), "token-major attention")
+    kn = synth.fill(61, 90, (B, H, 1, D))
+    vn = synth.fill(61, 91, (B, H, 1, D))
+    out2 = fq.flexq_append_decode_attention(q.to(cuda), kn[:, :, 0].to(cuda), vn[:, :, 0].to(cuda), cache, cur + 1)
+    orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, cur)
+    torch.cuda.synchronize()
+    assert_attn_close(out2.cpu().numpy(), orc.attention_f64(q.numpy(), okc, ovc, cur + 1), "token-major fused step")
+    assert np.array_equal(cache.v_codes()[:, :, :cur + 1].cpu().numpy(), orc.pack4(ovc[0][:, :, :cur + 1]))
+    # the same plain bytes leave both layouts
+    dense, _, _, _, _ = build_case(orc, cuda, B, H, D, s, n, 2, seed=61, outliers=True, qfactor=4)
+    fq.flexq_append_kv(kn.to(cuda), vn.to(cuda), dense, pos=cur)
+    for a, b in zip(fq.flexq_kv_export(cache, 0, cur + 1), fq.flexq_kv_export(dense, 0, cur + 1)):
+        assert torch.equal(a, b)
