@@ -363,6 +363,12 @@ class DecodeModel:
         fq, st = self.fq, self.stream
         L = self.L if layers is None else min(layers, self.L)
         keep = fq.topk_keep(cur)
+        if which == "topk_tm":           # build the token-major copies and the workspace outside the capture
+            for j in range(L):
+                self.tm_cache(j)
+        if which in ("topk", "topk_tm"):
+            self.topk_ws()
+        torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
             for j in range(L):

@@ -402,8 +402,12 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         __syncwarp();
         uint32_t done = 0;
         if (lane == 0) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            done = atomicAdd(&P.tickets[bh], uint32_t(len)) + uint32_t(len);
+            // release-add (MEMBAR, no L1 invalidation: a full fence.acq_rel here was the largest
+            // single stall of the small-batch launches, ncu); only the merging piece acquires
+            uint32_t old;
+            asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(&P.tickets[bh]), "r"(uint32_t(len))
+                         : "memory");
+            done = old + uint32_t(len);
             if (done == uint32_t(P.cur_len)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
         done = __shfl_sync(0xffffffffu, done, 0);
@@ -524,7 +528,8 @@ WsLayout ws_layout(int bh, int d) {
 //   FLEXQ_ATTN_SPLIT="<min heads per warp x 100 for all-ticket mode>,<tail heads per warp x 100>,<pieces per tail head>"
 //   FLEXQ_ATTN_HYBRID="<static share of the heads, %>,<chunks per ticket piece>"
 //   FLEXQ_ATTN_CTRS=<ticket counters, 1..16>
-constexpr int kDynHeadsPerWarpX100 = 150;   // B200 sweep: whole-head tickets win from ~1.5 heads per warp
+constexpr int kDynHeadsPerWarpX100 = 50;    // B200 sweep: whole-head tickets win from ~0.5 heads per warp
+                                            // (batch 18 / 36 shards of OPT-175B: 33 / 55 us vs 37.7 / 59.7 static)
 constexpr int kHybridStaticPct = 100;       // below that: static stream-K (the static-prefix + ticket-piece
                                             // hybrid measured slower at every share; tuning only)
 constexpr int kHybridPieceChunks = 3;
@@ -641,7 +646,18 @@ cudaError_t launch_ring(const AttnArgs& a, cudaStream_t stream) {
         const char* e = getenv("FLEXQ_ATTN_RING");
         return e ? atoi(e) : 0;
     }();
-    const int S = ring_env >= 2 && ring_env <= 4 ? ring_env : 2;
+    // default: S = 2 (16 warps per SM); S = 3 (11 warps per SM, two stages in flight) when the launch
+    // holds 1.2 - 2 heads per S = 2 warp -- the batch-36 shard of OPT-175B: 48 us vs 55 us (B200 sweep)
+    int S = 2;
+    if (ring_env >= 2 && ring_env <= 4) {
+        S = ring_env;
+    } else {
+        const int bh = a.batch * a.heads;
+        const int w2 = dev_info<D, MAXT, 2>().sms * dev_info<D, MAXT, 2>().occ;
+        if (int64_t(bh) * 10 >= int64_t(w2) * 12 && int64_t(bh) * 10 <= int64_t(w2) * 20 &&
+            (a.cur_len + kChunk - 1) / kChunk >= 4)
+            S = 3;
+    }
     if (S == 4) return launch<D, MAXT, 4>(a, stream);
     if (S == 3) return launch<D, MAXT, 3>(a, stream);
     return launch<D, MAXT, 2>(a, stream);

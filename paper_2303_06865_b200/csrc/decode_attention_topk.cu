@@ -29,6 +29,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "attn_common.cuh"
@@ -193,16 +195,19 @@ topk_select_kernel(const SelectParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    constexpr int PW = S * C::STG + 2 * D + MAXT * 6;   // per warp: ring, q, scores, kept list
+    // q is refilled at the next unit's first stage, S - 1 stages ahead: with S > 2 a unit of fewer
+    // than S stages could still be reading it, so deeper rings alternate two q areas
+    constexpr int NQ = S > 2 ? 2 : 1;
+    constexpr int PW = S * C::STG + NQ * 2 * D + MAXT * 6;   // per warp: ring, q, scores, kept list
     uint8_t* ring = smem + warp * PW;
-    uint8_t* qsm = ring + S * C::STG;
-    float* scores = reinterpret_cast<float*>(qsm + 2 * D);
-    uint16_t* kept = reinterpret_cast<uint16_t*>(qsm + 2 * D + MAXT * 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * (S + 1);   // + q's barrier
+    uint8_t* qsm0 = ring + S * C::STG;
+    float* scores = reinterpret_cast<float*>(qsm0 + NQ * 2 * D);
+    uint16_t* kept = reinterpret_cast<uint16_t*>(qsm0 + NQ * 2 * D + MAXT * 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * (S + NQ);   // + the q barriers
 
     const uint64_t policy = evict_first_policy();
     if (lane == 0) {
-        for (int s = 0; s <= S; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S + NQ; ++s) mbar_init(&bars[s], 1);
         fence_proxy_async();
     }
     __syncwarp();
@@ -210,9 +215,9 @@ topk_select_kernel(const SelectParams P) {
 
     // ---------------- producer: the K stages of whole (b, h) units (no split)
     const int nst = (P.cur_len + C::CH - 1) / C::CH;
-    int p_bh = -1, p_stage = 0;
+    int p_bh = -1, p_stage = 0, p_units = 0;
     const uint8_t* p_k = nullptr;
-    int fq0 = -1, fq1 = -1, fq2 = -1, fcount = 0;
+    int fq0 = -1, fq1 = -1, fq2 = -1, fq3 = -1, fcount = 0;
     auto next_unit = [&]() {
         int t = 0;
         if (lane == 0) t = int(atomicAdd(P.ctrl, 1u));
@@ -220,7 +225,7 @@ topk_select_kernel(const SelectParams P) {
         p_bh = t < P.bh_total ? t : -1;
         p_stage = 0;
         if (p_bh >= 0) p_k = P.kc + int64_t(p_bh) * P.chunks * C::CHB;
-        if (fcount == 0) fq0 = p_bh; else if (fcount == 1) fq1 = p_bh; else fq2 = p_bh;
+        if (fcount == 0) fq0 = p_bh; else if (fcount == 1) fq1 = p_bh; else if (fcount == 2) fq2 = p_bh; else fq3 = p_bh;
         ++fcount;
     };
     auto issue = [&](int slot) {   // warp-collective (elect.sync issues)
@@ -234,8 +239,10 @@ topk_select_kernel(const SelectParams P) {
         bulk_g2s_elect(ring + slot * C::STG, p_k + int64_t(p_stage) * C::STG, bytes, &bars[slot], policy);
         if (p_stage == 0) {   // the unit's q, on its own barrier (one phase per unit)
             fence_proxy_async();
-            mbar_expect_tx_elect(&bars[S], 2 * D);
-            bulk_g2s_elect(qsm, P.q + int64_t(p_bh) * D, 2 * D, &bars[S], policy);
+            const int qb = NQ == 1 ? 0 : (p_units & 1);
+            ++p_units;
+            mbar_expect_tx_elect(&bars[S + qb], 2 * D);
+            bulk_g2s_elect(qsm0 + qb * 2 * D, P.q + int64_t(p_bh) * D, 2 * D, &bars[S + qb], policy);
         }
         if (++p_stage == nst) next_unit();
     };
@@ -248,7 +255,8 @@ topk_select_kernel(const SelectParams P) {
     const int keep = P.keep;
 
     int slot = 0;
-    uint32_t parity = 0, qparity = 0;
+    uint32_t parity = 0, qparity = 0;   // qparity: bit b = phase of q area b
+    int c_units = 0;
     auto acquire = [&]() -> const uint8_t* {
         issue(slot == 0 ? S - 1 : slot - 1);
         mbar_wait(&bars[slot], parity);
@@ -267,6 +275,7 @@ topk_select_kernel(const SelectParams P) {
         const int bh = fq0;
         fq0 = fq1;
         fq1 = fq2;
+        fq2 = fq3;
         --fcount;
         if (bh < 0) break;
 
@@ -274,8 +283,11 @@ topk_select_kernel(const SelectParams P) {
         float M;
         {
             const uint8_t* sb = acquire();
-            mbar_wait(&bars[S], qparity);
-            qparity ^= 1u;
+            const int qb = NQ == 1 ? 0 : (c_units & 1);
+            ++c_units;
+            mbar_wait(&bars[S + qb], (qparity >> qb) & 1u);
+            qparity ^= 1u << qb;
+            const uint8_t* qsm = qsm0 + qb * 2 * D;
             KFrag<D> kf;                      // the lane's q digits + epilogue weights
             load_q_mma<D>(qsm, P.qscale, lane, kf);
             float mx = -INFINITY;
@@ -401,7 +413,7 @@ struct GatherParams {
 template <int D, bool VTM>
 __global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) {
     constexpr int CB = D / 2, MB = D / 16, CHB = kChunk * (CB + MB);
-    constexpr int LPT = D / 32, TPI = 32 / LPT, GB = 4;
+    constexpr int LPT = D / 32, TPI = 32 / LPT, GB = VTM ? 8 : 4;   // row groups loaded before use
     const int lane = threadIdx.x & 31;
     const int bh = int(blockIdx.x) * (blockDim.x >> 5) + int(threadIdx.x >> 5);
     asm volatile("griddepcontrol.wait;" ::: "memory");   // the kept lists of the select kernel
@@ -472,7 +484,8 @@ __global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) 
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t select_smem_bytes() {
-    return size_t(WPC) * (S * Cfg<D, NCH>::STG + 2 * D + MAXT * 6 + (S + 1) * 8);
+    constexpr int NQ = S > 2 ? 2 : 1;
+    return size_t(WPC) * (S * Cfg<D, NCH>::STG + NQ * 2 * D + MAXT * 6 + (S + NQ) * 8);
 }
 
 constexpr size_t kTopkCtrlBytes = 2048;
@@ -545,13 +558,29 @@ size_t topk_workspace_bytes(int batch, int heads, int t_cap) {
     return kTopkCtrlBytes + size_t(batch) * size_t(heads) * size_t(t_cap) * 8;
 }
 
-cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
+template <int S>
+cudaError_t launch_topk_s(const TopkArgs& a, cudaStream_t stream) {
     constexpr int W = FLEXQ_TOPK_WPC;
     if (a.head_dim == 128)
-        return a.cur_len <= 576 ? launch_topk<128, 2, 2, W, 576>(a, stream)
-                                : launch_topk<128, 2, 2, W, kTopkMaxTokens>(a, stream);
-    return a.cur_len <= 576 ? launch_topk<64, 2, 2, W, 576>(a, stream)
-                            : launch_topk<64, 2, 2, W, kTopkMaxTokens>(a, stream);
+        return a.cur_len <= 576 ? launch_topk<128, 2, S, W, 576>(a, stream)
+                                : launch_topk<128, 2, S, W, kTopkMaxTokens>(a, stream);
+    return a.cur_len <= 576 ? launch_topk<64, 2, S, W, 576>(a, stream)
+                            : launch_topk<64, 2, S, W, kTopkMaxTokens>(a, stream);
+}
+
+cudaError_t launch_decode_attention_topk(const TopkArgs& a, cudaStream_t stream) {
+    // select kernel ring depth (tuning: FLEXQ_TOPK_RING=2|3|4): more stages in flight while a head's
+    // keys are selected, but fewer resident warps; 16 warps x 2 stages measured fastest
+    static const int ring = [] {
+        const char* e = getenv("FLEXQ_TOPK_RING");
+        const int r = e ? atoi(e) : 2;   // B200: 2 stages 143 us, 3 stages 156 us, 4 stages 192 us (OPT-175B)
+        return r >= 2 && r <= 4 ? r : 2;
+    }();
+    // two alternating q areas are safe for S - 1 <= 2 nst - 1 stages ahead (nst: stages per
+    // unit); single-stage units (cur_len <= 64) keep the 2-stage ring
+    if (ring == 2 || a.cur_len <= 64) return launch_topk_s<2>(a, stream);
+    if (ring == 4) return launch_topk_s<4>(a, stream);
+    return launch_topk_s<3>(a, stream);
 }
 
 }  // namespace flexq

@@ -12,10 +12,12 @@
 //   * Persistent CTAs, one per SM; CTA c streams the contiguous panel range
 //     [c T / G, (c + 1) T / G) of the T = tiles x KB panels in (tile, k-block) order
 //     (stream-K), so every SM moves the same number of bytes.
-//   * Four producer warps take every fourth stage of a 12-stage ring; per stage one lane issues
-//     three copies: the 9216-byte panel, its 16-byte clamp flag and the M x 64 tile of x (2-D
-//     TMA).  (One producer lane issuing per-row copies of x was the bound of the first version:
-//     ~90 cycles per copy, 141 us at M = 1 and 313 us at M = 16.)
+//   * Four producer warps take every fourth stage of a 16-stage ring; per stage one lane issues
+//     two copies: the 9216-byte panel and the M x 64 tile of x (2-D TMA).  (One producer lane
+//     issuing per-row copies of x was the bound of the first version: ~90 cycles per copy, 141 us
+//     at M = 1 and 313 us at M = 16.)  The panels' clamp flags (flexq_pack_weight) are OR-ed over
+//     the CTA's range once, at the start: the CTA runs the clamp-free conversion unless one of its
+//     panels can reconstruct above 65504 (a per-stage flag test stalled on its shared load).
 //   * Sixteen consumer warps each own 16 weight columns of the 256-column tile (one MMA row
 //     block).  Per stage a lane loads two code words per column (k 8t..8t+7 and
 //     32+8t..32+8t+7), dequantizes them into fp16 pairs (LOP3 + HADD2 + HFMA2 [+ HMNMX2] per pair,
@@ -37,14 +39,16 @@
 namespace flexq {
 namespace {
 
+#ifndef FLEXQ_GEMV_PROBE
+#define FLEXQ_GEMV_PROBE 0   // tuning only (wrong results): 1 no x copy, 3 no math, 4 = 1 + 3
+#endif
 constexpr int kConsumers = 16;                        // consumer warps (16 columns each)
 constexpr int kProducers = 4;                         // producer warps (every 4th stage each)
 constexpr int kThreadsV = (kConsumers + kProducers) * 32;
-constexpr int kStagesV = 12;
+constexpr int kStagesV = 16;                          // a power of two: ring slot / phase by masks
 constexpr int kPanelData = kGemmTileN * kGemmTileK / 2 + 1024;   // 9216: codes + meta
 constexpr int kXOff = kPanelData;                     // the x tile [M][64] fp16 (128-B aligned for the 2-D TMA)
-constexpr int kFlagOff = kXOff + kGemvMaxRows * 128;  // the panel's 16-byte clamp flag
-constexpr int kStageBytes = (kFlagOff + 16 + 127) / 128 * 128;   // 11392
+constexpr int kStageBytes = kXOff + kGemvMaxRows * 128;           // 11264
 static_assert(kXOff % 128 == 0 && kStageBytes % 128 == 0, "tensor-copy destination alignment");
 constexpr int kSmemV = kStagesV * kStageBytes + 2 * kStagesV * 8 + 16;
 
@@ -97,13 +101,34 @@ __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__
 // dequant_gemm.cu's conversion, operation for operation (reading G2): nibbles 0 and 4 of t ->
 // fp16 1024 + c (exact), - 1024 (exact), one fp16 FMA with the pair's (scale, min), clamp.
 template <bool CLAMP>
-__device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t mp) {
+__device__ __forceinline__ uint32_t deq_pair(uint32_t t, uint32_t sp, uint32_t mp, uint32_t magic) {
     uint32_t m;
-    asm("lop3.b32 %0, %1, 0x000F000F, 0x64006400, 0xEA;" : "=r"(m) : "r"(t));
+    asm("lop3.b32 %0, %1, 0x000F000F, %2, 0xEA;" : "=r"(m) : "r"(t), "r"(magic));   // (t & mask) | magic
     const __half2 c = __hsub2(u2h(m), u2h(0x64006400u));
     const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
     if constexpr (CLAMP) return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));
     else return h2u(v);
+}
+// The same value from nibbles 1 and 5 of t without shifting t first: (t & 0x00F000F0) | magic is
+// the fp16 pair 1024 + 16 c (exact), and (1024 + 16 c) / 16 - 64 = c exactly (one HFMA2, the
+// product is exact and so is the sum), then the same HFMA2 with (scale, min).
+template <bool CLAMP>
+__device__ __forceinline__ uint32_t deq_pair_hi(uint32_t t, uint32_t sp, uint32_t mp, uint32_t magic) {
+    uint32_t m;
+    asm("lop3.b32 %0, %1, 0x00F000F0, %2, 0xEA;" : "=r"(m) : "r"(t), "r"(magic));
+    const __half2 c = __hfma2(u2h(m), u2h(0x2C002C00u), u2h(0xD400D400u));           // x / 16 - 64
+    const __half2 v = __hfma2(c, u2h(sp), u2h(mp));
+    if constexpr (CLAMP) return h2u(__hmin2(v, u2h(0x7BFF7BFFu)));
+    else return h2u(v);
+}
+template <bool V>
+struct BoolTag {
+    static constexpr bool value = V;
+};
+__device__ __forceinline__ uint32_t magic_h2() {   // 0x64006400 in a register (LOP3 takes one immediate)
+    uint32_t m;
+    asm volatile("mov.b32 %0, 0x64006400;" : "=r"(m));
+    return m;
 }
 
 __device__ __forceinline__ void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -121,41 +146,60 @@ __device__ __forceinline__ int owner(int64_t total, int G, int64_t i) {   // CTA
 
 // One stage of a consumer warp: 16 columns x 64 k against MB blocks of 8 rows; step s of the
 // four accumulates into acc[s].
+// Per-lane shared-memory offsets inside a stage (computed once).
+struct LaneOff {
+    uint32_t cw;   // code word: column n0 + g, hk0 word t
+    uint32_t me;   // meta of k pairs 4t .. 4t + 3 of the warp's group
+    uint32_t xr;   // x: row g, k 8t
+};
 template <int MB, bool CLAMP>
-__device__ __forceinline__ void stage_math(const uint8_t* st, int n0, int lane, float (&acc)[4][MB][4]) {
-    const int g = lane >> 2, t = lane & 3;
+__device__ __forceinline__ void stage_math(const uint8_t* st, const LaneOff& lo, uint32_t magic,
+                                           float (&acc)[4][MB][4]) {
     // code words: column n0 + g (A rows 0..7) and n0 + g + 8 (rows 8..15); hk0 word t, hk1 word t
-    const uint8_t* cw = st + (n0 + g) * 16 + 4 * t;
+    const uint8_t* cw = st + lo.cw;
     const uint32_t w00 = *reinterpret_cast<const uint32_t*>(cw);
     const uint32_t w01 = *reinterpret_cast<const uint32_t*>(cw + 4096);
     const uint32_t w10 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16);
     const uint32_t w11 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16 + 4096);
     // meta {scale pair, min pair} of k pairs 4t + s (hk0 word t) and 16 + 4t + s (hk1 word t)
-    const uint8_t* me = st + kGemmTileN * kGemmTileK / 2 + (n0 >> 6) * 256 + 32 * t;
+    const uint8_t* me = st + lo.me;
     const uint4 ma0 = *reinterpret_cast<const uint4*>(me);            // pairs 4t, 4t + 1
     const uint4 ma1 = *reinterpret_cast<const uint4*>(me + 16);       // 4t + 2, 4t + 3
     const uint4 mb0 = *reinterpret_cast<const uint4*>(me + 128);      // 16 + 4t, ..
     const uint4 mb1 = *reinterpret_cast<const uint4*>(me + 144);
     const uint32_t slo[4] = {ma0.x, ma0.z, ma1.x, ma1.z}, mlo[4] = {ma0.y, ma0.w, ma1.y, ma1.w};
     const uint32_t shi[4] = {mb0.x, mb0.z, mb1.x, mb1.z}, mhi[4] = {mb0.y, mb0.w, mb1.y, mb1.w};
-    // x: row 8 mb + g, k 8t .. 8t+7 (b0 of steps 0..3) and 32 + 8t .. (b1)
+    // k order of the 4 MMA steps: step s takes code word hk = s / 2 of each column (hk0 word t:
+    // k 8t .. 8t+7; hk1 word t: 32 + 8t ..) and its sub-pairs 2 (s % 2) (MMA k pair t) and
+    // 2 (s % 2) + 1 (k pair t + 4), i.e. k = 32 hk + 8t + 4 (s % 2) + {0, 1} and {2, 3}: the B
+    // fragment (b0, b1) of step s is then one 8-byte run of the x row, adjacent registers of one
+    // LDS.128 (x row 8 mb + g: k 8t .. 8t+7 -> steps 0, 1; 32 + 8t .. -> steps 2, 3)
     uint4 xa[MB], xb[MB];
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) {
-        const uint8_t* xr = st + kXOff + (8 * mb + g) * 128 + 16 * t;
+        const uint8_t* xr = st + lo.xr + mb * 8 * 128;
         xa[mb] = *reinterpret_cast<const uint4*>(xr);
         xb[mb] = *reinterpret_cast<const uint4*>(xr + 64);
     }
+    // sub-pair q of a word: nibbles q, 4 + q; q = 0, 1 straight from the word, q = 2, 3 from w >> 8
+    const uint32_t v00 = w00 >> 8, v01 = w01 >> 8, v10 = w10 >> 8, v11 = w11 >> 8;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-        const uint32_t a0 = deq_pair<CLAMP>(w00 >> (4 * s), slo[s], mlo[s]);
-        const uint32_t a1 = deq_pair<CLAMP>(w10 >> (4 * s), slo[s], mlo[s]);
-        const uint32_t a2 = deq_pair<CLAMP>(w01 >> (4 * s), shi[s], mhi[s]);
-        const uint32_t a3 = deq_pair<CLAMP>(w11 >> (4 * s), shi[s], mhi[s]);
+        const int hk = s >> 1, q0 = 2 * (s & 1);         // word, first sub-pair
+        const uint32_t r0 = hk ? w01 : w00, r8 = hk ? w11 : w10;             // rows g, g + 8
+        const uint32_t u0 = hk ? v01 : v00, u8 = hk ? v11 : v10;
+        const uint32_t* sc = hk ? shi : slo;
+        const uint32_t* mn = hk ? mhi : mlo;
+        const uint32_t x0 = q0 ? u0 : r0, x8 = q0 ? u8 : r8;               // sub-pairs q0 (even), q0 + 1 (odd)
+        const uint32_t a0 = deq_pair<CLAMP>(x0, sc[q0], mn[q0], magic);
+        const uint32_t a1 = deq_pair<CLAMP>(x8, sc[q0], mn[q0], magic);
+        const uint32_t a2 = deq_pair_hi<CLAMP>(x0, sc[q0 + 1], mn[q0 + 1], magic);
+        const uint32_t a3 = deq_pair_hi<CLAMP>(x8, sc[q0 + 1], mn[q0 + 1], magic);
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
-            const uint32_t b0 = s == 0 ? xa[mb].x : s == 1 ? xa[mb].y : s == 2 ? xa[mb].z : xa[mb].w;
-            const uint32_t b1 = s == 0 ? xb[mb].x : s == 1 ? xb[mb].y : s == 2 ? xb[mb].z : xb[mb].w;
+            const uint4& xv = hk ? xb[mb] : xa[mb];
+            const uint32_t b0 = (s & 1) ? xv.z : xv.x;
+            const uint32_t b1 = (s & 1) ? xv.w : xv.y;
             mma_f16(acc[s][mb], a0, a1, a2, a3, b0, b1);
         }
     }
@@ -198,6 +242,7 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
             mbar_init(full + s, 1);
             mbar_init(empty + s, kConsumers);
         }
+        flag[1] = 0u;   // the CTA's clamp flag (consumers OR the panels' flags into it)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -208,18 +253,17 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
             const int r = warp - kConsumers;
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
             const uint64_t pol_w = policy_fractional(false), pol_x = policy_fractional(true);
-            const uint8_t* flags = p.panels + p.total * kPanelData;
-            const uint32_t bytes = uint32_t(kPanelData + 16 + p.M * 128);
+            constexpr bool kNoX = FLEXQ_GEMV_PROBE == 1 || FLEXQ_GEMV_PROBE == 4;
+            const uint32_t bytes = uint32_t(kPanelData + (kNoX ? 0 : p.M * 128));
             int64_t i = i0 + r;
             int kb = int(i % p.KB);
             for (int j = r; j < n; j += kProducers, i += kProducers) {
-                const int s = j % kStagesV;
+                const int s = j & (kStagesV - 1);
                 mbar_wait(empty + s, ((j / kStagesV) & 1) ^ 1);
                 const uint32_t dst = su32(smem + s * kStageBytes);
                 mbar_expect_tx(full + s, bytes);
                 bulk_g2s(dst, p.panels + i * kPanelData, kPanelData, full + s, pol_w);
-                bulk_g2s(dst + kFlagOff, flags + i * 16, 16, full + s, pol_w);
-                asm volatile(
+                if (!kNoX) asm volatile(
                     "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
                     " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst + kXOff),
                     "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(kb * kGemmTileK), "r"(0), "r"(su32(full + s)),
@@ -235,8 +279,21 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
     // ---------------- consumers: warp owns columns n0 .. n0 + 15 of the tile
     const int n0 = warp * 16;
     const int t = lane & 3, g = lane >> 2;
+    const LaneOff lo{uint32_t((n0 + g) * 16 + 4 * t),
+                     uint32_t(kGemmTileN * kGemmTileK / 2 + (n0 >> 6) * 256 + 32 * t),
+                     uint32_t(kXOff + g * 128 + 16 * t)};
+    {   // the CTA's clamp flag: OR of its panels' flags (first word of each 16-byte flag)
+        const uint32_t* flags = reinterpret_cast<const uint32_t*>(p.panels + p.total * kPanelData);
+        uint32_t f = 0;
+        for (int k = int(threadIdx.x); k < n; k += kConsumers * 32) f |= __ldg(flags + (i0 + k) * 4);
+        if (__any_sync(0xffffffffu, f != 0) && lane == 0) atomicOr(flag + 1, 1u);
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+    }
+    const bool clamp_cta = flag[1] != 0u;
+    const uint32_t magic = magic_h2();
     float acc[4][MB][4];
-    int j = 0;
+    int s = 0;                 // ring slot and its phase
+    uint32_t ph = 0;
     int64_t i = i0;
     const int64_t first_tile = i0 / p.KB;
     while (i < i1) {
@@ -244,18 +301,31 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         const int64_t seg_end = min(i1, (tile + 1) * p.KB);
         const bool whole = (i == tile * p.KB) && (seg_end == (tile + 1) * p.KB);
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) acc[s][mb][0] = acc[s][mb][1] = acc[s][mb][2] = acc[s][mb][3] = 0.0f;
-        for (; i < seg_end; ++i, ++j) {
-            const int s = j % kStagesV;
-            mbar_wait(full + s, (j / kStagesV) & 1);
-            const uint8_t* st = smem + s * kStageBytes;
-            if (*reinterpret_cast<const uint32_t*>(st + kFlagOff)) stage_math<MB, true>(st, n0, lane, acc);
-            else stage_math<MB, false>(st, n0, lane, acc);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);
-        }
+            for (int mb = 0; mb < MB; ++mb) acc[q][mb][0] = acc[q][mb][1] = acc[q][mb][2] = acc[q][mb][3] = 0.0f;
+        auto run = [&](auto clamp_tag) {
+            constexpr bool kClamp = decltype(clamp_tag)::value;
+#pragma unroll 1
+            for (int left = int(seg_end - i); left > 0; --left) {
+                mbar_wait(full + s, ph);
+                const uint8_t* st = smem + s * kStageBytes;
+#if FLEXQ_GEMV_PROBE >= 3
+                if (lane == 0 && *reinterpret_cast<const uint32_t*>(st) == 0x12345678u) acc[0][0][0] += 1.0f;
+#else
+                stage_math<MB, kClamp>(st, lo, magic, acc);
+#endif
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+                if (++s == kStagesV) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        };
+        if (clamp_cta) run(BoolTag<true>{});
+        else run(BoolTag<false>{});
+        i = seg_end;
         float v[MB][4];   // the four step accumulators, summed in a fixed order
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb)
