@@ -155,9 +155,9 @@ __device__ int head_pieces(const Params& P, int W, int bh, int o, int& count) {
 template <int S>
 constexpr int kXtraBufs = S > 2 ? 2 : 1;
 
-template <int D, int MAXT, int S>
+template <int D, int MAXT, int S, int NCH>
 __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const Params P) {
-    using C = Cfg<D, kNch>;
+    using C = Cfg<D, NCH>;
     constexpr int NX = kXtraBufs<S>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     uint8_t* xtra0 = smem + S * C::STG;   // NX extra areas
     float* scores = reinterpret_cast<float*>(xtra0 + NX * C::XTRA);
     uint32_t* limbs = reinterpret_cast<uint32_t*>(scores + MAXT);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(limbs + kLimbWords<D, kNch>);   // S stages, then NX extra
+    uint64_t* bars = reinterpret_cast<uint64_t*>(limbs + kLimbWords<D, NCH>);   // S stages, then NX extra
 
     const uint64_t policy = evict_first_policy();
     // Programmatic dependent launch (NEXT-3 multi-layer decode): let the next layer's launch be
@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         }
         p_stage = 0;
         if (p_valid) {
-            p_nst = (pp.nch + kNch - 1) / kNch;
-            p_last = pp.nch - kNch * (p_nst - 1);
+            p_nst = (pp.nch + NCH - 1) / NCH;
+            p_last = pp.nch - NCH * (p_nst - 1);
             const int64_t c0 = int64_t(pp.bh) * P.chunks + pp.o;
             p_k = P.kc + c0 * C::CHB;
             p_v = P.vc + c0 * C::CHB;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         }
         const bool vpass = p_stage >= p_nst;
         const int si = vpass ? p_stage - p_nst : p_stage;
-        const uint32_t bytes = uint32_t(si == p_nst - 1 ? p_last : kNch) * C::CHB;
+        const uint32_t bytes = uint32_t(si == p_nst - 1 ? p_last : NCH) * C::CHB;
         const bool first = p_stage == 0;
         // the extra area (q, k_new, v_new) is rewritten by the async proxy for the next item: order
         mbar_expect_tx_elect(&bars[slot], bytes);
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     for (int s = 0; s < S - 1; ++s) issue(s);
 
     // ---------------- consumer: the same item sequence, one stage behind
-    const VLane<D> vlane = v_lane<D, kNch>(lane);
+    const VLane<D> vlane = v_lane<D, NCH>(lane);
     int slot = 0, c_items = 0;
     uint32_t parity = 0, xparity = 0;      // xparity: bit b = phase of extra area b
     auto acquire = [&]() -> const uint8_t* {   // issue S - 1 stages ahead, then wait for the current slot
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         const int bh = pc.bh;
         const int first = pc.o * kChunk;
         const int len = min(P.cur_len - first, pc.nch * kChunk);
-        const int nst = (pc.nch + kNch - 1) / kNch;
+        const int nst = (pc.nch + NCH - 1) / NCH;
 
         // fused append: the piece holding token cur_len - 1 quantizes k_new / v_new (they
         // arrive with its first stage), and patches the stage images of its last K and V
@@ -357,11 +357,11 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
                 const int n = min(C::CH, len - t0);
                 if (n == C::CH) {
 #pragma unroll
-                    for (int b = 0; b < C::CH / 16; ++b) k_block_mma<D, kNch>(b, kf, sb, scores, t0, C::CH, lane, mx);
+                    for (int b = 0; b < C::CH / 16; ++b) k_block_mma<D, NCH>(b, kf, sb, scores, t0, C::CH, lane, mx);
                 } else {
 #pragma unroll
                     for (int b = 0; b < C::CH / 16; ++b)
-                        if (b * 16 < n) k_block_mma<D, kNch>(b, kf, sb, scores, t0, n, lane, mx);
+                        if (b * 16 < n) k_block_mma<D, NCH>(b, kf, sb, scores, t0, n, lane, mx);
                 }
                 release();
                 if (++st == nst) break;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
             const uint8_t* sb = acquire();
             if (owns_new && st == nst - 1) patch(sb, true);
             const int t0 = st * C::CH;
-            v_stage_mma<D, kNch>(va, vlane, sb, scores + t0, M, min(C::CH, len - t0), lane, limbs);
+            v_stage_mma<D, NCH>(va, vlane, sb, scores + t0, M, min(C::CH, len - t0), lane, limbs);
             release();
         }
 
@@ -479,9 +479,9 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
 #endif
 }
 
-template <int D, int MAXT, int S>
+template <int D, int MAXT, int S, int NCH>
 constexpr size_t smem_bytes() {
-    return size_t(S) * Cfg<D, kNch>::STG + kXtraBufs<S> * Cfg<D, kNch>::XTRA + MAXT * 4 + kLimbWords<D, kNch> * 4 +
+    return size_t(S) * Cfg<D, NCH>::STG + kXtraBufs<S> * Cfg<D, NCH>::XTRA + MAXT * 4 + kLimbWords<D, NCH> * 4 +
            (S + kXtraBufs<S>) * 8;
 }
 
@@ -491,7 +491,7 @@ struct DevInfo {
     int sms = 0;
     int occ = 0;
 };
-template <int D, int MAXT, int S>
+template <int D, int MAXT, int S, int NCH>
 DevInfo dev_info() {
     constexpr int kMaxDev = 64;
     static DevInfo info[kMaxDev];
@@ -500,11 +500,11 @@ DevInfo dev_info() {
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDev) dev = 0;
     std::call_once(once[dev], [dev] {
-        auto k = decode_attention_kernel<D, MAXT, S>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, MAXT, S>()));
+        auto k = decode_attention_kernel<D, MAXT, S, NCH>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, MAXT, S, NCH>()));
         int sms = 0, o = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, smem_bytes<D, MAXT, S>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, smem_bytes<D, MAXT, S, NCH>());
         info[dev].sms = sms > 0 ? sms : 148;
         info[dev].occ = o > 0 ? o : 1;
     });
@@ -547,10 +547,10 @@ void tune_split(int& dyn_min_x100, int& nb_per_warp_x100, int& kb, int& hyb_pct,
     if (v[4] > 0) hyb_q = v[4];
 }
 
-template <int D, int MAXT, int S>
+template <int D, int MAXT, int S, int NCH>
 cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     const int bh = a.batch * a.heads;
-    const DevInfo di = dev_info<D, MAXT, S>();
+    const DevInfo di = dev_info<D, MAXT, S, NCH>();
     const int Wres = std::min(di.sms * di.occ, kMaxWarps);
     const int nck = (a.cur_len + kChunk - 1) / kChunk;
     const int maxch = MAXT / kChunk;
@@ -629,17 +629,18 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));   // dynamic: no more warps than items
     cfg.blockDim = dim3(32);
-    cfg.dynamicSmemBytes = smem_bytes<D, MAXT, S>();
+    cfg.dynamicSmemBytes = smem_bytes<D, MAXT, S, NCH>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<D, MAXT, S>, P);
+    return cudaLaunchKernelEx(&cfg, decode_attention_kernel<D, MAXT, S, NCH>, P);
 }
 
-// Ring depth (tuning: FLEXQ_ATTN_RING=2|3|4).
+// Ring depth (tuning: FLEXQ_ATTN_RING=2|3).  Measured and dropped: 4 stages of 64 tokens (9 warps
+// per SM) and 4 stages of 32 tokens (15 warps per SM) -- slower at every BASELINE shape.
 template <int D, int MAXT>
 cudaError_t launch_ring(const AttnArgs& a, cudaStream_t stream) {
     static const int ring_env = [] {
@@ -649,18 +650,17 @@ cudaError_t launch_ring(const AttnArgs& a, cudaStream_t stream) {
     // default: S = 2 (16 warps per SM); S = 3 (11 warps per SM, two stages in flight) when the launch
     // holds 1.2 - 2 heads per S = 2 warp -- the batch-36 shard of OPT-175B: 48 us vs 55 us (B200 sweep)
     int S = 2;
-    if (ring_env >= 2 && ring_env <= 4) {
+    if (ring_env == 2 || ring_env == 3) {
         S = ring_env;
     } else {
         const int bh = a.batch * a.heads;
-        const int w2 = dev_info<D, MAXT, 2>().sms * dev_info<D, MAXT, 2>().occ;
+        const int w2 = dev_info<D, MAXT, 2, kNch>().sms * dev_info<D, MAXT, 2, kNch>().occ;
         if (int64_t(bh) * 10 >= int64_t(w2) * 12 && int64_t(bh) * 10 <= int64_t(w2) * 20 &&
             (a.cur_len + kChunk - 1) / kChunk >= 4)
             S = 3;
     }
-    if (S == 4) return launch<D, MAXT, 4>(a, stream);
-    if (S == 3) return launch<D, MAXT, 3>(a, stream);
-    return launch<D, MAXT, 2>(a, stream);
+    if (S == 3) return launch<D, MAXT, 3, kNch>(a, stream);
+    return launch<D, MAXT, 2, kNch>(a, stream);
 }
 
 }  // namespace

@@ -195,9 +195,11 @@ topk_select_kernel(const SelectParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // q is refilled at the next unit's first stage, S - 1 stages ahead: with S > 2 a unit of fewer
-    // than S stages could still be reading it, so deeper rings alternate two q areas
-    constexpr int NQ = S > 2 ? 2 : 1;
+    // q is refilled at a unit's first stage, issued S - 1 stages ahead -- before the previous unit
+    // has read its own q when units are a single stage (cur_len <= 64) -- so two q areas alternate,
+    // each on its own barrier: unit u + 2's q is issued after unit u has read its q for
+    // S - 1 <= 2 nst - 1 (the launcher keeps S = 2 for single-stage units)
+    constexpr int NQ = 2;
     constexpr int PW = S * C::STG + NQ * 2 * D + MAXT * 6;   // per warp: ring, q, scores, kept list
     uint8_t* ring = smem + warp * PW;
     uint8_t* qsm0 = ring + S * C::STG;
@@ -239,7 +241,7 @@ topk_select_kernel(const SelectParams P) {
         bulk_g2s_elect(ring + slot * C::STG, p_k + int64_t(p_stage) * C::STG, bytes, &bars[slot], policy);
         if (p_stage == 0) {   // the unit's q, on its own barrier (one phase per unit)
             fence_proxy_async();
-            const int qb = NQ == 1 ? 0 : (p_units & 1);
+            const int qb = p_units & 1;
             ++p_units;
             mbar_expect_tx_elect(&bars[S + qb], 2 * D);
             bulk_g2s_elect(qsm0 + qb * 2 * D, P.q + int64_t(p_bh) * D, 2 * D, &bars[S + qb], policy);
@@ -283,7 +285,7 @@ topk_select_kernel(const SelectParams P) {
         float M;
         {
             const uint8_t* sb = acquire();
-            const int qb = NQ == 1 ? 0 : (c_units & 1);
+            const int qb = c_units & 1;
             ++c_units;
             mbar_wait(&bars[S + qb], (qparity >> qb) & 1u);
             qparity ^= 1u << qb;
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) 
 
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t select_smem_bytes() {
-    constexpr int NQ = S > 2 ? 2 : 1;
+    constexpr int NQ = 2;
     return size_t(WPC) * (S * Cfg<D, NCH>::STG + NQ * 2 * D + MAXT * 6 + (S + NQ) * 8);
 }
 

@@ -398,7 +398,6 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
     uint64_t* tmem_full = done + kDoneSlots;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-    uint32_t* epi_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bstage = uint32_t(PAIR ? p.mpad / 2 : p.mpad) * 128u;   // this CTA's x rows per stage
@@ -685,57 +684,74 @@ dequant_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const GemmParams 
                 else mbar_arrive(tmem_empty);
             }
             if (!full) {
-                // Split-k fixup: the last of the tile's S contributors (CTAs r + R p) sums their
-                // partials in p order (deterministic) and stores fp16.
+                // Split-k fixup, spread over the tile's S contributors (CTAs r + R p, all resident:
+                // the grid is at most one CTA per SM): each announces its partial on the tile's
+                // arrival ticket, waits for all S, then sums a 1/S slice of the rows over the S
+                // partials in p order (deterministic) and stores fp16; the last to finish its
+                // slice resets both tickets.  (A single last contributor summing every row was
+                // latency-bound: ~30 us of the 12288 x 12288 launch.)
                 const int r = c % S.R;                                  // remainder tile (pair tile)
                 const int tk = PAIR ? 2 * r + int(rank) : r;             // ticket of this CTA's half
+                const int ntk = p.N / kBN;                              // done tickets follow
+                const int my_part = c / S.R;
                 __threadfence();
                 epi_bar();
                 if (q == 0 && lane == 0) {
-                    const uint32_t old = atomicAdd(p.tickets + tk, 1u);
-                    const bool last = old == uint32_t(S.S - 1);
-                    if (last) p.tickets[tk] = 0u;
-                    *epi_flag = last ? 1u : 0u;
-                }
-                epi_bar();
-                if (*epi_flag) {
-                    __threadfence();
-                    for (int h = 0; h < 2; ++h) {
-                        const int n0 = t256 * kBN + h * 128 + q * 32;
-                        const int64_t col = int64_t(h * 128 + nl) * mp;
-                        for (int m0 = 0; m0 < mp; m0 += 16) {
-                            float v[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) v[i] = 0.f;
-                            for (int pp = 0; pp < S.S; pp += 2) {
-                                // two contributors per round: 8 independent 16-byte loads in flight
-                                float4 a[8];
-#pragma unroll
-                                for (int u = 0; u < 2; ++u) {
-                                    const int kp = r + S.R * (pp + u < S.S ? pp + u : pp);   // contributor
-                                    const int k = PAIR ? 2 * kp + int(rank) : kp;            // its slot
-                                    const float4* src =
-                                        reinterpret_cast<const float4*>(p.partials + int64_t(k) * mp * kBN + col + m0);
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) a[4 * u + i] = __ldcg(src + i);
-                                }
-#pragma unroll
-                                for (int u = 0; u < 2; ++u) {
-                                    if (pp + u >= S.S) break;
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) {
-                                        v[4 * i] += a[4 * u + i].x;
-                                        v[4 * i + 1] += a[4 * u + i].y;
-                                        v[4 * i + 2] += a[4 * u + i].z;
-                                        v[4 * i + 3] += a[4 * u + i].w;
-                                    }
-                                }
-                            }
-                            store_rows16(v, scratch, lane, p.y, p.N, m0, p.M, n0);
-                        }
+                    atomicAdd(p.tickets + tk, 1u);
+                    uint32_t seen = 0;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.tickets + tk) : "memory");
+                        if (seen >= uint32_t(S.S)) break;
+                        __nanosleep(256);
                     }
                 }
                 epi_bar();
+                __threadfence();
+                const int nmb = mp / 16;
+                const int mb0 = my_part * nmb / S.S, mb1 = (my_part + 1) * nmb / S.S;
+                for (int h = 0; h < 2; ++h) {
+                    const int n0 = t256 * kBN + h * 128 + q * 32;
+                    const int64_t col = int64_t(h * 128 + nl) * mp;
+                    for (int mb = mb0; mb < mb1; ++mb) {
+                        const int m0 = mb * 16;
+                        float v[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+                        for (int pp = 0; pp < S.S; pp += 2) {
+                            // two contributors per round: 8 independent 16-byte loads in flight
+                            float4 a[8];
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const int kp = r + S.R * (pp + u < S.S ? pp + u : pp);   // contributor
+                                const int k = PAIR ? 2 * kp + int(rank) : kp;            // its slot
+                                const float4* src =
+                                    reinterpret_cast<const float4*>(p.partials + int64_t(k) * mp * kBN + col + m0);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) a[4 * u + i] = __ldcg(src + i);
+                            }
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                if (pp + u >= S.S) break;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    v[4 * i] += a[4 * u + i].x;
+                                    v[4 * i + 1] += a[4 * u + i].y;
+                                    v[4 * i + 2] += a[4 * u + i].z;
+                                    v[4 * i + 3] += a[4 * u + i].w;
+                                }
+                            }
+                        }
+                        store_rows16(v, scratch, lane, p.y, p.N, m0, p.M, n0);
+                    }
+                }
+                epi_bar();
+                if (q == 0 && lane == 0) {
+                    __threadfence();
+                    if (atomicAdd(p.tickets + ntk + tk, 1u) == uint32_t(S.S - 1)) {
+                        p.tickets[tk] = 0u;
+                        p.tickets[ntk + tk] = 0u;
+                    }
+                }
             }
         }
     }
@@ -872,7 +888,7 @@ cudaError_t launch_pack_weight(const void* codes, const void* meta, int64_t K, i
 size_t dequant_gemm_workspace_bytes(int64_t m, int64_t k, int64_t n) {
     (void)k;
     const int64_t tiles = n / kBN;
-    const size_t tickets = size_t((tiles * 4 + 255) / 256 * 256);
+    const size_t tickets = size_t((tiles * 8 + 255) / 256 * 256);   // arrival + done ticket per tile
     const size_t tc = tickets + size_t(kGemmMaxGrid) * size_t(mpad_of(m)) * kBN * sizeof(float);
     const size_t gv = m <= kGemvMaxRows ? dequant_gemv_workspace_bytes(n) : 0;
     return tc > gv ? tc : gv;
@@ -920,7 +936,7 @@ cudaError_t launch_dequant_gemm(const void* x, const void* panels, int64_t M, in
     sc.G = Gs;
     const int units = sc.dp_waves > 0 ? Gs : sc.R * sc.S;
     const int grid = pair ? 2 * units : units;
-    const size_t tick_bytes = size_t((N / kBN * 4 + 255) / 256 * 256);
+    const size_t tick_bytes = size_t((N / kBN * 8 + 255) / 256 * 256);
     uint32_t* tickets = static_cast<uint32_t*>(workspace);
     float* partials = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + tick_bytes);
     {   // the shared-memory attribute, once per device (under a lock)

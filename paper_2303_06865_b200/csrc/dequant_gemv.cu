@@ -306,8 +306,30 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
             for (int mb = 0; mb < MB; ++mb) acc[q][mb][0] = acc[q][mb][1] = acc[q][mb][2] = acc[q][mb][3] = 0.0f;
         auto run = [&](auto clamp_tag) {
             constexpr bool kClamp = decltype(clamp_tag)::value;
+            int left = int(seg_end - i);
+#if FLEXQ_GEMV_PROBE < 3
+            // two stages per iteration: their loads and conversions interleave (the stage's own
+            // dependency chain -- shared load, LOP3, HADD2, HFMA2, HMMA -- is long against 4 warps
+            // per scheduler); both are released together
 #pragma unroll 1
-            for (int left = int(seg_end - i); left > 0; --left) {
+            for (; left >= 2; left -= 2) {
+                const int s1 = s + 1 == kStagesV ? 0 : s + 1;
+                const uint32_t ph1 = s1 == 0 ? ph ^ 1u : ph;
+                mbar_wait(full + s, ph);
+                mbar_wait(full + s1, ph1);
+                stage_math<MB, kClamp>(smem + s * kStageBytes, lo, magic, acc);
+                stage_math<MB, kClamp>(smem + s1 * kStageBytes, lo, magic, acc);
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(empty + s);
+                    mbar_arrive(empty + s1);
+                }
+                s = s1 + 1 == kStagesV ? 0 : s1 + 1;
+                ph = s == 0 ? ph1 ^ 1u : ph1;
+            }
+#endif
+#pragma unroll 1
+            for (; left > 0; --left) {
                 mbar_wait(full + s, ph);
                 const uint8_t* st = smem + s * kStageBytes;
 #if FLEXQ_GEMV_PROBE >= 3

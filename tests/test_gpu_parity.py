@@ -490,3 +490,24 @@ def test_token_major_layout(orc, cuda, D):
     fq.flexq_append_kv(kn.to(cuda), vn.to(cuda), dense, pos=cur)
     for a, b in zip(fq.flexq_kv_export(cache, 0, cur + 1), fq.flexq_kv_export(dense, 0, cur + 1)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("layout", ["dense", "token_major"])
+def test_topk_short_contexts(orc, cuda, layout):
+    """Contexts of one 64-token stage or less (a select unit of a single stage: the next unit's q
+    is issued before this unit has read its own) and the stage boundary, through the full path
+    against the oracle on the GPU's kept set."""
+    B, H, D = 3, 7, 128
+    for cur in (1, 2, 31, 64, 65, 129):
+        cache, okc, ovc, q, cur_len = build_case(orc, cuda, B, H, D, cur, 1, 0, seed=62, layout=layout)
+        keep = fq.topk_keep(cur_len)
+        sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
+        out = fq.flexq_decode_attention_topk(q.to(cuda), cache, cur_len, keep, sel=sel)
+        torch.cuda.synchronize()
+        mask = np.zeros((B, H, cur_len), np.uint8)
+        for b in range(B):
+            for h in range(H):
+                mask[b, h, sel.cpu().numpy()[b, h]] = 1
+        assert int(mask.sum()) == B * H * keep
+        ref, _, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, cur_len, keep, sel=mask)
+        assert_attn_close(out.cpu().numpy(), ref, f"short context {cur_len}")

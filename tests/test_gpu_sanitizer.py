@@ -21,10 +21,11 @@ def test_compute_sanitizer(cuda, tool, sched):
     env = dict(os.environ)
     if sched == "dynamic":
         env["FLEXQ_ATTN_SPLIT"] = "0,0,0"
-    # initcheck: kernel accesses only -- with --kernel-name the writes of torch's own kernels (the
-    # synthetic inputs) are not tracked, so its host-API check would flag torch's copies of them
-    extra = ["--check-api-memory-access", "no"] if tool == "initcheck" else []
-    r = subprocess.run([cs, "--tool", tool, *extra, "--error-exitcode", "3", "--kernel-name", "kns=flexq",
+    # initcheck tracks initialisation through every kernel: with --kernel-name the writes of torch's
+    # own kernels (the synthetic inputs, the zero-filled caches) would go unseen and every read of
+    # them would be reported; racecheck / memcheck / synccheck look at the library's kernels only
+    filt = [] if tool == "initcheck" else ["--kernel-name", "kns=flexq"]
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", *filt,
                         sys.executable, os.path.join(ROOT, "scripts", "sanitize_case.py")],
                        capture_output=True, text=True, timeout=900, env=env)
     out = r.stdout + r.stderr
