@@ -88,8 +88,9 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=4", "FLEXQ_DEQ_CS=0"), tag="deq4n"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_DEQ_UNROLL=2",), tag="deq2"))
     if "--gemv-ab" in sys.argv:
-        for v in (1, 2, 3, 4):
+        for v in (1, 3, 4):
             print(build(force="--force" in sys.argv, defines=(f"FLEXQ_GEMV_PROBE={v}",), tag=f"gemv{v}"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMV_CTAS=1",), tag="gemv1cta"))
     if "--trace" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_ATTN_TRACE=1",), tag="trace"))
     if "--topk-ab" in sys.argv:

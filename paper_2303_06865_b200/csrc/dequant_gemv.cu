@@ -18,15 +18,16 @@
 //     at M = 1 and 313 us at M = 16.)  The panels' clamp flags (flexq_pack_weight) are OR-ed over
 //     the CTA's range once, at the start: the CTA runs the clamp-free conversion unless one of its
 //     panels can reconstruct above 65504 (a per-stage flag test stalled on its shared load).
-//   * Sixteen consumer warps each own 16 weight columns of the 256-column tile (one MMA row
-//     block).  Per stage a lane loads two code words per column (k 8t..8t+7 and
+//   * Eight consumer warps each own 32 weight columns of the 256-column tile (two MMA row
+//     blocks of 16).  Per stage a lane loads two code words per column (k 8t..8t+7 and
 //     32+8t..32+8t+7), dequantizes them into fp16 pairs (LOP3 + HADD2 + HFMA2 [+ HMNMX2] per pair,
 //     exactly dequant_gemm.cu's deq_pair), and runs 4 mma.sync.m16n8k16 (f16 x f16 -> f32) per
-//     8 rows of x: A = 16 columns x 16 k, B = x.  The k order inside an MMA is a permutation
-//     (step s takes sub-pair s of every code word), applied to x identically.  Each step has its
-//     own accumulator, so the 4 MMAs of a stage are independent (summed once per tile); with
-//     8 consumer warps and one accumulator chain (the second version) a stage took ~800 cycles,
-//     latency-bound at 2 warps per scheduler.
+//     row block and 8 rows of x: A = 16 columns x 16 k, B = x.  The k order inside an MMA is a
+//     permutation applied to x identically (below).  The bound of this loop is the shared-memory
+//     pipe, not the ALUs: every warp re-reads its group's (scale, min) pairs and the x tile, and a
+//     128-bit load costs 4 wavefronts however many lanes share an address -- 16 warps of 16
+//     columns needed 576 wavefronts per panel (ncu), 8 warps of 32 columns and x loads only for
+//     the rows that exist (M = 1: one of eight) need ~200.
 //   * A tile split between CTAs writes fp32 partials; the last of its contributors (ticket)
 //     sums them in CTA order -- deterministic -- and stores fp16.
 #include <cuda_fp16.h>
@@ -42,10 +43,15 @@ namespace {
 #ifndef FLEXQ_GEMV_PROBE
 #define FLEXQ_GEMV_PROBE 0   // tuning only (wrong results): 1 no x copy, 3 no math, 4 = 1 + 3
 #endif
-constexpr int kConsumers = 16;                        // consumer warps (16 columns each)
-constexpr int kProducers = 4;                         // producer warps (every 4th stage each)
+constexpr int kConsumers = 8;                         // consumer warps (32 columns each)
+#ifndef FLEXQ_GEMV_CTAS
+#define FLEXQ_GEMV_CTAS 2    // CTAs per SM, each with half the ring and two producers: 16 consumer
+                             // warps per SM (M <= 8: 70.8 us vs 74.6 us with one CTA of 8)
+#endif
+constexpr int kCtasV = FLEXQ_GEMV_CTAS;
+constexpr int kProducers = kCtasV == 1 ? 4 : 2;       // producer warps (every kProducers-th stage each)
 constexpr int kThreadsV = (kConsumers + kProducers) * 32;
-constexpr int kStagesV = 16;                          // a power of two: ring slot / phase by masks
+constexpr int kStagesV = 16 / kCtasV;                 // a power of two: ring slot / phase by masks
 constexpr int kPanelData = kGemmTileN * kGemmTileK / 2 + 1024;   // 9216: codes + meta
 constexpr int kXOff = kPanelData;                     // the x tile [M][64] fp16 (128-B aligned for the 2-D TMA)
 constexpr int kStageBytes = kXOff + kGemvMaxRows * 128;           // 11264
@@ -79,6 +85,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra W_%=;\n}" ::"r"(su32(b)),
         "r"(parity)
+        : "memory");
+}
+// Blocking wait.  The producer lanes wait on "empty" most of the time (the consumers bound the
+// loop); a plain try_wait loop returned almost at once and re-polled, ~1/3 of all issued
+// instructions of the SM (ncu: 637 spin instructions per 9 KB panel).
+// try_wait with an explicit suspend-time hint: the thread is suspended until the phase completes
+// (or ~1 ms passes) instead of polling -- test_wait + nanosleep still polled every ~6 ns.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WS_%=;\n}" ::"r"(su32(b)),
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -148,19 +168,14 @@ __device__ __forceinline__ int owner(int64_t total, int G, int64_t i) {   // CTA
 // four accumulates into acc[s].
 // Per-lane shared-memory offsets inside a stage (computed once).
 struct LaneOff {
-    uint32_t cw;   // code word: column n0 + g, hk0 word t
-    uint32_t me;   // meta of k pairs 4t .. 4t + 3 of the warp's group
-    uint32_t xr;   // x: row g, k 8t
+    uint32_t cw;     // code word: column n0 + g, hk0 word t
+    uint32_t me;     // meta of k pairs 4t .. 4t + 3 of the warp's group
+    uint32_t xr;     // x: row g, k 8t
+    uint32_t xrows;  // bit mb: x row 8 mb + g exists (< M); other rows only feed discarded outputs
 };
 template <int MB, bool CLAMP>
 __device__ __forceinline__ void stage_math(const uint8_t* st, const LaneOff& lo, uint32_t magic,
-                                           float (&acc)[4][MB][4]) {
-    // code words: column n0 + g (A rows 0..7) and n0 + g + 8 (rows 8..15); hk0 word t, hk1 word t
-    const uint8_t* cw = st + lo.cw;
-    const uint32_t w00 = *reinterpret_cast<const uint32_t*>(cw);
-    const uint32_t w01 = *reinterpret_cast<const uint32_t*>(cw + 4096);
-    const uint32_t w10 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16);
-    const uint32_t w11 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16 + 4096);
+                                           float (&acc)[2][2][MB][4]) {
     // meta {scale pair, min pair} of k pairs 4t + s (hk0 word t) and 16 + 4t + s (hk1 word t)
     const uint8_t* me = st + lo.me;
     const uint4 ma0 = *reinterpret_cast<const uint4*>(me);            // pairs 4t, 4t + 1
@@ -177,10 +192,21 @@ __device__ __forceinline__ void stage_math(const uint8_t* st, const LaneOff& lo,
     uint4 xa[MB], xb[MB];
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) {
-        const uint8_t* xr = st + lo.xr + mb * 8 * 128;
-        xa[mb] = *reinterpret_cast<const uint4*>(xr);
-        xb[mb] = *reinterpret_cast<const uint4*>(xr + 64);
+        xa[mb] = xb[mb] = make_uint4(0u, 0u, 0u, 0u);
+        if (lo.xrows & (1u << mb)) {
+            const uint8_t* xr = st + lo.xr + mb * 8 * 128;
+            xa[mb] = *reinterpret_cast<const uint4*>(xr);
+            xb[mb] = *reinterpret_cast<const uint4*>(xr + 64);
+        }
     }
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+    // code words: column n0 + 16 nb + g (A rows 0..7) and + 8 (rows 8..15); hk0 word t, hk1 word t
+    const uint8_t* cw = st + lo.cw + nb * 16 * 16;
+    const uint32_t w00 = *reinterpret_cast<const uint32_t*>(cw);
+    const uint32_t w01 = *reinterpret_cast<const uint32_t*>(cw + 4096);
+    const uint32_t w10 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16);
+    const uint32_t w11 = *reinterpret_cast<const uint32_t*>(cw + 8 * 16 + 4096);
     // sub-pair q of a word: nibbles q, 4 + q; q = 0, 1 straight from the word, q = 2, 3 from w >> 8
     const uint32_t v00 = w00 >> 8, v01 = w01 >> 8, v10 = w10 >> 8, v11 = w11 >> 8;
 #pragma unroll
@@ -200,19 +226,23 @@ __device__ __forceinline__ void stage_math(const uint8_t* st, const LaneOff& lo,
             const uint4& xv = hk ? xb[mb] : xa[mb];
             const uint32_t b0 = (s & 1) ? xv.z : xv.x;
             const uint32_t b1 = (s & 1) ? xv.w : xv.y;
-            mma_f16(acc[s][mb], a0, a1, a2, a3, b0, b1);
+            mma_f16(acc[nb][s & 1][mb], a0, a1, a2, a3, b0, b1);
         }
+    }
     }
 }
 
 // y (fp16) of the lane's fragment values: v[mb] = (column col0 + n0 + g, rows 8 mb + 2t, +1) and
 // (column + 8, same rows)
 template <int MB>
-__device__ __forceinline__ void store_y(const GemvParams& p, int col0, int n0, int lane, const float (&v)[MB][4]) {
+__device__ __forceinline__ void store_y(const GemvParams& p, int col0, int n0, int lane, const float (&vv)[2][MB][4]) {
     const int g = lane >> 2, t = lane & 3;
-    const int col = col0 + n0 + g;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) {
+        const int col = col0 + n0 + 16 * nb + g;
+        const float (&v)[MB][4] = vv[nb];
         const int m = 8 * mb + 2 * t;
         if (m < p.M) {
             p.y[int64_t(m) * p.N + col] = __float2half_rn(v[mb][0]);
@@ -226,7 +256,7 @@ __device__ __forceinline__ void store_y(const GemvParams& p, int col0, int n0, i
 }
 
 template <int MB>
-__global__ void __launch_bounds__(kThreadsV, 1)
+__global__ void __launch_bounds__(kThreadsV, kCtasV)
 dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesV * kStageBytes);
@@ -259,7 +289,7 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
             int kb = int(i % p.KB);
             for (int j = r; j < n; j += kProducers, i += kProducers) {
                 const int s = j & (kStagesV - 1);
-                mbar_wait(empty + s, ((j / kStagesV) & 1) ^ 1);
+                mbar_wait_sleep(empty + s, ((j / kStagesV) & 1) ^ 1);
                 const uint32_t dst = su32(smem + s * kStageBytes);
                 mbar_expect_tx(full + s, bytes);
                 bulk_g2s(dst, p.panels + i * kPanelData, kPanelData, full + s, pol_w);
@@ -276,12 +306,13 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         return;
     }
 
-    // ---------------- consumers: warp owns columns n0 .. n0 + 15 of the tile
-    const int n0 = warp * 16;
+    // ---------------- consumers: warp owns columns n0 .. n0 + 31 of the tile (two row blocks)
+    const int n0 = warp * 32;
     const int t = lane & 3, g = lane >> 2;
     const LaneOff lo{uint32_t((n0 + g) * 16 + 4 * t),
                      uint32_t(kGemmTileN * kGemmTileK / 2 + (n0 >> 6) * 256 + 32 * t),
-                     uint32_t(kXOff + g * 128 + 16 * t)};
+                     uint32_t(kXOff + g * 128 + 16 * t),
+                     (g < p.M ? 1u : 0u) | (8 + g < p.M ? 2u : 0u)};
     {   // the CTA's clamp flag: OR of its panels' flags (first word of each 16-byte flag)
         const uint32_t* flags = reinterpret_cast<const uint32_t*>(p.panels + p.total * kPanelData);
         uint32_t f = 0;
@@ -291,7 +322,7 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
     }
     const bool clamp_cta = flag[1] != 0u;
     const uint32_t magic = magic_h2();
-    float acc[4][MB][4];
+    float acc[2][2][MB][4];    // [row block][step parity][8-row block of x][fragment]
     int s = 0;                 // ring slot and its phase
     uint32_t ph = 0;
     int64_t i = i0;
@@ -301,22 +332,24 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         const int64_t seg_end = min(i1, (tile + 1) * p.KB);
         const bool whole = (i == tile * p.KB) && (seg_end == (tile + 1) * p.KB);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) acc[q][mb][0] = acc[q][mb][1] = acc[q][mb][2] = acc[q][mb][3] = 0.0f;
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb)
+                    acc[nb][q][mb][0] = acc[nb][q][mb][1] = acc[nb][q][mb][2] = acc[nb][q][mb][3] = 0.0f;
         auto run = [&](auto clamp_tag) {
             constexpr bool kClamp = decltype(clamp_tag)::value;
             int left = int(seg_end - i);
 #if FLEXQ_GEMV_PROBE < 3
-            // two stages per iteration: their loads and conversions interleave (the stage's own
-            // dependency chain -- shared load, LOP3, HADD2, HFMA2, HMMA -- is long against 4 warps
-            // per scheduler); both are released together
+            // two stages per iteration: their loads and conversions interleave; both are
+            // released together
 #pragma unroll 1
             for (; left >= 2; left -= 2) {
                 const int s1 = s + 1 == kStagesV ? 0 : s + 1;
                 const uint32_t ph1 = s1 == 0 ? ph ^ 1u : ph;
-                mbar_wait(full + s, ph);
-                mbar_wait(full + s1, ph1);
+                mbar_wait_sleep(full + s, ph);
+                mbar_wait_sleep(full + s1, ph1);
                 stage_math<MB, kClamp>(smem + s * kStageBytes, lo, magic, acc);
                 stage_math<MB, kClamp>(smem + s1 * kStageBytes, lo, magic, acc);
                 __syncwarp();
@@ -330,10 +363,10 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
 #endif
 #pragma unroll 1
             for (; left > 0; --left) {
-                mbar_wait(full + s, ph);
+                mbar_wait_sleep(full + s, ph);
                 const uint8_t* st = smem + s * kStageBytes;
 #if FLEXQ_GEMV_PROBE >= 3
-                if (lane == 0 && *reinterpret_cast<const uint32_t*>(st) == 0x12345678u) acc[0][0][0] += 1.0f;
+                if (lane == 0 && *reinterpret_cast<const uint32_t*>(st) == 0x12345678u) acc[0][0][0][0] += 1.0f;
 #else
                 stage_math<MB, kClamp>(st, lo, magic, acc);
 #endif
@@ -348,11 +381,13 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         if (clamp_cta) run(BoolTag<true>{});
         else run(BoolTag<false>{});
         i = seg_end;
-        float v[MB][4];   // the four step accumulators, summed in a fixed order
+        float v[2][MB][4];   // the two step-parity accumulators, summed in a fixed order
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
+        for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) v[mb][r] = (acc[0][mb][r] + acc[1][mb][r]) + (acc[2][mb][r] + acc[3][mb][r]);
+            for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[nb][mb][r] = acc[nb][0][mb][r] + acc[nb][1][mb][r];
         const int col0 = int(tile) * kGemmTileN;
         if (whole) {
             store_y<MB>(p, col0, n0, lane, v);
@@ -361,12 +396,15 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         // a split tile: partial [256 n][16 m] in this CTA's slot (0: its first tile, 1: its last)
         const int slot = tile == first_tile ? 0 : 1;
         float* part = p.partials + (int64_t(c) * 2 + slot) * kGemmTileN * 16;
-        const int cl0 = n0 + g;
 #pragma unroll
-        for (int mb = 0; mb < MB; ++mb) {
-            const int m = 8 * mb + 2 * t;
-            __stcg(reinterpret_cast<float2*>(part + cl0 * 16 + m), make_float2(v[mb][0], v[mb][1]));
-            __stcg(reinterpret_cast<float2*>(part + (cl0 + 8) * 16 + m), make_float2(v[mb][2], v[mb][3]));
+        for (int nb = 0; nb < 2; ++nb) {
+            const int cl0 = n0 + 16 * nb + g;
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+                const int m = 8 * mb + 2 * t;
+                __stcg(reinterpret_cast<float2*>(part + cl0 * 16 + m), make_float2(v[nb][mb][0], v[nb][mb][1]));
+                __stcg(reinterpret_cast<float2*>(part + (cl0 + 8) * 16 + m), make_float2(v[nb][mb][2], v[nb][mb][3]));
+            }
         }
         __threadfence();
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
@@ -380,21 +418,27 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
         if (*flag) {
             __threadfence();
-            float y[MB][4];
+            float y[2][MB][4];
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) y[mb][0] = y[mb][1] = y[mb][2] = y[mb][3] = 0.0f;
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) y[nb][mb][0] = y[nb][mb][1] = y[nb][mb][2] = y[nb][mb][3] = 0.0f;
             for (int cc = cf; cc <= cl; ++cc) {   // contributors in CTA order: deterministic
                 const int sl = (tile == range_start(p.total, cc, p.G) / p.KB) ? 0 : 1;
                 const float* pp = p.partials + (int64_t(cc) * 2 + sl) * kGemmTileN * 16;
 #pragma unroll
-                for (int mb = 0; mb < MB; ++mb) {
-                    const int m = 8 * mb + 2 * t;
-                    const float2 a = __ldcg(reinterpret_cast<const float2*>(pp + cl0 * 16 + m));
-                    const float2 b = __ldcg(reinterpret_cast<const float2*>(pp + (cl0 + 8) * 16 + m));
-                    y[mb][0] += a.x;
-                    y[mb][1] += a.y;
-                    y[mb][2] += b.x;
-                    y[mb][3] += b.y;
+                for (int nb = 0; nb < 2; ++nb) {
+                    const int cl0 = n0 + 16 * nb + g;
+#pragma unroll
+                    for (int mb = 0; mb < MB; ++mb) {
+                        const int m = 8 * mb + 2 * t;
+                        const float2 a2 = __ldcg(reinterpret_cast<const float2*>(pp + cl0 * 16 + m));
+                        const float2 b2 = __ldcg(reinterpret_cast<const float2*>(pp + (cl0 + 8) * 16 + m));
+                        y[nb][mb][0] += a2.x;
+                        y[nb][mb][1] += a2.y;
+                        y[nb][mb][2] += b2.x;
+                        y[nb][mb][3] += b2.y;
+                    }
                 }
             }
             store_y<MB>(p, col0, n0, lane, y);
@@ -407,7 +451,7 @@ dequant_gemv_kernel(const __grid_constant__ CUtensorMap map_x, const GemvParams 
 
 size_t dequant_gemv_workspace_bytes(int64_t n) {
     const size_t tickets = size_t((n / kGemmTileN * 4 + 255) / 256 * 256);
-    return tickets + size_t(kGemmMaxGrid) * 2 * kGemmTileN * 16 * sizeof(float);
+    return tickets + size_t(kCtasV) * kGemmMaxGrid * 2 * kGemmTileN * 16 * sizeof(float);
 }
 
 cudaError_t launch_dequant_gemv(const void* x, const void* panels, int64_t M, int64_t K, int64_t N, void* y,
@@ -415,7 +459,8 @@ cudaError_t launch_dequant_gemv(const void* x, const void* panels, int64_t M, in
     const int KB = int(K / kGemmTileK);
     const int64_t total = (N / kGemmTileN) * KB;
     const int sms = device_sm_count();
-    const int G = int(total < sms ? total : (sms < kGemmMaxGrid ? sms : kGemmMaxGrid));
+    const int cap = kCtasV * (sms < kGemmMaxGrid ? sms : kGemmMaxGrid);
+    const int G = int(total < cap ? total : cap);
     {   // the shared-memory attribute, once per device (under a lock)
         static cudaError_t attr_err[kMaxDevices];
         static std::once_flag attr_once[kMaxDevices];
