@@ -27,7 +27,6 @@ SOURCES = {
     "flexq_api.cu": [],
     "quant.cu": ["-fmad=false", "-prec-div=true", "-ftz=false"],
     "decode_attention.cu": [],
-    "decode_attention_coop.cu": [],
     "decode_attention_topk.cu": [],
     "decode_attention_variants.cu": [],
     "dequant_gemm.cu": [],

@@ -48,7 +48,6 @@ constexpr int kMaxPieces = 32;      // pieces per head (partial slots per head)
 constexpr int kMinPieceChunks = 2;  // smallest piece
 constexpr int kCtasPerSm = 16;      // one-warp CTAs resident per SM (register / smem budget)
 constexpr int kMaxCtrs = 16;        // ticket counters, 64 B apart in the 1 KB control block
-constexpr int kCoopHeadsPerWarpX100 = 120;   // below: the cooperative schedule (B200 sweep)
 constexpr int kRetire = 16 * kMaxCtrs;
 
 #ifndef FLEXQ_ATTN_TRACE
@@ -674,18 +673,6 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap) 
 // Score buffer sized to the context: 576 tokens covers every prompt-512 step in one piece
 // per head, 1088 the prompt-1024 steps; longer contexts are cut into 1088-token pieces.
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream) {
-    // few heads per resident warp: the cooperative schedule (decode_attention_coop.cu);
-    // FLEXQ_ATTN_COOP=0 / 1 forces it off / on (tuning and tests)
-    static const int coop_env = [] {
-        const char* e = getenv("FLEXQ_ATTN_COOP");
-        return e ? atoi(e) : -1;
-    }();
-    if (coop_env != 0 && coop_attention_fits(a.head_dim, a.cur_len)) {
-        const int bh = a.batch * a.heads;
-        const int w2 = device_sm_count() * kCtasPerSm;
-        const bool few = int64_t(bh) * 100 < int64_t(w2) * kCoopHeadsPerWarpX100;
-        if (coop_env == 1 || (few && bh * 4 >= device_sm_count())) return launch_decode_attention_coop(a, stream);
-    }
     if (a.head_dim == 128)
         return a.cur_len <= 576 ? launch_ring<128, 576>(a, stream) : launch_ring<128, 1088>(a, stream);
     return a.cur_len <= 576 ? launch_ring<64, 576>(a, stream) : launch_ring<64, 1088>(a, stream);

@@ -75,10 +75,6 @@ size_t attention_workspace_bytes(int batch, int heads, int head_dim, int t_cap);
 // Longest context of the (4, 64) tensor-core kernel: 16 pieces of its 1088-token score buffer.
 constexpr int kDenseMaxTokens = 16 * 1088;
 cudaError_t launch_decode_attention(const AttnArgs& a, cudaStream_t stream);
-// Few-heads launches (decode_attention_coop.cu): one head per CTA at a time, its stages split over
-// several consumer warps fed by a producer warp through a deep ring; cur_len <= 576.
-bool coop_attention_fits(int head_dim, int cur_len);
-cudaError_t launch_decode_attention_coop(const AttnArgs& a, cudaStream_t stream);
 
 // Decode attention over the (b, g) variant caches (NEXT-3; decode_attention_variants.cu):
 // token-major bit-stream rows for K and V, CUDA-core arithmetic, split-K over 128-token tiles.

@@ -34,15 +34,6 @@ elif what == "attn":
         fq.flexq_append_kv(k, k, c, pos=0)
         q = synth.fill(2, 3, (B, H, D), device=dev)
         fq.flexq_append_decode_attention(q, q, q, c, s + 1)
-elif what == "coop":   # run with FLEXQ_ATTN_COOP=1
-    for (B, H, D, s, n) in ((2, 3, 128, 100, 3), (1, 5, 64, 40, 2), (3, 7, 128, 500, 4)):
-        c = fq.KVCache(B, H, D, s, n, device=dev)
-        k = synth.fill(2, 1, (B, H, s, D), device=dev)
-        fq.flexq_append_kv(k, k, c, pos=0)
-        q = synth.fill(2, 3, (B, H, D), device=dev)
-        for cur in (1, 64, s):
-            fq.flexq_decode_attention(q, c, cur)
-        fq.flexq_append_decode_attention(q, q, q, c, s + n)
 elif what == "tm":
     B, H, D, s, n = 2, 3, 128, 100, 3
     c = fq.KVCache(B, H, D, s, n, device=dev, layout="token_major")
