@@ -511,3 +511,51 @@ def test_topk_short_contexts(orc, cuda, layout):
         assert int(mask.sum()) == B * H * keep
         ref, _, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, cur_len, keep, sel=mask)
         assert_attn_close(out.cpu().numpy(), ref, f"short context {cur_len}")
+
+
+def test_schedule_variants_within_tolerance(orc, cuda, tmp_path):
+    """The tuning schedules (static stream-K, whole-head tickets, ticket pieces, the static prefix
+    + ticket hybrid, one ticket counter, the 3-stage ring) all compute the same attention: each,
+    forced through its environment switch in a fresh process, is within reading Q of the oracle
+    on a launch whose heads get split (B*H = 40 over ~2,400 warps) and on one whose heads do not."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "sched_case.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_2303_06865_b200 import flexq as fq, synth\n"
+        "dev = torch.device('cuda:0')\n"
+        "outs = []\n"
+        "for (B, H, s) in ((2, 20, 600), (16, 160, 300)):\n"
+        "    c = fq.KVCache(B, H, 128, s, 2, device=dev)\n"
+        "    k = synth.fill(63, 1, (B, H, s, 128), device=dev)\n"
+        "    v = synth.fill(63, 2, (B, H, s, 128), device=dev)\n"
+        "    fq.flexq_append_kv(k, v, c, pos=0)\n"
+        "    q = synth.fill(63, 3, (B, H, 128), device=dev)\n"
+        "    kn = synth.fill(63, 4, (B, H, 128), device=dev)\n"
+        "    vn = synth.fill(63, 5, (B, H, 128), device=dev)\n"
+        "    outs.append(fq.flexq_append_decode_attention(q, kn, vn, c, s + 1).cpu().numpy())\n"
+        "np.savez(sys.argv[1], *outs)\n")
+    envs = {"default": {}, "static": {"FLEXQ_ATTN_SPLIT": "100000,0,0"}, "tickets": {"FLEXQ_ATTN_SPLIT": "0,0,0"},
+            "ticket_pieces": {"FLEXQ_ATTN_SPLIT": "0,100,3"}, "hybrid": {"FLEXQ_ATTN_SPLIT": "100000,0,0", "FLEXQ_ATTN_HYBRID": "70,4"},
+            "one_counter": {"FLEXQ_ATTN_CTRS": "1", "FLEXQ_ATTN_SPLIT": "0,0,0"}, "ring3": {"FLEXQ_ATTN_RING": "3"}}
+    refs = []
+    for (B, H, s) in ((2, 20, 600), (16, 160, 300)):
+        k = synth.fill(63, 1, (B, H, s, 128))
+        v = synth.fill(63, 2, (B, H, s, 128))
+        kn = synth.fill(63, 4, (B, H, 1, 128))
+        vn = synth.fill(63, 5, (B, H, 1, 128))
+        okc, ovc = orc.empty_cache(B, H, s + 2, 128), orc.empty_cache(B, H, s + 2, 128)
+        orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+        orc.append_kv(kn.numpy(), vn.numpy(), okc, ovc, s)
+        refs.append(orc.attention_f64(synth.fill(63, 3, (B, H, 128)).numpy(), okc, ovc, s + 1))
+    for name, extra in envs.items():
+        f = tmp_path / f"{name}.npz"
+        r = subprocess.run([sys.executable, str(script), str(f)], env=dict(os.environ, **extra), capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got = np.load(f)
+        for i, ref in enumerate(refs):
+            assert_attn_close(got[f"arr_{i}"], ref, f"schedule {name}, case {i}")
