@@ -220,7 +220,8 @@ __device__ __forceinline__ void load_q_mma(const uint8_t* qs, float qscale, int 
 }
 
 // Pass 1, one 16-token block `blk` of the stage at sb (tokens 16 blk + [0, 16)): scores -> sc
-// (stage-relative index t0 + token), running max mx over tokens < n.
+// (stage-relative index t0 + token), running max mx over tokens < n (per lane: the caller
+// reduces it over the whole warp, xor 1 .. 16).
 template <int D, int NCH>
 __device__ __forceinline__ void k_block_mma(int blk, const KFrag<D>& kf, const uint8_t* sb, float* sc, int t0,
                                             int n, int lane, float& mx) {
@@ -259,17 +260,16 @@ __device__ __forceinline__ void k_block_mma(int blk, const KFrag<D>& kf, const u
     const float hB8 = __half2float(*reinterpret_cast<const __half*>(mr + 8 * C::MB + kf.offB));
     float v0 = fmaf(fmaf(float(c[0] + kf.k256 * c[1]), kf.wA, kf.bA), hA0, fmaf(float(c[1]), kf.wB, kf.bB) * hB0);
     float v8 = fmaf(fmaf(float(c[2] + kf.k256 * c[3]), kf.wA, kf.bA), hA8, fmaf(float(c[3]), kf.wB, kf.bB) * hB8);
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-    v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-    v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
-    if (tok < n) {
-        mx = fmaxf(mx, v0);
-        if (j == 0) sc[t0 + tok] = v0;
-    }
-    if (tok + 8 < n) {
-        mx = fmaxf(mx, v8);
-        if (j == 1) sc[t0 + tok + 8] = v8;
+    // quad sum as a reduce-scatter: after the xor-1 round even lanes hold row r's pair sum and
+    // odd lanes row r + 8's, after the xor-2 round the full sums (the same additions in the same
+    // order as two all-reduces, half the shuffles)
+    const bool odd = j & 1;
+    float v = (odd ? v8 : v0) + __shfl_xor_sync(0xffffffffu, odd ? v0 : v8, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    const int mine = tok + (odd ? 8 : 0);
+    if (mine < n) {
+        mx = fmaxf(mx, v);
+        if (j < 2) sc[t0 + mine] = v;
     }
 }
 

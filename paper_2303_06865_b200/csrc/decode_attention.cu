@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
                 if (owns_new && st == nst - 1) patch(sb, false);
             }
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            for (int o = 1; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             M = mx;
         }
 

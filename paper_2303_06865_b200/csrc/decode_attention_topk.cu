@@ -310,7 +310,7 @@ topk_select_kernel(const SelectParams P) {
                 sb = acquire();
             }
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            for (int o = 1; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             M = mx;   // the largest score is always kept, so M is the kept set's max
         }
 
