@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--fused", action="store_true")
+    ap.add_argument("--dump", default="", help="save the raw per-warp stamps (.npy) for offline analysis")
     a = ap.parse_args()
     w = wl.CONFIGS[a.config]
     B = a.batch or w.batch
@@ -73,6 +74,8 @@ def main():
     rc = fq.lib().flexq_debug_attn_trace(ctypes.c_void_p(buf.ctypes.data), W)
     assert rc == 0, rc
     used = buf[:, 2] > 0
+    if a.dump:
+        np.save(a.dump, buf[used])
     t = buf[used].astype(np.int64)
     t0 = t[:, 0].min()
     res, go, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
