@@ -200,7 +200,13 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
     int p_cur = r0;                        // the producer's next static chunk
     uint32_t tk_raw = 0;
     const int ctr = int(blockIdx.x) % P.nctr;
-    if (r0 >= r1 && P.items > 0 && lane == 0) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);
+    // Pure ticket launches (no static prefix; grid <= items): warp w's first item is ticket w, the
+    // counters deal tickets grid, grid + 1, ... from then on.  (When every warp drew its first
+    // ticket from the counters too, the prefetch of a fast warp's second ticket could take a slow
+    // warp's first: with about one head per warp that warp idled while another walked two heads.)
+    bool tk_static = P.total == 0 && P.items > 0;
+    const int tk_base = P.total == 0 ? int(gridDim.x) : 0;
+    if (!tk_static && r0 >= r1 && P.items > 0 && lane == 0) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);
     Piece pp{0, 0, 0, 0, 1};
     bool p_valid = false, p_new = false;
     int p_stage = 0, p_nst = 0, p_last = 0;
@@ -217,7 +223,8 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
             p_valid = true;
             if (p_cur >= r1 && P.items > 0 && lane == 0) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);
         } else {
-            const int tk = int(__shfl_sync(0xffffffffu, tk_raw, 0)) * P.nctr + ctr;
+            const int tk = tk_static ? int(blockIdx.x) : int(__shfl_sync(0xffffffffu, tk_raw, 0)) * P.nctr + ctr + tk_base;
+            tk_static = false;
             p_valid = P.items > 0 && decode_item(P, tk, pp);
             if (lane == 0 && p_valid) tk_raw = atomicAdd(P.ctrl + 16 * ctr, 1u);   // prefetch the following ticket
             t = P.total + tk;
@@ -490,9 +497,10 @@ constexpr size_t smem_bytes() {
 struct DevInfo {
     int sms = 0;
     int occ = 0;
+    int cap_smem[kCtasPerSm + 1] = {};   // [r]: dynamic smem that leaves at most r CTAs resident per SM
 };
 template <int D, int MAXT, int S, int NCH>
-DevInfo dev_info() {
+const DevInfo& dev_info() {
     constexpr int kMaxDev = 64;
     static DevInfo info[kMaxDev];
     static std::once_flag once[kMaxDev];
@@ -501,12 +509,35 @@ DevInfo dev_info() {
     if (dev < 0 || dev >= kMaxDev) dev = 0;
     std::call_once(once[dev], [dev] {
         auto k = decode_attention_kernel<D, MAXT, S, NCH>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<D, MAXT, S, NCH>()));
+        constexpr int need = int(smem_bytes<D, MAXT, S, NCH>());
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        optin = std::max(optin, need);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
         int sms = 0, o = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, smem_bytes<D, MAXT, S, NCH>());
-        info[dev].sms = sms > 0 ? sms : 148;
-        info[dev].occ = o > 0 ? o : 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32, need);
+        DevInfo& d = info[dev];
+        d.sms = sms > 0 ? sms : 148;
+        d.occ = o > 0 ? o : 1;
+        // the smallest dynamic smem (a multiple of 128 B) at which at most r CTAs fit on an SM
+        for (int r = 1; r <= kCtasPerSm; ++r) {
+            int lo = need, hi = optin;
+            int best = need;
+            while (lo <= hi) {
+                const int mid = (lo + hi) / 2 / 128 * 128;
+                int om = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&om, k, 32, std::max(mid, need));
+                if (om > r) {
+                    lo = mid + 128;
+                } else {
+                    best = std::max(mid, need);
+                    hi = mid - 128;
+                }
+            }
+            d.cap_smem[r] = best;
+        }
+        cudaGetLastError();
     });
     return info[dev];
 }
@@ -630,6 +661,18 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     cfg.gridDim = dim3(unsigned(grid));   // dynamic: no more warps than items
     cfg.blockDim = dim3(32);
     cfg.dynamicSmemBytes = smem_bytes<D, MAXT, S, NCH>();
+    // At most one item per warp: cap the CTAs resident per SM at ceil(items / SMs) by asking for
+    // more (unused) shared memory.  With programmatic dependent launch the CTAs land on the SMs in
+    // the order the previous grid frees them; uncapped, the early SMs took 16 heads and late ones
+    // as few as 4, and the launch lasted as long as the 16-head SMs (B200 trace, batch 18).
+    static const bool cap_env = [] {
+        const char* e = getenv("FLEXQ_ATTN_CAP");
+        return !(e && e[0] == '0');
+    }();
+    if (cap_env && dynamic && P.items <= grid) {
+        const int r = (P.items + di.sms - 1) / di.sms;
+        if (r < di.occ) cfg.dynamicSmemBytes = size_t(di.cap_smem[r]);
+    }
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

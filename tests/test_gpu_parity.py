@@ -129,6 +129,11 @@ ATTN_CASES = [
     ("d128_opt30b_len", 2, 4, 128, 1024, 32, 31, False, 1),          # cur_len 1055: the 1088-token buffer
     ("d128_beyond_buffer", 1, 3, 128, 1500, 8, 2, True, 16),         # cur_len 1502 > 1088: context split
     ("d64_beyond_buffer", 1, 2, 64, 2000, 1, 1, False, 4),           # cur_len 2001
+    # about one head per warp (first ticket = warp index, residency capped at ceil(heads / SMs)):
+    ("d128_one_per_warp", 3, 100, 128, 300, 8, 3, False, 1),         # 300 heads: 2 CTAs per SM
+    ("d128_one_chunk_heads", 8, 40, 128, 30, 4, 2, True, 16),        # cur_len 32: one stage per head
+    ("d128_576", 4, 80, 128, 574, 2, 2, False, 4),                   # cur_len 576: the score buffer, full
+    ("d64_one_per_warp", 10, 32, 64, 200, 4, 2, True, 16),
 ]
 
 
@@ -333,6 +338,8 @@ TOPK_CASES = [
     ("d128_keep_all", 1, 4, 128, 70, 2, 1, False, 1, 1.0),
     ("d128_keep_one", 2, 3, 128, 90, 2, 2, False, 8, 0.0),
     ("d128_opt175b_len", 2, 16, 128, 512, 32, 31, False, 1, 0.1),
+    ("d128_long_1152_buffer", 1, 4, 128, 1100, 2, 1, True, 4, 0.1),   # cur_len 1101: 36 keys per lane
+    ("d64_peaky_half", 2, 5, 64, 400, 2, 1, False, 64, 0.5),
 ]
 
 
@@ -378,6 +385,9 @@ FUSED_CASES = [
     ("d128_first_token_of_chunk", 2, 4, 128, 95, 4, 2, True, 16),  # cur_len 96, 97: chunk boundary
     ("d128_one_token", 3, 2, 128, 0, 2, 1, False, 1),             # cur_len = 1: the new token alone
     ("d128_no_split", 24, 128, 128, 40, 2, 1, False, 4),          # B*H = 3072 units
+    ("d128_fused_one_per_warp", 3, 100, 128, 290, 4, 3, True, 4),
+    ("d64_fused_chunk_edge", 10, 32, 64, 127, 2, 2, False, 1),    # cur_len 128, 129
+    ("d128_opt175b_shard_b18", 18, 96, 128, 541, 2, 2, False, 1),  # the N = 8 shard, cur_len 542, 543
     ("d64_tiny", 4, 12, 64, 512, 1, 1, False, 1),                 # configs[0] with the fused step
     ("d64_full_capacity", 2, 3, 64, 60, 3, 3, True, 16),          # last step: cur_len = T_cap
 ]
@@ -515,7 +525,7 @@ def test_topk_short_contexts(orc, cuda, layout):
 
 def test_schedule_variants_within_tolerance(orc, cuda, tmp_path):
     """The tuning schedules (static stream-K, whole-head tickets, ticket pieces, the static prefix
-    + ticket hybrid, one ticket counter, the 3-stage ring) all compute the same attention: each,
+    + ticket hybrid, one ticket counter, the 3-stage ring, no residency cap, no programmatic dependent launch) all compute the same attention: each,
     forced through its environment switch in a fresh process, is within reading Q of the oracle
     on a launch whose heads get split (B*H = 40 over ~2,400 warps) and on one whose heads do not."""
     import os
@@ -540,7 +550,8 @@ def test_schedule_variants_within_tolerance(orc, cuda, tmp_path):
         "np.savez(sys.argv[1], *outs)\n")
     envs = {"default": {}, "static": {"FLEXQ_ATTN_SPLIT": "100000,0,0"}, "tickets": {"FLEXQ_ATTN_SPLIT": "0,0,0"},
             "ticket_pieces": {"FLEXQ_ATTN_SPLIT": "0,100,3"}, "hybrid": {"FLEXQ_ATTN_SPLIT": "100000,0,0", "FLEXQ_ATTN_HYBRID": "70,4"},
-            "one_counter": {"FLEXQ_ATTN_CTRS": "1", "FLEXQ_ATTN_SPLIT": "0,0,0"}, "ring3": {"FLEXQ_ATTN_RING": "3"}}
+            "one_counter": {"FLEXQ_ATTN_CTRS": "1", "FLEXQ_ATTN_SPLIT": "0,0,0"}, "ring3": {"FLEXQ_ATTN_RING": "3"},
+            "cap_off": {"FLEXQ_ATTN_CAP": "0"}, "pdl_off": {"FLEXQ_PDL": "0"}}
     refs = []
     for (B, H, s) in ((2, 20, 600), (16, 160, 300)):
         k = synth.fill(63, 1, (B, H, s, 128))
