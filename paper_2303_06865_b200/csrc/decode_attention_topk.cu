@@ -13,11 +13,11 @@
 // Two launches:
 //  * topk_select_kernel -- persistent warps, one warp = one (b, h) (no context split; the
 //    per-warp score buffer holds kTopkMaxTokens).  The K pass is the dense kernel's TMA-bulk-
-//    staged tensor-core pass (attn_common.cuh).  Selection is an exact bitwise select on
-//    order-preserving 32-bit keys of the fp32 scores held in registers (one warp-wide REDUX
-//    count per bit, stopping once exactly `keep` keys lie above the candidate); ties at the
-//    threshold key go to the lowest token indices (ballot prefix counts), so the kept set is the
-//    definition's.  The head's kept list (index, weight p_t / l) goes to the workspace.  With
+//    staged tensor-core pass (attn_common.cuh).  Selection is an exact radix select on
+//    order-preserving 32-bit keys of the fp32 scores held in registers (a histogram of 1/16-wide
+//    log2 bins below the max, radix digits only if the threshold bin is crowded, then a rank
+//    among the last <= 32 candidates: radix_select); ties at the threshold key go to
+//    the lowest token indices (ballot prefix counts), so the kept set is the definition's.  The head's kept list (index, weight p_t / l) goes to the workspace.  With
 //    the V gather out of this kernel the warp's K stream only pauses for the select.
 //  * topk_gather_kernel -- one warp per (b, h) reads the kept V rows and accumulates
 //    sum w_t V^_t in fp32; groups of rows are loaded before any is used, so the gathers of a
@@ -158,15 +158,25 @@ __device__ __forceinline__ void write_out(__half* dst, const float (&v)[32], flo
     }
 }
 
+// The gather's row loads carry the 64-byte L2 fetch hint (SASS LDG...LTC64B): a kept token's code
+// row is one aligned 64-byte run and its (scale, min) pair 8 bytes, so a larger line fill only
+// drags in neighbours that are mostly not kept (FLEXQ_TOPK_L2HINT=0: no hint, A/B builds).
+#ifndef FLEXQ_TOPK_L2HINT
+#define FLEXQ_TOPK_L2HINT 1
+#endif
+#if FLEXQ_TOPK_L2HINT
+#define FLEXQ_LDG_ROW "ld.global.nc.L1::no_allocate.L2::64B"
+#else
+#define FLEXQ_LDG_ROW "ld.global.nc.L1::no_allocate"
+#endif
 __device__ __forceinline__ uint4 ldg_nc128(const void* p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm volatile(FLEXQ_LDG_ROW ".v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ldg_nc32(const void* p) {
     uint32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile(FLEXQ_LDG_ROW ".u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 
@@ -184,6 +194,152 @@ struct SelectParams {
 __device__ __forceinline__ uint32_t order_key(float f) {
     const uint32_t u = __float_as_uint(f);
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
+}
+
+// One histogram pass of the select: digit(j) in [0, 256) for a candidate key j, -1 otherwise
+// (a larger digit never holds a smaller key).  Counts are 16-bit, packed in pairs (shared atomics);
+// a warp suffix scan finds the digit d holding rank `need` counted from the top, the candidates
+// above it (acc) and in it (cd).
+template <int KPL, typename DigitF>
+__device__ __forceinline__ void top_bin(DigitF digit, int need, int lane, uint32_t* hist, int& d, int& acc, int& cd) {
+    *reinterpret_cast<uint4*>(hist + 4 * lane) = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+        const int b = digit(j);
+        if (b >= 0) atomicAdd(hist + (b >> 1), (b & 1) ? 65536u : 1u);
+    }
+    __syncwarp();
+    const uint4 h = *reinterpret_cast<const uint4*>(hist + 4 * lane);   // bins 8 lane .. 8 lane + 7
+    const int c[8] = {int(h.x & 0xFFFFu), int(h.x >> 16), int(h.y & 0xFFFFu), int(h.y >> 16),
+                      int(h.z & 0xFFFFu), int(h.z >> 16), int(h.w & 0xFFFFu), int(h.w >> 16)};
+    const int own = c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
+    int incl = own;   // candidates in the bins of lanes >= lane
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += v;
+    }
+    const int above = incl - own;
+    const bool mine = above < need && need <= incl;
+    const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    d = 0;
+    acc = above;
+    cd = 0;
+    if (mine) {
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+            if (cd == 0 && acc + c[i] >= need) {
+                d = 8 * lane + i;
+                cd = c[i];
+            } else if (cd == 0) {
+                acc += c[i];
+            }
+        }
+    }
+    d = __shfl_sync(0xffffffffu, d, owner);
+    acc = __shfl_sync(0xffffffffu, acc, owner);
+    cd = __shfl_sync(0xffffffffu, cd, owner);
+}
+
+// The key T of rank `keep` (counting multiplicity) among the n_tok keys of a head (token j 32 + lane
+// is order_key(sc[j 32 + lane]), read from the warp's score buffer on every visit so the keys hold
+// no registers; M = the largest score) and krem = how many keys equal to T are kept (keep - #keys > T):
+// an exact select.
+//  1. Bins of width 1/16 in the log2 domain below the max: digit = 255 - min(255, trunc((M - s) 16)).
+//     Rounded subtraction is monotone, so a larger digit always holds a larger score; the bin of
+//     rank `keep` leaves a few candidates (keep = 10 %: ~3-6).
+//  2. Only if that bin holds more than 32: 8-bit radix digits of the candidates' keys below the
+//     bits they all share, until <= 32 remain or every bit is fixed (then all are equal).
+//  3. The <= 32 candidates are compacted and each ranks itself against the others (key descending,
+//     index ascending -- the order the kept-list code uses for ties at T).
+// ~420 warp instructions per head in the common case, against ~1,950 for the bit-by-bit search
+// this replaced.  sm: 224 words of per-warp scratch (histogram 128, candidate keys 32, indices 32).
+template <int KPL>
+__device__ __forceinline__ void radix_select(const float* sc, int n_tok, int keep, float M, int lane, uint32_t* sm,
+                                             uint32_t& T, int& krem) {
+    auto key = [&](int j) -> uint32_t { return order_key(sc[j * 32 + lane]); };
+    uint32_t* hist = sm;
+    uint32_t* ckey = sm + 128;
+    uint32_t* cidx = sm + 160;
+    auto bin0 = [&](int j) -> int {
+        if (j * 32 + lane >= n_tok) return -1;
+        const float u = (M - sc[j * 32 + lane]) * 16.0f;
+        return 255 - min(255, __float2int_rz(u));
+    };
+    int d0, acc, cd;
+    top_bin<KPL>(bin0, keep, lane, hist, d0, acc, cd);
+    int need = keep - acc;
+    uint32_t pre = 0u, hi = 0u;   // candidates: bin0 == d0 and (key & hi) == pre
+    if (cd > 32) {
+        uint32_t kx = 0u, kn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            if (bin0(j) == d0) {
+                kx = max(kx, key(j));
+                kn = min(kn, key(j));
+            }
+        }
+        kx = __reduce_max_sync(0xffffffffu, kx);
+        kn = __reduce_min_sync(0xffffffffu, kn);
+        if (kx == kn) {   // every candidate equal: the lowest `need` indices among them
+            T = kx;
+            krem = need;
+            return;
+        }
+        const int hb = 31 - __clz(kx ^ kn);   // the candidates share the bits above hb
+        int shift = max(0, hb - 7);
+        hi = ~((2u << hb) - 1u);
+        pre = kx & hi;
+#pragma unroll 1
+        for (;;) {
+            auto digit = [&](int j) -> int {
+                return (bin0(j) == d0 && (key(j) & hi) == pre) ? int((key(j) >> shift) & 255u) : -1;
+            };
+            int d;
+            top_bin<KPL>(digit, need, lane, hist, d, acc, cd);
+            need -= acc;
+            pre |= uint32_t(d) << shift;
+            hi |= 255u << shift;
+            if (shift == 0) {   // every bit fixed: the candidates are equal
+                T = pre;
+                krem = need;
+                return;
+            }
+            if (cd <= 32) break;
+            shift = max(0, shift - 8);
+        }
+    }
+    // at most 32 candidates: compact them, each ranks itself (key desc, index asc)
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int base = 0;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+        const int t = j * 32 + lane;
+        const bool cnd = bin0(j) == d0 && (key(j) & hi) == pre;
+        const unsigned b = __ballot_sync(0xffffffffu, cnd);
+        if (cnd) {
+            const int pos = base + __popc(b & lt_mask);
+            ckey[pos] = key(j);
+            cidx[pos] = uint32_t(t);
+        }
+        base += __popc(b);
+    }
+    __syncwarp();
+    const bool live = lane < base;
+    const uint32_t kk = live ? ckey[lane] : 0u;
+    const uint32_t ii = live ? cidx[lane] : 0u;
+    int rank = 0;
+#pragma unroll 1
+    for (int m = 0; m < base; ++m) {
+        const uint32_t km = __shfl_sync(0xffffffffu, kk, m);
+        const uint32_t im = __shfl_sync(0xffffffffu, ii, m);
+        rank += (km > kk || (km == kk && im < ii)) ? 1 : 0;
+    }
+    const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
+    T = __shfl_sync(0xffffffffu, kk, at);
+    krem = need - __popc(__ballot_sync(0xffffffffu, live && kk > T));
+    __syncwarp();   // the scratch is reused (kept list)
 }
 
 // Kernel 1: scores of every cached token (the dense kernel's tensor-core K pass over a TMA-bulk
@@ -315,52 +471,24 @@ topk_select_kernel(const SelectParams P) {
         }
 
         // ------------------------------------------------ select: key T of rank `keep`
-        // Keys live in registers (token j * 32 + lane); T is built bit by bit from the
-        // top: a bit is set when at least `keep` keys are >= the candidate.  The search
-        // stops as soon as exactly `keep` keys are >= the candidate (then every kept
-        // key is >= T and no tie needs breaking); otherwise T ends as the exact key of
-        // rank `keep`.  Padding slots hold key 0, below every candidate.
+        // radix_select finds the key T of rank `keep` and how many keys equal to T are kept
+        // (keys: order_key of the scores, token j * 32 + lane; padding slots are never candidates)
         constexpr int KPL = MAXT / 32;
-        uint32_t key[KPL];
-#pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const int t = j * 32 + lane;
-            key[j] = t < n_tok ? order_key(scores[t]) : 0u;
-        }
         uint32_t T = 0u;
-        bool exact = false;
-#pragma unroll 1
-        for (int bit = 31; bit >= 0; --bit) {
-            const uint32_t cand = T | (1u << bit);
-            int c = 0;
-#pragma unroll
-            for (int j = 0; j < KPL; ++j) c += key[j] >= cand ? 1 : 0;
-            c = int(__reduce_add_sync(0xffffffffu, uint32_t(c)));
-            if (c >= keep) {
-                T = cand;
-                if (c == keep) {
-                    exact = true;
-                    break;
-                }
-            }
-        }
+        int krem_sel = 0;
+        radix_select<KPL>(scores, n_tok, keep, M, lane, reinterpret_cast<uint32_t*>(kept), T, krem_sel);
         // kept: key > T, or key == T among the first krem such tokens by index; the list is
         // built in ascending token order with its weights p_t = 2^(s_t - M)
         float l = 0.0f;
         {
-            int krem = keep;
-            if (!exact) {
-                int gt = 0;
-#pragma unroll
-                for (int j = 0; j < KPL; ++j) gt += key[j] > T ? 1 : 0;
-                krem = keep - int(__reduce_add_sync(0xffffffffu, uint32_t(gt)));
-            }
+            const int krem = krem_sel;
             int base = 0, ties = 0;
 #pragma unroll
             for (int j = 0; j < KPL; ++j) {
                 if (j * 32 >= n_tok) break;
-                const bool gt = key[j] > T;
-                const bool eq = key[j] == T;
+                const uint32_t kj = j * 32 + lane < n_tok ? order_key(scores[j * 32 + lane]) : 0u;
+                const bool gt = kj > T;
+                const bool eq = kj == T;
                 const unsigned beq = __ballot_sync(0xffffffffu, eq);
                 const bool keepit = gt || (eq && ties + __popc(beq & lt_mask) < krem);
                 const unsigned bk = __ballot_sync(0xffffffffu, keepit);
