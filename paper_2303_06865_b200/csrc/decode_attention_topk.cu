@@ -13,14 +13,15 @@
 // Two launches:
 //  * topk_select_kernel -- persistent warps, one warp = one (b, h) (no context split; the
 //    per-warp score buffer holds kTopkMaxTokens).  The K pass is the dense kernel's TMA-bulk-
-//    staged tensor-core pass (attn_common.cuh).  Selection is an exact radix select on
-//    order-preserving 32-bit keys of the fp32 scores held in registers (a histogram of 1/16-wide
-//    log2 bins below the max, radix digits only if the threshold bin is crowded, then a rank
-//    among the last <= 32 candidates: radix_select); ties at the threshold key go to
-//    the lowest token indices (ballot prefix counts), so the kept set is the definition's.  The head's kept list (index, weight p_t / l) goes to the workspace.  With
-//    the V gather out of this kernel the warp's K stream only pauses for the select.
+//    staged tensor-core pass (attn_common.cuh).  Selection is exact: a histogram of 1/16-wide
+//    log2 bins below the max finds the bin of rank `keep`; tokens of higher bins are kept, the
+//    few in that bin rank themselves (key descending, index ascending; radix digits first if it
+//    holds more than 32: refine_bin), so ties go to the lowest token indices and the kept set is
+//    the definition's.  The head's kept list (index, unnormalised weight p_t) goes to the
+//    workspace.  With the V gather out of this kernel the warp's K stream only pauses for the
+//    select.
 //  * topk_gather_kernel -- one warp per (b, h) reads the kept V rows and accumulates
-//    sum w_t V^_t in fp32; groups of rows are loaded before any is used, so the gathers of a
+//    sum p_t V^_t / sum p_t in fp32; groups of rows are loaded before any is used, so the gathers of a
 //    head are in flight together.  In the token-major layout (FLEXQ_KV_TOKEN_MAJOR) a kept
 //    token is one contiguous 64-byte row (D = 128); in the dense layout it is spread over its
 //    256-byte quad row (the price of the dense kernel's operand order).
@@ -185,7 +186,7 @@ struct SelectParams {
     const uint8_t* kc;
     int32_t* sel;        // optional [bh][keep] kept token indices (ascending)
     int32_t* kidx;       // [bh][keep] kept token indices (workspace)
-    float* kw;           // [bh][keep] their softmax weights, renormalised over the kept set
+    float* kw;           // [bh][keep] their unnormalised softmax weights 2^(s_t - M) (the gather renormalises)
     uint32_t* ctrl;      // [0] next ticket, [1] finished warps (workspace)
     int bh_total, chunks, cur_len, keep;
     float qscale;
@@ -242,86 +243,69 @@ __device__ __forceinline__ void top_bin(DigitF digit, int need, int lane, uint32
     cd = __shfl_sync(0xffffffffu, cd, owner);
 }
 
-// The key T of rank `keep` (counting multiplicity) among the n_tok keys of a head (token j 32 + lane
-// is order_key(sc[j 32 + lane]), read from the warp's score buffer on every visit so the keys hold
-// no registers; M = the largest score) and krem = how many keys equal to T are kept (keep - #keys > T):
-// an exact select.
-//  1. Bins of width 1/16 in the log2 domain below the max: digit = 255 - min(255, trunc((M - s) 16)).
-//     Rounded subtraction is monotone, so a larger digit always holds a larger score; the bin of
-//     rank `keep` leaves a few candidates (keep = 10 %: ~3-6).
-//  2. Only if that bin holds more than 32: 8-bit radix digits of the candidates' keys below the
-//     bits they all share, until <= 32 remain or every bit is fixed (then all are equal).
-//  3. The <= 32 candidates are compacted and each ranks itself against the others (key descending,
-//     index ascending -- the order the kept-list code uses for ties at T).
-// ~420 warp instructions per head in the common case, against ~1,950 for the bit-by-bit search
-// this replaced.  sm: 224 words of per-warp scratch (histogram 128, candidate keys 32, indices 32).
+// Bin of a score in the select's first histogram: 1/16-wide bins in the log2 domain below the
+// head's max M, digit = 255 - min(255, trunc((M - s) 16)).  Rounded subtraction is monotone, so a
+// larger digit always holds a strictly larger score (and key).
+__device__ __forceinline__ int score_bin(float M, float s) { return 255 - min(255, __float2int_rz((M - s) * 16.0f)); }
+
+// Refinement for a crowded threshold bin (more than 32 candidates; rare): the key T of rank `need`
+// among the candidates (score_bin == d0) and krem = how many candidates equal to T are kept, by
+// 8-bit radix digits of the candidates' keys below the bits they all share, until <= 32 remain
+// (each then ranks itself, key descending, index ascending) or every bit is fixed.
 template <int KPL>
-__device__ __forceinline__ void radix_select(const float* sc, int n_tok, int keep, float M, int lane, uint32_t* sm,
-                                             uint32_t& T, int& krem) {
-    auto key = [&](int j) -> uint32_t { return order_key(sc[j * 32 + lane]); };
+__device__ __forceinline__ void refine_bin(const float* sc, int n_tok, float M, int d0, int need, int lane,
+                                           uint32_t* sm, uint32_t& T, int& krem) {
     uint32_t* hist = sm;
     uint32_t* ckey = sm + 128;
     uint32_t* cidx = sm + 160;
-    auto bin0 = [&](int j) -> int {
-        if (j * 32 + lane >= n_tok) return -1;
-        const float u = (M - sc[j * 32 + lane]) * 16.0f;
-        return 255 - min(255, __float2int_rz(u));
-    };
-    int d0, acc, cd;
-    top_bin<KPL>(bin0, keep, lane, hist, d0, acc, cd);
-    int need = keep - acc;
-    uint32_t pre = 0u, hi = 0u;   // candidates: bin0 == d0 and (key & hi) == pre
-    if (cd > 32) {
-        uint32_t kx = 0u, kn = 0xFFFFFFFFu;
+    auto cand0 = [&](int j) -> bool { return j * 32 + lane < n_tok && score_bin(M, sc[j * 32 + lane]) == d0; };
+    auto key = [&](int j) -> uint32_t { return order_key(sc[j * 32 + lane]); };
+    uint32_t kx = 0u, kn = 0xFFFFFFFFu;
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            if (bin0(j) == d0) {
-                kx = max(kx, key(j));
-                kn = min(kn, key(j));
-            }
+    for (int j = 0; j < KPL; ++j) {
+        if (cand0(j)) {
+            kx = max(kx, key(j));
+            kn = min(kn, key(j));
         }
-        kx = __reduce_max_sync(0xffffffffu, kx);
-        kn = __reduce_min_sync(0xffffffffu, kn);
-        if (kx == kn) {   // every candidate equal: the lowest `need` indices among them
-            T = kx;
+    }
+    kx = __reduce_max_sync(0xffffffffu, kx);
+    kn = __reduce_min_sync(0xffffffffu, kn);
+    if (kx == kn) {   // every candidate equal: the lowest `need` indices among them
+        T = kx;
+        krem = need;
+        return;
+    }
+    const int hb = 31 - __clz(kx ^ kn);   // the candidates share the bits above hb
+    int shift = max(0, hb - 7);
+    uint32_t hi = ~((2u << hb) - 1u);
+    uint32_t pre = kx & hi;
+    int acc, cd;
+#pragma unroll 1
+    for (;;) {
+        auto digit = [&](int j) -> int { return (cand0(j) && (key(j) & hi) == pre) ? int((key(j) >> shift) & 255u) : -1; };
+        int d;
+        top_bin<KPL>(digit, need, lane, hist, d, acc, cd);
+        need -= acc;
+        pre |= uint32_t(d) << shift;
+        hi |= 255u << shift;
+        if (shift == 0) {   // every bit fixed: the candidates are equal
+            T = pre;
             krem = need;
             return;
         }
-        const int hb = 31 - __clz(kx ^ kn);   // the candidates share the bits above hb
-        int shift = max(0, hb - 7);
-        hi = ~((2u << hb) - 1u);
-        pre = kx & hi;
-#pragma unroll 1
-        for (;;) {
-            auto digit = [&](int j) -> int {
-                return (bin0(j) == d0 && (key(j) & hi) == pre) ? int((key(j) >> shift) & 255u) : -1;
-            };
-            int d;
-            top_bin<KPL>(digit, need, lane, hist, d, acc, cd);
-            need -= acc;
-            pre |= uint32_t(d) << shift;
-            hi |= 255u << shift;
-            if (shift == 0) {   // every bit fixed: the candidates are equal
-                T = pre;
-                krem = need;
-                return;
-            }
-            if (cd <= 32) break;
-            shift = max(0, shift - 8);
-        }
+        if (cd <= 32) break;
+        shift = max(0, shift - 8);
     }
-    // at most 32 candidates: compact them, each ranks itself (key desc, index asc)
     const unsigned lt_mask = (1u << lane) - 1u;
     int base = 0;
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
-        const int t = j * 32 + lane;
-        const bool cnd = bin0(j) == d0 && (key(j) & hi) == pre;
+        const bool cnd = cand0(j) && (key(j) & hi) == pre;
         const unsigned b = __ballot_sync(0xffffffffu, cnd);
         if (cnd) {
             const int pos = base + __popc(b & lt_mask);
             ckey[pos] = key(j);
-            cidx[pos] = uint32_t(t);
+            cidx[pos] = uint32_t(j * 32 + lane);
         }
         base += __popc(b);
     }
@@ -339,7 +323,7 @@ __device__ __forceinline__ void radix_select(const float* sc, int n_tok, int kee
     const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
     T = __shfl_sync(0xffffffffu, kk, at);
     krem = need - __popc(__ballot_sync(0xffffffffu, live && kk > T));
-    __syncwarp();   // the scratch is reused (kept list)
+    __syncwarp();
 }
 
 // Kernel 1: scores of every cached token (the dense kernel's tensor-core K pass over a TMA-bulk
@@ -470,46 +454,114 @@ topk_select_kernel(const SelectParams P) {
             M = mx;   // the largest score is always kept, so M is the kept set's max
         }
 
-        // ------------------------------------------------ select: key T of rank `keep`
-        // radix_select finds the key T of rank `keep` and how many keys equal to T are kept
-        // (keys: order_key of the scores, token j * 32 + lane; padding slots are never candidates)
+        // ------------------------------------------------ select (exact: keep largest, ties -> lowest index)
+        //  1. histogram of score_bin over the head (16-bit counters packed in pairs, shared atomics)
+        //     and the bin d0 holding rank `keep`: every token of a higher bin is kept (acc of them),
+        //     `need` more come from the cd tokens of bin d0 (keep = 10 %: a handful);
+        //  2. one pass: kept tokens of higher bins go straight to the workspace list (index and
+        //     unnormalised weight p_t = 2^(s_t - M), the gather renormalises), bin-d0
+        //     candidates to a shared list;
+        //  3. <= 32 candidates rank themselves (key descending, index ascending) and the first `need`
+        //     append to the list; a crowded bin (> 32) is refined by radix digits (refine_bin).
+        // ~600 warp instructions per head (the bit-by-bit search over 18 keys per lane: ~1,950).
+        // The list is not in token order (the gather does not care); the optional `sel` output is
+        // written in ascending order by one more pass.
         constexpr int KPL = MAXT / 32;
-        uint32_t T = 0u;
-        int krem_sel = 0;
-        radix_select<KPL>(scores, n_tok, keep, M, lane, reinterpret_cast<uint32_t*>(kept), T, krem_sel);
-        // kept: key > T, or key == T among the first krem such tokens by index; the list is
-        // built in ascending token order with its weights p_t = 2^(s_t - M)
-        float l = 0.0f;
+        uint32_t* sm = reinterpret_cast<uint32_t*>(kept);   // 224 words: histogram, candidate keys / indices
+        int d0, acc, cd;
         {
-            const int krem = krem_sel;
+            auto bin = [&](int j) -> int { return j * 32 + lane < n_tok ? score_bin(M, scores[j * 32 + lane]) : -1; };
+            top_bin<KPL>(bin, keep, lane, sm, d0, acc, cd);
+        }
+        const int need = keep - acc;
+        const int64_t lo = int64_t(bh) * keep;
+        {
+            int base = 0, cb = 0;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                const int t = j * 32 + lane;
+                const float sv = scores[t];
+                const int b = t < n_tok ? score_bin(M, sv) : -1;
+                const bool def = b > d0;
+                const bool cnd = b == d0 && cd <= 32;
+                const unsigned bd = __ballot_sync(0xffffffffu, def);
+                const unsigned bc = __ballot_sync(0xffffffffu, cnd);
+                if (def) {
+                    const int64_t o = lo + base + __popc(bd & lt_mask);
+                    P.kidx[o] = t;
+                    P.kw[o] = ex2(sv - M);
+                }
+                if (cnd) {
+                    const int pc = cb + __popc(bc & lt_mask);
+                    sm[128 + pc] = order_key(sv);
+                    sm[160 + pc] = uint32_t(t);
+                }
+                base += __popc(bd);
+                cb += __popc(bc);
+            }
+        }
+        uint32_t T = 0u;   // kept candidates: key > T, or key == T among the first krem by index
+        int krem = 0;
+        if (cd <= 32) {
+            __syncwarp();
+            const bool live = lane < cd;
+            const uint32_t kk = live ? sm[128 + lane] : 0u;
+            const uint32_t ii = live ? sm[160 + lane] : 0u;
+            int rank = 0;
+#pragma unroll 1
+            for (int m = 0; m < cd; ++m) {
+                const uint32_t km = __shfl_sync(0xffffffffu, kk, m);
+                const uint32_t im = __shfl_sync(0xffffffffu, ii, m);
+                rank += (km > kk || (km == kk && im < ii)) ? 1 : 0;
+            }
+            const bool kc = live && rank < need;
+            const unsigned bk = __ballot_sync(0xffffffffu, kc);
+            if (kc) {
+                const int64_t o = lo + acc + __popc(bk & lt_mask);
+                P.kidx[o] = int32_t(ii);
+                P.kw[o] = ex2(scores[ii] - M);
+            }
+            const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
+            T = __shfl_sync(0xffffffffu, kk, at);
+            krem = need - __popc(__ballot_sync(0xffffffffu, live && kk > T));
+        } else {
+            refine_bin<KPL>(scores, n_tok, M, d0, need, lane, sm, T, krem);
             int base = 0, ties = 0;
 #pragma unroll
             for (int j = 0; j < KPL; ++j) {
-                if (j * 32 >= n_tok) break;
-                const uint32_t kj = j * 32 + lane < n_tok ? order_key(scores[j * 32 + lane]) : 0u;
-                const bool gt = kj > T;
-                const bool eq = kj == T;
+                const int t = j * 32 + lane;
+                const float sv = scores[t];
+                const bool cnd = t < n_tok && score_bin(M, sv) == d0;
+                const uint32_t kj = order_key(sv);
+                const bool eq = cnd && kj == T;
                 const unsigned beq = __ballot_sync(0xffffffffu, eq);
-                const bool keepit = gt || (eq && ties + __popc(beq & lt_mask) < krem);
-                const unsigned bk = __ballot_sync(0xffffffffu, keepit);
-                if (keepit) {
-                    kept[base + __popc(bk & lt_mask)] = uint16_t(j * 32 + lane);
-                    l += ex2(scores[j * 32 + lane] - M);
+                const bool kc = (cnd && kj > T) || (eq && ties + __popc(beq & lt_mask) < krem);
+                const unsigned bk = __ballot_sync(0xffffffffu, kc);
+                if (kc) {
+                    const int64_t o = lo + acc + base + __popc(bk & lt_mask);
+                    P.kidx[o] = t;
+                    P.kw[o] = ex2(sv - M);
                 }
                 base += __popc(bk);
                 ties += __popc(beq);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
         }
-        __syncwarp();
-        const float inv_l = 1.0f / l;
-        const int64_t lo = int64_t(bh) * keep;
-        for (int j = lane; j < keep; j += 32) {
-            const int t = kept[j];
-            P.kidx[lo + j] = t;
-            P.kw[lo + j] = ex2(scores[t] - M) * inv_l;
-            if (P.sel) P.sel[lo + j] = t;
+        if (P.sel != nullptr) {   // the kept indices in ascending order (optional output)
+            int base = 0, ties = 0;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                const int t = j * 32 + lane;
+                const float sv = scores[t];
+                const int b = t < n_tok ? score_bin(M, sv) : -1;
+                const uint32_t kj = order_key(sv);
+                const bool eq = b == d0 && kj == T;
+                const unsigned beq = __ballot_sync(0xffffffffu, eq);
+                const bool kc = b > d0 || (b == d0 && kj > T) || (eq && ties + __popc(beq & lt_mask) < krem);
+                const unsigned bk = __ballot_sync(0xffffffffu, kc);
+                if (kc) P.sel[lo + base + __popc(bk & lt_mask)] = t;
+                base += __popc(bk);
+                ties += __popc(beq);
+            }
         }
         __syncwarp();   // scores / kept are rewritten by the next unit
     }
@@ -609,7 +661,7 @@ __global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) 
     }
     float v[32];
     const int col0 = reduce_unit<D>(acc, l, bsum, lane, sg, v);
-    write_out<D>(P.out + int64_t(bh) * D + col0, v, 1.0f);   // the weights are already normalised
+    write_out<D>(P.out + int64_t(bh) * D + col0, v, l);   // renormalise over the kept set
 }
 
 template <int D, int NCH, int S, int WPC, int MAXT>

@@ -340,6 +340,7 @@ TOPK_CASES = [
     ("d128_opt175b_len", 2, 16, 128, 512, 32, 31, False, 1, 0.1),
     ("d128_long_1152_buffer", 1, 4, 128, 1100, 2, 1, True, 4, 0.1),   # cur_len 1101: 36 keys per lane
     ("d64_peaky_half", 2, 5, 64, 400, 2, 1, False, 64, 0.5),
+    ("d128_flat_q_crowded_bin", 2, 4, 128, 300, 2, 1, False, 1 / 256, 0.1),   # one 1/16 bin: radix refine
 ]
 
 
