@@ -95,6 +95,7 @@ if __name__ == "__main__":
         print(build(force="--force" in sys.argv, defines=("FLEXQ_ATTN_TRACE=1",), tag="trace"))
     if "--topk-hint-ab" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_L2HINT=0",), tag="nohint"))
+        print(build(force="--force" in sys.argv, defines=("FLEXQ_TOPK_GATHER_MINB=4",), tag="gmin4"))
     if "--topk-ab" in sys.argv:
         for w, m in ((2, 8), (4, 4), (2, 6), (3, 5)):
             print(build(force="--force" in sys.argv, defines=(f"FLEXQ_TOPK_WPC={w}", f"FLEXQ_TOPK_MINB={m}"),

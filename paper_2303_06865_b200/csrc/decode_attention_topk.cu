@@ -475,6 +475,8 @@ topk_select_kernel(const SelectParams P) {
         }
         const int need = keep - acc;
         const int64_t lo = int64_t(bh) * keep;
+        int32_t* const hk = P.kidx + lo;   // the head's list (32-bit offsets below)
+        float* const hw = P.kw + lo;
         {
             int base = 0, cb = 0;
 #pragma unroll
@@ -487,9 +489,9 @@ topk_select_kernel(const SelectParams P) {
                 const unsigned bd = __ballot_sync(0xffffffffu, def);
                 const unsigned bc = __ballot_sync(0xffffffffu, cnd);
                 if (def) {
-                    const int64_t o = lo + base + __popc(bd & lt_mask);
-                    P.kidx[o] = t;
-                    P.kw[o] = ex2(sv - M);
+                    const int o = base + __popc(bd & lt_mask);
+                    hk[o] = t;
+                    hw[o] = ex2(sv - M);
                 }
                 if (cnd) {
                     const int pc = cb + __popc(bc & lt_mask);
@@ -517,9 +519,9 @@ topk_select_kernel(const SelectParams P) {
             const bool kc = live && rank < need;
             const unsigned bk = __ballot_sync(0xffffffffu, kc);
             if (kc) {
-                const int64_t o = lo + acc + __popc(bk & lt_mask);
-                P.kidx[o] = int32_t(ii);
-                P.kw[o] = ex2(scores[ii] - M);
+                const int o = acc + __popc(bk & lt_mask);
+                hk[o] = int32_t(ii);
+                hw[o] = ex2(scores[ii] - M);
             }
             const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
             T = __shfl_sync(0xffffffffu, kk, at);
@@ -538,9 +540,9 @@ topk_select_kernel(const SelectParams P) {
                 const bool kc = (cnd && kj > T) || (eq && ties + __popc(beq & lt_mask) < krem);
                 const unsigned bk = __ballot_sync(0xffffffffu, kc);
                 if (kc) {
-                    const int64_t o = lo + acc + base + __popc(bk & lt_mask);
-                    P.kidx[o] = t;
-                    P.kw[o] = ex2(sv - M);
+                    const int o = acc + base + __popc(bk & lt_mask);
+                    hk[o] = t;
+                    hw[o] = ex2(sv - M);
                 }
                 base += __popc(bk);
                 ties += __popc(beq);
@@ -593,7 +595,10 @@ struct GatherParams {
 // four 16-byte loads of the token's quad row and a byte gather (PRMT).  GB groups of TPI tokens
 // are loaded before any is accumulated (the loads are independent gathers).
 template <int D, bool VTM>
-__global__ void __launch_bounds__(256) topk_gather_kernel(const GatherParams P) {
+#ifndef FLEXQ_TOPK_GATHER_MINB
+#define FLEXQ_TOPK_GATHER_MINB 3   // gather CTAs (of 8 warps) per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(256, FLEXQ_TOPK_GATHER_MINB) topk_gather_kernel(const GatherParams P) {
     constexpr int CB = D / 2, MB = D / 16, CHB = kChunk * (CB + MB);
     constexpr int LPT = D / 32, TPI = 32 / LPT, GB = VTM ? 8 : 4;   // row groups loaded before use
     const int lane = threadIdx.x & 31;
