@@ -246,6 +246,7 @@ __device__ __forceinline__ void top_bin(DigitF digit, int need, int lane, uint32
 // Bin of a score in the select's first histogram: 1/16-wide bins in the log2 domain below the
 // head's max M, digit = 255 - min(255, trunc((M - s) 16)).  Rounded subtraction is monotone, so a
 // larger digit always holds a strictly larger score (and key).
+constexpr int kRankCap = 64;   // candidates of the threshold bin ranked directly (two per lane)
 __device__ __forceinline__ int score_bin(float M, float s) { return 255 - min(255, __float2int_rz((M - s) * 16.0f)); }
 
 // Refinement for a crowded threshold bin (more than 32 candidates; rare): the key T of rank `need`
@@ -461,13 +462,13 @@ topk_select_kernel(const SelectParams P) {
         //  2. one pass: kept tokens of higher bins go straight to the workspace list (index and
         //     unnormalised weight p_t = 2^(s_t - M), the gather renormalises), bin-d0
         //     candidates to a shared list;
-        //  3. <= 32 candidates rank themselves (key descending, index ascending) and the first `need`
-        //     append to the list; a crowded bin (> 32) is refined by radix digits (refine_bin).
+        //  3. <= 64 candidates rank themselves (key descending, index ascending) and the first `need`
+        //     append to the list; a crowded bin (> 64) is refined by radix digits (refine_bin).
         // ~600 warp instructions per head (the bit-by-bit search over 18 keys per lane: ~1,950).
         // The list is not in token order (the gather does not care); the optional `sel` output is
         // written in ascending order by one more pass.
         constexpr int KPL = MAXT / 32;
-        uint32_t* sm = reinterpret_cast<uint32_t*>(kept);   // 224 words: histogram, candidate keys / indices
+        uint32_t* sm = reinterpret_cast<uint32_t*>(kept);   // 256 words: histogram, candidate keys / indices
         int d0, acc, cd;
         {
             auto bin = [&](int j) -> int { return j * 32 + lane < n_tok ? score_bin(M, scores[j * 32 + lane]) : -1; };
@@ -485,7 +486,7 @@ topk_select_kernel(const SelectParams P) {
                 const float sv = scores[t];
                 const int b = t < n_tok ? score_bin(M, sv) : -1;
                 const bool def = b > d0;
-                const bool cnd = b == d0 && cd <= 32;
+                const bool cnd = b == d0 && cd <= kRankCap;
                 const unsigned bd = __ballot_sync(0xffffffffu, def);
                 const unsigned bc = __ballot_sync(0xffffffffu, cnd);
                 if (def) {
@@ -496,7 +497,7 @@ topk_select_kernel(const SelectParams P) {
                 if (cnd) {
                     const int pc = cb + __popc(bc & lt_mask);
                     sm[128 + pc] = order_key(sv);
-                    sm[160 + pc] = uint32_t(t);
+                    sm[128 + kRankCap + pc] = uint32_t(t);
                 }
                 base += __popc(bd);
                 cb += __popc(bc);
@@ -504,28 +505,47 @@ topk_select_kernel(const SelectParams P) {
         }
         uint32_t T = 0u;   // kept candidates: key > T, or key == T among the first krem by index
         int krem = 0;
-        if (cd <= 32) {
+        if (cd <= kRankCap) {
+            // each candidate ranks itself against all of them (key descending, index ascending);
+            // up to two per lane, so a group of up to 64 equal scores (e.g. repeated rows) is ranked
+            // here rather than refined digit by digit
             __syncwarp();
-            const bool live = lane < cd;
-            const uint32_t kk = live ? sm[128 + lane] : 0u;
-            const uint32_t ii = live ? sm[160 + lane] : 0u;
-            int rank = 0;
+            const bool live0 = lane < cd, live1 = lane + 32 < cd;
+            const uint32_t k0 = live0 ? sm[128 + lane] : 0u, i0 = live0 ? sm[128 + kRankCap + lane] : 0u;
+            const uint32_t k1 = live1 ? sm[160 + lane] : 0u, i1 = live1 ? sm[160 + kRankCap + lane] : 0u;
+            int r0 = 0, r1 = 0;
+            const int c0 = min(cd, 32);
 #pragma unroll 1
-            for (int m = 0; m < cd; ++m) {
-                const uint32_t km = __shfl_sync(0xffffffffu, kk, m);
-                const uint32_t im = __shfl_sync(0xffffffffu, ii, m);
-                rank += (km > kk || (km == kk && im < ii)) ? 1 : 0;
+            for (int m = 0; m < c0; ++m) {
+                const uint32_t km = __shfl_sync(0xffffffffu, k0, m);
+                const uint32_t im = __shfl_sync(0xffffffffu, i0, m);
+                r0 += (km > k0 || (km == k0 && im < i0)) ? 1 : 0;
+                r1 += (km > k1 || (km == k1 && im < i1)) ? 1 : 0;
             }
-            const bool kc = live && rank < need;
-            const unsigned bk = __ballot_sync(0xffffffffu, kc);
-            if (kc) {
-                const int o = acc + __popc(bk & lt_mask);
-                hk[o] = int32_t(ii);
-                hw[o] = ex2(scores[ii] - M);
+#pragma unroll 1
+            for (int m = 32; m < cd; ++m) {
+                const uint32_t km = __shfl_sync(0xffffffffu, k1, m - 32);
+                const uint32_t im = __shfl_sync(0xffffffffu, i1, m - 32);
+                r0 += (km > k0 || (km == k0 && im < i0)) ? 1 : 0;
+                r1 += (km > k1 || (km == k1 && im < i1)) ? 1 : 0;
             }
-            const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
-            T = __shfl_sync(0xffffffffu, kk, at);
-            krem = need - __popc(__ballot_sync(0xffffffffu, live && kk > T));
+            const bool kc0 = live0 && r0 < need, kc1 = live1 && r1 < need;
+            const unsigned b0 = __ballot_sync(0xffffffffu, kc0), b1 = __ballot_sync(0xffffffffu, kc1);
+            if (kc0) {
+                const int o = acc + __popc(b0 & lt_mask);
+                hk[o] = int32_t(i0);
+                hw[o] = ex2(scores[i0] - M);
+            }
+            if (kc1) {
+                const int o = acc + __popc(b0) + __popc(b1 & lt_mask);
+                hk[o] = int32_t(i1);
+                hw[o] = ex2(scores[i1] - M);
+            }
+            const unsigned a0 = __ballot_sync(0xffffffffu, live0 && r0 == need - 1);
+            const unsigned a1 = __ballot_sync(0xffffffffu, live1 && r1 == need - 1);
+            T = a0 ? __shfl_sync(0xffffffffu, k0, __ffs(a0) - 1) : __shfl_sync(0xffffffffu, k1, __ffs(a1) - 1);
+            krem = need - __popc(__ballot_sync(0xffffffffu, live0 && k0 > T)) -
+                   __popc(__ballot_sync(0xffffffffu, live1 && k1 > T));
         } else {
             refine_bin<KPL>(scores, n_tok, M, d0, need, lane, sm, T, krem);
             int base = 0, ties = 0;

@@ -308,7 +308,12 @@ def test_topk_exact_ties_bit_exact(orc, cuda, D, layout):
     distinct rows, so identical codes + meta give identical scores on both sides) the GPU's
     kept set must equal the oracle's -- score descending, then lowest token index -- with zero
     mismatches; the output is then within reading Q of the oracle on that set."""
-    B, H, T = 2, 3, 150
+    for T in (150, 300):   # ~50 copies of each score (ranked directly), ~100 (refined digit by digit)
+        _topk_ties_case(orc, cuda, D, layout, T)
+
+
+def _topk_ties_case(orc, cuda, D, layout, T):
+    B, H = 2, 3
     base = synth.fill(59, 1, (B, H, 3, D))
     cls = torch.stack([torch.arange(T) % 3, 2 - torch.arange(T) % 3, (torch.arange(T) // 7) % 3])
     k = torch.stack([torch.stack([base[b, h][cls[h]] for h in range(H)]) for b in range(B)])
@@ -318,7 +323,7 @@ def test_topk_exact_ties_bit_exact(orc, cuda, D, layout):
     okc, ovc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
     orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
     q = synth.fill(59, 3, (B, H, D))
-    for keep in (1, 15, 50, 73, 149):
+    for keep in (1, 15, 50, 73, T - 1):
         sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
         out = fq.flexq_decode_attention_topk(q.to(cuda), cache, T, keep, sel=sel)
         torch.cuda.synchronize()
@@ -329,6 +334,46 @@ def test_topk_exact_ties_bit_exact(orc, cuda, D, layout):
                 mask[b, h, sel.cpu().numpy()[b, h]] = 1
         assert int((mask != omask).sum()) == 0, f"keep={keep}: kept sets differ"
         assert_attn_close(out.cpu().numpy(), ref, f"ties keep={keep}")
+
+
+@pytest.mark.parametrize("layout", ["dense", "token_major"])
+def test_topk_repeated_tail(orc, cuda, layout):
+    """The bench's decode step rewrites one k_new row per layer, so its caches end in 31 copies of
+    one K row: a group of equal scores that often lands in the select's threshold bin.  The kept
+    set must be a valid top-`keep` set (ties inside the group broken by lowest index) and the output
+    within reading Q on it."""
+    B, H, D, s, rep = 3, 16, 128, 512, 31
+    T = s + rep
+    k = synth.fill(64, 1, (B, H, T, D))
+    v = synth.fill(64, 2, (B, H, T, D))
+    k[:, :, s:] = k[:, :, s:s + 1]
+    v[:, :, s:] = v[:, :, s:s + 1]
+    cache = fq.KVCache(B, H, D, T, 1, device=cuda, layout=layout)
+    fq.flexq_append_kv(k.to(cuda), v.to(cuda), cache, pos=0)
+    okc, ovc = orc.empty_cache(B, H, T, D), orc.empty_cache(B, H, T, D)
+    orc.append_kv(k.numpy(), v.numpy(), okc, ovc, 0)
+    for qs in (0, 1, 2):
+        q = synth.fill(65 + qs, 3, (B, H, D))
+        keep = fq.topk_keep(T)
+        sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
+        out = fq.flexq_decode_attention_topk(q.to(cuda), cache, T, keep, sel=sel)
+        torch.cuda.synchronize()
+        sel_np = sel.cpu().numpy()
+        _, omask, scores = orc.attention_topk_f64(q.numpy(), okc, ovc, T, keep)
+        mask = np.zeros((B, H, T), np.uint8)
+        for b in range(B):
+            for h in range(H):
+                idx = sel_np[b, h]
+                assert np.all(np.diff(idx) > 0) and idx.min() >= 0 and idx.max() < T, (b, h)
+                mask[b, h, idx] = 1
+                sc = scores[b, h]
+                eps = 1e-4 * max(1.0, np.abs(sc).max())
+                assert sc[idx].min() >= sc[mask[b, h] == 0].max() - eps, (b, h)
+                grp = mask[b, h, s:]            # equal scores: the kept part of the group is a prefix
+                assert np.all(np.diff(grp.astype(np.int8)) <= 0), (b, h, grp)
+        assert (mask != omask).sum() <= 2 * B * H
+        ref, _, _ = orc.attention_topk_f64(q.numpy(), okc, ovc, T, keep, sel=mask)
+        assert_attn_close(out.cpu().numpy(), ref, f"repeated tail q{qs}")
 
 
 TOPK_CASES = [
