@@ -412,7 +412,7 @@ __device__ __forceinline__ void v_stage_mma(VAccM<D>& va, const VLane<D>& vl, co
             // weights < 2^es with es = exponent field - 126 (0 -> tiny, dropped below)
             const int es = int((mb >> 23) & 0xFFu) - 126;
             if (es > va.e[gg]) {                  // warp-uniform: the running scale grows
-                if (vl.gr == gg) {                // flush the lane row's sums of this group (exact)
+                if (vl.gr == gg && va.e[gg] > -100) {   // flush the lane row's sums of this group (exact; none before its first weights)
                     const float f = unit_of(va.e[gg]);
                     const float w0 = vl.w0 * f, w1 = vl.w1 * f;
 #pragma unroll
