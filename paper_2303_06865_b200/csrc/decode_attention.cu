@@ -101,22 +101,16 @@ struct Piece {
 };
 __device__ __forceinline__ bool decode_item(const Params& P, int t, Piece& p) {
     if (t >= P.items) return false;
-
     const int ta = P.na * P.ka;
-    if (t < ta) {
-        p.np = P.ka;
-        const int ha = t / P.ka;
-        p.k = t - ha * P.ka;
-        p.bh = P.hs + ha;
-    } else {
-        const int t2 = t - ta;
-        p.np = P.kb;
-        const int hb = t2 / P.kb;
-        p.k = t2 - hb * P.kb;
-        p.bh = P.hs + P.na + hb;
-    }
-    p.o = p.k * P.nck / p.np;
-    p.nch = (p.k + 1) * P.nck / p.np - p.o;
+    const bool in_a = t < ta;
+    const int np = in_a ? P.ka : P.kb;
+    const int tt = in_a ? t : t - ta;
+    const int h = np == 1 ? tt : tt / np;   // whole heads (np = 1: every BASELINE launch but tiny) skip the divisions
+    p.np = np;
+    p.k = tt - h * np;
+    p.bh = P.hs + (in_a ? 0 : P.na) + h;
+    p.o = np == 1 ? 0 : p.k * P.nck / np;
+    p.nch = np == 1 ? P.nck : (p.k + 1) * P.nck / np - p.o;
     return true;
 }
 
