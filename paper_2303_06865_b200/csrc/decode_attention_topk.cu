@@ -13,13 +13,13 @@
 // Two launches:
 //  * topk_select_kernel -- persistent warps, one warp = one (b, h) (no context split; the
 //    per-warp score buffer holds kTopkMaxTokens).  The K pass is the dense kernel's TMA-bulk-
-//    staged tensor-core pass (attn_common.cuh).  Selection is exact: a histogram of 1/16-wide
-//    log2 bins below the max finds the bin of rank `keep`; tokens of higher bins are kept, the
-//    few in that bin rank themselves (key descending, index ascending; radix digits first if it
-//    holds more than 32: refine_bin), so ties go to the lowest token indices and the kept set is
-//    the definition's.  The head's kept list (index, unnormalised weight p_t) goes to the
-//    workspace.  With the V gather out of this kernel the warp's K stream only pauses for the
-//    select.
+//    staged tensor-core pass (attn_common.cuh).  Selection is an exact bitwise select on
+//    order-preserving 32-bit keys of the fp32 scores held in registers (one warp-wide REDUX
+//    count per bit below the bits all keys share, stopping once exactly `keep` keys lie above
+//    the candidate); ties at the threshold key go to the lowest token indices (ballot prefix
+//    counts), so the kept set is the definition's.  The head's kept list (index, unnormalised
+//    weight p_t) goes to the workspace.  With the V gather out of this kernel the warp's K
+//    stream only pauses for the select.
 //  * topk_gather_kernel -- one warp per (b, h) reads the kept V rows and accumulates
 //    sum p_t V^_t / sum p_t in fp32; groups of rows are loaded before any is used, so the gathers of a
 //    head are in flight together.  In the token-major layout (FLEXQ_KV_TOKEN_MAJOR) a kept
@@ -197,136 +197,6 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
 }
 
-// One histogram pass of the select: digit(j) in [0, 256) for a candidate key j, -1 otherwise
-// (a larger digit never holds a smaller key).  Counts are 16-bit, packed in pairs (shared atomics);
-// a warp suffix scan finds the digit d holding rank `need` counted from the top, the candidates
-// above it (acc) and in it (cd).
-template <int KPL, typename DigitF>
-__device__ __forceinline__ void top_bin(DigitF digit, int need, int lane, uint32_t* hist, int& d, int& acc, int& cd) {
-    *reinterpret_cast<uint4*>(hist + 4 * lane) = make_uint4(0u, 0u, 0u, 0u);
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < KPL; ++j) {
-        const int b = digit(j);
-        if (b >= 0) atomicAdd(hist + (b >> 1), (b & 1) ? 65536u : 1u);
-    }
-    __syncwarp();
-    const uint4 h = *reinterpret_cast<const uint4*>(hist + 4 * lane);   // bins 8 lane .. 8 lane + 7
-    const int c[8] = {int(h.x & 0xFFFFu), int(h.x >> 16), int(h.y & 0xFFFFu), int(h.y >> 16),
-                      int(h.z & 0xFFFFu), int(h.z >> 16), int(h.w & 0xFFFFu), int(h.w >> 16)};
-    const int own = c[0] + c[1] + c[2] + c[3] + c[4] + c[5] + c[6] + c[7];
-    int incl = own;   // candidates in the bins of lanes >= lane
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_down_sync(0xffffffffu, incl, o);
-        if (lane + o < 32) incl += v;
-    }
-    const int above = incl - own;
-    const bool mine = above < need && need <= incl;
-    const int owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-    d = 0;
-    acc = above;
-    cd = 0;
-    if (mine) {
-#pragma unroll
-        for (int i = 7; i >= 0; --i) {
-            if (cd == 0 && acc + c[i] >= need) {
-                d = 8 * lane + i;
-                cd = c[i];
-            } else if (cd == 0) {
-                acc += c[i];
-            }
-        }
-    }
-    d = __shfl_sync(0xffffffffu, d, owner);
-    acc = __shfl_sync(0xffffffffu, acc, owner);
-    cd = __shfl_sync(0xffffffffu, cd, owner);
-}
-
-// Bin of a score in the select's first histogram: 1/16-wide bins in the log2 domain below the
-// head's max M, digit = 255 - min(255, trunc((M - s) 16)).  Rounded subtraction is monotone, so a
-// larger digit always holds a strictly larger score (and key).
-constexpr int kRankCap = 64;   // candidates of the threshold bin ranked directly (two per lane)
-__device__ __forceinline__ int score_bin(float M, float s) { return 255 - min(255, __float2int_rz((M - s) * 16.0f)); }
-
-// Refinement for a crowded threshold bin (more than 32 candidates; rare): the key T of rank `need`
-// among the candidates (score_bin == d0) and krem = how many candidates equal to T are kept, by
-// 8-bit radix digits of the candidates' keys below the bits they all share, until <= 32 remain
-// (each then ranks itself, key descending, index ascending) or every bit is fixed.
-template <int KPL>
-__device__ __forceinline__ void refine_bin(const float* sc, int n_tok, float M, int d0, int need, int lane,
-                                           uint32_t* sm, uint32_t& T, int& krem) {
-    uint32_t* hist = sm;
-    uint32_t* ckey = sm + 128;
-    uint32_t* cidx = sm + 160;
-    auto cand0 = [&](int j) -> bool { return j * 32 + lane < n_tok && score_bin(M, sc[j * 32 + lane]) == d0; };
-    auto key = [&](int j) -> uint32_t { return order_key(sc[j * 32 + lane]); };
-    uint32_t kx = 0u, kn = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < KPL; ++j) {
-        if (cand0(j)) {
-            kx = max(kx, key(j));
-            kn = min(kn, key(j));
-        }
-    }
-    kx = __reduce_max_sync(0xffffffffu, kx);
-    kn = __reduce_min_sync(0xffffffffu, kn);
-    if (kx == kn) {   // every candidate equal: the lowest `need` indices among them
-        T = kx;
-        krem = need;
-        return;
-    }
-    const int hb = 31 - __clz(kx ^ kn);   // the candidates share the bits above hb
-    int shift = max(0, hb - 7);
-    uint32_t hi = ~((2u << hb) - 1u);
-    uint32_t pre = kx & hi;
-    int acc, cd;
-#pragma unroll 1
-    for (;;) {
-        auto digit = [&](int j) -> int { return (cand0(j) && (key(j) & hi) == pre) ? int((key(j) >> shift) & 255u) : -1; };
-        int d;
-        top_bin<KPL>(digit, need, lane, hist, d, acc, cd);
-        need -= acc;
-        pre |= uint32_t(d) << shift;
-        hi |= 255u << shift;
-        if (shift == 0) {   // every bit fixed: the candidates are equal
-            T = pre;
-            krem = need;
-            return;
-        }
-        if (cd <= 32) break;
-        shift = max(0, shift - 8);
-    }
-    const unsigned lt_mask = (1u << lane) - 1u;
-    int base = 0;
-#pragma unroll
-    for (int j = 0; j < KPL; ++j) {
-        const bool cnd = cand0(j) && (key(j) & hi) == pre;
-        const unsigned b = __ballot_sync(0xffffffffu, cnd);
-        if (cnd) {
-            const int pos = base + __popc(b & lt_mask);
-            ckey[pos] = key(j);
-            cidx[pos] = uint32_t(j * 32 + lane);
-        }
-        base += __popc(b);
-    }
-    __syncwarp();
-    const bool live = lane < base;
-    const uint32_t kk = live ? ckey[lane] : 0u;
-    const uint32_t ii = live ? cidx[lane] : 0u;
-    int rank = 0;
-#pragma unroll 1
-    for (int m = 0; m < base; ++m) {
-        const uint32_t km = __shfl_sync(0xffffffffu, kk, m);
-        const uint32_t im = __shfl_sync(0xffffffffu, ii, m);
-        rank += (km > kk || (km == kk && im < ii)) ? 1 : 0;
-    }
-    const int at = __ffs(__ballot_sync(0xffffffffu, live && rank == need - 1)) - 1;
-    T = __shfl_sync(0xffffffffu, kk, at);
-    krem = need - __popc(__ballot_sync(0xffffffffu, live && kk > T));
-    __syncwarp();
-}
-
 // Kernel 1: scores of every cached token (the dense kernel's tensor-core K pass over a TMA-bulk
 // ring), the exact top-`keep` selection, and the kept list with its weights.
 template <int D, int NCH, int S, int WPC, int MAXT>
@@ -341,11 +211,10 @@ topk_select_kernel(const SelectParams P) {
     // each on its own barrier: unit u + 2's q is issued after unit u has read its q for
     // S - 1 <= 2 nst - 1 (the launcher keeps S = 2 for single-stage units)
     constexpr int NQ = 2;
-    constexpr int PW = S * C::STG + NQ * 2 * D + MAXT * 6;   // per warp: ring, q, scores, kept list
+    constexpr int PW = S * C::STG + NQ * 2 * D + MAXT * 4;   // per warp: ring, q, scores
     uint8_t* ring = smem + warp * PW;
     uint8_t* qsm0 = ring + S * C::STG;
     float* scores = reinterpret_cast<float*>(qsm0 + NQ * 2 * D);
-    uint16_t* kept = reinterpret_cast<uint16_t*>(qsm0 + NQ * 2 * D + MAXT * 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WPC * PW) + warp * (S + NQ);   // + the q barriers
 
     const uint64_t policy = evict_first_policy();
@@ -456,131 +325,75 @@ topk_select_kernel(const SelectParams P) {
         }
 
         // ------------------------------------------------ select (exact: keep largest, ties -> lowest index)
-        //  1. histogram of score_bin over the head (16-bit counters packed in pairs, shared atomics)
-        //     and the bin d0 holding rank `keep`: every token of a higher bin is kept (acc of them),
-        //     `need` more come from the cd tokens of bin d0 (keep = 10 %: a handful);
-        //  2. one pass: kept tokens of higher bins go straight to the workspace list (index and
-        //     unnormalised weight p_t = 2^(s_t - M), the gather renormalises), bin-d0
-        //     candidates to a shared list;
-        //  3. <= 64 candidates rank themselves (key descending, index ascending) and the first `need`
-        //     append to the list; a crowded bin (> 64) is refined by radix digits (refine_bin).
-        // ~600 warp instructions per head (the bit-by-bit search over 18 keys per lane: ~1,950).
-        // The list is not in token order (the gather does not care); the optional `sel` output is
-        // written in ascending order by one more pass.
+        // The key T of rank `keep` is built bit by bit over the order-preserving 32-bit keys of
+        // the scores, held in registers (token j * 32 + lane; padding 0, below every candidate):
+        // a bit is set when at least `keep` keys are >= the candidate, and the search stops as
+        // soon as exactly `keep` are.  It starts below the bits every key shares (the highest bit
+        // where the largest and smallest key differ): the sign and exponent bits are common to
+        // most heads' scores, so ~9 of the 32 count rounds were spent confirming them.  Kept:
+        // key > T, or key == T among the first krem by index.  (A shared-atomic histogram of
+        // score bins with a rank among the threshold bin's candidates issued ~25 % fewer
+        // instructions but ran slower inside the bench's decode step: DESIGN.md section 3.)
         constexpr int KPL = MAXT / 32;
-        uint32_t* sm = reinterpret_cast<uint32_t*>(kept);   // 256 words: histogram, candidate keys / indices
-        int d0, acc, cd;
-        {
-            auto bin = [&](int j) -> int { return j * 32 + lane < n_tok ? score_bin(M, scores[j * 32 + lane]) : -1; };
-            top_bin<KPL>(bin, keep, lane, sm, d0, acc, cd);
-        }
-        const int need = keep - acc;
-        const int64_t lo = int64_t(bh) * keep;
-        int32_t* const hk = P.kidx + lo;   // the head's list (32-bit offsets below)
-        float* const hw = P.kw + lo;
-        {
-            int base = 0, cb = 0;
+        uint32_t key[KPL];
+        uint32_t kmin = 0xFFFFFFFFu;
 #pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                const int t = j * 32 + lane;
-                const float sv = scores[t];
-                const int b = t < n_tok ? score_bin(M, sv) : -1;
-                const bool def = b > d0;
-                const bool cnd = b == d0 && cd <= kRankCap;
-                const unsigned bd = __ballot_sync(0xffffffffu, def);
-                const unsigned bc = __ballot_sync(0xffffffffu, cnd);
-                if (def) {
-                    const int o = base + __popc(bd & lt_mask);
-                    hk[o] = t;
-                    hw[o] = ex2(sv - M);
+        for (int j = 0; j < KPL; ++j) {
+            const int t = j * 32 + lane;
+            key[j] = t < n_tok ? order_key(scores[t]) : 0u;
+            if (t < n_tok) kmin = min(kmin, key[j]);
+        }
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        const uint32_t kmax = order_key(M);
+        uint32_t T = kmax;
+        int krem = keep;                     // every key equal: the lowest `keep` indices
+        if (kmin != kmax) {
+            const int hb = 31 - __clz(kmax ^ kmin);
+            T = kmax & ~((2u << hb) - 1u);   // the shared prefix: every key is >= it
+            bool exact = false;
+#pragma unroll 1
+            for (int bit = hb; bit >= 0; --bit) {
+                const uint32_t cand = T | (1u << bit);
+                int c = 0;
+#pragma unroll
+                for (int j = 0; j < KPL; ++j) c += key[j] >= cand ? 1 : 0;
+                c = int(__reduce_add_sync(0xffffffffu, uint32_t(c)));
+                if (c >= keep) {
+                    T = cand;
+                    if (c == keep) {         // exactly `keep` keys >= T: all of them (no tie to break)
+                        exact = true;
+                        break;
+                    }
                 }
-                if (cnd) {
-                    const int pc = cb + __popc(bc & lt_mask);
-                    sm[128 + pc] = order_key(sv);
-                    sm[128 + kRankCap + pc] = uint32_t(t);
-                }
-                base += __popc(bd);
-                cb += __popc(bc);
+            }
+            if (!exact) {
+                int gt = 0;
+#pragma unroll
+                for (int j = 0; j < KPL; ++j) gt += key[j] > T ? 1 : 0;
+                krem = keep - int(__reduce_add_sync(0xffffffffu, uint32_t(gt)));
             }
         }
-        uint32_t T = 0u;   // kept candidates: key > T, or key == T among the first krem by index
-        int krem = 0;
-        if (cd <= kRankCap) {
-            // each candidate ranks itself against all of them (key descending, index ascending);
-            // up to two per lane, so a group of up to 64 equal scores (e.g. repeated rows) is ranked
-            // here rather than refined digit by digit
-            __syncwarp();
-            const bool live0 = lane < cd, live1 = lane + 32 < cd;
-            const uint32_t k0 = live0 ? sm[128 + lane] : 0u, i0 = live0 ? sm[128 + kRankCap + lane] : 0u;
-            const uint32_t k1 = live1 ? sm[160 + lane] : 0u, i1 = live1 ? sm[160 + kRankCap + lane] : 0u;
-            int r0 = 0, r1 = 0;
-            const int c0 = min(cd, 32);
-#pragma unroll 1
-            for (int m = 0; m < c0; ++m) {
-                const uint32_t km = __shfl_sync(0xffffffffu, k0, m);
-                const uint32_t im = __shfl_sync(0xffffffffu, i0, m);
-                r0 += (km > k0 || (km == k0 && im < i0)) ? 1 : 0;
-                r1 += (km > k1 || (km == k1 && im < i1)) ? 1 : 0;
-            }
-#pragma unroll 1
-            for (int m = 32; m < cd; ++m) {
-                const uint32_t km = __shfl_sync(0xffffffffu, k1, m - 32);
-                const uint32_t im = __shfl_sync(0xffffffffu, i1, m - 32);
-                r0 += (km > k0 || (km == k0 && im < i0)) ? 1 : 0;
-                r1 += (km > k1 || (km == k1 && im < i1)) ? 1 : 0;
-            }
-            const bool kc0 = live0 && r0 < need, kc1 = live1 && r1 < need;
-            const unsigned b0 = __ballot_sync(0xffffffffu, kc0), b1 = __ballot_sync(0xffffffffu, kc1);
-            if (kc0) {
-                const int o = acc + __popc(b0 & lt_mask);
-                hk[o] = int32_t(i0);
-                hw[o] = ex2(scores[i0] - M);
-            }
-            if (kc1) {
-                const int o = acc + __popc(b0) + __popc(b1 & lt_mask);
-                hk[o] = int32_t(i1);
-                hw[o] = ex2(scores[i1] - M);
-            }
-            const unsigned a0 = __ballot_sync(0xffffffffu, live0 && r0 == need - 1);
-            const unsigned a1 = __ballot_sync(0xffffffffu, live1 && r1 == need - 1);
-            T = a0 ? __shfl_sync(0xffffffffu, k0, __ffs(a0) - 1) : __shfl_sync(0xffffffffu, k1, __ffs(a1) - 1);
-            krem = need - __popc(__ballot_sync(0xffffffffu, live0 && k0 > T)) -
-                   __popc(__ballot_sync(0xffffffffu, live1 && k1 > T));
-        } else {
-            refine_bin<KPL>(scores, n_tok, M, d0, need, lane, sm, T, krem);
+        // the kept list, straight to the workspace in ascending token order, with the unnormalised
+        // weights p_t = 2^(s_t - M) (the gather renormalises over the kept set): two ballots
+        // and predicated stores per 32 tokens; the optional `sel` output is the same list
+        {
+            const int64_t lo = int64_t(bh) * keep;
+            int32_t* const hk = P.kidx + lo;
+            float* const hw = P.kw + lo;
             int base = 0, ties = 0;
 #pragma unroll
             for (int j = 0; j < KPL; ++j) {
                 const int t = j * 32 + lane;
-                const float sv = scores[t];
-                const bool cnd = t < n_tok && score_bin(M, sv) == d0;
-                const uint32_t kj = order_key(sv);
-                const bool eq = cnd && kj == T;
+                const bool eq = key[j] == T && t < n_tok;
                 const unsigned beq = __ballot_sync(0xffffffffu, eq);
-                const bool kc = (cnd && kj > T) || (eq && ties + __popc(beq & lt_mask) < krem);
+                const bool kc = key[j] > T || (eq && ties + __popc(beq & lt_mask) < krem);
                 const unsigned bk = __ballot_sync(0xffffffffu, kc);
                 if (kc) {
-                    const int o = acc + base + __popc(bk & lt_mask);
+                    const int o = base + __popc(bk & lt_mask);
                     hk[o] = t;
-                    hw[o] = ex2(sv - M);
+                    hw[o] = ex2(scores[t] - M);
+                    if (P.sel != nullptr) P.sel[lo + o] = t;
                 }
-                base += __popc(bk);
-                ties += __popc(beq);
-            }
-        }
-        if (P.sel != nullptr) {   // the kept indices in ascending order (optional output)
-            int base = 0, ties = 0;
-#pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                const int t = j * 32 + lane;
-                const float sv = scores[t];
-                const int b = t < n_tok ? score_bin(M, sv) : -1;
-                const uint32_t kj = order_key(sv);
-                const bool eq = b == d0 && kj == T;
-                const unsigned beq = __ballot_sync(0xffffffffu, eq);
-                const bool kc = b > d0 || (b == d0 && kj > T) || (eq && ties + __popc(beq & lt_mask) < krem);
-                const unsigned bk = __ballot_sync(0xffffffffu, kc);
-                if (kc) P.sel[lo + base + __popc(bk & lt_mask)] = t;
                 base += __popc(bk);
                 ties += __popc(beq);
             }
@@ -692,7 +505,7 @@ __global__ void __launch_bounds__(256, FLEXQ_TOPK_GATHER_MINB) topk_gather_kerne
 template <int D, int NCH, int S, int WPC, int MAXT>
 constexpr size_t select_smem_bytes() {
     constexpr int NQ = 2;
-    return size_t(WPC) * (S * Cfg<D, NCH>::STG + NQ * 2 * D + MAXT * 6 + (S + NQ) * 8);
+    return size_t(WPC) * (S * Cfg<D, NCH>::STG + NQ * 2 * D + MAXT * 4 + (S + NQ) * 8);
 }
 
 constexpr size_t kTopkCtrlBytes = 2048;
