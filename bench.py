@@ -404,13 +404,20 @@ class DecodeModel:
     def tm_cache(self, j):
         """Layer j's cache in the token-major layout (Top-K's): the same bytes moved with
         flexq_kv_export / flexq_kv_import (no requantization)."""
+        import torch
         self.tm = getattr(self, "tm", {})
         if j not in self.tm:
             fq, c = self.fq, self.caches[j]
-            t = fq.KVCache(c.batch, c.heads, c.head_dim, c.prompt_len, c.gen_len, device=c.k.device,
-                           layout="token_major")
-            plain = fq.flexq_kv_export(c, stream=self.stream)
-            fq.flexq_kv_import(t, *plain, stream=self.stream)
+            # allocations (zero-filled by torch) and the two copy kernels all on the model's stream,
+            # and the plain arrays freed only after it drains: exporting on self.stream into arrays
+            # zero-filled on the default stream (and freed while the import still read them) left
+            # some layers' token-major copies empty, so Top-K timed them on all-equal scores
+            with torch.cuda.stream(self.stream):
+                t = fq.KVCache(c.batch, c.heads, c.head_dim, c.prompt_len, c.gen_len, device=c.k.device,
+                               layout="token_major")
+                plain = fq.flexq_kv_export(c)
+                fq.flexq_kv_import(t, *plain)
+            self.stream.synchronize()
             del plain
             self.tm[j] = t
         return self.tm[j]

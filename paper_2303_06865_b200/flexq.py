@@ -99,6 +99,20 @@ def _stream(stream, device=None) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _cross_stream(stream, device, *tensors):
+    """When a call runs on a torch stream other than the current one: order it after the current
+    stream's pending work (e.g. the zero-fill of arrays allocated here) and mark the tensors as used
+    on it, so the caching allocator does not hand their memory out again before it is done."""
+    if stream is None or not isinstance(stream, torch.cuda.Stream):
+        return
+    cur = torch.cuda.current_stream(device)
+    if stream == cur:
+        return
+    stream.wait_stream(cur)
+    for t in tensors:
+        t.record_stream(stream)
+
+
 def _need(t: torch.Tensor, dtype, name: str, shape=None, device=None):
     """A contiguous CUDA tensor of `dtype` (and `shape` / on `device` when given); the C ABI
     takes raw pointers, so a mismatch must be caught here, not as an illegal address."""
@@ -244,6 +258,7 @@ def flexq_kv_import(cache: "KVCache", k_codes, k_meta, v_codes, v_meta, t0: int 
     for t in (k_codes, k_meta, v_codes, v_meta):
         if t.device != dev:
             raise ValueError(f"plain arrays must be on {dev}")
+    _cross_stream(stream, dev, k_codes, k_meta, v_codes, v_meta, cache.k, cache.v)
     with torch.cuda.device(dev):
         _check(lib().flexq_kv_import(_ptr(k_codes), _ptr(k_meta), _ptr(v_codes), _ptr(v_meta), cache.batch, cache.heads,
                                      cache.head_dim, cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits,
@@ -261,6 +276,7 @@ def flexq_kv_export(cache: "KVCache", t0: int = 0, n_tok=None, plain_tokens=None
     dev = cache.k.device
     kc, vc = torch.zeros(cs, dtype=torch.uint8, device=dev), torch.zeros(cs, dtype=torch.uint8, device=dev)
     km, vm = torch.zeros(ms, dtype=torch.float16, device=dev), torch.zeros(ms, dtype=torch.float16, device=dev)
+    _cross_stream(stream, dev, kc, km, vc, vm)
     with torch.cuda.device(dev):
         _check(lib().flexq_kv_export(_ptr(cache.k), _ptr(cache.v), cache.batch, cache.heads, cache.head_dim,
                                      cache.prompt_len, cache.gen_len, T, t0, n_tok, cache.bits, cache.group_size,

@@ -91,3 +91,30 @@ def test_imported_cache_attends_like_appended(orc, cuda):
     fq.flexq_append_kv(k, v, app, pos=0)
     q = synth.fill(83, 3, (B, H, D)).to(cuda)
     assert torch.equal(fq.flexq_decode_attention(q, imp, T), fq.flexq_decode_attention(q, app, T))
+
+
+def test_export_import_on_a_side_stream(cuda):
+    """Export / import issued on a stream other than the current one (bench.py's token-major
+    copies): the binding orders the calls after the current stream's zero-fill of the arrays it
+    allocates and keeps their memory alive for the side stream, so every copy is complete --
+    before the fix some of the copies came out empty."""
+    B, H, D, s, n = 16, 12, 128, 300, 4
+    srcs = []
+    for j in range(4):
+        c = fq.KVCache(B, H, D, s, n, device=cuda)
+        fq.flexq_append_kv(synth.fill(82, 2 * j, (B, H, s + n, D), device=cuda),
+                           synth.fill(82, 2 * j + 1, (B, H, s + n, D), device=cuda), c, pos=0)
+        srcs.append(c)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    outs = []
+    for c in srcs:
+        t = fq.KVCache(B, H, D, s, n, device=cuda, layout="token_major")
+        plain = fq.flexq_kv_export(c, stream=side)
+        fq.flexq_kv_import(t, *plain, stream=side)
+        del plain
+        outs.append(t)
+    side.synchronize()
+    for c, t in zip(srcs, outs):
+        for a, b in zip(fq.flexq_kv_export(c), fq.flexq_kv_export(t)):
+            assert torch.equal(a, b)
