@@ -192,6 +192,11 @@ struct SelectParams {
     float qscale;
 };
 
+// c += (a >= b), unsigned, as a compare and a predicated add (the ternary form compiled to a
+// compare, an add and a predicated move per key: the select's count rounds are its hot loop)
+__device__ __forceinline__ void count_ge(int& c, uint32_t a, uint32_t b) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}" : "+r"(c) : "r"(a), "r"(b));
+}
 __device__ __forceinline__ uint32_t order_key(float f) {
     const uint32_t u = __float_as_uint(f);
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);   // larger float <=> larger key
@@ -356,7 +361,7 @@ topk_select_kernel(const SelectParams P) {
                 const uint32_t cand = T | (1u << bit);
                 int c = 0;
 #pragma unroll
-                for (int j = 0; j < KPL; ++j) c += key[j] >= cand ? 1 : 0;
+                for (int j = 0; j < KPL; ++j) count_ge(c, key[j], cand);
                 c = int(__reduce_add_sync(0xffffffffu, uint32_t(c)));
                 if (c >= keep) {
                     T = cand;
