@@ -92,7 +92,7 @@ if __name__ == "__main__":
             print(build(force="--force" in sys.argv, defines=(f"FLEXQ_GEMV_PROBE={v}",), tag=f"gemv{v}"))
         print(build(force="--force" in sys.argv, defines=("FLEXQ_GEMV_CTAS=1",), tag="gemv1cta"))
     if "--l2pf-ab" in sys.argv:
-        for n in (1, 2):
+        for n in (4, 9):
             print(build(force="--force" in sys.argv, defines=(f"FLEXQ_ATTN_L2PF={n}",), tag=f"l2pf{n}"))
     if "--trace" in sys.argv:
         print(build(force="--force" in sys.argv, defines=("FLEXQ_ATTN_TRACE=1",), tag="trace"))

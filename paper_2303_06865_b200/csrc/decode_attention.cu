@@ -47,6 +47,7 @@ constexpr int kMaxWarps = 4096;     // grid cap
 constexpr int kMaxPieces = 32;      // pieces per head (partial slots per head)
 constexpr int kMinPieceChunks = 2;  // smallest piece
 constexpr int kCtasPerSm = 16;      // one-warp CTAs resident per SM (register / smem budget)
+constexpr int kPfWholeHeadsPerWarp = 3;   // from this many items per warp the L2 prefetch takes the whole first K pass
 constexpr int kMaxCtrs = 16;        // ticket counters, 64 B apart in the 1 KB control block
 constexpr int kRetire = 16 * kMaxCtrs;
 
@@ -93,6 +94,7 @@ struct Params {
     const __half* v_new;   //   nullptr = the cache already holds it
     uint8_t* kc_w;         // writable aliases of kc / vc for the fused append
     uint8_t* vc_w;
+    int pf_chunks;         // K chunks of the first item prefetched to L2 before griddepcontrol.wait
 };
 
 // Work item t: piece k of np of head bh = chunks [o, o + nch) (np = 1: the whole head).
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(32, kCtasPerSm) decode_attention_kernel(const 
         Piece f;
         if (decode_item(P, int(blockIdx.x), f)) {
             const uint8_t* src = P.kc + (int64_t(f.bh) * P.chunks + f.o) * C::CHB;
-            const uint32_t bytes = uint32_t(min(f.nch, FLEXQ_ATTN_L2PF * NCH)) * C::CHB;
+            const uint32_t bytes = uint32_t(min(f.nch, P.pf_chunks)) * C::CHB;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
         }
     }
@@ -665,6 +667,10 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t stream) {
     P.v_new = static_cast<const __half*>(a.v_new);
     P.kc_w = static_cast<uint8_t*>(const_cast<void*>(a.k_cache));
     P.vc_w = static_cast<uint8_t*>(const_cast<void*>(a.v_cache));
+    // L2 prefetch depth (r3g, r3u): with about one head per warp the first two K stages (batch 18:
+    // 26.6 -> 25.9 us; the whole first head's K: 27.9 us); with many heads per warp the whole
+    // first head's K pass, fetched while the previous grid drains (batch 144: 169.8 -> 165.7 us)
+    P.pf_chunks = P.items >= kPfWholeHeadsPerWarp * grid ? nck : FLEXQ_ATTN_L2PF * NCH;
     static const bool pdl = [] {
         const char* e = getenv("FLEXQ_PDL");
         return !(e && e[0] == '0');
