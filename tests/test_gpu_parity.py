@@ -424,6 +424,25 @@ def test_topk_attention_parity(orc, cuda, case, layout):
     assert_attn_close(out.cpu().numpy(), ref, name)
 
 
+@pytest.mark.parametrize("layout", ["dense", "token_major"])
+def test_topk_workspace_reuse(orc, cuda, layout):
+    """Every call leaves the Top-K workspace's scheduler counters zero (include/flexq.h): calls on
+    one workspace, with different q and keep, give the bytes a fresh zeroed workspace gives, and the
+    workspace's control area is zero again afterwards."""
+    B, H, D, s, n, steps = 3, 40, 128, 300, 4, 3
+    cache, okc, ovc, q, cur = build_case(orc, cuda, B, H, D, s, n, steps, seed=61, layout=layout)
+    ws = fq.make_topk_workspace(cache)
+    gen = torch.Generator().manual_seed(7)
+    for rep, frac in enumerate([0.1, 0.3, 0.1, 0.05]):
+        qq = (q + 0.25 * rep * torch.randn(q.shape, generator=gen).to(q.dtype)).to(cuda)
+        keep = fq.topk_keep(cur, frac)
+        got = fq.flexq_decode_attention_topk(qq, cache, cur, keep, workspace=ws)
+        ref = fq.flexq_decode_attention_topk(qq, cache, cur, keep)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), rep
+        assert int(ws[:2048].count_nonzero()) == 0, rep   # the select kernel's tickets
+
+
 # ---------------------------------------------------------------- fused append + attention (NEXT-3)
 FUSED_CASES = [
     # name, B, H, D, s, n, steps (fused decode steps after the prompt), outliers, qfactor
