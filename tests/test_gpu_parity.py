@@ -301,6 +301,53 @@ def test_full_size_fused_sampled(orc, cuda):
 
 
 # ---------------------------------------------------------------- NEXT-1: Top-K sparse attention
+def test_topk_full_size_sampled(orc, cuda):
+    """The Top-K launch bench.py times (topk_sparse): OPT-175B at full size (B=144, H=96, D=128),
+    token-major cache, cur_len 543, keep = ceil(0.1 * 543) = 55.  For 12 sampled heads
+    the oracle quantizes the head's 543 K / V rows and recomputes scores, kept set and output: the
+    head's cache bytes are identical, the GPU's kept set is a valid top-55 set of the oracle's
+    scores (it may differ from the oracle's only at near-ties), and the output is within reading Q
+    of the oracle evaluated on the GPU's set."""
+    B, H, D, T = 144, 96, 128, 543
+    seed = synth.BASE_SEED + 5
+    cache = fq.KVCache(B, H, D, T, 1, device=cuda, layout="token_major")
+    k = synth.fill(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, T, D), device=cuda)
+    v = synth.fill(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, T, D), device=cuda)
+    fq.flexq_append_kv(k, v, cache, pos=0)
+    del k, v
+    q = synth.fill(seed, synth.tensor_id(0, synth.Q, 1), (B, H, D), device=cuda)
+    keep = fq.topk_keep(T)
+    assert keep == 55
+    sel = torch.full((B, H, keep), -1, dtype=torch.int32, device=cuda)
+    out = fq.flexq_decode_attention_topk(q, cache, T, keep, sel=sel).cpu().numpy()
+    sel = sel.cpu().numpy()
+    kc_all, vc_all = cache.k_codes().cpu().numpy(), cache.v_codes().cpu().numpy()
+    rng = np.random.default_rng(12)
+    samples = [(0, 0), (B - 1, H - 1)] + [(int(rng.integers(B)), int(rng.integers(H))) for _ in range(10)]
+    sl = lambda b, h, *rest: [b, h, *rest]   # noqa: E731
+    mismatched = 0
+    for b, h in samples:
+        okc, ovc = orc.empty_cache(1, 1, T + 1, D), orc.empty_cache(1, 1, T + 1, D)
+        kp = synth.gather(seed, synth.tensor_id(0, synth.K_PROMPT), (B, H, T, D), sl(b, h, slice(None), slice(None)))
+        vp = synth.gather(seed, synth.tensor_id(0, synth.V_PROMPT), (B, H, T, D), sl(b, h, slice(None), slice(None)))
+        orc.append_kv(kp.numpy(), vp.numpy(), okc, ovc, 0)
+        assert np.array_equal(kc_all[b, h, :T], orc.pack4(okc[0][0, 0, :T])), (b, h)
+        assert np.array_equal(vc_all[b, h, :T], orc.pack4(ovc[0][0, 0, :T])), (b, h)
+        qh = synth.gather(seed, synth.tensor_id(0, synth.Q, 1), (B, H, D), sl(b, h, slice(None))).numpy()
+        _, omask, scores = orc.attention_topk_f64(qh.reshape(1, 1, D), okc, ovc, T, keep)
+        idx = sel[b, h]
+        assert np.all(np.diff(idx) > 0) and idx.min() >= 0 and idx.max() < T, (b, h)
+        mask = np.zeros((1, 1, T), np.uint8)
+        mask[0, 0, idx] = 1
+        sc = scores[0, 0]
+        eps = 1e-4 * max(1.0, np.abs(sc).max())
+        assert sc[idx].min() >= sc[mask[0, 0] == 0].max() - eps, (b, h)
+        mismatched += int((mask != omask).sum())
+        ref, _, _ = orc.attention_topk_f64(qh.reshape(1, 1, D), okc, ovc, T, keep, sel=mask)
+        assert_attn_close(out[b:b + 1, h:h + 1], ref, f"(b={b}, h={h})")
+    assert mismatched <= 2 * len(samples)   # differences only at near-ties
+
+
 @pytest.mark.parametrize("layout", ["dense", "token_major"])
 @pytest.mark.parametrize("D", [64, 128])
 def test_topk_exact_ties_bit_exact(orc, cuda, D, layout):
