@@ -86,3 +86,19 @@ def test_bench_line_e2e_and_clocks(path):
     assert 0 < c["sm_mhz"] <= c["sm_max_mhz"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0
+
+
+def test_reference_arm_line():
+    """The reference arm (the oracle on the host's cores): same metric, unit
+    and workload as the device line, its own value in cpu_baseline and e2e, no transfers."""
+    d, dev = load("profiles/r2_bench_reference.json"), load(LINES[0])
+    assert d["impl"] == "reference"
+    for k in ("metric", "unit", "higher_is_better", "dtype", "scaling"):
+        assert d[k] == dev[k], k
+    assert d["config"]["global_batch"] == dev["config"]["global_batch"] and d["warmup"] >= 3
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    e = d["e2e"]
+    assert e["value"] == d["value"] and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+    # bytes per sampled token: the sample's unit is one 96-head sequence at cur_len 543
+    assert d["value"] * 1e9 / d["tokens_per_s"] == pytest.approx(L * fused_launch_bytes(S + N - 1) / B, rel=0.05)
